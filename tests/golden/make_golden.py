@@ -1,0 +1,210 @@
+"""Generate the golden vectors that pin the oracle (and through it the CUDA path).
+
+Runs the REFERENCE itself (semsplat 0.1.0 at /root/reference/pkg/src, imported
+read-only) on seeded inputs and stores inputs + outputs as small .npz fixtures.
+Only this script reads /root/reference; the fixtures travel with the repo.
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.dont_write_bytecode = True
+sys.path.insert(0, REF)
+
+from semsplat.core import (CameraIntrinsics, CameraPose, Codebook,  # noqa: E402
+                           FeatureReservoir, GaussianField)
+from semsplat import slam, vq  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def mixture(rng, n, D, centres, sigma):
+    C = rng.normal(size=(centres, D))
+    C /= np.linalg.norm(C, axis=1, keepdims=True)
+    ids = rng.integers(0, centres, n)
+    x = C[ids] + sigma * rng.normal(size=(n, D))
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    return x.astype(np.float32)
+
+
+def make_cb(E, lam=0.96, eps=1e-5, cap=64):
+    E = np.asarray(E, dtype=float)
+    return Codebook(E=E, N=np.zeros(E.shape[0]), M=np.zeros_like(E), lam=lam, epsilon=eps,
+                    reservoir=FeatureReservoir(cap, E.shape[1]))
+
+
+def gen_distances():
+    rng = np.random.default_rng(100)
+    out = {}
+    for D in (1, 3, 7, 8, 9, 17, 100, 128, 129, 255, 512, 768, 1152):
+        x = rng.normal(size=(6, D))
+        E = rng.normal(size=(5, D))
+        out[f"x_{D}"] = x
+        out[f"E_{D}"] = E
+        out[f"d_{D}"] = vq.squared_distances(x, make_cb(E))
+    np.savez_compressed(os.path.join(OUT, "sqdist.npz"), **out)
+
+
+def gen_assign():
+    rng = np.random.default_rng(101)
+    out = {}
+    # C1-like: K=256, D=512, 64-centre mixture sigma 0.1, E from random rows
+    x = mixture(rng, 512, 512, 64, 0.1)
+    E = x[rng.choice(512, 256, replace=False)].astype(np.float64)
+    out["c1_x"], out["c1_E"] = x, E.astype(np.float32)  # exact: rows of x
+    out["c1_codes"] = vq.assign_batch(x, make_cb(E))
+    # C2-like subset: K=1024, D=512, 1024-centre sigma 0.05
+    x = mixture(rng, 384, 512, 1024, 0.05)
+    E = mixture(rng, 512, 512, 1024, 0.05).astype(np.float64)
+    out["c2_x"], out["c2_E"] = x, E.astype(np.float32)  # exact upcast
+    out["c2_codes"] = vq.assign_batch(x, make_cb(E))
+    # exact ties: duplicated codewords and equidistant points -> lowest index
+    E = rng.normal(size=(16, 8))
+    E[9] = E[3]
+    E[12] = E[3]
+    xs = np.concatenate([E[[3, 9, 12]], rng.normal(size=(61, 8))])
+    out["tie_x"], out["tie_E"] = xs, E
+    out["tie_codes"] = vq.assign_batch(xs, make_cb(E))
+    E = np.array([[0.0, 0.0], [2.0, 0.0], [1.0, 1.0], [1.0, -1.0]])
+    xs = np.array([[1.0, 0.0], [0.5, 0.5], [3.0, 0.0], [-1.0, 0.0]])
+    out["tie2_x"], out["tie2_E"] = xs, E
+    out["tie2_codes"] = vq.assign_batch(xs, make_cb(E))
+    np.savez_compressed(os.path.join(OUT, "assign.npz"), **out)
+
+
+def gen_accumulate_ema():
+    rng = np.random.default_rng(102)
+    out = {}
+    x = mixture(rng, 2000, 64, 16, 0.1)
+    E = x[:32].astype(np.float64) + 0.01
+    cb = make_cb(E, lam=0.99)
+    st = vq.accumulate(x, cb)
+    out["x"], out["E"] = x, E
+    out["counts"], out["sums"] = st.counts, st.sums
+    cb.N[:] = rng.uniform(0, 5, 32)
+    cb.M[:] = rng.normal(size=(32, 64))
+    out["N0"], out["M0"] = cb.N.copy(), cb.M.copy()
+    e = vq.ema_step(cb, st)
+    out["N1"], out["M1"], out["E1"] = e.N, e.M, e.E
+    np.savez_compressed(os.path.join(OUT, "accumulate.npz"), **out)
+
+
+def gen_online():
+    out = {}
+    # (a) confidence path active (gamma=0.5, tau=0.7): small clustered stream
+    rng = np.random.default_rng(103)
+    centres = np.array([[0.0, 0, 0], [1.0, 0, 0], [0.0, 1, 0], [0.0, 0, 1]])
+    cfg = vq.VqConfig(K=4, lam=0.8, gamma=0.5, tau_warm=0.7, delta_dead=1e-2)
+    batches = [centres[rng.integers(0, 4, 64)] + rng.normal(0, 0.05, (64, 3)) for _ in range(12)]
+    batches += [centres[rng.integers(0, 3, 64)] + rng.normal(0, 0.05, (64, 3)) for _ in range(40)]
+    batches += [np.concatenate([centres[rng.integers(0, 4, 60)] + rng.normal(0, 0.05, (60, 3)),
+                                rng.uniform(-3, 3, (4, 3))]) for _ in range(20)]
+    E0 = centres + 0.1
+    cb = make_cb(E0, lam=0.8, cap=128)
+    rrng = np.random.default_rng(7)
+    Es, Ns, Ms, rev = [], [], [], []
+    for b in batches:
+        cb, res = vq.online_step(cb, b, cfg, rrng)
+        Es.append(cb.E)
+        Ns.append(cb.N)
+        Ms.append(cb.M)
+        rev.append(len(res.revived))
+    out["a_batches"] = np.stack(batches)
+    out["a_E0"] = E0
+    out["a_E"], out["a_N"], out["a_M"] = np.stack(Es), np.stack(Ns), np.stack(Ms)
+    out["a_nrev"] = np.array(rev)
+    # (b) BASELINE-style: gamma = 0.5/K (mask all-true), lam 0.99, delta 1e-3
+    rng = np.random.default_rng(104)
+    K, D, n = 64, 32, 256
+    x = mixture(rng, n * 8, D, 48, 0.05)
+    E0 = x[rng.choice(x.shape[0], K, replace=False)].astype(np.float64)
+    cfg = vq.VqConfig(K=K, lam=0.99, gamma=0.5 / K, delta_dead=1e-3)
+    cb = make_cb(E0, lam=0.99, cap=300)
+    rrng = np.random.default_rng(12)
+    Es, Ns, rev = [], [], []
+    for i in range(8):
+        cb, res = vq.online_step(cb, x[i * n:(i + 1) * n], cfg, rrng)
+        Es.append(cb.E)
+        Ns.append(cb.N)
+        rev.append(len(res.revived))
+    out["b_x"], out["b_E0"] = x, E0
+    out["b_E"], out["b_N"], out["b_nrev"] = np.stack(Es), np.stack(Ns), np.array(rev)
+    # (c) confidence scores / mask values
+    rng = np.random.default_rng(105)
+    E = rng.normal(size=(7, 5))
+    xs = rng.normal(size=(40, 5))
+    cbc = make_cb(E)
+    out["c_x"], out["c_E"] = xs, E
+    out["c_p"] = vq.confidence_scores(xs, cbc, 0.7)
+    out["c_mask"] = vq.confidence_mask(xs, cbc, vq.VqConfig(K=7, gamma=0.4))
+    # (d) warm start + farthest point seeding
+    rng = np.random.default_rng(106)
+    buf = rng.normal(size=(50, 3))
+    seeds = vq.seed_from_samples(buf, 4)
+    ws = vq.warm_start(buf, make_cb(seeds), vq.VqConfig(K=4, gamma=0.3))
+    out["d_buf"], out["d_seeds"] = buf, seeds
+    out["d_E"], out["d_N"], out["d_used"] = ws.codebook.E, ws.codebook.N, np.array(ws.used)
+    np.savez_compressed(os.path.join(OUT, "online.npz"), **out)
+
+
+def gen_backproject():
+    from scipy.spatial.transform import Rotation
+    rng = np.random.default_rng(107)
+    n = 12000
+    R = Rotation.random(16, random_state=3).as_matrix()
+    t = rng.normal(size=(16, 3))
+    intr = CameraIntrinsics(fx=525.0, fy=525.0, cx=239.5, cy=319.5, height=480, width=640)
+    pose_id = rng.integers(0, 16, n)
+    u = rng.integers(0, 480, n)
+    v = rng.integers(0, 640, n)
+    d = rng.uniform(0.3, 8.0, n).astype(np.float32)
+    p = np.empty((n, 3))
+    for i in range(n):
+        pose = CameraPose(R[pose_id[i]], t[pose_id[i]])
+        p[i] = slam.backproject(pose, intr, int(u[i]), int(v[i]), float(d[i]))
+    np.savez_compressed(os.path.join(OUT, "backproject.npz"), R=R, t=t,
+                        intr=np.array([525.0, 525.0, 239.5, 319.5]), pose_id=pose_id,
+                        u=u, v=v, d=d, p=p)
+
+
+def gen_densify():
+    """densify_and_prune on an EMPTY field (coverage alpha == 0, no render):
+    every stride-4 lattice pixel is inserted (slam.py:601-651)."""
+    from semsplat.world import CameraFrame
+    rng = np.random.default_rng(108)
+    H, W = 24, 32
+    depth = rng.uniform(0.5, 5.0, (H, W)).astype(np.float32)
+    depth[rng.random((H, W)) < 0.2] = 0.0
+    color = rng.random((3, H, W))
+    from scipy.spatial.transform import Rotation
+    pose = CameraPose(Rotation.random(random_state=5).as_matrix(), rng.normal(size=3))
+    frame = CameraFrame(frame_id=0, pose=pose, color=color, depth=depth)
+    win = slam.KeyframeWindow(4)
+    win.insert(frame, pose)
+    empty = GaussianField(mu=np.zeros((0, 3)), quat=np.zeros((0, 4)), scale=np.zeros((0, 3)),
+                          opacity=np.zeros(0), color=np.zeros((0, 3)), logits=np.zeros((0, 5)))
+    cfg = slam.SlamConfig()
+    out = slam.densify_and_prune(empty, win, cfg, K=5)
+    np.savez_compressed(os.path.join(OUT, "densify.npz"), depth=depth, color=color,
+                        R=pose.rotation, t=pose.translation, mu=out.mu, scale=out.scale,
+                        col=out.color, opacity=out.opacity, quat=out.quat,
+                        generation=np.array(out.generation))
+
+
+if __name__ == "__main__":
+    gen_distances()
+    gen_assign()
+    gen_accumulate_ema()
+    gen_online()
+    gen_backproject()
+    gen_densify()
+    for f in sorted(os.listdir(OUT)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(OUT, f)))
