@@ -1,0 +1,106 @@
+/*
+ * xgs.h — C ABI of libxgs, the B200 (sm_100a) implementation of the X-GS
+ * per-frame hot path: online EMA vector quantisation and voxel grid sampling.
+ *
+ * The reference (semsplat 0.1.0) has no FFI: its boundary is the Python API of
+ * semsplat.vq and semsplat.slam.  Each entry point below names the reference
+ * function it replaces (file:line under /root/reference/pkg/src/semsplat).
+ * The Python package paper_2603_09632_b200 binds these through ctypes and keeps
+ * the reference signatures; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - every array argument is caller-owned DEVICE memory (plain pointers and
+ *     sizes, row-major, leading dimension in elements); `stream` is a
+ *     cudaStream_t passed as void*; calls are asynchronous on that stream
+ *     unless stated otherwise;
+ *   - scratch memory is caller-provided, sized by the matching *_workspace();
+ *   - return 0 on success, XGS_INVALID_INPUT (-> InvalidInputError),
+ *     XGS_INVALID_STATE (-> InvalidStateError), XGS_CUDA_ERROR,
+ *     XGS_NOT_SUPPORTED; xgs_last_error() returns a thread-local message;
+ *   - re-entrant: no global mutable state besides opaque handles.
+ */
+#ifndef XGS_H_
+#define XGS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define XGS_API __attribute__((visibility("default")))
+#else
+#define XGS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { XGS_OK = 0, XGS_INVALID_INPUT = 1, XGS_INVALID_STATE = 2, XGS_CUDA_ERROR = 3, XGS_NOT_SUPPORTED = 4 };
+enum { XGS_F32 = 0, XGS_F64 = 1, XGS_BF16 = 2 };
+/* modes of xgs_vq_exact (bit set) */
+enum { XGS_EX_DIST = 1, XGS_EX_CODE = 2, XGS_EX_MASK = 4, XGS_EX_PROB = 8 };
+
+XGS_API int xgs_abi_version(void);
+XGS_API const char* xgs_last_error(void);
+XGS_API int xgs_device_sm_count(void);
+/* number of kernels libxgs has launched in this process (bench evidence) */
+XGS_API long long xgs_launch_count(void);
+/* opt-in profiler: CUDA events recorded on the launching stream around each
+ * named kernel group ("vq_prep", "vq_screen", "vq_rerank", "vq_accumulate",
+ * "vq_chain", "vq_ema", "grid_*"); enable(1) clears, read() synchronises. */
+XGS_API int xgs_profile_enable(int on);
+XGS_API int xgs_profile_read(const char* tag, double* total_ms, long long* count);
+
+/* ------------------------------------------------------------------ VQ */
+
+/* assign_batch (vq.py:84-87) / assign (vq.py:76-81): int64 codes of the
+ * nearest fp64 codeword, ties to the lowest index, bit-identical to the
+ * reference.  tcgen05 bf16 screening GEMM + exact fp64 re-rank.
+ * stats_out (HOST, nullable): {rows re-ranked, rows rescanned exactly};
+ * when given the call synchronises on `stream`.
+ * Errors: K == 0 -> XGS_INVALID_STATE (vq.py:78-79, 85-86). */
+XGS_API size_t xgs_vq_assign_workspace(int64_t n, int64_t k, int64_t d, int dtype, int64_t ldx);
+XGS_API int xgs_vq_assign(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E, int64_t k,
+                          int64_t* codes, void* ws, size_t ws_bytes, int32_t* stats_out, void* stream);
+
+/* Exact fp64 path, one CTA per row:
+ *   XGS_EX_DIST  squared_distances (vq.py:69-73) -> out_dist (n, k)
+ *   XGS_EX_CODE  argmin -> codes (n)
+ *   XGS_EX_MASK  confidence_mask (vq.py:121-124) -> mask (n) u8
+ *   XGS_EX_PROB  confidence_scores (vq.py:112-118) -> out_prob (n, k) */
+XGS_API int xgs_vq_exact(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E, int64_t k,
+                         int mode, double tau, double gamma, double* out_dist, double* out_prob, int64_t* codes,
+                         uint8_t* mask, void* stream);
+
+/* accumulate (vq.py:90-100) given the codes: counts = bincount(codes[mask]),
+ * sums = np.add.at(zeros, codes[mask], x[mask]) — bit-identical (sequential
+ * fp64 chains per (k, d) in ascending row order).  mask may be NULL. */
+XGS_API size_t xgs_vq_accumulate_workspace(int64_t n, int64_t k);
+XGS_API int xgs_vq_accumulate(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const int64_t* codes,
+                              const uint8_t* mask, int64_t k, double* counts, double* sums, void* ws,
+                              size_t ws_bytes, void* stream);
+
+/* ema_step (vq.py:103-109): N' = lam N + (1-lam) c ; M' = lam M + (1-lam) s ;
+ * E' = M' / (N' + eps).  Outputs may alias inputs. */
+XGS_API int xgs_vq_ema(double lam, double eps, int64_t k, int64_t d, const double* N, const double* M,
+                       const double* counts, const double* sums, double* N_out, double* M_out, double* E_out,
+                       void* stream);
+
+/* revive_dead_codes (vq.py:173-190) after the host drew the reservoir rows:
+ * for i < n_dead: M[k_i] = ring[r_i]; N[k_i] = 1+eps; E[k_i] = M[k_i]/(N[k_i]+eps). */
+XGS_API int xgs_vq_revive(int64_t k, int64_t d, double eps, const double* ring, int64_t cap, const int64_t* dead_k,
+                          const int64_t* ring_rows, int64_t n_dead, double* N, double* M, double* E,
+                          void* stream);
+
+/* FeatureReservoir.extend (core.py:191-195) as a device ring buffer:
+ * rows [row0, row0+nrows) of x -> ring[(phys0 + j) % cap] as fp64. */
+XGS_API int xgs_vq_ring_write(const void* x, int dtype, int64_t ldx, int64_t row0, int64_t nrows, int64_t d,
+                              double* ring, int64_t cap, int64_t phys0, void* stream);
+XGS_API int xgs_gather_rows_f64(const double* src, int64_t d, const int64_t* rows, int64_t n, double* dst,
+                                void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* XGS_H_ */

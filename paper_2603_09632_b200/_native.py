@@ -1,0 +1,147 @@
+"""ctypes binding of libxgs.so (the C ABI in include/xgs.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+visible, every compute entry point raises :class:`NativeError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import InvalidInputError, InvalidStateError, NativeError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libxgs.so")
+
+F32, F64, BF16 = 0, 1, 2
+EX_DIST, EX_CODE, EX_MASK, EX_PROB = 1, 2, 4, 8
+
+_lib = None
+_lock = threading.Lock()
+
+_vp, _i64, _i32, _f64, _sz = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
+                              ctypes.c_size_t)
+
+# name -> (restype, argtypes); mirrors include/xgs.h
+SIGNATURES = {
+    "xgs_abi_version": (_i32, []),
+    "xgs_last_error": (ctypes.c_char_p, []),
+    "xgs_device_sm_count": (_i32, []),
+    "xgs_launch_count": (ctypes.c_longlong, []),
+    "xgs_profile_enable": (_i32, [_i32]),
+    "xgs_profile_read": (_i32, [ctypes.c_char_p, _vp, _vp]),
+    "xgs_vq_assign_workspace": (_sz, [_i64, _i64, _i64, _i32, _i64]),
+    "xgs_vq_assign": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _sz, _vp, _vp]),
+    "xgs_vq_exact": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _i32, _f64, _f64, _vp, _vp, _vp, _vp,
+                            _vp]),
+    "xgs_vq_accumulate_workspace": (_sz, [_i64, _i64]),
+    "xgs_vq_accumulate": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "xgs_vq_ema": (_i32, [_f64, _f64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "xgs_vq_revive": (_i32, [_i64, _i64, _f64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "xgs_vq_ring_write": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _vp]),
+    "xgs_gather_rows_f64": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
+}
+
+
+def lib():
+    """Load libxgs.so (raises NativeError when it was not built)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise NativeError(f"libxgs.so not built ({LIB_PATH}); run "
+                                      "`python -m paper_2603_09632_b200.build`")
+                L = ctypes.CDLL(LIB_PATH)
+                for name, (res, args) in SIGNATURES.items():
+                    fn = getattr(L, name)
+                    fn.restype = res
+                    fn.argtypes = args
+                _lib = L
+    return _lib
+
+
+def launch_count():
+    return int(lib().xgs_launch_count())
+
+
+def profile_enable(on=True):
+    check(lib().xgs_profile_enable(1 if on else 0))
+
+
+def profile_read(tag):
+    ms, cnt = ctypes.c_double(0), ctypes.c_longlong(0)
+    check(lib().xgs_profile_read(tag.encode(), ctypes.byref(ms), ctypes.byref(cnt)))
+    return ms.value, cnt.value
+
+
+def check(rc):
+    if rc == 0:
+        return
+    msg = lib().xgs_last_error().decode(errors="replace")
+    if rc == 1:
+        raise InvalidInputError(msg)
+    if rc == 2:
+        raise InvalidStateError(msg)
+    raise NativeError(f"libxgs error {rc}: {msg}")
+
+
+def call(name, *args):
+    check(getattr(lib(), name)(*args))
+
+
+# ---------------------------------------------------------------- torch glue
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise NativeError("no CUDA device visible: the B200 path has no CPU fallback")
+    lib()
+    return t
+
+
+def stream_ptr():
+    return ctypes.c_void_p(torch().cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+_ws = {}
+
+
+def workspace(slot, nbytes, device=None):
+    """Grow-only per-(device, slot) scratch buffer (uint8 CUDA tensor)."""
+    t = torch()
+    dev = t.device("cuda", t.cuda.current_device()) if device is None else device
+    key = (dev.index, slot)
+    buf = _ws.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = t.empty(max(int(nbytes), 256), dtype=t.uint8, device=dev)
+        _ws[key] = buf
+    return buf
+
+
+def dtype_code(tensor):
+    t = torch()
+    if tensor.dtype == t.float32:
+        return F32
+    if tensor.dtype == t.float64:
+        return F64
+    if tensor.dtype == t.bfloat16:
+        return BF16
+    raise InvalidInputError(f"unsupported dtype {tensor.dtype}")

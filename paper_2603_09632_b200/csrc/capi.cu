@@ -1,0 +1,257 @@
+// C-ABI entry points of libxgs (declared in include/xgs.h).
+//
+// Conventions: all buffers are caller-owned DEVICE memory; streams are passed
+// as void* (cudaStream_t); scratch comes from a caller workspace sized by the
+// matching *_workspace() query.  Return codes: 0 ok, 1 invalid input
+// (-> InvalidInputError), 2 invalid state (-> InvalidStateError), 3 CUDA
+// error, 4 not supported; xgs_last_error() holds the thread-local message.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "launchers.h"
+#include "xgs.h"
+
+using namespace xgs;
+
+namespace xgs {
+static std::atomic<long long> g_launches{0};
+static std::atomic<int> g_prof_on{0};
+static std::mutex g_prof_mu;
+static std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> g_prof;
+
+void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+ProfScope::ProfScope(const char* t, cudaStream_t st) : tag(t), s(st), ev0(nullptr) {
+  if (!g_prof_on.load()) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) == cudaSuccess && cudaEventRecord(e, s) == cudaSuccess) ev0 = e;
+}
+ProfScope::~ProfScope() {
+  if (!ev0) return;
+  cudaEvent_t e1;
+  if (cudaEventCreate(&e1) != cudaSuccess) return;
+  cudaEventRecord(e1, s);
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof[tag].push_back({(cudaEvent_t)ev0, e1});
+}
+}  // namespace xgs
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return CUDA_ERROR;
+}
+int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+bool valid_dtype(int dt) { return dt == F32 || dt == F64 || dt == BF16; }
+
+int check_rows(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx) {
+  if (!valid_dtype(dtype)) return fail(INVALID_INPUT, "unsupported dtype");
+  if (n < 0 || d < 1 || ldx < d) return fail(INVALID_INPUT, "bad row shape");
+  if (d > 8192) return fail(NOT_SUPPORTED, "feature dim > 8192");
+  if (n > 0 && !x) return fail(INVALID_INPUT, "null rows");
+  return OK;
+}
+}  // namespace
+
+extern "C" {
+
+int xgs_abi_version(void) { return 1; }
+
+const char* xgs_last_error(void) { return g_err.c_str(); }
+
+int xgs_device_sm_count(void) { return sm_count(); }
+
+long long xgs_launch_count(void) { return g_launches.load(); }
+
+int xgs_profile_enable(int on) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  for (auto& kv : g_prof)
+    for (auto& pr : kv.second) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+  g_prof.clear();
+  g_prof_on.store(on ? 1 : 0);
+  return OK;
+}
+
+int xgs_profile_read(const char* tag, double* total_ms, long long* count) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  double tot = 0.0;
+  long long c = 0;
+  auto it = g_prof.find(tag ? tag : "");
+  if (it != g_prof.end())
+    for (auto& pr : it->second) {
+      if (cudaEventSynchronize(pr.second) != cudaSuccess) return cuda_fail(cudaGetLastError(), "profile");
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, pr.first, pr.second);
+      tot += ms;
+      c++;
+    }
+  if (total_ms) *total_ms = tot;
+  if (count) *count = c;
+  return OK;
+}
+
+// ---------------------------------------------------------------- VQ
+
+size_t xgs_vq_assign_workspace(int64_t n, int64_t k, int64_t d, int dtype, int64_t ldx) {
+  return screen_workspace_bytes(n, k, d, dtype, ldx);
+}
+
+int xgs_vq_assign(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E, int64_t k,
+                  int64_t* codes, void* ws, size_t ws_bytes, int32_t* stats_out, void* stream) {
+  int rc = check_rows(x, dtype, n, d, ldx);
+  if (rc) return rc;
+  if (k == 0) return fail(INVALID_STATE, "cannot assign against an empty codebook");
+  if (k < 0 || !E || (n > 0 && !codes)) return fail(INVALID_INPUT, "bad codebook or output");
+  if (n > 0x7fffffff) return fail(NOT_SUPPORTED, "more than 2^31-1 rows per call");
+  if (n == 0) return OK;
+  if (ws_bytes < screen_workspace_bytes(n, k, d, dtype, ldx)) return fail(INVALID_INPUT, "workspace too small");
+  SumPlan pd;
+  if (!build_sum_plan((int)d, &pd)) return fail(NOT_SUPPORTED, "feature dim too large for the exact plan");
+  // Rigorous screening bound (see vq_screen_sm100.cu): fp16 unit roundoff u
+  // on power-of-2-scaled operands, fp32 accumulation over Dp products (2 ulp
+  // per add), fp32 epilogue rounding, subnormal term c4, 25% slack.
+  const double u = std::ldexp(1.0, -11);
+  const double dp = (double)((d + 63) / 64 * 64);
+  const double gacc = (dp + 32.0) * std::ldexp(1.0, -22);
+  const double c1 = 1.25 * (2.0 * ((2 * u + u * u) + gacc * (1 + u) * (1 + u)) + std::ldexp(1.0, -21));
+  const double c2 = 1.25 * std::ldexp(1.0, -21);
+  const double c4 = 1.25 * 4.0 * std::sqrt(dp) * std::ldexp(1.0, -37);
+  ScreenArgs a;
+  a.x = x;
+  a.dtype = dtype;
+  a.n = n;
+  a.d = d;
+  a.ldx = ldx;
+  a.E = E;
+  a.k = k;
+  a.codes = codes;
+  a.ws = ws;
+  a.ws_bytes = ws_bytes;
+  a.c1 = (float)c1;
+  a.c2 = (float)c2;
+  a.c4 = (float)c4;
+  a.pd = &pd;
+  a.sm_count = sm_count();
+  cudaError_t e = launch_screen_assign(a, (cudaStream_t)stream, stats_out);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_vq_assign");
+  return OK;
+}
+
+// Exact fp64 path: squared distances / codes / confidence mask / probabilities.
+int xgs_vq_exact(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E, int64_t k,
+                 int mode, double tau, double gamma, double* out_dist, double* out_prob, int64_t* codes,
+                 uint8_t* mask, void* stream) {
+  int rc = check_rows(x, dtype, n, d, ldx);
+  if (rc) return rc;
+  if (k == 0) return fail(INVALID_STATE, "cannot assign against an empty codebook");
+  if (k < 0 || !E) return fail(INVALID_INPUT, "bad codebook");
+  if (n == 0) return OK;
+  if (((mode & EX_WRITE_DIST) && !out_dist) || ((mode & EX_WRITE_PROB) && !out_prob) ||
+      ((mode & EX_WRITE_CODE) && !codes) || ((mode & EX_CONF_MASK) && !mask))
+    return fail(INVALID_INPUT, "null output for requested mode");
+  if ((mode & (EX_CONF_MASK | EX_WRITE_PROB)) && k > 16384) return fail(NOT_SUPPORTED, "confidence with K > 16384");
+  if ((mode & (EX_CONF_MASK | EX_WRITE_PROB)) && !(tau > 0)) return fail(INVALID_INPUT, "tau must be positive");
+  SumPlan pd, pk;
+  if (!build_sum_plan((int)d, &pd)) return fail(NOT_SUPPORTED, "feature dim too large");
+  if (!build_sum_plan((int)(k <= 8192 ? k : 0), &pk) && (mode & (EX_CONF_MASK | EX_WRITE_PROB)))
+    return fail(NOT_SUPPORTED, "K too large for the exact softmax plan");
+  if (k > 8192 && (mode & (EX_CONF_MASK | EX_WRITE_PROB))) return fail(NOT_SUPPORTED, "confidence with K > 8192");
+  ExactArgs a{};
+  a.x = x;
+  a.dtype = dtype;
+  a.n = n;
+  a.d = d;
+  a.ldx = ldx;
+  a.E = E;
+  a.k = k;
+  a.mode = mode;
+  a.tau = tau;
+  a.gamma = gamma;
+  a.out_dist = out_dist;
+  a.out_prob = out_prob;
+  a.codes = codes;
+  a.mask = mask;
+  cudaError_t e = launch_exact_rows(a, pd, pk, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_vq_exact");
+  return OK;
+}
+
+size_t xgs_vq_accumulate_workspace(int64_t n, int64_t k) { return accumulate_workspace_bytes(n, k); }
+
+int xgs_vq_accumulate(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const int64_t* codes,
+                      const uint8_t* mask, int64_t k, double* counts, double* sums, void* ws, size_t ws_bytes,
+                      void* stream) {
+  int rc = check_rows(x, dtype, n, d, ldx);
+  if (rc) return rc;
+  if (k < 1 || !counts || !sums || (n > 0 && !codes)) return fail(INVALID_INPUT, "bad accumulate arguments");
+  if (n > 0x7fffffff) return fail(NOT_SUPPORTED, "more than 2^31-1 rows per call");
+  if (ws_bytes < accumulate_workspace_bytes(n, k)) return fail(INVALID_INPUT, "workspace too small");
+  cudaError_t e = launch_accumulate(x, dtype, n, d, ldx, codes, mask, k, counts, sums, ws, ws_bytes, sm_count(),
+                                    (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_vq_accumulate");
+  return OK;
+}
+
+int xgs_vq_ema(double lam, double eps, int64_t k, int64_t d, const double* N, const double* M,
+               const double* counts, const double* sums, double* N_out, double* M_out, double* E_out,
+               void* stream) {
+  if (!(lam >= 0.0 && lam < 1.0)) return fail(INVALID_INPUT, "EMA decay must lie in [0, 1)");
+  if (k < 0 || d < 1) return fail(INVALID_INPUT, "bad codebook shape");
+  if (k > 0 && (!N || !M || !counts || !sums || !N_out || !M_out || !E_out))
+    return fail(INVALID_INPUT, "null buffer");
+  cudaError_t e = launch_ema(lam, 1.0 - lam, eps, k, d, N, M, counts, sums, N_out, M_out, E_out,
+                             (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_vq_ema");
+  return OK;
+}
+
+int xgs_vq_revive(int64_t k, int64_t d, double eps, const double* ring, int64_t cap, const int64_t* dead_k,
+                  const int64_t* ring_rows, int64_t n_dead, double* N, double* M, double* E, void* stream) {
+  if (n_dead < 0 || n_dead > k || d < 1) return fail(INVALID_INPUT, "bad revive arguments");
+  if (n_dead > 0 && (!ring || !dead_k || !ring_rows || !N || !M || !E)) return fail(INVALID_INPUT, "null buffer");
+  const double n_new = 1.0 + eps;
+  const double denom = n_new + eps;
+  cudaError_t e = launch_revive(k, d, n_new, denom, ring, cap, dead_k, ring_rows, n_dead, N, M, E,
+                                (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_vq_revive");
+  return OK;
+}
+
+int xgs_vq_ring_write(const void* x, int dtype, int64_t ldx, int64_t row0, int64_t nrows, int64_t d,
+                      double* ring, int64_t cap, int64_t phys0, void* stream) {
+  if (!valid_dtype(dtype) || nrows < 0 || row0 < 0 || cap < 1 || nrows > cap || phys0 < 0 || phys0 >= cap)
+    return fail(INVALID_INPUT, "bad ring write");
+  if (nrows > 0 && (!x || !ring)) return fail(INVALID_INPUT, "null buffer");
+  cudaError_t e = launch_ring_write(x, dtype, ldx, row0, nrows, d, ring, cap, phys0, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_vq_ring_write");
+  return OK;
+}
+
+int xgs_gather_rows_f64(const double* src, int64_t d, const int64_t* rows, int64_t n, double* dst, void* stream) {
+  if (n < 0 || d < 1) return fail(INVALID_INPUT, "bad gather");
+  if (n > 0 && (!src || !rows || !dst)) return fail(INVALID_INPUT, "null buffer");
+  cudaError_t e = launch_gather_rows(src, d, rows, n, dst, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_gather_rows_f64");
+  return OK;
+}
+
+}  // extern "C"

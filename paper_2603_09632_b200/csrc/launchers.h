@@ -1,0 +1,96 @@
+// Host-side launchers shared between the kernel translation units and the
+// C-ABI layer (capi.cu).  No torch types anywhere: plain pointers + sizes.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include "common.cuh"
+
+namespace xgs {
+
+// ---------------- launch accounting + opt-in event profiler (capi.cu) ----------------
+// Every kernel launch is counted; when profiling is on, the named kernels are
+// bracketed by CUDA events recorded on their own stream.
+void count_launches(int n);
+struct ProfScope {
+  ProfScope(const char* tag, cudaStream_t s);
+  ~ProfScope();
+  const char* tag;
+  cudaStream_t s;
+  void* ev0;
+};
+
+// ---------------- exact fp64 path (vq_exact.cu) ----------------
+enum ExactMode : int {
+  EX_WRITE_DIST = 1,   // out_dist[row*K + k] = exact squared distance
+  EX_WRITE_CODE = 2,   // codes[row] = argmin (first minimum)
+  EX_CONF_MASK = 4,    // mask[row] = max softmax(-sqrt(d)/tau) >= gamma
+  EX_WRITE_PROB = 8,   // out_prob[row*K + k] = softmax probabilities
+};
+struct ExactArgs {
+  const void* x;
+  int dtype;
+  int64_t n, d, ldx;
+  const double* E;
+  int64_t k;
+  const int32_t* rows;      // optional row list (else rows 0..n-1)
+  const int32_t* nrows_dev; // optional device count for the row list
+  int mode;
+  double tau, gamma;
+  double* out_dist;
+  double* out_prob;
+  int64_t* codes;
+  uint8_t* mask;
+};
+cudaError_t launch_exact_rows(const ExactArgs& a, const SumPlan& pd, const SumPlan& pk,
+                              cudaStream_t s);
+
+// Candidate re-rank queue entries written by the screening GEMM.
+constexpr int kCandCap = 8;
+struct RerankEntry {
+  int32_t row;
+  int32_t cnt;
+  int32_t cand[kCandCap];
+};
+cudaError_t launch_rerank(const void* x, int dtype, int64_t d, int64_t ldx, const double* E,
+                          const RerankEntry* q, const int32_t* qcount, int64_t qcap,
+                          int64_t* codes, const SumPlan& pd, cudaStream_t s);
+
+// ---------------- tcgen05 screening GEMM (vq_screen_sm100.cu) ----------------
+struct ScreenArgs {
+  const void* x;        // input rows (any dtype); scaled fp16 copy made per call
+  int dtype;
+  int64_t n, d, ldx;
+  const double* E;      // fp64 master codebook (K x D)
+  int64_t k;
+  int64_t* codes;       // out: int64 codes for rows resolved in the epilogue
+  void* ws;             // workspace (see screen_workspace_bytes)
+  size_t ws_bytes;
+  float c1, c2, c4;     // error-bound coefficients (host computed)
+  const SumPlan* pd;
+  int sm_count;
+};
+size_t screen_workspace_bytes(int64_t n, int64_t k, int64_t d, int dtype, int64_t ldx);
+cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* host_stats);
+
+// ---------------- codebook update (vq_update.cu) ----------------
+size_t accumulate_workspace_bytes(int64_t n, int64_t k);
+cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx,
+                              const int64_t* codes, const uint8_t* mask, int64_t k,
+                              double* counts, double* sums, void* ws, size_t ws_bytes,
+                              int sm_count, cudaStream_t s);
+cudaError_t launch_ema(double lam, double one_minus_lam, double eps, int64_t k, int64_t d,
+                       const double* N, const double* M, const double* counts, const double* sums,
+                       double* N_out, double* M_out, double* E_out, cudaStream_t s);
+cudaError_t launch_revive(int64_t k, int64_t d, double n_new, double denom, const double* ring,
+                          int64_t cap, const int64_t* dead_k, const int64_t* ring_rows,
+                          int64_t n_dead, double* N, double* M, double* E, cudaStream_t s);
+cudaError_t launch_ring_write(const void* x, int dtype, int64_t ldx, int64_t row0, int64_t nrows,
+                              int64_t d, double* ring, int64_t cap, int64_t phys0,
+                              cudaStream_t s);
+cudaError_t launch_gather_rows(const double* src, int64_t d, const int64_t* rows, int64_t n,
+                               double* dst, cudaStream_t s);
+
+}  // namespace xgs

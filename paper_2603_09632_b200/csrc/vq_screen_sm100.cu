@@ -1,0 +1,562 @@
+// tcgen05 screening GEMM for VQ assignment (sm_100a) with an exact re-rank.
+//
+// The reference's assignment (vq.py:69-87) is argmin_k of fp64 pairwise-summed
+// ||x - e_k||^2.  On B200 we split it into
+//   1. screen:  s_k = ||e_k||^2 - 2 x.e_k with an fp16 x fp16 -> fp32 tcgen05
+//      GEMM (kind::f16; TMA-staged 128x64 / 256x64 SW128 tiles, 4-stage
+//      mbarrier ring, fp32 accumulators in TMEM, double-buffered 2 x 256
+//      columns).  Rows and the codebook are scaled by exact powers of two so
+//      their max |element| lands in [2^14, 2^15): fp16 then rounds with unit
+//      roundoff u = 2^-11 (8x tighter than bf16 at the same tensor rate) and
+//      subnormals are negligible.  A rigorous per-(row, code) error bound
+//      B_k = c1*|x|*|e_k| + c2*|e_k|^2 (+ c3*|x|^2) covers fp16 operand
+//      rounding, fp32 accumulation and the fp64 reference's own rounding;
+//   2. candidate epilogue: TMEM lane i IS row i of the tile, so each epilogue
+//      thread owns one row and keeps U = min_k (s_k + B_k) and the codes with
+//      s_k - B_k <= U in registers/local memory (no shuffles needed).  The true
+//      fp64 argmin is provably in that set;
+//   3. rows with exactly one candidate are resolved in the epilogue; rows with
+//      2..8 are queued for the exact fp64 re-rank (rerank_kernel); rows whose
+//      list overflowed go to the exact all-codes kernel.
+// Codes are therefore bit-identical to the reference for every row.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cuda_fp16.h>
+
+#include "launchers.h"
+
+namespace xgs {
+
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int THREADS = 192;  // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2..5 epilogue
+constexpr int CONST_BYTES = 2 * 3 * BN * 4;
+constexpr int BAR_BYTES = (2 * STAGES + 4) * 8 + 16;
+constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + CONST_BYTES + BAR_BYTES;
+// kind::f16 instruction descriptor: D=f32, A=B=f16 (format 0), both K-major,
+// N=256, M=128.
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+struct ScreenParams {
+  int64_t n;
+  int num_m_tiles, num_n_chunks, num_k_blocks;
+  const float* xn;
+  const float* xf;
+  const float* cn;
+  const float* ce1;
+  const float* ce2;
+  float c3;
+  int64_t* codes;
+  RerankEntry* rq;
+  int32_t* rq_count;
+  int32_t* fq;
+  int32_t* fq_count;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_try_wait(a, parity)) {
+  }
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__global__ void __launch_bounds__(THREADS, 1)
+screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              ScreenParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* cconst = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + CONST_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < STAGES; i++) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; i++) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_m_tiles; tile += gridDim.x)
+        for (int nc = 0; nc < p.num_n_chunks; nc++)
+          for (int kb = 0; kb < p.num_k_blocks; kb++) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * STAGE_BYTES;
+            mbar_expect_tx(&full[stage], STAGE_BYTES);
+            tma_load_2d(sa, &tmA, kb * BK, tile * BM, &full[stage]);
+            tma_load_2d(sa + A_BYTES, &tmB, kb * BK, nc * BN, &full[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (int tile = blockIdx.x; tile < p.num_m_tiles; tile += gridDim.x)
+        for (int nc = 0; nc < p.num_n_chunks; nc++) {
+          mbar_wait(&tempty[acc], aphase ^ 1);
+          tc_after();
+          const uint32_t dt = tmem_base + (uint32_t)(acc * BN);
+          for (int kb = 0; kb < p.num_k_blocks; kb++) {
+            mbar_wait(&full[stage], phase);
+            tc_after();
+            const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+            const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; kk++)
+              mma_f16(dt, sw128_desc(sa + kk * 32), sw128_desc(sb + kk * 32), (kb | kk) != 0);
+            umma_commit(&empty[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          umma_commit(&tfull[acc]);
+          acc ^= 1;
+          if (acc == 0) aphase ^= 1;
+        }
+    }
+  } else {
+    // ---------------- epilogue: one thread per tile row ----------------
+    const int q = warp & 3;
+    const int et = threadIdx.x - 64;
+    const unsigned lt = (1u << lane) - 1u;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < p.num_m_tiles; tile += gridDim.x) {
+      const int64_t row = (int64_t)tile * BM + q * 32 + lane;
+      const bool live = row < p.n;
+      const float xn = live ? p.xn[row] : 0.f;
+      const float xf = live ? p.xf[row] : 0.f;   // -2 * (row scale)^-1 * (codebook scale)^-1
+      const float slack = 2.f * p.c3 * xn * xn;  // fp64-reference rounding margin
+      float U = __int_as_float(0x7f800000);
+      int cnt = 0;
+      bool ovf = false;
+      int ck[kCandCap];
+      float cl[kCandCap];
+      for (int nc = 0; nc < p.num_n_chunks; nc++) {
+        float* cc = cconst + acc * 3 * BN;
+        for (int i = et; i < BN; i += 128) {
+          const int kk = nc * BN + i;
+          cc[i] = p.cn[kk];
+          cc[BN + i] = p.ce1[kk];
+          cc[2 * BN + i] = p.ce2[kk];
+        }
+        epi_bar();
+        mbar_wait(&tfull[acc], aphase);
+        tc_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c0, r);
+#pragma unroll
+          for (int i = 0; i < 32; i++) {
+            const int c = c0 + i;
+            const float s = fmaf(xf, __uint_as_float(r[i]), cc[c]);
+            const float b = fmaf(xn, cc[BN + c], cc[2 * BN + c]);
+            const float lo = s - b;
+            U = fminf(U, s + b);
+            if (lo <= U + slack && !ovf) {
+              if (cnt == kCandCap) {
+                int w = 0;
+                for (int j = 0; j < kCandCap; j++)
+                  if (cl[j] <= U + slack) {
+                    ck[w] = ck[j];
+                    cl[w] = cl[j];
+                    w++;
+                  }
+                cnt = w;
+              }
+              if (cnt < kCandCap) {
+                ck[cnt] = nc * BN + c;
+                cl[cnt] = lo;
+                cnt++;
+              } else {
+                ovf = true;
+              }
+            }
+          }
+        }
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+      // ---- finalize the row ----
+      int nk = 0, kbest = -1;
+      int fin[kCandCap];
+      if (!ovf)
+        for (int j = 0; j < cnt; j++)
+          if (cl[j] <= U + slack) {
+            fin[nk++] = ck[j];
+            kbest = ck[j];
+          }
+      const bool to_fallback = live && (ovf || nk == 0);
+      const bool to_rerank = live && !to_fallback && nk > 1;
+      if (live && !to_fallback && nk == 1) p.codes[row] = kbest;
+      unsigned m = __ballot_sync(FULL, to_rerank);
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(p.rq_count, __popc(m));
+        base = __shfl_sync(FULL, base, leader);
+        if (to_rerank) {
+          RerankEntry* e = p.rq + base + __popc(m & lt);
+          e->row = (int32_t)row;
+          e->cnt = nk;
+          for (int j = 0; j < kCandCap; j++) e->cand[j] = j < nk ? fin[j] : 0;
+        }
+      }
+      m = __ballot_sync(FULL, to_fallback);
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(p.fq_count, __popc(m));
+        base = __shfl_sync(FULL, base, leader);
+        if (to_fallback) p.fq[base + __popc(m & lt)] = (int32_t)row;
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+}
+
+// ---- operand preparation ----
+
+// max |E| over the whole fp64 codebook (non-negative floats order like ints).
+__global__ void absmax_kernel(const double* __restrict__ E, int64_t n, unsigned* out) {
+  float m = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, (float)fabs(E[i]));
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(FULL, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+// exponent e with m = f * 2^e, f in [0.5, 1); 0 for m == 0
+__device__ __forceinline__ int exp_of(float m) {
+  int e = 0;
+  if (m > 0.f) frexpf(m, &e);
+  return e;
+}
+
+// Codebook: fp64 E (K x D) -> power-of-2-scaled, zero-padded fp16 (Kp x Dp) +
+// per-code bound constants.  Padded codes get s = +inf (never candidates).
+__global__ void prep_codebook_kernel(const double* __restrict__ E, int64_t k, int64_t d, int64_t kp, int64_t dp,
+                                     float c1, float c2, float c4, const unsigned* __restrict__ emax_bits,
+                                     __half* __restrict__ Eb, float* cn, float* ce1, float* ce2) {
+  const int64_t code = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (code >= kp) return;
+  const float emax = __uint_as_float(*emax_bits);
+  const double sc = ldexp(1.0, 15 - exp_of(emax));
+  double ss = 0.0;
+  for (int64_t j = lane; j < dp; j += 32) {
+    const double v = (code < k && j < d) ? E[code * d + j] : 0.0;
+    ss = fma(v, v, ss);
+    Eb[code * dp + j] = __double2half(v * sc);
+  }
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(FULL, ss, o);
+  if (lane == 0) {
+    if (code < k) {
+      const float en = (float)sqrt(ss) * (1.f + 1e-6f);
+      cn[code] = (float)ss;
+      ce1[code] = c1 * en + c4 * emax;
+      ce2[code] = c2 * en * en;
+    } else {
+      cn[code] = __int_as_float(0x7f800000);
+      ce1[code] = 0.f;
+      ce2[code] = 0.f;
+    }
+  }
+}
+
+// Rows: any dtype -> power-of-2-scaled, zero-padded fp16 (n x dp), an upper
+// bound on |x| and the epilogue factor xf = -2 / (row scale * codebook scale).
+template <typename X>
+__global__ void prep_rows_kernel(const X* __restrict__ x, int64_t n, int64_t d, int64_t ldx, int64_t dp,
+                                 const unsigned* __restrict__ emax_bits, __half* __restrict__ Ab,
+                                 float* __restrict__ xn, float* __restrict__ xf, float inflate) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const X* xr = x + row * ldx;
+  double ss = 0.0;
+  float mx = 0.f;
+  for (int64_t j = lane; j < d; j += 32) {
+    const double v = ld64(xr, j);
+    ss = fma(v, v, ss);
+    mx = fmaxf(mx, (float)fabs(v));
+  }
+  for (int o = 16; o; o >>= 1) {
+    ss += __shfl_xor_sync(FULL, ss, o);
+    mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
+  }
+  const int ex = exp_of(mx);
+  const double sc = ldexp(1.0, 15 - ex);
+  for (int64_t j0 = (int64_t)lane * 8; j0 < dp; j0 += 256) {
+    __align__(16) __half v8[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int64_t j = j0 + u;
+      v8[u] = __double2half(j < d ? ld64(xr, j) * sc : 0.0);
+    }
+    *reinterpret_cast<uint4*>(Ab + row * dp + j0) = *reinterpret_cast<const uint4*>(v8);
+  }
+  if (lane == 0) {
+    xn[row] = (float)sqrt(ss) * inflate;
+    const int ee = exp_of(__uint_as_float(*emax_bits));
+    xf[row] = -ldexpf(1.f, (ex - 15) + (ee - 15) + 1);
+  }
+}
+
+struct ScreenWs {
+  size_t off_ab, off_xn, off_xf, off_eb, off_cn, off_ce1, off_ce2, off_rq, off_fq, off_cnt, total;
+  int64_t kp, dp;
+};
+
+ScreenWs screen_ws(int64_t n, int64_t k, int64_t d) {
+  ScreenWs w;
+  w.kp = (k + BN - 1) / BN * BN;
+  w.dp = (d + BK - 1) / BK * BK;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 1023) / 1024 * 1024; return r; };
+  const size_t nn = (size_t)(n > 0 ? n : 1);
+  w.off_ab = take(nn * (size_t)w.dp * 2);
+  w.off_xn = take(nn * 4);
+  w.off_xf = take(nn * 4);
+  w.off_eb = take((size_t)w.kp * (size_t)w.dp * 2);
+  w.off_cn = take((size_t)w.kp * 4);
+  w.off_ce1 = take((size_t)w.kp * 4);
+  w.off_ce2 = take((size_t)w.kp * 4);
+  w.off_rq = take(nn * sizeof(RerankEntry));
+  w.off_fq = take(nn * 4);
+  w.off_cnt = take(64);
+  w.total = o;
+  return w;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint64_t ld_bytes, uint32_t box_inner,
+              uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {ld_bytes};
+  cuuint32_t box[2] = {box_inner, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+size_t screen_workspace_bytes(int64_t n, int64_t k, int64_t d, int dtype, int64_t ldx) {
+  (void)dtype;
+  (void)ldx;
+  return screen_ws(n, k, d).total;
+}
+
+cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* host_stats) {
+  const ScreenWs w = screen_ws(a.n, a.k, a.d);
+  if (a.ws_bytes < w.total) return cudaErrorInvalidValue;
+  char* base = static_cast<char*>(a.ws);
+  __half* Ab = reinterpret_cast<__half*>(base + w.off_ab);
+  float* xn = reinterpret_cast<float*>(base + w.off_xn);
+  float* xf = reinterpret_cast<float*>(base + w.off_xf);
+  __half* Eb = reinterpret_cast<__half*>(base + w.off_eb);
+  float* cn = reinterpret_cast<float*>(base + w.off_cn);
+  float* ce1 = reinterpret_cast<float*>(base + w.off_ce1);
+  float* ce2 = reinterpret_cast<float*>(base + w.off_ce2);
+  RerankEntry* rq = reinterpret_cast<RerankEntry*>(base + w.off_rq);
+  int32_t* fq = reinterpret_cast<int32_t*>(base + w.off_fq);
+  int32_t* cnt = reinterpret_cast<int32_t*>(base + w.off_cnt);
+  unsigned* emax = reinterpret_cast<unsigned*>(cnt + 4);
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(cnt, 0, 64, s)) != cudaSuccess) return e;
+
+  {
+  ProfScope prof("vq_prep", s);
+  absmax_kernel<<<148, 256, 0, s>>>(a.E, a.k * a.d, emax); count_launches(1);
+  prep_codebook_kernel<<<(unsigned)((w.kp + 7) / 8), 256, 0, s>>>(a.E, a.k, a.d, w.kp, w.dp, a.c1, a.c2, a.c4,
+                                                                  emax, Eb, cn, ce1, ce2); count_launches(1);
+  const float inflate = 1.f + 1e-6f;
+  const unsigned rblocks = (unsigned)((a.n + 7) / 8);
+  switch (a.dtype) {
+    case F32: prep_rows_kernel<float><<<rblocks, 256, 0, s>>>((const float*)a.x, a.n, a.d, a.ldx, w.dp, emax, Ab, xn, xf, inflate); count_launches(1); break;
+    case F64: prep_rows_kernel<double><<<rblocks, 256, 0, s>>>((const double*)a.x, a.n, a.d, a.ldx, w.dp, emax, Ab, xn, xf, inflate); count_launches(1); break;
+    default: prep_rows_kernel<uint16_t><<<rblocks, 256, 0, s>>>((const uint16_t*)a.x, a.n, a.d, a.ldx, w.dp, emax, Ab, xn, xf, inflate); count_launches(1);
+  }
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+
+  CUtensorMap tmA, tmB;
+  if (!make_map(&tmA, Ab, (uint64_t)w.dp, (uint64_t)a.n, (uint64_t)w.dp * 2, BK, BM) ||
+      !make_map(&tmB, Eb, (uint64_t)w.dp, (uint64_t)w.kp, (uint64_t)w.dp * 2, BK, BN))
+    return cudaErrorInvalidValue;
+
+  ScreenParams p;
+  p.n = a.n;
+  p.num_m_tiles = (int)((a.n + BM - 1) / BM);
+  p.num_n_chunks = (int)(w.kp / BN);
+  p.num_k_blocks = (int)(w.dp / BK);
+  p.xn = xn;
+  p.xf = xf;
+  p.cn = cn;
+  p.ce1 = ce1;
+  p.ce2 = ce2;
+  p.c3 = 1.0e-12f;
+  p.codes = a.codes;
+  p.rq = rq;
+  p.rq_count = cnt;
+  p.fq = fq;
+  p.fq_count = cnt + 1;
+  static bool attr = false;
+  if (!attr) {
+    if ((e = cudaFuncSetAttribute(screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) !=
+        cudaSuccess)
+      return e;
+    attr = true;
+  }
+  int grid = p.num_m_tiles < a.sm_count ? p.num_m_tiles : a.sm_count;
+  if (grid < 1) grid = 1;
+  {
+    ProfScope prof("vq_screen", s);
+    screen_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, p); count_launches(1);
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+
+  // exact re-rank of the multi-candidate rows, exact scan of overflowed rows
+  ProfScope prof("vq_rerank", s);
+  if ((e = launch_rerank(a.x, a.dtype, a.d, a.ldx, a.E, rq, cnt, a.n, a.codes, *a.pd, s)) != cudaSuccess) return e;
+  ExactArgs ea{};
+  ea.x = a.x;
+  ea.dtype = a.dtype;
+  ea.n = a.n;
+  ea.d = a.d;
+  ea.ldx = a.ldx;
+  ea.E = a.E;
+  ea.k = a.k;
+  ea.rows = fq;
+  ea.nrows_dev = cnt + 1;
+  ea.mode = EX_WRITE_CODE;
+  ea.codes = a.codes;
+  SumPlan pk_unused;
+  pk_unused.n = 0;
+  pk_unused.n_leaves = 0;
+  pk_unused.n_ops = 0;
+  if ((e = launch_exact_rows(ea, *a.pd, pk_unused, s)) != cudaSuccess) return e;
+  if (host_stats) {
+    if ((e = cudaMemcpyAsync(host_stats, cnt, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace xgs

@@ -1,0 +1,365 @@
+// Codebook-update kernels: accumulate (vq.py:90-100), EMA (vq.py:103-109),
+// dead-code revival (vq.py:173-190) and the reservoir ring (core.py:178-203).
+//
+// accumulate is bit-identical to bincount + np.add.at: np.add.at adds rows
+// into sums[code] sequentially in ascending row order, i.e. one fp64 chain per
+// (k, d) starting from +0.0.  We (1) count rows per (tile, code), (2) scan to
+// per-(tile, code) offsets, (3) stably scatter row ids into code-sorted order
+// (warp match_any ranks, tiles walked in order) and (4) run one chain per
+// (k, d) over the sorted row ids: lanes own consecutive d so each row read is
+// a coalesced 128-512 B segment.  HBM traffic ~ one read of X + 8 B/row.
+#include "launchers.h"
+
+namespace xgs {
+
+namespace {
+
+constexpr int kTileTarget = 2048;  // number of row tiles (bounds the T x K table)
+
+struct AccPlan {
+  int64_t tile_rows, tiles;
+  size_t off_tile_counts, off_code_count, off_code_start, off_sorted, total;
+};
+
+AccPlan acc_plan(int64_t n, int64_t k) {
+  AccPlan p;
+  int64_t tr = (n + kTileTarget - 1) / kTileTarget;
+  if (tr < 256) tr = 256;
+  tr = (tr + 31) / 32 * 32;
+  p.tile_rows = tr;
+  p.tiles = n > 0 ? (n + tr - 1) / tr : 1;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 255) / 256 * 256; return r; };
+  p.off_tile_counts = take(sizeof(int32_t) * (size_t)p.tiles * (size_t)k);
+  p.off_code_count = take(sizeof(int32_t) * (size_t)k);
+  p.off_code_start = take(sizeof(int32_t) * (size_t)(k + 1));
+  p.off_sorted = take(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+  p.total = o;
+  return p;
+}
+
+__device__ __forceinline__ int row_code(const int64_t* codes, const uint8_t* mask, int64_t r) {
+  if (mask && !mask[r]) return -1;
+  return (int)codes[r];
+}
+
+// (1) per-(tile, code) counts; one warp per tile.
+__global__ void acc_hist_kernel(const int64_t* __restrict__ codes, const uint8_t* __restrict__ mask,
+                                int64_t n, int64_t k, int64_t tile_rows, int32_t* tile_counts) {
+  const int64_t t = blockIdx.x;
+  const int lane = threadIdx.x;
+  int32_t* tc = tile_counts + t * k;
+  const int64_t r0 = t * tile_rows, r1 = min(n, r0 + tile_rows);
+  for (int64_t base = r0; base < r1; base += 32) {
+    const int64_t r = base + lane;
+    const int c = r < r1 ? row_code(codes, mask, r) : -1;
+    const unsigned peers = __match_any_sync(FULL, c);
+    if (c >= 0 && lane == __ffs(peers) - 1) tc[c] += __popc(peers);
+    __syncwarp();
+  }
+}
+
+// (2a) exclusive scan over tiles for 32 codes per block; writes per-code totals.
+__global__ void __launch_bounds__(1024)
+acc_scan_tiles_kernel(int32_t* tile_counts, int64_t tiles, int64_t k, int32_t* code_count) {
+  __shared__ int32_t part[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t code = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t per = (tiles + 31) / 32;
+  const int64_t t0 = warp * per, t1 = min(tiles, t0 + per);
+  int32_t s = 0;
+  if (code < k)
+    for (int64_t t = t0; t < t1; t++) s += tile_counts[t * k + code];
+  part[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t run = 0;
+    for (int w = 0; w < 32; w++) {
+      const int32_t v = part[w][lane];
+      part[w][lane] = run;
+      run += v;
+    }
+    if (code < k) code_count[code] = run;
+  }
+  __syncthreads();
+  int32_t run = part[warp][lane];
+  if (code < k)
+    for (int64_t t = t0; t < t1; t++) {
+      const int32_t v = tile_counts[t * k + code];
+      tile_counts[t * k + code] = run;
+      run += v;
+    }
+}
+
+// (2b) exclusive scan of the K code totals -> code_start[0..K].
+__global__ void __launch_bounds__(1024)
+acc_scan_codes_kernel(const int32_t* __restrict__ code_count, int64_t k, int32_t* code_start) {
+  __shared__ int32_t part[1024];
+  const int64_t per = (k + 1023) / 1024;
+  const int64_t c0 = threadIdx.x * per, c1 = min(k, c0 + per);
+  int32_t s = 0;
+  for (int64_t c = c0; c < c1; c++) s += code_count[c];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t run = 0;
+    for (int i = 0; i < 1024; i++) {
+      const int32_t v = part[i];
+      part[i] = run;
+      run += v;
+    }
+    code_start[k] = run;
+  }
+  __syncthreads();
+  int32_t run = part[threadIdx.x];
+  for (int64_t c = c0; c < c1; c++) {
+    code_start[c] = run;
+    run += code_count[c];
+  }
+}
+
+// (3) stable scatter of row ids into code-sorted order; one warp per tile.
+__global__ void acc_scatter_kernel(const int64_t* __restrict__ codes, const uint8_t* __restrict__ mask,
+                                   int64_t n, int64_t k, int64_t tile_rows, int32_t* tile_off,
+                                   const int32_t* __restrict__ code_start, int32_t* sorted) {
+  const int64_t t = blockIdx.x;
+  const int lane = threadIdx.x;
+  int32_t* to = tile_off + t * k;
+  const int64_t r0 = t * tile_rows, r1 = min(n, r0 + tile_rows);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t base = r0; base < r1; base += 32) {
+    const int64_t r = base + lane;
+    const int c = r < r1 ? row_code(codes, mask, r) : -1;
+    const unsigned peers = __match_any_sync(FULL, c);
+    if (c >= 0) {
+      const int32_t pos = code_start[c] + to[c] + __popc(peers & lt);
+      sorted[pos] = (int32_t)r;
+    }
+    __syncwarp();
+    if (c >= 0 && lane == __ffs(peers) - 1) to[c] += __popc(peers);
+    __syncwarp();
+  }
+}
+
+template <typename X, int VEC>
+struct VecLoad;
+template <> struct VecLoad<float, 4> {
+  static __device__ __forceinline__ void go(const float* p, double* v) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  }
+};
+template <> struct VecLoad<uint16_t, 8> {
+  static __device__ __forceinline__ void go(const uint16_t* p, double* v) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      v[2 * i] = (double)__uint_as_float(w[i] << 16);
+      v[2 * i + 1] = (double)__uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+};
+template <typename X> struct VecLoad<X, 1> {
+  static __device__ __forceinline__ void go(const X* p, double* v) { v[0] = ld64(p, 0); }
+};
+template <> struct VecLoad<double, 2> {
+  static __device__ __forceinline__ void go(const double* p, double* v) {
+    const double2 q = __ldg(reinterpret_cast<const double2*>(p));
+    v[0] = q.x; v[1] = q.y;
+  }
+};
+
+// (4) one sequential fp64 chain per (k, d): warp = (code, 32*VEC dims).
+template <typename X, int VEC>
+__global__ void __launch_bounds__(256)
+acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
+                 const int32_t* __restrict__ code_start, const int32_t* __restrict__ sorted,
+                 double* __restrict__ counts, double* __restrict__ sums) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t nchunks = (d + 32 * VEC - 1) / (32 * VEC);
+  const int64_t code = gw / nchunks;
+  if (code >= k) return;
+  const int64_t d0 = (gw % nchunks) * 32 * VEC + (int64_t)lane * VEC;
+  const bool live = d0 < d;
+  const int32_t beg = code_start[code], end = code_start[code + 1];
+  double acc[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; v++) acc[v] = 0.0;
+  constexpr int U = 8;
+  for (int32_t b = beg; b < end; b += 32) {
+    const int cnt = min(32, end - b);
+    const int32_t my_row = lane < cnt ? sorted[b + lane] : 0;
+    int j = 0;
+    for (; j + U <= cnt; j += U) {
+      double val[U][VEC];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t row = __shfl_sync(FULL, my_row, j + u);
+        if (live) VecLoad<X, VEC>::go(x + row * ldx + d0, val[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++)
+#pragma unroll
+        for (int v = 0; v < VEC; v++) acc[v] = dadd(acc[v], val[u][v]);
+    }
+    for (; j < cnt; j++) {
+      const int64_t row = __shfl_sync(FULL, my_row, j);
+      double val[VEC];
+      if (live) {
+        VecLoad<X, VEC>::go(x + row * ldx + d0, val);
+#pragma unroll
+        for (int v = 0; v < VEC; v++) acc[v] = dadd(acc[v], val[v]);
+      }
+    }
+  }
+  if (live) {
+#pragma unroll
+    for (int v = 0; v < VEC; v++) sums[code * d + d0 + v] = acc[v];
+  }
+  if (d0 == 0) counts[code] = (double)(end - beg);
+}
+
+template <typename X, int VEC>
+cudaError_t launch_chain(const X* x, int64_t d, int64_t ldx, int64_t k, const int32_t* cs,
+                         const int32_t* sorted, double* counts, double* sums, cudaStream_t s) {
+  const int64_t nchunks = (d + 32 * VEC - 1) / (32 * VEC);
+  const int64_t warps = k * nchunks;
+  ProfScope prof("vq_chain", s);
+  acc_chain_kernel<X, VEC><<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(x, d, ldx, k, cs, sorted, counts, sums); count_launches(1);
+  return cudaGetLastError();
+}
+
+// EMA (vq.py:103-109): N' = lam*N + (1-lam)*c ; M' = lam*M + (1-lam)*s ;
+// E' = M' / (N' + eps).  One CTA per code row; safe in place.
+__global__ void ema_kernel(double lam, double oml, double eps, int64_t d, const double* N, const double* M,
+                           const double* __restrict__ counts, const double* __restrict__ sums,
+                           double* N_out, double* M_out, double* E_out) {
+  const int64_t k = blockIdx.x;
+  __shared__ double nk;
+  if (threadIdx.x == 0) nk = dadd(dmul(lam, N[k]), dmul(oml, counts[k]));
+  __syncthreads();
+  const double den = dadd(nk, eps);
+  for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+    const int64_t e = k * d + j;
+    const double m = dadd(dmul(lam, M[e]), dmul(oml, sums[e]));
+    M_out[e] = m;
+    E_out[e] = ddiv(m, den);
+  }
+  if (threadIdx.x == 0) N_out[k] = nk;
+}
+
+// Revival (vq.py:184-188): M_k = x ; N_k = 1+eps ; E_k = M_k / (N_k + eps).
+__global__ void revive_kernel(int64_t d, double n_new, double denom, const double* __restrict__ ring,
+                              const int64_t* __restrict__ dead_k, const int64_t* __restrict__ ring_rows,
+                              double* N, double* M, double* E) {
+  const int64_t i = blockIdx.x;
+  const int64_t k = dead_k[i];
+  const double* src = ring + ring_rows[i] * d;
+  for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+    const double v = src[j];
+    M[k * d + j] = v;
+    E[k * d + j] = ddiv(v, denom);
+  }
+  if (threadIdx.x == 0) N[k] = n_new;
+}
+
+template <typename X>
+__global__ void ring_write_kernel(const X* __restrict__ x, int64_t ldx, int64_t row0, int64_t d,
+                                  double* ring, int64_t cap, int64_t phys0) {
+  const int64_t j = blockIdx.x;
+  double* dst = ring + ((phys0 + j) % cap) * d;
+  const X* src = x + (row0 + j) * ldx;
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) dst[i] = ld64(src, i);
+}
+
+__global__ void gather_rows_kernel(const double* __restrict__ src, int64_t d, const int64_t* __restrict__ rows,
+                                   double* dst) {
+  const int64_t i = blockIdx.x;
+  for (int64_t j = threadIdx.x; j < d; j += blockDim.x) dst[i * d + j] = src[rows[i] * d + j];
+}
+
+}  // namespace
+
+size_t accumulate_workspace_bytes(int64_t n, int64_t k) { return acc_plan(n, k).total; }
+
+cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx,
+                              const int64_t* codes, const uint8_t* mask, int64_t k, double* counts,
+                              double* sums, void* ws, size_t ws_bytes, int sm_count, cudaStream_t s) {
+  (void)sm_count;
+  const AccPlan p = acc_plan(n, k);
+  if (ws_bytes < p.total) return cudaErrorInvalidValue;
+  char* w = static_cast<char*>(ws);
+  int32_t* tile_counts = reinterpret_cast<int32_t*>(w + p.off_tile_counts);
+  int32_t* code_count = reinterpret_cast<int32_t*>(w + p.off_code_count);
+  int32_t* code_start = reinterpret_cast<int32_t*>(w + p.off_code_start);
+  int32_t* sorted = reinterpret_cast<int32_t*>(w + p.off_sorted);
+  ProfScope prof("vq_accumulate", s);
+  cudaError_t e = cudaMemsetAsync(tile_counts, 0, sizeof(int32_t) * (size_t)p.tiles * (size_t)k, s);
+  if (e != cudaSuccess) return e;
+  if (n > 0) {
+    acc_hist_kernel<<<(unsigned)p.tiles, 32, 0, s>>>(codes, mask, n, k, p.tile_rows, tile_counts); count_launches(1);
+  }
+  acc_scan_tiles_kernel<<<(unsigned)((k + 31) / 32), 1024, 0, s>>>(tile_counts, p.tiles, k, code_count); count_launches(1);
+  acc_scan_codes_kernel<<<1, 1024, 0, s>>>(code_count, k, code_start); count_launches(1);
+  if (n > 0) {
+    acc_scatter_kernel<<<(unsigned)p.tiles, 32, 0, s>>>(codes, mask, n, k, p.tile_rows, tile_counts,
+                                                        code_start, sorted); count_launches(1);
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(x);
+  switch (dtype) {
+    case F32:
+      if (d % 4 == 0 && ldx % 4 == 0 && xa % 16 == 0)
+        return launch_chain<float, 4>((const float*)x, d, ldx, k, code_start, sorted, counts, sums, s);
+      return launch_chain<float, 1>((const float*)x, d, ldx, k, code_start, sorted, counts, sums, s);
+    case F64:
+      if (d % 2 == 0 && ldx % 2 == 0 && xa % 16 == 0)
+        return launch_chain<double, 2>((const double*)x, d, ldx, k, code_start, sorted, counts, sums, s);
+      return launch_chain<double, 1>((const double*)x, d, ldx, k, code_start, sorted, counts, sums, s);
+    default:
+      if (d % 8 == 0 && ldx % 8 == 0 && xa % 16 == 0)
+        return launch_chain<uint16_t, 8>((const uint16_t*)x, d, ldx, k, code_start, sorted, counts, sums, s);
+      return launch_chain<uint16_t, 1>((const uint16_t*)x, d, ldx, k, code_start, sorted, counts, sums, s);
+  }
+}
+
+cudaError_t launch_ema(double lam, double one_minus_lam, double eps, int64_t k, int64_t d, const double* N,
+                       const double* M, const double* counts, const double* sums, double* N_out,
+                       double* M_out, double* E_out, cudaStream_t s) {
+  if (k == 0) return cudaSuccess;
+  ProfScope prof("vq_ema", s);
+  ema_kernel<<<(unsigned)k, 128, 0, s>>>(lam, one_minus_lam, eps, d, N, M, counts, sums, N_out, M_out, E_out); count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_revive(int64_t k, int64_t d, double n_new, double denom, const double* ring, int64_t cap,
+                          const int64_t* dead_k, const int64_t* ring_rows, int64_t n_dead, double* N,
+                          double* M, double* E, cudaStream_t s) {
+  (void)k;
+  (void)cap;
+  if (n_dead == 0) return cudaSuccess;
+  revive_kernel<<<(unsigned)n_dead, 128, 0, s>>>(d, n_new, denom, ring, dead_k, ring_rows, N, M, E); count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ring_write(const void* x, int dtype, int64_t ldx, int64_t row0, int64_t nrows, int64_t d,
+                              double* ring, int64_t cap, int64_t phys0, cudaStream_t s) {
+  if (nrows == 0) return cudaSuccess;
+  switch (dtype) {
+    case F32: ring_write_kernel<float><<<(unsigned)nrows, 128, 0, s>>>((const float*)x, ldx, row0, d, ring, cap, phys0); count_launches(1); break;
+    case F64: ring_write_kernel<double><<<(unsigned)nrows, 128, 0, s>>>((const double*)x, ldx, row0, d, ring, cap, phys0); count_launches(1); break;
+    default: ring_write_kernel<uint16_t><<<(unsigned)nrows, 128, 0, s>>>((const uint16_t*)x, ldx, row0, d, ring, cap, phys0); count_launches(1);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_rows(const double* src, int64_t d, const int64_t* rows, int64_t n, double* dst,
+                               cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  gather_rows_kernel<<<(unsigned)n, 128, 0, s>>>(src, d, rows, dst); count_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace xgs
