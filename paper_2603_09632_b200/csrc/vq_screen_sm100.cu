@@ -34,10 +34,21 @@ constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int THREADS = 192;  // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2..5 epilogue
+constexpr int EPI_WARPS = 8;                  // 2 per TMEM lane quadrant (column halves)
+constexpr int EPI_THREADS = EPI_WARPS * 32;
+constexpr int THREADS = 64 + EPI_THREADS;     // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2..9 epilogue
+constexpr int HALF = BN / 2;                  // columns per epilogue warp per chunk
 constexpr int CONST_BYTES = 2 * 3 * BN * 4;
+struct HalfState {                            // column-half 1 -> half 0 hand-off at tile end
+  float U;
+  int cnt;
+  int ovf;
+  int ck[kCandCap];
+  float cl[kCandCap];
+};
+constexpr int MERGE_BYTES = BM * (int)sizeof(HalfState);
 constexpr int BAR_BYTES = (2 * STAGES + 4) * 8 + 16;
-constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + CONST_BYTES + BAR_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + CONST_BYTES + MERGE_BYTES + BAR_BYTES;
 // kind::f16 instruction descriptor: D=f32, A=B=f16 (format 0), both K-major,
 // N=256, M=128.
 constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
@@ -113,6 +124,29 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+// wait for outstanding tcgen05.ld; the registers are tied in so no use can be
+// scheduled before the wait.
+__device__ __forceinline__ void tmem_wait(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -125,15 +159,92 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory"); }
+
+// Per-row candidate state of one epilogue thread (one row, one column half).
+struct Cands {
+  float U;      // min_k (s_k + B_k) seen so far
+  int cnt;
+  bool ovf;
+  int ck[kCandCap];
+  float cl[kCandCap];
+
+  __device__ __forceinline__ void insert(int k, float lo, float thr) {
+    if (ovf) return;
+    if (cnt == kCandCap) {
+      int w = 0;
+      for (int j = 0; j < kCandCap; j++)
+        if (cl[j] <= thr) {
+          ck[w] = ck[j];
+          cl[w] = cl[j];
+          w++;
+        }
+      cnt = w;
+    }
+    if (cnt < kCandCap) {
+      ck[cnt] = k;
+      cl[cnt] = lo;
+      cnt++;
+    } else {
+      ovf = true;
+    }
+  }
+};
+
+// Screen 32 accumulator columns of one row: block min of s+B first (no serial
+// dependence on U per element), then a single lo-vs-threshold test; only
+// blocks that can hold a candidate take the (rare) insertion path.
+__device__ __forceinline__ void screen_block(const uint32_t (&r)[32], const float* __restrict__ cn,
+                                            const float* __restrict__ ce1, const float* __restrict__ ce2,
+                                            float xf, float xn, float slack, int kbase, Cands& st) {
+  float lo[32];
+  float h0 = __int_as_float(0x7f800000), h1 = h0, h2 = h0, h3 = h0;
+  float l0 = h0, l1 = h0, l2 = h0, l3 = h0;
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) {
+    const float4 a = *reinterpret_cast<const float4*>(cn + i);
+    const float4 b1 = *reinterpret_cast<const float4*>(ce1 + i);
+    const float4 b2 = *reinterpret_cast<const float4*>(ce2 + i);
+    const float s0 = fmaf(xf, __uint_as_float(r[i + 0]), a.x), bb0 = fmaf(xn, b1.x, b2.x);
+    const float s1 = fmaf(xf, __uint_as_float(r[i + 1]), a.y), bb1 = fmaf(xn, b1.y, b2.y);
+    const float s2 = fmaf(xf, __uint_as_float(r[i + 2]), a.z), bb2 = fmaf(xn, b1.z, b2.z);
+    const float s3 = fmaf(xf, __uint_as_float(r[i + 3]), a.w), bb3 = fmaf(xn, b1.w, b2.w);
+    lo[i + 0] = s0 - bb0;
+    lo[i + 1] = s1 - bb1;
+    lo[i + 2] = s2 - bb2;
+    lo[i + 3] = s3 - bb3;
+    h0 = fminf(h0, s0 + bb0);
+    h1 = fminf(h1, s1 + bb1);
+    h2 = fminf(h2, s2 + bb2);
+    h3 = fminf(h3, s3 + bb3);
+    l0 = fminf(l0, lo[i + 0]);
+    l1 = fminf(l1, lo[i + 1]);
+    l2 = fminf(l2, lo[i + 2]);
+    l3 = fminf(l3, lo[i + 3]);
+  }
+  st.U = fminf(st.U, fminf(fminf(h0, h1), fminf(h2, h3)));
+  const float thr = st.U + slack;
+  if (fminf(fminf(l0, l1), fminf(l2, l3)) <= thr) {
+    unsigned m = 0;
+#pragma unroll
+    for (int i = 0; i < 32; i++) m |= (lo[i] <= thr ? 1u : 0u) << i;
+    float lv[32];
+#pragma unroll
+    for (int i = 0; i < 32; i++) lv[i] = lo[i];
+    while (m) {
+      const int i = __ffs(m) - 1;
+      m &= m - 1;
+      st.insert(kbase + i, lv[i], thr);
+    }
+  }
+}
 
 __global__ void __launch_bounds__(THREADS, 1)
 screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               ScreenParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   float* cconst = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + CONST_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + CONST_BYTES + MERGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -147,7 +258,7 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     }
     for (int i = 0; i < 2; i++) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -209,26 +320,29 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
     }
   } else {
-    // ---------------- epilogue: one thread per tile row ----------------
-    const int q = warp & 3;
+    // ---------------- epilogue: one thread per (tile row, column half) ----------------
+    const int ew = warp - 2;                 // 0..7
+    const int q = warp & 3;                  // TMEM lane quadrant this warp may access
+    const int half = ew >> 2;                // column half of every chunk
     const int et = threadIdx.x - 64;
+    const int rl = q * 32 + lane;            // row within the tile
     const unsigned lt = (1u << lane) - 1u;
+    HalfState* merge = reinterpret_cast<HalfState*>(smem + STAGES * STAGE_BYTES + CONST_BYTES);
     int acc = 0;
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < p.num_m_tiles; tile += gridDim.x) {
-      const int64_t row = (int64_t)tile * BM + q * 32 + lane;
+      const int64_t row = (int64_t)tile * BM + rl;
       const bool live = row < p.n;
       const float xn = live ? p.xn[row] : 0.f;
-      const float xf = live ? p.xf[row] : 0.f;   // -2 * (row scale)^-1 * (codebook scale)^-1
+      const float xf = live ? p.xf[row] : 0.f;   // -2 / (row scale * codebook scale)
       const float slack = 2.f * p.c3 * xn * xn;  // fp64-reference rounding margin
-      float U = __int_as_float(0x7f800000);
-      int cnt = 0;
-      bool ovf = false;
-      int ck[kCandCap];
-      float cl[kCandCap];
+      Cands st;
+      st.U = __int_as_float(0x7f800000);
+      st.cnt = 0;
+      st.ovf = false;
       for (int nc = 0; nc < p.num_n_chunks; nc++) {
         float* cc = cconst + acc * 3 * BN;
-        for (int i = et; i < BN; i += 128) {
+        for (int i = et; i < BN; i += EPI_THREADS) {
           const int kk = nc * BN + i;
           cc[i] = p.cn[kk];
           cc[BN + i] = p.ce1[kk];
@@ -237,37 +351,21 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         epi_bar();
         mbar_wait(&tfull[acc], aphase);
         tc_after();
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c0, r);
-#pragma unroll
-          for (int i = 0; i < 32; i++) {
-            const int c = c0 + i;
-            const float s = fmaf(xf, __uint_as_float(r[i]), cc[c]);
-            const float b = fmaf(xn, cc[BN + c], cc[2 * BN + c]);
-            const float lo = s - b;
-            U = fminf(U, s + b);
-            if (lo <= U + slack && !ovf) {
-              if (cnt == kCandCap) {
-                int w = 0;
-                for (int j = 0; j < kCandCap; j++)
-                  if (cl[j] <= U + slack) {
-                    ck[w] = ck[j];
-                    cl[w] = cl[j];
-                    w++;
-                  }
-                cnt = w;
-              }
-              if (cnt < kCandCap) {
-                ck[cnt] = nc * BN + c;
-                cl[cnt] = lo;
-                cnt++;
-              } else {
-                ovf = true;
-              }
-            }
-          }
+        const int cbase = half * HALF;
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + cbase);
+        uint32_t ra[32], rb[32];
+        tmem_ld32_async(taddr, ra);
+        tmem_wait(ra);
+#pragma unroll 1
+        for (int c0 = 0; c0 < HALF; c0 += 64) {
+          tmem_ld32_async(taddr + c0 + 32, rb);
+          screen_block(ra, cc + cbase + c0, cc + BN + cbase + c0, cc + 2 * BN + cbase + c0, xf, xn, slack,
+                       nc * BN + cbase + c0, st);
+          tmem_wait(rb);
+          if (c0 + 64 < HALF) tmem_ld32_async(taddr + c0 + 64, ra);
+          screen_block(rb, cc + cbase + c0 + 32, cc + BN + cbase + c0 + 32, cc + 2 * BN + cbase + c0 + 32, xf,
+                       xn, slack, nc * BN + cbase + c0 + 32, st);
+          if (c0 + 64 < HALF) tmem_wait(ra);
         }
         tc_before();
         __syncwarp();
@@ -275,39 +373,65 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
       }
-      // ---- finalize the row ----
-      int nk = 0, kbest = -1;
-      int fin[kCandCap];
-      if (!ovf)
-        for (int j = 0; j < cnt; j++)
-          if (cl[j] <= U + slack) {
-            fin[nk++] = ck[j];
-            kbest = ck[j];
-          }
-      const bool to_fallback = live && (ovf || nk == 0);
-      const bool to_rerank = live && !to_fallback && nk > 1;
-      if (live && !to_fallback && nk == 1) p.codes[row] = kbest;
-      unsigned m = __ballot_sync(FULL, to_rerank);
-      if (m) {
-        const int leader = __ffs(m) - 1;
-        int base = 0;
-        if (lane == leader) base = atomicAdd(p.rq_count, __popc(m));
-        base = __shfl_sync(FULL, base, leader);
-        if (to_rerank) {
-          RerankEntry* e = p.rq + base + __popc(m & lt);
-          e->row = (int32_t)row;
-          e->cnt = nk;
-          for (int j = 0; j < kCandCap; j++) e->cand[j] = j < nk ? fin[j] : 0;
+      // ---- merge the two column halves, finalize the row ----
+      if (half == 1) {
+        HalfState& hs = merge[rl];
+        hs.U = st.U;
+        hs.cnt = st.cnt;
+        hs.ovf = st.ovf;
+        for (int j = 0; j < kCandCap; j++) {
+          hs.ck[j] = st.ck[j];
+          hs.cl[j] = st.cl[j];
         }
       }
-      m = __ballot_sync(FULL, to_fallback);
-      if (m) {
-        const int leader = __ffs(m) - 1;
-        int base = 0;
-        if (lane == leader) base = atomicAdd(p.fq_count, __popc(m));
-        base = __shfl_sync(FULL, base, leader);
-        if (to_fallback) p.fq[base + __popc(m & lt)] = (int32_t)row;
+      epi_bar();
+      if (half == 0) {
+        const HalfState& hs = merge[rl];
+        const float U = fminf(st.U, hs.U);
+        const float thr = U + slack;
+        bool ovf = st.ovf || hs.ovf;
+        int nk = 0, kbest = -1;
+        int fin[kCandCap];
+        for (int j = 0; j < st.cnt && !ovf; j++)
+          if (st.cl[j] <= thr) {
+            fin[nk++] = st.ck[j];
+            kbest = st.ck[j];
+          }
+        for (int j = 0; j < hs.cnt && !ovf; j++)
+          if (hs.cl[j] <= thr) {
+            if (nk == kCandCap) {
+              ovf = true;
+              break;
+            }
+            fin[nk++] = hs.ck[j];
+            kbest = hs.ck[j];
+          }
+        const bool to_fallback = live && (ovf || nk == 0);
+        const bool to_rerank = live && !to_fallback && nk > 1;
+        if (live && !to_fallback && nk == 1) p.codes[row] = kbest;
+        unsigned m = __ballot_sync(FULL, to_rerank);
+        if (m) {
+          const int leader = __ffs(m) - 1;
+          int base = 0;
+          if (lane == leader) base = atomicAdd(p.rq_count, __popc(m));
+          base = __shfl_sync(FULL, base, leader);
+          if (to_rerank) {
+            RerankEntry* e = p.rq + base + __popc(m & lt);
+            e->row = (int32_t)row;
+            e->cnt = nk;
+            for (int j = 0; j < kCandCap; j++) e->cand[j] = j < nk ? fin[j] : 0;
+          }
+        }
+        m = __ballot_sync(FULL, to_fallback);
+        if (m) {
+          const int leader = __ffs(m) - 1;
+          int base = 0;
+          if (lane == leader) base = atomicAdd(p.fq_count, __popc(m));
+          base = __shfl_sync(FULL, base, leader);
+          if (to_fallback) p.fq[base + __popc(m & lt)] = (int32_t)row;
+        }
       }
+      epi_bar();   // merge slots are reused by the next tile
     }
   }
   tc_before();
@@ -367,38 +491,62 @@ __global__ void prep_codebook_kernel(const double* __restrict__ E, int64_t k, in
 
 // Rows: any dtype -> power-of-2-scaled, zero-padded fp16 (n x dp), an upper
 // bound on |x| and the epilogue factor xf = -2 / (row scale * codebook scale).
+// One warp per row; fp32 (and bf16) rows use fp32 arithmetic (the norm is only
+// an upper bound: host-side `inflate` covers its rounding), fp64 rows fp64.
 template <typename X>
-__global__ void prep_rows_kernel(const X* __restrict__ x, int64_t n, int64_t d, int64_t ldx, int64_t dp,
-                                 const unsigned* __restrict__ emax_bits, __half* __restrict__ Ab,
-                                 float* __restrict__ xn, float* __restrict__ xf, float inflate) {
+struct RowMath { using T = float; };
+template <>
+struct RowMath<double> { using T = double; };
+
+template <typename X>
+__global__ void __launch_bounds__(256)
+prep_rows_kernel(const X* __restrict__ x, int64_t n, int64_t d, int64_t ldx, int64_t dp,
+                 const unsigned* __restrict__ emax_bits, __half* __restrict__ Ab, float* __restrict__ xn,
+                 float* __restrict__ xf, float inflate) {
+  using T = typename RowMath<X>::T;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
   const X* xr = x + row * ldx;
-  double ss = 0.0;
+  T ss = 0;
   float mx = 0.f;
-  for (int64_t j = lane; j < d; j += 32) {
-    const double v = ld64(xr, j);
-    ss = fma(v, v, ss);
-    mx = fmaxf(mx, (float)fabs(v));
+  const bool vec4 = sizeof(X) == 4 && (d % 4) == 0 && (ldx % 4) == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+  if (vec4) {
+    for (int64_t j = (int64_t)lane * 4; j < d; j += 128) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(xr + j));
+      ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, (float)ss))));
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+  } else {
+    for (int64_t j = lane; j < d; j += 32) {
+      const T v = (T)ld64(xr, j);
+      ss += v * v;
+      mx = fmaxf(mx, (float)fabs((double)v));
+    }
   }
   for (int o = 16; o; o >>= 1) {
     ss += __shfl_xor_sync(FULL, ss, o);
     mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
   }
   const int ex = exp_of(mx);
-  const double sc = ldexp(1.0, 15 - ex);
-  for (int64_t j0 = (int64_t)lane * 8; j0 < dp; j0 += 256) {
-    __align__(16) __half v8[8];
-#pragma unroll
-    for (int u = 0; u < 8; u++) {
-      const int64_t j = j0 + u;
-      v8[u] = __double2half(j < d ? ld64(xr, j) * sc : 0.0);
+  const T sc = (T)ldexp(1.0, 15 - ex);
+  __half* ar = Ab + row * dp;
+  if (vec4) {
+    for (int64_t j = (int64_t)lane * 4; j < dp; j += 128) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j < d) v = __ldg(reinterpret_cast<const float4*>(xr + j));
+      const __half2 h0 = __floats2half2_rn(v.x * (float)sc, v.y * (float)sc);
+      const __half2 h1 = __floats2half2_rn(v.z * (float)sc, v.w * (float)sc);
+      uint2 w;
+      w.x = *reinterpret_cast<const uint32_t*>(&h0);
+      w.y = *reinterpret_cast<const uint32_t*>(&h1);
+      *reinterpret_cast<uint2*>(ar + j) = w;
     }
-    *reinterpret_cast<uint4*>(Ab + row * dp + j0) = *reinterpret_cast<const uint4*>(v8);
+  } else {
+    for (int64_t j = lane; j < dp; j += 32) ar[j] = __double2half(j < d ? (double)((T)ld64(xr, j) * sc) : 0.0);
   }
   if (lane == 0) {
-    xn[row] = (float)sqrt(ss) * inflate;
+    xn[row] = (float)sqrt((double)ss) * inflate;
     const int ee = exp_of(__uint_as_float(*emax_bits));
     xf[row] = -ldexpf(1.f, (ex - 15) + (ee - 15) + 1);
   }
@@ -486,7 +634,7 @@ cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* h
   absmax_kernel<<<148, 256, 0, s>>>(a.E, a.k * a.d, emax); count_launches(1);
   prep_codebook_kernel<<<(unsigned)((w.kp + 7) / 8), 256, 0, s>>>(a.E, a.k, a.d, w.kp, w.dp, a.c1, a.c2, a.c4,
                                                                   emax, Eb, cn, ce1, ce2); count_launches(1);
-  const float inflate = 1.f + 1e-6f;
+  const float inflate = 1.f + (float)(a.d + 8) * 1.2e-7f;
   const unsigned rblocks = (unsigned)((a.n + 7) / 8);
   switch (a.dtype) {
     case F32: prep_rows_kernel<float><<<rblocks, 256, 0, s>>>((const float*)a.x, a.n, a.d, a.ldx, w.dp, emax, Ab, xn, xf, inflate); count_launches(1); break;

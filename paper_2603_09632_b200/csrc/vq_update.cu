@@ -141,38 +141,59 @@ __global__ void acc_scatter_kernel(const int64_t* __restrict__ codes, const uint
   }
 }
 
+// Raw vector loads (no widening) so a warp can keep U rows in flight; the
+// loads are volatile asm so ptxas keeps them ahead of the dependent adds.
 template <typename X, int VEC>
-struct VecLoad;
-template <> struct VecLoad<float, 4> {
-  static __device__ __forceinline__ void go(const float* p, double* v) {
-    const float4 q = __ldg(reinterpret_cast<const float4*>(p));
-    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+struct Raw;
+template <> struct Raw<float, 2> {
+  uint32_t w[2];
+  __device__ __forceinline__ void load(const float* p) {
+    asm volatile("ld.global.nc.L1::no_allocate.v2.b32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "l"(p));
+  }
+  __device__ __forceinline__ void pin() { asm volatile("" : "+r"(w[0]), "+r"(w[1])); }
+  __device__ __forceinline__ double get(int i) const { return (double)__uint_as_float(w[i]); }
+};
+template <> struct Raw<float, 4> {
+  uint32_t w[4];
+  __device__ __forceinline__ void load(const float* p) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p));
+  }
+  __device__ __forceinline__ void pin() { asm volatile("" : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3])); }
+  __device__ __forceinline__ double get(int i) const { return (double)__uint_as_float(w[i]); }
+};
+template <> struct Raw<uint16_t, 8> {
+  uint32_t w[4];
+  __device__ __forceinline__ void load(const uint16_t* p) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p));
+  }
+  __device__ __forceinline__ void pin() { asm volatile("" : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3])); }
+  __device__ __forceinline__ double get(int i) const {
+    return (double)__uint_as_float((i & 1) ? (w[i >> 1] & 0xffff0000u) : (w[i >> 1] << 16));
   }
 };
-template <> struct VecLoad<uint16_t, 8> {
-  static __device__ __forceinline__ void go(const uint16_t* p, double* v) {
-    const uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
-    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-      v[2 * i] = (double)__uint_as_float(w[i] << 16);
-      v[2 * i + 1] = (double)__uint_as_float(w[i] & 0xffff0000u);
-    }
+template <> struct Raw<double, 2> {
+  double w[2];
+  __device__ __forceinline__ void load(const double* p) {
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(w[0]), "=d"(w[1]) : "l"(p));
   }
+  __device__ __forceinline__ void pin() { asm volatile("" : "+d"(w[0]), "+d"(w[1])); }
+  __device__ __forceinline__ double get(int i) const { return w[i]; }
 };
-template <typename X> struct VecLoad<X, 1> {
-  static __device__ __forceinline__ void go(const X* p, double* v) { v[0] = ld64(p, 0); }
-};
-template <> struct VecLoad<double, 2> {
-  static __device__ __forceinline__ void go(const double* p, double* v) {
-    const double2 q = __ldg(reinterpret_cast<const double2*>(p));
-    v[0] = q.x; v[1] = q.y;
-  }
+template <typename X> struct Raw<X, 1> {
+  double w;
+  __device__ __forceinline__ void load(const X* p) { w = ld64(p, 0); }
+  __device__ __forceinline__ void pin() { asm volatile("" : "+d"(w)); }
+  __device__ __forceinline__ double get(int) const { return w; }
 };
 
-// (4) one sequential fp64 chain per (k, d): warp = (code, 32*VEC dims).
-template <typename X, int VEC>
-__global__ void __launch_bounds__(256)
+// (4) one sequential fp64 chain per (k, d): warp = (code, 32*VEC dims).  A
+// chain is inherently serial, so a warp's speed is its memory-level
+// parallelism: U rows are loaded ahead (U*32*VEC*sizeof(X) bytes in flight per
+// warp) before the U dependent adds.
+template <typename X, int VEC, int U>
+__global__ void __launch_bounds__(256, 2)
 acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
                  const int32_t* __restrict__ code_start, const int32_t* __restrict__ sorted,
                  double* __restrict__ counts, double* __restrict__ sums) {
@@ -187,32 +208,31 @@ acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
   double acc[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; v++) acc[v] = 0.0;
-  constexpr int U = 8;
-  for (int32_t b = beg; b < end; b += 32) {
-    const int cnt = min(32, end - b);
-    const int32_t my_row = lane < cnt ? sorted[b + lane] : 0;
-    int j = 0;
-    for (; j + U <= cnt; j += U) {
-      double val[U][VEC];
+  const X* xd = x + (live ? d0 : 0);
+  int32_t b = beg;
+  for (; b + U <= end; b += U) {
+    Raw<X, VEC> val[U];
+    int32_t rows[U];
 #pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int64_t row = __shfl_sync(FULL, my_row, j + u);
-        if (live) VecLoad<X, VEC>::go(x + row * ldx + d0, val[u]);
-      }
+    for (int u = 0; u < U; u += 32) {
+      const int32_t r = sorted[b + u + lane];
 #pragma unroll
-      for (int u = 0; u < U; u++)
-#pragma unroll
-        for (int v = 0; v < VEC; v++) acc[v] = dadd(acc[v], val[u][v]);
+      for (int t = 0; t < 32 && u + t < U; t++) rows[u + t] = __shfl_sync(FULL, r, t);
     }
-    for (; j < cnt; j++) {
-      const int64_t row = __shfl_sync(FULL, my_row, j);
-      double val[VEC];
-      if (live) {
-        VecLoad<X, VEC>::go(x + row * ldx + d0, val);
 #pragma unroll
-        for (int v = 0; v < VEC; v++) acc[v] = dadd(acc[v], val[v]);
-      }
-    }
+    for (int u = 0; u < U; u++) val[u].load(xd + (int64_t)rows[u] * ldx);
+#pragma unroll
+    for (int u = 0; u < U; u++) val[u].pin();   // all U loads issue before the first add
+#pragma unroll
+    for (int u = 0; u < U; u++)
+#pragma unroll
+      for (int v = 0; v < VEC; v++) acc[v] = dadd(acc[v], val[u].get(v));
+  }
+  for (; b < end; b++) {
+    Raw<X, VEC> val;
+    val.load(xd + (int64_t)sorted[b] * ldx);
+#pragma unroll
+    for (int v = 0; v < VEC; v++) acc[v] = dadd(acc[v], val.get(v));
   }
   if (live) {
 #pragma unroll
@@ -226,8 +246,9 @@ cudaError_t launch_chain(const X* x, int64_t d, int64_t ldx, int64_t k, const in
                          const int32_t* sorted, double* counts, double* sums, cudaStream_t s) {
   const int64_t nchunks = (d + 32 * VEC - 1) / (32 * VEC);
   const int64_t warps = k * nchunks;
+  constexpr int U = VEC >= 4 ? 16 : 32;
   ProfScope prof("vq_chain", s);
-  acc_chain_kernel<X, VEC><<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(x, d, ldx, k, cs, sorted, counts, sums); count_launches(1);
+  acc_chain_kernel<X, VEC, U><<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(x, d, ldx, k, cs, sorted, counts, sums); count_launches(1);
   return cudaGetLastError();
 }
 
@@ -311,8 +332,8 @@ cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, in
   const uintptr_t xa = reinterpret_cast<uintptr_t>(x);
   switch (dtype) {
     case F32:
-      if (d % 4 == 0 && ldx % 4 == 0 && xa % 16 == 0)
-        return launch_chain<float, 4>((const float*)x, d, ldx, k, code_start, sorted, counts, sums, s);
+      if (d % 2 == 0 && ldx % 2 == 0 && xa % 8 == 0)
+        return launch_chain<float, 2>((const float*)x, d, ldx, k, code_start, sorted, counts, sums, s);
       return launch_chain<float, 1>((const float*)x, d, ldx, k, code_start, sorted, counts, sums, s);
     case F64:
       if (d % 2 == 0 && ldx % 2 == 0 && xa % 16 == 0)
