@@ -41,8 +41,7 @@ constexpr int HALF = BN / 2;                  // columns per epilogue warp per c
 constexpr int CONST_BYTES = 2 * 3 * BN * 4;
 struct HalfState {                            // column-half 1 -> half 0 hand-off at tile end
   float U;
-  int cnt;
-  int ovf;
+  float dropped;
   int ck[kCandCap];
   float cl[kCandCap];
 };
@@ -161,39 +160,44 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory"); }
 
-// Per-row candidate state of one epilogue thread (one row, one column half).
+// Per-row candidate state of one epilogue thread (one row, one column half):
+// the kCandCap smallest lower bounds lo_k = s_k - B_k seen so far, kept sorted
+// in registers (static indices only), plus the smallest lo ever pushed out.
+// At the end the candidates are {k : lo_k <= U + slack}; if a pushed-out lo
+// also satisfies that, the list overflowed and the row is rescanned exactly.
 struct Cands {
-  float U;      // min_k (s_k + B_k) seen so far
-  int cnt;
-  bool ovf;
-  int ck[kCandCap];
-  float cl[kCandCap];
+  float U;        // min_k (s_k + B_k) seen so far
+  float dropped;  // min lo among entries evicted from the full list
+  float L[kCandCap];
+  int Kx[kCandCap];
 
-  __device__ __forceinline__ void insert(int k, float lo, float thr) {
-    if (ovf) return;
-    if (cnt == kCandCap) {
-      int w = 0;
-      for (int j = 0; j < kCandCap; j++)
-        if (cl[j] <= thr) {
-          ck[w] = ck[j];
-          cl[w] = cl[j];
-          w++;
-        }
-      cnt = w;
+  __device__ __forceinline__ void init() {
+    U = __int_as_float(0x7f800000);
+    dropped = U;
+#pragma unroll
+    for (int j = 0; j < kCandCap; j++) {
+      L[j] = U;
+      Kx[j] = -1;
     }
-    if (cnt < kCandCap) {
-      ck[cnt] = k;
-      cl[cnt] = lo;
-      cnt++;
-    } else {
-      ovf = true;
+  }
+  __device__ __forceinline__ void insert(float lo, int k) {
+#pragma unroll
+    for (int j = 0; j < kCandCap; j++) {
+      const bool sw = lo < L[j];
+      const float tl = L[j];
+      const int tk = Kx[j];
+      L[j] = sw ? lo : tl;
+      Kx[j] = sw ? k : tk;
+      lo = sw ? tl : lo;
+      k = sw ? tk : k;
     }
+    if (k >= 0) dropped = fminf(dropped, lo);
   }
 };
 
 // Screen 32 accumulator columns of one row: block min of s+B first (no serial
 // dependence on U per element), then a single lo-vs-threshold test; only
-// blocks that can hold a candidate take the (rare) insertion path.
+// blocks that can hold a candidate take the insertion path.
 __device__ __forceinline__ void screen_block(const uint32_t (&r)[32], const float* __restrict__ cn,
                                             const float* __restrict__ ce1, const float* __restrict__ ce2,
                                             float xf, float xn, float slack, int kbase, Cands& st) {
@@ -225,16 +229,19 @@ __device__ __forceinline__ void screen_block(const uint32_t (&r)[32], const floa
   st.U = fminf(st.U, fminf(fminf(h0, h1), fminf(h2, h3)));
   const float thr = st.U + slack;
   if (fminf(fminf(l0, l1), fminf(l2, l3)) <= thr) {
+    // rare per lane, frequent per warp (32 rows): stash the block with 8
+    // vector stores, then insert only the qualifying columns
     unsigned m = 0;
+    float4 lv[8];
 #pragma unroll
     for (int i = 0; i < 32; i++) m |= (lo[i] <= thr ? 1u : 0u) << i;
-    float lv[32];
 #pragma unroll
-    for (int i = 0; i < 32; i++) lv[i] = lo[i];
+    for (int i = 0; i < 8; i++) lv[i] = make_float4(lo[4 * i], lo[4 * i + 1], lo[4 * i + 2], lo[4 * i + 3]);
+    const float* lf = reinterpret_cast<const float*>(lv);
     while (m) {
       const int i = __ffs(m) - 1;
       m &= m - 1;
-      st.insert(kbase + i, lv[i], thr);
+      st.insert(lf[i], kbase + i);
     }
   }
 }
@@ -337,9 +344,7 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       const float xf = live ? p.xf[row] : 0.f;   // -2 / (row scale * codebook scale)
       const float slack = 2.f * p.c3 * xn * xn;  // fp64-reference rounding margin
       Cands st;
-      st.U = __int_as_float(0x7f800000);
-      st.cnt = 0;
-      st.ovf = false;
+      st.init();
       for (int nc = 0; nc < p.num_n_chunks; nc++) {
         float* cc = cconst + acc * 3 * BN;
         for (int i = et; i < BN; i += EPI_THREADS) {
@@ -377,28 +382,28 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       if (half == 1) {
         HalfState& hs = merge[rl];
         hs.U = st.U;
-        hs.cnt = st.cnt;
-        hs.ovf = st.ovf;
+        hs.dropped = st.dropped;
+#pragma unroll
         for (int j = 0; j < kCandCap; j++) {
-          hs.ck[j] = st.ck[j];
-          hs.cl[j] = st.cl[j];
+          hs.ck[j] = st.Kx[j];
+          hs.cl[j] = st.L[j];
         }
       }
       epi_bar();
       if (half == 0) {
         const HalfState& hs = merge[rl];
-        const float U = fminf(st.U, hs.U);
-        const float thr = U + slack;
-        bool ovf = st.ovf || hs.ovf;
+        const float thr = fminf(st.U, hs.U) + slack;
+        bool ovf = st.dropped <= thr || hs.dropped <= thr;
         int nk = 0, kbest = -1;
         int fin[kCandCap];
-        for (int j = 0; j < st.cnt && !ovf; j++)
-          if (st.cl[j] <= thr) {
-            fin[nk++] = st.ck[j];
-            kbest = st.ck[j];
+#pragma unroll
+        for (int j = 0; j < kCandCap; j++)
+          if (st.Kx[j] >= 0 && st.L[j] <= thr) {
+            fin[nk++] = st.Kx[j];
+            kbest = st.Kx[j];
           }
-        for (int j = 0; j < hs.cnt && !ovf; j++)
-          if (hs.cl[j] <= thr) {
+        for (int j = 0; j < kCandCap && !ovf; j++)
+          if (hs.ck[j] >= 0 && hs.cl[j] <= thr) {
             if (nk == kCandCap) {
               ovf = true;
               break;
