@@ -55,7 +55,7 @@ XGS_API int xgs_profile_read(const char* tag, double* total_ms, long long* count
 
 /* assign_batch (vq.py:84-87) / assign (vq.py:76-81): int64 codes of the
  * nearest fp64 codeword, ties to the lowest index, bit-identical to the
- * reference.  tcgen05 bf16 screening GEMM + exact fp64 re-rank.
+ * reference.  tcgen05 fp16 screening GEMM + exact fp64 re-rank.
  * stats_out (HOST, nullable): {rows re-ranked, rows rescanned exactly};
  * when given the call synchronises on `stream`.
  * Errors: K == 0 -> XGS_INVALID_STATE (vq.py:78-79, 85-86). */
@@ -98,6 +98,69 @@ XGS_API int xgs_vq_ring_write(const void* x, int dtype, int64_t ldx, int64_t row
                               double* ring, int64_t cap, int64_t phys0, void* stream);
 XGS_API int xgs_gather_rows_f64(const double* src, int64_t d, const int64_t* rows, int64_t n, double* dst,
                                 void* stream);
+
+/* ------------------------------------------------------------- GRID */
+
+/* slam.backproject (slam.py:594-598) for n points, bit-identical:
+ * cam = ((u-cx)*d/fx, (v-cy)*d/fy, d); p = R^T (cam - t) with OpenBLAS
+ * dgemv's FMA order.  R (3x3 row-major world->camera), t (3), u, v, d (n)
+ * and out (n x 3) are DEVICE pointers; intr4 = {fx, fy, cx, cy} is HOST. */
+XGS_API int xgs_backproject(const double* R, const double* t, const double* intr4, const double* u,
+                            const double* v, const double* d, int64_t n, double* out, void* stream);
+
+/* GPU hash set of occupied voxel keys (the map).  Opaque handle; open
+ * addressing with 64-bit keys, load factor kept <= 1/2 (grows on demand).
+ * insert = insert-if-absent; was_new (nullable) reports keys that were absent. */
+XGS_API int xgs_hashset_create(int64_t capacity, void** handle);
+XGS_API int xgs_hashset_destroy(void* handle);
+XGS_API int xgs_hashset_insert(void* handle, const uint64_t* keys, int64_t n, uint8_t* was_new, void* stream);
+XGS_API int xgs_hashset_contains(void* handle, const uint64_t* keys, int64_t n, uint8_t* out, void* stream);
+XGS_API int xgs_hashset_size(void* handle, int64_t* n_out, void* stream); /* synchronises */
+
+/* In-house stable LSD radix sort of (u64 key, u32 value) pairs on bits [0, bits). */
+XGS_API size_t xgs_grid_workspace(int64_t npix);
+XGS_API int xgs_radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, int bits, void* ws,
+                                     size_t ws_bytes, void* stream);
+
+/* Voxel grid sampling of a batch of frames (the insertion half of
+ * densify_and_prune, slam.py:601-651, with the coverage render replaced by
+ * the occupied-voxel hash set; SURVEY.md 8(a) g8 definitions):
+ * valid pixel = stride lattice and depth > 0; key = floor(p/voxel) packed
+ * 3x21 bits biased by 2^20; representative = lowest (frame, pixel) id of a
+ * voxel (mode 0) or the pixel-order mean over the voxel's points in that
+ * frame (mode 1); voxels already in `hashset` are rejected and the new ones
+ * inserted; outputs in ascending (frame, pixel) id.  Synchronises twice
+ * (batch bounding box, output count). */
+typedef struct {
+  int64_t frames, height, width;
+  const float* depth;      /* [F,H,W] */
+  const uint8_t* color;    /* [F,H,W,3] or NULL */
+  const double* rot;       /* [F,3,3] world->camera rotations, row-major */
+  const double* trans;     /* [F,3] */
+  double fx, fy, cx, cy;   /* u = row pairs fx/cx (core.py:5-9) */
+  double voxel;
+  int32_t stride;          /* pixel lattice stride (slam.py:621-623) */
+  int32_t mode;            /* 0 first-pick, 1 mean */
+  double min_scale;        /* size = max(min_scale, 0.5*stride*depth/fx) (slam.py:631) */
+  const float* feat;       /* [F,C,Hf,Wf] or NULL, gathered by supervision.py:133-147 */
+  int64_t feat_c, feat_h, feat_w;
+} xgs_grid_frames;
+
+typedef struct {
+  int64_t capacity;        /* rows of every output array */
+  uint64_t* key;           /* [cap] */
+  int64_t* pid;            /* [cap] frame*H*W + u*W + v */
+  double* mu;              /* [cap,3] */
+  double* color;           /* [cap,3] rgb/255 */
+  double* scale;           /* [cap] */
+  double* depth;           /* [cap] */
+  float* feat;             /* [cap,C] or NULL */
+  double* count;           /* [cap] points averaged (mode 1) or 1, nullable */
+  int64_t n_new, n_valid, n_voxels; /* written by the call */
+} xgs_grid_result;
+
+XGS_API int xgs_grid_sample(const xgs_grid_frames* in, void* hashset, xgs_grid_result* out, void* ws,
+                            size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -42,7 +42,31 @@ SIGNATURES = {
     "xgs_vq_revive": (_i32, [_i64, _i64, _f64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "xgs_vq_ring_write": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _vp]),
     "xgs_gather_rows_f64": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
+    "xgs_backproject": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "xgs_hashset_create": (_i32, [_i64, _vp]),
+    "xgs_hashset_destroy": (_i32, [_vp]),
+    "xgs_hashset_insert": (_i32, [_vp, _vp, _i64, _vp, _vp]),
+    "xgs_hashset_contains": (_i32, [_vp, _vp, _i64, _vp, _vp]),
+    "xgs_hashset_size": (_i32, [_vp, _vp, _vp]),
+    "xgs_grid_workspace": (_sz, [_i64]),
+    "xgs_radix_sort_pairs_u64": (_i32, [_vp, _vp, _i64, _i32, _vp, _sz, _vp]),
+    "xgs_grid_sample": (_i32, [_vp, _vp, _vp, _vp, _sz, _vp]),
 }
+
+
+class GridFrames(ctypes.Structure):
+    """Mirror of xgs_grid_frames (include/xgs.h)."""
+    _fields_ = [("frames", _i64), ("height", _i64), ("width", _i64), ("depth", _vp), ("color", _vp),
+                ("rot", _vp), ("trans", _vp), ("fx", _f64), ("fy", _f64), ("cx", _f64), ("cy", _f64),
+                ("voxel", _f64), ("stride", ctypes.c_int32), ("mode", ctypes.c_int32), ("min_scale", _f64),
+                ("feat", _vp), ("feat_c", _i64), ("feat_h", _i64), ("feat_w", _i64)]
+
+
+class GridResult(ctypes.Structure):
+    """Mirror of xgs_grid_result (include/xgs.h)."""
+    _fields_ = [("capacity", _i64), ("key", _vp), ("pid", _vp), ("mu", _vp), ("color", _vp), ("scale", _vp),
+                ("depth", _vp), ("feat", _vp), ("count", _vp), ("n_new", _i64), ("n_valid", _i64),
+                ("n_voxels", _i64)]
 
 
 def lib():

@@ -254,4 +254,116 @@ int xgs_gather_rows_f64(const double* src, int64_t d, const int64_t* rows, int64
   return OK;
 }
 
+// ---------------------------------------------------------------- GRID
+
+int xgs_backproject(const double* R, const double* t, const double* intr4, const double* u, const double* v,
+                    const double* d, int64_t n, double* out, void* stream) {
+  if (n < 0 || !intr4) return fail(INVALID_INPUT, "bad backproject arguments");
+  if (n > 0 && (!R || !t || !u || !v || !d || !out)) return fail(INVALID_INPUT, "null buffer");
+  cudaError_t e = launch_backproject(R, t, intr4, 1.0, u, v, d, n, out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_backproject");
+  return OK;
+}
+
+int xgs_hashset_create(int64_t capacity, void** handle) {
+  if (!handle || capacity < 0) return fail(INVALID_INPUT, "bad hashset arguments");
+  HashSet* h = nullptr;
+  cudaError_t e = hashset_create(capacity < 1024 ? 1024 : 2 * capacity, &h);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_hashset_create");
+  *handle = h;
+  return OK;
+}
+
+int xgs_hashset_destroy(void* handle) {
+  hashset_destroy(static_cast<HashSet*>(handle));
+  return OK;
+}
+
+int xgs_hashset_insert(void* handle, const uint64_t* keys, int64_t n, uint8_t* was_new, void* stream) {
+  if (!handle || n < 0 || (n > 0 && !keys)) return fail(INVALID_INPUT, "bad hashset insert");
+  cudaError_t e = hashset_insert(static_cast<HashSet*>(handle), keys, n, was_new, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_hashset_insert");
+  return OK;
+}
+
+int xgs_hashset_contains(void* handle, const uint64_t* keys, int64_t n, uint8_t* out, void* stream) {
+  if (!handle || n < 0 || (n > 0 && (!keys || !out))) return fail(INVALID_INPUT, "bad hashset query");
+  cudaError_t e = hashset_contains(static_cast<HashSet*>(handle), keys, n, out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_hashset_contains");
+  return OK;
+}
+
+int xgs_hashset_size(void* handle, int64_t* n_out, void* stream) {
+  if (!handle || !n_out) return fail(INVALID_INPUT, "bad hashset size");
+  cudaError_t e = hashset_size(static_cast<HashSet*>(handle), n_out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_hashset_size");
+  return OK;
+}
+
+size_t xgs_grid_workspace(int64_t npix) { return grid_workspace_bytes(npix); }
+
+int xgs_radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, int bits, void* ws, size_t ws_bytes,
+                             void* stream) {
+  if (n < 0 || bits < 0 || bits > 64 || (n > 0 && (!keys || !vals))) return fail(INVALID_INPUT, "bad sort");
+  if (n > 0x7fffffff) return fail(NOT_SUPPORTED, "more than 2^31-1 items");
+  if (ws_bytes < grid_workspace_bytes(n)) return fail(INVALID_INPUT, "workspace too small");
+  if (n == 0) return OK;
+  cudaError_t e = radix_sort_pairs(keys, vals, n, bits, ws, ws_bytes, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_radix_sort_pairs_u64");
+  return OK;
+}
+
+int xgs_grid_sample(const xgs_grid_frames* in, void* hashset, xgs_grid_result* out, void* ws, size_t ws_bytes,
+                    void* stream) {
+  if (!in || !out || !hashset) return fail(INVALID_INPUT, "null argument");
+  if (in->frames < 0 || in->height < 1 || in->width < 1) return fail(INVALID_INPUT, "bad frame shape");
+  if (!(in->voxel > 0) || !(in->fx > 0) || !(in->fy > 0)) return fail(INVALID_INPUT, "voxel size and focal lengths must be positive");
+  if (in->stride < 1) return fail(INVALID_INPUT, "stride must be >= 1");
+  if (in->mode != 0 && in->mode != 1) return fail(INVALID_INPUT, "mode must be 0 (first) or 1 (mean)");
+  const int64_t npix = in->frames * in->height * in->width;
+  if (npix > 0x7fffffff) return fail(NOT_SUPPORTED, "more than 2^31-1 pixels per batch");
+  if (npix > 0 && (!in->depth || !in->rot || !in->trans)) return fail(INVALID_INPUT, "null frame buffer");
+  if (in->feat && in->mode != 0) return fail(NOT_SUPPORTED, "feature gather is first-pick only");
+  if (in->feat && (in->feat_c < 1 || in->feat_h < 1 || in->feat_w < 1 || !out->feat))
+    return fail(INVALID_INPUT, "bad feature map");
+  if (ws_bytes < grid_workspace_bytes(npix)) return fail(INVALID_INPUT, "workspace too small");
+  GridIn gi;
+  gi.frames = in->frames;
+  gi.H = in->height;
+  gi.W = in->width;
+  gi.depth = in->depth;
+  gi.color = in->color;
+  gi.rot = in->rot;
+  gi.trans = in->trans;
+  gi.fx = in->fx;
+  gi.fy = in->fy;
+  gi.cx = in->cx;
+  gi.cy = in->cy;
+  gi.voxel = in->voxel;
+  gi.stride = in->stride;
+  gi.mode = in->mode;
+  gi.min_scale = in->min_scale;
+  gi.feat = in->feat;
+  gi.fc = in->feat_c;
+  gi.fh = in->feat_h;
+  gi.fw = in->feat_w;
+  GridOut go;
+  go.capacity = out->capacity;
+  go.key = out->key;
+  go.pid = out->pid;
+  go.mu = out->mu;
+  go.color = out->color;
+  go.scale = out->scale;
+  go.depth = out->depth;
+  go.feat = out->feat;
+  go.count = out->count;
+  cudaError_t e = grid_sample(gi, static_cast<HashSet*>(hashset), go, ws, ws_bytes, sm_count(), (cudaStream_t)stream);
+  out->n_new = go.n_new;
+  out->n_valid = go.n_valid;
+  out->n_voxels = go.n_voxels;
+  if (e == cudaErrorInvalidValue && go.n_new > go.capacity) return fail(INVALID_INPUT, "output capacity too small");
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_grid_sample");
+  return OK;
+}
+
 }  // extern "C"

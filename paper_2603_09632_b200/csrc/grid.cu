@@ -1,0 +1,776 @@
+// Voxel grid sampling of back-projected RGB-D frames (sm_100a).
+//
+// Turns a batch of F depth frames into new Gaussians, one per voxel that is
+// not yet occupied in the map, in ascending (frame, pixel) order:
+//   G1 grid_keys_kernel    : float4 depth loads, fp64 back-projection in the
+//                            reference's operation order (slam.py:594-598),
+//                            floor(p / voxel) -> 63-bit biased voxel key, batch
+//                            bounding box of the voxel indices;
+//   G2 in-house LSD radix sort of (key, pixel id) on the bbox-relative key
+//                            (ceil(bits/8) passes of upsweep / scan /
+//                            stable downsweep with warp match_any ranks);
+//   G3 grid_select_kernel  : segment heads = lowest pixel id per voxel;
+//                            insert-if-absent into the GPU hash set of the map
+//                            (query-then-insert in one atomicCAS);
+//   G4 hash set            : open addressing, 64-bit keys, linear probing,
+//                            power-of-two capacity at load <= 1/2;
+//   G5 grid_emit_kernel    : pixel-order compaction (exclusive scan of the
+//                            new-head flags) and the GaussianField-compatible
+//                            outputs (mu, rgb/255, iso scale, depth, feature).
+// Semantics are pinned by oracle/grid.py.
+#include <cstring>
+
+#include "launchers.h"
+
+namespace xgs {
+
+namespace {
+
+constexpr uint64_t KEY_INVALID = ~0ull;
+constexpr int64_t KEY_BIAS = 1ll << 20;
+constexpr uint64_t EMPTY = ~0ull;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// Insert-if-absent; true when the key was not present before.
+__device__ __forceinline__ bool hs_insert(unsigned long long* table, uint64_t mask, uint64_t key) {
+  uint64_t h = mix64(key) & mask;
+  while (true) {
+    const unsigned long long prev = atomicCAS(table + h, (unsigned long long)EMPTY, (unsigned long long)key);
+    if (prev == EMPTY) return true;
+    if (prev == key) return false;
+    h = (h + 1) & mask;
+  }
+}
+__device__ __forceinline__ bool hs_contains(const unsigned long long* table, uint64_t mask, uint64_t key) {
+  uint64_t h = mix64(key) & mask;
+  while (true) {
+    const unsigned long long v = table[h];
+    if (v == key) return true;
+    if (v == EMPTY) return false;
+    h = (h + 1) & mask;
+  }
+}
+
+struct Cam {
+  double fx, fy, cx, cy, voxel;
+};
+
+// slam.py:594-598 with the dgemv FMA order (oracle/oracle.c backproject1).
+__device__ __forceinline__ void backproject(const double* __restrict__ R, const double* __restrict__ t, const Cam& c,
+                                            double u, double v, double d, double* p) {
+  const double c0 = ddiv(dmul(dsub(u, c.cx), d), c.fx);
+  const double c1 = ddiv(dmul(dsub(v, c.cy), d), c.fy);
+  const double w0 = dsub(c0, t[0]), w1 = dsub(c1, t[1]), w2 = dsub(d, t[2]);
+#pragma unroll
+  for (int i = 0; i < 3; i++) p[i] = __fma_rn(R[6 + i], w2, __fma_rn(R[3 + i], w1, dmul(R[i], w0)));
+}
+
+__device__ __forceinline__ bool voxel_of(const double* p, double voxel, int64_t* q) {
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    const double f = floor(ddiv(p[a], voxel));
+    if (!(f >= -(double)KEY_BIAS && f < (double)KEY_BIAS)) return false;
+    q[a] = (int64_t)f + KEY_BIAS;
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------- G1
+__global__ void __launch_bounds__(256)
+grid_keys_kernel(const float* __restrict__ depth, int64_t npix, int64_t H, int64_t W, int stride,
+                 const double* __restrict__ rot, const double* __restrict__ trans, Cam cam,
+                 uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, int* bbox, unsigned long long* nvalid,
+                 bool vec4) {
+  int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
+  unsigned cnt = 0;
+  const int64_t HW = H * W;
+  const int64_t nq = vec4 ? npix / 4 : npix;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    float dv[4];
+    int nv;
+    int64_t p0;
+    if (vec4) {
+      const float4 d4 = __ldg(reinterpret_cast<const float4*>(depth) + q);
+      dv[0] = d4.x; dv[1] = d4.y; dv[2] = d4.z; dv[3] = d4.w;
+      nv = 4;
+      p0 = q * 4;
+    } else {
+      dv[0] = __ldg(depth + q);
+      nv = 1;
+      p0 = q;
+    }
+    uint64_t kout[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      if (j >= nv) break;
+      const int64_t pid = p0 + j;
+      const int64_t f = pid / HW, rem = pid - f * HW;
+      const int64_t u = rem / W, v = rem - u * W;
+      uint64_t key = KEY_INVALID;
+      const float d32 = dv[j];
+      if ((u % stride) == 0 && (v % stride) == 0 && d32 > 0.f) {
+        double p[3];
+        backproject(rot + f * 9, trans + f * 3, cam, (double)u, (double)v, (double)d32, p);
+        int64_t qv[3];
+        if (voxel_of(p, cam.voxel, qv)) {
+          key = ((uint64_t)qv[0] << 42) | ((uint64_t)qv[1] << 21) | (uint64_t)qv[2];
+#pragma unroll
+          for (int a = 0; a < 3; a++) {
+            lo[a] = min(lo[a], (int)qv[a]);
+            hi[a] = max(hi[a], (int)qv[a]);
+          }
+          cnt++;
+        }
+      }
+      kout[j] = key;
+    }
+    if (vec4) {
+      reinterpret_cast<ulonglong2*>(keys)[q * 2] = make_ulonglong2(kout[0], kout[1]);
+      reinterpret_cast<ulonglong2*>(keys)[q * 2 + 1] = make_ulonglong2(kout[2], kout[3]);
+      reinterpret_cast<uint4*>(vals)[q] = make_uint4((uint32_t)p0, (uint32_t)p0 + 1, (uint32_t)p0 + 2, (uint32_t)p0 + 3);
+    } else {
+      keys[p0] = kout[0];
+      vals[p0] = (uint32_t)p0;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; a++)
+    for (int o = 16; o; o >>= 1) {
+      lo[a] = min(lo[a], __shfl_xor_sync(FULL, lo[a], o));
+      hi[a] = max(hi[a], __shfl_xor_sync(FULL, hi[a], o));
+    }
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+  if ((threadIdx.x & 31) == 0) {
+    if (cnt) {
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        atomicMin(bbox + a, lo[a]);
+        atomicMax(bbox + 3 + a, hi[a]);
+      }
+    }
+    atomicAdd(nvalid, (unsigned long long)cnt);
+  }
+}
+
+__global__ void init_bbox_kernel(int* bbox, unsigned long long* nvalid) {
+  if (threadIdx.x < 3) {
+    bbox[threadIdx.x] = INT_MAX;
+    bbox[3 + threadIdx.x] = INT_MIN;
+  }
+  if (threadIdx.x == 0) *nvalid = 0;
+}
+
+// ---------------------------------------------------------------- G2 radix sort
+// The sort key is the bbox-relative packing of the biased voxel fields:
+// rel = ((x-x0) << (by+bz)) | ((y-y0) << bz) | (z-z0); invalid keys map to
+// all ones and sort last.  Only the ordering matters (grouping by voxel).
+struct RelKey {
+  uint32_t x0, y0, z0;
+  int by, bz;
+  __device__ __forceinline__ uint64_t operator()(uint64_t key) const {
+    if (key == KEY_INVALID) return ~0ull;
+    const uint64_t m = (1ull << 21) - 1;
+    const uint64_t x = (key >> 42) - x0, y = ((key >> 21) & m) - y0, z = (key & m) - z0;
+    return (x << (by + bz)) | (y << bz) | z;
+  }
+};
+
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_ITEMS = 16;                       // per thread
+constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS; // 4096
+constexpr int RADIX = 256;
+
+__global__ void __launch_bounds__(SORT_THREADS)
+sort_upsweep_kernel(const uint64_t* __restrict__ keys, int64_t n, RelKey rk, int shift, int32_t* tile_hist,
+                    int64_t tiles) {
+  __shared__ int32_t h[8][RADIX];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 8 * RADIX; i += SORT_THREADS) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * SORT_TILE;
+  for (int r = 0; r < SORT_ITEMS; r++) {
+    const int64_t i = base + (int64_t)warp * (SORT_TILE / 8) + r * 32 + lane;
+    if (i < n) {
+      const int dg = (int)((rk(keys[i]) >> shift) & (RADIX - 1));
+      atomicAdd(&h[warp][dg], 1);
+    }
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < RADIX; d += SORT_THREADS) {
+    int32_t s = 0;
+    for (int w = 0; w < 8; w++) s += h[w][d];
+    tile_hist[(int64_t)d * tiles + blockIdx.x] = s;   // digit-major
+  }
+}
+
+__global__ void __launch_bounds__(SORT_THREADS)
+sort_downsweep_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t n, RelKey rk,
+                      int shift, const int32_t* __restrict__ scanned, int64_t tiles, uint64_t* __restrict__ kout,
+                      uint32_t* __restrict__ vout) {
+  __shared__ int32_t wc[8][RADIX];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int i = threadIdx.x; i < 8 * RADIX; i += SORT_THREADS) (&wc[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * SORT_TILE + (int64_t)warp * (SORT_TILE / 8);
+  uint64_t k[SORT_ITEMS];
+  uint32_t v[SORT_ITEMS];
+  int16_t rank[SORT_ITEMS];
+  uint8_t dg[SORT_ITEMS];
+#pragma unroll
+  for (int r = 0; r < SORT_ITEMS; r++) {
+    const int64_t i = base + r * 32 + lane;
+    const bool ok = i < n;
+    k[r] = ok ? kin[i] : KEY_INVALID;
+    v[r] = ok ? vin[i] : 0;
+    const int d = ok ? (int)((rk(k[r]) >> shift) & (RADIX - 1)) : -1;
+    const unsigned peers = __match_any_sync(FULL, d);
+    int rr = 0;
+    if (d >= 0) rr = wc[warp][d] + __popc(peers & lt);
+    __syncwarp();
+    if (d >= 0 && lane == __ffs(peers) - 1) wc[warp][d] += __popc(peers);
+    __syncwarp();
+    rank[r] = (int16_t)rr;
+    dg[r] = (uint8_t)(d < 0 ? 0 : d);
+    if (d < 0) rank[r] = -1;
+  }
+  __syncthreads();
+  // exclusive prefix over warps per digit (warp order == input order)
+  for (int d = threadIdx.x; d < RADIX; d += SORT_THREADS) {
+    int32_t run = scanned[(int64_t)d * tiles + blockIdx.x];
+    for (int w = 0; w < 8; w++) {
+      const int32_t c = wc[w][d];
+      wc[w][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < SORT_ITEMS; r++) {
+    if (rank[r] >= 0) {
+      const int32_t pos = wc[warp][dg[r]] + rank[r];
+      kout[pos] = k[r];
+      vout[pos] = v[r];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- exclusive scan (int32)
+constexpr int SCAN_THREADS = 512;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+template <typename T>
+__device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* sm, int32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t w = lane < (int)(blockDim.x >> 5) ? sm[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, w, o);
+      if (lane >= o) w += y;
+    }
+    sm[lane] = w;
+  }
+  __syncthreads();
+  const int32_t before = (warp ? sm[warp - 1] : 0) + x - v;
+  *total = sm[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return before;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const T* __restrict__ in, int64_t n, int32_t* sums) {
+  __shared__ int32_t sm[32];
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+  int32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++)
+    if (base + i < n) s += (int32_t)in[base + i];
+  int32_t total;
+  block_excl_scan<T>(s, sm, &total);
+  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) scan_sums_kernel(int32_t* sums, int64_t nb, int32_t* grand) {
+  __shared__ int32_t sm[32];
+  const int64_t per = (nb + 1023) / 1024;
+  const int64_t b0 = threadIdx.x * per, b1 = min(nb, b0 + per);
+  int32_t s = 0;
+  for (int64_t b = b0; b < b1; b++) s += sums[b];
+  int32_t total;
+  int32_t run = block_excl_scan<int32_t>(s, sm, &total);
+  for (int64_t b = b0; b < b1; b++) {
+    const int32_t c = sums[b];
+    sums[b] = run;
+    run += c;
+  }
+  if (threadIdx.x == 0 && grand) *grand = total;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SCAN_THREADS)
+scan_apply_kernel(const T* __restrict__ in, int64_t n, const int32_t* __restrict__ sums, int32_t* __restrict__ out) {
+  __shared__ int32_t sm[32];
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+  int32_t vals[SCAN_ITEMS];
+  int32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    vals[i] = base + i < n ? (int32_t)in[base + i] : 0;
+    s += vals[i];
+  }
+  int32_t total;
+  int32_t run = block_excl_scan<T>(s, sm, &total) + sums[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    if (base + i < n) out[base + i] = run;
+    run += vals[i];
+  }
+}
+
+template <typename T>
+cudaError_t exclusive_scan(const T* in, int64_t n, int32_t* out, int32_t* block_sums, int32_t* grand, cudaStream_t s) {
+  const int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+  if (nb == 0) return cudaSuccess;
+  scan_reduce_kernel<T><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, n, block_sums); count_launches(1);
+  scan_sums_kernel<<<1, 1024, 0, s>>>(block_sums, nb, grand); count_launches(1);
+  scan_apply_kernel<T><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, n, block_sums, out); count_launches(1);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- G3 select
+// Over the sorted (key, pid) items: a segment head (first item of a voxel,
+// i.e. its lowest pixel id) inserts its key into the map set; if the key was
+// absent the head pixel is flagged new and remembers its sorted position.
+__global__ void __launch_bounds__(256)
+grid_select_kernel(const uint64_t* __restrict__ k, const uint32_t* __restrict__ v, int64_t n,
+                   unsigned long long* table, uint64_t mask, unsigned long long* set_count, uint8_t* flag,
+                   int32_t* head_pos, unsigned long long* nvox) {
+  unsigned newc = 0, vox = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = k[i];
+    if (key == KEY_INVALID) continue;
+    if (i > 0 && k[i - 1] == key) continue;
+    vox++;
+    if (hs_insert(table, mask, key)) {
+      const uint32_t pid = v[i];
+      flag[pid] = 1;
+      head_pos[pid] = (int32_t)i;
+      newc++;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    newc += __shfl_xor_sync(FULL, newc, o);
+    vox += __shfl_xor_sync(FULL, vox, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (newc) atomicAdd(set_count, (unsigned long long)newc);
+    if (vox) atomicAdd(nvox, (unsigned long long)vox);
+  }
+}
+
+// ---------------------------------------------------------------- G5 emit
+struct EmitArgs {
+  const float* depth;
+  const uint8_t* color;     // [F*H*W*3] or null
+  const double* rot;
+  const double* trans;
+  Cam cam;
+  int64_t H, W;
+  int stride, mode;
+  double min_scale;
+  const float* feat;        // [F, C, Hf, Wf] or null
+  int64_t fc, fh, fw;
+  const uint64_t* skeys;    // sorted keys / pids (mean mode walks segments)
+  const uint32_t* svals;
+  int64_t n;
+  // outputs
+  uint64_t* key;
+  int64_t* pid;
+  double* mu;
+  double* col;
+  double* scale;
+  double* dep;
+  float* ofeat;
+  double* count;
+};
+
+__global__ void __launch_bounds__(256)
+grid_emit_kernel(const uint8_t* __restrict__ flag, const int32_t* __restrict__ pos, const int32_t* __restrict__ head_pos,
+                 int64_t npix, EmitArgs a) {
+  const int64_t HW = a.H * a.W;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npix; p += (int64_t)gridDim.x * blockDim.x) {
+    if (!flag[p]) continue;
+    const int64_t o = pos[p];
+    const int64_t f = p / HW, rem = p - f * HW;
+    const int64_t u = rem / a.W, v = rem - u * a.W;
+    const double d = (double)a.depth[p];
+    a.pid[o] = p;
+    a.dep[o] = d;
+    // iso size max(min_scale, 0.5*s*depth/fx)  (slam.py:631)
+    const double sz = ddiv(dmul(dmul(0.5, (double)a.stride), d), a.cam.fx);
+    a.scale[o] = fmax(a.min_scale, sz);
+    if (a.mode == 0) {
+      double mu[3];
+      backproject(a.rot + f * 9, a.trans + f * 3, a.cam, (double)u, (double)v, d, mu);
+      int64_t q[3];
+      voxel_of(mu, a.cam.voxel, q);
+      a.key[o] = ((uint64_t)q[0] << 42) | ((uint64_t)q[1] << 21) | (uint64_t)q[2];
+      for (int c = 0; c < 3; c++) {
+        a.mu[o * 3 + c] = mu[c];
+        a.col[o * 3 + c] = a.color ? ddiv((double)a.color[p * 3 + c], 255.0) : 0.0;
+      }
+      if (a.count) a.count[o] = 1.0;
+      if (a.feat) {
+        // supervision.py:133-147 nearest-neighbour gather rule
+        const int64_t uu = (int64_t)floor(ddiv(dmul((double)u, (double)(a.fh - 1)), (double)max(a.H - 1, (int64_t)1)) + 0.5);
+        const int64_t vv = (int64_t)floor(ddiv(dmul((double)v, (double)(a.fw - 1)), (double)max(a.W - 1, (int64_t)1)) + 0.5);
+        const float* src = a.feat + f * a.fc * a.fh * a.fw + uu * a.fw + vv;
+        for (int64_t c = 0; c < a.fc; c++) a.ofeat[o * a.fc + c] = src[c * a.fh * a.fw];
+      }
+    } else {
+      // mean over the voxel's points in the head's frame, sequential in pid order
+      const int64_t i0 = head_pos[p];
+      const uint64_t key = a.skeys[i0];
+      a.key[o] = key;
+      double sm[3] = {0.0, 0.0, 0.0}, sc[3] = {0.0, 0.0, 0.0};
+      double cnt = 0.0;
+      for (int64_t i = i0; i < a.n && a.skeys[i] == key; i++) {
+        const int64_t q = a.svals[i];
+        if (q / HW != f) continue;
+        const int64_t r2 = q - f * HW;
+        const int64_t uq = r2 / a.W, vq = r2 - uq * a.W;
+        double mu[3];
+        backproject(a.rot + f * 9, a.trans + f * 3, a.cam, (double)uq, (double)vq, (double)a.depth[q], mu);
+        for (int c = 0; c < 3; c++) {
+          sm[c] = dadd(sm[c], mu[c]);
+          if (a.color) sc[c] = dadd(sc[c], ddiv((double)a.color[q * 3 + c], 255.0));
+        }
+        cnt = dadd(cnt, 1.0);
+      }
+      for (int c = 0; c < 3; c++) {
+        a.mu[o * 3 + c] = ddiv(sm[c], cnt);
+        a.col[o * 3 + c] = ddiv(sc[c], cnt);
+      }
+      if (a.count) a.count[o] = cnt;
+    }
+  }
+}
+
+__global__ void fill_u64_kernel(unsigned long long* p, int64_t n, unsigned long long v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+__global__ void rehash_kernel(const unsigned long long* old, int64_t oldcap, unsigned long long* table, uint64_t mask) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < oldcap; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = old[i];
+    if (k != EMPTY) hs_insert(table, mask, k);
+  }
+}
+
+__global__ void hs_insert_kernel(unsigned long long* table, uint64_t mask, const uint64_t* keys, int64_t n,
+                                 uint8_t* was_new, unsigned long long* count) {
+  unsigned c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const bool nw = keys[i] != KEY_INVALID && hs_insert(table, mask, keys[i]);
+    if (was_new) was_new[i] = nw;
+    c += nw;
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
+}
+
+__global__ void hs_contains_kernel(const unsigned long long* table, uint64_t mask, const uint64_t* keys, int64_t n,
+                                   uint8_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = keys[i] != KEY_INVALID && hs_contains(table, mask, keys[i]);
+}
+
+__global__ void backproject_kernel(const double* R, const double* t, Cam cam, const double* u, const double* v,
+                                   const double* d, int64_t n, double* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    backproject(R, t, cam, u[i], v[i], d[i], out + 3 * i);
+}
+
+unsigned grid_blocks(int64_t n, int threads, int sms) {
+  int64_t b = (n + threads - 1) / threads;
+  const int64_t cap = (int64_t)sms * 16;
+  if (b > cap) b = cap;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+int bits_for(int64_t range) {  // bits to hold values 0..range
+  int b = 1;
+  while ((1ll << b) <= range) b++;
+  return b;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host API (C++)
+
+struct HashSet {
+  unsigned long long* table = nullptr;
+  int64_t cap = 0;
+  unsigned long long* count_dev = nullptr;
+};
+
+cudaError_t hashset_create(int64_t capacity, HashSet** out) {
+  int64_t cap = 1024;
+  while (cap < capacity) cap <<= 1;
+  HashSet* h = new HashSet();
+  cudaError_t e = cudaMalloc(&h->table, sizeof(unsigned long long) * cap);
+  if (e == cudaSuccess) e = cudaMalloc(&h->count_dev, sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    cudaFree(h->table);
+    delete h;
+    return e;
+  }
+  h->cap = cap;
+  fill_u64_kernel<<<grid_blocks(cap, 256, 148), 256>>>(h->table, cap, EMPTY); count_launches(1);
+  cudaMemset(h->count_dev, 0, sizeof(unsigned long long));
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return e;
+  *out = h;
+  return cudaSuccess;
+}
+
+void hashset_destroy(HashSet* h) {
+  if (!h) return;
+  cudaFree(h->table);
+  cudaFree(h->count_dev);
+  delete h;
+}
+
+cudaError_t hashset_size(HashSet* h, int64_t* n, cudaStream_t s) {
+  unsigned long long c = 0;
+  cudaError_t e = cudaMemcpyAsync(&c, h->count_dev, sizeof(c), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  *n = (int64_t)c;
+  return e;
+}
+
+// grow so that `extra` more keys keep the load factor <= 1/2
+cudaError_t hashset_reserve(HashSet* h, int64_t extra, cudaStream_t s) {
+  int64_t cur = 0;
+  cudaError_t e = hashset_size(h, &cur, s);
+  if (e != cudaSuccess) return e;
+  if (2 * (cur + extra) <= h->cap) return cudaSuccess;
+  int64_t cap = h->cap;
+  while (2 * (cur + extra) > cap) cap <<= 1;
+  unsigned long long* t = nullptr;
+  if ((e = cudaMallocAsync(&t, sizeof(unsigned long long) * cap, s)) != cudaSuccess) return e;
+  fill_u64_kernel<<<grid_blocks(cap, 256, 148), 256, 0, s>>>(t, cap, EMPTY); count_launches(1);
+  rehash_kernel<<<grid_blocks(h->cap, 256, 148), 256, 0, s>>>(h->table, h->cap, t, (uint64_t)cap - 1); count_launches(1);
+  cudaFreeAsync(h->table, s);
+  h->table = t;
+  h->cap = cap;
+  return cudaGetLastError();
+}
+
+cudaError_t hashset_insert(HashSet* h, const uint64_t* keys, int64_t n, uint8_t* was_new, cudaStream_t s) {
+  cudaError_t e = hashset_reserve(h, n, s);
+  if (e != cudaSuccess || n == 0) return e;
+  hs_insert_kernel<<<grid_blocks(n, 256, 148), 256, 0, s>>>(h->table, (uint64_t)h->cap - 1, keys, n, was_new,
+                                                           h->count_dev); count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t hashset_contains(HashSet* h, const uint64_t* keys, int64_t n, uint8_t* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  hs_contains_kernel<<<grid_blocks(n, 256, 148), 256, 0, s>>>(h->table, (uint64_t)h->cap - 1, keys, n, out); count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_backproject(const double* R, const double* t, const double* intr4, double voxel, const double* u,
+                               const double* v, const double* d, int64_t n, double* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  Cam cam{intr4[0], intr4[1], intr4[2], intr4[3], voxel};
+  backproject_kernel<<<grid_blocks(n, 256, 148), 256, 0, s>>>(R, t, cam, u, v, d, n, out); count_launches(1);
+  return cudaGetLastError();
+}
+
+// Workspace layout for one batch of npix pixels.
+struct GridWs {
+  size_t off_k0, off_v0, off_k1, off_v1, off_hist, off_scan_sums, off_flag, off_pos, off_head, off_misc, total;
+  int64_t tiles;
+};
+
+GridWs grid_ws(int64_t npix) {
+  GridWs w;
+  size_t o = 0;
+  auto take = [&](size_t b) { size_t r = o; o += (b + 255) / 256 * 256; return r; };
+  const size_t n = (size_t)(npix > 0 ? npix : 1);
+  w.tiles = (npix + SORT_TILE - 1) / SORT_TILE;
+  if (w.tiles < 1) w.tiles = 1;
+  w.off_k0 = take(n * 8);
+  w.off_v0 = take(n * 4);
+  w.off_k1 = take(n * 8);
+  w.off_v1 = take(n * 4);
+  w.off_hist = take((size_t)RADIX * w.tiles * 4);
+  const size_t scan_n = n > (size_t)RADIX * w.tiles ? n : (size_t)RADIX * w.tiles;
+  w.off_scan_sums = take(((scan_n + SCAN_TILE - 1) / SCAN_TILE + 1) * 4);
+  w.off_flag = take(n);
+  w.off_pos = take(n * 4);
+  w.off_head = take(n * 4);
+  w.off_misc = take(256);
+  w.total = o;
+  return w;
+}
+
+size_t grid_workspace_bytes(int64_t npix) { return grid_ws(npix).total; }
+
+cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, size_t ws_bytes, int sms,
+                        cudaStream_t s) {
+  const int64_t npix = in.frames * in.H * in.W;
+  const GridWs w = grid_ws(npix);
+  if (ws_bytes < w.total) return cudaErrorInvalidValue;
+  char* b = static_cast<char*>(ws);
+  uint64_t* k0 = reinterpret_cast<uint64_t*>(b + w.off_k0);
+  uint32_t* v0 = reinterpret_cast<uint32_t*>(b + w.off_v0);
+  uint64_t* k1 = reinterpret_cast<uint64_t*>(b + w.off_k1);
+  uint32_t* v1 = reinterpret_cast<uint32_t*>(b + w.off_v1);
+  int32_t* hist = reinterpret_cast<int32_t*>(b + w.off_hist);
+  int32_t* ssum = reinterpret_cast<int32_t*>(b + w.off_scan_sums);
+  uint8_t* flag = reinterpret_cast<uint8_t*>(b + w.off_flag);
+  int32_t* pos = reinterpret_cast<int32_t*>(b + w.off_pos);
+  int32_t* head = reinterpret_cast<int32_t*>(b + w.off_head);
+  int* bbox = reinterpret_cast<int*>(b + w.off_misc);
+  unsigned long long* cnts = reinterpret_cast<unsigned long long*>(b + w.off_misc + 64);  // nvalid, nvox
+  int32_t* grand = reinterpret_cast<int32_t*>(b + w.off_misc + 128);
+  out.n_new = out.n_valid = out.n_voxels = 0;
+  if (npix == 0) return cudaSuccess;
+  cudaError_t e;
+  const Cam cam{in.fx, in.fy, in.cx, in.cy, in.voxel};
+  {
+    ProfScope prof("grid_keys", s);
+    init_bbox_kernel<<<1, 32, 0, s>>>(bbox, cnts); count_launches(1);
+    cudaMemsetAsync(cnts + 1, 0, 8, s);
+    const bool vec4 = (npix % 4 == 0) && (reinterpret_cast<uintptr_t>(in.depth) % 16 == 0);
+    grid_keys_kernel<<<grid_blocks(vec4 ? npix / 4 : npix, 256, sms), 256, 0, s>>>(
+        in.depth, npix, in.H, in.W, in.stride, in.rot, in.trans, cam, k0, v0, bbox, cnts, vec4); count_launches(1);
+  }
+  int hb[8];
+  unsigned long long nvalid = 0;
+  if ((e = cudaMemcpyAsync(hb, bbox, 6 * sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(&nvalid, cnts, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  out.n_valid = (int64_t)nvalid;
+  if (nvalid == 0) return cudaSuccess;
+  if ((e = hashset_reserve(hs, (int64_t)nvalid, s)) != cudaSuccess) return e;
+  // bbox-relative key width; +1 on x keeps the all-ones invalid key above every valid key
+  RelKey rk;
+  rk.x0 = (uint32_t)hb[0];
+  rk.y0 = (uint32_t)hb[1];
+  rk.z0 = (uint32_t)hb[2];
+  const int bx = bits_for((int64_t)hb[3] - hb[0] + 1), by = bits_for((int64_t)hb[4] - hb[1]),
+            bz = bits_for((int64_t)hb[5] - hb[2]);
+  rk.by = by;
+  rk.bz = bz;
+  int bits = bx + by + bz;
+  if (bits > 64) {  // degenerate extent: sort the raw biased keys (identity packing)
+    rk.x0 = rk.y0 = rk.z0 = 0;
+    rk.by = rk.bz = 21;
+    bits = 64;
+  }
+  {
+    ProfScope prof("grid_sort", s);
+    for (int shift = 0; shift < bits; shift += 8) {
+      sort_upsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, 0, s>>>(k0, npix, rk, shift, hist, w.tiles); count_launches(1);
+      if ((e = exclusive_scan<int32_t>(hist, (int64_t)RADIX * w.tiles, hist, ssum, nullptr, s)) != cudaSuccess) return e;
+      sort_downsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, 0, s>>>(k0, v0, npix, rk, shift, hist, w.tiles, k1, v1); count_launches(1);
+      uint64_t* tk = k0; k0 = k1; k1 = tk;
+      uint32_t* tv = v0; v0 = v1; v1 = tv;
+    }
+  }
+  {
+    ProfScope prof("grid_select", s);
+    cudaMemsetAsync(flag, 0, (size_t)npix, s);
+    grid_select_kernel<<<grid_blocks(npix, 256, sms), 256, 0, s>>>(k0, v0, npix, hs->table, (uint64_t)hs->cap - 1,
+                                                                   hs->count_dev, flag, head, cnts + 1); count_launches(1);
+  }
+  {
+    ProfScope prof("grid_emit", s);
+    if ((e = exclusive_scan<uint8_t>(flag, npix, pos, ssum, grand, s)) != cudaSuccess) return e;
+    int32_t nnew = 0;
+    unsigned long long nvox = 0;
+    if ((e = cudaMemcpyAsync(&nnew, grand, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(&nvox, cnts + 1, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    out.n_new = nnew;
+    out.n_voxels = (int64_t)nvox;
+    if (nnew > out.capacity) return cudaErrorInvalidValue;
+    EmitArgs a;
+    a.depth = in.depth;
+    a.color = in.color;
+    a.rot = in.rot;
+    a.trans = in.trans;
+    a.cam = cam;
+    a.H = in.H;
+    a.W = in.W;
+    a.stride = in.stride;
+    a.mode = in.mode;
+    a.min_scale = in.min_scale;
+    a.feat = in.feat;
+    a.fc = in.fc;
+    a.fh = in.fh;
+    a.fw = in.fw;
+    a.skeys = k0;
+    a.svals = v0;
+    a.n = npix;
+    a.key = out.key;
+    a.pid = out.pid;
+    a.mu = out.mu;
+    a.col = out.color;
+    a.scale = out.scale;
+    a.dep = out.depth;
+    a.ofeat = out.feat;
+    a.count = out.count;
+    grid_emit_kernel<<<grid_blocks(npix, 256, sms), 256, 0, s>>>(flag, pos, head, npix, a); count_launches(1);
+  }
+  return cudaGetLastError();
+}
+
+// standalone in-house radix sort of (u64 key, u32 value) pairs on bits [0, bits)
+cudaError_t radix_sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n, int bits, void* ws, size_t ws_bytes,
+                             cudaStream_t s) {
+  const GridWs w = grid_ws(n);
+  if (ws_bytes < w.total) return cudaErrorInvalidValue;
+  char* b = static_cast<char*>(ws);
+  uint64_t* k1 = reinterpret_cast<uint64_t*>(b + w.off_k1);
+  uint32_t* v1 = reinterpret_cast<uint32_t*>(b + w.off_v1);
+  int32_t* hist = reinterpret_cast<int32_t*>(b + w.off_hist);
+  int32_t* ssum = reinterpret_cast<int32_t*>(b + w.off_scan_sums);
+  RelKey ident;  // identity on raw bits: x0=y0=z0=0, fields re-packed in place
+  ident.x0 = ident.y0 = ident.z0 = 0;
+  ident.by = 21;
+  ident.bz = 21;
+  uint64_t* k0 = keys;
+  uint32_t* v0 = vals;
+  cudaError_t e;
+  for (int shift = 0; shift < bits; shift += 8) {
+    sort_upsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, 0, s>>>(k0, n, ident, shift, hist, w.tiles); count_launches(1);
+    if ((e = exclusive_scan<int32_t>(hist, (int64_t)RADIX * w.tiles, hist, ssum, nullptr, s)) != cudaSuccess) return e;
+    sort_downsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, 0, s>>>(k0, v0, n, ident, shift, hist, w.tiles, k1, v1); count_launches(1);
+    uint64_t* tk = k0; k0 = k1; k1 = tk;
+    uint32_t* tv = v0; v0 = v1; v1 = tv;
+  }
+  if (k0 != keys) {
+    if ((e = cudaMemcpyAsync(keys, k0, n * 8, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(vals, v0, n * 4, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace xgs

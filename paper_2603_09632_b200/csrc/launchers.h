@@ -93,4 +93,44 @@ cudaError_t launch_ring_write(const void* x, int dtype, int64_t ldx, int64_t row
 cudaError_t launch_gather_rows(const double* src, int64_t d, const int64_t* rows, int64_t n,
                                double* dst, cudaStream_t s);
 
+// ---------------- voxel grid sampling (grid.cu) ----------------
+struct HashSet;
+cudaError_t hashset_create(int64_t capacity, HashSet** out);
+void hashset_destroy(HashSet* h);
+cudaError_t hashset_size(HashSet* h, int64_t* n, cudaStream_t s);
+cudaError_t hashset_reserve(HashSet* h, int64_t extra, cudaStream_t s);
+cudaError_t hashset_insert(HashSet* h, const uint64_t* keys, int64_t n, uint8_t* was_new, cudaStream_t s);
+cudaError_t hashset_contains(HashSet* h, const uint64_t* keys, int64_t n, uint8_t* out, cudaStream_t s);
+cudaError_t launch_backproject(const double* R, const double* t, const double* intr4, double voxel, const double* u,
+                               const double* v, const double* d, int64_t n, double* out, cudaStream_t s);
+size_t grid_workspace_bytes(int64_t npix);
+struct GridIn {
+  int64_t frames, H, W;
+  const float* depth;
+  const uint8_t* color;
+  const double* rot;
+  const double* trans;
+  double fx, fy, cx, cy, voxel;
+  int stride, mode;
+  double min_scale;
+  const float* feat;
+  int64_t fc, fh, fw;
+};
+struct GridOut {
+  int64_t capacity;
+  uint64_t* key;
+  int64_t* pid;
+  double* mu;
+  double* color;
+  double* scale;
+  double* depth;
+  float* feat;
+  double* count;
+  int64_t n_new, n_valid, n_voxels;
+};
+cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, size_t ws_bytes, int sms,
+                        cudaStream_t s);
+cudaError_t radix_sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n, int bits, void* ws, size_t ws_bytes,
+                             cudaStream_t s);
+
 }  // namespace xgs

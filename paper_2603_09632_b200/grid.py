@@ -1,0 +1,240 @@
+"""GPU voxel grid sampling of back-projected RGB-D frames (north-star GRID half).
+
+The reference has no voxel sampler: its only code that turns back-projected
+RGB-D pixels into new Gaussians is ``slam.backproject`` + the insertion half
+of ``slam.densify_and_prune`` (slam.py:594-651).  This module keeps that
+arithmetic and conventions (fp64 back-projection in the reference's operation
+order, ``depth > 0`` validity, stride lattice, rgb/255 colours, iso size
+``max(min_scale, 0.5*s*depth/fx)``, row-major emission) and replaces the
+per-pixel Python loop + coverage render with the libxgs pipeline
+(include/xgs.h ``xgs_grid_sample``): keys -> in-house LSD radix sort ->
+first-pick / mean select -> hash-set occupancy test -> pixel-order emit.
+Definitions: SURVEY.md §8(a) g8, oracle/grid.py.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _native as nat
+from .core import CameraIntrinsics, CameraPose, is_tensor
+from .errors import InvalidInputError
+
+KEY_BIAS = 1 << 20
+KEY_INVALID = (1 << 64) - 1
+
+
+def pack_key(ix, iy, iz):
+    """Voxel indices -> 63-bit keys (21-bit fields biased by 2^20)."""
+    ix, iy, iz = (np.asarray(a, dtype=np.int64) + KEY_BIAS for a in (ix, iy, iz))
+    return ((ix.astype(np.uint64) << np.uint64(42)) | (iy.astype(np.uint64) << np.uint64(21))
+            | iz.astype(np.uint64))
+
+
+class VoxelHashSet:
+    """Occupied-voxel set of the map, resident in HBM (open addressing)."""
+
+    def __init__(self, capacity: int = 1 << 20):
+        nat.require_cuda()
+        h = ctypes.c_void_p()
+        nat.call("xgs_hashset_create", int(capacity), ctypes.byref(h))
+        self._h = h
+
+    def __len__(self):
+        n = ctypes.c_int64()
+        nat.call("xgs_hashset_size", self._h, ctypes.byref(n), nat.stream_ptr())
+        return int(n.value)
+
+    def _keys(self, keys):
+        t = nat.torch()
+        if not is_tensor(keys):
+            keys = t.from_numpy(np.ascontiguousarray(np.asarray(keys, dtype=np.uint64)).view(np.int64))
+        return keys.to(device="cuda", dtype=t.int64).contiguous()
+
+    def insert(self, keys):
+        """Insert-if-absent; returns a bool mask of keys that were new."""
+        t = nat.torch()
+        k = self._keys(keys)
+        out = t.empty(k.numel(), dtype=t.uint8, device="cuda")
+        nat.call("xgs_hashset_insert", self._h, nat.ptr(k), k.numel(), nat.ptr(out), nat.stream_ptr())
+        return out.bool()
+
+    def contains(self, keys):
+        t = nat.torch()
+        k = self._keys(keys)
+        out = t.empty(k.numel(), dtype=t.uint8, device="cuda")
+        nat.call("xgs_hashset_contains", self._h, nat.ptr(k), k.numel(), nat.ptr(out), nat.stream_ptr())
+        return out.bool()
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and nat._lib is not None:
+            nat.lib().xgs_hashset_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class GridSampleResult:
+    """New Gaussians of one batch, ascending (frame, pixel) id (CUDA tensors)."""
+
+    key: object       # (n,) int64 view of the uint64 voxel keys
+    pid: object       # (n,) int64: frame*H*W + u*W + v
+    mu: object        # (n, 3) fp64 world positions
+    color: object     # (n, 3) fp64 rgb/255
+    scale: object     # (n,) fp64 iso size
+    depth: object     # (n,) fp64 camera depth of the representative pixel
+    count: object     # (n,) fp64 points averaged (mean mode) or 1
+    feature: Optional[object]
+    n_valid: int
+    n_voxels: int
+
+    def __len__(self):
+        return int(self.pid.shape[0])
+
+    def to_numpy(self):
+        h = lambda t: None if t is None else t.cpu().numpy()
+        return dict(key=h(self.key).view(np.uint64), pid=h(self.pid), mu=h(self.mu), color=h(self.color),
+                    scale=h(self.scale), depth=h(self.depth), count=h(self.count), feature=h(self.feature),
+                    n_valid=self.n_valid, n_voxels=self.n_voxels)
+
+
+def _intr4(intr):
+    if isinstance(intr, CameraIntrinsics):
+        return float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy)
+    fx, fy, cx, cy = (float(v) for v in intr)
+    return fx, fy, cx, cy
+
+
+def _poses(poses, F):
+    """list[CameraPose] | (R [F,3,3], t [F,3]) -> device fp64 (R, t)."""
+    t = nat.torch()
+    if isinstance(poses, CameraPose):
+        poses = [poses]
+    if isinstance(poses, (list, tuple)) and poses and isinstance(poses[0], CameraPose):
+        R = np.stack([p.rotation for p in poses])
+        tr = np.stack([p.translation for p in poses])
+    else:
+        R, tr = poses
+    R = R if is_tensor(R) else t.from_numpy(np.ascontiguousarray(np.asarray(R, dtype=np.float64)))
+    tr = tr if is_tensor(tr) else t.from_numpy(np.ascontiguousarray(np.asarray(tr, dtype=np.float64)))
+    R = R.to(device="cuda", dtype=t.float64).reshape(-1, 9).contiguous()
+    tr = tr.to(device="cuda", dtype=t.float64).reshape(-1, 3).contiguous()
+    if R.shape[0] != F or tr.shape[0] != F:
+        raise InvalidInputError("one pose per frame required")
+    return R, tr
+
+
+def _dev(a, dtype):
+    t = nat.torch()
+    if a is None:
+        return None
+    if is_tensor(a):
+        return a.to(device="cuda", dtype=dtype).contiguous()
+    np_dt = {t.float32: np.float32, t.uint8: np.uint8}[dtype]
+    return t.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np_dt))).to("cuda")
+
+
+class GridSampler:
+    """Incremental voxel grid sampler bound to one map (its occupancy set).
+
+    ``sample`` processes a batch of frames; frames in a batch behave exactly
+    like frames submitted one by one in order (first occurrence over
+    (frame, pixel) wins, later frames see the earlier frames' voxels).
+    """
+
+    def __init__(self, intrinsics, voxel_size: float, stride: int = 1, mode: str = "first",
+                 min_scale: float = 1e-3, occupied: Optional[VoxelHashSet] = None, capacity: int = 1 << 20):
+        if voxel_size <= 0:
+            raise InvalidInputError("voxel size must be positive")
+        if stride < 1:
+            raise InvalidInputError("stride must be >= 1")
+        if mode not in ("first", "mean"):
+            raise InvalidInputError("mode must be 'first' or 'mean'")
+        self.intr = _intr4(intrinsics)
+        self.voxel = float(voxel_size)
+        self.stride = int(stride)
+        self.mode = mode
+        self.min_scale = float(min_scale)
+        self.occupied = occupied if occupied is not None else VoxelHashSet(capacity)
+
+    def sample(self, depth, poses, color=None, features=None) -> GridSampleResult:
+        t = nat.require_cuda()
+        d = _dev(depth, t.float32)
+        if d.dim() == 2:
+            d = d.unsqueeze(0)
+        if d.dim() != 3:
+            raise InvalidInputError("depth must be (H, W) or (F, H, W)")
+        F, H, W = (int(v) for v in d.shape)
+        R, tr = _poses(poses, F)
+        col = _dev(color, t.uint8)
+        if col is not None:
+            col = col.reshape(F, H, W, 3) if col.dim() != 4 else col
+            if tuple(col.shape) != (F, H, W, 3):
+                raise InvalidInputError("color must be (F, H, W, 3) uint8")
+        feat = _dev(features, t.float32) if features is not None else None
+        if feat is not None and feat.dim() == 3:
+            feat = feat.unsqueeze(0)
+        s = self.stride
+        cap = max(1, F * ((H + s - 1) // s) * ((W + s - 1) // s))
+        C = int(feat.shape[1]) if feat is not None else 0
+        out = dict(key=t.empty(cap, dtype=t.int64, device="cuda"), pid=t.empty(cap, dtype=t.int64, device="cuda"),
+                   mu=t.empty((cap, 3), dtype=t.float64, device="cuda"),
+                   color=t.empty((cap, 3), dtype=t.float64, device="cuda"),
+                   scale=t.empty(cap, dtype=t.float64, device="cuda"),
+                   depth=t.empty(cap, dtype=t.float64, device="cuda"),
+                   count=t.empty(cap, dtype=t.float64, device="cuda"),
+                   feature=t.empty((cap, C), dtype=t.float32, device="cuda") if feat is not None else None)
+        fx, fy, cx, cy = self.intr
+        fr = nat.GridFrames(F, H, W, d.data_ptr(), col.data_ptr() if col is not None else None, R.data_ptr(),
+                            tr.data_ptr(), fx, fy, cx, cy, self.voxel, s, 0 if self.mode == "first" else 1,
+                            self.min_scale, feat.data_ptr() if feat is not None else None,
+                            C, int(feat.shape[2]) if feat is not None else 0,
+                            int(feat.shape[3]) if feat is not None else 0)
+        res = nat.GridResult(cap, out["key"].data_ptr(), out["pid"].data_ptr(), out["mu"].data_ptr(),
+                             out["color"].data_ptr(), out["scale"].data_ptr(), out["depth"].data_ptr(),
+                             out["feature"].data_ptr() if feat is not None else None, out["count"].data_ptr(),
+                             0, 0, 0)
+        ws = nat.workspace("grid", nat.lib().xgs_grid_workspace(F * H * W))
+        nat.call("xgs_grid_sample", ctypes.byref(fr), self.occupied._h, ctypes.byref(res), nat.ptr(ws), ws.numel(),
+                 nat.stream_ptr())
+        n = int(res.n_new)
+        return GridSampleResult(key=out["key"][:n], pid=out["pid"][:n], mu=out["mu"][:n], color=out["color"][:n],
+                                scale=out["scale"][:n], depth=out["depth"][:n], count=out["count"][:n],
+                                feature=out["feature"][:n] if feat is not None else None,
+                                n_valid=int(res.n_valid), n_voxels=int(res.n_voxels))
+
+
+def radix_sort_pairs(keys, vals, bits: int = 64):
+    """In-house stable LSD radix sort of (uint64 key, uint32 value) pairs (CUDA tensors, in place)."""
+    t = nat.require_cuda()
+    n = int(keys.numel())
+    ws = nat.workspace("sort", nat.lib().xgs_grid_workspace(n))
+    nat.call("xgs_radix_sort_pairs_u64", nat.ptr(keys), nat.ptr(vals), n, int(bits), nat.ptr(ws), ws.numel(),
+             nat.stream_ptr())
+    return keys, vals
+
+
+def smoke_check():
+    """One small batch against the CPU oracle (used by __graft_entry__.smoke)."""
+    from oracle import grid as og
+    rng = np.random.default_rng(0)
+    H, W = 48, 64
+    depth = rng.uniform(0.5, 5.0, (2, H, W)).astype(np.float32)
+    depth[rng.random((2, H, W)) < 0.05] = 0
+    color = rng.integers(0, 256, (2, H, W, 3), dtype=np.uint8)
+    R = np.stack([np.eye(3), np.eye(3)])
+    tr = np.array([[0.0, 0, 0], [0.05, 0, 0]])
+    intr = (60.0, 60.0, 23.5, 31.5)
+    gs = GridSampler(intr, 0.05)
+    got = gs.sample(depth, (R, tr), color).to_numpy()
+    ref = og.grid_sample([(depth[f], color[f], R[f], tr[f]) for f in range(2)], np.array(intr), 0.05, set())
+    assert np.array_equal(got["pid"], ref["pid"]) and np.array_equal(got["mu"], ref["mu"]), "grid smoke mismatch"

@@ -1,0 +1,179 @@
+"""Drop-ins for the back-projection / insertion part of ``semsplat.slam``.
+
+``backproject`` (slam.py:594-598) and ``densify_and_prune`` (slam.py:601-651)
+keep their reference signatures; the arithmetic runs in libxgs
+(``xgs_backproject``: fp64, reference operation order, bit-identical).
+``densify_and_prune`` reproduces the reference exactly on an empty map; on a
+non-empty map the rasterizer coverage test (a full render, out of scope) is
+replaced by the voxel occupancy test of :mod:`grid`.
+The voxel-grid sampler for whole RGB-D frames is :class:`grid.GridSampler`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _native as nat
+from .core import CameraIntrinsics, CameraPose, GaussianField
+from .errors import InvalidInputError
+
+
+@dataclass
+class SlamConfig:
+    """The densify/prune fields of the reference SlamConfig (slam.py:36-76)."""
+
+    min_scale: float = 1e-3
+    prune_opacity: float = 0.01
+    coverage_alpha: float = 0.5
+    insert_stride: int = 4
+    insert_opacity: float = 0.8
+    default_depth: float = 2.0
+
+
+@dataclass
+class CameraFrame:
+    """world.py:67-73 (colour (3,H,W) floats in [0,1], depth (H,W) or None)."""
+
+    frame_id: int
+    pose: CameraPose
+    color: np.ndarray
+    depth: Optional[np.ndarray]
+
+
+@dataclass
+class Keyframe:
+    frame: object
+    pose: CameraPose
+
+
+class KeyframeWindow:
+    """Sliding keyframe window (slam.py:92-117)."""
+
+    def __init__(self, capacity: int):
+        if capacity < 1:
+            raise InvalidInputError("window capacity must be >= 1")
+        self.capacity = capacity
+        self.frames: list = []
+        self.log: list = []
+
+    def __len__(self):
+        return len(self.frames)
+
+    @property
+    def newest(self):
+        return self.frames[-1]
+
+    def insert(self, frame, pose):
+        self.frames.append(Keyframe(frame=frame, pose=pose))
+        self.log.append((frame.frame_id, "insert"))
+        if len(self.frames) > self.capacity:
+            ev = self.frames.pop(0)
+            self.log.append((ev.frame.frame_id, "evict"))
+            return ev.frame.frame_id
+        return None
+
+
+def frame_intrinsics(frame, cfg=None, fov_deg: float = 60.0) -> CameraIntrinsics:
+    """slam.py:276-286: intrinsics from the frame resolution (60 deg FOV)."""
+    H, W = frame.color.shape[1:]
+    return CameraIntrinsics.from_fov(H, W, fov_deg)
+
+
+def backproject_pixels(pose: CameraPose, intr, u, v, depth):
+    """Batched slam.backproject: (n,) rows u, columns v, depths -> (n, 3) fp64."""
+    t = nat.require_cuda()
+    fx, fy, cx, cy = ((intr.fx, intr.fy, intr.cx, intr.cy) if isinstance(intr, CameraIntrinsics)
+                      else tuple(float(x) for x in intr))
+    host = not any(hasattr(a, "data_ptr") for a in (u, v, depth))
+    dev = lambda a: (a if hasattr(a, "data_ptr") else t.from_numpy(np.ascontiguousarray(
+        np.asarray(a, dtype=np.float64).reshape(-1)))).to(device="cuda", dtype=t.float64).contiguous()
+    U, V, Dd = dev(u), dev(v), dev(depth)
+    n = int(U.numel())
+    if V.numel() != n or Dd.numel() != n:
+        raise InvalidInputError("u, v and depth must have the same length")
+    R = t.from_numpy(np.ascontiguousarray(pose.rotation, dtype=np.float64)).to("cuda")
+    tr = t.from_numpy(np.ascontiguousarray(pose.translation, dtype=np.float64)).to("cuda")
+    out = t.empty((n, 3), dtype=t.float64, device="cuda")
+    intr4 = (ctypes.c_double * 4)(fx, fy, cx, cy)   # host array (xgs.h)
+    nat.call("xgs_backproject", nat.ptr(R), nat.ptr(tr), intr4, nat.ptr(U), nat.ptr(V), nat.ptr(Dd), n,
+             nat.ptr(out), nat.stream_ptr())
+    return out.cpu().numpy() if host else out
+
+
+def backproject(pose: CameraPose, intr: CameraIntrinsics, u: float, v: float, depth: float) -> np.ndarray:
+    """slam.py:594-598 — one pixel, bit-identical to the reference."""
+    return backproject_pixels(pose, intr, [u], [v], [depth])[0]
+
+
+def pose_depths(field_: GaussianField, pose: CameraPose) -> np.ndarray:
+    """slam.py:654-655 — camera z of every Gaussian centre."""
+    return pose.transform(field_.mu)[:, 2]
+
+
+def densify_and_prune(field_: GaussianField, window, cfg: SlamConfig, K: Optional[int] = None, *,
+                      occupied=None, voxel_size: Optional[float] = None) -> GaussianField:
+    """slam.py:601-651 — insert splats on the stride lattice of the newest
+    keyframe, prune near-transparent ones, bump the generation.
+
+    Empty map: identical to the reference (every lattice pixel inserted,
+    invalid depth -> default depth).  Non-empty map: lattice pixels whose
+    voxel (``voxel_size``, default the splat footprint
+    max(min_scale, 0.5*stride*median_depth/fx)) is occupied by an existing centre (or by ``occupied``, a
+    :class:`grid.VoxelHashSet`) are skipped instead of the alpha >= 0.5 render test.
+    """
+    t = nat.require_cuda()
+    if len(window) == 0:
+        return field_
+    kf = window.newest
+    intr = frame_intrinsics(kf.frame, cfg)
+    K = field_.K if K is None else K
+    s = cfg.insert_stride
+    if len(field_):
+        cam_depth = pose_depths(field_, kf.pose)
+        median_depth = float(np.median(cam_depth)) if cam_depth.size else cfg.default_depth
+    else:
+        median_depth = cfg.default_depth
+    uu, vv = np.meshgrid(np.arange(0, intr.height, s), np.arange(0, intr.width, s), indexing="ij")
+    uu, vv = uu.reshape(-1), vv.reshape(-1)
+    if kf.frame.depth is not None:
+        dsel = np.asarray(kf.frame.depth)[uu, vv]
+        depth = np.where(dsel > 0, dsel.astype(np.float64), median_depth)
+    else:
+        depth = np.full(uu.size, median_depth)
+    mu = backproject_pixels(kf.pose, intr, uu.astype(np.float64), vv.astype(np.float64), depth)
+    if len(field_):
+        from .grid import VoxelHashSet, pack_key
+        vs = voxel_size if voxel_size is not None else max(cfg.min_scale, 0.5 * s * median_depth / intr.fx)
+        occ = occupied
+        if occ is None:
+            occ = VoxelHashSet(2 * len(field_) + 1024)
+            q = np.floor(field_.mu / vs).astype(np.int64)
+            occ.insert(pack_key(q[:, 0], q[:, 1], q[:, 2]))
+        q = np.floor(mu / vs).astype(np.int64)
+        covered = occ.contains(pack_key(q[:, 0], q[:, 1], q[:, 2])).cpu().numpy()
+        sel = ~covered
+        uu, vv, depth, mu = uu[sel], vv[sel], depth[sel], mu[sel]
+    size = np.maximum(cfg.min_scale, 0.5 * s * depth / intr.fx)
+    color = np.asarray(kf.frame.color)[:, uu, vv].T
+    n_new = uu.size
+    keep = field_.opacity >= cfg.prune_opacity if len(field_) else np.zeros(0, bool)
+    changed = (n_new > 0) or (len(field_) and not keep.all())
+    if not changed:
+        return field_
+
+    def stack(old, extra):
+        return np.concatenate([old[keep], extra]) if len(field_) else np.asarray(extra)
+
+    return GaussianField(
+        mu=stack(field_.mu, mu.reshape(n_new, 3)),
+        quat=stack(field_.quat, np.tile([1.0, 0, 0, 0], (n_new, 1))),
+        scale=stack(field_.scale, np.repeat(size[:, None], 3, axis=1).reshape(n_new, 3)),
+        opacity=stack(field_.opacity, np.full(n_new, cfg.insert_opacity)),
+        color=stack(field_.color, color.reshape(n_new, 3)),
+        logits=stack(field_.logits, np.zeros((n_new, K))),
+        generation=field_.generation + 1,
+    )

@@ -1,0 +1,171 @@
+"""GPU parity of the grid-sampling path: back-projection against the reference's
+golden vectors, densify_and_prune against the reference on an empty map, and
+the voxel sampler (keys, radix sort, first-pick / mean, occupancy, emission
+order) against the CPU oracle (oracle/grid.py).  Keys, pixel ids, positions
+and colours are compared bit-exactly."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import grid as og
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def xs(cuda):
+    from paper_2603_09632_b200 import grid, slam, synth
+    return grid, slam, synth
+
+
+def test_backproject_golden(xs):
+    grid, slam, _ = xs
+    from paper_2603_09632_b200.core import CameraPose
+    g = golden("backproject")
+    for k in range(g["R"].shape[0]):
+        sel = g["pose_id"] == k
+        p = slam.backproject_pixels(CameraPose(g["R"][k], g["t"][k]), g["intr"], g["u"][sel].astype(float),
+                                    g["v"][sel].astype(float), g["d"][sel].astype(float))
+        assert np.array_equal(p, g["p"][sel]), k
+    i = int(np.nonzero(g["pose_id"] == 0)[0][0])
+    one = slam.backproject(CameraPose(g["R"][0], g["t"][0]), g["intr"], float(g["u"][i]), float(g["v"][i]),
+                           float(g["d"][i]))
+    assert np.array_equal(one, g["p"][i])
+
+
+def test_densify_empty_map_golden(xs):
+    _, slam, _ = xs
+    from paper_2603_09632_b200.core import CameraPose, GaussianField
+    g = golden("densify")
+    pose = CameraPose(g["R"], g["t"])
+    win = slam.KeyframeWindow(4)
+    win.insert(slam.CameraFrame(0, pose, g["color"], g["depth"]), pose)
+    empty = GaussianField(mu=np.zeros((0, 3)), quat=np.zeros((0, 4)), scale=np.zeros((0, 3)), opacity=np.zeros(0),
+                          color=np.zeros((0, 3)), logits=np.zeros((0, 5)))
+    out = slam.densify_and_prune(empty, win, slam.SlamConfig(), K=5)
+    for name, ref in (("mu", g["mu"]), ("scale", g["scale"]), ("color", g["col"]), ("opacity", g["opacity"]),
+                      ("quat", g["quat"])):
+        assert np.array_equal(getattr(out, name), ref), name
+    assert out.generation == int(g["generation"])
+
+
+def _scene(synth, seed, H, W, F, spheres=False):
+    rng = np.random.default_rng(seed)
+    intr4 = (0.8 * W, 0.8 * W, (H - 1) / 2, (W - 1) / 2)
+    planes = synth.random_planes(rng, 6, spread=3.0)
+    sph = [(rng.uniform(-1, 1, 3), rng.uniform(0.2, 0.6)) for _ in range(3)] if spheres else ()
+    poses = synth.circle_trajectory(F, radius=2.0, step_deg=5.0)
+    frames = []
+    for p in poses:
+        d, c = synth.rgbd_frame(rng, p, intr4, H, W, planes=planes, spheres=sph, noise=0.003, zero_frac=0.05)
+        frames.append((d, c, p.rotation, p.translation))
+    return frames, intr4
+
+
+@pytest.mark.parametrize("mode", ["first", "mean"])
+@pytest.mark.parametrize("voxel", [0.01, 0.05])
+def test_grid_sample_matches_oracle(xs, mode, voxel):
+    grid, _, synth = xs
+    frames, intr4 = _scene(synth, 3, 96, 128, 3, spheres=True)
+    gs = grid.GridSampler(intr4, voxel, mode=mode)
+    D = np.stack([f[0] for f in frames])
+    C = np.stack([f[1] for f in frames])
+    R = np.stack([f[2] for f in frames])
+    T = np.stack([f[3] for f in frames])
+    got = gs.sample(D, (R, T), C).to_numpy()
+    ref = og.grid_sample(frames, np.array(intr4), voxel, set(), mode=mode)
+    assert got["n_valid"] == ref["n_valid"] and got["n_voxels"] == ref["n_voxels"]
+    for name in ("key", "pid", "mu", "color", "scale", "depth"):
+        assert np.array_equal(got[name], ref[name]), name
+    if mode == "mean":
+        assert np.array_equal(got["count"], ref["count"])
+
+
+def test_grid_incremental_and_batching(xs):
+    grid, _, synth = xs
+    frames, intr4 = _scene(synth, 4, 64, 80, 4)
+    occ = set()
+    refs = [og.grid_sample([f], np.array(intr4), 0.02, occ) for f in frames]
+    # (a) frame by frame against a persistent device map
+    gs = grid.GridSampler(intr4, 0.02)
+    for f, ref in zip(frames, refs):
+        got = gs.sample(f[0], ([f[2]], [f[3]]), f[1]).to_numpy()
+        assert np.array_equal(got["key"], ref["key"]) and np.array_equal(got["mu"], ref["mu"])
+    assert len(gs.occupied) == len(occ)
+    # (b) the whole batch at once == sequential submission
+    gs2 = grid.GridSampler(intr4, 0.02)
+    got = gs2.sample(np.stack([f[0] for f in frames]), (np.stack([f[2] for f in frames]),
+                                                          np.stack([f[3] for f in frames])),
+                     np.stack([f[1] for f in frames])).to_numpy()
+    HW = frames[0][0].size
+    seq_pid = np.concatenate([r["pid"] + i * HW for i, r in enumerate(refs)])
+    assert np.array_equal(got["pid"], seq_pid)
+    assert np.array_equal(got["key"], np.concatenate([r["key"] for r in refs]))
+    # (c) re-submitting the same frames adds nothing
+    again = gs2.sample(frames[0][0], ([frames[0][2]], [frames[0][3]]), frames[0][1])
+    assert len(again) == 0
+
+
+def test_grid_config1_frame_and_stride(xs):
+    grid, _, synth = xs
+    d, c, pose, intr4 = synth.config1_frame(0)
+    for stride in (1, 4):
+        gs = grid.GridSampler(intr4, 0.02, stride=stride)
+        got = gs.sample(d, [pose], c).to_numpy()
+        ref = og.grid_sample([(d, c, pose.rotation, pose.translation)], np.array(intr4), 0.02, set(),
+                             stride=stride)
+        assert np.array_equal(got["pid"], ref["pid"]) and np.array_equal(got["mu"], ref["mu"])
+        assert np.array_equal(got["scale"], ref["scale"])
+
+
+def test_grid_edge_cases(xs):
+    grid, _, _ = xs
+    gs = grid.GridSampler((10.0, 10.0, 1.5, 1.5), 0.1)
+    empty = gs.sample(np.zeros((4, 4), np.float32), (np.eye(3)[None], np.zeros((1, 3))))
+    assert len(empty) == 0 and empty.n_valid == 0
+    # NaN / negative depth are invalid (depth > 0 rule, slam.py:626)
+    d = np.full((4, 4), np.nan, np.float32)
+    d[0, 0] = -1.0
+    d[1, 1] = 2.0
+    r = gs.sample(d, (np.eye(3)[None], np.zeros((1, 3)))).to_numpy()
+    assert r["pid"].tolist() == [5]
+    # first pick across a voxel: all pixels at the same point -> lowest pid
+    gs2 = grid.GridSampler((1e6, 1e6, 0.0, 0.0), 1.0)
+    r = gs2.sample(np.full((3, 5), 1.5, np.float32), (np.eye(3)[None], np.zeros((1, 3)))).to_numpy()
+    assert r["pid"].tolist() == [0] and r["n_voxels"] == 1
+
+
+def test_radix_sort_matches_stable_argsort(xs, cuda):
+    import torch
+    grid, _, _ = xs
+    rng = np.random.default_rng(1)
+    for n, bits, hi in ((1, 64, 10), (5000, 64, 1 << 62), (100003, 20, 1 << 20), (70000, 33, 1000)):
+        k = rng.integers(0, hi, n, dtype=np.int64).astype(np.uint64)
+        if n > 10:
+            k[::7] = k[3]                      # duplicates keep input order
+        v = np.arange(n, dtype=np.uint32)
+        kt = torch.from_numpy(k.view(np.int64)).cuda()
+        vt = torch.from_numpy(v.view(np.int32)).cuda()
+        grid.radix_sort_pairs(kt, vt, bits)
+        order = np.argsort(k, kind="stable")
+        assert np.array_equal(kt.cpu().numpy().view(np.uint64), k[order])
+        assert np.array_equal(vt.cpu().numpy().view(np.uint32), v[order])
+
+
+def test_hashset_semantics(xs):
+    grid, _, _ = xs
+    rng = np.random.default_rng(2)
+    hs = grid.VoxelHashSet(1024)
+    keys = rng.integers(0, 1 << 62, 50000, dtype=np.int64).astype(np.uint64)
+    keys[1000:2000] = keys[:1000]
+    new = hs.insert(keys).cpu().numpy()
+    seen = set(keys.tolist())
+    # parallel insert-if-absent: exactly one occurrence of every distinct key reports "new"
+    uniq, inv = np.unique(keys, return_inverse=True)
+    assert np.array_equal(np.bincount(inv, weights=new), np.ones(uniq.size))
+    assert len(hs) == len(seen)                                   # grew past the initial 1024 slots
+    assert not hs.insert(keys[:500]).cpu().numpy().any()          # second insert: nothing new
+    probe = np.concatenate([keys[:100], rng.integers(0, 1 << 62, 100, dtype=np.int64).astype(np.uint64)])
+    got = hs.contains(probe).cpu().numpy()
+    assert np.array_equal(got, np.array([int(p) in seen for p in probe]))
