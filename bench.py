@@ -113,6 +113,82 @@ def make_data(torch, rank, device):
     return x, E0
 
 
+GRID_F, GRID_H, GRID_W = 16, 720, 1280
+GRID_INTR = (1050.0, 1050.0, 359.5, 639.5)   # BASELINE leaves C3 intrinsics open
+GRID_MAP = 4_000_000
+
+
+def grid_scene(seed=20):
+    """C3: 16 frames 1280x720, random planes + spheres 0.3-8 m, sigma 3 mm,
+    circle of radius 2 m with 5 deg yaw steps, uint8 colour (seeds 20/21)."""
+    from paper_2603_09632_b200 import synth
+    rng = np.random.default_rng(seed)
+    planes = synth.random_planes(rng, 6, spread=3.0)
+    spheres = [(rng.uniform(-1.0, 1.0, 3), rng.uniform(0.2, 0.6)) for _ in range(4)]
+    poses = synth.circle_trajectory(GRID_F, radius=2.0, step_deg=5.0)
+    crng = np.random.default_rng(seed + 1)
+    D = np.empty((GRID_F, GRID_H, GRID_W), np.float32)
+    C = np.empty((GRID_F, GRID_H, GRID_W, 3), np.uint8)
+    for i, p in enumerate(poses):
+        D[i], C[i] = synth.rgbd_frame(crng, p, GRID_INTR, GRID_H, GRID_W, planes=planes, spheres=spheres,
+                                      dmin=0.3, dmax=8.0, noise=0.003, zero_frac=0.0)
+    R = np.stack([p.rotation for p in poses])
+    T = np.stack([p.translation for p in poses])
+    return D, C, R, T
+
+
+def run_grid(torch, steps, cpu=True):
+    """C3 grid sampling: Mpts/s = 16*1280*720 input pixels / batch time, map
+    reset to the ~4M-voxel warm-up state before every timed batch."""
+    from paper_2603_09632_b200 import _native as nat
+    from paper_2603_09632_b200.grid import GridSampler, VoxelHashSet, pack_key
+    D, C, R, T = grid_scene()
+    Dd, Cd = torch.from_numpy(D).cuda(), torch.from_numpy(C).cuda()
+    Rd, Td = torch.from_numpy(R).cuda(), torch.from_numpy(T).cuda()
+    rng = np.random.default_rng(22)
+    out = {}
+    for voxel in (0.01, 0.05):
+        # warm-up map: 4M voxels of random points in the scene volume (seeded)
+        pts = rng.uniform(-4.0, 4.0, (GRID_MAP, 3))
+        q = np.floor(pts / voxel).astype(np.int64)
+        warm = torch.from_numpy(pack_key(q[:, 0], q[:, 1], q[:, 2]).view(np.int64)).cuda()
+        times, n_new, n_valid, map_size = [], 0, 0, 0
+        for it in range(steps + 1):
+            hs = VoxelHashSet(GRID_MAP + GRID_F * GRID_H * GRID_W)
+            hs.insert(warm)
+            map_size = len(hs)
+            gs = GridSampler(GRID_INTR, voxel, occupied=hs)
+            torch.cuda.synchronize()
+            if it == steps:
+                nat.profile_enable(True)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = gs.sample(Dd, (Rd, Td), Cd)
+            e1.record()
+            torch.cuda.synchronize()
+            if it > 0:
+                times.append(e0.elapsed_time(e1))
+            n_new, n_valid = len(r), r.n_valid
+            hs.close()
+        prof = {t: nat.profile_read(t)[0] for t in ("grid_keys", "grid_sort", "grid_select", "grid_emit")}
+        nat.profile_enable(False)
+        ms = float(np.median(times))
+        npix = GRID_F * GRID_H * GRID_W
+        out[str(voxel)] = {"Mpts_per_s": npix / (ms * 1e-3) / 1e6, "ms_per_batch": ms, "pixels": npix,
+                           "valid_points": n_valid, "new_voxels": n_new, "map_voxels_before": map_size,
+                           "per_kernel_ms": prof}
+    if cpu:
+        from oracle import grid as og
+        t0 = time.perf_counter()
+        nf = 2
+        og.grid_sample([(D[i], C[i], R[i], T[i]) for i in range(nf)], np.array(GRID_INTR), 0.01, set())
+        el = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": nf * GRID_H * GRID_W / el / 1e6, "unit": "Mpts/s", "cores": 1,
+                               "kind": "port", "sample": f"{nf} C3 frames, voxel 0.01, oracle/grid.py "
+                                                         "(C back-projection + NumPy sort/unique/isin)"}
+    return out
+
+
 def cpu_port_rate(x_host, E, seconds=10.0, threads=None):
     """The reference's assign+accumulate restated in C (oracle/oracle.c), timed
     on host cores over row chunks until ~`seconds` elapse (bounded sample)."""
@@ -178,6 +254,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-grid", action="store_true")
+    ap.add_argument("--grid-steps", type=int, default=5)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -280,6 +358,9 @@ def main():
         cpu = {"value": v, "unit": "Mfeat/s", "cores": thr, "kind": "port",
                "sample": f"{rows} rows of the C2 batch in {el:.1f}s (assign+accumulate, oracle/oracle.c, "
                          f"{thr} threads)"}
+    grid = None
+    if rank == 0 and world == 1 and not args.no_grid:
+        grid = run_grid(torch, args.grid_steps, cpu=not args.no_cpu)
     if rank == 0:
         per_kernel = {t: {"ms_per_step": m / args.steps, "launches": c} for t, (m, c) in prof.items()}
         line = {
@@ -301,6 +382,7 @@ def main():
             "assign_exact_rows": {"rerank": n_rerank, "fallback": n_fallback},
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "grid": grid,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
