@@ -38,7 +38,7 @@ constexpr int EPI_WARPS = 8;                  // 2 per TMEM lane quadrant (colum
 constexpr int EPI_THREADS = EPI_WARPS * 32;
 constexpr int THREADS = 64 + EPI_THREADS;     // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2..9 epilogue
 constexpr int HALF = BN / 2;                  // columns per epilogue warp per chunk
-constexpr int CONST_BYTES = 2 * 3 * BN * 4;
+constexpr int CONST_BYTES = 2 * BN * 4;
 struct HalfState {                            // column-half 1 -> half 0 hand-off at tile end
   float U;
   float dropped;
@@ -55,12 +55,9 @@ constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)
 struct ScreenParams {
   int64_t n;
   int num_m_tiles, num_n_chunks, num_k_blocks;
-  const float* xn;
+  const float* xband;   // per row: 2 * max_k B_k + fp64-reference slack
   const float* xf;
   const float* cn;
-  const float* ce1;
-  const float* ce2;
-  float c3;
   int64_t* codes;
   RerankEntry* rq;
   int32_t* rq_count;
@@ -161,12 +158,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory"); }
 
 // Per-row candidate state of one epilogue thread (one row, one column half):
-// the kCandCap smallest lower bounds lo_k = s_k - B_k seen so far, kept sorted
-// in registers (static indices only), plus the smallest lo ever pushed out.
-// At the end the candidates are {k : lo_k <= U + slack}; if a pushed-out lo
-// also satisfies that, the list overflowed and the row is rescanned exactly.
+// the kCandCap smallest screen values s_k seen so far, kept sorted in
+// registers (static indices only), plus the smallest s ever pushed out.  At
+// the end the candidates are {k : s_k <= U + band}; if a pushed-out value also
+// satisfies that, the list overflowed and the row is rescanned exactly.
 struct Cands {
-  float U;        // min_k (s_k + B_k) seen so far
+  float U;        // min_k s_k seen so far
   float dropped;  // min lo among entries evicted from the full list
   float L[kCandCap];
   int Kx[kCandCap];
@@ -195,48 +192,36 @@ struct Cands {
   }
 };
 
-// Screen 32 accumulator columns of one row: block min of s+B first (no serial
-// dependence on U per element), then a single lo-vs-threshold test; only
-// blocks that can hold a candidate take the insertion path.
-__device__ __forceinline__ void screen_block(const uint32_t (&r)[32], const float* __restrict__ cn,
-                                            const float* __restrict__ ce1, const float* __restrict__ ce2,
-                                            float xf, float xn, float slack, int kbase, Cands& st) {
-  float lo[32];
-  float h0 = __int_as_float(0x7f800000), h1 = h0, h2 = h0, h3 = h0;
-  float l0 = h0, l1 = h0, l2 = h0, l3 = h0;
+// Screen 32 accumulator columns of one row.  With the per-row uniform bound
+// (B_row >= B_k for every k) the candidate test is s_k <= min_j s_j + band,
+// band = 2 * B_row: the fast path is one FFMA + one FMNMX per element; only
+// blocks holding an element inside the band take the insertion path.
+__device__ __forceinline__ void screen_block(const uint32_t (&r)[32], const float* __restrict__ cn, float xf,
+                                            float band, int kbase, Cands& st) {
+  float sv[32];
+  float m0 = __int_as_float(0x7f800000), m1 = m0, m2 = m0, m3 = m0;
 #pragma unroll
   for (int i = 0; i < 32; i += 4) {
     const float4 a = *reinterpret_cast<const float4*>(cn + i);
-    const float4 b1 = *reinterpret_cast<const float4*>(ce1 + i);
-    const float4 b2 = *reinterpret_cast<const float4*>(ce2 + i);
-    const float s0 = fmaf(xf, __uint_as_float(r[i + 0]), a.x), bb0 = fmaf(xn, b1.x, b2.x);
-    const float s1 = fmaf(xf, __uint_as_float(r[i + 1]), a.y), bb1 = fmaf(xn, b1.y, b2.y);
-    const float s2 = fmaf(xf, __uint_as_float(r[i + 2]), a.z), bb2 = fmaf(xn, b1.z, b2.z);
-    const float s3 = fmaf(xf, __uint_as_float(r[i + 3]), a.w), bb3 = fmaf(xn, b1.w, b2.w);
-    lo[i + 0] = s0 - bb0;
-    lo[i + 1] = s1 - bb1;
-    lo[i + 2] = s2 - bb2;
-    lo[i + 3] = s3 - bb3;
-    h0 = fminf(h0, s0 + bb0);
-    h1 = fminf(h1, s1 + bb1);
-    h2 = fminf(h2, s2 + bb2);
-    h3 = fminf(h3, s3 + bb3);
-    l0 = fminf(l0, lo[i + 0]);
-    l1 = fminf(l1, lo[i + 1]);
-    l2 = fminf(l2, lo[i + 2]);
-    l3 = fminf(l3, lo[i + 3]);
+    sv[i + 0] = fmaf(xf, __uint_as_float(r[i + 0]), a.x);
+    sv[i + 1] = fmaf(xf, __uint_as_float(r[i + 1]), a.y);
+    sv[i + 2] = fmaf(xf, __uint_as_float(r[i + 2]), a.z);
+    sv[i + 3] = fmaf(xf, __uint_as_float(r[i + 3]), a.w);
+    m0 = fminf(m0, sv[i + 0]);
+    m1 = fminf(m1, sv[i + 1]);
+    m2 = fminf(m2, sv[i + 2]);
+    m3 = fminf(m3, sv[i + 3]);
   }
-  st.U = fminf(st.U, fminf(fminf(h0, h1), fminf(h2, h3)));
-  const float thr = st.U + slack;
-  if (fminf(fminf(l0, l1), fminf(l2, l3)) <= thr) {
-    // rare per lane, frequent per warp (32 rows): stash the block with 8
-    // vector stores, then insert only the qualifying columns
+  const float bmin = fminf(fminf(m0, m1), fminf(m2, m3));
+  st.U = fminf(st.U, bmin);
+  const float thr = st.U + band;
+  if (bmin <= thr) {
     unsigned m = 0;
     float4 lv[8];
 #pragma unroll
-    for (int i = 0; i < 32; i++) m |= (lo[i] <= thr ? 1u : 0u) << i;
+    for (int i = 0; i < 32; i++) m |= (sv[i] <= thr ? 1u : 0u) << i;
 #pragma unroll
-    for (int i = 0; i < 8; i++) lv[i] = make_float4(lo[4 * i], lo[4 * i + 1], lo[4 * i + 2], lo[4 * i + 3]);
+    for (int i = 0; i < 8; i++) lv[i] = make_float4(sv[4 * i], sv[4 * i + 1], sv[4 * i + 2], sv[4 * i + 3]);
     const float* lf = reinterpret_cast<const float*>(lv);
     while (m) {
       const int i = __ffs(m) - 1;
@@ -340,19 +325,13 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     for (int tile = blockIdx.x; tile < p.num_m_tiles; tile += gridDim.x) {
       const int64_t row = (int64_t)tile * BM + rl;
       const bool live = row < p.n;
-      const float xn = live ? p.xn[row] : 0.f;
+      const float band = live ? p.xband[row] : 0.f;
       const float xf = live ? p.xf[row] : 0.f;   // -2 / (row scale * codebook scale)
-      const float slack = 2.f * p.c3 * xn * xn;  // fp64-reference rounding margin
       Cands st;
       st.init();
       for (int nc = 0; nc < p.num_n_chunks; nc++) {
-        float* cc = cconst + acc * 3 * BN;
-        for (int i = et; i < BN; i += EPI_THREADS) {
-          const int kk = nc * BN + i;
-          cc[i] = p.cn[kk];
-          cc[BN + i] = p.ce1[kk];
-          cc[2 * BN + i] = p.ce2[kk];
-        }
+        float* cc = cconst + acc * BN;
+        for (int i = et; i < BN; i += EPI_THREADS) cc[i] = p.cn[nc * BN + i];
         epi_bar();
         mbar_wait(&tfull[acc], aphase);
         tc_after();
@@ -364,12 +343,10 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 #pragma unroll 1
         for (int c0 = 0; c0 < HALF; c0 += 64) {
           tmem_ld32_async(taddr + c0 + 32, rb);
-          screen_block(ra, cc + cbase + c0, cc + BN + cbase + c0, cc + 2 * BN + cbase + c0, xf, xn, slack,
-                       nc * BN + cbase + c0, st);
+          screen_block(ra, cc + cbase + c0, xf, band, nc * BN + cbase + c0, st);
           tmem_wait(rb);
           if (c0 + 64 < HALF) tmem_ld32_async(taddr + c0 + 64, ra);
-          screen_block(rb, cc + cbase + c0 + 32, cc + BN + cbase + c0 + 32, cc + 2 * BN + cbase + c0 + 32, xf,
-                       xn, slack, nc * BN + cbase + c0 + 32, st);
+          screen_block(rb, cc + cbase + c0 + 32, xf, band, nc * BN + cbase + c0 + 32, st);
           if (c0 + 64 < HALF) tmem_wait(ra);
         }
         tc_before();
@@ -392,7 +369,7 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       epi_bar();
       if (half == 0) {
         const HalfState& hs = merge[rl];
-        const float thr = fminf(st.U, hs.U) + slack;
+        const float thr = fminf(st.U, hs.U) + band;
         bool ovf = st.dropped <= thr || hs.dropped <= thr;
         int nk = 0, kbest = -1;
         int fin[kCandCap];
@@ -467,7 +444,7 @@ __device__ __forceinline__ int exp_of(float m) {
 // per-code bound constants.  Padded codes get s = +inf (never candidates).
 __global__ void prep_codebook_kernel(const double* __restrict__ E, int64_t k, int64_t d, int64_t kp, int64_t dp,
                                      float c1, float c2, float c4, const unsigned* __restrict__ emax_bits,
-                                     __half* __restrict__ Eb, float* cn, float* ce1, float* ce2) {
+                                     __half* __restrict__ Eb, float* cn, unsigned* cmax_bits) {
   const int64_t code = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (code >= kp) return;
@@ -484,12 +461,10 @@ __global__ void prep_codebook_kernel(const double* __restrict__ E, int64_t k, in
     if (code < k) {
       const float en = (float)sqrt(ss) * (1.f + 1e-6f);
       cn[code] = (float)ss;
-      ce1[code] = c1 * en + c4 * emax;
-      ce2[code] = c2 * en * en;
+      atomicMax(cmax_bits, __float_as_uint(c1 * en + c4 * emax));
+      atomicMax(cmax_bits + 1, __float_as_uint(c2 * en * en));
     } else {
       cn[code] = __int_as_float(0x7f800000);
-      ce1[code] = 0.f;
-      ce2[code] = 0.f;
     }
   }
 }
@@ -506,8 +481,9 @@ struct RowMath<double> { using T = double; };
 template <typename X>
 __global__ void __launch_bounds__(256)
 prep_rows_kernel(const X* __restrict__ x, int64_t n, int64_t d, int64_t ldx, int64_t dp,
-                 const unsigned* __restrict__ emax_bits, __half* __restrict__ Ab, float* __restrict__ xn,
-                 float* __restrict__ xf, float inflate) {
+                 const unsigned* __restrict__ emax_bits, const unsigned* __restrict__ cmax_bits,
+                 float c3, __half* __restrict__ Ab, float* __restrict__ xband, float* __restrict__ xf,
+                 float inflate) {
   using T = typename RowMath<X>::T;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -551,14 +527,17 @@ prep_rows_kernel(const X* __restrict__ x, int64_t n, int64_t d, int64_t ldx, int
     for (int64_t j = lane; j < dp; j += 32) ar[j] = __double2half(j < d ? (double)((T)ld64(xr, j) * sc) : 0.0);
   }
   if (lane == 0) {
-    xn[row] = (float)sqrt((double)ss) * inflate;
+    const float xn = (float)sqrt((double)ss) * inflate;
+    // band = 2 * max_k B_k (+ fp64-reference slack), rounded up by 2^-20
+    const float c1m = __uint_as_float(cmax_bits[0]), c2m = __uint_as_float(cmax_bits[1]);
+    xband[row] = (2.f * fmaf(xn, c1m, c2m) + 2.f * c3 * xn * xn) * (1.f + 1e-6f);
     const int ee = exp_of(__uint_as_float(*emax_bits));
     xf[row] = -ldexpf(1.f, (ex - 15) + (ee - 15) + 1);
   }
 }
 
 struct ScreenWs {
-  size_t off_ab, off_xn, off_xf, off_eb, off_cn, off_ce1, off_ce2, off_rq, off_fq, off_cnt, total;
+  size_t off_ab, off_xn, off_xf, off_eb, off_cn, off_rq, off_fq, off_cnt, total;
   int64_t kp, dp;
 };
 
@@ -574,8 +553,6 @@ ScreenWs screen_ws(int64_t n, int64_t k, int64_t d) {
   w.off_xf = take(nn * 4);
   w.off_eb = take((size_t)w.kp * (size_t)w.dp * 2);
   w.off_cn = take((size_t)w.kp * 4);
-  w.off_ce1 = take((size_t)w.kp * 4);
-  w.off_ce2 = take((size_t)w.kp * 4);
   w.off_rq = take(nn * sizeof(RerankEntry));
   w.off_fq = take(nn * 4);
   w.off_cnt = take(64);
@@ -625,8 +602,6 @@ cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* h
   float* xf = reinterpret_cast<float*>(base + w.off_xf);
   __half* Eb = reinterpret_cast<__half*>(base + w.off_eb);
   float* cn = reinterpret_cast<float*>(base + w.off_cn);
-  float* ce1 = reinterpret_cast<float*>(base + w.off_ce1);
-  float* ce2 = reinterpret_cast<float*>(base + w.off_ce2);
   RerankEntry* rq = reinterpret_cast<RerankEntry*>(base + w.off_rq);
   int32_t* fq = reinterpret_cast<int32_t*>(base + w.off_fq);
   int32_t* cnt = reinterpret_cast<int32_t*>(base + w.off_cnt);
@@ -638,13 +613,13 @@ cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* h
   ProfScope prof("vq_prep", s);
   absmax_kernel<<<148, 256, 0, s>>>(a.E, a.k * a.d, emax); count_launches(1);
   prep_codebook_kernel<<<(unsigned)((w.kp + 7) / 8), 256, 0, s>>>(a.E, a.k, a.d, w.kp, w.dp, a.c1, a.c2, a.c4,
-                                                                  emax, Eb, cn, ce1, ce2); count_launches(1);
+                                                                  emax, Eb, cn, emax + 1); count_launches(1);
   const float inflate = 1.f + (float)(a.d + 8) * 1.2e-7f;
   const unsigned rblocks = (unsigned)((a.n + 7) / 8);
   switch (a.dtype) {
-    case F32: prep_rows_kernel<float><<<rblocks, 256, 0, s>>>((const float*)a.x, a.n, a.d, a.ldx, w.dp, emax, Ab, xn, xf, inflate); count_launches(1); break;
-    case F64: prep_rows_kernel<double><<<rblocks, 256, 0, s>>>((const double*)a.x, a.n, a.d, a.ldx, w.dp, emax, Ab, xn, xf, inflate); count_launches(1); break;
-    default: prep_rows_kernel<uint16_t><<<rblocks, 256, 0, s>>>((const uint16_t*)a.x, a.n, a.d, a.ldx, w.dp, emax, Ab, xn, xf, inflate); count_launches(1);
+    case F32: prep_rows_kernel<float><<<rblocks, 256, 0, s>>>((const float*)a.x, a.n, a.d, a.ldx, w.dp, emax, emax + 1, 1.0e-12f, Ab, xn, xf, inflate); count_launches(1); break;
+    case F64: prep_rows_kernel<double><<<rblocks, 256, 0, s>>>((const double*)a.x, a.n, a.d, a.ldx, w.dp, emax, emax + 1, 1.0e-12f, Ab, xn, xf, inflate); count_launches(1); break;
+    default: prep_rows_kernel<uint16_t><<<rblocks, 256, 0, s>>>((const uint16_t*)a.x, a.n, a.d, a.ldx, w.dp, emax, emax + 1, 1.0e-12f, Ab, xn, xf, inflate); count_launches(1);
   }
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -659,12 +634,9 @@ cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* h
   p.num_m_tiles = (int)((a.n + BM - 1) / BM);
   p.num_n_chunks = (int)(w.kp / BN);
   p.num_k_blocks = (int)(w.dp / BK);
-  p.xn = xn;
+  p.xband = xn;
   p.xf = xf;
   p.cn = cn;
-  p.ce1 = ce1;
-  p.ce2 = ce2;
-  p.c3 = 1.0e-12f;
   p.codes = a.codes;
   p.rq = rq;
   p.rq_count = cnt;

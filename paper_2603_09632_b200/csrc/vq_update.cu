@@ -18,7 +18,7 @@ constexpr int kTileTarget = 2048;  // number of row tiles (bounds the T x K tabl
 
 struct AccPlan {
   int64_t tile_rows, tiles;
-  size_t off_tile_counts, off_code_count, off_code_start, off_sorted, total;
+  size_t off_tile_counts, off_code_count, off_code_start, off_sorted, off_order, total;
 };
 
 AccPlan acc_plan(int64_t n, int64_t k) {
@@ -34,6 +34,7 @@ AccPlan acc_plan(int64_t n, int64_t k) {
   p.off_code_count = take(sizeof(int32_t) * (size_t)k);
   p.off_code_start = take(sizeof(int32_t) * (size_t)(k + 1));
   p.off_sorted = take(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+  p.off_order = take(sizeof(int32_t) * (size_t)k);
   p.total = o;
   return p;
 }
@@ -118,6 +119,20 @@ acc_scan_codes_kernel(const int32_t* __restrict__ code_count, int64_t k, int32_t
   }
 }
 
+// (2c) codes by descending row count (ties by index): the serial chains of the
+// biggest codes start first, so the largest code overlaps the rest of the work.
+__global__ void acc_order_kernel(const int32_t* __restrict__ code_count, int64_t k, int32_t* order) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= k) return;
+  const int32_t mine = code_count[c];
+  int32_t rank = 0;
+  for (int64_t j = 0; j < k; j++) {
+    const int32_t o = __ldg(code_count + j);
+    rank += (o > mine) || (o == mine && j < c);
+  }
+  order[rank] = (int32_t)c;
+}
+
 // (3) stable scatter of row ids into code-sorted order; one warp per tile.
 __global__ void acc_scatter_kernel(const int64_t* __restrict__ codes, const uint8_t* __restrict__ mask,
                                    int64_t n, int64_t k, int64_t tile_rows, int32_t* tile_off,
@@ -196,12 +211,12 @@ template <typename X, int VEC, int U>
 __global__ void __launch_bounds__(256, 2)
 acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
                  const int32_t* __restrict__ code_start, const int32_t* __restrict__ sorted,
-                 double* __restrict__ counts, double* __restrict__ sums) {
+                 const int32_t* __restrict__ order, double* __restrict__ counts, double* __restrict__ sums) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int64_t nchunks = (d + 32 * VEC - 1) / (32 * VEC);
-  const int64_t code = gw / nchunks;
-  if (code >= k) return;
+  if (gw / nchunks >= k) return;
+  const int64_t code = order[gw / nchunks];
   const int64_t d0 = (gw % nchunks) * 32 * VEC + (int64_t)lane * VEC;
   const bool live = d0 < d;
   const int32_t beg = code_start[code], end = code_start[code + 1];
@@ -243,12 +258,13 @@ acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
 
 template <typename X, int VEC>
 cudaError_t launch_chain(const X* x, int64_t d, int64_t ldx, int64_t k, const int32_t* cs,
-                         const int32_t* sorted, double* counts, double* sums, cudaStream_t s) {
+                         const int32_t* sorted, const int32_t* order, double* counts, double* sums,
+                         cudaStream_t s) {
   const int64_t nchunks = (d + 32 * VEC - 1) / (32 * VEC);
   const int64_t warps = k * nchunks;
   constexpr int U = VEC >= 4 ? 16 : 32;
   ProfScope prof("vq_chain", s);
-  acc_chain_kernel<X, VEC, U><<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(x, d, ldx, k, cs, sorted, counts, sums); count_launches(1);
+  acc_chain_kernel<X, VEC, U><<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(x, d, ldx, k, cs, sorted, order, counts, sums); count_launches(1);
   return cudaGetLastError();
 }
 
@@ -316,6 +332,7 @@ cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, in
   int32_t* code_count = reinterpret_cast<int32_t*>(w + p.off_code_count);
   int32_t* code_start = reinterpret_cast<int32_t*>(w + p.off_code_start);
   int32_t* sorted = reinterpret_cast<int32_t*>(w + p.off_sorted);
+  int32_t* order = reinterpret_cast<int32_t*>(w + p.off_order);
   ProfScope prof("vq_accumulate", s);
   cudaError_t e = cudaMemsetAsync(tile_counts, 0, sizeof(int32_t) * (size_t)p.tiles * (size_t)k, s);
   if (e != cudaSuccess) return e;
@@ -324,6 +341,7 @@ cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, in
   }
   acc_scan_tiles_kernel<<<(unsigned)((k + 31) / 32), 1024, 0, s>>>(tile_counts, p.tiles, k, code_count); count_launches(1);
   acc_scan_codes_kernel<<<1, 1024, 0, s>>>(code_count, k, code_start); count_launches(1);
+  acc_order_kernel<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(code_count, k, order); count_launches(1);
   if (n > 0) {
     acc_scatter_kernel<<<(unsigned)p.tiles, 32, 0, s>>>(codes, mask, n, k, p.tile_rows, tile_counts,
                                                         code_start, sorted); count_launches(1);
@@ -333,16 +351,16 @@ cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, in
   switch (dtype) {
     case F32:
       if (d % 2 == 0 && ldx % 2 == 0 && xa % 8 == 0)
-        return launch_chain<float, 2>((const float*)x, d, ldx, k, code_start, sorted, counts, sums, s);
-      return launch_chain<float, 1>((const float*)x, d, ldx, k, code_start, sorted, counts, sums, s);
+        return launch_chain<float, 2>((const float*)x, d, ldx, k, code_start, sorted, order, counts, sums, s);
+      return launch_chain<float, 1>((const float*)x, d, ldx, k, code_start, sorted, order, counts, sums, s);
     case F64:
       if (d % 2 == 0 && ldx % 2 == 0 && xa % 16 == 0)
-        return launch_chain<double, 2>((const double*)x, d, ldx, k, code_start, sorted, counts, sums, s);
-      return launch_chain<double, 1>((const double*)x, d, ldx, k, code_start, sorted, counts, sums, s);
+        return launch_chain<double, 2>((const double*)x, d, ldx, k, code_start, sorted, order, counts, sums, s);
+      return launch_chain<double, 1>((const double*)x, d, ldx, k, code_start, sorted, order, counts, sums, s);
     default:
       if (d % 8 == 0 && ldx % 8 == 0 && xa % 16 == 0)
-        return launch_chain<uint16_t, 8>((const uint16_t*)x, d, ldx, k, code_start, sorted, counts, sums, s);
-      return launch_chain<uint16_t, 1>((const uint16_t*)x, d, ldx, k, code_start, sorted, counts, sums, s);
+        return launch_chain<uint16_t, 8>((const uint16_t*)x, d, ldx, k, code_start, sorted, order, counts, sums, s);
+      return launch_chain<uint16_t, 1>((const uint16_t*)x, d, ldx, k, code_start, sorted, order, counts, sums, s);
   }
 }
 
