@@ -81,6 +81,8 @@ __device__ __forceinline__ bool voxel_of(const double* p, double voxel, int64_t*
 }
 
 // ---------------------------------------------------------------- G1
+// One thread per 4 consecutive pixels of a row (float4 depth load when W % 4
+// == 0); 32-bit index math (npix < 2^31 is checked by the C ABI).
 __global__ void __launch_bounds__(256)
 grid_keys_kernel(const float* __restrict__ depth, int64_t npix, int64_t H, int64_t W, int stride,
                  const double* __restrict__ rot, const double* __restrict__ trans, Cam cam,
@@ -88,34 +90,35 @@ grid_keys_kernel(const float* __restrict__ depth, int64_t npix, int64_t H, int64
                  bool vec4) {
   int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
   unsigned cnt = 0;
-  const int64_t HW = H * W;
-  const int64_t nq = vec4 ? npix / 4 : npix;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+  const uint32_t HW = (uint32_t)(H * W), Wu = (uint32_t)W, su = (uint32_t)stride;
+  const uint32_t nq = (uint32_t)(vec4 ? npix / 4 : npix);
+  const int per = vec4 ? 4 : 1;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
     float dv[4];
-    int nv;
-    int64_t p0;
+    uint32_t p0;
     if (vec4) {
       const float4 d4 = __ldg(reinterpret_cast<const float4*>(depth) + q);
       dv[0] = d4.x; dv[1] = d4.y; dv[2] = d4.z; dv[3] = d4.w;
-      nv = 4;
       p0 = q * 4;
     } else {
       dv[0] = __ldg(depth + q);
-      nv = 1;
       p0 = q;
     }
+    const uint32_t f = p0 / HW, rem = p0 - f * HW;
+    const uint32_t u = rem / Wu, v0 = rem - u * Wu;
+    const bool row_on = (u % su) == 0;
+    const double* R = rot + (size_t)f * 9;
+    const double* T = trans + (size_t)f * 3;
     uint64_t kout[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      if (j >= nv) break;
-      const int64_t pid = p0 + j;
-      const int64_t f = pid / HW, rem = pid - f * HW;
-      const int64_t u = rem / W, v = rem - u * W;
+      if (j >= per) break;
+      const uint32_t v = v0 + j;
       uint64_t key = KEY_INVALID;
       const float d32 = dv[j];
-      if ((u % stride) == 0 && (v % stride) == 0 && d32 > 0.f) {
+      if (row_on && (v % su) == 0 && d32 > 0.f) {
         double p[3];
-        backproject(rot + f * 9, trans + f * 3, cam, (double)u, (double)v, (double)d32, p);
+        backproject(R, T, cam, (double)u, (double)v, (double)d32, p);
         int64_t qv[3];
         if (voxel_of(p, cam.voxel, qv)) {
           key = ((uint64_t)qv[0] << 42) | ((uint64_t)qv[1] << 21) | (uint64_t)qv[2];
@@ -130,12 +133,12 @@ grid_keys_kernel(const float* __restrict__ depth, int64_t npix, int64_t H, int64
       kout[j] = key;
     }
     if (vec4) {
-      reinterpret_cast<ulonglong2*>(keys)[q * 2] = make_ulonglong2(kout[0], kout[1]);
-      reinterpret_cast<ulonglong2*>(keys)[q * 2 + 1] = make_ulonglong2(kout[2], kout[3]);
-      reinterpret_cast<uint4*>(vals)[q] = make_uint4((uint32_t)p0, (uint32_t)p0 + 1, (uint32_t)p0 + 2, (uint32_t)p0 + 3);
+      reinterpret_cast<ulonglong2*>(keys)[(size_t)q * 2] = make_ulonglong2(kout[0], kout[1]);
+      reinterpret_cast<ulonglong2*>(keys)[(size_t)q * 2 + 1] = make_ulonglong2(kout[2], kout[3]);
+      reinterpret_cast<uint4*>(vals)[q] = make_uint4(p0, p0 + 1, p0 + 2, p0 + 3);
     } else {
       keys[p0] = kout[0];
-      vals[p0] = (uint32_t)p0;
+      vals[p0] = p0;
     }
   }
 #pragma unroll
@@ -184,6 +187,10 @@ constexpr int SORT_THREADS = 256;
 constexpr int SORT_ITEMS = 16;                       // per thread
 constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS; // 4096
 constexpr int RADIX = 256;
+constexpr int STAGE_BYTES_SORT = SORT_TILE * 12;
+
+bool sort_attr_set = false;
+cudaError_t sort_init();
 
 __global__ void __launch_bounds__(SORT_THREADS)
 sort_upsweep_kernel(const uint64_t* __restrict__ keys, int64_t n, RelKey rk, int shift, int32_t* tile_hist,
@@ -208,16 +215,26 @@ sort_upsweep_kernel(const uint64_t* __restrict__ keys, int64_t n, RelKey rk, int
   }
 }
 
+// Stable downsweep: warp w owns tile items [w*512, w*512+512) in input order;
+// ranks come from match_any per 32-item round + per-warp digit counters.  The
+// tile is then re-ordered by digit in shared memory so the global writes are
+// contiguous runs per digit (coalesced) instead of 32 scattered addresses.
 __global__ void __launch_bounds__(SORT_THREADS)
 sort_downsweep_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t n, RelKey rk,
                       int shift, const int32_t* __restrict__ scanned, int64_t tiles, uint64_t* __restrict__ kout,
                       uint32_t* __restrict__ vout) {
   __shared__ int32_t wc[8][RADIX];
+  __shared__ int32_t toff[RADIX];
+  __shared__ int32_t gbase[RADIX];
+  extern __shared__ __align__(16) uint8_t stage_smem[];   // SORT_TILE keys + values (dynamic)
+  uint64_t* sk = reinterpret_cast<uint64_t*>(stage_smem);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(stage_smem + SORT_TILE * 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   for (int i = threadIdx.x; i < 8 * RADIX; i += SORT_THREADS) (&wc[0][0])[i] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * SORT_TILE + (int64_t)warp * (SORT_TILE / 8);
+  const int64_t tile0 = (int64_t)blockIdx.x * SORT_TILE;
+  const int64_t base = tile0 + (int64_t)warp * (SORT_TILE / 8);
   uint64_t k[SORT_ITEMS];
   uint32_t v[SORT_ITEMS];
   int16_t rank[SORT_ITEMS];
@@ -230,34 +247,74 @@ sort_downsweep_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restri
     v[r] = ok ? vin[i] : 0;
     const int d = ok ? (int)((rk(k[r]) >> shift) & (RADIX - 1)) : -1;
     const unsigned peers = __match_any_sync(FULL, d);
-    int rr = 0;
+    int rr = -1;
     if (d >= 0) rr = wc[warp][d] + __popc(peers & lt);
     __syncwarp();
     if (d >= 0 && lane == __ffs(peers) - 1) wc[warp][d] += __popc(peers);
     __syncwarp();
     rank[r] = (int16_t)rr;
     dg[r] = (uint8_t)(d < 0 ? 0 : d);
-    if (d < 0) rank[r] = -1;
   }
   __syncthreads();
-  // exclusive prefix over warps per digit (warp order == input order)
-  for (int d = threadIdx.x; d < RADIX; d += SORT_THREADS) {
-    int32_t run = scanned[(int64_t)d * tiles + blockIdx.x];
+  // per digit: exclusive prefix over warps (input order), tile total, global base
+  {
+    const int d = threadIdx.x;   // SORT_THREADS == RADIX
+    int32_t run = 0;
     for (int w = 0; w < 8; w++) {
       const int32_t c = wc[w][d];
       wc[w][d] = run;
       run += c;
+    }
+    toff[d] = run;   // tile count of digit d (scanned below)
+    gbase[d] = scanned[(int64_t)d * tiles + blockIdx.x];
+  }
+  __syncthreads();
+  // exclusive scan of the 256 tile counts -> tile-local digit offsets
+  if (warp == 0) {
+    int32_t c[8], s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      c[j] = toff[lane * 8 + j];
+      s += c[j];
+    }
+    int32_t x = s;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    int32_t run = x - s;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      toff[lane * 8 + j] = run;
+      run += c[j];
     }
   }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < SORT_ITEMS; r++) {
     if (rank[r] >= 0) {
-      const int32_t pos = wc[warp][dg[r]] + rank[r];
-      kout[pos] = k[r];
-      vout[pos] = v[r];
+      const int pos = toff[dg[r]] + wc[warp][dg[r]] + rank[r];
+      sk[pos] = k[r];
+      sv[pos] = v[r];
     }
   }
+  __syncthreads();
+  const int cnt = (int)min((int64_t)SORT_TILE, n - tile0);
+  for (int i = threadIdx.x; i < cnt; i += SORT_THREADS) {
+    const uint64_t key = sk[i];
+    const int d = (int)((rk(key) >> shift) & (RADIX - 1));
+    const int64_t pos = (int64_t)gbase[d] + (i - toff[d]);
+    kout[pos] = key;
+    vout[pos] = sv[i];
+  }
+}
+
+cudaError_t sort_init() {
+  if (sort_attr_set) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(sort_downsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       STAGE_BYTES_SORT);
+  if (e == cudaSuccess) sort_attr_set = true;
+  return e;
 }
 
 // ---------------------------------------------------------------- exclusive scan (int32)
@@ -657,7 +714,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     ProfScope prof("grid_keys", s);
     init_bbox_kernel<<<1, 32, 0, s>>>(bbox, cnts); count_launches(1);
     cudaMemsetAsync(cnts + 1, 0, 8, s);
-    const bool vec4 = (npix % 4 == 0) && (reinterpret_cast<uintptr_t>(in.depth) % 16 == 0);
+    const bool vec4 = (in.W % 4 == 0) && (reinterpret_cast<uintptr_t>(in.depth) % 16 == 0);
     grid_keys_kernel<<<grid_blocks(vec4 ? npix / 4 : npix, 256, sms), 256, 0, s>>>(
         in.depth, npix, in.H, in.W, in.stride, in.rot, in.trans, cam, k0, v0, bbox, cnts, vec4); count_launches(1);
   }
@@ -684,12 +741,13 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     rk.by = rk.bz = 21;
     bits = 64;
   }
+  if ((e = sort_init()) != cudaSuccess) return e;
   {
     ProfScope prof("grid_sort", s);
     for (int shift = 0; shift < bits; shift += 8) {
       sort_upsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, 0, s>>>(k0, npix, rk, shift, hist, w.tiles); count_launches(1);
       if ((e = exclusive_scan<int32_t>(hist, (int64_t)RADIX * w.tiles, hist, ssum, nullptr, s)) != cudaSuccess) return e;
-      sort_downsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, 0, s>>>(k0, v0, npix, rk, shift, hist, w.tiles, k1, v1); count_launches(1);
+      sort_downsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, STAGE_BYTES_SORT, s>>>(k0, v0, npix, rk, shift, hist, w.tiles, k1, v1); count_launches(1);
       uint64_t* tk = k0; k0 = k1; k1 = tk;
       uint32_t* tv = v0; v0 = v1; v1 = tv;
     }
@@ -758,11 +816,12 @@ cudaError_t radix_sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n, int bits
   ident.bz = 21;
   uint64_t* k0 = keys;
   uint32_t* v0 = vals;
-  cudaError_t e;
+  cudaError_t e = sort_init();
+  if (e != cudaSuccess) return e;
   for (int shift = 0; shift < bits; shift += 8) {
     sort_upsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, 0, s>>>(k0, n, ident, shift, hist, w.tiles); count_launches(1);
     if ((e = exclusive_scan<int32_t>(hist, (int64_t)RADIX * w.tiles, hist, ssum, nullptr, s)) != cudaSuccess) return e;
-    sort_downsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, 0, s>>>(k0, v0, n, ident, shift, hist, w.tiles, k1, v1); count_launches(1);
+    sort_downsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, STAGE_BYTES_SORT, s>>>(k0, v0, n, ident, shift, hist, w.tiles, k1, v1); count_launches(1);
     uint64_t* tk = k0; k0 = k1; k1 = tk;
     uint32_t* tv = v0; v0 = v1; v1 = tv;
   }
