@@ -57,7 +57,7 @@ __device__ __forceinline__ bool hs_contains(const unsigned long long* table, uin
 }
 
 struct Cam {
-  double fx, fy, cx, cy, voxel;
+  double fx, fy, cx, cy, voxel, inv_voxel;
 };
 
 // slam.py:594-598 with the dgemv FMA order (oracle/oracle.c backproject1).
@@ -70,10 +70,21 @@ __device__ __forceinline__ void backproject(const double* __restrict__ R, const 
   for (int i = 0; i < 3; i++) p[i] = __fma_rn(R[6 + i], w2, __fma_rn(R[3 + i], w1, dmul(R[i], w0)));
 }
 
-__device__ __forceinline__ bool voxel_of(const double* p, double voxel, int64_t* q) {
+// floor(RN(p / vs)) without a division in the common case: q = RN(p * RN(1/vs))
+// is within 3*2^-53*|p/vs| of RN(p/vs), so unless q lies within that band of an
+// integer both floors agree; inside the band fall back to the exact quotient.
+__device__ __forceinline__ double floor_div(double p, double vs, double inv) {
+  const double q = dmul(p, inv);
+  const double f = floor(q);
+  const double band = fabs(q) * 1e-15 + 1e-300;
+  if (dsub(q, f) > band && dsub(dadd(f, 1.0), q) > band) return f;
+  return floor(ddiv(p, vs));
+}
+
+__device__ __forceinline__ bool voxel_of(const double* p, double voxel, int64_t* q, double inv) {
 #pragma unroll
   for (int a = 0; a < 3; a++) {
-    const double f = floor(ddiv(p[a], voxel));
+    const double f = floor_div(p[a], voxel, inv);
     if (!(f >= -(double)KEY_BIAS && f < (double)KEY_BIAS)) return false;
     q[a] = (int64_t)f + KEY_BIAS;
   }
@@ -120,7 +131,7 @@ grid_keys_kernel(const float* __restrict__ depth, int64_t npix, int64_t H, int64
         double p[3];
         backproject(R, T, cam, (double)u, (double)v, (double)d32, p);
         int64_t qv[3];
-        if (voxel_of(p, cam.voxel, qv)) {
+        if (voxel_of(p, cam.voxel, qv, cam.inv_voxel)) {
           key = ((uint64_t)qv[0] << 42) | ((uint64_t)qv[1] << 21) | (uint64_t)qv[2];
 #pragma unroll
           for (int a = 0; a < 3; a++) {
@@ -168,6 +179,186 @@ __global__ void init_bbox_kernel(int* bbox, unsigned long long* nvalid) {
   if (threadIdx.x == 0) *nvalid = 0;
 }
 
+// First-pick mode variant of G1: a pixel whose key equals the previous pixel's
+// (same thread, or the previous lane's last pixel) is dropped -- the earlier
+// one has the lower pixel id -- and the survivors are compacted IN PIXEL ORDER
+// with a single-pass decoupled look-back over 1024-pixel tiles (dynamic tile
+// ids, so earlier tiles are always in flight).  After the stable sort the
+// first item of every voxel segment is therefore its lowest pixel id.
+constexpr int KT_THREADS = 256;
+constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_VAL = (1ull << 62) - 1;
+
+constexpr int KT_GROUPS = 4;   // pixel groups (of 4 with float4) per thread and tile
+
+__global__ void __launch_bounds__(KT_THREADS)
+grid_keys_compact_kernel(const float* __restrict__ depth, int64_t npix, int64_t H, int64_t W, int stride,
+                         const double* __restrict__ rot, const double* __restrict__ trans, Cam cam,
+                         uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, int* bbox,
+                         unsigned long long* nvalid, bool vec4, unsigned* tile_counter,
+                         unsigned long long* status, int64_t ntiles, unsigned long long* n_items) {
+  __shared__ unsigned s_tile;
+  __shared__ uint32_t wtot[KT_THREADS / 32];
+  __shared__ uint32_t s_excl;
+  int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
+  unsigned cnt = 0;
+  const uint32_t HW = (uint32_t)(H * W), Wu = (uint32_t)W, su = (uint32_t)stride;
+  const uint32_t nq = (uint32_t)(vec4 ? npix / 4 : npix);
+  const int per = vec4 ? 4 : 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  while (true) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const unsigned t = s_tile;
+    __syncthreads();
+    if (t >= ntiles) break;
+    // warp w owns 32*G consecutive pixel groups of the tile; group g of a lane is
+    // q = tile_base + w*32*G + g*32 + lane, so pixel order = (warp, g, lane)
+    uint64_t kout[KT_GROUPS][4];
+    uint32_t p0s[KT_GROUPS];
+    float dv[KT_GROUPS][4];
+#pragma unroll
+    for (int g = 0; g < KT_GROUPS; g++) {
+      const uint32_t q = t * KT_THREADS * KT_GROUPS + (uint32_t)warp * 32 * KT_GROUPS + g * 32 + lane;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        kout[g][j] = KEY_INVALID;
+        dv[g][j] = 0.f;
+      }
+      p0s[g] = 0;
+      if (q < nq) {
+        if (vec4) {
+          const float4 d4 = __ldg(reinterpret_cast<const float4*>(depth) + q);
+          dv[g][0] = d4.x; dv[g][1] = d4.y; dv[g][2] = d4.z; dv[g][3] = d4.w;
+          p0s[g] = q * 4;
+        } else {
+          dv[g][0] = __ldg(depth + q);
+          p0s[g] = q;
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < KT_GROUPS; g++) {
+      const uint32_t q = t * KT_THREADS * KT_GROUPS + (uint32_t)warp * 32 * KT_GROUPS + g * 32 + lane;
+      if (q >= nq) continue;
+      const uint32_t p0 = p0s[g];
+      const uint32_t f = p0 / HW, rem = p0 - f * HW;
+      const uint32_t u = rem / Wu, v0 = rem - u * Wu;
+      const bool row_on = (u % su) == 0;
+      const double* R = rot + (size_t)f * 9;
+      const double* T = trans + (size_t)f * 3;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if (j >= per) break;
+        const uint32_t v = v0 + j;
+        const float d32 = dv[g][j];
+        if (row_on && (v % su) == 0 && d32 > 0.f) {
+          double p[3];
+          backproject(R, T, cam, (double)u, (double)v, (double)d32, p);
+          int64_t qv[3];
+          if (voxel_of(p, cam.voxel, qv, cam.inv_voxel)) {
+            kout[g][j] = ((uint64_t)qv[0] << 42) | ((uint64_t)qv[1] << 21) | (uint64_t)qv[2];
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+              lo[a] = min(lo[a], (int)qv[a]);
+              hi[a] = max(hi[a], (int)qv[a]);
+            }
+            cnt++;
+          }
+        }
+      }
+    }
+    // drop repeats of the previous pixel in pixel order, count survivors
+    uint32_t keep[KT_GROUPS], c = 0;
+#pragma unroll
+    for (int g = 0; g < KT_GROUPS; g++) {
+      const uint64_t prev = __shfl_up_sync(FULL, kout[g][per - 1], 1);
+      const uint64_t wrap = g ? __shfl_sync(FULL, kout[g > 0 ? g - 1 : 0][per - 1], 31) : KEY_INVALID;
+      keep[g] = 0;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if (j >= per) break;
+        const uint64_t before = j ? kout[g][j - 1] : (lane ? prev : wrap);
+        if (kout[g][j] != KEY_INVALID && kout[g][j] != before) keep[g] |= 1u << j;
+      }
+      c += __popc(keep[g]);
+    }
+    // order inside the tile is (warp, g, lane): scan per group over the warp
+    uint32_t goff[KT_GROUPS], wsum = 0;
+#pragma unroll
+    for (int g = 0; g < KT_GROUPS; g++) {
+      const uint32_t cg = __popc(keep[g]);
+      uint32_t x = cg;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      goff[g] = wsum + x - cg;
+      wsum += __shfl_sync(FULL, x, 31);
+    }
+    if (lane == 0) wtot[warp] = wsum;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t wv = lane < KT_THREADS / 32 ? wtot[lane] : 0, wx = wv;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, wx, o);
+        if (lane >= o) wx += y;
+      }
+      const uint32_t agg = __shfl_sync(FULL, wx, KT_THREADS / 32 - 1);
+      if (lane < KT_THREADS / 32) wtot[lane] = wx - wv;   // exclusive warp offsets
+      if (lane == 0) {
+        unsigned long long excl = 0;
+        if (t == 0) {
+          atomicExch(status, LB_PRE | agg);
+        } else {
+          atomicExch(status + t, LB_AGG | agg);
+          for (int64_t j = (int64_t)t - 1; j >= 0; j--) {
+            unsigned long long sv;
+            do {
+              sv = *reinterpret_cast<volatile unsigned long long*>(status + j);
+            } while ((sv & ~LB_VAL) == 0);
+            excl += sv & LB_VAL;
+            if (sv & LB_PRE) break;
+          }
+          atomicExch(status + t, LB_PRE | (excl + agg));
+        }
+        s_excl = (uint32_t)excl;
+        if (t == ntiles - 1) *n_items = excl + agg;
+      }
+    }
+    __syncthreads();
+    (void)c;
+    const uint32_t wbase = s_excl + wtot[warp];
+#pragma unroll
+    for (int g = 0; g < KT_GROUPS; g++) {
+      uint32_t o2 = wbase + goff[g];
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        if (keep[g] & (1u << j)) {
+          keys[o2] = kout[g][j];
+          vals[o2] = p0s[g] + j;
+          o2++;
+        }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; a++)
+    for (int o = 16; o; o >>= 1) {
+      lo[a] = min(lo[a], __shfl_xor_sync(FULL, lo[a], o));
+      hi[a] = max(hi[a], __shfl_xor_sync(FULL, hi[a], o));
+    }
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+  if (lane == 0) {
+    if (cnt) {
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        atomicMin(bbox + a, lo[a]);
+        atomicMax(bbox + 3 + a, hi[a]);
+      }
+    }
+    atomicAdd(nvalid, (unsigned long long)cnt);
+  }
+}
+
 // ---------------------------------------------------------------- G2 radix sort
 // The sort key is the bbox-relative packing of the biased voxel fields:
 // rel = ((x-x0) << (by+bz)) | ((y-y0) << bz) | (z-z0); invalid keys map to
@@ -199,13 +390,19 @@ sort_upsweep_kernel(const uint64_t* __restrict__ keys, int64_t n, RelKey rk, int
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 8 * RADIX; i += SORT_THREADS) (&h[0][0])[i] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * SORT_TILE;
+  const int64_t base = (int64_t)blockIdx.x * SORT_TILE + (int64_t)warp * (SORT_TILE / 8);
+  uint64_t k[SORT_ITEMS];
+#pragma unroll
+  for (int r = 0; r < SORT_ITEMS; r++) {   // all loads first (memory-level parallelism)
+    const int64_t i = base + r * 32 + lane;
+    k[r] = i < n ? __ldg(keys + i) : KEY_INVALID;
+  }
+#pragma unroll
   for (int r = 0; r < SORT_ITEMS; r++) {
-    const int64_t i = base + (int64_t)warp * (SORT_TILE / 8) + r * 32 + lane;
-    if (i < n) {
-      const int dg = (int)((rk(keys[i]) >> shift) & (RADIX - 1));
-      atomicAdd(&h[warp][dg], 1);
-    }
+    const bool ok = base + r * 32 + lane < n;
+    const int dg = ok ? (int)((rk(k[r]) >> shift) & (RADIX - 1)) : -1;
+    const unsigned peers = __match_any_sync(FULL, dg);   // one smem atomic per distinct digit
+    if (dg >= 0 && lane == __ffs(peers) - 1) atomicAdd(&h[warp][dg], __popc(peers));
   }
   __syncthreads();
   for (int d = threadIdx.x; d < RADIX; d += SORT_THREADS) {
@@ -219,7 +416,7 @@ sort_upsweep_kernel(const uint64_t* __restrict__ keys, int64_t n, RelKey rk, int
 // ranks come from match_any per 32-item round + per-warp digit counters.  The
 // tile is then re-ordered by digit in shared memory so the global writes are
 // contiguous runs per digit (coalesced) instead of 32 scattered addresses.
-__global__ void __launch_bounds__(SORT_THREADS)
+__global__ void __launch_bounds__(SORT_THREADS, 3)
 sort_downsweep_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t n, RelKey rk,
                       int shift, const int32_t* __restrict__ scanned, int64_t tiles, uint64_t* __restrict__ kout,
                       uint32_t* __restrict__ vout) {
@@ -240,11 +437,14 @@ sort_downsweep_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restri
   int16_t rank[SORT_ITEMS];
   uint8_t dg[SORT_ITEMS];
 #pragma unroll
-  for (int r = 0; r < SORT_ITEMS; r++) {
+  for (int r = 0; r < SORT_ITEMS; r++) {   // all loads first (memory-level parallelism)
     const int64_t i = base + r * 32 + lane;
-    const bool ok = i < n;
-    k[r] = ok ? kin[i] : KEY_INVALID;
-    v[r] = ok ? vin[i] : 0;
+    k[r] = i < n ? __ldg(kin + i) : KEY_INVALID;
+    v[r] = i < n ? __ldg(vin + i) : 0u;
+  }
+#pragma unroll
+  for (int r = 0; r < SORT_ITEMS; r++) {
+    const bool ok = base + r * 32 + lane < n;
     const int d = ok ? (int)((rk(k[r]) >> shift) & (RADIX - 1)) : -1;
     const unsigned peers = __match_any_sync(FULL, d);
     int rr = -1;
@@ -413,8 +613,8 @@ cudaError_t exclusive_scan(const T* in, int64_t n, int32_t* out, int32_t* block_
 // absent the head pixel is flagged new and remembers its sorted position.
 __global__ void __launch_bounds__(256)
 grid_select_kernel(const uint64_t* __restrict__ k, const uint32_t* __restrict__ v, int64_t n,
-                   unsigned long long* table, uint64_t mask, unsigned long long* set_count, uint8_t* flag,
-                   int32_t* head_pos, unsigned long long* nvox) {
+                   unsigned long long* table, uint64_t mask, unsigned long long* set_count, unsigned* flag_bits,
+                   int32_t* head_pos, unsigned long long* nvox, bool min_scan) {
   unsigned newc = 0, vox = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t key = k[i];
@@ -422,8 +622,10 @@ grid_select_kernel(const uint64_t* __restrict__ k, const uint32_t* __restrict__ 
     if (i > 0 && k[i - 1] == key) continue;
     vox++;
     if (hs_insert(table, mask, key)) {
-      const uint32_t pid = v[i];
-      flag[pid] = 1;
+      uint32_t pid = v[i];
+      if (min_scan)   // compacted input: the representative is the min pixel id of the segment
+        for (int64_t j = i + 1; j < n && k[j] == key; j++) pid = min(pid, v[j]);
+      atomicOr(flag_bits + (pid >> 5), 1u << (pid & 31));
       head_pos[pid] = (int32_t)i;
       newc++;
     }
@@ -464,13 +666,24 @@ struct EmitArgs {
   double* count;
 };
 
+__global__ void popc_kernel(const unsigned* __restrict__ bits, int64_t nw, int32_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __popc(bits[i]);
+}
+
+// One thread per 32-pixel word of the new-voxel bitmask; outputs land at the
+// word's exclusive popcount offset + the bit's rank -> ascending pixel order.
 __global__ void __launch_bounds__(256)
-grid_emit_kernel(const uint8_t* __restrict__ flag, const int32_t* __restrict__ pos, const int32_t* __restrict__ head_pos,
-                 int64_t npix, EmitArgs a) {
+grid_emit_kernel(const unsigned* __restrict__ flag_bits, const int32_t* __restrict__ wpos,
+                 const int32_t* __restrict__ head_pos, int64_t nwords, EmitArgs a) {
   const int64_t HW = a.H * a.W;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npix; p += (int64_t)gridDim.x * blockDim.x) {
-    if (!flag[p]) continue;
-    const int64_t o = pos[p];
+  for (int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; wi < nwords; wi += (int64_t)gridDim.x * blockDim.x) {
+  unsigned word = flag_bits[wi];
+  int64_t o = wpos[wi];
+  while (word) {
+    const int b = __ffs(word) - 1;
+    word &= word - 1;
+    const int64_t p = wi * 32 + b;
     const int64_t f = p / HW, rem = p - f * HW;
     const int64_t u = rem / a.W, v = rem - u * a.W;
     const double d = (double)a.depth[p];
@@ -483,7 +696,7 @@ grid_emit_kernel(const uint8_t* __restrict__ flag, const int32_t* __restrict__ p
       double mu[3];
       backproject(a.rot + f * 9, a.trans + f * 3, a.cam, (double)u, (double)v, d, mu);
       int64_t q[3];
-      voxel_of(mu, a.cam.voxel, q);
+      voxel_of(mu, a.cam.voxel, q, a.cam.inv_voxel);
       a.key[o] = ((uint64_t)q[0] << 42) | ((uint64_t)q[1] << 21) | (uint64_t)q[2];
       for (int c = 0; c < 3; c++) {
         a.mu[o * 3 + c] = mu[c];
@@ -523,6 +736,8 @@ grid_emit_kernel(const uint8_t* __restrict__ flag, const int32_t* __restrict__ p
       }
       if (a.count) a.count[o] = cnt;
     }
+    o++;
+  }
   }
 }
 
@@ -653,14 +868,14 @@ cudaError_t hashset_contains(HashSet* h, const uint64_t* keys, int64_t n, uint8_
 cudaError_t launch_backproject(const double* R, const double* t, const double* intr4, double voxel, const double* u,
                                const double* v, const double* d, int64_t n, double* out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  Cam cam{intr4[0], intr4[1], intr4[2], intr4[3], voxel};
+  Cam cam{intr4[0], intr4[1], intr4[2], intr4[3], voxel, 1.0 / voxel};
   backproject_kernel<<<grid_blocks(n, 256, 148), 256, 0, s>>>(R, t, cam, u, v, d, n, out); count_launches(1);
   return cudaGetLastError();
 }
 
 // Workspace layout for one batch of npix pixels.
 struct GridWs {
-  size_t off_k0, off_v0, off_k1, off_v1, off_hist, off_scan_sums, off_flag, off_pos, off_head, off_misc, total;
+  size_t off_k0, off_v0, off_k1, off_v1, off_hist, off_scan_sums, off_flag, off_pos, off_head, off_lb, off_misc, total;
   int64_t tiles;
 };
 
@@ -678,9 +893,10 @@ GridWs grid_ws(int64_t npix) {
   w.off_hist = take((size_t)RADIX * w.tiles * 4);
   const size_t scan_n = n > (size_t)RADIX * w.tiles ? n : (size_t)RADIX * w.tiles;
   w.off_scan_sums = take(((scan_n + SCAN_TILE - 1) / SCAN_TILE + 1) * 4);
-  w.off_flag = take(n);
+  w.off_flag = take((n / 32 + 1) * 4);
   w.off_pos = take(n * 4);
   w.off_head = take(n * 4);
+  w.off_lb = take((n / KT_THREADS + 2) * 8);
   w.off_misc = take(256);
   w.total = o;
   return w;
@@ -706,25 +922,41 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   int* bbox = reinterpret_cast<int*>(b + w.off_misc);
   unsigned long long* cnts = reinterpret_cast<unsigned long long*>(b + w.off_misc + 64);  // nvalid, nvox
   int32_t* grand = reinterpret_cast<int32_t*>(b + w.off_misc + 128);
+  unsigned long long* lb_status = reinterpret_cast<unsigned long long*>(b + w.off_lb);
   out.n_new = out.n_valid = out.n_voxels = 0;
   if (npix == 0) return cudaSuccess;
   cudaError_t e;
-  const Cam cam{in.fx, in.fy, in.cx, in.cy, in.voxel};
+  const Cam cam{in.fx, in.fy, in.cx, in.cy, in.voxel, 1.0 / in.voxel};
+  const bool compact = in.mode == 0;   // first-pick: dedup runs + compaction before the sort
+  const int64_t nwords = (npix + 31) / 32;
   {
     ProfScope prof("grid_keys", s);
     init_bbox_kernel<<<1, 32, 0, s>>>(bbox, cnts); count_launches(1);
-    cudaMemsetAsync(cnts + 1, 0, 8, s);
+    cudaMemsetAsync(cnts + 1, 0, 40, s);
     const bool vec4 = (in.W % 4 == 0) && (reinterpret_cast<uintptr_t>(in.depth) % 16 == 0);
-    grid_keys_kernel<<<grid_blocks(vec4 ? npix / 4 : npix, 256, sms), 256, 0, s>>>(
-        in.depth, npix, in.H, in.W, in.stride, in.rot, in.trans, cam, k0, v0, bbox, cnts, vec4); count_launches(1);
+    if (compact) {
+      const int64_t nq = vec4 ? npix / 4 : npix;
+      const int64_t ntiles = (nq + KT_THREADS * KT_GROUPS - 1) / (KT_THREADS * KT_GROUPS);
+      unsigned* tile_counter = reinterpret_cast<unsigned*>(cnts + 4);
+      cudaMemsetAsync(tile_counter, 0, 4, s);
+      cudaMemsetAsync(lb_status, 0, sizeof(unsigned long long) * ntiles, s);
+      grid_keys_compact_kernel<<<grid_blocks(ntiles * KT_THREADS, KT_THREADS, sms), KT_THREADS, 0, s>>>(
+          in.depth, npix, in.H, in.W, in.stride, in.rot, in.trans, cam, k0, v0, bbox, cnts, vec4, tile_counter,
+          lb_status, ntiles, cnts + 2); count_launches(1);
+    } else {
+      grid_keys_kernel<<<grid_blocks(vec4 ? npix / 4 : npix, 256, sms), 256, 0, s>>>(
+          in.depth, npix, in.H, in.W, in.stride, in.rot, in.trans, cam, k0, v0, bbox, cnts, vec4); count_launches(1);
+    }
   }
   int hb[8];
-  unsigned long long nvalid = 0;
+  unsigned long long hc[3] = {0, 0, 0};
   if ((e = cudaMemcpyAsync(hb, bbox, 6 * sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-  if ((e = cudaMemcpyAsync(&nvalid, cnts, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(hc, cnts, 24, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  const unsigned long long nvalid = hc[0];
   out.n_valid = (int64_t)nvalid;
   if (nvalid == 0) return cudaSuccess;
+  const int64_t nitems = compact ? (int64_t)hc[2] : npix;   // items to sort
   if ((e = hashset_reserve(hs, (int64_t)nvalid, s)) != cudaSuccess) return e;
   // bbox-relative key width; +1 on x keeps the all-ones invalid key above every valid key
   RelKey rk;
@@ -742,25 +974,28 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     bits = 64;
   }
   if ((e = sort_init()) != cudaSuccess) return e;
+  const int64_t tiles = (nitems + SORT_TILE - 1) / SORT_TILE;
+  if (nitems == 0) return cudaSuccess;
   {
     ProfScope prof("grid_sort", s);
     for (int shift = 0; shift < bits; shift += 8) {
-      sort_upsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, 0, s>>>(k0, npix, rk, shift, hist, w.tiles); count_launches(1);
-      if ((e = exclusive_scan<int32_t>(hist, (int64_t)RADIX * w.tiles, hist, ssum, nullptr, s)) != cudaSuccess) return e;
-      sort_downsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, STAGE_BYTES_SORT, s>>>(k0, v0, npix, rk, shift, hist, w.tiles, k1, v1); count_launches(1);
+      sort_upsweep_kernel<<<(unsigned)tiles, SORT_THREADS, 0, s>>>(k0, nitems, rk, shift, hist, tiles); count_launches(1);
+      if ((e = exclusive_scan<int32_t>(hist, (int64_t)RADIX * tiles, hist, ssum, nullptr, s)) != cudaSuccess) return e;
+      sort_downsweep_kernel<<<(unsigned)tiles, SORT_THREADS, STAGE_BYTES_SORT, s>>>(k0, v0, nitems, rk, shift, hist, tiles, k1, v1); count_launches(1);
       uint64_t* tk = k0; k0 = k1; k1 = tk;
       uint32_t* tv = v0; v0 = v1; v1 = tv;
     }
   }
   {
     ProfScope prof("grid_select", s);
-    cudaMemsetAsync(flag, 0, (size_t)npix, s);
-    grid_select_kernel<<<grid_blocks(npix, 256, sms), 256, 0, s>>>(k0, v0, npix, hs->table, (uint64_t)hs->cap - 1,
-                                                                   hs->count_dev, flag, head, cnts + 1); count_launches(1);
+    cudaMemsetAsync(flag, 0, (size_t)nwords * 4, s);
+    grid_select_kernel<<<grid_blocks(nitems, 256, sms), 256, 0, s>>>(k0, v0, nitems, hs->table, (uint64_t)hs->cap - 1,
+                                                                     hs->count_dev, reinterpret_cast<unsigned*>(flag), head, cnts + 1, false); count_launches(1);
   }
   {
     ProfScope prof("grid_emit", s);
-    if ((e = exclusive_scan<uint8_t>(flag, npix, pos, ssum, grand, s)) != cudaSuccess) return e;
+    popc_kernel<<<grid_blocks(nwords, 256, sms), 256, 0, s>>>(reinterpret_cast<const unsigned*>(flag), nwords, pos); count_launches(1);
+    if ((e = exclusive_scan<int32_t>(pos, nwords, pos, ssum, grand, s)) != cudaSuccess) return e;
     int32_t nnew = 0;
     unsigned long long nvox = 0;
     if ((e = cudaMemcpyAsync(&nnew, grand, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
@@ -786,7 +1021,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     a.fw = in.fw;
     a.skeys = k0;
     a.svals = v0;
-    a.n = npix;
+    a.n = nitems;
     a.key = out.key;
     a.pid = out.pid;
     a.mu = out.mu;
@@ -795,7 +1030,8 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     a.dep = out.depth;
     a.ofeat = out.feat;
     a.count = out.count;
-    grid_emit_kernel<<<grid_blocks(npix, 256, sms), 256, 0, s>>>(flag, pos, head, npix, a); count_launches(1);
+    grid_emit_kernel<<<grid_blocks(nwords, 256, sms), 256, 0, s>>>(reinterpret_cast<const unsigned*>(flag), pos, head,
+                                                                    nwords, a); count_launches(1);
   }
   return cudaGetLastError();
 }

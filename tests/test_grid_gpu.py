@@ -136,6 +136,23 @@ def test_grid_edge_cases(xs):
     assert r["pid"].tolist() == [0] and r["n_voxels"] == 1
 
 
+def test_voxel_boundaries_bit_exact(xs):
+    """Depths exactly on / one float32 ulp around voxel boundaries (the floor
+    fast path's guard band must fall back to the exact quotient)."""
+    grid, _, _ = xs
+    base = np.array([0.25 * k for k in range(1, 40)] + [0.1 * k for k in range(1, 40)], np.float32)
+    d = np.concatenate([base, np.nextafter(base, np.float32(0)), np.nextafter(base, np.float32(10))])
+    H, W = 6, d.size // 6
+    depth = d[:H * W].reshape(H, W)
+    for vs in (0.25, 0.1, 0.05, 1.0 / 3.0):
+        intr = (7.0, 11.0, 2.5, 3.0)
+        gs = grid.GridSampler(intr, vs)
+        got = gs.sample(depth, (np.eye(3)[None], np.zeros((1, 3)))).to_numpy()
+        ref = og.grid_sample([(depth, np.zeros((H, W, 3), np.uint8), np.eye(3), np.zeros(3))], np.array(intr), vs,
+                             set())
+        assert np.array_equal(got["key"], ref["key"]) and np.array_equal(got["pid"], ref["pid"]), vs
+
+
 def test_radix_sort_matches_stable_argsort(xs, cuda):
     import torch
     grid, _, _ = xs
