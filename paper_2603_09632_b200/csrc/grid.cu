@@ -146,10 +146,10 @@ grid_keys_kernel(const float* __restrict__ depth, int64_t npix, int64_t H, int64
     if (vec4) {
       reinterpret_cast<ulonglong2*>(keys)[(size_t)q * 2] = make_ulonglong2(kout[0], kout[1]);
       reinterpret_cast<ulonglong2*>(keys)[(size_t)q * 2 + 1] = make_ulonglong2(kout[2], kout[3]);
-      reinterpret_cast<uint4*>(vals)[q] = make_uint4(p0, p0 + 1, p0 + 2, p0 + 3);
+      if (vals) reinterpret_cast<uint4*>(vals)[q] = make_uint4(p0, p0 + 1, p0 + 2, p0 + 3);
     } else {
       keys[p0] = kout[0];
-      vals[p0] = p0;
+      if (vals) vals[p0] = p0;
     }
   }
 #pragma unroll
@@ -179,31 +179,23 @@ __global__ void init_bbox_kernel(int* bbox, unsigned long long* nvalid) {
   if (threadIdx.x == 0) *nvalid = 0;
 }
 
-// First-pick mode variant of G1: a pixel whose key equals the previous pixel's
-// (same thread, or the previous lane's last pixel) is dropped -- the earlier
-// one has the lower pixel id -- and the survivors are compacted IN PIXEL ORDER
-// with a single-pass decoupled look-back over 1024-pixel tiles (dynamic tile
-// ids, so earlier tiles are always in flight).  After the stable sort the
-// first item of every voxel segment is therefore its lowest pixel id.
-constexpr int KT_THREADS = 256;
+// First-pick mode: compact the per-pixel keys before the sort.  A pixel whose
+// key equals the previous pixel's (keys[p-1], pixel order) is dropped -- the
+// earlier one has the lower pixel id -- and invalid pixels go too.  The
+// survivors are written IN PIXEL ORDER by a single-pass decoupled look-back
+// over 4096-pixel tiles (dynamic tile ids, so earlier tiles are always in
+// flight).  After the stable sort the first item of every voxel segment is
+// therefore its lowest pixel id.
+constexpr int CT_THREADS = 256, CT_ITEMS = 16, CT_TILE = CT_THREADS * CT_ITEMS;
 constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_VAL = (1ull << 62) - 1;
 
-constexpr int KT_GROUPS = 4;   // pixel groups (of 4 with float4) per thread and tile
-
-__global__ void __launch_bounds__(KT_THREADS)
-grid_keys_compact_kernel(const float* __restrict__ depth, int64_t npix, int64_t H, int64_t W, int stride,
-                         const double* __restrict__ rot, const double* __restrict__ trans, Cam cam,
-                         uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, int* bbox,
-                         unsigned long long* nvalid, bool vec4, unsigned* tile_counter,
-                         unsigned long long* status, int64_t ntiles, unsigned long long* n_items) {
+__global__ void __launch_bounds__(CT_THREADS)
+compact_keys_kernel(const uint64_t* __restrict__ kin, int64_t n, uint64_t* __restrict__ kout,
+                    uint32_t* __restrict__ vout, unsigned* tile_counter, unsigned long long* status, int64_t ntiles,
+                    unsigned long long* n_items) {
   __shared__ unsigned s_tile;
-  __shared__ uint32_t wtot[KT_THREADS / 32];
+  __shared__ uint32_t wtot[CT_THREADS / 32];
   __shared__ uint32_t s_excl;
-  int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
-  unsigned cnt = 0;
-  const uint32_t HW = (uint32_t)(H * W), Wu = (uint32_t)W, su = (uint32_t)stride;
-  const uint32_t nq = (uint32_t)(vec4 ? npix / 4 : npix);
-  const int per = vec4 ? 4 : 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   while (true) {
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
@@ -211,100 +203,34 @@ grid_keys_compact_kernel(const float* __restrict__ depth, int64_t npix, int64_t 
     const unsigned t = s_tile;
     __syncthreads();
     if (t >= ntiles) break;
-    // warp w owns 32*G consecutive pixel groups of the tile; group g of a lane is
-    // q = tile_base + w*32*G + g*32 + lane, so pixel order = (warp, g, lane)
-    uint64_t kout[KT_GROUPS][4];
-    uint32_t p0s[KT_GROUPS];
-    float dv[KT_GROUPS][4];
+    // warp w owns items [tile + w*512, +512), round r covers 32 consecutive items
+    const int64_t base = (int64_t)t * CT_TILE + (int64_t)warp * (CT_TILE / 8);
+    uint64_t k[CT_ITEMS], pk[CT_ITEMS];
 #pragma unroll
-    for (int g = 0; g < KT_GROUPS; g++) {
-      const uint32_t q = t * KT_THREADS * KT_GROUPS + (uint32_t)warp * 32 * KT_GROUPS + g * 32 + lane;
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        kout[g][j] = KEY_INVALID;
-        dv[g][j] = 0.f;
-      }
-      p0s[g] = 0;
-      if (q < nq) {
-        if (vec4) {
-          const float4 d4 = __ldg(reinterpret_cast<const float4*>(depth) + q);
-          dv[g][0] = d4.x; dv[g][1] = d4.y; dv[g][2] = d4.z; dv[g][3] = d4.w;
-          p0s[g] = q * 4;
-        } else {
-          dv[g][0] = __ldg(depth + q);
-          p0s[g] = q;
-        }
-      }
+    for (int r = 0; r < CT_ITEMS; r++) {
+      const int64_t i = base + r * 32 + lane;
+      k[r] = i < n ? __ldg(kin + i) : KEY_INVALID;
+      pk[r] = (i > 0 && i <= n) ? __ldg(kin + i - 1) : KEY_INVALID;
     }
+    uint32_t keep = 0, roff[CT_ITEMS], wsum = 0;
 #pragma unroll
-    for (int g = 0; g < KT_GROUPS; g++) {
-      const uint32_t q = t * KT_THREADS * KT_GROUPS + (uint32_t)warp * 32 * KT_GROUPS + g * 32 + lane;
-      if (q >= nq) continue;
-      const uint32_t p0 = p0s[g];
-      const uint32_t f = p0 / HW, rem = p0 - f * HW;
-      const uint32_t u = rem / Wu, v0 = rem - u * Wu;
-      const bool row_on = (u % su) == 0;
-      const double* R = rot + (size_t)f * 9;
-      const double* T = trans + (size_t)f * 3;
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        if (j >= per) break;
-        const uint32_t v = v0 + j;
-        const float d32 = dv[g][j];
-        if (row_on && (v % su) == 0 && d32 > 0.f) {
-          double p[3];
-          backproject(R, T, cam, (double)u, (double)v, (double)d32, p);
-          int64_t qv[3];
-          if (voxel_of(p, cam.voxel, qv, cam.inv_voxel)) {
-            kout[g][j] = ((uint64_t)qv[0] << 42) | ((uint64_t)qv[1] << 21) | (uint64_t)qv[2];
-#pragma unroll
-            for (int a = 0; a < 3; a++) {
-              lo[a] = min(lo[a], (int)qv[a]);
-              hi[a] = max(hi[a], (int)qv[a]);
-            }
-            cnt++;
-          }
-        }
-      }
-    }
-    // drop repeats of the previous pixel in pixel order, count survivors
-    uint32_t keep[KT_GROUPS], c = 0;
-#pragma unroll
-    for (int g = 0; g < KT_GROUPS; g++) {
-      const uint64_t prev = __shfl_up_sync(FULL, kout[g][per - 1], 1);
-      const uint64_t wrap = g ? __shfl_sync(FULL, kout[g > 0 ? g - 1 : 0][per - 1], 31) : KEY_INVALID;
-      keep[g] = 0;
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        if (j >= per) break;
-        const uint64_t before = j ? kout[g][j - 1] : (lane ? prev : wrap);
-        if (kout[g][j] != KEY_INVALID && kout[g][j] != before) keep[g] |= 1u << j;
-      }
-      c += __popc(keep[g]);
-    }
-    // order inside the tile is (warp, g, lane): scan per group over the warp
-    uint32_t goff[KT_GROUPS], wsum = 0;
-#pragma unroll
-    for (int g = 0; g < KT_GROUPS; g++) {
-      const uint32_t cg = __popc(keep[g]);
-      uint32_t x = cg;
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(FULL, x, o);
-        if (lane >= o) x += y;
-      }
-      goff[g] = wsum + x - cg;
-      wsum += __shfl_sync(FULL, x, 31);
+    for (int r = 0; r < CT_ITEMS; r++) {
+      const bool kp = k[r] != KEY_INVALID && k[r] != pk[r];
+      const unsigned b = __ballot_sync(FULL, kp);
+      roff[r] = wsum + __popc(b & ((1u << lane) - 1u));
+      wsum += __popc(b);
+      keep |= (kp ? 1u : 0u) << r;
     }
     if (lane == 0) wtot[warp] = wsum;
     __syncthreads();
     if (warp == 0) {
-      uint32_t wv = lane < KT_THREADS / 32 ? wtot[lane] : 0, wx = wv;
+      uint32_t wv = lane < CT_THREADS / 32 ? wtot[lane] : 0, wx = wv;
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(FULL, wx, o);
         if (lane >= o) wx += y;
       }
-      const uint32_t agg = __shfl_sync(FULL, wx, KT_THREADS / 32 - 1);
-      if (lane < KT_THREADS / 32) wtot[lane] = wx - wv;   // exclusive warp offsets
+      const uint32_t agg = __shfl_sync(FULL, wx, CT_THREADS / 32 - 1);
+      if (lane < CT_THREADS / 32) wtot[lane] = wx - wv;   // exclusive warp offsets
       if (lane == 0) {
         unsigned long long excl = 0;
         if (t == 0) {
@@ -326,36 +252,13 @@ grid_keys_compact_kernel(const float* __restrict__ depth, int64_t npix, int64_t 
       }
     }
     __syncthreads();
-    (void)c;
     const uint32_t wbase = s_excl + wtot[warp];
 #pragma unroll
-    for (int g = 0; g < KT_GROUPS; g++) {
-      uint32_t o2 = wbase + goff[g];
-#pragma unroll
-      for (int j = 0; j < 4; j++)
-        if (keep[g] & (1u << j)) {
-          keys[o2] = kout[g][j];
-          vals[o2] = p0s[g] + j;
-          o2++;
-        }
-    }
-  }
-#pragma unroll
-  for (int a = 0; a < 3; a++)
-    for (int o = 16; o; o >>= 1) {
-      lo[a] = min(lo[a], __shfl_xor_sync(FULL, lo[a], o));
-      hi[a] = max(hi[a], __shfl_xor_sync(FULL, hi[a], o));
-    }
-  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
-  if (lane == 0) {
-    if (cnt) {
-#pragma unroll
-      for (int a = 0; a < 3; a++) {
-        atomicMin(bbox + a, lo[a]);
-        atomicMax(bbox + 3 + a, hi[a]);
+    for (int r = 0; r < CT_ITEMS; r++)
+      if (keep & (1u << r)) {
+        kout[wbase + roff[r]] = k[r];
+        vout[wbase + roff[r]] = (uint32_t)(base + r * 32 + lane);
       }
-    }
-    atomicAdd(nvalid, (unsigned long long)cnt);
   }
 }
 
@@ -896,7 +799,7 @@ GridWs grid_ws(int64_t npix) {
   w.off_flag = take((n / 32 + 1) * 4);
   w.off_pos = take(n * 4);
   w.off_head = take(n * 4);
-  w.off_lb = take((n / KT_THREADS + 2) * 8);
+  w.off_lb = take((n / CT_TILE + 2) * 8);
   w.off_misc = take(256);
   w.total = o;
   return w;
@@ -934,18 +837,16 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     init_bbox_kernel<<<1, 32, 0, s>>>(bbox, cnts); count_launches(1);
     cudaMemsetAsync(cnts + 1, 0, 40, s);
     const bool vec4 = (in.W % 4 == 0) && (reinterpret_cast<uintptr_t>(in.depth) % 16 == 0);
+    grid_keys_kernel<<<grid_blocks(vec4 ? npix / 4 : npix, 256, sms), 256, 0, s>>>(
+        in.depth, npix, in.H, in.W, in.stride, in.rot, in.trans, cam, compact ? k1 : k0, compact ? nullptr : v0,
+        bbox, cnts, vec4); count_launches(1);
     if (compact) {
-      const int64_t nq = vec4 ? npix / 4 : npix;
-      const int64_t ntiles = (nq + KT_THREADS * KT_GROUPS - 1) / (KT_THREADS * KT_GROUPS);
+      const int64_t ntiles = (npix + CT_TILE - 1) / CT_TILE;
       unsigned* tile_counter = reinterpret_cast<unsigned*>(cnts + 4);
       cudaMemsetAsync(tile_counter, 0, 4, s);
       cudaMemsetAsync(lb_status, 0, sizeof(unsigned long long) * ntiles, s);
-      grid_keys_compact_kernel<<<grid_blocks(ntiles * KT_THREADS, KT_THREADS, sms), KT_THREADS, 0, s>>>(
-          in.depth, npix, in.H, in.W, in.stride, in.rot, in.trans, cam, k0, v0, bbox, cnts, vec4, tile_counter,
-          lb_status, ntiles, cnts + 2); count_launches(1);
-    } else {
-      grid_keys_kernel<<<grid_blocks(vec4 ? npix / 4 : npix, 256, sms), 256, 0, s>>>(
-          in.depth, npix, in.H, in.W, in.stride, in.rot, in.trans, cam, k0, v0, bbox, cnts, vec4); count_launches(1);
+      compact_keys_kernel<<<grid_blocks(ntiles * CT_THREADS, CT_THREADS, sms), CT_THREADS, 0, s>>>(
+          k1, npix, k0, v0, tile_counter, lb_status, ntiles, cnts + 2); count_launches(1);
     }
   }
   int hb[8];
