@@ -189,6 +189,89 @@ def run_grid(torch, steps, cpu=True):
     return out
 
 
+STREAM_H, STREAM_W, STREAM_D, STREAM_K = 480, 640, 768, 512
+STREAM_INTR = (525.0, 525.0, 239.5, 319.5)
+
+
+def stream_depth(torch, planes, R, t, device):
+    """C4 frames: ray-cast random planes on the device (camera z = ray t)."""
+    fx, fy, cx, cy = STREAM_INTR
+    u = torch.arange(STREAM_H, device=device, dtype=torch.float64)[:, None].expand(STREAM_H, STREAM_W)
+    v = torch.arange(STREAM_W, device=device, dtype=torch.float64)[None, :].expand(STREAM_H, STREAM_W)
+    dcam = torch.stack([(u - cx) / fx, (v - cy) / fy, torch.ones_like(u)], dim=-1)
+    dw = dcam @ R                       # R^T d
+    C = -(R.T @ t)
+    best = torch.full((STREAM_H, STREAM_W), float("inf"), device=device, dtype=torch.float64)
+    for n, c in planes:
+        den = dw @ n
+        tt = (c - n @ C) / den
+        tt = torch.where((tt > 0) & torch.isfinite(tt), tt, torch.full_like(tt, float("inf")))
+        best = torch.minimum(best, tt)
+    best = torch.where((best >= 0.3) & (best <= 8.0), best, torch.zeros_like(best))
+    return best
+
+
+def run_stream(torch, frames, device):
+    """C4: per-frame grid sampling at 0.02 m growing the map + online VQ (K=512,
+    D=768) on the new points' features; per-frame latency p50 / p99."""
+    from paper_2603_09632_b200 import synth
+    from paper_2603_09632_b200.distributed import CudaBackend, DataParallelVQ
+    from paper_2603_09632_b200.grid import GridSampler, VoxelHashSet
+    import paper_2603_09632_b200 as xv
+    rng = np.random.default_rng(30)
+    planes_np = synth.random_planes(rng, 8, centre=np.array([0.0, 0.0, 2.5]), spread=2.5)
+    planes = [(torch.tensor(n, device=device), float(c)) for n, c in planes_np]
+    poses = synth.random_walk_trajectory(frames, rng, step_t=0.01, step_deg=1.0)
+    g = torch.Generator(device=device)
+    g.manual_seed(31)
+    Cn = torch.randn(512, STREAM_D, generator=g, device=device)
+    Cn /= Cn.norm(dim=1, keepdim=True)
+    pool = 4_000_000
+    ids = torch.randint(0, 512, (pool,), generator=g, device=device)
+    feats = torch.empty(pool, STREAM_D, device=device)
+    for s0 in range(0, pool, 1 << 18):
+        sl = slice(s0, min(pool, s0 + (1 << 18)))
+        f = Cn[ids[sl]] + 0.05 * torch.randn(sl.stop - sl.start, STREAM_D, generator=g, device=device)
+        feats[sl] = f / f.norm(dim=1, keepdim=True)
+    del ids
+    E0 = feats[:STREAM_K].double().clone()
+    cfg = xv.VqConfig(K=STREAM_K, lam=0.99, gamma=0.5 / STREAM_K, delta_dead=1e-3)
+    vq = DataParallelVQ((E0, torch.zeros(STREAM_K, dtype=torch.float64, device=device),
+                         torch.zeros(STREAM_K, STREAM_D, dtype=torch.float64, device=device)), cfg,
+                        np.random.default_rng(32), CudaBackend(STREAM_K, STREAM_D, 0.99, 1e-5))
+    gs = GridSampler(STREAM_INTR, 0.02, occupied=VoxelHashSet(4_000_000))
+    noise = torch.Generator(device=device)
+    noise.manual_seed(33)
+    lat, used, newpts = [], 0, []
+    for i, p in enumerate(poses):
+        R = torch.tensor(p.rotation, device=device)
+        t = torch.tensor(p.translation, device=device)
+        d = stream_depth(torch, planes, R, t, device)
+        d = d + 0.005 * torch.randn(d.shape, generator=noise, device=device, dtype=torch.float64) * (d > 0)
+        d = torch.where(torch.rand(d.shape, generator=noise, device=device) < 0.05, torch.zeros_like(d), d)
+        d = d.float().contiguous()
+        col = torch.randint(0, 256, (STREAM_H, STREAM_W, 3), generator=noise, device=device, dtype=torch.uint8)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = gs.sample(d, (R[None], t[None]), col)                  # new Gaussians of this frame
+        n = len(r)
+        if n:
+            x = feats[used % (pool - n):used % (pool - n) + n]         # their semantic features
+            vq.step(x, [n])
+            used += n
+        e1.record()
+        torch.cuda.synchronize()
+        lat.append(e0.elapsed_time(e1))
+        newpts.append(n)
+    lat = np.array(lat[5:])
+    return {"frames": frames, "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
+            "mean_ms": float(lat.mean()), "frames_per_s": float(1e3 / lat.mean()),
+            "map_voxels": int(len(gs.occupied)), "mean_new_per_frame": float(np.mean(newpts)),
+            "workload": "C4: 640x480 random-plane RGB-D, random-walk poses (1 cm / 1 deg), grid 0.02 m, "
+                        "VQ K=512 D=768 on the new points (synthetic 512-centre features)"}
+
+
 def cpu_port_rate(x_host, E, seconds=10.0, threads=None):
     """The reference's assign+accumulate restated in C (oracle/oracle.c), timed
     on host cores over row chunks until ~`seconds` elapse (bounded sample)."""
@@ -221,7 +304,7 @@ def run_reference(args, rank, world):
     E = x[rng.choice(n, K, replace=False)].astype(np.float64)
     from oracle import native as on
     threads = os.cpu_count() or 1
-    per_step = 32 * threads
+    per_step = 8 * threads          # ~1-2 s of CPU per step on the box's cores
     t_all, rows_all = 0.0, 0
     for it in range(args.warmup + args.steps):
         lo = (it * per_step) % (n - per_step)
@@ -256,6 +339,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-grid", action="store_true")
     ap.add_argument("--grid-steps", type=int, default=5)
+    ap.add_argument("--stream-frames", type=int, default=1000)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -358,9 +442,11 @@ def main():
         cpu = {"value": v, "unit": "Mfeat/s", "cores": thr, "kind": "port",
                "sample": f"{rows} rows of the C2 batch in {el:.1f}s (assign+accumulate, oracle/oracle.c, "
                          f"{thr} threads)"}
-    grid = None
+    grid = stream = None
     if rank == 0 and world == 1 and not args.no_grid:
         grid = run_grid(torch, args.grid_steps, cpu=not args.no_cpu)
+    if rank == 0 and world == 1 and args.stream_frames > 0:
+        stream = run_stream(torch, args.stream_frames, device)
     if rank == 0:
         per_kernel = {t: {"ms_per_step": m / args.steps, "launches": c} for t, (m, c) in prof.items()}
         line = {
@@ -383,6 +469,7 @@ def main():
             "clocks": clocks,
             "cpu_baseline": cpu,
             "grid": grid,
+            "stream": stream,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
