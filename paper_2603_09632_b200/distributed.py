@@ -101,6 +101,12 @@ class DataParallelVQ:
         self.be = backend
         self.res = ReservoirMap(cfg.reservoir_capacity, self.world)
         self.ring = backend.new_ring(cfg.reservoir_capacity)
+        E, N, M = codebook_state
+        K, D = getattr(backend, "K", None), getattr(backend, "D", None)
+        if (tuple(E.shape) != (K, D) or tuple(M.shape) != (K, D) or tuple(N.shape) != (K,)):
+            from .errors import InvalidInputError
+            raise InvalidInputError(f"codebook state shapes {tuple(E.shape)}, {tuple(N.shape)}, {tuple(M.shape)} "
+                                    f"do not match K={K}, D={D}")
 
     def _sizes(self, n_local):
         if self.world == 1:

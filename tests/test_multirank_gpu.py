@@ -16,12 +16,12 @@ K, D, STEPS, SIZES = 64, 96, 6, (700, 1300)
 
 def stream():
     rng = np.random.default_rng(8)
-    C = rng.normal(size=(40, D))
+    C = rng.normal(size=(80, D))
     C /= np.linalg.norm(C, axis=1, keepdims=True)
     n = sum(SIZES)
     batches = []
     for _ in range(STEPS):
-        x = C[rng.integers(0, 40, n)] + 0.1 * rng.normal(size=(n, D))
+        x = C[rng.integers(0, 70, n)] + 0.1 * rng.normal(size=(n, D))
         batches.append((x / np.linalg.norm(x, axis=1, keepdims=True)).astype(np.float32))
     E0 = np.concatenate([C[:K - 8] + 0.01, rng.normal(size=(8, D)) * 20]).astype(np.float64)  # 8 die
     return E0, batches
@@ -69,3 +69,24 @@ def test_two_ranks_on_one_gpu_match_single(tmp_path, cuda):
     assert np.array_equal(a["N"], b["N"])
     np.testing.assert_allclose(b["M"], a["M"], rtol=1e-12, atol=1e-14)
     np.testing.assert_allclose(b["E"], a["E"], rtol=1e-12, atol=1e-14)
+
+
+def test_dataparallel_world1_matches_online_step(tmp_path, cuda):
+    """DataParallelVQ (world 1) == the drop-in online_step, bit-exact, with revival."""
+    import torch
+    import paper_2603_09632_b200 as xv
+    single = str(tmp_path / "s.npz")
+    run(0, 1, 0, single)
+    a = np.load(single)
+    E0, batches = stream()
+    cb = xv.Codebook(E=torch.from_numpy(E0).cuda(), N=torch.zeros(K, dtype=torch.float64, device="cuda"),
+                     M=torch.zeros(K, D, dtype=torch.float64, device="cuda"), lam=0.9, epsilon=1e-5,
+                     reservoir=xv.FeatureReservoir(1000, D))
+    cfg = xv.VqConfig(K=K, lam=0.9, gamma=0.5 / K, delta_dead=1e-2, reservoir_capacity=1000)
+    rng = np.random.default_rng(5)
+    revived = []
+    for b in batches:
+        cb, res = xv.online_step(cb, torch.from_numpy(b).cuda(), cfg, rng)
+        revived.append(len(res.revived))
+    assert list(a["rev"]) == revived
+    assert np.array_equal(a["N"], cb.N.cpu().numpy()) and np.array_equal(a["E"], cb.E.cpu().numpy())
