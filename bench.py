@@ -272,6 +272,55 @@ def run_stream(torch, frames, device):
                         "VQ K=512 D=768 on the new points (synthetic 512-centre features)"}
 
 
+C5_ROWS, C5_D, C5_K = 67_108_864 // 8, 1152, 4096
+
+
+def run_c5(torch, iters, device):
+    """C5 per-GPU shard: N = 67,108,864/8 bf16 unit-norm D=1152 rows (4096-centre
+    mixture, sigma 0.05), K=4096 -- the share of one GPU in the 8-GPU C5 run."""
+    from paper_2603_09632_b200 import _native as nat
+    from paper_2603_09632_b200.distributed import CudaBackend, DataParallelVQ
+    import paper_2603_09632_b200 as xv
+    g = torch.Generator(device=device)
+    g.manual_seed(40)
+    C = torch.randn(C5_K, C5_D, generator=g, device=device)
+    C /= C.norm(dim=1, keepdim=True)
+    x = torch.empty(C5_ROWS, C5_D, device=device, dtype=torch.bfloat16)
+    for s0 in range(0, C5_ROWS, 1 << 20):
+        m = min(1 << 20, C5_ROWS - s0)
+        v = C[torch.randint(0, C5_K, (m,), generator=g, device=device)] + 0.05 * torch.randn(
+            m, C5_D, generator=g, device=device)
+        x[s0:s0 + m] = (v / v.norm(dim=1, keepdim=True)).to(torch.bfloat16)
+    E0 = x[torch.randint(0, C5_ROWS, (C5_K,), generator=g, device=device)].double()
+    cfg = xv.VqConfig(K=C5_K, lam=0.99, gamma=0.5 / C5_K, delta_dead=1e-3)
+    vq = DataParallelVQ((E0, torch.zeros(C5_K, dtype=torch.float64, device=device),
+                         torch.zeros(C5_K, C5_D, dtype=torch.float64, device=device)), cfg,
+                        np.random.default_rng(41), CudaBackend(C5_K, C5_D, 0.99, 1e-5))
+    vq.step(x, [C5_ROWS])
+    torch.cuda.synchronize()
+    nat.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        vq.step(x, [C5_ROWS])
+    e1.record()
+    torch.cuda.synchronize()
+    prof = {t: nat.profile_read(t)[0] / iters for t in ("vq_prep", "vq_screen", "vq_rerank", "vq_accumulate",
+                                                          "vq_chain", "vq_ema")}
+    scr = nat.profile_read("vq_screen")
+    nat.profile_enable(False)
+    ms = e0.elapsed_time(e1) / iters
+    flops = 2.0 * C5_ROWS * C5_K * C5_D
+    cb_now = xv.Codebook._make(vq.state[0], vq.state[1], vq.state[2], 0.99, 1e-5, None)
+    _, (n_rerank, n_fallback) = xv.vq.assign_batch_stats(x, cb_now)
+    del x
+    return {"rows": C5_ROWS, "D": C5_D, "K": C5_K, "dtype": "bf16 rows", "iters": iters, "ms_per_iter": ms,
+            "Mfeat_per_s": C5_ROWS / (ms * 1e-3) / 1e6, "screen_ms": scr[0] / max(1, scr[1]),
+            "screen_TFLOPs": flops / (scr[0] / max(1, scr[1]) * 1e-3) / 1e12 if scr[1] else None,
+            "per_kernel_ms": prof, "assign_exact_rows": {"rerank": n_rerank, "fallback": n_fallback},
+            "workload": "C5 per-GPU shard (67,108,864 rows / 8 GPUs), one online_step per iteration"}
+
+
 def cpu_port_rate(x_host, E, seconds=10.0, threads=None):
     """The reference's assign+accumulate restated in C (oracle/oracle.c), timed
     on host cores over row chunks until ~`seconds` elapse (bounded sample)."""
@@ -340,6 +389,7 @@ def main():
     ap.add_argument("--no-grid", action="store_true")
     ap.add_argument("--grid-steps", type=int, default=5)
     ap.add_argument("--stream-frames", type=int, default=1000)
+    ap.add_argument("--c5-iters", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -447,6 +497,11 @@ def main():
         grid = run_grid(torch, args.grid_steps, cpu=not args.no_cpu)
     if rank == 0 and world == 1 and args.stream_frames > 0:
         stream = run_stream(torch, args.stream_frames, device)
+    c5 = None
+    if rank == 0 and world == 1 and args.c5_iters > 0:
+        del x
+        torch.cuda.empty_cache()
+        c5 = run_c5(torch, args.c5_iters, device)
     if rank == 0:
         per_kernel = {t: {"ms_per_step": m / args.steps, "launches": c} for t, (m, c) in prof.items()}
         line = {
@@ -470,6 +525,7 @@ def main():
             "cpu_baseline": cpu,
             "grid": grid,
             "stream": stream,
+            "c5_shard": c5,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

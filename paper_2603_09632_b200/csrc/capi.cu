@@ -127,12 +127,15 @@ int xgs_vq_assign(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, c
   SumPlan pd;
   if (!build_sum_plan((int)d, &pd)) return fail(NOT_SUPPORTED, "feature dim too large for the exact plan");
   // Rigorous screening bound (see vq_screen_sm100.cu): fp16 unit roundoff u
-  // on power-of-2-scaled operands, fp32 accumulation over Dp products (2 ulp
-  // per add), fp32 epilogue rounding, subnormal term c4, 25% slack.
+  // on power-of-2-scaled operands (bf16 rows convert to scaled fp16 exactly,
+  // so only the codebook rounds), fp32 accumulation over Dp products (1 ulp =
+  // 2^-23 per add, covering round-to-nearest and truncation), fp32 epilogue
+  // rounding, subnormal term c4, 25% slack.
   const double u = std::ldexp(1.0, -11);
+  const double ux = dtype == BF16 ? 0.0 : u;
   const double dp = (double)((d + 63) / 64 * 64);
-  const double gacc = (dp + 32.0) * std::ldexp(1.0, -22);
-  const double c1 = 1.25 * (2.0 * ((2 * u + u * u) + gacc * (1 + u) * (1 + u)) + std::ldexp(1.0, -21));
+  const double gacc = (dp + 32.0) * std::ldexp(1.0, -23);
+  const double c1 = 1.25 * (2.0 * ((ux + u + ux * u) + gacc * (1 + u) * (1 + u)) + std::ldexp(1.0, -21));
   const double c2 = 1.25 * std::ldexp(1.0, -21);
   const double c4 = 1.25 * 4.0 * std::sqrt(dp) * std::ldexp(1.0, -37);
   ScreenArgs a;

@@ -48,7 +48,7 @@ cudaError_t launch_exact_rows(const ExactArgs& a, const SumPlan& pd, const SumPl
                               cudaStream_t s);
 
 // Candidate re-rank queue entries written by the screening GEMM.
-constexpr int kCandCap = 8;
+constexpr int kCandCap = 16;
 struct RerankEntry {
   int32_t row;
   int32_t cnt;
