@@ -389,7 +389,7 @@ def main():
     ap.add_argument("--no-grid", action="store_true")
     ap.add_argument("--grid-steps", type=int, default=5)
     ap.add_argument("--stream-frames", type=int, default=1000)
-    ap.add_argument("--c5-iters", type=int, default=3)
+    ap.add_argument("--c5-iters", type=int, default=20)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
