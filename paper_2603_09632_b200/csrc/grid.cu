@@ -190,7 +190,7 @@ constexpr int CT_THREADS = 256, CT_ITEMS = 16, CT_TILE = CT_THREADS * CT_ITEMS;
 constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_VAL = (1ull << 62) - 1;
 
 __global__ void __launch_bounds__(CT_THREADS)
-compact_keys_kernel(const uint64_t* __restrict__ kin, int64_t n, uint64_t* __restrict__ kout,
+compact_keys_kernel(const uint64_t* __restrict__ kin, int64_t n, int64_t W, uint64_t* __restrict__ kout,
                     uint32_t* __restrict__ vout, unsigned* tile_counter, unsigned long long* status, int64_t ntiles,
                     unsigned long long* n_items) {
   __shared__ unsigned s_tile;
@@ -205,17 +205,21 @@ compact_keys_kernel(const uint64_t* __restrict__ kin, int64_t n, uint64_t* __res
     if (t >= ntiles) break;
     // warp w owns items [tile + w*512, +512), round r covers 32 consecutive items
     const int64_t base = (int64_t)t * CT_TILE + (int64_t)warp * (CT_TILE / 8);
-    uint64_t k[CT_ITEMS], pk[CT_ITEMS];
+    // drop a pixel whose key equals its left (p-1) or upper (p-W) neighbour's: any
+    // earlier pixel of the same voxel may stand in, so the lowest pixel id of
+    // every voxel always survives
+    uint64_t k[CT_ITEMS], pk[CT_ITEMS], uk[CT_ITEMS];
 #pragma unroll
     for (int r = 0; r < CT_ITEMS; r++) {
       const int64_t i = base + r * 32 + lane;
       k[r] = i < n ? __ldg(kin + i) : KEY_INVALID;
       pk[r] = (i > 0 && i <= n) ? __ldg(kin + i - 1) : KEY_INVALID;
+      uk[r] = (i >= W && i - W < n) ? __ldg(kin + i - W) : KEY_INVALID;
     }
     uint32_t keep = 0, roff[CT_ITEMS], wsum = 0;
 #pragma unroll
     for (int r = 0; r < CT_ITEMS; r++) {
-      const bool kp = k[r] != KEY_INVALID && k[r] != pk[r];
+      const bool kp = k[r] != KEY_INVALID && k[r] != pk[r] && k[r] != uk[r];
       const unsigned b = __ballot_sync(FULL, kp);
       roff[r] = wsum + __popc(b & ((1u << lane) - 1u));
       wsum += __popc(b);
@@ -846,7 +850,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
       cudaMemsetAsync(tile_counter, 0, 4, s);
       cudaMemsetAsync(lb_status, 0, sizeof(unsigned long long) * ntiles, s);
       compact_keys_kernel<<<grid_blocks(ntiles * CT_THREADS, CT_THREADS, sms), CT_THREADS, 0, s>>>(
-          k1, npix, k0, v0, tile_counter, lb_status, ntiles, cnts + 2); count_launches(1);
+          k1, npix, in.W, k0, v0, tile_counter, lb_status, ntiles, cnts + 2); count_launches(1);
     }
   }
   int hb[8];

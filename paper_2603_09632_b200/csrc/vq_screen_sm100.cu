@@ -39,13 +39,14 @@ constexpr int EPI_THREADS = EPI_WARPS * 32;
 constexpr int THREADS = 64 + EPI_THREADS;     // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2..9 epilogue
 constexpr int HALF = BN / 2;                  // columns per epilogue warp per chunk
 constexpr int CONST_BYTES = 2 * BN * 4;
+template <int CAP>
 struct HalfState {                            // column-half 1 -> half 0 hand-off at tile end
   float U;
   float dropped;
-  int ck[kCandCap];
-  float cl[kCandCap];
+  int ck[CAP];
+  float cl[CAP];
 };
-constexpr int MERGE_BYTES = BM * (int)sizeof(HalfState);
+constexpr int MERGE_BYTES = BM * (int)sizeof(HalfState<kCandCap>);
 constexpr int BAR_BYTES = (2 * STAGES + 4) * 8 + 16;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + CONST_BYTES + MERGE_BYTES + BAR_BYTES;
 // kind::f16 instruction descriptor: D=f32, A=B=f16 (format 0), both K-major,
@@ -162,24 +163,25 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"
 // registers (static indices only), plus the smallest s ever pushed out.  At
 // the end the candidates are {k : s_k <= U + band}; if a pushed-out value also
 // satisfies that, the list overflowed and the row is rescanned exactly.
+template <int CAP>
 struct Cands {
   float U;        // min_k s_k seen so far
   float dropped;  // min lo among entries evicted from the full list
-  float L[kCandCap];
-  int Kx[kCandCap];
+  float L[CAP];
+  int Kx[CAP];
 
   __device__ __forceinline__ void init() {
     U = __int_as_float(0x7f800000);
     dropped = U;
 #pragma unroll
-    for (int j = 0; j < kCandCap; j++) {
+    for (int j = 0; j < CAP; j++) {
       L[j] = U;
       Kx[j] = -1;
     }
   }
   __device__ __forceinline__ void insert(float lo, int k) {
 #pragma unroll
-    for (int j = 0; j < kCandCap; j++) {
+    for (int j = 0; j < CAP; j++) {
       const bool sw = lo < L[j];
       const float tl = L[j];
       const int tk = Kx[j];
@@ -196,8 +198,9 @@ struct Cands {
 // (B_row >= B_k for every k) the candidate test is s_k <= min_j s_j + band,
 // band = 2 * B_row: the fast path is one FFMA + one FMNMX per element; only
 // blocks holding an element inside the band take the insertion path.
+template <int CAP>
 __device__ __forceinline__ void screen_block(const uint32_t (&r)[32], const float* __restrict__ cn, float xf,
-                                            float band, int kbase, Cands& st) {
+                                            float band, int kbase, Cands<CAP>& st) {
   float sv[32];
   float m0 = __int_as_float(0x7f800000), m1 = m0, m2 = m0, m3 = m0;
 #pragma unroll
@@ -231,6 +234,7 @@ __device__ __forceinline__ void screen_block(const uint32_t (&r)[32], const floa
   }
 }
 
+template <int CAP>
 __global__ void __launch_bounds__(THREADS, 1)
 screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               ScreenParams p) {
@@ -319,7 +323,7 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const int et = threadIdx.x - 64;
     const int rl = q * 32 + lane;            // row within the tile
     const unsigned lt = (1u << lane) - 1u;
-    HalfState* merge = reinterpret_cast<HalfState*>(smem + STAGES * STAGE_BYTES + CONST_BYTES);
+    HalfState<CAP>* merge = reinterpret_cast<HalfState<CAP>*>(smem + STAGES * STAGE_BYTES + CONST_BYTES);
     int acc = 0;
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < p.num_m_tiles; tile += gridDim.x) {
@@ -327,7 +331,7 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       const bool live = row < p.n;
       const float band = live ? p.xband[row] : 0.f;
       const float xf = live ? p.xf[row] : 0.f;   // -2 / (row scale * codebook scale)
-      Cands st;
+      Cands<CAP> st;
       st.init();
       for (int nc = 0; nc < p.num_n_chunks; nc++) {
         float* cc = cconst + acc * BN;
@@ -357,31 +361,31 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       }
       // ---- merge the two column halves, finalize the row ----
       if (half == 1) {
-        HalfState& hs = merge[rl];
+        HalfState<CAP>& hs = merge[rl];
         hs.U = st.U;
         hs.dropped = st.dropped;
 #pragma unroll
-        for (int j = 0; j < kCandCap; j++) {
+        for (int j = 0; j < CAP; j++) {
           hs.ck[j] = st.Kx[j];
           hs.cl[j] = st.L[j];
         }
       }
       epi_bar();
       if (half == 0) {
-        const HalfState& hs = merge[rl];
+        const HalfState<CAP>& hs = merge[rl];
         const float thr = fminf(st.U, hs.U) + band;
         bool ovf = st.dropped <= thr || hs.dropped <= thr;
         int nk = 0, kbest = -1;
-        int fin[kCandCap];
+        int fin[CAP];
 #pragma unroll
-        for (int j = 0; j < kCandCap; j++)
+        for (int j = 0; j < CAP; j++)
           if (st.Kx[j] >= 0 && st.L[j] <= thr) {
             fin[nk++] = st.Kx[j];
             kbest = st.Kx[j];
           }
-        for (int j = 0; j < kCandCap && !ovf; j++)
+        for (int j = 0; j < CAP && !ovf; j++)
           if (hs.ck[j] >= 0 && hs.cl[j] <= thr) {
-            if (nk == kCandCap) {
+            if (nk == CAP) {
               ovf = true;
               break;
             }
@@ -401,7 +405,7 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             RerankEntry* e = p.rq + base + __popc(m & lt);
             e->row = (int32_t)row;
             e->cnt = nk;
-            for (int j = 0; j < kCandCap; j++) e->cand[j] = j < nk ? fin[j] : 0;
+            for (int j = 0; j < CAP; j++) e->cand[j] = j < nk ? fin[j] : 0;
           }
         }
         m = __ballot_sync(FULL, to_fallback);
@@ -642,18 +646,21 @@ cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* h
   p.rq_count = cnt;
   p.fq = fq;
   p.fq_count = cnt + 1;
-  static bool attr = false;
-  if (!attr) {
-    if ((e = cudaFuncSetAttribute(screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) !=
-        cudaSuccess)
+  // candidate capacity: 8 keeps the C2-sized epilogue lean; large codebooks
+  // (more near-ties) use the full RerankEntry capacity of 16
+  const bool big = a.k >= 2048;
+  auto kern = big ? screen_kernel<kCandCap> : screen_kernel<8>;
+  static bool attr[2] = {false, false};
+  if (!attr[big]) {
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
       return e;
-    attr = true;
+    attr[big] = true;
   }
   int grid = p.num_m_tiles < a.sm_count ? p.num_m_tiles : a.sm_count;
   if (grid < 1) grid = 1;
   {
     ProfScope prof("vq_screen", s);
-    screen_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, p); count_launches(1);
+    kern<<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, p); count_launches(1);
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
