@@ -37,3 +37,59 @@ def test_workspace_queries_without_gpu():
     L = _native.lib()
     assert L.xgs_vq_assign_workspace(1 << 20, 1024, 512, 0, 512) > (1 << 20) * 512 * 2
     assert L.xgs_vq_accumulate_workspace(1000, 16) > 4000
+
+
+def test_error_codes_map_to_reference_exceptions():
+    """Argument validation happens before any CUDA call, so the status codes
+    and the InvalidInputError / InvalidStateError mapping are checkable here."""
+    import ctypes
+
+    import pytest
+
+    from paper_2603_09632_b200 import _native as nat
+    from paper_2603_09632_b200.errors import InvalidInputError, InvalidStateError
+    L = nat.lib()
+    dummy = ctypes.c_void_p(16)
+    # K == 0 -> invalid state (vq.py:85-86)
+    rc = L.xgs_vq_assign(dummy, 0, 4, 3, 3, dummy, 0, dummy, dummy, 1 << 30, None, None)
+    assert rc == 2 and b"empty codebook" in L.xgs_last_error()
+    with pytest.raises(InvalidStateError):
+        nat.check(rc)
+    # bad dtype / shape / ldx < d -> invalid input
+    assert L.xgs_vq_assign(dummy, 7, 4, 3, 3, dummy, 5, dummy, dummy, 1 << 30, None, None) == 1
+    assert L.xgs_vq_assign(dummy, 0, 4, 3, 2, dummy, 5, dummy, dummy, 1 << 30, None, None) == 1
+    with pytest.raises(InvalidInputError):
+        nat.check(1)
+    # workspace too small
+    assert L.xgs_vq_assign(dummy, 0, 4, 3, 3, dummy, 5, dummy, dummy, 16, None, None) == 1
+    # EMA decay outside [0, 1) (core.py:223-224)
+    assert L.xgs_vq_ema(1.0, 1e-5, 2, 2, dummy, dummy, dummy, dummy, dummy, dummy, dummy, None) == 1
+    # ring write larger than the capacity
+    assert L.xgs_vq_ring_write(dummy, 0, 3, 0, 10, 3, dummy, 4, 0, None) == 1
+    # grid: non-positive voxel / bad mode
+    fr = nat.GridFrames(1, 4, 4, 16, None, 16, 16, 1.0, 1.0, 0.0, 0.0, 0.0, 1, 0, 1e-3, None, 0, 0, 0)
+    res = nat.GridResult(16, 16, 16, 16, 16, 16, 16, None, 16, 0, 0, 0)
+    assert L.xgs_grid_sample(ctypes.byref(fr), dummy, ctypes.byref(res), dummy, 1 << 30, None) == 1
+    fr.voxel, fr.mode = 0.1, 3
+    assert L.xgs_grid_sample(ctypes.byref(fr), dummy, ctypes.byref(res), dummy, 1 << 30, None) == 1
+
+
+def test_python_api_validation_without_gpu():
+    import numpy as np
+    import pytest
+
+    import paper_2603_09632_b200 as xv
+    with pytest.raises(xv.InvalidInputError):
+        xv.VqConfig(lam=1.0)
+    with pytest.raises(xv.InvalidInputError):
+        xv.VqConfig(gamma=0.0)
+    with pytest.raises(xv.InvalidInputError):
+        xv.VqConfig(K=0)
+    with pytest.raises(xv.InvalidInputError):
+        xv.Codebook(E=np.zeros((3, 2)), N=np.zeros(2), M=np.zeros((3, 2)), lam=0.5, epsilon=1e-5)
+    with pytest.raises(xv.InvalidInputError):
+        xv.Codebook(E=np.zeros((2, 2)), N=-np.ones(2), M=np.zeros((2, 2)), lam=0.5, epsilon=1e-5)
+    with pytest.raises(xv.InvalidInputError):
+        xv.FeatureReservoir(0, 3)
+    with pytest.raises(xv.InvalidInputError):
+        xv.CameraPose(np.diag([1.0, 1.0, -1.0]), np.zeros(3))

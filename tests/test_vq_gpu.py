@@ -276,3 +276,38 @@ def test_online_step_device_matches_oracle(xv):
         assert np.array_equal(c.N, oc.N) and np.array_equal(c.M, oc.M) and np.array_equal(c.E, oc.E), i
         assert res.revived == rev
     assert np.array_equal(cb.reservoir.as_array(), oc.reservoir.buf)
+
+
+def test_assign_edge_cases(xv):
+    rng = np.random.default_rng(11)
+    # single row, single code, D = 1
+    cb = make_cb(xv, [[0.5]])
+    assert xv.assign_batch(np.array([[3.0]]), cb).tolist() == [0]
+    # all-identical codebook (Codebook.zeros): every row ties -> lowest index 0 (overflow path)
+    cb = xv.Codebook.zeros(40, 16)
+    x = rng.normal(size=(300, 16))
+    codes, (nr, nf) = xv.vq.assign_batch_stats(x, cb)
+    assert (codes == 0).all() and nf == 300
+    # extreme magnitudes: power-of-two scaling keeps the fp16 screen exact enough
+    E = rng.normal(size=(50, 24))
+    for scale in (1e-30, 1e-8, 1.0, 1e8, 1e30):
+        xs = rng.normal(size=(200, 24)) * scale
+        cbs = make_cb(xv, E * scale)
+        assert np.array_equal(xv.assign_batch(xs, cbs), on.assign(xs, E * scale)), scale
+    # zero rows and rows equal to codewords
+    xs = np.concatenate([np.zeros((3, 24)), E[[7, 7, 49]]])
+    assert np.array_equal(xv.assign_batch(xs, make_cb(xv, E)), on.assign(xs, E))
+
+
+def test_float64_and_strided_inputs(xv):
+    import torch
+    rng = np.random.default_rng(12)
+    E = rng.normal(size=(300, 40))
+    x = rng.normal(size=(1000, 80))[:, ::2]          # non-contiguous float64 view
+    assert np.array_equal(xv.assign_batch(x, make_cb(xv, E)), on.assign(np.ascontiguousarray(x), E))
+    xt = torch.from_numpy(rng.normal(size=(1000, 48)).astype(np.float32)).cuda()[:, :40]   # ldx = 48
+    got = xv.assign_batch(xt, make_cb(xv, E).to_device()).cpu().numpy()
+    assert np.array_equal(got, on.assign(xt.cpu().numpy(), E))
+    st = xv.accumulate(xt, make_cb(xv, E).to_device())
+    c, s = on.accumulate(xt.cpu().numpy(), got, 300)
+    assert np.array_equal(st.counts.cpu().numpy(), c) and np.array_equal(st.sums.cpu().numpy(), s)
