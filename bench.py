@@ -152,7 +152,7 @@ def run_grid(torch, steps, cpu=True):
         pts = rng.uniform(-4.0, 4.0, (GRID_MAP, 3))
         q = np.floor(pts / voxel).astype(np.int64)
         warm = torch.from_numpy(pack_key(q[:, 0], q[:, 1], q[:, 2]).view(np.int64)).cuda()
-        times, n_new, n_valid, map_size = [], 0, 0, 0
+        times, n_new, n_valid, map_size, n_sorted, passes = [], 0, 0, 0, 0, 0
         for it in range(steps + 1):
             hs = VoxelHashSet(GRID_MAP + GRID_F * GRID_H * GRID_W)
             hs.insert(warm)
@@ -168,15 +168,29 @@ def run_grid(torch, steps, cpu=True):
             torch.cuda.synchronize()
             if it > 0:
                 times.append(e0.elapsed_time(e1))
-            n_new, n_valid = len(r), r.n_valid
+            n_new, n_valid, n_sorted, passes = len(r), r.n_valid, r.n_sorted, r.sort_passes
             hs.close()
         prof = {t: nat.profile_read(t)[0] for t in ("grid_keys", "grid_sort", "grid_select", "grid_emit")}
         nat.profile_enable(False)
         ms = float(np.median(times))
         npix = GRID_F * GRID_H * GRID_W
+        pk_, _ = peaks()
+        # sort: per 8-bit pass the upsweep reads the keys (8 B) and the downsweep reads
+        # and writes key + pixel id (12 + 12 B) -> 32 B per item per pass
+        sort_bytes = 32.0 * n_sorted * passes
+        sort_gbs = sort_bytes / (prof["grid_sort"] * 1e-3) / 1e9 if prof["grid_sort"] else None
+        # keys + compaction: depth read 4 B + key write 8 B per pixel, compaction reads the
+        # key 3x (self, left, up; L2 for the neighbours) and writes 12 B per surviving item
+        keys_bytes = 12.0 * npix + 8.0 * npix + 12.0 * n_sorted
         out[str(voxel)] = {"Mpts_per_s": npix / (ms * 1e-3) / 1e6, "ms_per_batch": ms, "pixels": npix,
                            "valid_points": n_valid, "new_voxels": n_new, "map_voxels_before": map_size,
-                           "per_kernel_ms": prof}
+                           "sorted_items": n_sorted, "sort_passes": passes, "per_kernel_ms": prof,
+                           "roofline": {"bound": "hbm", "kernel": "radix sort (upsweep + stable downsweep)",
+                                        "achieved": sort_gbs, "peak": pk_["hbm_gbs"], "unit": "GB/s",
+                                        "frac": sort_gbs / pk_["hbm_gbs"] if sort_gbs else None,
+                                        "algorithmic_bytes": sort_bytes},
+                           "keys_compaction_GBps": keys_bytes / (prof["grid_keys"] * 1e-3) / 1e9
+                           if prof["grid_keys"] else None}
     if cpu:
         from oracle import grid as og
         t0 = time.perf_counter()
@@ -482,6 +496,12 @@ def main():
 
     pk, pk_kind = peaks()
     scr_ms, scr_n = prof["vq_screen"]
+    traffic = None
+    try:   # DRAM bytes of screen_kernel from the committed `ncu --set full` capture
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get("screen_kernel_C2")
+    except (OSError, ValueError):
+        pass
     flops = 2.0 * N_ROWS * K * D
     achieved = flops / (scr_ms / max(1, scr_n) * 1e-3) / 1e12 if scr_n else None
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
@@ -516,7 +536,7 @@ def main():
             "gpu_launches": launches,
             "roofline": {"bound": "tensor", "kernel": "screen_kernel (tcgen05 kind::f16)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "peak_kind": f"{pk_kind} bf16 dense sustained (f16 rate == bf16 rate)",
                          "algorithmic_flops_per_launch": flops},
             "per_kernel": per_kernel,

@@ -157,6 +157,7 @@ typedef struct {
   float* feat;             /* [cap,C] or NULL */
   double* count;           /* [cap] points averaged (mode 1) or 1, nullable */
   int64_t n_new, n_valid, n_voxels; /* written by the call */
+  int64_t n_sorted, sort_passes;     /* radix-sort work of the call (items, 8-bit passes) */
 } xgs_grid_result;
 
 XGS_API int xgs_grid_sample(const xgs_grid_frames* in, void* hashset, xgs_grid_result* out, void* ws,

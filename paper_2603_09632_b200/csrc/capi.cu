@@ -364,6 +364,8 @@ int xgs_grid_sample(const xgs_grid_frames* in, void* hashset, xgs_grid_result* o
   out->n_new = go.n_new;
   out->n_valid = go.n_valid;
   out->n_voxels = go.n_voxels;
+  out->n_sorted = go.n_sorted;
+  out->sort_passes = go.sort_passes;
   if (e == cudaErrorInvalidValue && go.n_new > go.capacity) return fail(INVALID_INPUT, "output capacity too small");
   if (e != cudaSuccess) return cuda_fail(e, "xgs_grid_sample");
   return OK;

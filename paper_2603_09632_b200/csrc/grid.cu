@@ -831,6 +831,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   int32_t* grand = reinterpret_cast<int32_t*>(b + w.off_misc + 128);
   unsigned long long* lb_status = reinterpret_cast<unsigned long long*>(b + w.off_lb);
   out.n_new = out.n_valid = out.n_voxels = 0;
+  out.n_sorted = out.sort_passes = 0;
   if (npix == 0) return cudaSuccess;
   cudaError_t e;
   const Cam cam{in.fx, in.fy, in.cx, in.cy, in.voxel, 1.0 / in.voxel};
@@ -881,6 +882,8 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   if ((e = sort_init()) != cudaSuccess) return e;
   const int64_t tiles = (nitems + SORT_TILE - 1) / SORT_TILE;
   if (nitems == 0) return cudaSuccess;
+  out.n_sorted = nitems;
+  out.sort_passes = (bits + 7) / 8;
   {
     ProfScope prof("grid_sort", s);
     for (int shift = 0; shift < bits; shift += 8) {

@@ -127,6 +127,7 @@ struct GridOut {
   float* feat;
   double* count;
   int64_t n_new, n_valid, n_voxels;
+  int64_t n_sorted, sort_passes;
 };
 cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, size_t ws_bytes, int sms,
                         cudaStream_t s);

@@ -96,6 +96,8 @@ class GridSampleResult:
     feature: Optional[object]
     n_valid: int
     n_voxels: int
+    n_sorted: int = 0        # items the radix sort moved (after first-pick compaction)
+    sort_passes: int = 0     # 8-bit LSD passes
 
     def __len__(self):
         return int(self.pid.shape[0])
@@ -104,7 +106,8 @@ class GridSampleResult:
         h = lambda t: None if t is None else t.cpu().numpy()
         return dict(key=h(self.key).view(np.uint64), pid=h(self.pid), mu=h(self.mu), color=h(self.color),
                     scale=h(self.scale), depth=h(self.depth), count=h(self.count), feature=h(self.feature),
-                    n_valid=self.n_valid, n_voxels=self.n_voxels)
+                    n_valid=self.n_valid, n_voxels=self.n_voxels, n_sorted=self.n_sorted,
+                    sort_passes=self.sort_passes)
 
 
 def _intr4(intr):
@@ -202,7 +205,7 @@ class GridSampler:
         res = nat.GridResult(cap, out["key"].data_ptr(), out["pid"].data_ptr(), out["mu"].data_ptr(),
                              out["color"].data_ptr(), out["scale"].data_ptr(), out["depth"].data_ptr(),
                              out["feature"].data_ptr() if feat is not None else None, out["count"].data_ptr(),
-                             0, 0, 0)
+                             0, 0, 0, 0, 0)
         ws = nat.workspace("grid", nat.lib().xgs_grid_workspace(F * H * W))
         nat.call("xgs_grid_sample", ctypes.byref(fr), self.occupied._h, ctypes.byref(res), nat.ptr(ws), ws.numel(),
                  nat.stream_ptr())
@@ -210,7 +213,8 @@ class GridSampler:
         return GridSampleResult(key=out["key"][:n], pid=out["pid"][:n], mu=out["mu"][:n], color=out["color"][:n],
                                 scale=out["scale"][:n], depth=out["depth"][:n], count=out["count"][:n],
                                 feature=out["feature"][:n] if feat is not None else None,
-                                n_valid=int(res.n_valid), n_voxels=int(res.n_voxels))
+                                n_valid=int(res.n_valid), n_voxels=int(res.n_voxels),
+                                n_sorted=int(res.n_sorted), sort_passes=int(res.sort_passes))
 
 
 def radix_sort_pairs(keys, vals, bits: int = 64):

@@ -68,7 +68,7 @@ def test_error_codes_map_to_reference_exceptions():
     assert L.xgs_vq_ring_write(dummy, 0, 3, 0, 10, 3, dummy, 4, 0, None) == 1
     # grid: non-positive voxel / bad mode
     fr = nat.GridFrames(1, 4, 4, 16, None, 16, 16, 1.0, 1.0, 0.0, 0.0, 0.0, 1, 0, 1e-3, None, 0, 0, 0)
-    res = nat.GridResult(16, 16, 16, 16, 16, 16, 16, None, 16, 0, 0, 0)
+    res = nat.GridResult(16, 16, 16, 16, 16, 16, 16, None, 16, 0, 0, 0, 0, 0)
     assert L.xgs_grid_sample(ctypes.byref(fr), dummy, ctypes.byref(res), dummy, 1 << 30, None) == 1
     fr.voxel, fr.mode = 0.1, 3
     assert L.xgs_grid_sample(ctypes.byref(fr), dummy, ctypes.byref(res), dummy, 1 << 30, None) == 1
