@@ -335,6 +335,45 @@ def run_c5(torch, iters, device):
             "workload": "C5 per-GPU shard (67,108,864 rows / 8 GPUs), one online_step per iteration"}
 
 
+def run_targets(torch, iters, cpu=True):
+    """grid-sampled supervision-target prefetch for one keyframe
+    (480x640, stride 4 -> all 16 offsets, D=512 fp32 feature map at 1/16
+    resolution), padded fp64 targets as the reference's SupervisionTarget."""
+    from paper_2603_09632_b200 import _native as nat
+    from paper_2603_09632_b200 import supervision as sup
+    H, W, s, D = 480, 640, 4, 512
+    g = torch.Generator(device="cuda")
+    g.manual_seed(50)
+    P = torch.randn(D, H // 16, W // 16, generator=g, device="cuda")
+    src = sup.ContinuousFeatureSource(P)
+    sup.prefetch_targets(src, H, W, s, range(16))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        G, V = sup.prefetch_targets(src, H, W, s, range(16))
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    nbytes = G.numel() * 8 + V.numel() * 8          # outputs dominate (the source is L2-resident)
+    pk, _ = peaks()
+    out = {"ms_per_keyframe": ms, "offsets": 16, "target_shape": list(G.shape), "GB_per_s": nbytes / (ms * 1e-3) / 1e9,
+           "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+           "workload": "480x640 keyframe, stride 4 (16 offsets), D=512 continuous source at 30x40, fp64 targets"}
+    del G, V
+    if cpu:
+        from oracle import supervision as osup
+        Ph = P.double().cpu().numpy()
+        t0 = time.perf_counter()
+        for k in range(16):
+            oh, ow = sup.next_offset(k, s, 0)
+            Gc, Vc = osup.target_continuous(Ph, H, W, s, oh, ow)
+            osup.pad(Gc, Vc, H, W, s)
+        out["cpu_baseline"] = {"ms_per_keyframe": (time.perf_counter() - t0) * 1e3, "cores": 1, "kind": "port",
+                               "sample": "the same 16 offsets through oracle/supervision.py (NumPy)"}
+    return out
+
+
 def cpu_port_rate(x_host, E, seconds=10.0, threads=None):
     """The reference's assign+accumulate restated in C (oracle/oracle.c), timed
     on host cores over row chunks until ~`seconds` elapse (bounded sample)."""
@@ -517,6 +556,9 @@ def main():
         grid = run_grid(torch, args.grid_steps, cpu=not args.no_cpu)
     if rank == 0 and world == 1 and args.stream_frames > 0:
         stream = run_stream(torch, args.stream_frames, device)
+    targets = None
+    if rank == 0 and world == 1 and not args.no_grid:
+        targets = run_targets(torch, 10, cpu=not args.no_cpu)
     c5 = None
     if rank == 0 and world == 1 and args.c5_iters > 0:
         del x
@@ -546,6 +588,7 @@ def main():
             "grid": grid,
             "stream": stream,
             "c5_shard": c5,
+            "targets": targets,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

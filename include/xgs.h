@@ -163,6 +163,25 @@ typedef struct {
 XGS_API int xgs_grid_sample(const xgs_grid_frames* in, void* hashset, xgs_grid_result* out, void* ws,
                             size_t ws_bytes, void* stream);
 
+/* ------------------------------------------- SUPERVISION */
+
+/* Grid-sampled supervision targets for n_off lattice offsets in one launch
+ * ("target prefetch"): build_target_continuous (supervision.py:138-147) when
+ * P != NULL (P: [D, Hf, Wf], dtype XGS_F32/XGS_F64), else
+ * build_target_discrete (supervision.py:118-130) from S [H, W] int64 region ids
+ * (-1 background) and Phi [R, D] fp64.  offs: [n_off, 2] int32 (o_h, o_w).
+ * G: [n_off, D, Hp, Wp] fp64, V: [n_off, Hp, Wp] fp64; cells beyond the
+ * offset's (H_s, W_s) are padding (pad_target, supervision.py:208-221).
+ * corrupt (device int, nullable) is set to 1 for region ids outside [-1, R). */
+XGS_API int xgs_sup_gather(const void* P, int p_dtype, int64_t Hf, int64_t Wf, const int64_t* S, const double* Phi,
+                           int64_t R, int64_t D, int64_t H, int64_t W, int64_t s, const int32_t* offs, int64_t n_off,
+                           int64_t Hp, int64_t Wp, double* G, double* V, int* corrupt, void* stream);
+
+/* masked_semantic_loss (supervision.py:150-184) on [D, cells] fp64 arrays:
+ * acc (device, 3 doubles) <- {sum(1-cos), sum(l1/D), n_valid}; cot <- dloss/dpred. */
+XGS_API int xgs_sup_loss(const double* pred, const double* G, const double* V, int64_t D, int64_t cells, double lam,
+                         double* acc, double* cot, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -371,4 +371,31 @@ int xgs_grid_sample(const xgs_grid_frames* in, void* hashset, xgs_grid_result* o
   return OK;
 }
 
+// ---------------------------------------------------------------- SUPERVISION
+
+int xgs_sup_gather(const void* P, int p_dtype, int64_t Hf, int64_t Wf, const int64_t* S, const double* Phi, int64_t R,
+                   int64_t D, int64_t H, int64_t W, int64_t s, const int32_t* offs, int64_t n_off, int64_t Hp,
+                   int64_t Wp, double* G, double* V, int* corrupt, void* stream) {
+  if (s < 1) return fail(INVALID_INPUT, "stride must be >= 1");
+  if (H < 1 || W < 1 || D < 0 || n_off < 0 || Hp < 0 || Wp < 0) return fail(INVALID_INPUT, "bad target shape");
+  if (P && (Hf < 1 || Wf < 1 || (p_dtype != F32 && p_dtype != F64)))
+    return fail(INVALID_INPUT, "feature source must be (D, H_f, W_f) with H_f, W_f >= 1");
+  if (!P && (!S || (R > 0 && !Phi))) return fail(INVALID_INPUT, "need a feature source or an annotation");
+  if (n_off > 65535) return fail(NOT_SUPPORTED, "more than 65535 offsets per call");
+  if (n_off > 0 && (!offs || !G)) return fail(INVALID_INPUT, "null buffer");
+  cudaError_t e = launch_sup_gather(P, p_dtype, Hf, Wf, S, Phi, R, D, H, W, s, offs, n_off, Hp, Wp, G, V, corrupt,
+                                    (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_sup_gather");
+  return OK;
+}
+
+int xgs_sup_loss(const double* pred, const double* G, const double* V, int64_t D, int64_t cells, double lam,
+                 double* acc, double* cot, void* stream) {
+  if (D < 1 || cells < 0) return fail(INVALID_INPUT, "prediction and target shapes disagree");
+  if (cells > 0 && (!pred || !G || !V || !acc || !cot)) return fail(INVALID_INPUT, "null buffer");
+  cudaError_t e = launch_sup_loss(pred, G, V, D, cells, lam, acc, cot, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_sup_loss");
+  return OK;
+}
+
 }  // extern "C"

@@ -134,4 +134,12 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
 cudaError_t radix_sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n, int bits, void* ws, size_t ws_bytes,
                              cudaStream_t s);
 
+// ---------------- supervision targets (supervision.cu) ----------------
+cudaError_t launch_sup_gather(const void* P, int p_dtype, int64_t Hf, int64_t Wf, const int64_t* S, const double* Phi,
+                              int64_t R, int64_t D, int64_t H, int64_t W, int64_t s, const int32_t* offs,
+                              int64_t n_off, int64_t Hp, int64_t Wp, double* G, double* V, int* corrupt,
+                              cudaStream_t st);
+cudaError_t launch_sup_loss(const double* pred, const double* G, const double* V, int64_t D, int64_t cells, double lam,
+                            double* acc, double* cot, cudaStream_t st);
+
 }  // namespace xgs

@@ -198,7 +198,39 @@ def gen_densify():
                         generation=np.array(out.generation))
 
 
+def gen_supervision():
+    """supervision.py:21-221 — lattice, continuous / discrete targets, loss + cotangent,
+    offset schedule, padding."""
+    from semsplat import supervision as sup
+    rng = np.random.default_rng(109)
+    out = {}
+    H, W = 37, 53
+    P = rng.normal(size=(6, 5, 7))
+    S = rng.integers(-1, 4, (H, W))
+    Phi = rng.normal(size=(4, 6))
+    src = sup.ContinuousFeatureSource(P)
+    ann = sup.RegionAnnotation(S, Phi)
+    out["P"], out["S"], out["Phi"] = P, S, Phi
+    cases = [(1, 0, 0), (2, 1, 0), (3, 2, 1), (4, 3, 3), (5, 0, 4)]
+    for i, (s_, oh, ow) in enumerate(cases):
+        g = sup.GridSpec(H, W, s_, oh, ow)
+        tc = sup.build_target_continuous(src, g)
+        td = sup.build_target_discrete(ann, g)
+        out[f"cont_G_{i}"], out[f"disc_G_{i}"], out[f"disc_V_{i}"] = tc.G_star, td.G_star, td.V
+        pt = sup.pad_target(td, g)
+        out[f"pad_G_{i}"], out[f"pad_V_{i}"] = pt.G_star, pt.V
+        pred = rng.normal(size=td.G_star.shape)
+        pred[:, 0, 0] = 0.0
+        loss, cot = sup.masked_semantic_loss(pred, td, lambda_sem=0.7)
+        out[f"pred_{i}"], out[f"loss_{i}"], out[f"cot_{i}"] = pred, np.array(loss), cot
+    out["cases"] = np.array(cases)
+    out["offsets"] = np.array([sup.next_offset(k, 4, 3) for k in range(40)])
+    out["offsets_s1"] = np.array([sup.next_offset(k, 1, 3) for k in range(3)])
+    np.savez_compressed(os.path.join(OUT, "supervision.npz"), **out)
+
+
 if __name__ == "__main__":
+    gen_supervision()
     gen_distances()
     gen_assign()
     gen_accumulate_ema()
