@@ -19,6 +19,10 @@
 //      2..8 are queued for the exact fp64 re-rank (rerank_kernel); rows whose
 //      list overflowed go to the exact all-codes kernel.
 // Codes are therefore bit-identical to the reference for every row.
+//
+// The GEMM runs on CTA pairs (cta_group::2, M256 N256 K16): each CTA stages its
+// own 128 rows and half of every 256-code chunk, and for D <= 512 the row tile
+// stays resident in smem across all chunks.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -30,13 +34,18 @@ namespace xgs {
 
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN * BK * 2;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int BM = 128;                       // rows per CTA; the CTA pair covers 256 rows
+constexpr int BN = 256;                       // codes per chunk (pair MMA N)
+constexpr int BNH = BN / 2;                   // codes per CTA's half of B
+constexpr int BK = 64;                        // fp16 elements per 128-byte swizzled row
+constexpr int A_SLOTS = 8;                    // A ring: the whole 128 x 512 row tile when D <= 512
+constexpr int B_STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;          // 16 KB
+constexpr int B_BYTES = BNH * BK * 2;         // 16 KB
 constexpr int EPI_WARPS = 8;                  // 2 per TMEM lane quadrant (column halves)
 constexpr int EPI_THREADS = EPI_WARPS * 32;
-constexpr int THREADS = 64 + EPI_THREADS;     // warp0 TMA, warp1 MMA (+TMEM alloc), warps 2..9 epilogue
+constexpr int EPI_WARP0 = 3;                  // warp0 A-TMA, warp1 MMA (+TMEM alloc), warp2 B-TMA
+constexpr int THREADS = EPI_WARP0 * 32 + EPI_THREADS;
 constexpr int HALF = BN / 2;                  // columns per epilogue warp per chunk
 constexpr int CONST_BYTES = 2 * BN * 4;
 template <int CAP>
@@ -47,15 +56,22 @@ struct HalfState {                            // column-half 1 -> half 0 hand-of
   float cl[CAP];
 };
 constexpr int MERGE_BYTES = BM * (int)sizeof(HalfState<kCandCap>);
-constexpr int BAR_BYTES = (2 * STAGES + 4) * 8 + 16;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + CONST_BYTES + MERGE_BYTES + BAR_BYTES;
+constexpr int NBARS = 2 * A_SLOTS + 2 * B_STAGES + 4;
+constexpr int BAR_BYTES = NBARS * 8 + 16;
+constexpr int OFF_B = A_SLOTS * A_BYTES;
+constexpr int OFF_CONST = OFF_B + B_STAGES * B_BYTES;
+constexpr int OFF_MERGE = OFF_CONST + CONST_BYTES;
+constexpr int OFF_BAR = OFF_MERGE + MERGE_BYTES;
+constexpr int SMEM_BYTES = OFF_BAR + BAR_BYTES;
+static_assert(SMEM_BYTES <= 227 * 1024, "screen smem budget");
 // kind::f16 instruction descriptor: D=f32, A=B=f16 (format 0), both K-major,
-// N=256, M=128.
-constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// N=256, M=256 (cta_group::2: 128 rows of A and 128 codes of B per CTA).
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 
 struct ScreenParams {
   int64_t n;
-  int num_m_tiles, num_n_chunks, num_k_blocks;
+  int num_pair_tiles, num_n_chunks, num_k_blocks;
+  int resident;         // A row tile stays in smem across the N chunks (num_k_blocks <= A_SLOTS)
   const float* xband;   // per row: 2 * max_k B_k + fp64-reference slack
   const float* xf;
   const float* cn;
@@ -68,6 +84,20 @@ struct ScreenParams {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cta address -> shared::cluster address of the same offset in CTA `rank`
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -87,19 +117,43 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(a, parity)) {
   }
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+// wait with cluster-scope acquire (arrivals come from the peer CTA's threads)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+// remote (or local) arrive by cluster address; TMEM reads are ordered before
+// it by tcgen05.fence::before_thread_sync, so the default .release.cta
+// semantics suffice (a .cluster release costs a MEMBAR.GPU per arrive)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+// pair TMA: the data lands in this CTA's smem, the transaction bytes are
+// counted on the leader CTA's barrier (cluster address)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
 }
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
@@ -109,15 +163,19 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   d |= (uint64_t)2 << 61;            // SWIZZLE_128B
   return d;
 }
-__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+__device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accum));
 }
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
+// completion of the issued MMAs arrives on the same-offset barrier of both CTAs
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
 }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -144,25 +202,13 @@ __device__ __forceinline__ void tmem_wait(uint32_t (&r)[32]) {
                :
                : "memory");
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory"); }
 
 // Per-row candidate state of one epilogue thread (one row, one column half):
-// the kCandCap smallest screen values s_k seen so far, kept sorted in
-// registers (static indices only), plus the smallest s ever pushed out.  At
-// the end the candidates are {k : s_k <= U + band}; if a pushed-out value also
-// satisfies that, the list overflowed and the row is rescanned exactly.
+// the CAP smallest screen values s_k seen so far, kept sorted in registers
+// (static indices only), plus the smallest s ever pushed out.  At the end the
+// candidates are {k : s_k <= U + band}; if a pushed-out value also satisfies
+// that, the list overflowed and the row is rescanned exactly.
 template <int CAP>
 struct Cands {
   float U;        // min_k s_k seen so far
@@ -234,106 +280,145 @@ __device__ __forceinline__ void screen_block(const uint32_t (&r)[32], const floa
   }
 }
 
+// One CTA pair (cluster of 2, same TPC) per 256-row tile, persistent over
+// tiles.  Each CTA owns 128 rows (TMEM lanes) and stages its own A rows plus
+// one half (128 codes) of every codebook chunk; the leader CTA issues
+// tcgen05.mma.cta_group::2 M256 N256 K16, so every codebook byte fetched from
+// L2 feeds 256 rows and, with D <= 512, the A tile is fetched once per tile
+// instead of once per chunk (L2 traffic per MMA cycle: 96 B/SM -> 32 B/SM).
 template <int CAP>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               ScreenParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  float* cconst = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + CONST_BYTES + MERGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  float* cconst = reinterpret_cast<float*>(smem + OFF_CONST);
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* emptyA = fullA + A_SLOTS;
+  uint64_t* fullB = emptyA + A_SLOTS;
+  uint64_t* emptyB = fullB + B_STAGES;
+  uint64_t* tfull = emptyB + B_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int nkb = p.num_k_blocks, nnc = p.num_n_chunks;
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < STAGES; i++) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+    for (int i = 0; i < A_SLOTS; i++) {
+      mbar_init(&fullA[i], 1);
+      mbar_init(&emptyA[i], 1);
+    }
+    for (int i = 0; i < B_STAGES; i++) {
+      mbar_init(&fullB[i], 1);
+      mbar_init(&emptyB[i], 1);
     }
     for (int i = 0; i < 2; i++) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], EPI_WARPS);
+      mbar_init(&tempty[i], 2 * EPI_WARPS);   // both CTAs' epilogue warps (leader's copy is the one used)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   tc_before();
-  __syncthreads();
+  cluster_sync();
   tc_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
+    // ---------------- A producer: this CTA's 128 rows ----------------
     if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.num_m_tiles; tile += gridDim.x)
-        for (int nc = 0; nc < p.num_n_chunks; nc++)
-          for (int kb = 0; kb < p.num_k_blocks; kb++) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            uint8_t* sa = smem + stage * STAGE_BYTES;
-            mbar_expect_tx(&full[stage], STAGE_BYTES);
-            tma_load_2d(sa, &tmA, kb * BK, tile * BM, &full[stage]);
-            tma_load_2d(sa + A_BYTES, &tmB, kb * BK, nc * BN, &full[stage]);
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
+      const uint32_t lead_full = mapa(smem_u32(fullA), 0);
+      uint32_t idx = 0;
+      const int nload = p.resident ? nkb : nkb * nnc;
+      for (int t = cluster; t < p.num_pair_tiles; t += nclusters) {
+        const int row0 = t * 2 * BM + (int)rank * BM;
+        const int tn = t + nclusters;
+        if (tn < p.num_pair_tiles)   // warm L2 with the next tile's rows
+          for (int kb = 0; kb < nkb; kb++) tma_prefetch_2d(&tmA, kb * BK, tn * 2 * BM + (int)rank * BM);
+        for (int j = 0; j < nload; j++, idx++) {
+          const int kb = j % nkb;
+          const uint32_t slot = idx % A_SLOTS, ph = (idx / A_SLOTS) & 1;
+          mbar_wait(&emptyA[slot], ph ^ 1);
+          if (leader) mbar_expect_tx(&fullA[slot], 2 * A_BYTES);
+          tma_load_2d_pair(smem + slot * A_BYTES, &tmA, kb * BK, row0, lead_full + slot * 8);
+        }
+      }
+    }
+  } else if (warp == 2) {
+    // ---------------- B producer: this CTA's half of each codebook chunk ----------------
+    if (lane == 0) {
+      const uint32_t lead_full = mapa(smem_u32(fullB), 0);
+      uint32_t idx = 0;
+      for (int t = cluster; t < p.num_pair_tiles; t += nclusters)
+        for (int nc = 0; nc < nnc; nc++)
+          for (int kb = 0; kb < nkb; kb++, idx++) {
+            const uint32_t st = idx % B_STAGES, ph = (idx / B_STAGES) & 1;
+            mbar_wait(&emptyB[st], ph ^ 1);
+            if (leader) mbar_expect_tx(&fullB[st], 2 * B_BYTES);
+            tma_load_2d_pair(smem + OFF_B + st * B_BYTES, &tmB, kb * BK, nc * BN + (int)rank * BNH,
+                             lead_full + st * 8);
           }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      int stage = 0, acc = 0;
-      uint32_t phase = 0, aphase = 0;
-      for (int tile = blockIdx.x; tile < p.num_m_tiles; tile += gridDim.x)
-        for (int nc = 0; nc < p.num_n_chunks; nc++) {
-          mbar_wait(&tempty[acc], aphase ^ 1);
+    // ---------------- MMA issuer (leader CTA only) ----------------
+    if (leader && lane == 0) {
+      uint32_t abase = 0, bidx = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int t = cluster; t < p.num_pair_tiles; t += nclusters) {
+        for (int nc = 0; nc < nnc; nc++) {
+          mbar_wait_cluster(&tempty[acc], aphase ^ 1);
           tc_after();
           const uint32_t dt = tmem_base + (uint32_t)(acc * BN);
-          for (int kb = 0; kb < p.num_k_blocks; kb++) {
-            mbar_wait(&full[stage], phase);
+          for (int kb = 0; kb < nkb; kb++, bidx++) {
+            const uint32_t ai = abase + (uint32_t)(p.resident ? kb : nc * nkb + kb);
+            const uint32_t aslot = ai % A_SLOTS;
+            const uint32_t bst = bidx % B_STAGES;
+            mbar_wait(&fullA[aslot], (ai / A_SLOTS) & 1);
+            mbar_wait(&fullB[bst], (bidx / B_STAGES) & 1);
             tc_after();
-            const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
-            const uint32_t sb = sa + A_BYTES;
+            const uint32_t sa = smem_u32(smem + aslot * A_BYTES);
+            const uint32_t sb = smem_u32(smem + OFF_B + bst * B_BYTES);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; kk++)
-              mma_f16(dt, sw128_desc(sa + kk * 32), sw128_desc(sb + kk * 32), (kb | kk) != 0);
-            umma_commit(&empty[stage]);
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
+              mma_f16_pair(dt, sw128_desc(sa + kk * 32), sw128_desc(sb + kk * 32), (kb | kk) != 0);
+            umma_commit_pair(&emptyB[bst]);
+            if (!p.resident || nc == nnc - 1) umma_commit_pair(&emptyA[aslot]);
           }
-          umma_commit(&tfull[acc]);
+          umma_commit_pair(&tfull[acc]);
           acc ^= 1;
           if (acc == 0) aphase ^= 1;
         }
+        abase += (uint32_t)(p.resident ? nkb : nkb * nnc);
+      }
     }
   } else {
     // ---------------- epilogue: one thread per (tile row, column half) ----------------
-    const int ew = warp - 2;                 // 0..7
+    const int ew = warp - EPI_WARP0;         // 0..7
     const int q = warp & 3;                  // TMEM lane quadrant this warp may access
     const int half = ew >> 2;                // column half of every chunk
-    const int et = threadIdx.x - 64;
-    const int rl = q * 32 + lane;            // row within the tile
+    const int et = threadIdx.x - EPI_WARP0 * 32;
+    const int rl = q * 32 + lane;            // row within this CTA's 128 rows
     const unsigned lt = (1u << lane) - 1u;
-    HalfState<CAP>* merge = reinterpret_cast<HalfState<CAP>*>(smem + STAGES * STAGE_BYTES + CONST_BYTES);
+    const uint32_t lead_tempty = mapa(smem_u32(tempty), 0);
+    HalfState<CAP>* merge = reinterpret_cast<HalfState<CAP>*>(smem + OFF_MERGE);
     int acc = 0;
     uint32_t aphase = 0;
-    for (int tile = blockIdx.x; tile < p.num_m_tiles; tile += gridDim.x) {
-      const int64_t row = (int64_t)tile * BM + rl;
+    for (int t = cluster; t < p.num_pair_tiles; t += nclusters) {
+      const int64_t row = (int64_t)t * 2 * BM + (int64_t)rank * BM + rl;
       const bool live = row < p.n;
       const float band = live ? p.xband[row] : 0.f;
       const float xf = live ? p.xf[row] : 0.f;   // -2 / (row scale * codebook scale)
       Cands<CAP> st;
       st.init();
-      for (int nc = 0; nc < p.num_n_chunks; nc++) {
+      for (int nc = 0; nc < nnc; nc++) {
         float* cc = cconst + acc * BN;
         for (int i = et; i < BN; i += EPI_THREADS) cc[i] = p.cn[nc * BN + i];
         epi_bar();
@@ -355,7 +440,7 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
         tc_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) mbar_arrive_cluster(lead_tempty + acc * 8);
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
       }
@@ -397,10 +482,10 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (live && !to_fallback && nk == 1) p.codes[row] = kbest;
         unsigned m = __ballot_sync(FULL, to_rerank);
         if (m) {
-          const int leader = __ffs(m) - 1;
+          const int leader_lane = __ffs(m) - 1;
           int base = 0;
-          if (lane == leader) base = atomicAdd(p.rq_count, __popc(m));
-          base = __shfl_sync(FULL, base, leader);
+          if (lane == leader_lane) base = atomicAdd(p.rq_count, __popc(m));
+          base = __shfl_sync(FULL, base, leader_lane);
           if (to_rerank) {
             RerankEntry* e = p.rq + base + __popc(m & lt);
             e->row = (int32_t)row;
@@ -410,10 +495,10 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
         m = __ballot_sync(FULL, to_fallback);
         if (m) {
-          const int leader = __ffs(m) - 1;
+          const int leader_lane = __ffs(m) - 1;
           int base = 0;
-          if (lane == leader) base = atomicAdd(p.fq_count, __popc(m));
-          base = __shfl_sync(FULL, base, leader);
+          if (lane == leader_lane) base = atomicAdd(p.fq_count, __popc(m));
+          base = __shfl_sync(FULL, base, leader_lane);
           if (to_fallback) p.fq[base + __popc(m & lt)] = (int32_t)row;
         }
       }
@@ -421,9 +506,9 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     }
   }
   tc_before();
-  __syncthreads();
+  cluster_sync();
   tc_after();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
 }
 
 // ---- operand preparation ----
@@ -630,14 +715,15 @@ cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* h
 
   CUtensorMap tmA, tmB;
   if (!make_map(&tmA, Ab, (uint64_t)w.dp, (uint64_t)a.n, (uint64_t)w.dp * 2, BK, BM) ||
-      !make_map(&tmB, Eb, (uint64_t)w.dp, (uint64_t)w.kp, (uint64_t)w.dp * 2, BK, BN))
+      !make_map(&tmB, Eb, (uint64_t)w.dp, (uint64_t)w.kp, (uint64_t)w.dp * 2, BK, BNH))
     return cudaErrorInvalidValue;
 
   ScreenParams p;
   p.n = a.n;
-  p.num_m_tiles = (int)((a.n + BM - 1) / BM);
+  p.num_pair_tiles = (int)((a.n + 2 * BM - 1) / (2 * BM));
   p.num_n_chunks = (int)(w.kp / BN);
   p.num_k_blocks = (int)(w.dp / BK);
+  p.resident = p.num_k_blocks <= A_SLOTS;
   p.xband = xn;
   p.xf = xf;
   p.cn = cn;
@@ -656,8 +742,11 @@ cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* h
       return e;
     attr[big] = true;
   }
-  int grid = p.num_m_tiles < a.sm_count ? p.num_m_tiles : a.sm_count;
-  if (grid < 1) grid = 1;
+  // one CTA pair per TPC, persistent over 256-row tiles
+  int clusters = a.sm_count / 2;
+  if (clusters > p.num_pair_tiles) clusters = p.num_pair_tiles;
+  if (clusters < 1) clusters = 1;
+  const int grid = 2 * clusters;
   {
     ProfScope prof("vq_screen", s);
     kern<<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, p); count_launches(1);
