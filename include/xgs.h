@@ -50,6 +50,8 @@ XGS_API long long xgs_launch_count(void);
  * "vq_chain", "vq_ema", "grid_*"); enable(1) clears, read() synchronises. */
 XGS_API int xgs_profile_enable(int on);
 XGS_API int xgs_profile_read(const char* tag, double* total_ms, long long* count);
+/* CSV "tag,start_ms,end_ms" of every profiled launch, relative to the earliest */
+XGS_API int xgs_profile_dump(const char* path);
 
 /* ------------------------------------------------------------------ VQ */
 
@@ -79,6 +81,19 @@ XGS_API size_t xgs_vq_accumulate_workspace(int64_t n, int64_t k);
 XGS_API int xgs_vq_accumulate(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const int64_t* codes,
                               const uint8_t* mask, int64_t k, double* counts, double* sums, void* ws,
                               size_t ws_bytes, void* stream);
+
+/* assign_batch + accumulate of one online_step (vq.py:193-212, the
+ * accumulate(batch[mask]) at :206 when the confidence mask is all-true):
+ * codes, counts and sums bit-identical to xgs_vq_assign followed by
+ * xgs_vq_accumulate (mask NULL).  Rows are processed in chunks whose operand
+ * prep, screening GEMM and accumulate chains overlap on internal streams;
+ * the fp64 chains continue across chunks in row order, so the sums keep the
+ * np.add.at order.  Completion is ordered on `stream`.  stats_out as for
+ * xgs_vq_assign.  The enqueue is serialised by an internal lock. */
+XGS_API size_t xgs_vq_step_workspace(int64_t n, int64_t k, int64_t d, int dtype, int64_t ldx);
+XGS_API int xgs_vq_assign_accumulate(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E,
+                                     int64_t k, int64_t* codes, double* counts, double* sums, void* ws,
+                                     size_t ws_bytes, int32_t* stats_out, void* stream);
 
 /* ema_step (vq.py:103-109): N' = lam N + (1-lam) c ; M' = lam M + (1-lam) s ;
  * E' = M' / (N' + eps).  Outputs may alias inputs. */

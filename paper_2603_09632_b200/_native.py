@@ -32,10 +32,14 @@ SIGNATURES = {
     "xgs_launch_count": (ctypes.c_longlong, []),
     "xgs_profile_enable": (_i32, [_i32]),
     "xgs_profile_read": (_i32, [ctypes.c_char_p, _vp, _vp]),
+    "xgs_profile_dump": (_i32, [ctypes.c_char_p]),
     "xgs_vq_assign_workspace": (_sz, [_i64, _i64, _i64, _i32, _i64]),
     "xgs_vq_assign": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _sz, _vp, _vp]),
     "xgs_vq_exact": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _i32, _f64, _f64, _vp, _vp, _vp, _vp,
                             _vp]),
+    "xgs_vq_step_workspace": (_sz, [_i64, _i64, _i64, _i32, _i64]),
+    "xgs_vq_assign_accumulate": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp,
+                                        _vp]),
     "xgs_vq_accumulate_workspace": (_sz, [_i64, _i64]),
     "xgs_vq_accumulate": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "xgs_vq_ema": (_i32, [_f64, _f64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

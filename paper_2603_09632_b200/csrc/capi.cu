@@ -91,6 +91,39 @@ int xgs_profile_enable(int on) {
   return OK;
 }
 
+// Timeline of every profiled launch, "tag,start_ms,end_ms" relative to the
+// earliest recorded event (streams overlap: this is how the row-chunk
+// pipeline's concurrency is inspected).  Synchronises.
+int xgs_profile_dump(const char* path) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  FILE* f = std::fopen(path, "w");
+  if (!f) return fail(INVALID_INPUT, "cannot open profile dump path");
+  cudaEvent_t base = nullptr;
+  float best = 0.f;
+  for (auto& kv : g_prof)
+    for (auto& pr : kv.second) {
+      if (cudaEventSynchronize(pr.second) != cudaSuccess) {
+        std::fclose(f);
+        return cuda_fail(cudaGetLastError(), "profile");
+      }
+      float ms = 0.f;
+      if (!base || (cudaEventElapsedTime(&ms, base, pr.first) == cudaSuccess && ms < best)) {
+        base = pr.first;
+        best = 0.f;
+      }
+    }
+  std::fprintf(f, "tag,start_ms,end_ms\n");
+  for (auto& kv : g_prof)
+    for (auto& pr : kv.second) {
+      float a = 0.f, b = 0.f;
+      cudaEventElapsedTime(&a, base, pr.first);
+      cudaEventElapsedTime(&b, base, pr.second);
+      std::fprintf(f, "%s,%.4f,%.4f\n", kv.first.c_str(), a, b);
+    }
+  std::fclose(f);
+  return OK;
+}
+
 int xgs_profile_read(const char* tag, double* total_ms, long long* count) {
   std::lock_guard<std::mutex> g(g_prof_mu);
   double tot = 0.0;
@@ -115,22 +148,14 @@ size_t xgs_vq_assign_workspace(int64_t n, int64_t k, int64_t d, int dtype, int64
   return screen_workspace_bytes(n, k, d, dtype, ldx);
 }
 
-int xgs_vq_assign(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E, int64_t k,
-                  int64_t* codes, void* ws, size_t ws_bytes, int32_t* stats_out, void* stream) {
-  int rc = check_rows(x, dtype, n, d, ldx);
-  if (rc) return rc;
-  if (k == 0) return fail(INVALID_STATE, "cannot assign against an empty codebook");
-  if (k < 0 || !E || (n > 0 && !codes)) return fail(INVALID_INPUT, "bad codebook or output");
-  if (n > 0x7fffffff) return fail(NOT_SUPPORTED, "more than 2^31-1 rows per call");
-  if (n == 0) return OK;
-  if (ws_bytes < screen_workspace_bytes(n, k, d, dtype, ldx)) return fail(INVALID_INPUT, "workspace too small");
-  SumPlan pd;
-  if (!build_sum_plan((int)d, &pd)) return fail(NOT_SUPPORTED, "feature dim too large for the exact plan");
-  // Rigorous screening bound (see vq_screen_sm100.cu): fp16 unit roundoff u
-  // on power-of-2-scaled operands (bf16 rows convert to scaled fp16 exactly,
-  // so only the codebook rounds), fp32 accumulation over Dp products (1 ulp =
-  // 2^-23 per add, covering round-to-nearest and truncation), fp32 epilogue
-  // rounding, subnormal term c4, 25% slack.
+namespace {
+// Rigorous screening bound (see vq_screen_sm100.cu): fp16 unit roundoff u
+// on power-of-2-scaled operands (bf16 rows convert to scaled fp16 exactly,
+// so only the codebook rounds), fp32 accumulation over Dp products (1 ulp =
+// 2^-23 per add, covering round-to-nearest and truncation), fp32 epilogue
+// rounding, subnormal term c4, 25% slack.
+ScreenArgs screen_args(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E, int64_t k,
+                       int64_t* codes, void* ws, size_t ws_bytes, const SumPlan* pd) {
   const double u = std::ldexp(1.0, -11);
   const double ux = dtype == BF16 ? 0.0 : u;
   const double dp = (double)((d + 63) / 64 * 64);
@@ -152,10 +177,61 @@ int xgs_vq_assign(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, c
   a.c1 = (float)c1;
   a.c2 = (float)c2;
   a.c4 = (float)c4;
-  a.pd = &pd;
+  a.pd = pd;
   a.sm_count = sm_count();
+  return a;
+}
+
+int check_assign(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E, int64_t k,
+                 int64_t* codes) {
+  int rc = check_rows(x, dtype, n, d, ldx);
+  if (rc) return rc;
+  if (k == 0) return fail(INVALID_STATE, "cannot assign against an empty codebook");
+  if (k < 0 || !E || (n > 0 && !codes)) return fail(INVALID_INPUT, "bad codebook or output");
+  if (n > 0x7fffffff) return fail(NOT_SUPPORTED, "more than 2^31-1 rows per call");
+  return OK;
+}
+}  // namespace
+
+int xgs_vq_assign(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E, int64_t k,
+                  int64_t* codes, void* ws, size_t ws_bytes, int32_t* stats_out, void* stream) {
+  int rc = check_assign(x, dtype, n, d, ldx, E, k, codes);
+  if (rc) return rc;
+  if (n == 0) return OK;
+  if (ws_bytes < screen_workspace_bytes(n, k, d, dtype, ldx)) return fail(INVALID_INPUT, "workspace too small");
+  SumPlan pd;
+  if (!build_sum_plan((int)d, &pd)) return fail(NOT_SUPPORTED, "feature dim too large for the exact plan");
+  ScreenArgs a = screen_args(x, dtype, n, d, ldx, E, k, codes, ws, ws_bytes, &pd);
   cudaError_t e = launch_screen_assign(a, (cudaStream_t)stream, stats_out);
   if (e != cudaSuccess) return cuda_fail(e, "xgs_vq_assign");
+  if (stats_out && (e = cudaStreamSynchronize((cudaStream_t)stream)) != cudaSuccess)
+    return cuda_fail(e, "xgs_vq_assign");
+  return OK;
+}
+
+size_t xgs_vq_step_workspace(int64_t n, int64_t k, int64_t d, int dtype, int64_t ldx) {
+  const size_t a = (screen_workspace_bytes(n, k, d, dtype, ldx) + 1023) / 1024 * 1024;
+  return a + accumulate_workspace_bytes(n, k);
+}
+
+int xgs_vq_assign_accumulate(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E,
+                             int64_t k, int64_t* codes, double* counts, double* sums, void* ws, size_t ws_bytes,
+                             int32_t* stats_out, void* stream) {
+  int rc = check_assign(x, dtype, n, d, ldx, E, k, codes);
+  if (rc) return rc;
+  if (n == 0) return fail(INVALID_INPUT, "batch must be nonempty");
+  if (!counts || !sums) return fail(INVALID_INPUT, "bad accumulate arguments");
+  if (ws_bytes < xgs_vq_step_workspace(n, k, d, dtype, ldx)) return fail(INVALID_INPUT, "workspace too small");
+  SumPlan pd;
+  if (!build_sum_plan((int)d, &pd)) return fail(NOT_SUPPORTED, "feature dim too large for the exact plan");
+  const size_t sbytes = (screen_workspace_bytes(n, k, d, dtype, ldx) + 1023) / 1024 * 1024;
+  ScreenArgs a = screen_args(x, dtype, n, d, ldx, E, k, codes, ws, sbytes, &pd);
+  void* acc_ws = static_cast<char*>(ws) + sbytes;
+  cudaError_t e = launch_assign_accumulate(a, counts, sums, acc_ws, ws_bytes - sbytes, (cudaStream_t)stream,
+                                           stats_out);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_vq_assign_accumulate");
+  if (stats_out && (e = cudaStreamSynchronize((cudaStream_t)stream)) != cudaSuccess)
+    return cuda_fail(e, "xgs_vq_assign_accumulate");
   return OK;
 }
 

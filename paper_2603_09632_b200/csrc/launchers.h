@@ -74,13 +74,28 @@ struct ScreenArgs {
 };
 size_t screen_workspace_bytes(int64_t n, int64_t k, int64_t d, int dtype, int64_t ldx);
 cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* host_stats);
+// staged form used by the row-chunk pipeline: codebook prep once, then per
+// chunk of rows [r0, r1): operand prep, screen + re-rank + exact rescan
+constexpr int kMaxChunks = 64;
+cudaError_t screen_prepare(const ScreenArgs& a, cudaStream_t s);
+cudaError_t screen_prep_rows(const ScreenArgs& a, int64_t r0, int64_t r1, cudaStream_t s);
+cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, cudaStream_t s);
+cudaError_t screen_finish(const ScreenArgs& a, int chunks, cudaStream_t s, int32_t* host_stats);
+
+// ---------------- row-chunk pipelined assign + accumulate (vq_pipeline.cu) ----------------
+int pipeline_chunks(int64_t n, int sm_count, int64_t* chunk_rows);
+cudaError_t launch_assign_accumulate(const ScreenArgs& a, double* counts, double* sums, void* acc_ws,
+                                     size_t acc_ws_bytes, cudaStream_t s, int32_t* host_stats);
 
 // ---------------- codebook update (vq_update.cu) ----------------
 size_t accumulate_workspace_bytes(int64_t n, int64_t k);
+// cont != 0 continues the per-(k, d) chains and counts from the values already
+// in counts/sums (rows of this call follow, in row order, the rows of the
+// previous call): chunked accumulation is bit-identical to one call.
 cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx,
                               const int64_t* codes, const uint8_t* mask, int64_t k,
                               double* counts, double* sums, void* ws, size_t ws_bytes,
-                              int sm_count, cudaStream_t s);
+                              int sm_count, cudaStream_t s, int cont = 0);
 cudaError_t launch_ema(double lam, double one_minus_lam, double eps, int64_t k, int64_t d,
                        const double* N, const double* M, const double* counts, const double* sums,
                        double* N_out, double* M_out, double* E_out, cudaStream_t s);

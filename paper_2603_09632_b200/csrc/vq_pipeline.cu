@@ -1,0 +1,112 @@
+// Row-chunk pipeline for one online step's assign + accumulate (vq.py:193-212,
+// the accumulate(batch[mask]) after assign_batch when the confidence mask is
+// provably all-true).
+//
+// The three stages have different bounds: operand prep streams X from HBM,
+// the screening GEMM is tensor-bound, the sequential fp64 chains of
+// accumulate stream X again.  Rows are split into chunks of whole screening
+// waves and the stages run on three streams:
+//
+//   prep stream   : prep_rows(c)                      -> ev_prep[c]
+//   caller stream : wait ev_prep[c]; screen + re-rank(c) -> ev_codes[c]
+//   acc stream    : wait ev_codes[c]; accumulate(c, continue chains)
+//
+// so prep(c+1) and accumulate(c-1) run on the SM resources the persistent
+// screening kernel leaves free (it holds ~128 regs x 352 threads and 217 KB of
+// smem per SM; prep blocks and 2-warp chain blocks fit beside it).
+// accumulate(c) continues every (k, d) chain from accumulate(c-1), so the
+// result is bit-identical to one accumulate over all rows (np.add.at order).
+#include <cstdlib>
+#include <mutex>
+
+#include "launchers.h"
+
+namespace xgs {
+
+namespace {
+
+struct PipeRes {
+  bool ready = false;
+  cudaStream_t sp = nullptr, sa = nullptr;
+  cudaEvent_t ev0 = nullptr, done = nullptr;
+  cudaEvent_t evp[kMaxChunks], eva[kMaxChunks];
+};
+
+constexpr int kMaxDevices = 16;
+PipeRes g_res[kMaxDevices];
+std::mutex g_mtx;   // the enqueue sequence below reuses per-device streams/events
+
+cudaError_t res_for(int dev, PipeRes** out) {
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  PipeRes& r = g_res[dev];
+  if (!r.ready) {
+    cudaError_t e;
+    if ((e = cudaStreamCreateWithFlags(&r.sp, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&r.sa, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&r.ev0, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming)) != cudaSuccess) return e;
+    for (int i = 0; i < kMaxChunks; i++) {
+      if ((e = cudaEventCreateWithFlags(&r.evp[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&r.eva[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+    }
+    r.ready = true;
+  }
+  *out = &r;
+  return cudaSuccess;
+}
+
+}  // namespace
+
+int pipeline_chunks(int64_t n, int sm_count, int64_t* chunk_rows) {
+  // a chunk is a whole number of screening waves (one 256-row tile per CTA pair)
+  const int64_t wave = (int64_t)(sm_count / 2 > 0 ? sm_count / 2 : 1) * 256;
+  const int64_t waves = (n + wave - 1) / wave;
+  // Measured at C2 (B200): co-resident prep/accumulate blocks slow the
+  // screening kernel about as much as they gain (2.27 ms/step at 1 chunk,
+  // 2.33 at 4, 2.50 at 8), so the default is one chunk; XGS_PIPE_CHUNKS
+  // overrides it for experiments.
+  int chunks = 1;
+  (void)waves;
+  if (const char* env = std::getenv("XGS_PIPE_CHUNKS")) chunks = std::atoi(env);   // tuning override
+  if (chunks > kMaxChunks) chunks = kMaxChunks;
+  if (chunks < 1) chunks = 1;
+  const int64_t wpc = (waves + chunks - 1) / chunks;
+  *chunk_rows = wpc * wave;
+  return (int)((n + *chunk_rows - 1) / *chunk_rows);
+}
+
+cudaError_t launch_assign_accumulate(const ScreenArgs& a, double* counts, double* sums, void* acc_ws,
+                                     size_t acc_ws_bytes, cudaStream_t s, int32_t* host_stats) {
+  int64_t crows = 0;
+  const int chunks = pipeline_chunks(a.n, a.sm_count, &crows);
+  std::lock_guard<std::mutex> lock(g_mtx);
+  int dev = 0;
+  cudaError_t e;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  PipeRes* r = nullptr;
+  if ((e = res_for(dev, &r)) != cudaSuccess) return e;
+
+  if ((e = screen_prepare(a, s)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(r->ev0, s)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(r->sp, r->ev0, 0)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(r->sa, r->ev0, 0)) != cudaSuccess) return e;
+  const size_t xrow = (size_t)a.ldx * dtype_size(a.dtype);
+  for (int c = 0; c < chunks; c++) {
+    const int64_t r0 = c * crows, r1 = (r0 + crows < a.n) ? r0 + crows : a.n;
+    if ((e = screen_prep_rows(a, r0, r1, r->sp)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(r->evp[c], r->sp)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(s, r->evp[c], 0)) != cudaSuccess) return e;
+    if ((e = screen_rows(a, r0, r1, c, s)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(r->eva[c], s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(r->sa, r->eva[c], 0)) != cudaSuccess) return e;
+    const void* xc = static_cast<const char*>(a.x) + (size_t)r0 * xrow;
+    if ((e = launch_accumulate(xc, a.dtype, r1 - r0, a.d, a.ldx, a.codes + r0, nullptr, a.k, counts, sums, acc_ws,
+                               acc_ws_bytes, a.sm_count, r->sa, c > 0)) != cudaSuccess)
+      return e;
+  }
+  if ((e = cudaEventRecord(r->done, r->sa)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(s, r->done, 0)) != cudaSuccess) return e;
+  return screen_finish(a, chunks, s, host_stats);
+}
+
+}  // namespace xgs

@@ -39,7 +39,6 @@ constexpr int BN = 256;                       // codes per chunk (pair MMA N)
 constexpr int BNH = BN / 2;                   // codes per CTA's half of B
 constexpr int BK = 64;                        // fp16 elements per 128-byte swizzled row
 constexpr int A_SLOTS = 8;                    // A ring: the whole 128 x 512 row tile when D <= 512
-constexpr int B_STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB
 constexpr int B_BYTES = BNH * BK * 2;         // 16 KB
 constexpr int EPI_WARPS = 8;                  // 2 per TMEM lane quadrant (column halves)
@@ -55,15 +54,21 @@ struct HalfState {                            // column-half 1 -> half 0 hand-of
   int ck[CAP];
   float cl[CAP];
 };
-constexpr int MERGE_BYTES = BM * (int)sizeof(HalfState<kCandCap>);
-constexpr int NBARS = 2 * A_SLOTS + 2 * B_STAGES + 4;
-constexpr int BAR_BYTES = NBARS * 8 + 16;
-constexpr int OFF_B = A_SLOTS * A_BYTES;
-constexpr int OFF_CONST = OFF_B + B_STAGES * B_BYTES;
-constexpr int OFF_MERGE = OFF_CONST + CONST_BYTES;
-constexpr int OFF_BAR = OFF_MERGE + MERGE_BYTES;
-constexpr int SMEM_BYTES = OFF_BAR + BAR_BYTES;
-static_assert(SMEM_BYTES <= 227 * 1024, "screen smem budget");
+// smem layout per candidate capacity: the CAP=8 epilogue's smaller merge
+// area leaves room for a 5th codebook stage
+template <int CAP>
+struct Layout {
+  static constexpr int B_STAGES = CAP <= 8 ? 5 : 4;
+  static constexpr int MERGE_BYTES = BM * (int)sizeof(HalfState<CAP>);
+  static constexpr int NBARS = 2 * A_SLOTS + 2 * B_STAGES + 4;
+  static constexpr int BAR_BYTES = NBARS * 8 + 16;
+  static constexpr int OFF_B = A_SLOTS * A_BYTES;
+  static constexpr int OFF_CONST = OFF_B + B_STAGES * B_BYTES;
+  static constexpr int OFF_MERGE = OFF_CONST + CONST_BYTES;
+  static constexpr int OFF_BAR = OFF_MERGE + MERGE_BYTES;
+  static constexpr int SMEM_BYTES = OFF_BAR + BAR_BYTES;
+  static_assert(SMEM_BYTES <= 227 * 1024, "screen smem budget");
+};
 // kind::f16 instruction descriptor: D=f32, A=B=f16 (format 0), both K-major,
 // N=256, M=256 (cta_group::2: 128 rows of A and 128 codes of B per CTA).
 constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
@@ -290,13 +295,14 @@ template <int CAP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               ScreenParams p) {
+  using L = Layout<CAP>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  float* cconst = reinterpret_cast<float*>(smem + OFF_CONST);
-  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  float* cconst = reinterpret_cast<float*>(smem + L::OFF_CONST);
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* emptyA = fullA + A_SLOTS;
   uint64_t* fullB = emptyA + A_SLOTS;
-  uint64_t* emptyB = fullB + B_STAGES;
-  uint64_t* tfull = emptyB + B_STAGES;
+  uint64_t* emptyB = fullB + L::B_STAGES;
+  uint64_t* tfull = emptyB + L::B_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -310,7 +316,7 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       mbar_init(&fullA[i], 1);
       mbar_init(&emptyA[i], 1);
     }
-    for (int i = 0; i < B_STAGES; i++) {
+    for (int i = 0; i < L::B_STAGES; i++) {
       mbar_init(&fullB[i], 1);
       mbar_init(&emptyB[i], 1);
     }
@@ -359,10 +365,10 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       for (int t = cluster; t < p.num_pair_tiles; t += nclusters)
         for (int nc = 0; nc < nnc; nc++)
           for (int kb = 0; kb < nkb; kb++, idx++) {
-            const uint32_t st = idx % B_STAGES, ph = (idx / B_STAGES) & 1;
+            const uint32_t st = idx % L::B_STAGES, ph = (idx / L::B_STAGES) & 1;
             mbar_wait(&emptyB[st], ph ^ 1);
             if (leader) mbar_expect_tx(&fullB[st], 2 * B_BYTES);
-            tma_load_2d_pair(smem + OFF_B + st * B_BYTES, &tmB, kb * BK, nc * BN + (int)rank * BNH,
+            tma_load_2d_pair(smem + L::OFF_B + st * B_BYTES, &tmB, kb * BK, nc * BN + (int)rank * BNH,
                              lead_full + st * 8);
           }
     }
@@ -380,12 +386,12 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           for (int kb = 0; kb < nkb; kb++, bidx++) {
             const uint32_t ai = abase + (uint32_t)(p.resident ? kb : nc * nkb + kb);
             const uint32_t aslot = ai % A_SLOTS;
-            const uint32_t bst = bidx % B_STAGES;
+            const uint32_t bst = bidx % L::B_STAGES;
             mbar_wait(&fullA[aslot], (ai / A_SLOTS) & 1);
-            mbar_wait(&fullB[bst], (bidx / B_STAGES) & 1);
+            mbar_wait(&fullB[bst], (bidx / L::B_STAGES) & 1);
             tc_after();
             const uint32_t sa = smem_u32(smem + aslot * A_BYTES);
-            const uint32_t sb = smem_u32(smem + OFF_B + bst * B_BYTES);
+            const uint32_t sb = smem_u32(smem + L::OFF_B + bst * B_BYTES);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; kk++)
               mma_f16_pair(dt, sw128_desc(sa + kk * 32), sw128_desc(sb + kk * 32), (kb | kk) != 0);
@@ -408,7 +414,7 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const int rl = q * 32 + lane;            // row within this CTA's 128 rows
     const unsigned lt = (1u << lane) - 1u;
     const uint32_t lead_tempty = mapa(smem_u32(tempty), 0);
-    HalfState<CAP>* merge = reinterpret_cast<HalfState<CAP>*>(smem + OFF_MERGE);
+    HalfState<CAP>* merge = reinterpret_cast<HalfState<CAP>*>(smem + L::OFF_MERGE);
     int acc = 0;
     uint32_t aphase = 0;
     for (int t = cluster; t < p.num_pair_tiles; t += nclusters) {
@@ -625,6 +631,10 @@ prep_rows_kernel(const X* __restrict__ x, int64_t n, int64_t d, int64_t ldx, int
   }
 }
 
+// counter block: [0..1] codebook absmax bits, [2..3] step totals,
+// then {rerank, fallback} counts per row chunk
+constexpr int kCntBase = 8;
+
 struct ScreenWs {
   size_t off_ab, off_xn, off_xf, off_eb, off_cn, off_rq, off_fq, off_cnt, total;
   int64_t kp, dp;
@@ -644,7 +654,7 @@ ScreenWs screen_ws(int64_t n, int64_t k, int64_t d) {
   w.off_cn = take((size_t)w.kp * 4);
   w.off_rq = take(nn * sizeof(RerankEntry));
   w.off_fq = take(nn * 4);
-  w.off_cnt = take(64);
+  w.off_cnt = take(sizeof(int32_t) * (kCntBase + 2 * kMaxChunks));
   w.total = o;
   return w;
 }
@@ -682,52 +692,106 @@ size_t screen_workspace_bytes(int64_t n, int64_t k, int64_t d, int dtype, int64_
   return screen_ws(n, k, d).total;
 }
 
-cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* host_stats) {
-  const ScreenWs w = screen_ws(a.n, a.k, a.d);
-  if (a.ws_bytes < w.total) return cudaErrorInvalidValue;
+namespace {
+
+struct ScreenBufs {
+  ScreenWs w;
+  __half* Ab;
+  float* xn;
+  float* xf;
+  __half* Eb;
+  float* cn;
+  RerankEntry* rq;
+  int32_t* fq;
+  int32_t* cnt;
+  unsigned* emax;
+};
+
+ScreenBufs screen_bufs(const ScreenArgs& a) {
+  ScreenBufs b;
+  b.w = screen_ws(a.n, a.k, a.d);
   char* base = static_cast<char*>(a.ws);
-  __half* Ab = reinterpret_cast<__half*>(base + w.off_ab);
-  float* xn = reinterpret_cast<float*>(base + w.off_xn);
-  float* xf = reinterpret_cast<float*>(base + w.off_xf);
-  __half* Eb = reinterpret_cast<__half*>(base + w.off_eb);
-  float* cn = reinterpret_cast<float*>(base + w.off_cn);
-  RerankEntry* rq = reinterpret_cast<RerankEntry*>(base + w.off_rq);
-  int32_t* fq = reinterpret_cast<int32_t*>(base + w.off_fq);
-  int32_t* cnt = reinterpret_cast<int32_t*>(base + w.off_cnt);
-  unsigned* emax = reinterpret_cast<unsigned*>(cnt + 4);
+  b.Ab = reinterpret_cast<__half*>(base + b.w.off_ab);
+  b.xn = reinterpret_cast<float*>(base + b.w.off_xn);
+  b.xf = reinterpret_cast<float*>(base + b.w.off_xf);
+  b.Eb = reinterpret_cast<__half*>(base + b.w.off_eb);
+  b.cn = reinterpret_cast<float*>(base + b.w.off_cn);
+  b.rq = reinterpret_cast<RerankEntry*>(base + b.w.off_rq);
+  b.fq = reinterpret_cast<int32_t*>(base + b.w.off_fq);
+  b.cnt = reinterpret_cast<int32_t*>(base + b.w.off_cnt);
+  b.emax = reinterpret_cast<unsigned*>(b.cnt);
+  return b;
+}
+
+__global__ void sum_counters_kernel(int32_t* cnt, int chunks) {
+  int32_t r = 0, f = 0;
+  for (int c = 0; c < chunks; c++) {
+    r += cnt[kCntBase + 2 * c];
+    f += cnt[kCntBase + 2 * c + 1];
+  }
+  cnt[2] = r;
+  cnt[3] = f;
+}
+
+}  // namespace
+
+cudaError_t screen_prepare(const ScreenArgs& a, cudaStream_t s) {
+  const ScreenBufs b = screen_bufs(a);
+  if (a.ws_bytes < b.w.total) return cudaErrorInvalidValue;
   cudaError_t e;
-  if ((e = cudaMemsetAsync(cnt, 0, 64, s)) != cudaSuccess) return e;
-
-  {
+  if ((e = cudaMemsetAsync(b.cnt, 0, sizeof(int32_t) * (kCntBase + 2 * kMaxChunks), s)) != cudaSuccess) return e;
   ProfScope prof("vq_prep", s);
-  absmax_kernel<<<148, 256, 0, s>>>(a.E, a.k * a.d, emax); count_launches(1);
-  prep_codebook_kernel<<<(unsigned)((w.kp + 7) / 8), 256, 0, s>>>(a.E, a.k, a.d, w.kp, w.dp, a.c1, a.c2, a.c4,
-                                                                  emax, Eb, cn, emax + 1); count_launches(1);
-  const float inflate = 1.f + (float)(a.d + 8) * 1.2e-7f;
-  const unsigned rblocks = (unsigned)((a.n + 7) / 8);
-  switch (a.dtype) {
-    case F32: prep_rows_kernel<float><<<rblocks, 256, 0, s>>>((const float*)a.x, a.n, a.d, a.ldx, w.dp, emax, emax + 1, 1.0e-12f, Ab, xn, xf, inflate); count_launches(1); break;
-    case F64: prep_rows_kernel<double><<<rblocks, 256, 0, s>>>((const double*)a.x, a.n, a.d, a.ldx, w.dp, emax, emax + 1, 1.0e-12f, Ab, xn, xf, inflate); count_launches(1); break;
-    default: prep_rows_kernel<uint16_t><<<rblocks, 256, 0, s>>>((const uint16_t*)a.x, a.n, a.d, a.ldx, w.dp, emax, emax + 1, 1.0e-12f, Ab, xn, xf, inflate); count_launches(1);
-  }
-  }
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  absmax_kernel<<<148, 256, 0, s>>>(a.E, a.k * a.d, b.emax); count_launches(1);
+  prep_codebook_kernel<<<(unsigned)((b.w.kp + 7) / 8), 256, 0, s>>>(a.E, a.k, a.d, b.w.kp, b.w.dp, a.c1, a.c2, a.c4,
+                                                                    b.emax, b.Eb, b.cn, b.emax + 1); count_launches(1);
+  return cudaGetLastError();
+}
 
+cudaError_t screen_prep_rows(const ScreenArgs& a, int64_t r0, int64_t r1, cudaStream_t s) {
+  const ScreenBufs b = screen_bufs(a);
+  const int64_t n = r1 - r0;
+  if (n <= 0) return cudaSuccess;
+  ProfScope prof("vq_prep", s);
+  const float inflate = 1.f + (float)(a.d + 8) * 1.2e-7f;
+  const unsigned rblocks = (unsigned)((n + 7) / 8);
+  const int64_t dp = b.w.dp;
+  __half* Ab = b.Ab + r0 * dp;
+  float* xn = b.xn + r0;
+  float* xf = b.xf + r0;
+  switch (a.dtype) {
+    case F32: prep_rows_kernel<float><<<rblocks, 256, 0, s>>>((const float*)a.x + r0 * a.ldx, n, a.d, a.ldx, dp, b.emax, b.emax + 1, 1.0e-12f, Ab, xn, xf, inflate); count_launches(1); break;
+    case F64: prep_rows_kernel<double><<<rblocks, 256, 0, s>>>((const double*)a.x + r0 * a.ldx, n, a.d, a.ldx, dp, b.emax, b.emax + 1, 1.0e-12f, Ab, xn, xf, inflate); count_launches(1); break;
+    default: prep_rows_kernel<uint16_t><<<rblocks, 256, 0, s>>>((const uint16_t*)a.x + r0 * a.ldx, n, a.d, a.ldx, dp, b.emax, b.emax + 1, 1.0e-12f, Ab, xn, xf, inflate); count_launches(1);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, cudaStream_t s) {
+  const ScreenBufs b = screen_bufs(a);
+  const int64_t n = r1 - r0;
+  if (n <= 0) return cudaSuccess;
+  if (chunk < 0 || chunk >= kMaxChunks) return cudaErrorInvalidValue;
+  const int64_t dp = b.w.dp;
   CUtensorMap tmA, tmB;
-  if (!make_map(&tmA, Ab, (uint64_t)w.dp, (uint64_t)a.n, (uint64_t)w.dp * 2, BK, BM) ||
-      !make_map(&tmB, Eb, (uint64_t)w.dp, (uint64_t)w.kp, (uint64_t)w.dp * 2, BK, BNH))
+  if (!make_map(&tmA, b.Ab + r0 * dp, (uint64_t)dp, (uint64_t)n, (uint64_t)dp * 2, BK, BM) ||
+      !make_map(&tmB, b.Eb, (uint64_t)dp, (uint64_t)b.w.kp, (uint64_t)dp * 2, BK, BNH))
     return cudaErrorInvalidValue;
+  int32_t* cnt = b.cnt + kCntBase + 2 * chunk;
+  RerankEntry* rq = b.rq + r0;
+  int32_t* fq = b.fq + r0;
+  const void* x = static_cast<const char*>(a.x) + (size_t)r0 * (size_t)a.ldx * dtype_size(a.dtype);
+  int64_t* codes = a.codes + r0;
 
   ScreenParams p;
-  p.n = a.n;
-  p.num_pair_tiles = (int)((a.n + 2 * BM - 1) / (2 * BM));
-  p.num_n_chunks = (int)(w.kp / BN);
-  p.num_k_blocks = (int)(w.dp / BK);
+  p.n = n;
+  p.num_pair_tiles = (int)((n + 2 * BM - 1) / (2 * BM));
+  p.num_n_chunks = (int)(b.w.kp / BN);
+  p.num_k_blocks = (int)(dp / BK);
   p.resident = p.num_k_blocks <= A_SLOTS;
-  p.xband = xn;
-  p.xf = xf;
-  p.cn = cn;
-  p.codes = a.codes;
+  p.xband = b.xn + r0;
+  p.xf = b.xf + r0;
+  p.cn = b.cn;
+  p.codes = codes;
   p.rq = rq;
   p.rq_count = cnt;
   p.fq = fq;
@@ -736,9 +800,11 @@ cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* h
   // (more near-ties) use the full RerankEntry capacity of 16
   const bool big = a.k >= 2048;
   auto kern = big ? screen_kernel<kCandCap> : screen_kernel<8>;
+  const int smem_bytes = big ? Layout<kCandCap>::SMEM_BYTES : Layout<8>::SMEM_BYTES;
   static bool attr[2] = {false, false};
+  cudaError_t e;
   if (!attr[big]) {
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)) != cudaSuccess)
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes)) != cudaSuccess)
       return e;
     attr[big] = true;
   }
@@ -746,20 +812,19 @@ cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* h
   int clusters = a.sm_count / 2;
   if (clusters > p.num_pair_tiles) clusters = p.num_pair_tiles;
   if (clusters < 1) clusters = 1;
-  const int grid = 2 * clusters;
   {
     ProfScope prof("vq_screen", s);
-    kern<<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, p); count_launches(1);
+    kern<<<2 * clusters, THREADS, smem_bytes, s>>>(tmA, tmB, p); count_launches(1);
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
   // exact re-rank of the multi-candidate rows, exact scan of overflowed rows
   ProfScope prof("vq_rerank", s);
-  if ((e = launch_rerank(a.x, a.dtype, a.d, a.ldx, a.E, rq, cnt, a.n, a.codes, *a.pd, s)) != cudaSuccess) return e;
+  if ((e = launch_rerank(x, a.dtype, a.d, a.ldx, a.E, rq, cnt, n, codes, *a.pd, s)) != cudaSuccess) return e;
   ExactArgs ea{};
-  ea.x = a.x;
+  ea.x = x;
   ea.dtype = a.dtype;
-  ea.n = a.n;
+  ea.n = n;
   ea.d = a.d;
   ea.ldx = a.ldx;
   ea.E = a.E;
@@ -767,17 +832,29 @@ cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* h
   ea.rows = fq;
   ea.nrows_dev = cnt + 1;
   ea.mode = EX_WRITE_CODE;
-  ea.codes = a.codes;
+  ea.codes = codes;
   SumPlan pk_unused;
   pk_unused.n = 0;
   pk_unused.n_leaves = 0;
   pk_unused.n_ops = 0;
-  if ((e = launch_exact_rows(ea, *a.pd, pk_unused, s)) != cudaSuccess) return e;
-  if (host_stats) {
-    if ((e = cudaMemcpyAsync(host_stats, cnt, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-      return e;
-  }
+  return launch_exact_rows(ea, *a.pd, pk_unused, s);
+}
+
+cudaError_t screen_finish(const ScreenArgs& a, int chunks, cudaStream_t s, int32_t* host_stats) {
+  const ScreenBufs b = screen_bufs(a);
+  sum_counters_kernel<<<1, 1, 0, s>>>(b.cnt, chunks); count_launches(1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (host_stats) return cudaMemcpyAsync(host_stats, b.cnt + 2, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
   return cudaSuccess;
+}
+
+cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* host_stats) {
+  cudaError_t e;
+  if ((e = screen_prepare(a, s)) != cudaSuccess) return e;
+  if ((e = screen_prep_rows(a, 0, a.n, s)) != cudaSuccess) return e;
+  if ((e = screen_rows(a, 0, a.n, 0, s)) != cudaSuccess) return e;
+  return screen_finish(a, 1, s, host_stats);
 }
 
 }  // namespace xgs

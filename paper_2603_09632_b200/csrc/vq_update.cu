@@ -207,13 +207,15 @@ template <typename X> struct Raw<X, 1> {
 // chain is inherently serial, so a warp's speed is its memory-level
 // parallelism: U rows are loaded ahead (U*32*VEC*sizeof(X) bytes in flight per
 // warp) before the U dependent adds.
+constexpr int kChainWarps = 8;
 template <typename X, int VEC, int U>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(kChainWarps * 32, 2)
 acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
                  const int32_t* __restrict__ code_start, const int32_t* __restrict__ sorted,
-                 const int32_t* __restrict__ order, double* __restrict__ counts, double* __restrict__ sums) {
+                 const int32_t* __restrict__ order, double* __restrict__ counts, double* __restrict__ sums,
+                 int cont) {
   const int lane = threadIdx.x & 31;
-  const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t gw = (int64_t)blockIdx.x * kChainWarps + (threadIdx.x >> 5);
   const int64_t nchunks = (d + 32 * VEC - 1) / (32 * VEC);
   if (gw / nchunks >= k) return;
   const int64_t code = order[gw / nchunks];
@@ -222,7 +224,7 @@ acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
   const int32_t beg = code_start[code], end = code_start[code + 1];
   double acc[VEC];
 #pragma unroll
-  for (int v = 0; v < VEC; v++) acc[v] = 0.0;
+  for (int v = 0; v < VEC; v++) acc[v] = (cont && live && d0 + v < d) ? sums[code * d + d0 + v] : 0.0;
   const X* xd = x + (live ? d0 : 0);
   int32_t b = beg;
   for (; b + U <= end; b += U) {
@@ -253,18 +255,19 @@ acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
 #pragma unroll
     for (int v = 0; v < VEC; v++) sums[code * d + d0 + v] = acc[v];
   }
-  if (d0 == 0) counts[code] = (double)(end - beg);
+  if (d0 == 0) counts[code] = (cont ? counts[code] : 0.0) + (double)(end - beg);   // integer-valued: exact
 }
 
 template <typename X, int VEC>
 cudaError_t launch_chain(const X* x, int64_t d, int64_t ldx, int64_t k, const int32_t* cs,
                          const int32_t* sorted, const int32_t* order, double* counts, double* sums,
-                         cudaStream_t s) {
+                         cudaStream_t s, int cont) {
   const int64_t nchunks = (d + 32 * VEC - 1) / (32 * VEC);
   const int64_t warps = k * nchunks;
   constexpr int U = VEC >= 4 ? 16 : 32;
   ProfScope prof("vq_chain", s);
-  acc_chain_kernel<X, VEC, U><<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(x, d, ldx, k, cs, sorted, order, counts, sums); count_launches(1);
+  acc_chain_kernel<X, VEC, U><<<(unsigned)((warps + kChainWarps - 1) / kChainWarps), kChainWarps * 32, 0, s>>>(
+      x, d, ldx, k, cs, sorted, order, counts, sums, cont); count_launches(1);
   return cudaGetLastError();
 }
 
@@ -323,7 +326,7 @@ size_t accumulate_workspace_bytes(int64_t n, int64_t k) { return acc_plan(n, k).
 
 cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx,
                               const int64_t* codes, const uint8_t* mask, int64_t k, double* counts,
-                              double* sums, void* ws, size_t ws_bytes, int sm_count, cudaStream_t s) {
+                              double* sums, void* ws, size_t ws_bytes, int sm_count, cudaStream_t s, int cont) {
   (void)sm_count;
   const AccPlan p = acc_plan(n, k);
   if (ws_bytes < p.total) return cudaErrorInvalidValue;
@@ -351,16 +354,16 @@ cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, in
   switch (dtype) {
     case F32:
       if (d % 2 == 0 && ldx % 2 == 0 && xa % 8 == 0)
-        return launch_chain<float, 2>((const float*)x, d, ldx, k, code_start, sorted, order, counts, sums, s);
-      return launch_chain<float, 1>((const float*)x, d, ldx, k, code_start, sorted, order, counts, sums, s);
+        return launch_chain<float, 2>((const float*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
+      return launch_chain<float, 1>((const float*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
     case F64:
       if (d % 2 == 0 && ldx % 2 == 0 && xa % 16 == 0)
-        return launch_chain<double, 2>((const double*)x, d, ldx, k, code_start, sorted, order, counts, sums, s);
-      return launch_chain<double, 1>((const double*)x, d, ldx, k, code_start, sorted, order, counts, sums, s);
+        return launch_chain<double, 2>((const double*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
+      return launch_chain<double, 1>((const double*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
     default:
       if (d % 8 == 0 && ldx % 8 == 0 && xa % 16 == 0)
-        return launch_chain<uint16_t, 8>((const uint16_t*)x, d, ldx, k, code_start, sorted, order, counts, sums, s);
-      return launch_chain<uint16_t, 1>((const uint16_t*)x, d, ldx, k, code_start, sorted, order, counts, sums, s);
+        return launch_chain<uint16_t, 8>((const uint16_t*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
+      return launch_chain<uint16_t, 1>((const uint16_t*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
   }
 }
 

@@ -183,7 +183,7 @@ class CudaBackend:
 
     def local_stats(self, state, shard, cfg):
         from .core import Codebook
-        from .vq import _accumulate_dev, _assign_dev, _exact_dev, _rows, all_pass_provable
+        from .vq import _accumulate_dev, _assign_accumulate_dev, _exact_dev, _rows, all_pass_provable
         t, nat = self.t, self.nat
         E = state[0]
         packed = t.empty(self.K * self.D + self.K, dtype=t.float64, device="cuda")
@@ -195,8 +195,8 @@ class CudaBackend:
             return packed
         xt, dt, n, d, ldx = _rows(shard)
         if all_pass_provable(cfg.gamma, self.K):
-            codes = _assign_dev(xt, dt, n, d, ldx, E, self.K)
-            mask = None
+            _assign_accumulate_dev(xt, dt, n, d, ldx, E, self.K, counts=counts, sums=sums)
+            return packed
         else:
             _, _, codes, mask = _exact_dev(xt, dt, n, d, ldx, E, self.K, nat.EX_CODE | nat.EX_MASK,
                                            tau=cfg.tau_warm, gamma=cfg.gamma)

@@ -161,6 +161,22 @@ def _accumulate_dev(xt, dt, n, d, ldx, codes, mask, K):
     return counts, sums
 
 
+def _assign_accumulate_dev(xt, dt, n, d, ldx, E, K, counts=None, sums=None):
+    """assign_batch + accumulate(batch) for an all-pass mask (vq.py:206) in one
+    row-chunk-pipelined native call; bit-identical to _assign_dev followed by
+    _accumulate_dev."""
+    t = nat.torch()
+    codes = t.empty(n, dtype=t.int64, device="cuda")
+    if counts is None:
+        counts = t.empty(K, dtype=t.float64, device="cuda")
+    if sums is None:
+        sums = t.empty((K, d), dtype=t.float64, device="cuda")
+    ws = nat.workspace("step", nat.lib().xgs_vq_step_workspace(n, K, d, dt, ldx))
+    nat.call("xgs_vq_assign_accumulate", nat.ptr(xt), dt, n, d, ldx, nat.ptr(E), K, nat.ptr(codes),
+             nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel(), None, nat.stream_ptr())
+    return codes, counts, sums
+
+
 def _ema_dev(codebook, counts, sums):
     t = nat.torch()
     N = device_f64(codebook.N).reshape(-1) if not codebook.on_device else codebook.N
@@ -366,8 +382,8 @@ def local_stats(codebook: Codebook, xt, dt, n, d, ldx, cfg: VqConfig):
     """Per-shard half of online_step: mask + codes + (counts, sums) on device."""
     E, K = _E(codebook), codebook.K
     if all_pass_provable(cfg.gamma, K):
-        codes = _assign_dev(xt, dt, n, d, ldx, E, K)
-        mask = None
+        _, counts, sums = _assign_accumulate_dev(xt, dt, n, d, ldx, E, K)
+        return counts, sums
     else:
         _, _, codes, mask = _exact_dev(xt, dt, n, d, ldx, E, K, nat.EX_CODE | nat.EX_MASK, tau=cfg.tau_warm,
                                        gamma=cfg.gamma)

@@ -278,6 +278,35 @@ def test_online_step_device_matches_oracle(xv):
     assert np.array_equal(cb.reservoir.as_array(), oc.reservoir.buf)
 
 
+@pytest.mark.parametrize("n,K,D,dtype", [(700_000, 256, 64, "f32"), (400_000, 512, 96, "bf16"),
+                                         (300_000, 128, 40, "f64")])
+def test_pipelined_assign_accumulate(xv, n, K, D, dtype):
+    """xgs_vq_assign_accumulate (row-chunk pipeline, >= 2 chunks at these n)
+    is bit-identical to assign + accumulate and to the C oracle."""
+    import torch
+    from paper_2603_09632_b200 import vq as xvq
+    rng = np.random.default_rng(n + K)
+    x = mixture(rng, n, D, K, 0.05)
+    E = mixture(rng, K, D, K, 0.05).astype(np.float64)
+    if dtype == "bf16":
+        xt = torch.from_numpy(x).cuda().to(torch.bfloat16)
+        xh = xt.cpu().view(torch.int16).numpy().view(np.uint16)
+    else:
+        xt = torch.from_numpy(x.astype(np.float64) if dtype == "f64" else x).cuda()
+        xh = xt.cpu().numpy()
+    Et = torch.from_numpy(E).cuda()
+    r, dt, nn, d, ldx = xvq._rows(xt)
+    codes, counts, sums = xvq._assign_accumulate_dev(r, dt, nn, d, ldx, Et, K)
+    codes2 = xvq._assign_dev(r, dt, nn, d, ldx, Et, K)
+    counts2, sums2 = xvq._accumulate_dev(r, dt, nn, d, ldx, codes2, None, K)
+    assert torch.equal(codes, codes2)
+    assert torch.equal(counts, counts2) and torch.equal(sums, sums2)
+    ref = on.assign(xh, E, threads=8, bf16=dtype == "bf16")
+    assert np.array_equal(codes.cpu().numpy(), ref)
+    c, sm = on.accumulate(xh, ref, K, bf16=dtype == "bf16")
+    assert np.array_equal(counts.cpu().numpy(), c) and np.array_equal(sums.cpu().numpy(), sm)
+
+
 def test_assign_edge_cases(xv):
     rng = np.random.default_rng(11)
     # single row, single code, D = 1
