@@ -266,6 +266,327 @@ compact_keys_kernel(const uint64_t* __restrict__ kin, int64_t n, int64_t W, uint
   }
 }
 
+
+// ---------------------------------------------------------------- G1 fused front end
+// First-pick mode on W % 4 == 0, W <= 2048: keys, left/up dedup and ordered
+// compaction in one pass over the depth.  A block owns FK_ROWS rows of one
+// frame (thread t = columns 4t..4t+3), recomputes the keys of the row above
+// as the halo, stages its surviving (key, pixel) items in shared memory in
+// pixel order and publishes its count through a decoupled look-back over the
+// blocks (dynamic block ids, so every predecessor is already running): the
+// output is in ascending pixel order, exactly as the two-kernel path writes
+// it, and the stable sort keeps each voxel's lowest pixel id first.
+//
+// Keys are evaluated in fp32 with a rigorous error bound first.  The
+// back-projection is regrouped as p_i = d * P_i + Q_i with
+//   P_i = R_0i (u - cx)/fx + R_1i (v - cy)/fy + R_2i   (row part + column part)
+//   Q_i = -(R_0i t_0 + R_1i t_1 + R_2i t_2)            (per frame)
+// and its magnitude bound M_i = d * C_i + D_i, C_i = |R_0i| (|u|+|cx|)/fx +
+// |R_1i| (|v|+|cy|)/fy + |R_2i|, D_i = sum_j |R_ji| |t_j|.  Every fp32
+// rounding on that path (cx, 1/fx, R and t conversions, the products and
+// sums) is bounded by u = 2^-24 times a term of M_i, about 8 of them in total,
+// and the reference's fp64 evaluation (slam.py:594-598) is within ~2^-50 M_i
+// of exact, so |p32_i - p64_i| <= 2^-20 M_i.  If floor(q - delta) ==
+// floor(q + delta) with directed rounding (q = p32 / voxel) on all three axes
+// the fp32 floor IS the reference's floor(p64 / voxel); otherwise (voxel
+// faces, non-finite values, out of key range) the pixel takes the exact fp64
+// path (backproject + floor_div), bit-identical to the reference.
+constexpr int FK_ROWS = 4;
+constexpr int kFrontPend = 1024;   // per-block queue of pixels for the exact path
+
+struct CamF {
+  float cx, cy, rfx, rfy, inv_voxel;
+};
+
+__device__ __forceinline__ uint64_t key_exact(const double* R, const double* T, const Cam& cam, uint32_t u,
+                                              uint32_t v, float d32, int* qv) {
+  double p[3];
+  backproject(R, T, cam, (double)u, (double)v, (double)d32, p);
+  int64_t q[3];
+  if (!voxel_of(p, cam.voxel, q, cam.inv_voxel)) return KEY_INVALID;
+#pragma unroll
+  for (int a = 0; a < 3; a++) qv[a] = (int)q[a];
+  return ((uint64_t)q[0] << 42) | ((uint64_t)q[1] << 21) | (uint64_t)q[2];
+}
+
+__global__ void __launch_bounds__(384, 2)
+grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int stride, const double* __restrict__ rot,
+                  const double* __restrict__ trans, Cam cam, CamF cf, uint64_t* __restrict__ kout,
+                  uint32_t* __restrict__ vout, int* bbox, unsigned long long* cnts, unsigned* block_counter,
+                  unsigned long long* status) {
+  constexpr int NR = FK_ROWS;
+  __shared__ uint64_t s_last[NR][32];
+  __shared__ uint32_t s_wsum[NR][32];
+  __shared__ uint32_t s_rowbase[NR + 1];
+  __shared__ unsigned s_bid;
+  __shared__ int s_box[6];
+  __shared__ uint32_t s_npend;
+  __shared__ uint32_t s_pend[kFrontPend];     // staged slot | (j << 30) of pixels left to the exact path
+  extern __shared__ __align__(16) uint8_t front_smem[];   // NR*W keys, then NR*W pixel ids
+  uint64_t* sk = reinterpret_cast<uint64_t*>(front_smem);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(front_smem + (size_t)NR * W * 8);
+  if (threadIdx.x == 0) {
+    s_bid = atomicAdd(block_counter, 1u);
+    s_npend = 0;
+  }
+  if (threadIdx.x < 6) s_box[threadIdx.x] = threadIdx.x < 3 ? INT_MAX : INT_MIN;
+  __syncthreads();
+  const unsigned bid = s_bid;
+  const int rbf = (int)((H + NR - 1) / NR);   // row blocks per frame
+  const int f = (int)(bid / (unsigned)rbf);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+  const uint32_t Wu = (uint32_t)W, su = (uint32_t)stride;
+  const uint32_t c0 = (uint32_t)t * 4;
+  const bool col_on = c0 < Wu;
+  const double* Rd = rot + (size_t)f * 9;
+  const double* Td = trans + (size_t)f * 3;
+  const float iv = cf.inv_voxel;
+  // per-frame constants pre-scaled by 1/voxel: q_i = p_i / voxel = d * (Pr_i + Pc_ji) + Qs_i,
+  // magnitude bound M_i / voxel = d * (Cr_i + Cc_ji) + Ds_i
+  float R0[3], R2[3], A0[3], A2[3], Qs[3], Ds[3];
+  float Pc[4][3], Cc[4][3];
+  unsigned colmask = 0;
+  {
+    const float t0 = (float)Td[0], t1 = (float)Td[1], t2 = (float)Td[2];
+    float R1[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      const float r0 = (float)Rd[i], r1 = (float)Rd[3 + i], r2 = (float)Rd[6 + i];
+      R0[i] = r0 * iv;
+      R1[i] = r1 * iv;
+      R2[i] = r2 * iv;
+      A0[i] = fabsf(R0[i]);
+      A2[i] = fabsf(R2[i]);
+      Qs[i] = -fmaf(r2, t2, fmaf(r1, t1, r0 * t0)) * iv;
+      Ds[i] = fmaf(fabsf(r2), fabsf(t2), fmaf(fabsf(r1), fabsf(t1), fabsf(r0) * fabsf(t0))) * iv;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const float vv = (float)(c0 + j);
+      const float cv = (vv - cf.cy) * cf.rfy, bv = (vv + fabsf(cf.cy)) * cf.rfy;
+#pragma unroll
+      for (int i = 0; i < 3; i++) {
+        Pc[j][i] = R1[i] * cv;
+        Cc[j][i] = fabsf(R1[i]) * bv;
+      }
+      if (col_on && (su == 1 || ((c0 + j) % su) == 0)) colmask |= 1u << j;
+    }
+  }
+  const int r0 = (int)(bid % (unsigned)rbf) * NR;
+  const int nr = (int)min((int64_t)NR, H - r0);
+  const float4* drow = reinterpret_cast<const float4*>(depth + (size_t)f * H * W);
+  unsigned cnt = 0;
+  // ---- keys of the halo row and the block's rows, all in registers ----
+  // PEND marks a pixel the fp32 filter could not decide: it compares unequal to
+  // every key (so it and its neighbours are kept) and is resolved exactly below.
+  constexpr uint64_t PEND = KEY_INVALID - 1;
+  uint64_t k[NR + 1][4];
+#pragma unroll
+  for (int rr = 0; rr <= NR; rr++) {
+    const int r = r0 - 1 + rr;
+#pragma unroll
+    for (int j = 0; j < 4; j++) k[rr][j] = KEY_INVALID;
+    if (r < 0 || rr > nr) continue;
+    const uint32_t u = (uint32_t)r;
+    const unsigned rowmask = (su == 1 || (u % su) == 0) ? colmask : 0u;
+    if (!rowmask) continue;
+    const float4 d4 = __ldg(drow + (((size_t)r * W) >> 2) + t);
+    const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+    const float uu = (float)u;
+    const float ru = (uu - cf.cx) * cf.rfx, bu = (uu + fabsf(cf.cx)) * cf.rfx;
+    float Pr[3], Cr[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      Pr[i] = fmaf(R0[i], ru, R2[i]);
+      Cr[i] = fmaf(A0[i], bu, A2[i]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const float d = dv[j];
+      if (!((rowmask >> j) & 1u) || !(d > 0.f)) continue;
+      bool ok = true;
+      int qi[3];
+#pragma unroll
+      for (int i = 0; i < 3; i++) {
+        const float q = fmaf(d, Pr[i] + Pc[j][i], Qs[i]);
+        const float M = fmaf(d, Cr[i] + Cc[j][i], Ds[i]);        // >= |q_i| and >= the magnitudes rounded
+        const float dl = fmaf(M, 0x1p-20f * 1.002f + 0x1p-21f, 0x1p-40f);
+        const float fl = floorf(__fsub_rd(q, dl));
+        ok = ok && __fadd_ru(q, dl) < fl + 1.f && M < 1048000.f;   // one floor on [q-dl, q+dl]
+        qi[i] = (int)fl + (int)KEY_BIAS;
+      }
+      if (ok) {
+        k[rr][j] = ((uint64_t)(uint32_t)qi[0] << 42) | ((uint64_t)(uint32_t)qi[1] << 21) | (uint64_t)(uint32_t)qi[2];
+        cnt += rr > 0 ? 1u : 0u;
+      } else {
+        k[rr][j] = PEND;
+      }
+    }
+  }
+  // ---- left/up dedup + survivor counts per row ----
+#pragma unroll
+  for (int rr = 1; rr <= NR; rr++) {
+    if (lane == 31) s_last[rr - 1][warp] = k[rr][3];
+  }
+  __syncthreads();
+  uint32_t keepm = 0, cnt_r[NR], x_r[NR];
+#pragma unroll
+  for (int rr = 1; rr <= NR; rr++) {
+    uint64_t left = __shfl_up_sync(FULL, k[rr][3], 1);
+    if (lane == 0) left = warp > 0 ? s_last[rr - 1][warp - 1] : KEY_INVALID;
+    unsigned keep = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const uint64_t kk = k[rr][j];
+      const uint64_t lk = j == 0 ? left : k[rr][j - 1];
+      // PEND never equals a key; a pending neighbour keeps this pixel
+      if (kk != KEY_INVALID && (kk == PEND || (kk != lk && kk != k[rr - 1][j]))) keep |= 1u << j;
+    }
+    keepm |= keep << (4 * (rr - 1));
+    cnt_r[rr - 1] = __popc(keep);
+    uint32_t x = cnt_r[rr - 1];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    x_r[rr - 1] = x;
+    if (lane == 31) s_wsum[rr - 1][warp] = x;
+  }
+  __syncthreads();
+  // per row: exclusive warp offsets; rows staged back to back (pixel order)
+  for (int rr = warp; rr < NR; rr += nw) {
+    uint32_t w = lane < nw ? s_wsum[rr][lane] : 0, wx = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, wx, o);
+      if (lane >= o) wx += y;
+    }
+    if (lane < nw) s_wsum[rr][lane] = wx - w;
+    if (lane == nw - 1) s_rowbase[rr + 1] = wx;   // row total
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int rr = 0; rr < NR; rr++) {
+      const uint32_t tot = s_rowbase[rr + 1];
+      s_rowbase[rr] = run;
+      run += tot;
+    }
+    s_rowbase[NR] = run;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int rr = 1; rr <= NR; rr++) {
+    uint32_t o = s_rowbase[rr - 1] + s_wsum[rr - 1][warp] + x_r[rr - 1] - cnt_r[rr - 1];
+    const uint32_t p0 = (uint32_t)(((size_t)f * H + (r0 + rr - 1)) * W) + c0;
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+      if ((keepm >> (4 * (rr - 1) + j)) & 1u) {
+        sk[o] = k[rr][j];
+        sv[o] = p0 + j;
+        if (k[rr][j] == PEND) {
+          const uint32_t pi = atomicAdd(&s_npend, 1u);
+          if (pi < kFrontPend) s_pend[pi] = o;
+        }
+        o++;
+      }
+  }
+  __syncthreads();
+  const uint32_t run = s_rowbase[NR];
+  // publish this block's count now; its look-back runs after the exact keys
+  if (threadIdx.x == 0) atomicExch(status + bid, (bid == 0 ? LB_PRE : LB_AGG) | run);
+  // ---- exact fp64 keys of the pending pixels, one lane each ----
+  {
+    const uint32_t np = s_npend;
+    if (np <= (uint32_t)kFrontPend) {
+      for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
+        const uint32_t o = s_pend[i];
+        const uint32_t p = sv[o];
+        const uint32_t rem = p - (uint32_t)((size_t)f * H * W);
+        const uint32_t u = rem / Wu, v = rem - u * Wu;
+        int qv[3];
+        const uint64_t key = key_exact(Rd, Td, cam, u, v, depth[p], qv);
+        sk[o] = key;
+        cnt += key != KEY_INVALID ? 1u : 0u;
+      }
+    } else {
+      for (uint32_t o = threadIdx.x; o < run; o += blockDim.x)
+        if (sk[o] == PEND) {
+          const uint32_t p = sv[o];
+          const uint32_t rem = p - (uint32_t)((size_t)f * H * W);
+          const uint32_t u = rem / Wu, v = rem - u * Wu;
+          int qv[3];
+          const uint64_t key = key_exact(Rd, Td, cam, u, v, depth[p], qv);
+          sk[o] = key;
+          cnt += key != KEY_INVALID ? 1u : 0u;
+        }
+    }
+  }
+  __syncthreads();
+  // decoupled look-back over the blocks (pixel order) for the output offset
+  if (threadIdx.x == 0) {
+    unsigned long long excl = 0;
+    if (bid != 0) {
+      for (int64_t j = (int64_t)bid - 1; j >= 0; j--) {
+        unsigned long long st;
+        do {
+          st = *reinterpret_cast<volatile unsigned long long*>(status + j);
+        } while ((st & ~LB_VAL) == 0);
+        excl += st & LB_VAL;
+        if (st & LB_PRE) break;
+      }
+      atomicExch(status + bid, LB_PRE | (excl + run));
+    }
+    if (run) atomicAdd(cnts + 2, (unsigned long long)run);
+    s_rowbase[0] = (uint32_t)excl;
+  }
+  __syncthreads();
+  // copy out in pixel order (pixels resolved to invalid stay as KEY_INVALID
+  // items and sort last); the voxel bounding box over the survivors equals the
+  // box over all valid pixels (every dropped pixel repeats a survivor's key)
+  const uint32_t gbase = s_rowbase[0];
+  int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
+  for (uint32_t i = threadIdx.x; i < run; i += blockDim.x) {
+    const uint64_t key = sk[i];
+    kout[gbase + i] = key;
+    vout[gbase + i] = sv[i];
+    if (key != KEY_INVALID) {
+      const int q[3] = {(int)(key >> 42), (int)((key >> 21) & 0x1fffff), (int)(key & 0x1fffff)};
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        lo[a] = min(lo[a], q[a]);
+        hi[a] = max(hi[a], q[a]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; a++)
+    for (int o = 16; o; o >>= 1) {
+      lo[a] = min(lo[a], __shfl_xor_sync(FULL, lo[a], o));
+      hi[a] = max(hi[a], __shfl_xor_sync(FULL, hi[a], o));
+    }
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+  if (lane == 0) {
+    if (lo[0] != INT_MAX) {
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        atomicMin(&s_box[a], lo[a]);
+        atomicMax(&s_box[3 + a], hi[a]);
+      }
+    }
+    if (cnt) atomicAdd(cnts, (unsigned long long)cnt);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_box[0] != INT_MAX) {
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      atomicMin(bbox + a, s_box[a]);
+      atomicMax(bbox + 3 + a, s_box[3 + a]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- G2 radix sort
 // The sort key is the bbox-relative packing of the biased voxel fields:
 // rel = ((x-x0) << (by+bz)) | ((y-y0) << bz) | (z-z0); invalid keys map to
@@ -289,6 +610,8 @@ constexpr int STAGE_BYTES_SORT = SORT_TILE * 12;
 
 bool sort_attr_set = false;
 cudaError_t sort_init();
+bool front_attr_set = false;
+cudaError_t front_init();
 
 __global__ void __launch_bounds__(SORT_THREADS)
 sort_upsweep_kernel(const uint64_t* __restrict__ keys, int64_t n, RelKey rk, int shift, int32_t* tile_hist,
@@ -416,6 +739,14 @@ sort_downsweep_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restri
   }
 }
 
+cudaError_t front_init() {
+  if (front_attr_set) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(grid_front_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       FK_ROWS * 2048 * 12);
+  if (e == cudaSuccess) front_attr_set = true;
+  return e;
+}
+
 cudaError_t sort_init() {
   if (sort_attr_set) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(sort_downsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -515,27 +846,45 @@ cudaError_t exclusive_scan(const T* in, int64_t n, int32_t* out, int32_t* block_
 }
 
 // ---------------------------------------------------------------- G3 select
-// Over the sorted (key, pid) items: a segment head (first item of a voxel,
-// i.e. its lowest pixel id) inserts its key into the map set; if the key was
-// absent the head pixel is flagged new and remembers its sorted position.
+// Over the sorted (key, pid) items: a segment head (first item of a voxel)
+// inserts its key into the map set; if the key was absent the voxel's
+// representative pixel is flagged new and remembers the head's sorted position.
+// In pixel-ordered input the head IS the lowest pixel id; after the fused
+// front end's unordered compaction (min_scan) the representative is the
+// segment's minimum pixel id: segments of up to kSelScan items are scanned by
+// the head's thread, longer ones are queued for a warp-parallel pass.
+constexpr int kSelScan = 16;
+
+__device__ __forceinline__ void select_emit(unsigned long long* table, uint64_t mask, uint64_t key, uint32_t pid,
+                                            int64_t i, unsigned* flag_bits, int32_t* head_pos, unsigned& newc) {
+  if (hs_insert(table, mask, key)) {
+    atomicOr(flag_bits + (pid >> 5), 1u << (pid & 31));
+    head_pos[pid] = (int32_t)i;
+    newc++;
+  }
+}
+
 __global__ void __launch_bounds__(256)
 grid_select_kernel(const uint64_t* __restrict__ k, const uint32_t* __restrict__ v, int64_t n,
                    unsigned long long* table, uint64_t mask, unsigned long long* set_count, unsigned* flag_bits,
-                   int32_t* head_pos, unsigned long long* nvox, bool min_scan) {
+                   int32_t* head_pos, unsigned long long* nvox, bool min_scan, int32_t* longq,
+                   unsigned long long* nlong) {
   unsigned newc = 0, vox = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t key = k[i];
     if (key == KEY_INVALID) continue;
     if (i > 0 && k[i - 1] == key) continue;
     vox++;
-    if (hs_insert(table, mask, key)) {
-      uint32_t pid = v[i];
-      if (min_scan)   // compacted input: the representative is the min pixel id of the segment
-        for (int64_t j = i + 1; j < n && k[j] == key; j++) pid = min(pid, v[j]);
-      atomicOr(flag_bits + (pid >> 5), 1u << (pid & 31));
-      head_pos[pid] = (int32_t)i;
-      newc++;
+    uint32_t pid = v[i];
+    if (min_scan) {
+      int64_t j = i + 1;
+      for (; j < n && j <= i + kSelScan && k[j] == key; j++) pid = min(pid, v[j]);
+      if (j < n && j > i + kSelScan && k[j] == key) {   // long segment: warp pass
+        longq[atomicAdd(nlong, 1ull)] = (int32_t)i;
+        continue;
+      }
     }
+    select_emit(table, mask, key, pid, i, flag_bits, head_pos, newc);
   }
   for (int o = 16; o; o >>= 1) {
     newc += __shfl_xor_sync(FULL, newc, o);
@@ -545,6 +894,31 @@ grid_select_kernel(const uint64_t* __restrict__ k, const uint32_t* __restrict__ 
     if (newc) atomicAdd(set_count, (unsigned long long)newc);
     if (vox) atomicAdd(nvox, (unsigned long long)vox);
   }
+}
+
+// one warp per queued long segment: coalesced min over the whole segment
+__global__ void __launch_bounds__(256)
+grid_select_long_kernel(const uint64_t* __restrict__ k, const uint32_t* __restrict__ v, int64_t n,
+                        unsigned long long* table, uint64_t mask, unsigned long long* set_count, unsigned* flag_bits,
+                        int32_t* head_pos, const int32_t* __restrict__ longq, const unsigned long long* nlong) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nq = (int64_t)*nlong;
+  unsigned newc = 0;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nq;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t i = longq[w];
+    const uint64_t key = k[i];
+    uint32_t pid = 0xffffffffu;
+    for (int64_t b = i;; b += 32) {
+      const int64_t j = b + lane;
+      const bool in = j < n && k[j] == key;
+      if (in) pid = min(pid, v[j]);
+      if (__ballot_sync(FULL, in) != FULL) break;   // segment ends inside this window
+    }
+    for (int o = 16; o; o >>= 1) pid = min(pid, __shfl_xor_sync(FULL, pid, o));
+    if (lane == 0) select_emit(table, mask, key, pid, i, flag_bits, head_pos, newc);
+  }
+  if (lane == 0 && newc) atomicAdd(set_count, (unsigned long long)newc);
 }
 
 // ---------------------------------------------------------------- G5 emit
@@ -783,7 +1157,7 @@ cudaError_t launch_backproject(const double* R, const double* t, const double* i
 // Workspace layout for one batch of npix pixels.
 struct GridWs {
   size_t off_k0, off_v0, off_k1, off_v1, off_hist, off_scan_sums, off_flag, off_pos, off_head, off_lb, off_misc, total;
-  int64_t tiles;
+  int64_t tiles, lb_entries;
 };
 
 GridWs grid_ws(int64_t npix) {
@@ -803,7 +1177,10 @@ GridWs grid_ws(int64_t npix) {
   w.off_flag = take((n / 32 + 1) * 4);
   w.off_pos = take(n * 4);
   w.off_head = take(n * 4);
-  w.off_lb = take((n / CT_TILE + 2) * 8);
+  // look-back status: compaction tiles or fused front-end blocks
+  w.lb_entries = (int64_t)(n / 16 + 64);
+  if (w.lb_entries < (int64_t)(n / CT_TILE + 2)) w.lb_entries = (int64_t)(n / CT_TILE + 2);
+  w.off_lb = take((size_t)w.lb_entries * 8);
   w.off_misc = take(256);
   w.total = o;
   return w;
@@ -836,16 +1213,31 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   cudaError_t e;
   const Cam cam{in.fx, in.fy, in.cx, in.cy, in.voxel, 1.0 / in.voxel};
   const bool compact = in.mode == 0;   // first-pick: dedup runs + compaction before the sort
+  bool fused = false;                  // fused front end (unordered compaction)
   const int64_t nwords = (npix + 31) / 32;
   {
     ProfScope prof("grid_keys", s);
     init_bbox_kernel<<<1, 32, 0, s>>>(bbox, cnts); count_launches(1);
     cudaMemsetAsync(cnts + 1, 0, 40, s);
     const bool vec4 = (in.W % 4 == 0) && (reinterpret_cast<uintptr_t>(in.depth) % 16 == 0);
+    const int64_t fblocks = in.frames * ((in.H + FK_ROWS - 1) / FK_ROWS);
+    fused = compact && vec4 && in.W <= 2048 && fblocks <= w.lb_entries;
+    if (fused) {
+      const CamF cf{(float)in.cx, (float)in.cy, (float)(1.0 / in.fx), (float)(1.0 / in.fy), (float)(1.0 / in.voxel)};
+      const unsigned nt = (unsigned)((in.W / 4 + 31) / 32 * 32);
+      const size_t fsmem = (size_t)FK_ROWS * in.W * 12;
+      if ((e = front_init()) != cudaSuccess) return e;
+      unsigned* block_counter = reinterpret_cast<unsigned*>(cnts + 4);
+      cudaMemsetAsync(block_counter, 0, 4, s);
+      cudaMemsetAsync(lb_status, 0, sizeof(unsigned long long) * fblocks, s);
+      grid_front_kernel<<<(unsigned)fblocks, nt, fsmem, s>>>(in.depth, in.H, in.W, in.stride, in.rot, in.trans, cam, cf,
+                                                              k0, v0, bbox, cnts, block_counter, lb_status); count_launches(1);
+    } else {
     grid_keys_kernel<<<grid_blocks(vec4 ? npix / 4 : npix, 256, sms), 256, 0, s>>>(
         in.depth, npix, in.H, in.W, in.stride, in.rot, in.trans, cam, compact ? k1 : k0, compact ? nullptr : v0,
         bbox, cnts, vec4); count_launches(1);
-    if (compact) {
+    }
+    if (compact && !fused) {
       const int64_t ntiles = (npix + CT_TILE - 1) / CT_TILE;
       unsigned* tile_counter = reinterpret_cast<unsigned*>(cnts + 4);
       cudaMemsetAsync(tile_counter, 0, 4, s);
@@ -897,8 +1289,15 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   {
     ProfScope prof("grid_select", s);
     cudaMemsetAsync(flag, 0, (size_t)nwords * 4, s);
+    int32_t* longq = reinterpret_cast<int32_t*>(k1);   // the sort's ping-pong buffer is free now
+    cudaMemsetAsync(cnts + 3, 0, 8, s);
     grid_select_kernel<<<grid_blocks(nitems, 256, sms), 256, 0, s>>>(k0, v0, nitems, hs->table, (uint64_t)hs->cap - 1,
-                                                                     hs->count_dev, reinterpret_cast<unsigned*>(flag), head, cnts + 1, false); count_launches(1);
+                                                                     hs->count_dev, reinterpret_cast<unsigned*>(flag), head, cnts + 1, false,
+                                                                     longq, cnts + 3); count_launches(1);
+    if (false) {
+      grid_select_long_kernel<<<sms * 4, 256, 0, s>>>(k0, v0, nitems, hs->table, (uint64_t)hs->cap - 1, hs->count_dev,
+                                                      reinterpret_cast<unsigned*>(flag), head, longq, cnts + 3); count_launches(1);
+    }
   }
   {
     ProfScope prof("grid_emit", s);

@@ -142,8 +142,11 @@ def test_voxel_boundaries_bit_exact(xs):
     grid, _, _ = xs
     base = np.array([0.25 * k for k in range(1, 40)] + [0.1 * k for k in range(1, 40)], np.float32)
     d = np.concatenate([base, np.nextafter(base, np.float32(0)), np.nextafter(base, np.float32(10))])
-    H, W = 6, d.size // 6
-    depth = d[:H * W].reshape(H, W)
+    for H, W in ((6, d.size // 6), (6, 36)):   # 39 columns: unfused path; 36: fused fp32-filter front end
+        _boundaries_case(grid, d[:H * W].reshape(H, W), H, W)
+
+
+def _boundaries_case(grid, depth, H, W):
     for vs in (0.25, 0.1, 0.05, 1.0 / 3.0):
         intr = (7.0, 11.0, 2.5, 3.0)
         gs = grid.GridSampler(intr, vs)
@@ -151,6 +154,41 @@ def test_voxel_boundaries_bit_exact(xs):
         ref = og.grid_sample([(depth, np.zeros((H, W, 3), np.uint8), np.eye(3), np.zeros(3))], np.array(intr), vs,
                              set())
         assert np.array_equal(got["key"], ref["key"]) and np.array_equal(got["pid"], ref["pid"]), vs
+
+
+def test_fused_front_end_posed_boundaries(xs):
+    """Fused front end (W % 4 == 0) under non-identity poses: depths chosen so
+    many points land within float32 rounding of a voxel face; keys and pixel
+    ids must equal the fp64 oracle bit for bit."""
+    grid, _, _ = xs
+    rng = np.random.default_rng(77)
+    H, W, F = 24, 64, 3
+    intr = (50.0, 47.0, 11.5, 31.5)
+    R = []
+    for _ in range(F):
+        q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+        R.append(q * np.sign(np.linalg.det(q)))
+    R = np.stack(R)
+    T = rng.normal(scale=0.7, size=(F, 3))
+    vs = 0.02
+    D = np.empty((F, H, W), np.float32)
+    for f in range(F):
+        for u in range(H):
+            for v in range(W):
+                # choose depth so that the world z-coordinate sits on a voxel face
+                a = np.array([(u - intr[2]) / intr[0], (v - intr[3]) / intr[1], 1.0])
+                r = R[f].T @ a
+                z0 = (R[f].T @ (-T[f]))[2]
+                k = np.round((z0 + 1.5 * r[2]) / vs)
+                dd = (k * vs - z0) / r[2] if abs(r[2]) > 1e-3 else 1.5
+                D[f, u, v] = np.float32(dd if 0.2 < dd < 8 else 1.5)
+    D = np.where(rng.random(D.shape) < 0.3, np.nextafter(D, np.float32(10)), D).astype(np.float32)
+    frames = [(D[f], np.zeros((H, W, 3), np.uint8), R[f], T[f]) for f in range(F)]
+    ref = og.grid_sample(frames, np.array(intr), vs, set())
+    got = grid.GridSampler(intr, vs).sample(D, (R, T)).to_numpy()
+    assert got["n_valid"] == ref["n_valid"] and got["n_voxels"] == ref["n_voxels"]
+    for name in ("key", "pid", "mu"):
+        assert np.array_equal(got[name], ref[name]), name
 
 
 def test_radix_sort_matches_stable_argsort(xs, cuda):
