@@ -642,17 +642,56 @@ sort_upsweep_kernel(const uint64_t* __restrict__ keys, int64_t n, RelKey rk, int
   }
 }
 
+// Per-digit exclusive scan over the tiles (one CTA per digit): tile offsets
+// within the digit plus the digit total; the downsweep adds the digit base
+// (exclusive scan of the 256 totals) itself, so a pass has one scan launch.
+__global__ void __launch_bounds__(1024)
+sort_scan_digits_kernel(int32_t* __restrict__ hist, int64_t tiles, int32_t* __restrict__ digit_tot) {
+  __shared__ int32_t sm[32];
+  const int d = blockIdx.x;
+  int32_t* row = hist + (int64_t)d * tiles;
+  const int64_t per = (tiles + blockDim.x - 1) / blockDim.x;
+  const int64_t t0 = (int64_t)threadIdx.x * per, t1 = min(tiles, t0 + per);
+  int32_t sum = 0;
+  for (int64_t t = t0; t < t1; t++) sum += row[t];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t x = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t w = lane < (int)(blockDim.x >> 5) ? sm[lane] : 0, wx = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, wx, o);
+      if (lane >= o) wx += y;
+    }
+    sm[lane] = wx - w;
+    if (lane == 31) digit_tot[d] = wx;
+  }
+  __syncthreads();
+  int32_t run = sm[warp] + x - sum;
+  for (int64_t t = t0; t < t1; t++) {
+    const int32_t c = row[t];
+    row[t] = run;
+    run += c;
+  }
+}
+
 // Stable downsweep: warp w owns tile items [w*512, w*512+512) in input order;
 // ranks come from match_any per 32-item round + per-warp digit counters.  The
 // tile is then re-ordered by digit in shared memory so the global writes are
 // contiguous runs per digit (coalesced) instead of 32 scattered addresses.
 __global__ void __launch_bounds__(SORT_THREADS, 3)
 sort_downsweep_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t n, RelKey rk,
-                      int shift, const int32_t* __restrict__ scanned, int64_t tiles, uint64_t* __restrict__ kout,
-                      uint32_t* __restrict__ vout) {
+                      int shift, const int32_t* __restrict__ scanned, const int32_t* __restrict__ digit_tot,
+                      int64_t tiles, uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
   __shared__ int32_t wc[8][RADIX];
   __shared__ int32_t toff[RADIX];
   __shared__ int32_t gbase[RADIX];
+  __shared__ int32_t dbase[RADIX];
   extern __shared__ __align__(16) uint8_t stage_smem[];   // SORT_TILE keys + values (dynamic)
   uint64_t* sk = reinterpret_cast<uint64_t*>(stage_smem);
   uint32_t* sv = reinterpret_cast<uint32_t*>(stage_smem + SORT_TILE * 8);
@@ -697,8 +736,31 @@ sort_downsweep_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restri
     }
     toff[d] = run;   // tile count of digit d (scanned below)
     gbase[d] = scanned[(int64_t)d * tiles + blockIdx.x];
+    dbase[d] = digit_tot[d];
   }
   __syncthreads();
+  // digit bases: exclusive scan of the 256 digit totals
+  if (warp == 0) {
+    int32_t c[8], s2 = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      c[j] = dbase[lane * 8 + j];
+      s2 += c[j];
+    }
+    int32_t x = s2;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    int32_t run = x - s2;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      dbase[lane * 8 + j] = run;
+      run += c[j];
+    }
+  }
+  __syncthreads();
+  gbase[threadIdx.x] += dbase[threadIdx.x];
   // exclusive scan of the 256 tile counts -> tile-local digit offsets
   if (warp == 0) {
     int32_t c[8], s = 0;
@@ -1173,7 +1235,9 @@ GridWs grid_ws(int64_t npix) {
   w.off_v1 = take(n * 4);
   w.off_hist = take((size_t)RADIX * w.tiles * 4);
   const size_t scan_n = n > (size_t)RADIX * w.tiles ? n : (size_t)RADIX * w.tiles;
-  w.off_scan_sums = take(((scan_n + SCAN_TILE - 1) / SCAN_TILE + 1) * 4);
+  size_t ss = ((scan_n + SCAN_TILE - 1) / SCAN_TILE + 1) * 4;
+  if (ss < (size_t)RADIX * 4) ss = (size_t)RADIX * 4;   // also the sort's digit totals
+  w.off_scan_sums = take(ss);
   w.off_flag = take((n / 32 + 1) * 4);
   w.off_pos = take(n * 4);
   w.off_head = take(n * 4);
@@ -1280,8 +1344,8 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     ProfScope prof("grid_sort", s);
     for (int shift = 0; shift < bits; shift += 8) {
       sort_upsweep_kernel<<<(unsigned)tiles, SORT_THREADS, 0, s>>>(k0, nitems, rk, shift, hist, tiles); count_launches(1);
-      if ((e = exclusive_scan<int32_t>(hist, (int64_t)RADIX * tiles, hist, ssum, nullptr, s)) != cudaSuccess) return e;
-      sort_downsweep_kernel<<<(unsigned)tiles, SORT_THREADS, STAGE_BYTES_SORT, s>>>(k0, v0, nitems, rk, shift, hist, tiles, k1, v1); count_launches(1);
+      sort_scan_digits_kernel<<<RADIX, 1024, 0, s>>>(hist, tiles, ssum); count_launches(1);
+      sort_downsweep_kernel<<<(unsigned)tiles, SORT_THREADS, STAGE_BYTES_SORT, s>>>(k0, v0, nitems, rk, shift, hist, ssum, tiles, k1, v1); count_launches(1);
       uint64_t* tk = k0; k0 = k1; k1 = tk;
       uint32_t* tv = v0; v0 = v1; v1 = tv;
     }
@@ -1363,8 +1427,8 @@ cudaError_t radix_sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n, int bits
   if (e != cudaSuccess) return e;
   for (int shift = 0; shift < bits; shift += 8) {
     sort_upsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, 0, s>>>(k0, n, ident, shift, hist, w.tiles); count_launches(1);
-    if ((e = exclusive_scan<int32_t>(hist, (int64_t)RADIX * w.tiles, hist, ssum, nullptr, s)) != cudaSuccess) return e;
-    sort_downsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, STAGE_BYTES_SORT, s>>>(k0, v0, n, ident, shift, hist, w.tiles, k1, v1); count_launches(1);
+    sort_scan_digits_kernel<<<RADIX, 1024, 0, s>>>(hist, w.tiles, ssum); count_launches(1);
+    sort_downsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, STAGE_BYTES_SORT, s>>>(k0, v0, n, ident, shift, hist, ssum, w.tiles, k1, v1); count_launches(1);
     uint64_t* tk = k0; k0 = k1; k1 = tk;
     uint32_t* tv = v0; v0 = v1; v1 = tv;
   }
