@@ -114,6 +114,26 @@ XGS_API int xgs_vq_ring_write(const void* x, int dtype, int64_t ldx, int64_t row
 XGS_API int xgs_gather_rows_f64(const double* src, int64_t d, const int64_t* rows, int64_t n, double* dst,
                                 void* stream);
 
+/* ------------------------------------------------- codebook consumers */
+
+/* One fp64 row op over (n, k) logits, NumPy order (row max, exp(l - max),
+ * pairwise sums over k <= 8192):
+ *   mode 1  mixture_weights (core.py:473-480)  -> out (n, k)
+ *   mode 2  semantic_entropy (thinker.py:185-191) -> out_h (n)
+ *   mode 4  softmax_vjp (core.py:483-487) with upstream (n, k) -> out (n, k)
+ * Non-finite logits -> XGS_INVALID_INPUT (the reference raises); the call
+ * synchronises on `stream` to read that flag. */
+XGS_API int xgs_softmax_rows(const double* logits, int64_t n, int64_t k, int mode, const double* upstream,
+                             double* out, double* out_h, void* stream);
+/* _contrast_scores / relevance_per_gaussian (thinker.py:110-129) on decoded
+ * features F (n, d): q = 1 positive + nq-1 negative unit vectors (nq, d). */
+XGS_API int xgs_contrast_scores(const double* feats, int64_t n, int64_t d, const double* qvecs, int64_t nq,
+                                double tau, double eps, double* scores, void* stream);
+/* keys + indices for a stable descending argsort (np.argsort(-v, kind=
+ * "stable"), thinker.py:171, :202) through xgs_radix_sort_pairs_u64 with 64
+ * key bits; -0.0 ties with +0.0 as in NumPy. */
+XGS_API int xgs_desc_order_keys(const double* v, int64_t n, uint64_t* keys, uint32_t* idx, void* stream);
+
 /* ------------------------------------------------------------- GRID */
 
 /* slam.backproject (slam.py:594-598) for n points, bit-identical:

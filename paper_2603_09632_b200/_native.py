@@ -58,6 +58,9 @@ SIGNATURES = {
     "xgs_sup_gather": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _i64,
                               _i64, _vp, _vp, _vp, _vp]),
     "xgs_sup_loss": (_i32, [_vp, _vp, _vp, _i64, _i64, _f64, _vp, _vp, _vp]),
+    "xgs_softmax_rows": (_i32, [_vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
+    "xgs_contrast_scores": (_i32, [_vp, _i64, _i64, _vp, _i64, _f64, _f64, _vp, _vp]),
+    "xgs_desc_order_keys": (_i32, [_vp, _i64, _vp, _vp, _vp]),
 }
 
 

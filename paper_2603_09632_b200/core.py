@@ -270,3 +270,62 @@ class GaussianField:
     @property
     def K(self) -> int:
         return self.logits.shape[1]
+
+
+# ------------------------------------------------------------ codebook consumers
+# core.py:473-496 of the reference.  NumPy in -> NumPy out (one H2D/D2H copy per
+# call); CUDA tensors in -> CUDA tensors out.  The row ops run in libxgs
+# (xgs_softmax_rows: fp64, NumPy's max / exp / pairwise-sum order); the
+# codeword mixture softmax(logits) @ E is a plain fp64 GEMM (cuBLAS via torch).
+
+SOFTMAX_WEIGHTS, SOFTMAX_ENTROPY, SOFTMAX_VJP = 1, 2, 4
+
+
+def _logits_dev(logits):
+    host = not is_tensor(logits)
+    t = nat.require_cuda()
+    L = device_f64(logits)
+    squeeze = L.dim() == 1
+    if squeeze:
+        L = L.reshape(1, -1)
+    if L.dim() != 2:
+        raise InvalidInputError("logits must be (K,) or (N, K)")
+    return t, L.contiguous(), host, squeeze
+
+
+def _softmax_rows(L, mode, upstream=None):
+    t = nat.torch()
+    n, k = L.shape
+    out = t.empty((n, k), dtype=t.float64, device="cuda") if mode != SOFTMAX_ENTROPY else None
+    out_h = t.empty(n, dtype=t.float64, device="cuda") if mode == SOFTMAX_ENTROPY else None
+    nat.call("xgs_softmax_rows", nat.ptr(L), n, k, mode, nat.ptr(upstream), nat.ptr(out), nat.ptr(out_h),
+             nat.stream_ptr())
+    return out if mode != SOFTMAX_ENTROPY else out_h
+
+
+def _ret(x, host, squeeze):
+    if squeeze:
+        x = x[0]
+    return to_host(x) if host else x
+
+
+def mixture_weights(logits):
+    """core.py:473-480 — stable softmax over the codeword axis."""
+    t, L, host, squeeze = _logits_dev(logits)
+    return _ret(_softmax_rows(L, SOFTMAX_WEIGHTS), host, squeeze)
+
+
+def softmax_vjp(logits, upstream):
+    """core.py:483-487 — w * (upstream - sum(w * upstream))."""
+    t, L, host, squeeze = _logits_dev(logits)
+    U = device_f64(upstream).reshape(L.shape).contiguous()
+    return _ret(_softmax_rows(L, SOFTMAX_VJP, U), host, squeeze)
+
+
+def decode_feature(logits, codebook: "Codebook"):
+    """core.py:490-496 — softmax-weighted codeword mixture, (K,) or (N, K) logits."""
+    t, L, host, squeeze = _logits_dev(logits)
+    if L.shape[-1] != codebook.K:
+        raise InvalidInputError(f"logit length {L.shape[-1]} does not match codebook K={codebook.K}")
+    E = codebook.E if codebook.on_device else device_f64(codebook.E, True)
+    return _ret(t.matmul(_softmax_rows(L, SOFTMAX_WEIGHTS), E), host, squeeze)

@@ -474,4 +474,52 @@ int xgs_sup_loss(const double* pred, const double* G, const double* V, int64_t D
   return OK;
 }
 
+
+// ------------------------------------------------------- codebook consumers
+
+int xgs_softmax_rows(const double* logits, int64_t n, int64_t k, int mode, const double* upstream, double* out,
+                     double* out_h, void* stream) {
+  if (n < 0 || k < 1) return fail(INVALID_INPUT, "bad logits shape");
+  if (k > 8192) return fail(NOT_SUPPORTED, "K > 8192");
+  if (mode != CB_WEIGHTS && mode != CB_ENTROPY && mode != CB_VJP) return fail(INVALID_INPUT, "bad softmax mode");
+  if (n == 0) return OK;
+  if (!logits || ((mode != CB_ENTROPY) && !out) || (mode == CB_ENTROPY && !out_h) || (mode == CB_VJP && !upstream))
+    return fail(INVALID_INPUT, "null buffer");
+  SumPlan pk;
+  if (!build_sum_plan((int)k, &pk)) return fail(NOT_SUPPORTED, "K too large for the pairwise plan");
+  cudaStream_t s = (cudaStream_t)stream;
+  int* bad = nullptr;
+  cudaError_t e = cudaMallocAsync(&bad, sizeof(int), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int), s);
+  if (e == cudaSuccess) e = launch_softmax_rows(logits, n, k, mode, upstream, out, out_h, pk, bad, s);
+  int hbad = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (bad) cudaFreeAsync(bad, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_softmax_rows");
+  if (hbad) return fail(INVALID_INPUT, "logits must be finite");
+  return OK;
+}
+
+int xgs_contrast_scores(const double* feats, int64_t n, int64_t d, const double* qvecs, int64_t nq, double tau,
+                        double eps, double* scores, void* stream) {
+  if (n < 0 || d < 1 || d > 8192) return fail(INVALID_INPUT, "bad feature shape");
+  if (nq < 2) return fail(INVALID_INPUT, "query must carry at least one negative phrase");
+  if (n == 0) return OK;
+  if (!feats || !qvecs || !scores) return fail(INVALID_INPUT, "null buffer");
+  SumPlan pd;
+  if (!build_sum_plan((int)d, &pd)) return fail(NOT_SUPPORTED, "feature dim too large");
+  cudaError_t e = launch_contrast(feats, n, d, qvecs, nq, tau, eps, scores, pd, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_contrast_scores");
+  return OK;
+}
+
+int xgs_desc_order_keys(const double* v, int64_t n, uint64_t* keys, uint32_t* idx, void* stream) {
+  if (n < 0 || n > 0xffffffffll) return fail(INVALID_INPUT, "bad length");
+  if (n && (!v || !keys || !idx)) return fail(INVALID_INPUT, "null buffer");
+  cudaError_t e = launch_desc_keys(v, n, keys, idx, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_desc_order_keys");
+  return OK;
+}
+
 }  // extern "C"

@@ -1,0 +1,158 @@
+// Codebook consumers: the per-Gaussian softmax family of
+// core.py and the relevance / entropy / token sampling of thinker.py.
+//
+//   cb_rows_kernel     : one warp per logit row (K <= 8192), fp64.  Row max,
+//                        exp(l - max), NumPy pairwise sums over K (the same
+//                        leaf/combine order as np.sum along a contiguous
+//                        axis, see common.cuh), then per mode
+//                          WEIGHTS  mixture_weights      (core.py:473-480)
+//                          ENTROPY  semantic_entropy     (thinker.py:185-191)
+//                          VJP      softmax_vjp          (core.py:483-487)
+//                        Non-finite logits set a flag (the reference raises).
+//   cb_contrast_kernel : one warp per decoded feature row: pairwise L2 norm
+//                        (np.linalg.norm), normalise by (norm + eps), dot with
+//                        the positive and every negative query vector and take
+//                        the min over negatives of the two-way softmax
+//                        (thinker.py:110-129).
+//   cb_desc_keys_kernel: order-preserving u64 keys for a stable DESCENDING
+//                        argsort (np.argsort(-v, kind="stable")) through the
+//                        in-house radix sort (grid.cu); -0.0 folds onto +0.0
+//                        because NumPy's comparison sort treats them as ties.
+// The codeword mixture itself, softmax(logits) @ E, is a plain fp64 GEMM and
+// goes to cuBLAS from the host (core.decode_feature).
+#include "launchers.h"
+
+namespace xgs {
+
+namespace {
+
+constexpr int kCbWarps = 8;
+
+template <int MODE>
+__global__ void __launch_bounds__(kCbWarps * 32)
+cb_rows_kernel(const double* __restrict__ L, int64_t n, int64_t k, const double* __restrict__ up,
+               double* __restrict__ out, double* __restrict__ out_h, SumPlan pk, int* __restrict__ bad) {
+  __shared__ double scratch_all[kCbWarps][kMaxLeaves];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* scratch = scratch_all[warp];
+  for (int64_t r = (int64_t)blockIdx.x * kCbWarps + warp; r < n; r += (int64_t)gridDim.x * kCbWarps) {
+    const double* l = L + r * k;
+    double m = -__longlong_as_double(0x7ff0000000000000ll);
+    bool fin = true;
+    for (int64_t i = lane; i < k; i += 32) {
+      const double v = __ldg(l + i);
+      fin = fin && isfinite(v);
+      m = fmax(m, v);
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
+    if (!__all_sync(FULL, fin)) {
+      if (lane == 0) atomicOr(bad, 1);
+      continue;
+    }
+    // vq-style pairwise sums: S = sum exp(l - max)
+    const double S = warp_pairwise(pk, [&](int i) { return exp(dsub(__ldg(l + i), m)); }, scratch, lane);
+    if (MODE == CB_WEIGHTS) {
+      for (int64_t i = lane; i < k; i += 32) out[r * k + i] = ddiv(exp(dsub(__ldg(l + i), m)), S);
+    } else if (MODE == CB_ENTROPY) {
+      const double h = warp_pairwise(
+          pk,
+          [&](int i) {
+            const double p = ddiv(exp(dsub(__ldg(l + i), m)), S);
+            return p > 0.0 ? dmul(p, log(p)) : 0.0;
+          },
+          scratch, lane);
+      if (lane == 0) out_h[r] = -h;
+    } else {   // CB_VJP: w * (up - sum(w * up))
+      const double* u = up + r * k;
+      const double inner = warp_pairwise(
+          pk, [&](int i) { return dmul(ddiv(exp(dsub(__ldg(l + i), m)), S), __ldg(u + i)); }, scratch, lane);
+      for (int64_t i = lane; i < k; i += 32) {
+        const double w = ddiv(exp(dsub(__ldg(l + i), m)), S);
+        out[r * k + i] = dmul(w, dsub(__ldg(u + i), inner));
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kCbWarps * 32)
+cb_contrast_kernel(const double* __restrict__ F, int64_t n, int64_t d, const double* __restrict__ Q, int64_t nq,
+                   double tau, double eps, double* __restrict__ scores, SumPlan pd) {
+  __shared__ double scratch_all[kCbWarps][kMaxLeaves];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* scratch = scratch_all[warp];
+  for (int64_t r = (int64_t)blockIdx.x * kCbWarps + warp; r < n; r += (int64_t)gridDim.x * kCbWarps) {
+    const double* f = F + r * d;
+    const double ss = warp_pairwise(
+        pd,
+        [&](int i) {
+          const double v = __ldg(f + i);
+          return dmul(v, v);
+        },
+        scratch, lane);
+    const double den = dadd(sqrt(ss), eps);
+    double pos = 0.0, score = 1.0;
+    for (int64_t q = 0; q < nq; q++) {
+      double acc = 0.0;
+      for (int64_t i = lane; i < d; i += 32) acc = fma(ddiv(__ldg(f + i), den), __ldg(Q + q * d + i), acc);
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+      if (q == 0) {
+        pos = acc;
+      } else {
+        const double margin = dmul(tau, dsub(pos, acc));
+        score = fmin(score, ddiv(1.0, dadd(1.0, exp(-margin))));
+      }
+    }
+    if (lane == 0) scores[r] = score;
+  }
+}
+
+__global__ void cb_desc_keys_kernel(const double* __restrict__ v, int64_t n, uint64_t* __restrict__ keys,
+                                    uint32_t* __restrict__ idx) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double x = v[i];
+    if (x == 0.0) x = 0.0;   // -0.0 == +0.0 for the comparison sort
+    const uint64_t b = (uint64_t)__double_as_longlong(x);
+    const uint64_t asc = (b >> 63) ? ~b : (b | 0x8000000000000000ull);   // ascending order of x
+    keys[i] = ~asc;                                                      // descending
+    idx[i] = (uint32_t)i;
+  }
+}
+
+unsigned cb_blocks(int64_t rows) {
+  int64_t b = (rows + kCbWarps - 1) / kCbWarps;
+  if (b > 148 * 32) b = 148 * 32;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+cudaError_t launch_softmax_rows(const double* logits, int64_t n, int64_t k, int mode, const double* up, double* out,
+                                double* out_h, const SumPlan& pk, int* bad, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  ProfScope prof("cb_rows", s);
+  switch (mode) {
+    case CB_WEIGHTS: cb_rows_kernel<CB_WEIGHTS><<<cb_blocks(n), kCbWarps * 32, 0, s>>>(logits, n, k, up, out, out_h, pk, bad); break;
+    case CB_ENTROPY: cb_rows_kernel<CB_ENTROPY><<<cb_blocks(n), kCbWarps * 32, 0, s>>>(logits, n, k, up, out, out_h, pk, bad); break;
+    default: cb_rows_kernel<CB_VJP><<<cb_blocks(n), kCbWarps * 32, 0, s>>>(logits, n, k, up, out, out_h, pk, bad);
+  }
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_contrast(const double* F, int64_t n, int64_t d, const double* Q, int64_t nq, double tau, double eps,
+                            double* scores, const SumPlan& pd, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  ProfScope prof("cb_contrast", s);
+  cb_contrast_kernel<<<cb_blocks(n), kCbWarps * 32, 0, s>>>(F, n, d, Q, nq, tau, eps, scores, pd); count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_desc_keys(const double* v, int64_t n, uint64_t* keys, uint32_t* idx, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  cb_desc_keys_kernel<<<(unsigned)b, 256, 0, s>>>(v, n, keys, idx); count_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace xgs

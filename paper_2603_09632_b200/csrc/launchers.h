@@ -157,4 +157,12 @@ cudaError_t launch_sup_gather(const void* P, int p_dtype, int64_t Hf, int64_t Wf
 cudaError_t launch_sup_loss(const double* pred, const double* G, const double* V, int64_t D, int64_t cells, double lam,
                             double* acc, double* cot, cudaStream_t st);
 
+// ---------------- codebook consumers (codebook.cu) ----------------
+enum CbMode : int { CB_WEIGHTS = 1, CB_ENTROPY = 2, CB_VJP = 4 };
+cudaError_t launch_softmax_rows(const double* logits, int64_t n, int64_t k, int mode, const double* up, double* out,
+                                double* out_h, const SumPlan& pk, int* bad, cudaStream_t s);
+cudaError_t launch_contrast(const double* F, int64_t n, int64_t d, const double* Q, int64_t nq, double tau, double eps,
+                            double* scores, const SumPlan& pd, cudaStream_t s);
+cudaError_t launch_desc_keys(const double* v, int64_t n, uint64_t* keys, uint32_t* idx, cudaStream_t s);
+
 }  // namespace xgs

@@ -229,14 +229,56 @@ def gen_supervision():
     np.savez_compressed(os.path.join(OUT, "supervision.npz"), **out)
 
 
+def gen_thinker():
+    """core.mixture_weights / softmax_vjp / decode_feature and thinker.* (§8(f) #3)."""
+    from semsplat import thinker
+    from semsplat.core import decode_feature, mixture_weights, softmax_vjp
+    rng = np.random.default_rng(400)
+    out = {}
+    for tag, (n, K, D) in {"a": (300, 37, 24), "b": (129, 256, 64)}.items():
+        L = rng.normal(scale=3.0, size=(n, K))
+        L[0] = 0.0                            # uniform row: maximum entropy
+        L[1] = L[2]                           # duplicate rows: entropy ties -> lower index first
+        L[3, 5] = 40.0                        # near one-hot
+        L[4] = L[7]
+        E = rng.normal(size=(K, D))
+        up = rng.normal(size=(n, K))
+        cb = make_cb(E)
+        out[f"{tag}_L"], out[f"{tag}_E"], out[f"{tag}_up"] = L, E, up
+        out[f"{tag}_w"] = mixture_weights(L)
+        out[f"{tag}_vjp"] = softmax_vjp(L, up)
+        out[f"{tag}_dec"] = decode_feature(L, cb)
+        out[f"{tag}_dec1"] = decode_feature(L[5], cb)
+        out[f"{tag}_H"] = thinker.semantic_entropy(L)
+        field = GaussianField(mu=np.zeros((n, 3)), quat=np.tile([1.0, 0, 0, 0], (n, 1)), scale=np.ones((n, 3)),
+                              opacity=np.ones(n), color=np.zeros((n, 3)), logits=L)
+        enc = thinker.StubTextEncoder(D, region_table=E[:6])
+        q = thinker.TextQuery.from_prompt("region:2", enc)
+        out[f"{tag}_qpos"], out[f"{tag}_qneg"] = q.positive, np.stack(q.negatives)
+        out[f"{tag}_rel"] = thinker.relevance_per_gaussian(field, cb, q)
+        res = thinker.query_field(field, cb, q)
+        out[f"{tag}_mask"], out[f"{tag}_fallback"] = res.mask, np.array(res.fallback_used)
+        m2, fb2 = thinker.mask_gaussians(out[f"{tag}_rel"], 0.999999, fallback_frac=0.05)
+        out[f"{tag}_mask_fb"], out[f"{tag}_fb2"] = m2, np.array(fb2)
+        ts = thinker.sample_tokens(field, cb, 17)
+        out[f"{tag}_tok_idx"], out[f"{tag}_tok_H"], out[f"{tag}_tok_F"] = ts.indices, ts.entropies, ts.features
+        ts2 = thinker.sample_tokens(field, cb, n + 5)
+        out[f"{tag}_tok2_idx"], out[f"{tag}_tok2_clamped"] = ts2.indices, np.array(ts2.clamped)
+        W = rng.random(size=(K, 5, 7))
+        out[f"{tag}_wmap"] = W
+        out[f"{tag}_relpix"] = thinker.relevance_per_pixel([type("M", (), {"data": W})()], [cb], q)
+    out["neg_phrases_vecs"] = np.stack(thinker.StubTextEncoder(24).negatives())
+    out["hash_vec"] = thinker.StubTextEncoder(24).encode("a lamp")
+    np.savez_compressed(os.path.join(OUT, "thinker.npz"), **out)
+
+
+GENERATORS = {"supervision": gen_supervision, "distances": gen_distances, "assign": gen_assign,
+              "accumulate": gen_accumulate_ema, "online": gen_online, "backproject": gen_backproject,
+              "densify": gen_densify, "thinker": gen_thinker}
+
 if __name__ == "__main__":
-    gen_supervision()
-    gen_distances()
-    gen_assign()
-    gen_accumulate_ema()
-    gen_online()
-    gen_backproject()
-    gen_densify()
+    for name in (sys.argv[1:] or list(GENERATORS)):
+        GENERATORS[name]()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))
