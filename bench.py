@@ -374,6 +374,63 @@ def run_targets(torch, iters, cpu=True):
     return out
 
 
+def run_consumers(torch, iters, cpu=True):
+    """codebook consumers over a C4-sized map (about 2M
+    Gaussians, K=512 logits, D=768 codebook): semantic_entropy (HBM-bound fused
+    softmax + p log p over the fp64 logits), sample_tokens (entropy + stable
+    descending radix sort + decode of the top M) and relevance_per_gaussian
+    (decode = softmax rows + fp64 GEMM, then the contrast-score kernel)."""
+    from paper_2603_09632_b200 import thinker as xt
+    from paper_2603_09632_b200.core import Codebook, FeatureReservoir
+    n, K, D, M = 1 << 21, 512, 768, 4096
+    g = torch.Generator(device="cuda")
+    g.manual_seed(60)
+    L = torch.randn(n, K, generator=g, device="cuda", dtype=torch.float64) * 2.0
+    E = torch.randn(K, D, generator=g, device="cuda", dtype=torch.float64)
+    E = E / E.norm(dim=1, keepdim=True)
+    cb = Codebook._make(E, torch.zeros(K, dtype=torch.float64, device="cuda"), E.clone(), 0.99, 1e-5,
+                        FeatureReservoir(16, D))
+    field = type("DeviceField", (), {"logits": L, "__len__": lambda self: n})()
+    enc = xt.StubTextEncoder(D)
+    q = xt.TextQuery.from_prompt("a chair", enc)
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    pk, _ = peaks()
+    ms_h = timed(lambda: xt.semantic_entropy(L), iters)
+    ent_bytes = n * K * 8 + n * 8
+    ms_tok = timed(lambda: xt.sample_tokens(field, cb, M), max(1, iters // 2))
+    ms_rel = timed(lambda: xt.relevance_per_gaussian(field, cb, q), 1)
+    out = {"gaussians": n, "K": K, "D": D,
+           "semantic_entropy": {"ms": ms_h, "GB_per_s": ent_bytes / (ms_h * 1e-3) / 1e9,
+                                "hbm_frac": ent_bytes / (ms_h * 1e-3) / 1e9 / pk["hbm_gbs"],
+                                "algorithmic_bytes": ent_bytes},
+           "sample_tokens": {"ms": ms_tok, "M": M},
+           "relevance_per_gaussian": {"ms": ms_rel, "decode_gemm_fp64_TFLOPs": 2.0 * n * K * D / (ms_rel * 1e-3) / 1e12},
+           "workload": "2^21 Gaussians x K=512 fp64 logits (C4 map size), D=768 codebook, M=4096 tokens; "
+                       "synthetic N(0, 2^2) logits"}
+    if cpu:
+        from oracle import thinker as ot
+        Lh = L[:65536].cpu().numpy()
+        t0 = time.perf_counter()
+        ot.semantic_entropy(Lh)
+        el = time.perf_counter() - t0
+        out["cpu_baseline"] = {"semantic_entropy_ms_extrapolated": el * 1e3 * n / Lh.shape[0], "cores": 1,
+                               "kind": "port", "sample": "65536 rows through oracle/thinker.py (NumPy), x32"}
+    del L, E, cb, field
+    torch.cuda.empty_cache()
+    return out
+
+
 def cpu_port_rate(x_host, E, seconds=10.0, threads=None):
     """The reference's assign+accumulate restated in C (oracle/oracle.c), timed
     on host cores over row chunks until ~`seconds` elapse (bounded sample)."""
@@ -559,6 +616,9 @@ def main():
     targets = None
     if rank == 0 and world == 1 and not args.no_grid:
         targets = run_targets(torch, 10, cpu=not args.no_cpu)
+    consumers = None
+    if rank == 0 and world == 1 and not args.no_grid:
+        consumers = run_consumers(torch, 5, cpu=not args.no_cpu)
     c5 = None
     if rank == 0 and world == 1 and args.c5_iters > 0:
         del x
@@ -589,6 +649,7 @@ def main():
             "stream": stream,
             "c5_shard": c5,
             "targets": targets,
+            "consumers": consumers,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -28,17 +28,27 @@ namespace {
 
 constexpr int kCbWarps = 8;
 
-template <int MODE>
+// exp(l - max) of the row is evaluated once into per-warp shared memory
+// (CACHE: K <= kCbCacheK) and reused by the sums and the outputs.  The entropy
+// uses p = e * (1/S) and log p = (l - max) - log S instead of e / S and
+// log(e / S) (one division and one log per row, not per element; each differs
+// by a few ulps, inside the 1e-13 relative tolerance of the parity tests).
+constexpr int kCbCacheK = 1024;
+
+template <int MODE, bool CACHE>
 __global__ void __launch_bounds__(kCbWarps * 32)
 cb_rows_kernel(const double* __restrict__ L, int64_t n, int64_t k, const double* __restrict__ up,
                double* __restrict__ out, double* __restrict__ out_h, SumPlan pk, int* __restrict__ bad) {
   __shared__ double scratch_all[kCbWarps][kMaxLeaves];
+  extern __shared__ double ecache_all[];   // CACHE: kCbWarps x k
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* scratch = scratch_all[warp];
+  double* ec = CACHE ? ecache_all + (size_t)warp * k : nullptr;
   for (int64_t r = (int64_t)blockIdx.x * kCbWarps + warp; r < n; r += (int64_t)gridDim.x * kCbWarps) {
     const double* l = L + r * k;
     double m = -__longlong_as_double(0x7ff0000000000000ll);
     bool fin = true;
+#pragma unroll 8
     for (int64_t i = lane; i < k; i += 32) {
       const double v = __ldg(l + i);
       fin = fin && isfinite(v);
@@ -49,28 +59,32 @@ cb_rows_kernel(const double* __restrict__ L, int64_t n, int64_t k, const double*
       if (lane == 0) atomicOr(bad, 1);
       continue;
     }
-    // vq-style pairwise sums: S = sum exp(l - max)
-    const double S = warp_pairwise(pk, [&](int i) { return exp(dsub(__ldg(l + i), m)); }, scratch, lane);
+    if (CACHE) {
+#pragma unroll 4   // independent exp chains per lane (the fp64 pipe is latency-bound otherwise)
+      for (int64_t i = lane; i < k; i += 32) ec[i] = exp(dsub(__ldg(l + i), m));
+      __syncwarp();
+    }
+    auto ex = [&](int i) { return CACHE ? ec[i] : exp(dsub(__ldg(l + i), m)); };
+    // S = sum exp(l - max) in NumPy's pairwise order
+    const double S = warp_pairwise(pk, ex, scratch, lane);
     if (MODE == CB_WEIGHTS) {
-      for (int64_t i = lane; i < k; i += 32) out[r * k + i] = ddiv(exp(dsub(__ldg(l + i), m)), S);
+      for (int64_t i = lane; i < k; i += 32) out[r * k + i] = ddiv(ex((int)i), S);
     } else if (MODE == CB_ENTROPY) {
+      const double logS = log(S), invS = ddiv(1.0, S);
       const double h = warp_pairwise(
           pk,
           [&](int i) {
-            const double p = ddiv(exp(dsub(__ldg(l + i), m)), S);
-            return p > 0.0 ? dmul(p, log(p)) : 0.0;
+            const double p = dmul(ex(i), invS);   // within 1 ulp of e / S
+            return p > 0.0 ? dmul(p, dsub(dsub(__ldg(l + i), m), logS)) : 0.0;
           },
           scratch, lane);
       if (lane == 0) out_h[r] = -h;
     } else {   // CB_VJP: w * (up - sum(w * up))
       const double* u = up + r * k;
-      const double inner = warp_pairwise(
-          pk, [&](int i) { return dmul(ddiv(exp(dsub(__ldg(l + i), m)), S), __ldg(u + i)); }, scratch, lane);
-      for (int64_t i = lane; i < k; i += 32) {
-        const double w = ddiv(exp(dsub(__ldg(l + i), m)), S);
-        out[r * k + i] = dmul(w, dsub(__ldg(u + i), inner));
-      }
+      const double inner = warp_pairwise(pk, [&](int i) { return dmul(ddiv(ex(i), S), __ldg(u + i)); }, scratch, lane);
+      for (int64_t i = lane; i < k; i += 32) out[r * k + i] = dmul(ddiv(ex((int)i), S), dsub(__ldg(u + i), inner));
     }
+    __syncwarp();   // the cache is rewritten by the next row
   }
 }
 
@@ -130,10 +144,24 @@ cudaError_t launch_softmax_rows(const double* logits, int64_t n, int64_t k, int 
                                 double* out_h, const SumPlan& pk, int* bad, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   ProfScope prof("cb_rows", s);
-  switch (mode) {
-    case CB_WEIGHTS: cb_rows_kernel<CB_WEIGHTS><<<cb_blocks(n), kCbWarps * 32, 0, s>>>(logits, n, k, up, out, out_h, pk, bad); break;
-    case CB_ENTROPY: cb_rows_kernel<CB_ENTROPY><<<cb_blocks(n), kCbWarps * 32, 0, s>>>(logits, n, k, up, out, out_h, pk, bad); break;
-    default: cb_rows_kernel<CB_VJP><<<cb_blocks(n), kCbWarps * 32, 0, s>>>(logits, n, k, up, out, out_h, pk, bad);
+  const bool cache = k <= kCbCacheK;
+  const size_t smem = cache ? sizeof(double) * kCbWarps * (size_t)k : 0;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(cb_rows_kernel<CB_WEIGHTS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbWarps * kCbCacheK * 8);
+    cudaFuncSetAttribute(cb_rows_kernel<CB_ENTROPY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbWarps * kCbCacheK * 8);
+    cudaFuncSetAttribute(cb_rows_kernel<CB_VJP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbWarps * kCbCacheK * 8);
+    attr_set = true;
+  }
+  const unsigned b = cb_blocks(n);
+  const int T = kCbWarps * 32;
+  switch (mode * 2 + (cache ? 1 : 0)) {
+    case CB_WEIGHTS * 2 + 1: cb_rows_kernel<CB_WEIGHTS, true><<<b, T, smem, s>>>(logits, n, k, up, out, out_h, pk, bad); break;
+    case CB_WEIGHTS * 2: cb_rows_kernel<CB_WEIGHTS, false><<<b, T, 0, s>>>(logits, n, k, up, out, out_h, pk, bad); break;
+    case CB_ENTROPY * 2 + 1: cb_rows_kernel<CB_ENTROPY, true><<<b, T, smem, s>>>(logits, n, k, up, out, out_h, pk, bad); break;
+    case CB_ENTROPY * 2: cb_rows_kernel<CB_ENTROPY, false><<<b, T, 0, s>>>(logits, n, k, up, out, out_h, pk, bad); break;
+    case CB_VJP * 2 + 1: cb_rows_kernel<CB_VJP, true><<<b, T, smem, s>>>(logits, n, k, up, out, out_h, pk, bad); break;
+    default: cb_rows_kernel<CB_VJP, false><<<b, T, 0, s>>>(logits, n, k, up, out, out_h, pk, bad);
   }
   count_launches(1);
   return cudaGetLastError();
