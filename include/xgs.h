@@ -114,6 +114,45 @@ XGS_API int xgs_vq_ring_write(const void* x, int dtype, int64_t ldx, int64_t row
 XGS_API int xgs_gather_rows_f64(const double* src, int64_t d, const int64_t* rows, int64_t n, double* dst,
                                 void* stream);
 
+/* ------------------------------------------------ lattice rasterizer */
+
+/* build_blend_pairs (rasterizer.py:89-191): depth-sorted, 3-sigma-culled,
+ * transmittance-terminated blend pairs of a Gaussian field on the lattice
+ * rows = row0 + row_step*i (i < n_rows), cols = col0 + col_step*j (j < n_cols).
+ * Gaussian arrays are DEVICE fp64 (mu (n,3), quat wxyz (n,4), scale (n,3),
+ * opacity (n)); the pose (world->camera R row-major, t) and intrinsics are
+ * host values.  The handle owns the pairs (pixel-segmented, depth order
+ * within a pixel); build synchronises on `stream` to size them. */
+typedef struct {
+  int64_t n;
+  const double* mu;
+  const double* quat;
+  const double* scale;
+  const double* opacity;
+  double R[9], t[3];
+  double fx, fy, cx, cy, near_z, far_z;
+  int64_t n_rows, row0, row_step, n_cols, col0, col_step;
+  double term_threshold, cutoff_sigma, eig_floor;
+} xgs_raster_in;
+XGS_API int xgs_raster_build(const xgs_raster_in* in, void** handle, int64_t* n_pairs, int64_t* blend_steps,
+                             void* stream);
+/* BlendPairs arrays (any may be NULL): gauss/pixel int64, weight, alpha',
+ * T_before, depth fp64, alive u8, each of length n_pairs. */
+XGS_API int xgs_raster_fetch(void* handle, int64_t* gauss, int64_t* pixel, double* weight, double* alpha_prime,
+                             double* t_before, uint8_t* alive, double* depth, void* stream);
+/* _accumulate_channels / render (rasterizer.py:194-244): out (C, P) =
+ * sum of weight * payload[gauss, c] per lattice pixel (pair order, as
+ * np.bincount); alpha_out / depth_out (P) nullable. */
+XGS_API int xgs_raster_accumulate(void* handle, const double* payload, int64_t C, double* out, double* alpha_out,
+                                  double* depth_out, void* stream);
+/* render_argmax_ids (rasterizer.py:290-306): Gaussian of the largest blend
+ * weight per pixel, -1 where uncovered. */
+XGS_API int xgs_raster_argmax(void* handle, int64_t* out, void* stream);
+/* feature_gradients' blend cotangents (rasterizer.py:309-335): fg (n, D) =
+ * np.add.at over pairs of weight * upstream[:, pixel], upstream (D, P). */
+XGS_API int xgs_raster_vjp(void* handle, const double* upstream, int64_t D, double* feature_grads, void* stream);
+XGS_API int xgs_raster_free(void* handle);
+
 /* ------------------------------------------------- codebook consumers */
 
 /* One fp64 row op over (n, k) logits, NumPy order (row max, exp(l - max),

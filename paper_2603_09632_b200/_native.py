@@ -59,6 +59,12 @@ SIGNATURES = {
                               _i64, _vp, _vp, _vp, _vp]),
     "xgs_sup_loss": (_i32, [_vp, _vp, _vp, _i64, _i64, _f64, _vp, _vp, _vp]),
     "xgs_softmax_rows": (_i32, [_vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
+    "xgs_raster_build": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+    "xgs_raster_fetch": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "xgs_raster_accumulate": (_i32, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "xgs_raster_argmax": (_i32, [_vp, _vp, _vp]),
+    "xgs_raster_vjp": (_i32, [_vp, _vp, _i64, _vp, _vp]),
+    "xgs_raster_free": (_i32, [_vp]),
     "xgs_contrast_scores": (_i32, [_vp, _i64, _i64, _vp, _i64, _f64, _f64, _vp, _vp]),
     "xgs_desc_order_keys": (_i32, [_vp, _i64, _vp, _vp, _vp]),
 }
@@ -77,6 +83,15 @@ class GridResult(ctypes.Structure):
     _fields_ = [("capacity", _i64), ("key", _vp), ("pid", _vp), ("mu", _vp), ("color", _vp), ("scale", _vp),
                 ("depth", _vp), ("feat", _vp), ("count", _vp), ("n_new", _i64), ("n_valid", _i64),
                 ("n_voxels", _i64), ("n_sorted", _i64), ("sort_passes", _i64)]
+
+
+class RasterIn(ctypes.Structure):
+    """Mirror of xgs_raster_in (include/xgs.h)."""
+    _fields_ = [("n", _i64), ("mu", _vp), ("quat", _vp), ("scale", _vp), ("opacity", _vp),
+                ("R", _f64 * 9), ("t", _f64 * 3), ("fx", _f64), ("fy", _f64), ("cx", _f64), ("cy", _f64),
+                ("near_z", _f64), ("far_z", _f64), ("n_rows", _i64), ("row0", _i64), ("row_step", _i64),
+                ("n_cols", _i64), ("col0", _i64), ("col_step", _i64), ("term_threshold", _f64),
+                ("cutoff_sigma", _f64), ("eig_floor", _f64)]
 
 
 def lib():

@@ -522,4 +522,72 @@ int xgs_desc_order_keys(const double* v, int64_t n, uint64_t* keys, uint32_t* id
   return OK;
 }
 
+
+// ------------------------------------------------------- lattice rasterizer
+
+int xgs_raster_build(const xgs_raster_in* in, void** handle, int64_t* n_pairs, int64_t* blend_steps, void* stream) {
+  if (!in || !handle) return fail(INVALID_INPUT, "null argument");
+  *handle = nullptr;
+  if (in->n < 0 || in->n > 0x7fffffffll || in->n_rows < 0 || in->n_cols < 0 || in->row_step < 1 || in->col_step < 1)
+    return fail(INVALID_INPUT, "bad raster shape");
+  if (in->n_rows * in->n_cols > 0x7fffffffll) return fail(NOT_SUPPORTED, "lattice too large");
+  if (in->n > 0 && (!in->mu || !in->quat || !in->scale || !in->opacity)) return fail(INVALID_INPUT, "null field");
+  if (!(in->fx > 0) || !(in->fy > 0) || !(in->near_z > 0 && in->near_z < in->far_z))
+    return fail(INVALID_INPUT, "bad intrinsics");
+  RasterIn r;
+  r.n = in->n;
+  r.mu = in->mu;
+  r.quat = in->quat;
+  r.scale = in->scale;
+  r.opacity = in->opacity;
+  std::memcpy(r.R, in->R, sizeof(r.R));
+  std::memcpy(r.t, in->t, sizeof(r.t));
+  r.fx = in->fx; r.fy = in->fy; r.cx = in->cx; r.cy = in->cy; r.near_z = in->near_z; r.far_z = in->far_z;
+  r.n_rows = in->n_rows; r.row0 = in->row0; r.row_step = in->row_step;
+  r.n_cols = in->n_cols; r.col0 = in->col0; r.col_step = in->col_step;
+  r.term = in->term_threshold; r.cutoff = in->cutoff_sigma; r.eig_floor = in->eig_floor;
+  RasterState* st = nullptr;
+  cudaError_t e = raster_build(r, &st, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    raster_free(st);
+    return cuda_fail(e, "xgs_raster_build");
+  }
+  raster_stats(st, n_pairs, blend_steps, nullptr);
+  *handle = st;
+  return OK;
+}
+
+int xgs_raster_fetch(void* handle, int64_t* gauss, int64_t* pixel, double* weight, double* alpha_prime, double* t_before,
+                     uint8_t* alive, double* depth, void* stream) {
+  if (!handle) return fail(INVALID_INPUT, "null handle");
+  cudaError_t e = raster_fetch(static_cast<RasterState*>(handle), gauss, pixel, weight, alpha_prime, t_before, alive,
+                               depth, (cudaStream_t)stream);
+  return e == cudaSuccess ? OK : cuda_fail(e, "xgs_raster_fetch");
+}
+
+int xgs_raster_accumulate(void* handle, const double* payload, int64_t C, double* out, double* alpha_out,
+                          double* depth_out, void* stream) {
+  if (!handle || C < 0 || (C > 0 && (!payload || !out))) return fail(INVALID_INPUT, "bad accumulate arguments");
+  cudaError_t e = raster_accumulate(static_cast<RasterState*>(handle), payload, C, out, alpha_out, depth_out,
+                                    (cudaStream_t)stream);
+  return e == cudaSuccess ? OK : cuda_fail(e, "xgs_raster_accumulate");
+}
+
+int xgs_raster_argmax(void* handle, int64_t* out, void* stream) {
+  if (!handle || !out) return fail(INVALID_INPUT, "bad argmax arguments");
+  cudaError_t e = raster_argmax(static_cast<RasterState*>(handle), out, (cudaStream_t)stream);
+  return e == cudaSuccess ? OK : cuda_fail(e, "xgs_raster_argmax");
+}
+
+int xgs_raster_vjp(void* handle, const double* upstream, int64_t D, double* feature_grads, void* stream) {
+  if (!handle || D < 1 || !upstream || !feature_grads) return fail(INVALID_INPUT, "bad vjp arguments");
+  cudaError_t e = raster_vjp(static_cast<RasterState*>(handle), upstream, D, feature_grads, (cudaStream_t)stream);
+  return e == cudaSuccess ? OK : cuda_fail(e, "xgs_raster_vjp");
+}
+
+int xgs_raster_free(void* handle) {
+  raster_free(static_cast<RasterState*>(handle));
+  return OK;
+}
+
 }  // extern "C"

@@ -1407,6 +1407,13 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   return cudaGetLastError();
 }
 
+// exclusive scan of int32 counts (out may alias in); block_sums needs
+// n / 4096 + 2 entries; *grand (device, nullable) receives the total
+cudaError_t exclusive_scan_i32(const int32_t* in, int64_t n, int32_t* out, int32_t* block_sums, int32_t* grand,
+                               cudaStream_t s) {
+  return exclusive_scan<int32_t>(in, n, out, block_sums, grand, s);
+}
+
 // standalone in-house radix sort of (u64 key, u32 value) pairs on bits [0, bits)
 cudaError_t radix_sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n, int bits, void* ws, size_t ws_bytes,
                              cudaStream_t s) {

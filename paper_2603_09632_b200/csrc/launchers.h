@@ -148,6 +148,8 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
                         cudaStream_t s);
 cudaError_t radix_sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n, int bits, void* ws, size_t ws_bytes,
                              cudaStream_t s);
+cudaError_t exclusive_scan_i32(const int32_t* in, int64_t n, int32_t* out, int32_t* block_sums, int32_t* grand,
+                               cudaStream_t s);
 
 // ---------------- supervision targets (supervision.cu) ----------------
 cudaError_t launch_sup_gather(const void* P, int p_dtype, int64_t Hf, int64_t Wf, const int64_t* S, const double* Phi,
@@ -156,6 +158,29 @@ cudaError_t launch_sup_gather(const void* P, int p_dtype, int64_t Hf, int64_t Wf
                               cudaStream_t st);
 cudaError_t launch_sup_loss(const double* pred, const double* G, const double* V, int64_t D, int64_t cells, double lam,
                             double* acc, double* cot, cudaStream_t st);
+
+// ---------------- lattice rasterizer (raster.cu) ----------------
+struct RasterIn {
+  int64_t n;
+  const double* mu;
+  const double* quat;
+  const double* scale;
+  const double* opacity;
+  double R[9], t[3];
+  double fx, fy, cx, cy, near_z, far_z;
+  int64_t n_rows, row0, row_step, n_cols, col0, col_step;
+  double term, cutoff, eig_floor;
+};
+struct RasterState;
+cudaError_t raster_build(const RasterIn& in, RasterState** out, cudaStream_t s);
+void raster_free(RasterState* st);
+void raster_stats(RasterState* st, int64_t* npairs, int64_t* blend_steps, int64_t* nvis);
+cudaError_t raster_fetch(RasterState* st, int64_t* gauss, int64_t* pixel, double* weight, double* alpha, double* tb,
+                         uint8_t* alive, double* depth, cudaStream_t s);
+cudaError_t raster_accumulate(RasterState* st, const double* payload, int64_t C, double* out, double* alpha_out,
+                              double* depth_out, cudaStream_t s);
+cudaError_t raster_argmax(RasterState* st, int64_t* out, cudaStream_t s);
+cudaError_t raster_vjp(RasterState* st, const double* upstream, int64_t D, double* fg, cudaStream_t s);
 
 // ---------------- codebook consumers (codebook.cu) ----------------
 enum CbMode : int { CB_WEIGHTS = 1, CB_ENTROPY = 2, CB_VJP = 4 };

@@ -272,9 +272,69 @@ def gen_thinker():
     np.savez_compressed(os.path.join(OUT, "thinker.npz"), **out)
 
 
+def raster_scene(rng, n, H, W, K=6, D=5):
+    from semsplat.core import rot_to_quat
+    mu = np.column_stack([rng.uniform(-1.5, 1.5, n), rng.uniform(-1.5, 1.5, n), rng.uniform(-0.5, 4.0, n)])
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    scale = np.exp(rng.uniform(np.log(0.01), np.log(0.3), (n, 3)))
+    opacity = rng.uniform(0.05, 1.0, n)
+    opacity[: n // 10] = 0.999                     # near-opaque splats: early termination
+    color = rng.random((n, 3))
+    logits = rng.normal(size=(n, K))
+    field = GaussianField(mu=mu, quat=q, scale=scale, opacity=opacity, color=color, logits=logits)
+    ang = rng.normal(scale=0.1, size=3)
+    c, s_ = np.cos(ang), np.sin(ang)
+    Rz = np.array([[c[2], -s_[2], 0], [s_[2], c[2], 0], [0, 0, 1]])
+    Rx = np.array([[1, 0, 0], [0, c[0], -s_[0]], [0, s_[0], c[0]]])
+    pose = CameraPose(Rz @ Rx, np.array([0.05, -0.1, 1.2]))
+    intr = CameraIntrinsics(fx=0.9 * W, fy=0.85 * W, cx=(H - 1) / 2 + 0.3, cy=(W - 1) / 2 - 0.2, height=H, width=W)
+    E = rng.normal(size=(K, D))
+    return field, pose, intr, E
+
+
+def gen_raster():
+    """rasterizer.build_blend_pairs / render / render_channels_grid / argmax /
+    feature_gradients on seeded scenes (dense all-pairs path and the
+    per-Gaussian bounding-box path of the reference)."""
+    from semsplat import rasterizer as rz
+    from semsplat.supervision import GridSpec
+    rng = np.random.default_rng(500)
+    out = {}
+    for tag, (n, H, W, s, oh, ow) in {"dense": (150, 24, 32, 1, 0, 0), "bbox": (1200, 24, 44, 1, 0, 0),
+                                       "grid": (1200, 24, 44, 3, 1, 2)}.items():
+        field, pose, intr, E = raster_scene(rng, n, H, W)
+        for k in ("mu", "quat", "scale", "opacity", "color", "logits"):
+            out[f"{tag}_{k}"] = getattr(field, k)
+        out[f"{tag}_R"], out[f"{tag}_t"], out[f"{tag}_E"] = pose.rotation, pose.translation, E
+        out[f"{tag}_intr"] = np.array([intr.fx, intr.fy, intr.cx, intr.cy, H, W, intr.near, intr.far])
+        grid = GridSpec(H=H, W=W, s=s, o_h=oh, o_w=ow)
+        out[f"{tag}_grid"] = np.array([H, W, s, oh, ow])
+        bp = rz.build_blend_pairs(field, pose, intr, grid.rows(), grid.cols())
+        for k in ("gauss", "pixel", "weight", "alpha_prime", "t_before", "alive", "depth"):
+            out[f"{tag}_bp_{k}"] = getattr(bp, k)
+        out[f"{tag}_bp_steps"] = np.array(bp.blend_steps)
+        if s == 1:
+            r = rz.render(field, pose, intr)
+            out[f"{tag}_r_color"], out[f"{tag}_r_depth"], out[f"{tag}_r_alpha"] = r.color, r.depth, r.alpha
+            out[f"{tag}_steps"] = np.array(r.blend_steps)
+            out[f"{tag}_argmax"] = rz.render_argmax_ids(field, pose, intr)
+        payload = rng.normal(size=(n, 4))
+        out[f"{tag}_payload"] = payload
+        out[f"{tag}_chan"] = rz.render_channels_grid(field, payload, pose, intr, grid).data
+        cb = make_cb(E)
+        up = rng.normal(size=(E.shape[1], grid.H_s, grid.W_s))
+        out[f"{tag}_up"] = up
+        fgr = rz.feature_gradients(field, cb, pose, intr, grid, up)
+        out[f"{tag}_fg"], out[f"{tag}_lg"] = fgr.feature_grads, fgr.logit_grads
+        out[f"{tag}_feat"] = rz.render_features_grid(field, cb, pose, intr, grid).data
+    np.savez_compressed(os.path.join(OUT, "raster.npz"), **out)
+
+
 GENERATORS = {"supervision": gen_supervision, "distances": gen_distances, "assign": gen_assign,
               "accumulate": gen_accumulate_ema, "online": gen_online, "backproject": gen_backproject,
-              "densify": gen_densify, "thinker": gen_thinker}
+              "densify": gen_densify, "thinker": gen_thinker,
+              "raster": gen_raster}
 
 if __name__ == "__main__":
     for name in (sys.argv[1:] or list(GENERATORS)):
