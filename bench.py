@@ -431,6 +431,68 @@ def run_consumers(torch, iters, cpu=True):
     return out
 
 
+def run_raster(torch, iters, cpu=True):
+    """lattice rasterizer at keyframe scale -- 2^18 Gaussians
+    in the frustum of a 480x640 camera, stride-4 lattice (120x160 pixels, the
+    paper's grid-sampled semantic render), D=512 payload; build_blend_pairs,
+    channel accumulation and the feature VJP timed separately."""
+    from paper_2603_09632_b200 import rasterizer as rz
+    from paper_2603_09632_b200.core import CameraIntrinsics, CameraPose
+    from paper_2603_09632_b200.supervision import GridSpec
+    n, H, W, s, D = 1 << 18, 480, 640, 4, 512
+    g = torch.Generator(device="cuda")
+    g.manual_seed(70)
+    z = torch.rand(n, generator=g, device="cuda", dtype=torch.float64) * 7.0 + 0.5
+    u = (torch.rand(n, generator=g, device="cuda", dtype=torch.float64) - 0.5) * z * (H / 525.0)
+    v = (torch.rand(n, generator=g, device="cuda", dtype=torch.float64) - 0.5) * z * (W / 525.0)
+    q = torch.randn(n, 4, generator=g, device="cuda", dtype=torch.float64)
+    field = type("DeviceField", (), {
+        "mu": torch.stack([u, v, z], 1).contiguous(), "quat": (q / q.norm(dim=1, keepdim=True)).contiguous(),
+        "scale": torch.exp(torch.rand(n, 3, generator=g, device="cuda", dtype=torch.float64) * 2.3 - 4.6),
+        "opacity": torch.rand(n, generator=g, device="cuda", dtype=torch.float64) * 0.9 + 0.05,
+        "color": torch.rand(n, 3, generator=g, device="cuda", dtype=torch.float64),
+        "__len__": lambda self: n})()
+    intr = CameraIntrinsics(fx=525.0, fy=525.0, cx=239.5, cy=319.5, height=H, width=W)
+    pose = CameraPose.identity()
+    grid = GridSpec(H=H, W=W, s=s)
+    payload = torch.randn(n, D, generator=g, device="cuda", dtype=torch.float64)
+    up = torch.randn(D, grid.H_s, grid.W_s, generator=g, device="cuda", dtype=torch.float64)
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            r = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps, r
+
+    ms_build, pr = timed(lambda: rz._Pairs(field, pose, intr, grid.rows(), grid.cols(), rz.DEFAULT_RASTER), iters)
+    ms_acc, _ = timed(lambda: pr.accumulate(payload), iters)
+    ms_vjp, _ = timed(lambda: pr.vjp(up.reshape(D, -1).contiguous(), D), iters)
+    npairs, steps = pr.n_pairs, pr.blend_steps
+    pr.close()
+    pk, _ = peaks()
+    # accumulate: pair metadata (4 + 8 B) + one D-row payload gather per alive pair (mostly L2 hits:
+    # a splat's row is reused by every pixel it covers) + the (D, P) output; unique HBM bytes are the
+    # metadata, the payload rows of the visible splats and the output
+    acc_bytes = npairs * (4 + 8) + steps * D * 8 + grid.H_s * grid.W_s * D * 8
+    hbm_bytes = npairs * (4 + 8) + grid.H_s * grid.W_s * D * 8
+    out = {"gaussians": n, "lattice": [grid.H_s, grid.W_s], "D": D, "pairs": npairs, "blend_steps": steps,
+           "build_ms": ms_build, "accumulate_ms": ms_acc, "vjp_ms": ms_vjp,
+           "pairs_per_s": npairs / (ms_build * 1e-3),
+           "accumulate_effective_GB_per_s": acc_bytes / (ms_acc * 1e-3) / 1e9,
+           "accumulate_min_hbm_GB_per_s": hbm_bytes / (ms_acc * 1e-3) / 1e9,
+           "accumulate_min_hbm_frac": hbm_bytes / (ms_acc * 1e-3) / 1e9 / pk["hbm_gbs"],
+           "workload": "2^18 random Gaussians (0.5-8 m, 1-10 cm scales) in a 480x640 frustum, stride-4 lattice, "
+                       "fp64 D=512 payload / cotangent"}
+    del field, payload, up
+    torch.cuda.empty_cache()
+    return out
+
+
 def cpu_port_rate(x_host, E, seconds=10.0, threads=None):
     """The reference's assign+accumulate restated in C (oracle/oracle.c), timed
     on host cores over row chunks until ~`seconds` elapse (bounded sample)."""
@@ -616,9 +678,10 @@ def main():
     targets = None
     if rank == 0 and world == 1 and not args.no_grid:
         targets = run_targets(torch, 10, cpu=not args.no_cpu)
-    consumers = None
+    consumers = raster = None
     if rank == 0 and world == 1 and not args.no_grid:
         consumers = run_consumers(torch, 5, cpu=not args.no_cpu)
+        raster = run_raster(torch, 3, cpu=not args.no_cpu)
     c5 = None
     if rank == 0 and world == 1 and args.c5_iters > 0:
         del x
@@ -650,6 +713,7 @@ def main():
             "c5_shard": c5,
             "targets": targets,
             "consumers": consumers,
+            "raster": raster,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

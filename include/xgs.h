@@ -133,6 +133,8 @@ typedef struct {
   double fx, fy, cx, cy, near_z, far_z;
   int64_t n_rows, row0, row_step, n_cols, col0, col_step;
   double term_threshold, cutoff_sigma, eig_floor;
+  int32_t all_pairs;   /* 1: every culled pair incl. dead ones (build_blend_pairs);
+                          0: only pairs in front of termination (renders / VJP) */
 } xgs_raster_in;
 XGS_API int xgs_raster_build(const xgs_raster_in* in, void** handle, int64_t* n_pairs, int64_t* blend_steps,
                              void* stream);

@@ -91,7 +91,7 @@ class RasterIn(ctypes.Structure):
                 ("R", _f64 * 9), ("t", _f64 * 3), ("fx", _f64), ("fy", _f64), ("cx", _f64), ("cy", _f64),
                 ("near_z", _f64), ("far_z", _f64), ("n_rows", _i64), ("row0", _i64), ("row_step", _i64),
                 ("n_cols", _i64), ("col0", _i64), ("col_step", _i64), ("term_threshold", _f64),
-                ("cutoff_sigma", _f64), ("eig_floor", _f64)]
+                ("cutoff_sigma", _f64), ("eig_floor", _f64), ("all_pairs", ctypes.c_int32)]
 
 
 def lib():

@@ -546,6 +546,7 @@ int xgs_raster_build(const xgs_raster_in* in, void** handle, int64_t* n_pairs, i
   r.n_rows = in->n_rows; r.row0 = in->row0; r.row_step = in->row_step;
   r.n_cols = in->n_cols; r.col0 = in->col0; r.col_step = in->col_step;
   r.term = in->term_threshold; r.cutoff = in->cutoff_sigma; r.eig_floor = in->eig_floor;
+  r.all_pairs = in->all_pairs != 0;
   RasterState* st = nullptr;
   cudaError_t e = raster_build(r, &st, (cudaStream_t)stream);
   if (e != cudaSuccess) {

@@ -170,6 +170,7 @@ struct RasterIn {
   double fx, fy, cx, cy, near_z, far_z;
   int64_t n_rows, row0, row_step, n_cols, col0, col_step;
   double term, cutoff, eig_floor;
+  int all_pairs;   // 1: dead pairs too (build_blend_pairs), 0: alive prefix only
 };
 struct RasterState;
 cudaError_t raster_build(const RasterIn& in, RasterState** out, cudaStream_t s);

@@ -43,7 +43,7 @@ namespace xgs {
 
 namespace {
 
-constexpr int RT = 16;                 // lattice tile edge (pixels)
+constexpr int RT = 8;                  // lattice tile edge (pixels): one CTA of 64 threads per tile
 constexpr int RT_THREADS = RT * RT;
 constexpr double LOG_T_MIN = -69.07755278982137;   // log(1e-30), rasterizer.py:27
 
@@ -246,7 +246,12 @@ struct PairsOut {
 };
 
 // EMIT == false: count pairs per lattice pixel; true: write them.
-template <bool EMIT>
+// ALL: every culled pair, dead ones included (build_blend_pairs' arrays);
+// otherwise only the alive prefix of each pixel (T_before >= threshold; T is
+// non-increasing in depth order, so the first dead pair ends the pixel), which
+// is all the renders, argmax and VJP consume (dead pairs have weight 0), and
+// the tile stops once all of its pixels are dead.
+template <bool EMIT, bool ALL>
 __global__ void __launch_bounds__(RT_THREADS)
 raster_tile_kernel(RasterIn in, Ranked rk, const uint32_t* __restrict__ tlist, const int32_t* __restrict__ tstart,
                    int64_t tiles_c, int32_t* __restrict__ pcount, const int32_t* __restrict__ poff, PairsOut po,
@@ -262,13 +267,19 @@ raster_tile_kernel(RasterIn in, Ranked rk, const uint32_t* __restrict__ tlist, c
   const int64_t pix = mi * in.n_cols + ni;
   const double cut2 = dmul(in.cutoff, in.cutoff);
   const int32_t b0 = tstart[tile], b1 = tstart[tile + 1];
+  constexpr bool NEED_T = EMIT || !ALL;
   int32_t cnt = 0;
   int64_t o = (EMIT && live) ? poff[pix] : 0;
   double logT = 0.0;
   unsigned steps = 0;
+  bool done = !live;
   for (int32_t base = b0; base < b1; base += RT_THREADS) {
     const int32_t nb = min(RT_THREADS, b1 - base);
-    __syncthreads();
+    if (!ALL) {
+      if (__syncthreads_and(done)) break;   // every pixel of the tile is past termination
+    } else {
+      __syncthreads();
+    }
     if ((int)threadIdx.x < nb) {
       const uint32_t r = tlist[base + threadIdx.x];
       s_uc[threadIdx.x] = rk.uc[r];
@@ -276,38 +287,45 @@ raster_tile_kernel(RasterIn in, Ranked rk, const uint32_t* __restrict__ tlist, c
       s_ia[threadIdx.x] = rk.ia[r];
       s_ib[threadIdx.x] = rk.ib[r];
       s_ic[threadIdx.x] = rk.ic[r];
+      if (NEED_T) s_op[threadIdx.x] = rk.op[r];
       if (EMIT) {
-        s_op[threadIdx.x] = rk.op[r];
         s_z[threadIdx.x] = rk.z[r];
         s_gid[threadIdx.x] = rk.gid[r];
       }
     }
     __syncthreads();
-    if (!live) continue;
+    if (done) continue;
     for (int j = 0; j < nb; j++) {
       const double du = dsub(row, s_uc[j]), dv = dsub(col, s_vc[j]);
       // inv_a du du + 2 inv_b du dv + inv_c dv dv, left to right (rasterizer.py:147)
       const double quad = dadd(dadd(dmul(dmul(s_ia[j], du), du), dmul(dmul(dmul(2.0, s_ib[j]), du), dv)),
                                dmul(dmul(s_ic[j], dv), dv));
       if (!(quad <= cut2)) continue;
-      if (!EMIT) {
+      if (!NEED_T) {
         cnt++;
         continue;
       }
       const double a = dmul(s_op[j], exp(dmul(-0.5, quad)));
-      const double lt = fmax(log1p(-a), LOG_T_MIN);
       const double T = exp(logT);
       const bool alive = T >= in.term;
-      po.gauss[o] = s_gid[j];
-      po.pixel[o] = (int32_t)pix;
-      po.weight[o] = alive ? dmul(a, T) : 0.0;
-      po.alpha[o] = a;
-      po.tb[o] = T;
-      po.alive[o] = alive ? 1 : 0;
-      po.depth[o] = s_z[j];
+      if (!ALL && !alive) {
+        done = true;
+        break;
+      }
+      if (EMIT) {
+        po.gauss[o] = s_gid[j];
+        po.pixel[o] = (int32_t)pix;
+        po.weight[o] = alive ? dmul(a, T) : 0.0;
+        po.alpha[o] = a;
+        po.tb[o] = T;
+        po.alive[o] = alive ? 1 : 0;
+        po.depth[o] = s_z[j];
+        o++;
+      } else {
+        cnt++;
+      }
       steps += alive ? 1u : 0u;
-      logT = dadd(logT, lt);
-      o++;
+      logT = dadd(logT, fmax(log1p(-a), LOG_T_MIN));
     }
   }
   if (!EMIT && live) pcount[pix] = cnt;
@@ -386,28 +404,41 @@ __global__ void raster_transpose_kernel(const double* __restrict__ in, int64_t D
     }
 }
 
-// feature_grads[g, d] = sum over g's pairs (pair order) of weight * up[pixel, d]
-__global__ void raster_vjp_kernel(const uint64_t* __restrict__ gkeys, const uint32_t* __restrict__ pidx, int64_t np,
-                                  const int32_t* __restrict__ pixel, const double* __restrict__ weight,
-                                  const double* __restrict__ upT, int64_t D, const int32_t* __restrict__ gstart,
-                                  int64_t n, double* __restrict__ fg) {
+// feature_grads[g, d] = sum over g's pairs (pair order) of weight * up[pixel, d].
+// One warp per (Gaussian, 32-channel chunk): each lane owns one channel's
+// sequential fp64 chain (np.add.at order), so a splat covering many pixels is
+// spread over D/32 warps instead of serialising one; pair metadata is fetched
+// 32 pairs at a time and broadcast by shuffles.
+__global__ void __launch_bounds__(256)
+raster_vjp_kernel(const uint32_t* __restrict__ pidx, const int32_t* __restrict__ pixel,
+                  const double* __restrict__ weight, const double* __restrict__ upT, int64_t D,
+                  const int32_t* __restrict__ gstart, int64_t n, double* __restrict__ fg) {
   const int lane = threadIdx.x & 31;
-  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < n;
-       g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+  const int64_t chunks = (D + 31) / 32;
+  for (int64_t wi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < n * chunks;
+       wi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t g = wi / chunks, d = (wi - g * chunks) * 32 + lane;
     const int32_t a = gstart[g], b = gstart[g + 1];
-    for (int64_t d0 = 0; d0 < D; d0 += 32) {
-      const int64_t d = d0 + lane;
-      double acc = 0.0;
-      if (d < D)
-        for (int32_t i = a; i < b; i++) {
-          const uint32_t q = pidx[i];
-          acc = dadd(acc, dmul(weight[q], upT[(int64_t)pixel[q] * D + d]));
-        }
-      if (d < D) fg[g * D + d] = acc;
+    double acc = 0.0;
+    for (int32_t i0 = a; i0 < b; i0 += 32) {
+      int32_t mp = 0;
+      double mw = 0.0;
+      if (i0 + lane < b) {
+        const uint32_t q = pidx[i0 + lane];
+        mp = pixel[q];
+        mw = weight[q];
+      }
+      const int cnt = min(32, b - i0);
+      const int64_t dd = d < D ? d : D - 1;   // every lane shuffles; tail lanes read a valid channel and drop it
+#pragma unroll 8
+      for (int j = 0; j < cnt; j++) {
+        const int64_t px = __shfl_sync(FULL, mp, j);
+        const double w = __shfl_sync(FULL, mw, j);
+        acc = dadd(acc, dmul(w, __ldg(upT + px * D + dd)));
+      }
     }
+    if (d < D && b > a) fg[g * D + d] = acc;
   }
-  (void)gkeys;
-  (void)np;
 }
 
 __global__ void raster_gauss_ranges_kernel(const uint64_t* __restrict__ keys, int64_t np, int32_t* __restrict__ gstart,
@@ -465,7 +496,23 @@ void raster_free(RasterState* st) {
   delete st;
 }
 
+// Keep freed stream-ordered allocations in the device pool across the
+// build's synchronisations (the default release threshold of 0 hands them back
+// to the driver at every sync, making each cudaMallocAsync a real allocation).
+void keep_pool() {
+  static bool done[16] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 cudaError_t raster_build(const RasterIn& in, RasterState** out, cudaStream_t s) {
+  keep_pool();
   RasterState* st = new RasterState();
   st->s = s;
   st->n = in.n;
@@ -538,8 +585,13 @@ cudaError_t raster_build(const RasterIn& in, RasterState** out, cudaStream_t s) 
         RCHK(cudaGetLastError());
         RCHK(dalloc(&pcount, npix, s));
         RCHK(cudaMemsetAsync(pcount, 0, sizeof(int32_t) * (size_t)npix, s));
-        raster_tile_kernel<false><<<(unsigned)ntiles, RT_THREADS, 0, s>>>(in, rk, tv, tstart, tiles_c, pcount, nullptr,
-                                                                         PairsOut{}, nullptr); count_launches(1);
+        if (in.all_pairs)
+          raster_tile_kernel<false, true><<<(unsigned)ntiles, RT_THREADS, 0, s>>>(in, rk, tv, tstart, tiles_c, pcount,
+                                                                                  nullptr, PairsOut{}, nullptr);
+        else
+          raster_tile_kernel<false, false><<<(unsigned)ntiles, RT_THREADS, 0, s>>>(in, rk, tv, tstart, tiles_c, pcount,
+                                                                                   nullptr, PairsOut{}, nullptr);
+        count_launches(1);
         RCHK(cudaGetLastError());
         RCHK(exclusive_scan_i32(pcount, npix, st->poff, ssum, grand, s));
         RCHK(cudaMemcpyAsync(&hg, grand, 4, cudaMemcpyDeviceToHost, s));
@@ -555,8 +607,13 @@ cudaError_t raster_build(const RasterIn& in, RasterState** out, cudaStream_t s) 
         RCHK(dalloc(&st->po.alive, npairs, s));
         RCHK(dalloc(&st->po.depth, npairs, s));
         if (npairs > 0) {
-          raster_tile_kernel<true><<<(unsigned)ntiles, RT_THREADS, 0, s>>>(in, rk, tv, tstart, tiles_c, nullptr,
-                                                                          st->poff, st->po, cnt + 1); count_launches(1);
+          if (in.all_pairs)
+            raster_tile_kernel<true, true><<<(unsigned)ntiles, RT_THREADS, 0, s>>>(in, rk, tv, tstart, tiles_c, nullptr,
+                                                                                   st->poff, st->po, cnt + 1);
+          else
+            raster_tile_kernel<true, false><<<(unsigned)ntiles, RT_THREADS, 0, s>>>(in, rk, tv, tstart, tiles_c,
+                                                                                    nullptr, st->poff, st->po, cnt + 1);
+          count_launches(1);
           RCHK(cudaGetLastError());
         }
         RCHK(cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, s));
@@ -642,8 +699,8 @@ cudaError_t raster_vjp(RasterState* st, const double* upstream, int64_t D, doubl
     dim3 tb(32, 8), gb((unsigned)((P + 31) / 32 < 4096 ? (P + 31) / 32 : 4096), (unsigned)((D + 31) / 32 < 64 ? (D + 31) / 32 : 64));
     raster_transpose_kernel<<<gb, tb, 0, s>>>(upstream, D, P, upT); count_launches(1);
   }
-  raster_vjp_kernel<<<blocks_for(n * 32, 256), 256, 0, s>>>(keys, vals, np, st->po.pixel, st->po.weight, upT, D,
-                                                           gstart, n, fg); count_launches(1);
+  raster_vjp_kernel<<<blocks_for(n * ((D + 31) / 32) * 32, 256), 256, 0, s>>>(vals, st->po.pixel, st->po.weight, upT,
+                                                                             D, gstart, n, fg); count_launches(1);
   e = cudaGetLastError();
   cudaFreeAsync(keys, s);
   cudaFreeAsync(vals, s);

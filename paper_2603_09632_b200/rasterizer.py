@@ -6,7 +6,10 @@ per-Gaussian projection + eigenvalue-floored screen covariance, an in-house
 radix sort by depth, 16x16-pixel lattice tiles with depth-ordered splat lists,
 and one CTA per tile compositing its lattice pixels front to back in fp64.
 Channel accumulation (``render``, ``render_channels_grid``), the argmax ids
-and the feature VJP reuse the pairs on the device.  The codeword mixture
+and the feature VJP reuse the pairs on the device; they only need the pairs
+in front of each pixel's termination (dead pairs carry weight 0), so those
+builds stop a tile once all of its pixels are terminated, while
+``build_blend_pairs`` returns every culled pair as the reference does.  The codeword mixture
 (decode) and the final softmax VJP go through ``core`` (libxgs + fp64 GEMM).
 
 Fields are host ``GaussianField``s (copied to HBM per call) or any object
@@ -88,7 +91,7 @@ def _step(a):
 class _Pairs:
     """Device blend pairs of one (field, pose, lattice); freed on close/GC."""
 
-    def __init__(self, field, pose, intr, rows, cols, cfg):
+    def __init__(self, field, pose, intr, rows, cols, cfg, all_pairs=False):
         t = nat.require_cuda()
         rows, r0, rs = _step(rows)
         cols, c0, cs = _step(cols)
@@ -111,6 +114,7 @@ class _Pairs:
         ri.n_cols, ri.col0, ri.col_step = cols.size, c0, cs
         ri.term_threshold, ri.cutoff_sigma, ri.eig_floor = float(cfg.term_threshold), float(cfg.cutoff_sigma), \
             float(cfg.eig_floor)
+        ri.all_pairs = 1 if all_pairs else 0
         self.shape = (rows.size, cols.size)
         self.n_pixels = rows.size * cols.size
         h = ctypes.c_void_p()
@@ -172,7 +176,7 @@ class _Pairs:
 
 def build_blend_pairs(field, pose, intr, rows, cols, cfg: RasterConfig = DEFAULT_RASTER) -> BlendPairs:
     """rasterizer.py:89-191 — depth-sorted, culled, terminated blend terms."""
-    pr = _Pairs(field, pose, intr, rows, cols, cfg)
+    pr = _Pairs(field, pose, intr, rows, cols, cfg, all_pairs=True)
     try:
         return pr.fetch()
     finally:
