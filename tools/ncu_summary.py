@@ -12,7 +12,8 @@ METRICS = [
     ("dram__bytes_read.sum", "DRAM read (MB)", None),
     ("dram__bytes_write.sum", "DRAM write (MB)", None),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % peak", None),
-    ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor pipe %", None),
+    ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor pipe (realtime) %", None),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe %", None),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 %", None),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %", None),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %", None),
