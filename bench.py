@@ -175,9 +175,11 @@ def run_grid(torch, steps, cpu=True):
         ms = float(np.median(times))
         npix = GRID_F * GRID_H * GRID_W
         pk_, _ = peaks()
-        # sort: per 8-bit pass the upsweep reads the keys (8 B) and the downsweep reads
-        # and writes key + pixel id (12 + 12 B) -> 32 B per item per pass
-        sort_bytes = 32.0 * n_sorted * passes
+        # sort: relative keys computed once (read 8 B, write 4 B; u32 keys when the bbox-relative key
+        # fits 32 bits, i.e. <= 4 passes) and unpacked once after (read 4, write 8); per 8-bit pass the
+        # upsweep reads the key (4 B) and the downsweep reads and writes key + pixel id (8 + 8 B)
+        kb = 4 if passes <= 4 else 8
+        sort_bytes = float(n_sorted) * (passes * (kb + 2 * (kb + 4)) + 2 * (8 + kb))
         sort_gbs = sort_bytes / (prof["grid_sort"] * 1e-3) / 1e9 if prof["grid_sort"] else None
         # keys + compaction: depth read 4 B + key write 8 B per pixel, compaction reads the
         # key 3x (self, left, up; L2 for the neighbours) and writes 12 B per surviving item
@@ -185,7 +187,7 @@ def run_grid(torch, steps, cpu=True):
         out[str(voxel)] = {"Mpts_per_s": npix / (ms * 1e-3) / 1e6, "ms_per_batch": ms, "pixels": npix,
                            "valid_points": n_valid, "new_voxels": n_new, "map_voxels_before": map_size,
                            "sorted_items": n_sorted, "sort_passes": passes, "per_kernel_ms": prof,
-                           "roofline": {"bound": "hbm", "kernel": "radix sort (upsweep + stable downsweep)",
+                           "roofline": {"bound": "hbm", "kernel": "radix sort (rekey + upsweep/scan/stable downsweep passes + unpack)",
                                         "achieved": sort_gbs, "peak": pk_["hbm_gbs"], "unit": "GB/s",
                                         "frac": sort_gbs / pk_["hbm_gbs"] if sort_gbs else None,
                                         "algorithmic_bytes": sort_bytes},

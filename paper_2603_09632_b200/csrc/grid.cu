@@ -606,31 +606,31 @@ constexpr int SORT_THREADS = 256;
 constexpr int SORT_ITEMS = 16;                       // per thread
 constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS; // 4096
 constexpr int RADIX = 256;
-constexpr int STAGE_BYTES_SORT = SORT_TILE * 12;
+constexpr int STAGE_BYTES_SORT = SORT_TILE * 12;   // u64 keys + u32 values (u32 keys use 8 B)
 
 bool sort_attr_set = false;
 cudaError_t sort_init();
 bool front_attr_set = false;
 cudaError_t front_init();
 
+template <typename K>
 __global__ void __launch_bounds__(SORT_THREADS)
-sort_upsweep_kernel(const uint64_t* __restrict__ keys, int64_t n, RelKey rk, int shift, int32_t* tile_hist,
-                    int64_t tiles) {
+sort_upsweep_kernel(const K* __restrict__ keys, int64_t n, int shift, int32_t* tile_hist, int64_t tiles) {
   __shared__ int32_t h[8][RADIX];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 8 * RADIX; i += SORT_THREADS) (&h[0][0])[i] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * SORT_TILE + (int64_t)warp * (SORT_TILE / 8);
-  uint64_t k[SORT_ITEMS];
+  K k[SORT_ITEMS];
 #pragma unroll
   for (int r = 0; r < SORT_ITEMS; r++) {   // all loads first (memory-level parallelism)
     const int64_t i = base + r * 32 + lane;
-    k[r] = i < n ? __ldg(keys + i) : KEY_INVALID;
+    k[r] = i < n ? __ldg(keys + i) : (K)0;
   }
 #pragma unroll
   for (int r = 0; r < SORT_ITEMS; r++) {
     const bool ok = base + r * 32 + lane < n;
-    const int dg = ok ? (int)((rk(k[r]) >> shift) & (RADIX - 1)) : -1;
+    const int dg = ok ? (int)((k[r] >> shift) & (RADIX - 1)) : -1;
     const unsigned peers = __match_any_sync(FULL, dg);   // one smem atomic per distinct digit
     if (dg >= 0 && lane == __ffs(peers) - 1) atomicAdd(&h[warp][dg], __popc(peers));
   }
@@ -639,6 +639,30 @@ sort_upsweep_kernel(const uint64_t* __restrict__ keys, int64_t n, RelKey rk, int
     int32_t s = 0;
     for (int w = 0; w < 8; w++) s += h[w][d];
     tile_hist[(int64_t)d * tiles + blockIdx.x] = s;   // digit-major
+  }
+}
+
+// bbox-relative sort keys, computed once before the passes (K = u32 when the
+// relative key fits 32 bits: 4-byte keys halve the sort's key traffic)
+template <typename K>
+__global__ void rekey_kernel(const uint64_t* __restrict__ kin, int64_t n, RelKey rk, K* __restrict__ kout) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    kout[i] = (K)rk(kin[i]);
+}
+
+// back to the biased 63-bit voxel keys after the sort (select / emit use them)
+template <typename K>
+__global__ void unrekey_kernel(const K* __restrict__ kin, int64_t n, RelKey rk, int bits, uint64_t* __restrict__ kout) {
+  const uint64_t all = bits >= 64 ? ~0ull : ((1ull << bits) - 1);
+  const uint64_t mz = (1ull << rk.bz) - 1, my = (1ull << rk.by) - 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = (uint64_t)kin[i];
+    if ((r & all) == all) {
+      kout[i] = KEY_INVALID;
+      continue;
+    }
+    const uint64_t z = (r & mz) + rk.z0, y = ((r >> rk.bz) & my) + rk.y0, x = (r >> (rk.by + rk.bz)) + rk.x0;
+    kout[i] = (x << 42) | (y << 21) | z;
   }
 }
 
@@ -684,37 +708,38 @@ sort_scan_digits_kernel(int32_t* __restrict__ hist, int64_t tiles, int32_t* __re
 // ranks come from match_any per 32-item round + per-warp digit counters.  The
 // tile is then re-ordered by digit in shared memory so the global writes are
 // contiguous runs per digit (coalesced) instead of 32 scattered addresses.
+template <typename K>
 __global__ void __launch_bounds__(SORT_THREADS, 3)
-sort_downsweep_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t n, RelKey rk,
-                      int shift, const int32_t* __restrict__ scanned, const int32_t* __restrict__ digit_tot,
-                      int64_t tiles, uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
+sort_downsweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t n, int shift,
+                      const int32_t* __restrict__ scanned, const int32_t* __restrict__ digit_tot, int64_t tiles,
+                      K* __restrict__ kout, uint32_t* __restrict__ vout) {
   __shared__ int32_t wc[8][RADIX];
   __shared__ int32_t toff[RADIX];
   __shared__ int32_t gbase[RADIX];
   __shared__ int32_t dbase[RADIX];
   extern __shared__ __align__(16) uint8_t stage_smem[];   // SORT_TILE keys + values (dynamic)
-  uint64_t* sk = reinterpret_cast<uint64_t*>(stage_smem);
-  uint32_t* sv = reinterpret_cast<uint32_t*>(stage_smem + SORT_TILE * 8);
+  K* sk = reinterpret_cast<K*>(stage_smem);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(stage_smem + SORT_TILE * sizeof(K));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   for (int i = threadIdx.x; i < 8 * RADIX; i += SORT_THREADS) (&wc[0][0])[i] = 0;
   __syncthreads();
   const int64_t tile0 = (int64_t)blockIdx.x * SORT_TILE;
   const int64_t base = tile0 + (int64_t)warp * (SORT_TILE / 8);
-  uint64_t k[SORT_ITEMS];
+  K k[SORT_ITEMS];
   uint32_t v[SORT_ITEMS];
   int16_t rank[SORT_ITEMS];
   uint8_t dg[SORT_ITEMS];
 #pragma unroll
   for (int r = 0; r < SORT_ITEMS; r++) {   // all loads first (memory-level parallelism)
     const int64_t i = base + r * 32 + lane;
-    k[r] = i < n ? __ldg(kin + i) : KEY_INVALID;
+    k[r] = i < n ? __ldg(kin + i) : (K)0;
     v[r] = i < n ? __ldg(vin + i) : 0u;
   }
 #pragma unroll
   for (int r = 0; r < SORT_ITEMS; r++) {
     const bool ok = base + r * 32 + lane < n;
-    const int d = ok ? (int)((rk(k[r]) >> shift) & (RADIX - 1)) : -1;
+    const int d = ok ? (int)((k[r] >> shift) & (RADIX - 1)) : -1;
     const unsigned peers = __match_any_sync(FULL, d);
     int rr = -1;
     if (d >= 0) rr = wc[warp][d] + __popc(peers & lt);
@@ -793,8 +818,8 @@ sort_downsweep_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restri
   __syncthreads();
   const int cnt = (int)min((int64_t)SORT_TILE, n - tile0);
   for (int i = threadIdx.x; i < cnt; i += SORT_THREADS) {
-    const uint64_t key = sk[i];
-    const int d = (int)((rk(key) >> shift) & (RADIX - 1));
+    const K key = sk[i];
+    const int d = (int)((key >> shift) & (RADIX - 1));
     const int64_t pos = (int64_t)gbase[d] + (i - toff[d]);
     kout[pos] = key;
     vout[pos] = sv[i];
@@ -811,8 +836,11 @@ cudaError_t front_init() {
 
 cudaError_t sort_init() {
   if (sort_attr_set) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(sort_downsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(sort_downsweep_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        STAGE_BYTES_SORT);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sort_downsweep_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SORT_TILE * 8);
   if (e == cudaSuccess) sort_attr_set = true;
   return e;
 }
@@ -1014,23 +1042,33 @@ __global__ void popc_kernel(const unsigned* __restrict__ bits, int64_t nw, int32
     out[i] = __popc(bits[i]);
 }
 
-// One thread per 32-pixel word of the new-voxel bitmask; outputs land at the
-// word's exclusive popcount offset + the bit's rank -> ascending pixel order.
+// Pixel ids of the new voxels in ascending order: one thread per 32-pixel
+// word of the new-voxel bitmask writes its set bits at the word's exclusive
+// popcount offset.
 __global__ void __launch_bounds__(256)
-grid_emit_kernel(const unsigned* __restrict__ flag_bits, const int32_t* __restrict__ wpos,
-                 const int32_t* __restrict__ head_pos, int64_t nwords, EmitArgs a) {
-  const int64_t HW = a.H * a.W;
+grid_pidlist_kernel(const unsigned* __restrict__ flag_bits, const int32_t* __restrict__ wpos, int64_t nwords,
+                    int64_t* __restrict__ pid_out) {
   for (int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; wi < nwords; wi += (int64_t)gridDim.x * blockDim.x) {
-  unsigned word = flag_bits[wi];
-  int64_t o = wpos[wi];
-  while (word) {
-    const int b = __ffs(word) - 1;
-    word &= word - 1;
-    const int64_t p = wi * 32 + b;
+    unsigned word = flag_bits[wi];
+    int64_t o = wpos[wi];
+    while (word) {
+      const int b = __ffs(word) - 1;
+      word &= word - 1;
+      pid_out[o++] = wi * 32 + b;
+    }
+  }
+}
+
+// One thread per new voxel (output row o, pixel a.pid[o]): the
+// GaussianField-compatible attributes.
+__global__ void __launch_bounds__(256)
+grid_emit_kernel(const int32_t* __restrict__ head_pos, int64_t nnew, EmitArgs a) {
+  const int64_t HW = a.H * a.W;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < nnew; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = a.pid[o];
     const int64_t f = p / HW, rem = p - f * HW;
     const int64_t u = rem / a.W, v = rem - u * a.W;
     const double d = (double)a.depth[p];
-    a.pid[o] = p;
     a.dep[o] = d;
     // iso size max(min_scale, 0.5*s*depth/fx)  (slam.py:631)
     const double sz = ddiv(dmul(dmul(0.5, (double)a.stride), d), a.cam.fx);
@@ -1079,8 +1117,6 @@ grid_emit_kernel(const unsigned* __restrict__ flag_bits, const int32_t* __restri
       }
       if (a.count) a.count[o] = cnt;
     }
-    o++;
-  }
   }
 }
 
@@ -1140,6 +1176,7 @@ struct HashSet {
   unsigned long long* table = nullptr;
   int64_t cap = 0;
   unsigned long long* count_dev = nullptr;
+  int64_t count_ub = 0;   // host upper bound of the key count (no sync needed to size the table)
 };
 
 cudaError_t hashset_create(int64_t capacity, HashSet** out) {
@@ -1178,9 +1215,11 @@ cudaError_t hashset_size(HashSet* h, int64_t* n, cudaStream_t s) {
 
 // grow so that `extra` more keys keep the load factor <= 1/2
 cudaError_t hashset_reserve(HashSet* h, int64_t extra, cudaStream_t s) {
+  cudaError_t e;
+  if (2 * (h->count_ub + extra) <= h->cap) return cudaSuccess;   // bound suffices: no read-back
   int64_t cur = 0;
-  cudaError_t e = hashset_size(h, &cur, s);
-  if (e != cudaSuccess) return e;
+  if ((e = hashset_size(h, &cur, s)) != cudaSuccess) return e;
+  h->count_ub = cur;
   if (2 * (cur + extra) <= h->cap) return cudaSuccess;
   int64_t cap = h->cap;
   while (2 * (cur + extra) > cap) cap <<= 1;
@@ -1199,6 +1238,7 @@ cudaError_t hashset_insert(HashSet* h, const uint64_t* keys, int64_t n, uint8_t*
   if (e != cudaSuccess || n == 0) return e;
   hs_insert_kernel<<<grid_blocks(n, 256, 148), 256, 0, s>>>(h->table, (uint64_t)h->cap - 1, keys, n, was_new,
                                                            h->count_dev); count_launches(1);
+  h->count_ub += n;
   return cudaGetLastError();
 }
 
@@ -1213,6 +1253,24 @@ cudaError_t launch_backproject(const double* R, const double* t, const double* i
   if (n == 0) return cudaSuccess;
   Cam cam{intr4[0], intr4[1], intr4[2], intr4[3], voxel, 1.0 / voxel};
   backproject_kernel<<<grid_blocks(n, 256, 148), 256, 0, s>>>(R, t, cam, u, v, d, n, out); count_launches(1);
+  return cudaGetLastError();
+}
+
+// LSD passes over bits [0, bits) of K keys (ping-pong k0/k1, v0/v1); on
+// return k0/v0 hold the sorted pairs.
+template <typename K>
+cudaError_t lsd_passes(K*& k0, uint32_t*& v0, K*& k1, uint32_t*& v1, int64_t n, int bits, int32_t* hist,
+                       int32_t* ssum, cudaStream_t s) {
+  const int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
+  const int stage = SORT_TILE * (int)(sizeof(K) + 4);
+  for (int shift = 0; shift < bits; shift += 8) {
+    sort_upsweep_kernel<K><<<(unsigned)tiles, SORT_THREADS, 0, s>>>(k0, n, shift, hist, tiles); count_launches(1);
+    sort_scan_digits_kernel<<<RADIX, 1024, 0, s>>>(hist, tiles, ssum); count_launches(1);
+    sort_downsweep_kernel<K><<<(unsigned)tiles, SORT_THREADS, stage, s>>>(k0, v0, n, shift, hist, ssum, tiles, k1, v1);
+    count_launches(1);
+    K* tk = k0; k0 = k1; k1 = tk;
+    uint32_t* tv = v0; v0 = v1; v1 = tv;
+  }
   return cudaGetLastError();
 }
 
@@ -1319,7 +1377,9 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   out.n_valid = (int64_t)nvalid;
   if (nvalid == 0) return cudaSuccess;
   const int64_t nitems = compact ? (int64_t)hc[2] : npix;   // items to sort
-  if ((e = hashset_reserve(hs, (int64_t)nvalid, s)) != cudaSuccess) return e;
+  // every voxel of the batch keeps at least one item, so the sorted item count
+  // bounds the new keys (first-pick dedup makes it ~3x tighter than nvalid)
+  if ((e = hashset_reserve(hs, nitems, s)) != cudaSuccess) return e;
   // bbox-relative key width; +1 on x keeps the all-ones invalid key above every valid key
   RelKey rk;
   rk.x0 = (uint32_t)hb[0];
@@ -1342,13 +1402,27 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   out.sort_passes = (bits + 7) / 8;
   {
     ProfScope prof("grid_sort", s);
-    for (int shift = 0; shift < bits; shift += 8) {
-      sort_upsweep_kernel<<<(unsigned)tiles, SORT_THREADS, 0, s>>>(k0, nitems, rk, shift, hist, tiles); count_launches(1);
-      sort_scan_digits_kernel<<<RADIX, 1024, 0, s>>>(hist, tiles, ssum); count_launches(1);
-      sort_downsweep_kernel<<<(unsigned)tiles, SORT_THREADS, STAGE_BYTES_SORT, s>>>(k0, v0, nitems, rk, shift, hist, ssum, tiles, k1, v1); count_launches(1);
-      uint64_t* tk = k0; k0 = k1; k1 = tk;
-      uint32_t* tv = v0; v0 = v1; v1 = tv;
+    // relative keys once (u32 when they fit), LSD passes, biased keys back into k0
+    const unsigned rb = grid_blocks(nitems, 256, sms);
+    if (bits <= 32) {
+      uint32_t* r0 = reinterpret_cast<uint32_t*>(k1);
+      uint32_t* r1 = r0 + nitems;
+      rekey_kernel<uint32_t><<<rb, 256, 0, s>>>(k0, nitems, rk, r0); count_launches(1);
+      if ((e = lsd_passes<uint32_t>(r0, v0, r1, v1, nitems, bits, hist, ssum, s)) != cudaSuccess) return e;
+      unrekey_kernel<uint32_t><<<rb, 256, 0, s>>>(r0, nitems, rk, bits, k0); count_launches(1);
+    } else {
+      rekey_kernel<uint64_t><<<rb, 256, 0, s>>>(k0, nitems, rk, k1); count_launches(1);
+      uint64_t* r0 = k1;
+      uint64_t* r1 = k0;
+      if ((e = lsd_passes<uint64_t>(r0, v0, r1, v1, nitems, bits, hist, ssum, s)) != cudaSuccess) return e;
+      if (r0 == k0) {   // sorted relative keys landed in k0's buffer: unpack through k1
+        unrekey_kernel<uint64_t><<<rb, 256, 0, s>>>(r0, nitems, rk, bits, k1); count_launches(1);
+        uint64_t* t = k0; k0 = k1; k1 = t;
+      } else {
+        unrekey_kernel<uint64_t><<<rb, 256, 0, s>>>(r0, nitems, rk, bits, k0); count_launches(1);
+      }
     }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   {
     ProfScope prof("grid_select", s);
@@ -1373,6 +1447,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     if ((e = cudaMemcpyAsync(&nvox, cnts + 1, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
     out.n_new = nnew;
+    hs->count_ub += nnew;
     out.n_voxels = (int64_t)nvox;
     if (nnew > out.capacity) return cudaErrorInvalidValue;
     EmitArgs a;
@@ -1401,8 +1476,11 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     a.dep = out.depth;
     a.ofeat = out.feat;
     a.count = out.count;
-    grid_emit_kernel<<<grid_blocks(nwords, 256, sms), 256, 0, s>>>(reinterpret_cast<const unsigned*>(flag), pos, head,
-                                                                    nwords, a); count_launches(1);
+    grid_pidlist_kernel<<<grid_blocks(nwords, 256, sms), 256, 0, s>>>(reinterpret_cast<const unsigned*>(flag), pos,
+                                                                       nwords, out.pid); count_launches(1);
+    if (nnew > 0) {
+      grid_emit_kernel<<<grid_blocks(nnew, 128, sms), 128, 0, s>>>(head, nnew, a); count_launches(1);
+    }
   }
   return cudaGetLastError();
 }
@@ -1424,21 +1502,11 @@ cudaError_t radix_sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n, int bits
   uint32_t* v1 = reinterpret_cast<uint32_t*>(b + w.off_v1);
   int32_t* hist = reinterpret_cast<int32_t*>(b + w.off_hist);
   int32_t* ssum = reinterpret_cast<int32_t*>(b + w.off_scan_sums);
-  RelKey ident;  // identity on raw bits: x0=y0=z0=0, fields re-packed in place
-  ident.x0 = ident.y0 = ident.z0 = 0;
-  ident.by = 21;
-  ident.bz = 21;
   uint64_t* k0 = keys;
   uint32_t* v0 = vals;
   cudaError_t e = sort_init();
   if (e != cudaSuccess) return e;
-  for (int shift = 0; shift < bits; shift += 8) {
-    sort_upsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, 0, s>>>(k0, n, ident, shift, hist, w.tiles); count_launches(1);
-    sort_scan_digits_kernel<<<RADIX, 1024, 0, s>>>(hist, w.tiles, ssum); count_launches(1);
-    sort_downsweep_kernel<<<(unsigned)w.tiles, SORT_THREADS, STAGE_BYTES_SORT, s>>>(k0, v0, n, ident, shift, hist, ssum, w.tiles, k1, v1); count_launches(1);
-    uint64_t* tk = k0; k0 = k1; k1 = tk;
-    uint32_t* tv = v0; v0 = v1; v1 = tv;
-  }
+  if ((e = lsd_passes<uint64_t>(k0, v0, k1, v1, n, bits, hist, ssum, s)) != cudaSuccess) return e;
   if (k0 != keys) {
     if ((e = cudaMemcpyAsync(keys, k0, n * 8, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) return e;
     if ((e = cudaMemcpyAsync(vals, v0, n * 4, cudaMemcpyDeviceToDevice, s)) != cudaSuccess) return e;
