@@ -54,12 +54,20 @@ struct HalfState {                            // column-half 1 -> half 0 hand-of
   int ck[CAP];
   float cl[CAP];
 };
-// smem layout per candidate capacity: the CAP=8 epilogue's smaller merge
-// area leaves room for a 5th codebook stage
+struct Top2State {                            // CAP == 0 (top-2 epilogue) hand-off
+  float m1, m2;
+  int k1;
+};
+template <int CAP>
+struct MergeOf { using type = HalfState<CAP>; };
+template <>
+struct MergeOf<0> { using type = Top2State; };
+// smem layout per candidate capacity (CAP == 0: the top-2 epilogue): the
+// smaller merge areas leave room for a 5th codebook stage
 template <int CAP>
 struct Layout {
   static constexpr int B_STAGES = CAP <= 8 ? 5 : 4;
-  static constexpr int MERGE_BYTES = BM * (int)sizeof(HalfState<CAP>);
+  static constexpr int MERGE_BYTES = BM * (int)sizeof(typename MergeOf<CAP>::type);
   static constexpr int NBARS = 2 * A_SLOTS + 2 * B_STAGES + 4;
   static constexpr int BAR_BYTES = NBARS * 8 + 16;
   static constexpr int OFF_B = A_SLOTS * A_BYTES;
@@ -75,6 +83,11 @@ constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)
 
 struct ScreenParams {
   int64_t n;
+  const int32_t* n_dev;   // nullable: device row count (rescreen pass; n is then the capacity)
+  const int32_t* rowmap;  // nullable: output row of local row i (rescreen pass)
+  int32_t* sq;            // top-2 epilogue: rows whose best code is not unique -> rescreen
+  int32_t* sq_count;
+  int32_t sq_cap;
   int num_pair_tiles, num_n_chunks, num_k_blocks;
   int resident;         // A row tile stays in smem across the N chunks (num_k_blocks <= A_SLOTS)
   const float* xband;   // per row: 2 * max_k B_k + fp64-reference slack
@@ -285,6 +298,40 @@ __device__ __forceinline__ void screen_block(const uint32_t (&r)[32], const floa
   }
 }
 
+// Top-2 epilogue (CAP == 0, K < 2048): per row and column half the two
+// smallest screen values, tracked branch-free.  Each s is packed with its
+// column in the low 5 mantissa bits (|packed - s| < 2^-18 |s|; +inf padding
+// codes become NaN, which FMNMX ignores), so the minimum carries its own
+// index.  A row whose second value clears the first by more than the band
+// (+ the packing slack) has exactly one candidate, the fp64 argmin; the rest
+// are rescreened with candidate lists.
+__device__ __forceinline__ float pack_col(float s, int i) {
+  return __int_as_float((__float_as_int(s) & ~31) | i);
+}
+__device__ __forceinline__ void top2_block(const uint32_t (&r)[32], const float* __restrict__ cn, float xf, int kbase,
+                                           float& M1, float& M2, int& K1) {
+  const float inf = __int_as_float(0x7f800000);
+  float a1 = inf, a2 = inf, b1 = inf, b2 = inf;
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) {
+    const float4 c = *reinterpret_cast<const float4*>(cn + i);
+    const float p0 = pack_col(fmaf(xf, __uint_as_float(r[i + 0]), c.x), i + 0);
+    const float p1 = pack_col(fmaf(xf, __uint_as_float(r[i + 1]), c.y), i + 1);
+    const float p2 = pack_col(fmaf(xf, __uint_as_float(r[i + 2]), c.z), i + 2);
+    const float p3 = pack_col(fmaf(xf, __uint_as_float(r[i + 3]), c.w), i + 3);
+    const float lo0 = fminf(p0, p2), hi0 = fmaxf(p0, p2), lo1 = fminf(p1, p3), hi1 = fmaxf(p1, p3);
+    a2 = fminf(a2, fminf(hi0, fmaxf(a1, lo0)));
+    a1 = fminf(a1, lo0);
+    b2 = fminf(b2, fminf(hi1, fmaxf(b1, lo1)));
+    b1 = fminf(b1, lo1);
+  }
+  const float c1 = fminf(a1, b1), c2 = fminf(fmaxf(a1, b1), fminf(a2, b2));
+  const bool better = c1 < M1;
+  M2 = better ? fminf(M1, c2) : fminf(M2, c1);
+  K1 = better ? kbase : K1;
+  M1 = better ? c1 : M1;
+}
+
 // One CTA pair (cluster of 2, same TPC) per 256-row tile, persistent over
 // tiles.  Each CTA owns 128 rows (TMEM lanes) and stages its own A rows plus
 // one half (128 codes) of every codebook chunk; the leader CTA issues
@@ -311,6 +358,8 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   const int nkb = p.num_k_blocks, nnc = p.num_n_chunks;
+  const int64_t nrows = p.n_dev ? (int64_t)*p.n_dev : p.n;
+  const int ntiles = (int)((nrows + 2 * BM - 1) / (2 * BM));
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < A_SLOTS; i++) {
       mbar_init(&fullA[i], 1);
@@ -343,10 +392,10 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       const uint32_t lead_full = mapa(smem_u32(fullA), 0);
       uint32_t idx = 0;
       const int nload = p.resident ? nkb : nkb * nnc;
-      for (int t = cluster; t < p.num_pair_tiles; t += nclusters) {
+      for (int t = cluster; t < ntiles; t += nclusters) {
         const int row0 = t * 2 * BM + (int)rank * BM;
         const int tn = t + nclusters;
-        if (tn < p.num_pair_tiles)   // warm L2 with the next tile's rows
+        if (tn < ntiles)   // warm L2 with the next tile's rows
           for (int kb = 0; kb < nkb; kb++) tma_prefetch_2d(&tmA, kb * BK, tn * 2 * BM + (int)rank * BM);
         for (int j = 0; j < nload; j++, idx++) {
           const int kb = j % nkb;
@@ -362,7 +411,7 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     if (lane == 0) {
       const uint32_t lead_full = mapa(smem_u32(fullB), 0);
       uint32_t idx = 0;
-      for (int t = cluster; t < p.num_pair_tiles; t += nclusters)
+      for (int t = cluster; t < ntiles; t += nclusters)
         for (int nc = 0; nc < nnc; nc++)
           for (int kb = 0; kb < nkb; kb++, idx++) {
             const uint32_t st = idx % L::B_STAGES, ph = (idx / L::B_STAGES) & 1;
@@ -378,7 +427,7 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       uint32_t abase = 0, bidx = 0;
       int acc = 0;
       uint32_t aphase = 0;
-      for (int t = cluster; t < p.num_pair_tiles; t += nclusters) {
+      for (int t = cluster; t < ntiles; t += nclusters) {
         for (int nc = 0; nc < nnc; nc++) {
           mbar_wait_cluster(&tempty[acc], aphase ^ 1);
           tc_after();
@@ -414,16 +463,20 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const int rl = q * 32 + lane;            // row within this CTA's 128 rows
     const unsigned lt = (1u << lane) - 1u;
     const uint32_t lead_tempty = mapa(smem_u32(tempty), 0);
-    HalfState<CAP>* merge = reinterpret_cast<HalfState<CAP>*>(smem + L::OFF_MERGE);
+    HalfState<(CAP == 0 ? 1 : CAP)>* merge = reinterpret_cast<HalfState<(CAP == 0 ? 1 : CAP)>*>(smem + L::OFF_MERGE);
     int acc = 0;
     uint32_t aphase = 0;
-    for (int t = cluster; t < p.num_pair_tiles; t += nclusters) {
-      const int64_t row = (int64_t)t * 2 * BM + (int64_t)rank * BM + rl;
-      const bool live = row < p.n;
-      const float band = live ? p.xband[row] : 0.f;
-      const float xf = live ? p.xf[row] : 0.f;   // -2 / (row scale * codebook scale)
-      Cands<CAP> st;
-      st.init();
+    for (int t = cluster; t < ntiles; t += nclusters) {
+      const int64_t lrow = (int64_t)t * 2 * BM + (int64_t)rank * BM + rl;
+      const bool live = lrow < nrows;
+      const int64_t row = (live && p.rowmap) ? (int64_t)p.rowmap[lrow] : lrow;   // output row
+      const float band = live ? p.xband[lrow] : 0.f;
+      const float xf = live ? p.xf[lrow] : 0.f;   // -2 / (row scale * codebook scale)
+      constexpr int SCAP = CAP == 0 ? 1 : CAP;
+      Cands<SCAP> st;
+      float M1 = __int_as_float(0x7f800000), M2 = M1;
+      int K1 = 0;
+      if (CAP != 0) st.init();
       for (int nc = 0; nc < nnc; nc++) {
         float* cc = cconst + acc * BN;
         for (int i = et; i < BN; i += EPI_THREADS) cc[i] = p.cn[nc * BN + i];
@@ -438,10 +491,16 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 #pragma unroll 1
         for (int c0 = 0; c0 < HALF; c0 += 64) {
           tmem_ld32_async(taddr + c0 + 32, rb);
-          screen_block(ra, cc + cbase + c0, xf, band, nc * BN + cbase + c0, st);
+          if constexpr (CAP == 0)
+            top2_block(ra, cc + cbase + c0, xf, nc * BN + cbase + c0, M1, M2, K1);
+          else
+            screen_block(ra, cc + cbase + c0, xf, band, nc * BN + cbase + c0, st);
           tmem_wait(rb);
           if (c0 + 64 < HALF) tmem_ld32_async(taddr + c0 + 64, ra);
-          screen_block(rb, cc + cbase + c0 + 32, xf, band, nc * BN + cbase + c0 + 32, st);
+          if constexpr (CAP == 0)
+            top2_block(rb, cc + cbase + c0 + 32, xf, nc * BN + cbase + c0 + 32, M1, M2, K1);
+          else
+            screen_block(rb, cc + cbase + c0 + 32, xf, band, nc * BN + cbase + c0 + 32, st);
           if (c0 + 64 < HALF) tmem_wait(ra);
         }
         tc_before();
@@ -451,6 +510,38 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (acc == 0) aphase ^= 1;
       }
       // ---- merge the two column halves, finalize the row ----
+      if constexpr (CAP == 0) {
+        Top2State* t2 = reinterpret_cast<Top2State*>(smem + L::OFF_MERGE);
+        if (half == 1) t2[rl] = Top2State{M1, M2, K1};
+        epi_bar();
+        if (half == 0) {
+          const Top2State o = t2[rl];
+          const bool mine = M1 <= o.m1;
+          const float m1 = mine ? M1 : o.m1;
+          const int k1 = mine ? K1 : o.k1;
+          const float m2 = fminf(fmaxf(M1, o.m1), fminf(M2, o.m2));
+          // unique iff m2 - m1 > band + packing slack (2^-18 per packed value), rounded outward
+          const float slack = __fmul_ru(__fadd_ru(fabsf(m1), fabsf(m2)), 0x1p-18f);
+          const bool unique = __fsub_rd(m2, m1) > __fadd_ru(band, slack);
+          if (live && unique) p.codes[row] = k1 + (__float_as_int(m1) & 31);
+          const bool to_rs = live && !unique;
+          const unsigned m = __ballot_sync(FULL, to_rs);
+          if (m) {
+            const int leader_lane = __ffs(m) - 1;
+            int base = 0;
+            if (lane == leader_lane) base = atomicAdd(p.sq_count, __popc(m));
+            base = __shfl_sync(FULL, base, leader_lane);
+            if (to_rs) {
+              const int slot = base + __popc(m & lt);
+              if (slot < p.sq_cap) {
+                p.sq[slot] = (int32_t)row;
+              } else {   // rescreen queue full: exact scan instead
+                p.fq[atomicAdd(p.fq_count, 1)] = (int32_t)row;
+              }
+            }
+          }
+        }
+      } else {
       if (half == 1) {
         HalfState<CAP>& hs = merge[rl];
         hs.U = st.U;
@@ -507,6 +598,7 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           base = __shfl_sync(FULL, base, leader_lane);
           if (to_fallback) p.fq[base + __popc(m & lt)] = (int32_t)row;
         }
+      }
       }
       epi_bar();   // merge slots are reused by the next tile
     }
@@ -631,13 +723,15 @@ prep_rows_kernel(const X* __restrict__ x, int64_t n, int64_t d, int64_t ldx, int
   }
 }
 
-// counter block: [0..1] codebook absmax bits, [2..3] step totals,
-// then {rerank, fallback} counts per row chunk
+// counter block: [0..1] codebook absmax bits, [2..4] step totals, then per
+// row chunk {rerank, fallback, rescreen queued, rescreen rows}
 constexpr int kCntBase = 8;
+constexpr int kCntStride = 4;
 
 struct ScreenWs {
   size_t off_ab, off_xn, off_xf, off_eb, off_cn, off_rq, off_fq, off_cnt, total;
-  int64_t kp, dp;
+  size_t off_sq, off_ab2, off_xn2, off_xf2;   // top-2 rescreen: row queue + compact operand copies
+  int64_t kp, dp, sq_cap;
 };
 
 ScreenWs screen_ws(int64_t n, int64_t k, int64_t d) {
@@ -654,7 +748,13 @@ ScreenWs screen_ws(int64_t n, int64_t k, int64_t d) {
   w.off_cn = take((size_t)w.kp * 4);
   w.off_rq = take(nn * sizeof(RerankEntry));
   w.off_fq = take(nn * 4);
-  w.off_cnt = take(sizeof(int32_t) * (kCntBase + 2 * kMaxChunks));
+  w.off_cnt = take(sizeof(int32_t) * (kCntBase + kCntStride * kMaxChunks));
+  w.sq_cap = n / 8 > 4096 ? n / 8 : 4096;
+  const size_t sc = (size_t)w.sq_cap;
+  w.off_sq = take(sc * 4);
+  w.off_ab2 = take(sc * (size_t)w.dp * 2);
+  w.off_xn2 = take(sc * 4);
+  w.off_xf2 = take(sc * 4);
   w.total = o;
   return w;
 }
@@ -705,6 +805,10 @@ struct ScreenBufs {
   int32_t* fq;
   int32_t* cnt;
   unsigned* emax;
+  int32_t* sq;
+  __half* Ab2;
+  float* xn2;
+  float* xf2;
 };
 
 ScreenBufs screen_bufs(const ScreenArgs& a) {
@@ -720,17 +824,45 @@ ScreenBufs screen_bufs(const ScreenArgs& a) {
   b.fq = reinterpret_cast<int32_t*>(base + b.w.off_fq);
   b.cnt = reinterpret_cast<int32_t*>(base + b.w.off_cnt);
   b.emax = reinterpret_cast<unsigned*>(b.cnt);
+  b.sq = reinterpret_cast<int32_t*>(base + b.w.off_sq);
+  b.Ab2 = reinterpret_cast<__half*>(base + b.w.off_ab2);
+  b.xn2 = reinterpret_cast<float*>(base + b.w.off_xn2);
+  b.xf2 = reinterpret_cast<float*>(base + b.w.off_xf2);
   return b;
 }
 
 __global__ void sum_counters_kernel(int32_t* cnt, int chunks) {
-  int32_t r = 0, f = 0;
+  int32_t r = 0, f = 0, q = 0;
   for (int c = 0; c < chunks; c++) {
-    r += cnt[kCntBase + 2 * c];
-    f += cnt[kCntBase + 2 * c + 1];
+    r += cnt[kCntBase + kCntStride * c];
+    f += cnt[kCntBase + kCntStride * c + 1];
+    q += cnt[kCntBase + kCntStride * c + 3];
   }
   cnt[2] = r;
   cnt[3] = f;
+  cnt[4] = q;
+}
+
+// gather the rows queued for rescreening into compact operand copies; the
+// queue doubles as the row map of the rescreen pass
+__global__ void rescreen_gather_kernel(const int32_t* __restrict__ sq, int32_t* __restrict__ counts, int32_t cap,
+                                       const __half* __restrict__ Ab, const float* __restrict__ xn,
+                                       const float* __restrict__ xf, int64_t dp, __half* __restrict__ Ab2,
+                                       float* __restrict__ xn2, float* __restrict__ xf2) {
+  const int32_t nq = min(counts[0], cap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) counts[1] = nq;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nq;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t r = sq[i];
+    const uint4* src = reinterpret_cast<const uint4*>(Ab + r * dp);
+    uint4* dst = reinterpret_cast<uint4*>(Ab2 + i * dp);
+    for (int64_t j = lane; j < dp / 8; j += 32) dst[j] = src[j];
+    if (lane == 0) {
+      xn2[i] = xn[r];
+      xf2[i] = xf[r];
+    }
+  }
 }
 
 }  // namespace
@@ -739,7 +871,7 @@ cudaError_t screen_prepare(const ScreenArgs& a, cudaStream_t s) {
   const ScreenBufs b = screen_bufs(a);
   if (a.ws_bytes < b.w.total) return cudaErrorInvalidValue;
   cudaError_t e;
-  if ((e = cudaMemsetAsync(b.cnt, 0, sizeof(int32_t) * (kCntBase + 2 * kMaxChunks), s)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(b.cnt, 0, sizeof(int32_t) * (kCntBase + kCntStride * kMaxChunks), s)) != cudaSuccess) return e;
   ProfScope prof("vq_prep", s);
   absmax_kernel<<<148, 256, 0, s>>>(a.E, a.k * a.d, b.emax); count_launches(1);
   prep_codebook_kernel<<<(unsigned)((b.w.kp + 7) / 8), 256, 0, s>>>(a.E, a.k, a.d, b.w.kp, b.w.dp, a.c1, a.c2, a.c4,
@@ -776,7 +908,7 @@ cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, 
   if (!make_map(&tmA, b.Ab + r0 * dp, (uint64_t)dp, (uint64_t)n, (uint64_t)dp * 2, BK, BM) ||
       !make_map(&tmB, b.Eb, (uint64_t)dp, (uint64_t)b.w.kp, (uint64_t)dp * 2, BK, BNH))
     return cudaErrorInvalidValue;
-  int32_t* cnt = b.cnt + kCntBase + 2 * chunk;
+  int32_t* cnt = b.cnt + kCntBase + kCntStride * chunk;
   RerankEntry* rq = b.rq + r0;
   int32_t* fq = b.fq + r0;
   const void* x = static_cast<const char*>(a.x) + (size_t)r0 * (size_t)a.ldx * dtype_size(a.dtype);
@@ -784,6 +916,11 @@ cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, 
 
   ScreenParams p;
   p.n = n;
+  p.n_dev = nullptr;
+  p.rowmap = nullptr;
+  p.sq = b.sq;
+  p.sq_count = cnt + 2;
+  p.sq_cap = (int32_t)b.w.sq_cap;
   p.num_pair_tiles = (int)((n + 2 * BM - 1) / (2 * BM));
   p.num_n_chunks = (int)(b.w.kp / BN);
   p.num_k_blocks = (int)(dp / BK);
@@ -796,25 +933,51 @@ cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, 
   p.rq_count = cnt;
   p.fq = fq;
   p.fq_count = cnt + 1;
-  // candidate capacity: 8 keeps the C2-sized epilogue lean; large codebooks
-  // (more near-ties) use the full RerankEntry capacity of 16
+  // K < 2048: top-2 epilogue on all rows, then the candidate-list epilogue
+  // (CAP 8) on the rows whose best code was not unique; larger codebooks
+  // (more near-ties) use the CAP-16 list epilogue directly
   const bool big = a.k >= 2048;
-  auto kern = big ? screen_kernel<kCandCap> : screen_kernel<8>;
-  const int smem_bytes = big ? Layout<kCandCap>::SMEM_BYTES : Layout<8>::SMEM_BYTES;
-  static bool attr[2] = {false, false};
+  static bool attr[3] = {false, false, false};
   cudaError_t e;
-  if (!attr[big]) {
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes)) != cudaSuccess)
-      return e;
-    attr[big] = true;
-  }
-  // one CTA pair per TPC, persistent over 256-row tiles
-  int clusters = a.sm_count / 2;
-  if (clusters > p.num_pair_tiles) clusters = p.num_pair_tiles;
-  if (clusters < 1) clusters = 1;
+  auto prepare = [&](auto kern, int idx, int bytes) -> cudaError_t {
+    if (attr[idx]) return cudaSuccess;
+    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (r == cudaSuccess) attr[idx] = true;
+    return r;
+  };
+  auto clusters_for = [&](int64_t rows) {
+    int64_t c = a.sm_count / 2, t = (rows + 2 * BM - 1) / (2 * BM);
+    if (c > t) c = t;
+    return (int)(c < 1 ? 1 : c);
+  };
   {
     ProfScope prof("vq_screen", s);
-    kern<<<2 * clusters, THREADS, smem_bytes, s>>>(tmA, tmB, p); count_launches(1);
+    if (big) {
+      if ((e = prepare(screen_kernel<kCandCap>, 2, Layout<kCandCap>::SMEM_BYTES)) != cudaSuccess) return e;
+      screen_kernel<kCandCap><<<2 * clusters_for(n), THREADS, Layout<kCandCap>::SMEM_BYTES, s>>>(tmA, tmB, p);
+      count_launches(1);
+    } else {
+      if ((e = prepare(screen_kernel<0>, 0, Layout<0>::SMEM_BYTES)) != cudaSuccess) return e;
+      if ((e = prepare(screen_kernel<8>, 1, Layout<8>::SMEM_BYTES)) != cudaSuccess) return e;
+      screen_kernel<0><<<2 * clusters_for(n), THREADS, Layout<0>::SMEM_BYTES, s>>>(tmA, tmB, p);
+      count_launches(1);
+      const int64_t cap = b.w.sq_cap;
+      rescreen_gather_kernel<<<(unsigned)((cap + 7) / 8 < 148 * 8 ? (cap + 7) / 8 : 148 * 8), 256, 0, s>>>(
+          b.sq, cnt + 2, (int32_t)cap, b.Ab + r0 * dp, b.xn + r0, b.xf + r0, dp, b.Ab2, b.xn2, b.xf2);
+      count_launches(1);
+      CUtensorMap tmA2;
+      if (!make_map(&tmA2, b.Ab2, (uint64_t)dp, (uint64_t)cap, (uint64_t)dp * 2, BK, BM)) return cudaErrorInvalidValue;
+      ScreenParams p2 = p;
+      p2.n = cap;
+      p2.n_dev = cnt + 3;
+      p2.rowmap = b.sq;
+      p2.xband = b.xn2;
+      p2.xf = b.xf2;
+      p2.num_pair_tiles = (int)((cap + 2 * BM - 1) / (2 * BM));
+      p2.resident = p.resident;
+      screen_kernel<8><<<2 * clusters_for(cap), THREADS, Layout<8>::SMEM_BYTES, s>>>(tmA2, tmB, p2);
+      count_launches(1);
+    }
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
