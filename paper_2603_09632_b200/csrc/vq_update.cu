@@ -92,27 +92,35 @@ acc_scan_tiles_kernel(int32_t* tile_counts, int64_t tiles, int64_t k, int32_t* c
     }
 }
 
-// (2b) exclusive scan of the K code totals -> code_start[0..K].
+// (2b) exclusive scan of the K code totals -> code_start[0..K] (one block,
+// warp-shuffle scan of per-thread partials).
 __global__ void __launch_bounds__(1024)
 acc_scan_codes_kernel(const int32_t* __restrict__ code_count, int64_t k, int32_t* code_start) {
-  __shared__ int32_t part[1024];
+  __shared__ int32_t wsum[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t per = (k + 1023) / 1024;
   const int64_t c0 = threadIdx.x * per, c1 = min(k, c0 + per);
   int32_t s = 0;
   for (int64_t c = c0; c < c1; c++) s += code_count[c];
-  part[threadIdx.x] = s;
+  int32_t x = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t run = 0;
-    for (int i = 0; i < 1024; i++) {
-      const int32_t v = part[i];
-      part[i] = run;
-      run += v;
+  if (warp == 0) {
+    const int32_t w = wsum[lane];
+    int32_t wx = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, wx, o);
+      if (lane >= o) wx += y;
     }
-    code_start[k] = run;
+    wsum[lane] = wx - w;
+    if (lane == 31) code_start[k] = wx;
   }
   __syncthreads();
-  int32_t run = part[threadIdx.x];
+  int32_t run = wsum[warp] + x - s;
   for (int64_t c = c0; c < c1; c++) {
     code_start[c] = run;
     run += code_count[c];
@@ -121,16 +129,25 @@ acc_scan_codes_kernel(const int32_t* __restrict__ code_count, int64_t k, int32_t
 
 // (2c) codes by descending row count (ties by index): the serial chains of the
 // biggest codes start first, so the largest code overlaps the rest of the work.
-__global__ void acc_order_kernel(const int32_t* __restrict__ code_count, int64_t k, int32_t* order) {
+// Counts are staged through shared memory in 4096-code slabs.
+__global__ void __launch_bounds__(256)
+acc_order_kernel(const int32_t* __restrict__ code_count, int64_t k, int32_t* order) {
+  __shared__ int32_t cc[4096];
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= k) return;
-  const int32_t mine = code_count[c];
+  const int32_t mine = c < k ? code_count[c] : 0;
   int32_t rank = 0;
-  for (int64_t j = 0; j < k; j++) {
-    const int32_t o = __ldg(code_count + j);
-    rank += (o > mine) || (o == mine && j < c);
+  for (int64_t j0 = 0; j0 < k; j0 += 4096) {
+    const int64_t m = min((int64_t)4096, k - j0);
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < m; j += blockDim.x) cc[j] = code_count[j0 + j];
+    __syncthreads();
+    if (c < k)
+      for (int64_t j = 0; j < m; j++) {
+        const int32_t o = cc[j];
+        rank += (o > mine) || (o == mine && j0 + j < c);
+      }
   }
-  order[rank] = (int32_t)c;
+  if (c < k) order[rank] = (int32_t)c;
 }
 
 // (3) stable scatter of row ids into code-sorted order; one warp per tile.
