@@ -43,7 +43,7 @@ def peaks():
 
 class ClockSampler:
     """SM clocks + throttle reasons sampled DURING the timed region: an NVML
-    polling thread (2 ms period, so short timed regions still get samples);
+    polling thread (10 ms period: short timed regions still get samples, negligible GIL load);
     nvidia-smi -lms as the fallback when NVML is unavailable."""
 
     REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
@@ -84,7 +84,7 @@ class ClockSampler:
                                 self.reasons.add(nm)
                     except Exception:
                         pass
-                    time.sleep(0.002)
+                    time.sleep(0.01)
             self.thread = threading.Thread(target=poll, daemon=True)
             self.thread.start()
         except Exception:

@@ -46,6 +46,7 @@ constexpr int EPI_THREADS = EPI_WARPS * 32;
 constexpr int EPI_WARP0 = 3;                  // warp0 A-TMA, warp1 MMA (+TMEM alloc), warp2 B-TMA
 constexpr int THREADS = EPI_WARP0 * 32 + EPI_THREADS;
 constexpr int HALF = BN / 2;                  // columns per epilogue warp per chunk
+static_assert(BN == EPI_THREADS, "one codebook constant per epilogue thread per chunk");
 constexpr int CONST_BYTES = 2 * BN * 4;
 template <int CAP>
 struct HalfState {                            // column-half 1 -> half 0 hand-off at tile end
@@ -466,12 +467,27 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     HalfState<(CAP == 0 ? 1 : CAP)>* merge = reinterpret_cast<HalfState<(CAP == 0 ? 1 : CAP)>*>(smem + L::OFF_MERGE);
     int acc = 0;
     uint32_t aphase = 0;
+    // per-row operands and codebook constants are loaded one tile / one chunk
+    // ahead, so their L2 latency is not on the epilogue's critical path
+    auto row_of = [&](int tt) { return (int64_t)tt * 2 * BM + (int64_t)rank * BM + rl; };
+    float band_n = 0.f, xf_n = 0.f;
+    int64_t row_n = 0;
+    auto fetch_row = [&](int tt) {
+      const int64_t lr = row_of(tt);
+      const bool lv = tt < ntiles && lr < nrows;
+      band_n = lv ? p.xband[lr] : 0.f;
+      xf_n = lv ? p.xf[lr] : 0.f;
+      row_n = (lv && p.rowmap) ? (int64_t)p.rowmap[lr] : lr;
+    };
+    fetch_row(cluster);
+    float cn_n = p.cn[et];   // BN == EPI_THREADS: one constant per thread per chunk
     for (int t = cluster; t < ntiles; t += nclusters) {
-      const int64_t lrow = (int64_t)t * 2 * BM + (int64_t)rank * BM + rl;
+      const int64_t lrow = row_of(t);
       const bool live = lrow < nrows;
-      const int64_t row = (live && p.rowmap) ? (int64_t)p.rowmap[lrow] : lrow;   // output row
-      const float band = live ? p.xband[lrow] : 0.f;
-      const float xf = live ? p.xf[lrow] : 0.f;   // -2 / (row scale * codebook scale)
+      const int64_t row = row_n;                   // output row
+      const float band = band_n;
+      const float xf = xf_n;                       // -2 / (row scale * codebook scale)
+      fetch_row(t + nclusters);
       constexpr int SCAP = CAP == 0 ? 1 : CAP;
       Cands<SCAP> st;
       float M1 = __int_as_float(0x7f800000), M2 = M1;
@@ -479,7 +495,8 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       if (CAP != 0) st.init();
       for (int nc = 0; nc < nnc; nc++) {
         float* cc = cconst + acc * BN;
-        for (int i = et; i < BN; i += EPI_THREADS) cc[i] = p.cn[nc * BN + i];
+        cc[et] = cn_n;
+        cn_n = p.cn[(nc + 1 == nnc ? 0 : nc + 1) * BN + et];   // next chunk's constant, consumed next iteration
         epi_bar();
         mbar_wait(&tfull[acc], aphase);
         tc_after();
