@@ -124,13 +124,15 @@ class DataParallelVQ:
         if sum(sizes) == 0:
             from .errors import InvalidInputError
             raise InvalidInputError("batch must be nonempty")
-        # reservoir first (vq.py:203): every rank writes the tail of its shard
+        # local statistics first (the device's long pole), one packed all-reduce
+        packed = self.be.local_stats(self.state, shard, self.cfg)   # [sums | counts] fp64
+        # reservoir (vq.py:203: extended before the mask/accumulate; the ring is
+        # not read by the statistics, so enqueueing it second changes nothing):
+        # every rank writes the tail of its shard
         self.res.add_step(sizes)
         first, cnt, phys = self.res.ring_writes(self.rank, n_local)
         if cnt:
             self.be.ring_write(self.ring, shard, first, cnt, phys)
-        # local statistics, one packed all-reduce
-        packed = self.be.local_stats(self.state, shard, self.cfg)   # [sums | counts] fp64
         if self.world > 1:
             self.dist.all_reduce(packed, group=self.group)
         self.state = self.be.ema(self.state, packed)
