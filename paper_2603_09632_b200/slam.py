@@ -26,6 +26,7 @@ from .errors import InvalidInputError
 class SlamConfig:
     """The densify/prune fields of the reference SlamConfig (slam.py:36-76)."""
 
+    raster: object = None    # rasterizer.RasterConfig (None -> DEFAULT_RASTER), slam.py:76
     min_scale: float = 1e-3
     prune_opacity: float = 0.01
     coverage_alpha: float = 0.5
@@ -119,11 +120,12 @@ def densify_and_prune(field_: GaussianField, window, cfg: SlamConfig, K: Optiona
     """slam.py:601-651 — insert splats on the stride lattice of the newest
     keyframe, prune near-transparent ones, bump the generation.
 
-    Empty map: identical to the reference (every lattice pixel inserted,
-    invalid depth -> default depth).  Non-empty map: lattice pixels whose
-    voxel (``voxel_size``, default the splat footprint
-    max(min_scale, 0.5*stride*median_depth/fx)) is occupied by an existing centre (or by ``occupied``, a
-    :class:`grid.VoxelHashSet`) are skipped instead of the alpha >= 0.5 render test.
+    Reference semantics: lattice pixels whose rendered alpha (the GPU
+    rasterizer, rasterizer.render) reaches ``coverage_alpha`` are skipped.
+    Voxel variant (``occupied`` a :class:`grid.VoxelHashSet` and/or
+    ``voxel_size`` given): lattice pixels whose voxel (default size the splat
+    footprint max(min_scale, 0.5*stride*median_depth/fx)) is occupied by an
+    existing centre are skipped instead of rendering coverage.
     """
     t = nat.require_cuda()
     if len(window) == 0:
@@ -145,7 +147,13 @@ def densify_and_prune(field_: GaussianField, window, cfg: SlamConfig, K: Optiona
     else:
         depth = np.full(uu.size, median_depth)
     mu = backproject_pixels(kf.pose, intr, uu.astype(np.float64), vv.astype(np.float64), depth)
-    if len(field_):
+    if len(field_) and occupied is None and voxel_size is None:
+        from .rasterizer import DEFAULT_RASTER, render
+        alpha = render(field_, kf.pose, intr, cfg.raster if cfg.raster is not None else DEFAULT_RASTER).alpha
+        alpha = alpha if isinstance(alpha, np.ndarray) else alpha.cpu().numpy()
+        sel = ~(alpha[uu, vv] >= cfg.coverage_alpha)
+        uu, vv, depth, mu = uu[sel], vv[sel], depth[sel], mu[sel]
+    elif len(field_):
         from .grid import VoxelHashSet, pack_key
         vs = voxel_size if voxel_size is not None else max(cfg.min_scale, 0.5 * s * median_depth / intr.fx)
         occ = occupied

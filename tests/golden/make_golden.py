@@ -192,10 +192,30 @@ def gen_densify():
                           opacity=np.zeros(0), color=np.zeros((0, 3)), logits=np.zeros((0, 5)))
     cfg = slam.SlamConfig()
     out = slam.densify_and_prune(empty, win, cfg, K=5)
+    # non-empty map: the empty-map splats (some pruned, some re-weighted) seen
+    # from a nearby second keyframe -> render-coverage skipping (slam.py:610-626)
+    op = out.opacity.copy()
+    op[::7] = 0.005                                     # pruned
+    op[1::3] = rng.uniform(0.2, 0.95, op[1::3].size)
+    field1 = GaussianField(mu=out.mu, quat=out.quat, scale=out.scale * 1.5, opacity=op, color=out.color,
+                           logits=out.logits, generation=out.generation)
+    from scipy.spatial.transform import Rotation as Rt
+    pose2 = CameraPose(Rt.from_rotvec([0.02, -0.03, 0.01]).as_matrix() @ pose.rotation,
+                       pose.translation + np.array([0.05, 0.0, -0.03]))
+    depth2 = rng.uniform(0.5, 5.0, (H, W)).astype(np.float32)
+    depth2[rng.random((H, W)) < 0.2] = 0.0
+    frame2 = CameraFrame(frame_id=1, pose=pose2, color=rng.random((3, H, W)), depth=depth2)
+    win2 = slam.KeyframeWindow(4)
+    win2.insert(frame2, pose2)
+    out2 = slam.densify_and_prune(field1, win2, cfg, K=5)
     np.savez_compressed(os.path.join(OUT, "densify.npz"), depth=depth, color=color,
                         R=pose.rotation, t=pose.translation, mu=out.mu, scale=out.scale,
                         col=out.color, opacity=out.opacity, quat=out.quat,
-                        generation=np.array(out.generation))
+                        generation=np.array(out.generation),
+                        f1_mu=field1.mu, f1_quat=field1.quat, f1_scale=field1.scale, f1_opacity=field1.opacity,
+                        f1_color=field1.color, f1_logits=field1.logits, R2=pose2.rotation, t2=pose2.translation,
+                        depth2=depth2, color2=frame2.color, m2_mu=out2.mu, m2_scale=out2.scale,
+                        m2_color=out2.color, m2_opacity=out2.opacity, m2_generation=np.array(out2.generation))
 
 
 def gen_supervision():

@@ -50,6 +50,25 @@ def test_densify_empty_map_golden(xs):
     assert out.generation == int(g["generation"])
 
 
+def test_densify_nonempty_map_golden(xs):
+    """Render-coverage skipping on a non-empty map (slam.py:608-626) through the
+    GPU rasterizer: same inserted splats, prune set and order as the reference."""
+    from paper_2603_09632_b200.core import CameraPose, GaussianField
+    _, slam, _ = xs
+    g = golden("densify")
+    field = GaussianField(mu=g["f1_mu"], quat=g["f1_quat"], scale=g["f1_scale"], opacity=g["f1_opacity"],
+                          color=g["f1_color"], logits=g["f1_logits"], generation=int(g["generation"]))
+    pose2 = CameraPose(g["R2"], g["t2"])
+    win = slam.KeyframeWindow(4)
+    win.insert(slam.CameraFrame(1, pose2, g["color2"], g["depth2"]), pose2)
+    out = slam.densify_and_prune(field, win, slam.SlamConfig(), K=5)
+    assert len(out) == g["m2_mu"].shape[0]
+    for name, ref in (("mu", g["m2_mu"]), ("scale", g["m2_scale"]), ("color", g["m2_color"]),
+                      ("opacity", g["m2_opacity"])):
+        assert np.array_equal(getattr(out, name), ref), name
+    assert out.generation == int(g["m2_generation"])
+
+
 def _scene(synth, seed, H, W, F, spheres=False):
     rng = np.random.default_rng(seed)
     intr4 = (0.8 * W, 0.8 * W, (H - 1) / 2, (W - 1) / 2)
