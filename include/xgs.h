@@ -94,6 +94,13 @@ XGS_API size_t xgs_vq_step_workspace(int64_t n, int64_t k, int64_t d, int dtype,
 XGS_API int xgs_vq_assign_accumulate(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E,
                                      int64_t k, int64_t* codes, double* counts, double* sums, void* ws,
                                      size_t ws_bytes, int32_t* stats_out, void* stream);
+/* The same step with the rows in (pinned) HOST memory: x_host is copied into
+ * the device buffer x chunk by chunk on an internal stream, each chunk's copy
+ * overlapping the previous chunk's prep / screen / accumulate (the end-to-end
+ * path is PCIe-bound).  x_host may equal NULL (then x is already resident). */
+XGS_API int xgs_vq_assign_accumulate_h2d(const void* x_host, void* x, int dtype, int64_t n, int64_t d, int64_t ldx,
+                                         const double* E, int64_t k, int64_t* codes, double* counts, double* sums,
+                                         void* ws, size_t ws_bytes, int32_t* stats_out, void* stream);
 
 /* ema_step (vq.py:103-109): N' = lam N + (1-lam) c ; M' = lam M + (1-lam) s ;
  * E' = M' / (N' + eps).  Outputs may alias inputs. */

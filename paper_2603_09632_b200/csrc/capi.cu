@@ -217,6 +217,13 @@ size_t xgs_vq_step_workspace(int64_t n, int64_t k, int64_t d, int dtype, int64_t
 int xgs_vq_assign_accumulate(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E,
                              int64_t k, int64_t* codes, double* counts, double* sums, void* ws, size_t ws_bytes,
                              int32_t* stats_out, void* stream) {
+  return xgs_vq_assign_accumulate_h2d(nullptr, const_cast<void*>(x), dtype, n, d, ldx, E, k, codes, counts, sums, ws, ws_bytes,
+                                      stats_out, stream);
+}
+
+int xgs_vq_assign_accumulate_h2d(const void* x_host, void* x, int dtype, int64_t n, int64_t d, int64_t ldx,
+                                 const double* E, int64_t k, int64_t* codes, double* counts, double* sums, void* ws,
+                                 size_t ws_bytes, int32_t* stats_out, void* stream) {
   int rc = check_assign(x, dtype, n, d, ldx, E, k, codes);
   if (rc) return rc;
   if (n == 0) return fail(INVALID_INPUT, "batch must be nonempty");
@@ -228,7 +235,7 @@ int xgs_vq_assign_accumulate(const void* x, int dtype, int64_t n, int64_t d, int
   ScreenArgs a = screen_args(x, dtype, n, d, ldx, E, k, codes, ws, sbytes, &pd);
   void* acc_ws = static_cast<char*>(ws) + sbytes;
   cudaError_t e = launch_assign_accumulate(a, counts, sums, acc_ws, ws_bytes - sbytes, (cudaStream_t)stream,
-                                           stats_out);
+                                           stats_out, x_host);
   if (e != cudaSuccess) return cuda_fail(e, "xgs_vq_assign_accumulate");
   if (stats_out && (e = cudaStreamSynchronize((cudaStream_t)stream)) != cudaSuccess)
     return cuda_fail(e, "xgs_vq_assign_accumulate");

@@ -83,9 +83,12 @@ cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, 
 cudaError_t screen_finish(const ScreenArgs& a, int chunks, cudaStream_t s, int32_t* host_stats);
 
 // ---------------- row-chunk pipelined assign + accumulate (vq_pipeline.cu) ----------------
-int pipeline_chunks(int64_t n, int sm_count, int64_t* chunk_rows);
+int pipeline_chunks(int64_t n, int sm_count, int64_t* chunk_rows, bool host_src);
+// x_host (nullable): rows are streamed from this (pinned) host copy into a.x
+// chunk by chunk, each copy overlapping the previous chunk's device work
 cudaError_t launch_assign_accumulate(const ScreenArgs& a, double* counts, double* sums, void* acc_ws,
-                                     size_t acc_ws_bytes, cudaStream_t s, int32_t* host_stats);
+                                     size_t acc_ws_bytes, cudaStream_t s, int32_t* host_stats,
+                                     const void* x_host = nullptr);
 
 // ---------------- codebook update (vq_update.cu) ----------------
 size_t accumulate_workspace_bytes(int64_t n, int64_t k);

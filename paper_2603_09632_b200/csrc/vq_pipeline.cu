@@ -57,7 +57,7 @@ cudaError_t res_for(int dev, PipeRes** out) {
 
 }  // namespace
 
-int pipeline_chunks(int64_t n, int sm_count, int64_t* chunk_rows) {
+int pipeline_chunks(int64_t n, int sm_count, int64_t* chunk_rows, bool host_src) {
   // a chunk is a whole number of screening waves (one 256-row tile per CTA pair)
   const int64_t wave = (int64_t)(sm_count / 2 > 0 ? sm_count / 2 : 1) * 256;
   const int64_t waves = (n + wave - 1) / wave;
@@ -65,8 +65,9 @@ int pipeline_chunks(int64_t n, int sm_count, int64_t* chunk_rows) {
   // screening kernel about as much as they gain (2.27 ms/step at 1 chunk,
   // 2.33 at 4, 2.50 at 8), so the default is one chunk; XGS_PIPE_CHUNKS
   // overrides it for experiments.
-  int chunks = 1;
-  (void)waves;
+  // Streaming rows from host memory: the H2D copy of chunk c+1 overlaps the
+  // device work of chunk c (PCIe is ~20x slower than the step), so split.
+  int chunks = host_src ? (int)(waves / 4 > 8 ? 8 : (waves / 4 < 1 ? 1 : waves / 4)) : 1;
   if (const char* env = std::getenv("XGS_PIPE_CHUNKS")) chunks = std::atoi(env);   // tuning override
   if (chunks > kMaxChunks) chunks = kMaxChunks;
   if (chunks < 1) chunks = 1;
@@ -76,9 +77,9 @@ int pipeline_chunks(int64_t n, int sm_count, int64_t* chunk_rows) {
 }
 
 cudaError_t launch_assign_accumulate(const ScreenArgs& a, double* counts, double* sums, void* acc_ws,
-                                     size_t acc_ws_bytes, cudaStream_t s, int32_t* host_stats) {
+                                     size_t acc_ws_bytes, cudaStream_t s, int32_t* host_stats, const void* x_host) {
   int64_t crows = 0;
-  const int chunks = pipeline_chunks(a.n, a.sm_count, &crows);
+  const int chunks = pipeline_chunks(a.n, a.sm_count, &crows, x_host != nullptr);
   std::lock_guard<std::mutex> lock(g_mtx);
   int dev = 0;
   cudaError_t e;
@@ -93,6 +94,13 @@ cudaError_t launch_assign_accumulate(const ScreenArgs& a, double* counts, double
   const size_t xrow = (size_t)a.ldx * dtype_size(a.dtype);
   for (int c = 0; c < chunks; c++) {
     const int64_t r0 = c * crows, r1 = (r0 + crows < a.n) ? r0 + crows : a.n;
+    if (x_host) {   // rows [r0, r1) host -> device ahead of their prep, on the prep stream
+      const size_t off = (size_t)r0 * xrow, bytes = (size_t)(r1 - r0) * xrow;
+      if ((e = cudaMemcpyAsync(static_cast<char*>(const_cast<void*>(a.x)) + off,
+                               static_cast<const char*>(x_host) + off, bytes, cudaMemcpyHostToDevice, r->sp)) !=
+          cudaSuccess)
+        return e;
+    }
     if ((e = screen_prep_rows(a, r0, r1, r->sp)) != cudaSuccess) return e;
     if ((e = cudaEventRecord(r->evp[c], r->sp)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(s, r->evp[c], 0)) != cudaSuccess) return e;

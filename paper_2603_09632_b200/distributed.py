@@ -160,6 +160,7 @@ class CudaBackend:
         from . import _native as nat
         self.nat = nat
         self.t = nat.require_cuda()
+        self._h2d, self._pending_host = {}, None
         self.K, self.D, self.lam, self.eps = K, D, lam, eps
 
     def int_tensor(self, v):
@@ -169,8 +170,21 @@ class CudaBackend:
         return int(shard.shape[0])
 
     def prepare(self, shard):
-        """Host (pinned) or device rows -> one device copy, reused by every kernel."""
+        """Device rows as they are; pinned host rows get a (cached) device buffer
+        that the statistics call fills chunk by chunk (H2D overlapped with the
+        device work), see local_stats."""
+        t = self.t
+        if isinstance(shard, t.Tensor) and shard.device.type == "cpu" and shard.is_pinned() and shard.dim() == 2 \
+                and shard.is_contiguous() and shard.dtype in (t.float32, t.float64, t.bfloat16):
+            key = (tuple(shard.shape), shard.dtype)
+            buf = self._h2d.get(key)
+            if buf is None:
+                self._h2d = {key: t.empty(shard.shape, dtype=shard.dtype, device="cuda")}
+                buf = self._h2d[key]
+            self._pending_host = shard
+            return buf
         from .vq import _rows
+        self._pending_host = None
         return _rows(shard)[0]
 
     def new_ring(self, cap):
@@ -195,9 +209,14 @@ class CudaBackend:
         if n == 0:
             packed.zero_()
             return packed
+        host = getattr(self, "_pending_host", None)
+        self._pending_host = None
+        if host is not None and not all_pass_provable(cfg.gamma, self.K):
+            shard.copy_(host)          # the exact confidence path needs the whole batch first
+            host = None
         xt, dt, n, d, ldx = _rows(shard)
         if all_pass_provable(cfg.gamma, self.K):
-            _assign_accumulate_dev(xt, dt, n, d, ldx, E, self.K, counts=counts, sums=sums)
+            _assign_accumulate_dev(xt, dt, n, d, ldx, E, self.K, counts=counts, sums=sums, x_host=host)
             return packed
         else:
             _, _, codes, mask = _exact_dev(xt, dt, n, d, ldx, E, self.K, nat.EX_CODE | nat.EX_MASK,

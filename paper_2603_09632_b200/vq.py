@@ -161,10 +161,11 @@ def _accumulate_dev(xt, dt, n, d, ldx, codes, mask, K):
     return counts, sums
 
 
-def _assign_accumulate_dev(xt, dt, n, d, ldx, E, K, counts=None, sums=None):
+def _assign_accumulate_dev(xt, dt, n, d, ldx, E, K, counts=None, sums=None, x_host=None):
     """assign_batch + accumulate(batch) for an all-pass mask (vq.py:206) in one
     row-chunk-pipelined native call; bit-identical to _assign_dev followed by
-    _accumulate_dev."""
+    _accumulate_dev.  ``x_host`` (pinned CPU tensor, same layout as ``xt``):
+    the rows are streamed into ``xt`` chunk by chunk inside the call."""
     t = nat.torch()
     codes = t.empty(n, dtype=t.int64, device="cuda")
     if counts is None:
@@ -172,8 +173,8 @@ def _assign_accumulate_dev(xt, dt, n, d, ldx, E, K, counts=None, sums=None):
     if sums is None:
         sums = t.empty((K, d), dtype=t.float64, device="cuda")
     ws = nat.workspace("step", nat.lib().xgs_vq_step_workspace(n, K, d, dt, ldx))
-    nat.call("xgs_vq_assign_accumulate", nat.ptr(xt), dt, n, d, ldx, nat.ptr(E), K, nat.ptr(codes),
-             nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel(), None, nat.stream_ptr())
+    nat.call("xgs_vq_assign_accumulate_h2d", nat.ptr(x_host), nat.ptr(xt), dt, n, d, ldx, nat.ptr(E), K,
+             nat.ptr(codes), nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel(), None, nat.stream_ptr())
     return codes, counts, sums
 
 

@@ -340,3 +340,25 @@ def test_float64_and_strided_inputs(xv):
     st = xv.accumulate(xt, make_cb(xv, E).to_device())
     c, s = on.accumulate(xt.cpu().numpy(), got, 300)
     assert np.array_equal(st.counts.cpu().numpy(), c) and np.array_equal(st.sums.cpu().numpy(), s)
+
+
+def test_pinned_host_batch_streams_bit_identical(xv):
+    """DataParallelVQ on a pinned host batch (rows streamed H2D chunk by chunk
+    inside the pipelined call) == the same steps on the device batch."""
+    import torch
+    from paper_2603_09632_b200.distributed import CudaBackend, DataParallelVQ
+    rng = np.random.default_rng(77)
+    n, K, D = 400_000, 256, 64
+    x = mixture(rng, n, D, K, 0.05)
+    E0 = torch.from_numpy(mixture(rng, K, D, K, 0.05).astype(np.float64)).cuda()
+    cfg = xv.VqConfig(K=K, lam=0.99, gamma=0.5 / K, delta_dead=1e-3, reservoir_capacity=512)
+    runs = []
+    for src in (torch.from_numpy(x).cuda(), torch.from_numpy(x).pin_memory()):
+        st = (E0.clone(), torch.zeros(K, dtype=torch.float64, device="cuda"),
+              torch.zeros(K, D, dtype=torch.float64, device="cuda"))
+        vq = DataParallelVQ(st, cfg, np.random.default_rng(3), CudaBackend(K, D, 0.99, 1e-5))
+        for _ in range(3):
+            vq.step(src, [n])
+        runs.append([s.cpu().numpy() for s in vq.state] + [vq.ring.cpu().numpy()])
+    for a, b in zip(*runs):
+        assert np.array_equal(a, b)
