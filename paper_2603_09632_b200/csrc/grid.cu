@@ -936,45 +936,26 @@ cudaError_t exclusive_scan(const T* in, int64_t n, int32_t* out, int32_t* block_
 }
 
 // ---------------------------------------------------------------- G3 select
-// Over the sorted (key, pid) items: a segment head (first item of a voxel)
-// inserts its key into the map set; if the key was absent the voxel's
-// representative pixel is flagged new and remembers the head's sorted position.
-// In pixel-ordered input the head IS the lowest pixel id; after the fused
-// front end's unordered compaction (min_scan) the representative is the
-// segment's minimum pixel id: segments of up to kSelScan items are scanned by
-// the head's thread, longer ones are queued for a warp-parallel pass.
-constexpr int kSelScan = 16;
-
-__device__ __forceinline__ void select_emit(unsigned long long* table, uint64_t mask, uint64_t key, uint32_t pid,
-                                            int64_t i, unsigned* flag_bits, int32_t* head_pos, unsigned& newc) {
-  if (hs_insert(table, mask, key)) {
-    atomicOr(flag_bits + (pid >> 5), 1u << (pid & 31));
-    head_pos[pid] = (int32_t)i;
-    newc++;
-  }
-}
-
+// Over the sorted (key, pid) items: a segment head (first item of a voxel, i.e.
+// its lowest pixel id -- the input is in pixel order and the sort is stable)
+// inserts its key into the map set; if the key was absent the head pixel is
+// flagged new and remembers its sorted position.
 __global__ void __launch_bounds__(256)
 grid_select_kernel(const uint64_t* __restrict__ k, const uint32_t* __restrict__ v, int64_t n,
                    unsigned long long* table, uint64_t mask, unsigned long long* set_count, unsigned* flag_bits,
-                   int32_t* head_pos, unsigned long long* nvox, bool min_scan, int32_t* longq,
-                   unsigned long long* nlong) {
+                   int32_t* head_pos, unsigned long long* nvox) {
   unsigned newc = 0, vox = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t key = k[i];
     if (key == KEY_INVALID) continue;
     if (i > 0 && k[i - 1] == key) continue;
     vox++;
-    uint32_t pid = v[i];
-    if (min_scan) {
-      int64_t j = i + 1;
-      for (; j < n && j <= i + kSelScan && k[j] == key; j++) pid = min(pid, v[j]);
-      if (j < n && j > i + kSelScan && k[j] == key) {   // long segment: warp pass
-        longq[atomicAdd(nlong, 1ull)] = (int32_t)i;
-        continue;
-      }
+    if (hs_insert(table, mask, key)) {
+      const uint32_t pid = v[i];
+      atomicOr(flag_bits + (pid >> 5), 1u << (pid & 31));
+      head_pos[pid] = (int32_t)i;
+      newc++;
     }
-    select_emit(table, mask, key, pid, i, flag_bits, head_pos, newc);
   }
   for (int o = 16; o; o >>= 1) {
     newc += __shfl_xor_sync(FULL, newc, o);
@@ -984,31 +965,6 @@ grid_select_kernel(const uint64_t* __restrict__ k, const uint32_t* __restrict__ 
     if (newc) atomicAdd(set_count, (unsigned long long)newc);
     if (vox) atomicAdd(nvox, (unsigned long long)vox);
   }
-}
-
-// one warp per queued long segment: coalesced min over the whole segment
-__global__ void __launch_bounds__(256)
-grid_select_long_kernel(const uint64_t* __restrict__ k, const uint32_t* __restrict__ v, int64_t n,
-                        unsigned long long* table, uint64_t mask, unsigned long long* set_count, unsigned* flag_bits,
-                        int32_t* head_pos, const int32_t* __restrict__ longq, const unsigned long long* nlong) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nq = (int64_t)*nlong;
-  unsigned newc = 0;
-  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nq;
-       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t i = longq[w];
-    const uint64_t key = k[i];
-    uint32_t pid = 0xffffffffu;
-    for (int64_t b = i;; b += 32) {
-      const int64_t j = b + lane;
-      const bool in = j < n && k[j] == key;
-      if (in) pid = min(pid, v[j]);
-      if (__ballot_sync(FULL, in) != FULL) break;   // segment ends inside this window
-    }
-    for (int o = 16; o; o >>= 1) pid = min(pid, __shfl_xor_sync(FULL, pid, o));
-    if (lane == 0) select_emit(table, mask, key, pid, i, flag_bits, head_pos, newc);
-  }
-  if (lane == 0 && newc) atomicAdd(set_count, (unsigned long long)newc);
 }
 
 // ---------------------------------------------------------------- G5 emit
@@ -1427,15 +1383,9 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   {
     ProfScope prof("grid_select", s);
     cudaMemsetAsync(flag, 0, (size_t)nwords * 4, s);
-    int32_t* longq = reinterpret_cast<int32_t*>(k1);   // the sort's ping-pong buffer is free now
-    cudaMemsetAsync(cnts + 3, 0, 8, s);
     grid_select_kernel<<<grid_blocks(nitems, 256, sms), 256, 0, s>>>(k0, v0, nitems, hs->table, (uint64_t)hs->cap - 1,
-                                                                     hs->count_dev, reinterpret_cast<unsigned*>(flag), head, cnts + 1, false,
-                                                                     longq, cnts + 3); count_launches(1);
-    if (false) {
-      grid_select_long_kernel<<<sms * 4, 256, 0, s>>>(k0, v0, nitems, hs->table, (uint64_t)hs->cap - 1, hs->count_dev,
-                                                      reinterpret_cast<unsigned*>(flag), head, longq, cnts + 3); count_launches(1);
-    }
+                                                                     hs->count_dev, reinterpret_cast<unsigned*>(flag), head, cnts + 1);
+    count_launches(1);
   }
   {
     ProfScope prof("grid_emit", s);

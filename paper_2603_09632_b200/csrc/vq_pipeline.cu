@@ -11,9 +11,11 @@
 //   caller stream : wait ev_prep[c]; screen + re-rank(c) -> ev_codes[c]
 //   acc stream    : wait ev_codes[c]; accumulate(c, continue chains)
 //
-// so prep(c+1) and accumulate(c-1) run on the SM resources the persistent
-// screening kernel leaves free (it holds ~128 regs x 352 threads and 217 KB of
-// smem per SM; prep blocks and 2-warp chain blocks fit beside it).
+// so prep(c+1) and accumulate(c-1) can run on the SM resources the persistent
+// screening kernel leaves free.  Measured on the B200 the co-resident blocks
+// slow the screen about as much as they gain, so device-resident batches use
+// one chunk; host batches (xgs_vq_assign_accumulate_h2d) use up to 8, and the
+// H2D copy of chunk c+1 hides the device work of chunk c.
 // accumulate(c) continues every (k, d) chain from accumulate(c-1), so the
 // result is bit-identical to one accumulate over all rows (np.add.at order).
 #include <cstdlib>
