@@ -226,9 +226,24 @@ def run_grid(torch, steps, cpu=True):
         kb = 4 if passes <= 4 else 8
         sort_bytes = float(n_sorted) * (passes * (kb + 2 * (kb + 4)) + 2 * (8 + kb))
         sort_gbs = sort_bytes / (prof["grid_sort"] * 1e-3) / 1e9 if prof["grid_sort"] else None
-        # keys + compaction: depth read 4 B + key write 8 B per pixel, compaction reads the
-        # key 3x (self, left, up; L2 for the neighbours) and writes 12 B per surviving item
-        keys_bytes = 12.0 * npix + 8.0 * npix + 12.0 * n_sorted
+        # fused front end: depth read 4 B per pixel + 12 B (key + pixel id) per surviving item
+        keys_bytes = 4.0 * npix + 12.0 * n_sorted
+        # end to end through the public API: frames in pinned host memory (H2D of depth + colour),
+        # the batch, the new Gaussians back to host numpy (GridSampleResult.to_numpy)
+        Dh, Ch = torch.from_numpy(D).pin_memory(), torch.from_numpy(C).pin_memory()
+        e2e = []
+        for it in range(3):
+            hs = VoxelHashSet(GRID_MAP + GRID_F * GRID_H * GRID_W)
+            hs.insert(warm)
+            gs = GridSampler(GRID_INTR, voxel, occupied=hs)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            host_out = gs.sample(Dh, (Rd, Td), Ch).to_numpy()
+            e2e.append((time.perf_counter() - t0) * 1e3)
+            hs.close()
+        e2e_ms = float(np.median(e2e))
+        e2e_h2d = Dh.numel() * 4 + Ch.numel()
+        e2e_d2h = sum(v.nbytes for v in host_out.values() if isinstance(v, np.ndarray))
         out[str(voxel)] = {"Mpts_per_s": npix / (ms * 1e-3) / 1e6, "ms_per_batch": ms, "pixels": npix,
                            "valid_points": n_valid, "new_voxels": n_new, "map_voxels_before": map_size,
                            "sorted_items": n_sorted, "sort_passes": passes, "per_kernel_ms": prof,
@@ -236,8 +251,11 @@ def run_grid(torch, steps, cpu=True):
                                         "achieved": sort_gbs, "peak": pk_["hbm_gbs"], "unit": "GB/s",
                                         "frac": sort_gbs / pk_["hbm_gbs"] if sort_gbs else None,
                                         "algorithmic_bytes": sort_bytes},
-                           "keys_compaction_GBps": keys_bytes / (prof["grid_keys"] * 1e-3) / 1e9
-                           if prof["grid_keys"] else None}
+                           "front_GBps": keys_bytes / (prof["grid_keys"] * 1e-3) / 1e9
+                           if prof["grid_keys"] else None,
+                           "e2e": {"Mpts_per_s": npix / (e2e_ms * 1e-3) / 1e6, "ms_per_batch": e2e_ms,
+                                   "h2d_bytes": e2e_h2d, "d2h_bytes": e2e_d2h,
+                                   "note": "host wall clock around sample() + to_numpy(), pinned host frames"}}
     if cpu:
         from oracle import grid as og
         t0 = time.perf_counter()

@@ -343,7 +343,7 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
   const float iv = cf.inv_voxel;
   // per-frame constants pre-scaled by 1/voxel: q_i = p_i / voxel = d * (Pr_i + Pc_ji) + Qs_i,
   // magnitude bound M_i / voxel = d * (Cr_i + Cc_ji) + Ds_i
-  float R0[3], R2[3], A0[3], A2[3], Qs[3], Ds[3];
+  float R0[3], R2[3], A0[3], A2[3], Qs[3], Ds[3], Dmax;
   float Pc[4][3], Cc[4][3];
   unsigned colmask = 0;
   {
@@ -360,6 +360,7 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
       Qs[i] = -fmaf(r2, t2, fmaf(r1, t1, r0 * t0)) * iv;
       Ds[i] = fmaf(fabsf(r2), fabsf(t2), fmaf(fabsf(r1), fabsf(t1), fabsf(r0) * fabsf(t0))) * iv;
     }
+    Dmax = fmaxf(fmaxf(Ds[0], Ds[1]), Ds[2]);
 #pragma unroll
     for (int j = 0; j < 4; j++) {
       const float vv = (float)(c0 + j);
@@ -404,15 +405,16 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
     for (int j = 0; j < 4; j++) {
       const float d = dv[j];
       if (!((rowmask >> j) & 1u) || !(d > 0.f)) continue;
-      bool ok = true;
+      // one guard band for the three axes from the largest magnitude bound
+      const float M = fmaf(d, fmaxf(fmaxf(Cr[0] + Cc[j][0], Cr[1] + Cc[j][1]), Cr[2] + Cc[j][2]), Dmax);
+      const float dl = fmaf(M, 0x1p-20f * 1.002f + 0x1p-21f, 0x1p-40f);
+      bool ok = M < 1048000.f;
       int qi[3];
 #pragma unroll
       for (int i = 0; i < 3; i++) {
         const float q = fmaf(d, Pr[i] + Pc[j][i], Qs[i]);
-        const float M = fmaf(d, Cr[i] + Cc[j][i], Ds[i]);        // >= |q_i| and >= the magnitudes rounded
-        const float dl = fmaf(M, 0x1p-20f * 1.002f + 0x1p-21f, 0x1p-40f);
         const float fl = floorf(__fsub_rd(q, dl));
-        ok = ok && __fadd_ru(q, dl) < fl + 1.f && M < 1048000.f;   // one floor on [q-dl, q+dl]
+        ok = ok && __fadd_ru(q, dl) < fl + 1.f;   // one floor on [q-dl, q+dl]
         qi[i] = (int)fl + (int)KEY_BIAS;
       }
       if (ok) {
