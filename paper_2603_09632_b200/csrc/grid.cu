@@ -272,10 +272,11 @@ compact_keys_kernel(const uint64_t* __restrict__ kin, int64_t n, int64_t W, uint
 // compaction in one pass over the depth.  A block owns FK_ROWS rows of one
 // frame (thread t = columns 4t..4t+3), recomputes the keys of the row above
 // as the halo, stages its surviving (key, pixel) items in shared memory in
-// pixel order and publishes its count through a decoupled look-back over the
-// blocks (dynamic block ids, so every predecessor is already running): the
-// output is in ascending pixel order, exactly as the two-kernel path writes
-// it, and the stable sort keeps each voxel's lowest pixel id first.
+// pixel order and writes them to its own fixed slot plus a count; the sort's
+// rekey pass gathers the slots densely after an exclusive scan of the counts
+// (no block waits on another), so the items enter the sort in ascending pixel
+// order, exactly as the two-kernel path writes them, and the stable sort keeps
+// each voxel's lowest pixel id first.
 //
 // Keys are evaluated in fp32 with a rigorous error bound first.  The
 // back-projection is regrouped as p_i = d * P_i + Q_i with
@@ -312,8 +313,7 @@ __device__ __forceinline__ uint64_t key_exact(const double* R, const double* T, 
 __global__ void __launch_bounds__(384, 2)
 grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int stride, const double* __restrict__ rot,
                   const double* __restrict__ trans, Cam cam, CamF cf, uint64_t* __restrict__ kout,
-                  uint32_t* __restrict__ vout, int* bbox, unsigned long long* cnts, unsigned* block_counter,
-                  unsigned long long* status) {
+                  uint32_t* __restrict__ vout, int* bbox, unsigned long long* cnts, int32_t* __restrict__ block_count) {
   constexpr int NR = FK_ROWS;
   __shared__ uint64_t s_last[NR][32];
   __shared__ uint32_t s_wsum[NR][32];
@@ -326,7 +326,7 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
   uint64_t* sk = reinterpret_cast<uint64_t*>(front_smem);
   uint32_t* sv = reinterpret_cast<uint32_t*>(front_smem + (size_t)NR * W * 8);
   if (threadIdx.x == 0) {
-    s_bid = atomicAdd(block_counter, 1u);
+    s_bid = blockIdx.x;
     s_npend = 0;
   }
   if (threadIdx.x < 6) s_box[threadIdx.x] = threadIdx.x < 3 ? INT_MAX : INT_MIN;
@@ -496,8 +496,6 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
   }
   __syncthreads();
   const uint32_t run = s_rowbase[NR];
-  // publish this block's count now; its look-back runs after the exact keys
-  if (threadIdx.x == 0) atomicExch(status + bid, (bid == 0 ? LB_PRE : LB_AGG) | run);
   // ---- exact fp64 keys of the pending pixels, one lane each ----
   {
     const uint32_t np = s_npend;
@@ -526,28 +524,16 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
     }
   }
   __syncthreads();
-  // decoupled look-back over the blocks (pixel order) for the output offset
   if (threadIdx.x == 0) {
-    unsigned long long excl = 0;
-    if (bid != 0) {
-      for (int64_t j = (int64_t)bid - 1; j >= 0; j--) {
-        unsigned long long st;
-        do {
-          st = *reinterpret_cast<volatile unsigned long long*>(status + j);
-        } while ((st & ~LB_VAL) == 0);
-        excl += st & LB_VAL;
-        if (st & LB_PRE) break;
-      }
-      atomicExch(status + bid, LB_PRE | (excl + run));
-    }
+    block_count[bid] = (int32_t)run;
     if (run) atomicAdd(cnts + 2, (unsigned long long)run);
-    s_rowbase[0] = (uint32_t)excl;
   }
-  __syncthreads();
-  // copy out in pixel order (pixels resolved to invalid stay as KEY_INVALID
-  // items and sort last); the voxel bounding box over the survivors equals the
-  // box over all valid pixels (every dropped pixel repeats a survivor's key)
-  const uint32_t gbase = s_rowbase[0];
+  // copy out to this block's slot (FK_ROWS * W items; the rekey pass gathers
+  // the slots densely in block = pixel order, so no block waits on another);
+  // pixels resolved to invalid stay as KEY_INVALID items and sort last; the
+  // voxel bounding box over the survivors equals the box over all valid pixels
+  // (every dropped pixel repeats a survivor's key)
+  const size_t gbase = ((size_t)f * H + r0) * (size_t)W;   // the block's own pixels bound its survivors
   int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
   for (uint32_t i = threadIdx.x; i < run; i += blockDim.x) {
     const uint64_t key = sk[i];
@@ -650,6 +636,26 @@ template <typename K>
 __global__ void rekey_kernel(const uint64_t* __restrict__ kin, int64_t n, RelKey rk, K* __restrict__ kout) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     kout[i] = (K)rk(kin[i]);
+}
+
+// fused front end: gather the per-block slots densely (block order = pixel
+// order) while converting to relative keys; block_off = exclusive scan of the
+// block counts, n = total items
+template <typename K>
+__global__ void rekey_gather_kernel(const uint64_t* __restrict__ slot_k, const uint32_t* __restrict__ slot_v,
+                                    const int32_t* __restrict__ block_off, int64_t nblocks, int64_t H, int64_t W,
+                                    int64_t n, RelKey rk, K* __restrict__ kout, uint32_t* __restrict__ vout) {
+  const int64_t rbf = (H + FK_ROWS - 1) / FK_ROWS;
+  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {
+    const int64_t o = block_off[b], e = b + 1 < nblocks ? block_off[b + 1] : n;
+    const int64_t base = ((b / rbf) * H + (b % rbf) * FK_ROWS) * W;   // the block's first pixel
+    const uint64_t* sk = slot_k + base;
+    const uint32_t* sv = slot_v + base;
+    for (int64_t i = threadIdx.x; i < e - o; i += blockDim.x) {
+      kout[o + i] = (K)rk(sk[i]);
+      vout[o + i] = sv[i];
+    }
+  }
 }
 
 // back to the biased 63-bit voxel keys after the sort (select / emit use them)
@@ -927,10 +933,31 @@ scan_apply_kernel(const T* __restrict__ in, int64_t n, const int32_t* __restrict
   }
 }
 
+// one-CTA in-place exclusive scan for short arrays (one launch instead of three)
+__global__ void __launch_bounds__(1024) scan_small_kernel(int32_t* a, int64_t n, int32_t* grand) {
+  __shared__ int32_t sm[32];
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t b0 = threadIdx.x * per, b1 = min(n, b0 + per);
+  int32_t s = 0;
+  for (int64_t b = b0; b < b1; b++) s += a[b];
+  int32_t total;
+  int32_t run = block_excl_scan<int32_t>(s, sm, &total);
+  for (int64_t b = b0; b < b1; b++) {
+    const int32_t c = a[b];
+    a[b] = run;
+    run += c;
+  }
+  if (threadIdx.x == 0 && grand) *grand = total;
+}
+
 template <typename T>
 cudaError_t exclusive_scan(const T* in, int64_t n, int32_t* out, int32_t* block_sums, int32_t* grand, cudaStream_t s) {
   const int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (nb == 0) return cudaSuccess;
+  if (n <= 65536 && (const void*)in == (const void*)out && sizeof(T) == 4) {
+    scan_small_kernel<<<1, 1024, 0, s>>>(out, n, grand); count_launches(1);
+    return cudaGetLastError();
+  }
   scan_reduce_kernel<T><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, n, block_sums); count_launches(1);
   scan_sums_kernel<<<1, 1024, 0, s>>>(block_sums, nb, grand); count_launches(1);
   scan_apply_kernel<T><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, n, block_sums, out); count_launches(1);
@@ -1287,31 +1314,30 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   unsigned long long* cnts = reinterpret_cast<unsigned long long*>(b + w.off_misc + 64);  // nvalid, nvox
   int32_t* grand = reinterpret_cast<int32_t*>(b + w.off_misc + 128);
   unsigned long long* lb_status = reinterpret_cast<unsigned long long*>(b + w.off_lb);
+  int32_t* block_count = reinterpret_cast<int32_t*>(lb_status);   // fused front end: per-block item counts
   out.n_new = out.n_valid = out.n_voxels = 0;
   out.n_sorted = out.sort_passes = 0;
   if (npix == 0) return cudaSuccess;
   cudaError_t e;
   const Cam cam{in.fx, in.fy, in.cx, in.cy, in.voxel, 1.0 / in.voxel};
   const bool compact = in.mode == 0;   // first-pick: dedup runs + compaction before the sort
-  bool fused = false;                  // fused front end (unordered compaction)
+  bool fused = false;                  // fused front end (per-block slots, gathered by the rekey pass)
+  int64_t fblocks = 0;
   const int64_t nwords = (npix + 31) / 32;
   {
     ProfScope prof("grid_keys", s);
     init_bbox_kernel<<<1, 32, 0, s>>>(bbox, cnts); count_launches(1);
     cudaMemsetAsync(cnts + 1, 0, 40, s);
     const bool vec4 = (in.W % 4 == 0) && (reinterpret_cast<uintptr_t>(in.depth) % 16 == 0);
-    const int64_t fblocks = in.frames * ((in.H + FK_ROWS - 1) / FK_ROWS);
+    fblocks = in.frames * ((in.H + FK_ROWS - 1) / FK_ROWS);
     fused = compact && vec4 && in.W <= 2048 && fblocks <= w.lb_entries;
     if (fused) {
       const CamF cf{(float)in.cx, (float)in.cy, (float)(1.0 / in.fx), (float)(1.0 / in.fy), (float)(1.0 / in.voxel)};
       const unsigned nt = (unsigned)((in.W / 4 + 31) / 32 * 32);
       const size_t fsmem = (size_t)FK_ROWS * in.W * 12;
       if ((e = front_init()) != cudaSuccess) return e;
-      unsigned* block_counter = reinterpret_cast<unsigned*>(cnts + 4);
-      cudaMemsetAsync(block_counter, 0, 4, s);
-      cudaMemsetAsync(lb_status, 0, sizeof(unsigned long long) * fblocks, s);
       grid_front_kernel<<<(unsigned)fblocks, nt, fsmem, s>>>(in.depth, in.H, in.W, in.stride, in.rot, in.trans, cam, cf,
-                                                              k0, v0, bbox, cnts, block_counter, lb_status); count_launches(1);
+                                                              k0, v0, bbox, cnts, block_count); count_launches(1);
     } else {
     grid_keys_kernel<<<grid_blocks(vec4 ? npix / 4 : npix, 256, sms), 256, 0, s>>>(
         in.depth, npix, in.H, in.W, in.stride, in.rot, in.trans, cam, compact ? k1 : k0, compact ? nullptr : v0,
@@ -1362,14 +1388,29 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     ProfScope prof("grid_sort", s);
     // relative keys once (u32 when they fit), LSD passes, biased keys back into k0
     const unsigned rb = grid_blocks(nitems, 256, sms);
+    if (fused) {   // block slots -> dense: exclusive scan of the block counts
+      if ((e = exclusive_scan_i32(block_count, fblocks, block_count, ssum, nullptr, s)) != cudaSuccess) return e;
+    }
     if (bits <= 32) {
       uint32_t* r0 = reinterpret_cast<uint32_t*>(k1);
       uint32_t* r1 = r0 + nitems;
-      rekey_kernel<uint32_t><<<rb, 256, 0, s>>>(k0, nitems, rk, r0); count_launches(1);
+      if (fused) {   // items land in (r0, v1); the slots in (k0, v0) are dead afterwards
+        rekey_gather_kernel<uint32_t><<<grid_blocks(fblocks, 1, sms), 256, 0, s>>>(k0, v0, block_count, fblocks, in.H, in.W,
+                                                                                   nitems, rk, r0, v1); count_launches(1);
+        uint32_t* t = v0; v0 = v1; v1 = t;
+      } else {
+        rekey_kernel<uint32_t><<<rb, 256, 0, s>>>(k0, nitems, rk, r0); count_launches(1);
+      }
       if ((e = lsd_passes<uint32_t>(r0, v0, r1, v1, nitems, bits, hist, ssum, s)) != cudaSuccess) return e;
       unrekey_kernel<uint32_t><<<rb, 256, 0, s>>>(r0, nitems, rk, bits, k0); count_launches(1);
     } else {
-      rekey_kernel<uint64_t><<<rb, 256, 0, s>>>(k0, nitems, rk, k1); count_launches(1);
+      if (fused) {
+        rekey_gather_kernel<uint64_t><<<grid_blocks(fblocks, 1, sms), 256, 0, s>>>(k0, v0, block_count, fblocks, in.H, in.W,
+                                                                                   nitems, rk, k1, v1); count_launches(1);
+        uint32_t* t = v0; v0 = v1; v1 = t;
+      } else {
+        rekey_kernel<uint64_t><<<rb, 256, 0, s>>>(k0, nitems, rk, k1); count_launches(1);
+      }
       uint64_t* r0 = k1;
       uint64_t* r1 = k0;
       if ((e = lsd_passes<uint64_t>(r0, v0, r1, v1, nitems, bits, hist, ssum, s)) != cudaSuccess) return e;
