@@ -275,6 +275,32 @@ acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
   if (d0 == 0) counts[code] = (cont ? counts[code] : 0.0) + (double)(end - beg);   // integer-valued: exact
 }
 
+// Small batches (n <= kSmallRows, e.g. the per-frame C4 stream): one launch,
+// one warp per (code, 32-dim chunk) walking all n rows in ascending order and
+// adding the rows of its code -- the same per-(k, d) sequential chains in row
+// order (np.add.at) without the counting-sort kernels.
+constexpr int64_t kSmallRows = 1024;
+template <typename X>
+__global__ void __launch_bounds__(256)
+acc_small_kernel(const X* __restrict__ x, int64_t n, int64_t d, int64_t ldx, const int64_t* __restrict__ codes,
+                 const uint8_t* __restrict__ mask, int64_t k, double* __restrict__ counts, double* __restrict__ sums,
+                 int cont) {
+  const int lane = threadIdx.x & 31;
+  const int64_t chunks = (d + 31) / 32;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= k * chunks) return;
+  const int64_t code = w / chunks, j = (w - code * chunks) * 32 + lane;
+  double acc = (cont && j < d) ? sums[code * d + j] : 0.0;
+  int64_t cnt = 0;
+  for (int64_t r = 0; r < n; r++) {
+    if (row_code(codes, mask, r) != (int)code) continue;
+    cnt++;
+    if (j < d) acc = dadd(acc, ld64(x + r * ldx, j));
+  }
+  if (j < d) sums[code * d + j] = acc;
+  if (j == 0) counts[code] = (cont ? counts[code] : 0.0) + (double)cnt;
+}
+
 template <typename X, int VEC>
 cudaError_t launch_chain(const X* x, int64_t d, int64_t ldx, int64_t k, const int32_t* cs,
                          const int32_t* sorted, const int32_t* order, double* counts, double* sums,
@@ -354,6 +380,17 @@ cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, in
   int32_t* sorted = reinterpret_cast<int32_t*>(w + p.off_sorted);
   int32_t* order = reinterpret_cast<int32_t*>(w + p.off_order);
   ProfScope prof("vq_accumulate", s);
+  if (n <= kSmallRows) {
+    const int64_t warps = k * ((d + 31) / 32);
+    const unsigned blocks = (unsigned)((warps + 7) / 8);
+    switch (dtype) {
+      case F32: acc_small_kernel<float><<<blocks, 256, 0, s>>>((const float*)x, n, d, ldx, codes, mask, k, counts, sums, cont); break;
+      case F64: acc_small_kernel<double><<<blocks, 256, 0, s>>>((const double*)x, n, d, ldx, codes, mask, k, counts, sums, cont); break;
+      default: acc_small_kernel<uint16_t><<<blocks, 256, 0, s>>>((const uint16_t*)x, n, d, ldx, codes, mask, k, counts, sums, cont);
+    }
+    count_launches(1);
+    return cudaGetLastError();
+  }
   cudaError_t e = cudaMemsetAsync(tile_counts, 0, sizeof(int32_t) * (size_t)p.tiles * (size_t)k, s);
   if (e != cudaSuccess) return e;
   if (n > 0) {
