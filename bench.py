@@ -439,6 +439,51 @@ def run_targets(torch, iters, cpu=True):
     return out
 
 
+def run_init(torch, cpu=True):
+    """codebook initialisation -- seed_from_samples (K-1
+    farthest-point passes, queued without host syncs) then warm_start, on a
+    16,384 x 512 fp32 buffer with the C2 codebook size K=1024."""
+    import paper_2603_09632_b200 as xv
+    n, D, K = 16384, 512, 1024
+    g = torch.Generator(device="cuda")
+    g.manual_seed(70)
+    C = torch.randn(256, D, generator=g, device="cuda")
+    lab = torch.randint(0, 256, (n,), generator=g, device="cuda")
+    buf = C[lab] / C[lab].norm(dim=1, keepdim=True) + 0.05 * torch.randn(n, D, generator=g, device="cuda")
+    buf = (buf / buf.norm(dim=1, keepdim=True)).contiguous()
+    cfg = xv.VqConfig(K=K, gamma=0.5 / K)
+    xv.seed_from_samples(buf[:1024], 8)
+    torch.cuda.synchronize()
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record()
+    seeds = xv.seed_from_samples(buf, K)
+    e1.record()
+    cb = xv.Codebook._make(seeds, torch.zeros(K, dtype=torch.float64, device="cuda"), torch.zeros_like(seeds), 0.99,
+                           1e-5, xv.FeatureReservoir(16, D))
+    ws = xv.warm_start(buf, cb, cfg)
+    e2.record()
+    torch.cuda.synchronize()
+    ms_seed, ms_warm = e0.elapsed_time(e1), e1.elapsed_time(e2)
+    step_bytes = n * D * 4 + n * 8 * 2                 # rows + min_d read/write per seed pass
+    out = {"buffer_rows": n, "D": D, "K": K, "seed_ms": ms_seed, "seed_us_per_pass": ms_seed * 1e3 / (K - 1),
+           "seed_pass_GB_per_s": step_bytes * (K - 1) / (ms_seed * 1e-3) / 1e9,
+           "warm_start_ms": ms_warm, "warm_start_used": ws.used,
+           "workload": "16384 x 512 fp32 unit-norm 256-centre mixture (seed 70), K=1024; the buffer is L2-resident"}
+    if cpu:
+        from oracle import vq as ov
+        sample_k = 24
+        bh = buf.cpu().numpy()
+        t0 = time.perf_counter()
+        ov.seed_from_samples(bh, sample_k)
+        el = time.perf_counter() - t0
+        out["cpu_baseline"] = {"seed_ms_extrapolated": el * 1e3 * (K - 1) / (sample_k - 1), "cores": 1,
+                               "kind": "port", "sample": f"{sample_k} seeds through oracle/vq.py (NumPy), "
+                                                         f"x{(K - 1) / (sample_k - 1):.1f} (cost is linear in K)"}
+    del buf, seeds, cb, ws
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_consumers(torch, iters, cpu=True):
     """codebook consumers over a C4-sized map (about 2M
     Gaussians, K=512 logits, D=768 codebook): semantic_entropy (HBM-bound fused
@@ -743,8 +788,9 @@ def main():
     targets = None
     if rank == 0 and world == 1 and not args.no_grid:
         targets = run_targets(torch, 10, cpu=not args.no_cpu)
-    consumers = raster = None
+    consumers = raster = init = None
     if rank == 0 and world == 1 and not args.no_grid:
+        init = run_init(torch, cpu=not args.no_cpu)
         consumers = run_consumers(torch, 5, cpu=not args.no_cpu)
         raster = run_raster(torch, 3, cpu=not args.no_cpu)
     c5 = None
@@ -779,6 +825,7 @@ def main():
             "targets": targets,
             "consumers": consumers,
             "raster": raster,
+            "init": init,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

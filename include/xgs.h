@@ -77,6 +77,15 @@ XGS_API int xgs_vq_exact(const void* x, int dtype, int64_t n, int64_t d, int64_t
 /* accumulate (vq.py:90-100) given the codes: counts = bincount(codes[mask]),
  * sums = np.add.at(zeros, codes[mask], x[mask]) — bit-identical (sequential
  * fp64 chains per (k, d) in ascending row order).  mask may be NULL. */
+/* seed_from_samples (vq.py:126-147): greedy farthest-point traversal from row
+ * 0; seeds[t] = first argmax of min squared distance (NumPy pairwise order),
+ * or t % n once that maximum is 0.  K-1 kernel launches on `stream`, no host
+ * synchronisation; seeds (k int64) and ws (xgs_vq_seed_workspace(n) bytes)
+ * are device memory.  n == 0 -> invalid input. */
+XGS_API size_t xgs_vq_seed_workspace(int64_t n);
+XGS_API int xgs_vq_seed_farthest(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, int64_t k,
+                                 int64_t* seeds, void* ws, size_t ws_bytes, void* stream);
+
 XGS_API size_t xgs_vq_accumulate_workspace(int64_t n, int64_t k);
 XGS_API int xgs_vq_accumulate(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const int64_t* codes,
                               const uint8_t* mask, int64_t k, double* counts, double* sums, void* ws,

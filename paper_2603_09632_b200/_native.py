@@ -43,6 +43,8 @@ SIGNATURES = {
     "xgs_vq_assign_accumulate_h2d": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _sz,
                                             _vp, _vp]),
     "xgs_vq_accumulate_workspace": (_sz, [_i64, _i64]),
+    "xgs_vq_seed_workspace": (_sz, [_i64]),
+    "xgs_vq_seed_farthest": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _sz, _vp]),
     "xgs_vq_accumulate": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "xgs_vq_ema": (_i32, [_f64, _f64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "xgs_vq_revive": (_i32, [_i64, _i64, _f64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),

@@ -283,6 +283,23 @@ int xgs_vq_exact(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, co
 
 size_t xgs_vq_accumulate_workspace(int64_t n, int64_t k) { return accumulate_workspace_bytes(n, k); }
 
+// seed_from_samples (vq.py:126-147): K seed row indices, queued without a host sync.
+size_t xgs_vq_seed_workspace(int64_t n) { return seed_workspace_bytes(n < 0 ? 0 : n); }
+int xgs_vq_seed_farthest(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, int64_t k, int64_t* seeds,
+                         void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_rows(x, dtype, n, d, ldx);
+  if (rc) return rc;
+  if (n == 0) return fail(INVALID_INPUT, "seed buffer must be nonempty");
+  if (k < 0 || (k > 0 && !seeds)) return fail(INVALID_INPUT, "bad seed output");
+  if (k == 0) return OK;
+  if (!ws || ws_bytes < seed_workspace_bytes(n)) return fail(INVALID_INPUT, "seed workspace too small");
+  SumPlan pd;
+  if (!build_sum_plan((int)d, &pd)) return fail(NOT_SUPPORTED, "feature dim too large");
+  cudaError_t e = launch_seed_farthest(x, dtype, n, d, ldx, k, seeds, ws, pd, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_vq_seed_farthest");
+  return OK;
+}
+
 int xgs_vq_accumulate(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const int64_t* codes,
                       const uint8_t* mask, int64_t k, double* counts, double* sums, void* ws, size_t ws_bytes,
                       void* stream) {

@@ -21,6 +21,7 @@ enum DType : int { F32 = 0, F64 = 1, BF16 = 2 };
 constexpr unsigned FULL = 0xffffffffu;
 
 inline size_t dtype_size(int dtype) { return dtype == F64 ? 8 : dtype == F32 ? 4 : 2; }
+inline size_t align_up(size_t b, size_t a) { return (b + a - 1) / a * a; }
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }

@@ -92,6 +92,11 @@ cudaError_t launch_assign_accumulate(const ScreenArgs& a, double* counts, double
 
 // ---------------- codebook update (vq_update.cu) ----------------
 size_t accumulate_workspace_bytes(int64_t n, int64_t k);
+
+// farthest-point seeding (vq_seed.cu): K-1 launches, no host synchronisation
+size_t seed_workspace_bytes(int64_t n);
+cudaError_t launch_seed_farthest(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, int64_t k,
+                                 int64_t* seeds, void* ws, const SumPlan& pd, cudaStream_t s);
 // cont != 0 continues the per-(k, d) chains and counts from the values already
 // in counts/sums (rows of this call follow, in row order, the rows of the
 // previous call): chunked accumulation is bit-identical to one call.

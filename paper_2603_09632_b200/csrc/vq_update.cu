@@ -15,6 +15,16 @@ namespace xgs {
 namespace {
 
 constexpr int kTileTarget = 2048;  // number of row tiles (bounds the T x K table)
+// block-per-tile path: ~256 tiles of >= 256 rows, 8 warps per tile while the
+// per-warp shared counter rows fit (W * K * 4 B <= kScatterSmem)
+constexpr int kBlockTileTarget = 256;
+constexpr int64_t kScatterSmem = 160 * 1024;
+constexpr int64_t kBlockTileMaxK = kScatterSmem / 4;
+inline bool block_tiles(int64_t k) { return k <= kBlockTileMaxK; }
+inline int scatter_warps(int64_t k) {
+  const int64_t w = kScatterSmem / (4 * (k > 0 ? k : 1));
+  return (int)(w >= 8 ? 8 : (w < 1 ? 1 : w));
+}
 
 struct AccPlan {
   int64_t tile_rows, tiles;
@@ -23,9 +33,16 @@ struct AccPlan {
 
 AccPlan acc_plan(int64_t n, int64_t k) {
   AccPlan p;
-  int64_t tr = (n + kTileTarget - 1) / kTileTarget;
-  if (tr < 256) tr = 256;
-  tr = (tr + 31) / 32 * 32;
+  int64_t tr;
+  if (block_tiles(k)) {
+    tr = (n + kBlockTileTarget - 1) / kBlockTileTarget;
+    if (tr < 256) tr = 256;
+    tr = (tr + 255) / 256 * 256;
+  } else {
+    tr = (n + kTileTarget - 1) / kTileTarget;
+    if (tr < 256) tr = 256;
+    tr = (tr + 31) / 32 * 32;
+  }
   p.tile_rows = tr;
   p.tiles = n > 0 ? (n + tr - 1) / tr : 1;
   size_t o = 0;
@@ -173,6 +190,101 @@ __global__ void acc_scatter_kernel(const int64_t* __restrict__ codes, const uint
   }
 }
 
+// Block-per-tile variant of (1)-(3) (K <= kBlockTileMaxK): per-tile counters
+// live in shared memory instead of global read-modify-write chains, a tile
+// is 8 warps wide, and the codes-by-count order is one warp per code.
+//
+// (1') per-tile code histogram (shared atomics, one add per distinct code per
+//      32 rows), written out as one coalesced row of the tile table.
+__global__ void __launch_bounds__(256)
+acc_hist_block_kernel(const int64_t* __restrict__ codes, const uint8_t* __restrict__ mask, int64_t n, int64_t k,
+                      int64_t tile_rows, int32_t* __restrict__ tile_counts) {
+  extern __shared__ int32_t cnt[];   // k
+  const int64_t t = blockIdx.x;
+  for (int64_t c = threadIdx.x; c < k; c += blockDim.x) cnt[c] = 0;
+  __syncthreads();
+  const int64_t r0 = t * tile_rows, r1 = min(n, r0 + tile_rows);
+  const int lane = threadIdx.x & 31;
+#pragma unroll 4
+  for (int64_t base = r0; base < r1; base += blockDim.x) {
+    const int64_t r = base + threadIdx.x;
+    const int c = r < r1 ? row_code(codes, mask, r) : -1;
+    const unsigned peers = __match_any_sync(FULL, c);
+    if (c >= 0 && lane == __ffs(peers) - 1) atomicAdd(&cnt[c], __popc(peers));
+  }
+  __syncthreads();
+  for (int64_t c = threadIdx.x; c < k; c += blockDim.x) tile_counts[t * k + c] = cnt[c];
+}
+
+// (2c') codes by descending row count (ties by index), one warp per code.
+__global__ void __launch_bounds__(256)
+acc_order_warp_kernel(const int32_t* __restrict__ code_count, int64_t k, int32_t* order) {
+  __shared__ int32_t cc[4096];
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int32_t mine = c < k ? code_count[c] : 0;
+  int32_t rank = 0;
+  for (int64_t j0 = 0; j0 < k; j0 += 4096) {
+    const int64_t m = min((int64_t)4096, k - j0);
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < m; j += blockDim.x) cc[j] = code_count[j0 + j];
+    __syncthreads();
+    for (int64_t j = lane; j < m; j += 32) {
+      const int32_t o = cc[j];
+      rank += (o > mine) || (o == mine && j0 + j < c);
+    }
+  }
+  for (int o = 16; o; o >>= 1) rank += __shfl_xor_sync(FULL, rank, o);
+  if (c < k && lane == 0) order[rank] = (int32_t)c;
+}
+
+// (3') stable scatter, one block per tile: warp w owns the w-th contiguous
+// slice of the tile.  Pass 1 counts each slice per code into its own shared
+// row; a column scan turns the rows into the slice's first output slot per
+// code (code_start + the tile's offset + earlier slices); pass 2 re-walks the
+// slice in row order placing each row at slot + its rank among equal codes.
+__global__ void acc_scatter_block_kernel(const int64_t* __restrict__ codes, const uint8_t* __restrict__ mask,
+                                         int64_t n, int64_t k, int64_t tile_rows,
+                                         const int32_t* __restrict__ tile_off, const int32_t* __restrict__ code_start,
+                                         int32_t* __restrict__ sorted) {
+  extern __shared__ int32_t sc[];   // warps x k
+  const int W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t = blockIdx.x;
+  const int64_t r0 = t * tile_rows, r1 = min(n, r0 + tile_rows);
+  const int64_t slice = ((tile_rows + W - 1) / W + 31) / 32 * 32;
+  const int64_t s0 = min(r1, r0 + warp * slice), s1 = min(r1, s0 + slice);
+  int32_t* mine = sc + (int64_t)warp * k;
+  for (int64_t i = threadIdx.x; i < (int64_t)W * k; i += blockDim.x) sc[i] = 0;
+  __syncthreads();
+#pragma unroll 4
+  for (int64_t base = s0; base < s1; base += 32) {
+    const int64_t r = base + lane;
+    const int c = r < s1 ? row_code(codes, mask, r) : -1;
+    const unsigned peers = __match_any_sync(FULL, c);
+    if (c >= 0 && lane == __ffs(peers) - 1) mine[c] += __popc(peers);
+  }
+  __syncthreads();
+  for (int64_t c = threadIdx.x; c < k; c += blockDim.x) {
+    int32_t run = code_start[c] + tile_off[t * k + c];
+    for (int w = 0; w < W; w++) {
+      const int32_t v = sc[(int64_t)w * k + c];
+      sc[(int64_t)w * k + c] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t base = s0; base < s1; base += 32) {
+    const int64_t r = base + lane;
+    const int c = r < s1 ? row_code(codes, mask, r) : -1;
+    const unsigned peers = __match_any_sync(FULL, c);
+    if (c >= 0) sorted[mine[c] + __popc(peers & lt)] = (int32_t)r;
+    __syncwarp();
+    if (c >= 0 && lane == __ffs(peers) - 1) mine[c] += __popc(peers);
+    __syncwarp();
+  }
+}
+
 // Raw vector loads (no widening) so a warp can keep U rows in flight; the
 // loads are volatile asm so ptxas keeps them ahead of the dependent adds.
 template <typename X, int VEC>
@@ -243,18 +355,20 @@ acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
 #pragma unroll
   for (int v = 0; v < VEC; v++) acc[v] = (cont && live && d0 + v < d) ? sums[code * d + d0 + v] : 0.0;
   const X* xd = x + (live ? d0 : 0);
+  static_assert(U <= 32, "one sorted-index load per lane per batch");
   int32_t b = beg;
+  // the next batch's row ids are loaded one batch ahead, so each batch waits
+  // on one memory latency (the row values), not two (ids, then values)
+  int32_t rn = (lane < U && b + lane < end) ? __ldg(sorted + b + lane) : 0;
   for (; b + U <= end; b += U) {
     Raw<X, VEC> val[U];
     int32_t rows[U];
+    const int32_t r = rn;
 #pragma unroll
-    for (int u = 0; u < U; u += 32) {
-      const int32_t r = sorted[b + u + lane];
-#pragma unroll
-      for (int t = 0; t < 32 && u + t < U; t++) rows[u + t] = __shfl_sync(FULL, r, t);
-    }
+    for (int t = 0; t < U; t++) rows[t] = __shfl_sync(FULL, r, t);
 #pragma unroll
     for (int u = 0; u < U; u++) val[u].load(xd + (int64_t)rows[u] * ldx);
+    rn = (lane < U && b + U + lane < end) ? __ldg(sorted + b + U + lane) : 0;
 #pragma unroll
     for (int u = 0; u < U; u++) val[u].pin();   // all U loads issue before the first add
 #pragma unroll
@@ -391,17 +505,41 @@ cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, in
     count_launches(1);
     return cudaGetLastError();
   }
-  cudaError_t e = cudaMemsetAsync(tile_counts, 0, sizeof(int32_t) * (size_t)p.tiles * (size_t)k, s);
-  if (e != cudaSuccess) return e;
-  if (n > 0) {
-    acc_hist_kernel<<<(unsigned)p.tiles, 32, 0, s>>>(codes, mask, n, k, p.tile_rows, tile_counts); count_launches(1);
-  }
-  acc_scan_tiles_kernel<<<(unsigned)((k + 31) / 32), 1024, 0, s>>>(tile_counts, p.tiles, k, code_count); count_launches(1);
-  acc_scan_codes_kernel<<<1, 1024, 0, s>>>(code_count, k, code_start); count_launches(1);
-  acc_order_kernel<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(code_count, k, order); count_launches(1);
-  if (n > 0) {
-    acc_scatter_kernel<<<(unsigned)p.tiles, 32, 0, s>>>(codes, mask, n, k, p.tile_rows, tile_counts,
-                                                        code_start, sorted); count_launches(1);
+  cudaError_t e;
+  if (block_tiles(k)) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(acc_hist_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatterSmem);
+      cudaFuncSetAttribute(acc_scatter_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatterSmem);
+      attr = true;
+    }
+    const int W = scatter_warps(k);
+    if (n > 0) {
+      acc_hist_block_kernel<<<(unsigned)p.tiles, 256, sizeof(int32_t) * (size_t)k, s>>>(codes, mask, n, k, p.tile_rows,
+                                                                                         tile_counts); count_launches(1);
+    } else if ((e = cudaMemsetAsync(tile_counts, 0, sizeof(int32_t) * (size_t)k, s)) != cudaSuccess) {
+      return e;
+    }
+    acc_scan_tiles_kernel<<<(unsigned)((k + 31) / 32), 1024, 0, s>>>(tile_counts, p.tiles, k, code_count); count_launches(1);
+    acc_scan_codes_kernel<<<1, 1024, 0, s>>>(code_count, k, code_start); count_launches(1);
+    acc_order_warp_kernel<<<(unsigned)((k + 7) / 8), 256, 0, s>>>(code_count, k, order); count_launches(1);
+    if (n > 0) {
+      acc_scatter_block_kernel<<<(unsigned)p.tiles, 32 * W, sizeof(int32_t) * (size_t)W * (size_t)k, s>>>(
+          codes, mask, n, k, p.tile_rows, tile_counts, code_start, sorted); count_launches(1);
+    }
+  } else {
+    if ((e = cudaMemsetAsync(tile_counts, 0, sizeof(int32_t) * (size_t)p.tiles * (size_t)k, s)) != cudaSuccess)
+      return e;
+    if (n > 0) {
+      acc_hist_kernel<<<(unsigned)p.tiles, 32, 0, s>>>(codes, mask, n, k, p.tile_rows, tile_counts); count_launches(1);
+    }
+    acc_scan_tiles_kernel<<<(unsigned)((k + 31) / 32), 1024, 0, s>>>(tile_counts, p.tiles, k, code_count); count_launches(1);
+    acc_scan_codes_kernel<<<1, 1024, 0, s>>>(code_count, k, code_start); count_launches(1);
+    acc_order_kernel<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(code_count, k, order); count_launches(1);
+    if (n > 0) {
+      acc_scatter_kernel<<<(unsigned)p.tiles, 32, 0, s>>>(codes, mask, n, k, p.tile_rows, tile_counts,
+                                                          code_start, sorted); count_launches(1);
+    }
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const uintptr_t xa = reinterpret_cast<uintptr_t>(x);

@@ -287,24 +287,20 @@ def confidence_mask(batch, codebook: Codebook, cfg: VqConfig):
 
 
 def seed_from_samples(buffer, K: int):
-    """vq.py:127-147 — greedy farthest-point seeding (K exact distance passes)."""
+    """vq.py:126-147 — greedy farthest-point seeding.  The K-1 argmax passes run
+    as back-to-back launches of xgs_vq_seed_farthest (seed indices stay on the
+    device; no host round trip per seed)."""
     t = nat.require_cuda()
     host = _host_mode(buffer)
     xt, dt, n, d, ldx = _rows(buffer)
     if n == 0:
         raise InvalidInputError("seed buffer must be nonempty")
-    x64 = xt.to(t.float64)
-    seeds = [0]
-    one = lambda j: _exact_dev(xt, dt, n, d, ldx, x64[j:j + 1].contiguous(), 1, nat.EX_DIST)[0][:, 0]
-    min_d = one(0)
-    while len(seeds) < K:
-        j = int(t.argmax(min_d).item())
-        if float(min_d[j].item()) == 0.0:
-            seeds.append(len(seeds) % n)
-            continue
-        seeds.append(j)
-        min_d = t.minimum(min_d, one(j))
-    out = x64[seeds]
+    K = max(int(K), 1)   # the reference always returns at least buffer[0]
+    seeds = t.empty(K, dtype=t.int64, device="cuda")
+    ws = nat.workspace("seed", nat.lib().xgs_vq_seed_workspace(n))
+    nat.call("xgs_vq_seed_farthest", nat.ptr(xt), dt, n, d, ldx, K, nat.ptr(seeds), nat.ptr(ws), ws.numel(),
+             nat.stream_ptr())
+    out = xt.index_select(0, seeds).to(t.float64)
     return to_host(out) if host else out
 
 

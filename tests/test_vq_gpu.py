@@ -113,6 +113,39 @@ def test_warm_start_and_seeding_golden(xv):
     assert np.array_equal(ws.codebook.E, g["d_E"]) and np.array_equal(ws.codebook.N, g["d_N"])
 
 
+@pytest.mark.parametrize("case", ["mixture_f32", "odd_d_f64", "cycling", "single_row", "nan_row", "ties",
+                                  "bf16", "k_le_1"])
+def test_seed_from_samples_matches_oracle(xv, case):
+    """Device farthest-point seeding (xgs_vq_seed_farthest) vs the oracle
+    restatement of vq.py:126-147, bit-exact: argmax ties to the lower index,
+    cycling once the maximum is 0, NaN rows first (np.argmax / np.minimum)."""
+    import torch
+    rng = np.random.default_rng(77)
+    K = 24
+    if case == "mixture_f32":
+        buf, K = mixture(rng, 3000, 512, 40, 0.05), 64
+    elif case == "odd_d_f64":
+        buf = rng.normal(size=(777, 301))
+    elif case == "cycling":      # 3 distinct rows, K > 3: seeds cycle through the buffer
+        buf = np.repeat(rng.normal(size=(3, 16)), 4, axis=0)
+    elif case == "single_row":
+        buf = rng.normal(size=(1, 8))
+    elif case == "nan_row":
+        buf = rng.normal(size=(50, 8))
+        buf[17, 3] = np.nan
+    elif case == "ties":         # integer lattice: many equal distances
+        buf = rng.integers(0, 3, size=(200, 4)).astype(np.float64)
+    elif case == "bf16":
+        buf = torch.from_numpy(mixture(rng, 500, 128, 8, 0.1)).to(torch.bfloat16).cuda()
+    else:
+        buf, K = rng.normal(size=(10, 5)), 0
+    want = ov.seed_from_samples(buf.float().cpu().numpy() if torch.is_tensor(buf) else buf, K)
+    got = xv.seed_from_samples(buf, K)
+    got = got.cpu().numpy() if torch.is_tensor(got) else got
+    assert got.shape == want.shape
+    assert np.array_equal(got, want, equal_nan=True)
+
+
 # ------------------------------------------- restated reference KATs (test_vq.py)
 
 def test_kat_assign(xv):
@@ -304,6 +337,30 @@ def test_pipelined_assign_accumulate(xv, n, K, D, dtype):
     ref = on.assign(xh, E, threads=8, bf16=dtype == "bf16")
     assert np.array_equal(codes.cpu().numpy(), ref)
     c, sm = on.accumulate(xh, ref, K, bf16=dtype == "bf16")
+    assert np.array_equal(counts.cpu().numpy(), c) and np.array_equal(sums.cpu().numpy(), sm)
+
+
+@pytest.mark.parametrize("n,K,D,skew", [(50_000, 1024, 64, False), (50_000, 1024, 64, True),
+                                        (20_000, 8192, 16, False), (30_000, 50_000, 8, False), (1025, 7, 33, True)])
+def test_accumulate_counting_sort_paths(xv, n, K, D, skew):
+    """accumulate over given codes + confidence mask at n > 1024: the
+    block-per-tile counting sort (K <= 40960; 8 warps per tile, fewer at
+    K = 8192), the per-warp-tile fallback (K = 50000), skewed code counts
+    (one code holds half the rows: the longest chain) -- bit-identical to
+    bincount + np.add.at over the masked rows."""
+    import torch
+    from paper_2603_09632_b200 import vq as xvq
+    rng = np.random.default_rng(n + K)
+    x = rng.normal(size=(n, D)).astype(np.float32)
+    codes = rng.integers(0, K, n)
+    if skew:
+        codes[rng.random(n) < 0.5] = K // 2
+    mask = rng.random(n) < 0.9
+    xt = torch.from_numpy(x).cuda()
+    r, dt, nn, d, ldx = xvq._rows(xt)
+    counts, sums = xvq._accumulate_dev(r, dt, nn, d, ldx, torch.from_numpy(codes).cuda(),
+                                       torch.from_numpy(mask).cuda(), K)
+    c, sm = on.accumulate(x[mask], codes[mask], K)
     assert np.array_equal(counts.cpu().numpy(), c) and np.array_equal(sums.cpu().numpy(), sm)
 
 
