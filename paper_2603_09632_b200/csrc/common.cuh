@@ -93,8 +93,15 @@ __device__ __forceinline__ double warp_pairwise(const SumPlan& P, F f, double* s
     const int main = n >= 8 ? n - (n & 7) : 0;
     double acc = 0.0;
     if (n >= 8) {
-      acc = f(off + j);
-      for (int i = 8; i < main; i += 8) acc = dadd(acc, f(off + i + j));
+      // all of the lane's terms are evaluated (loads issued) before the
+      // sequential chain, which adds them in the same order as before
+      double v[16];   // leaf length <= 128 -> <= 16 terms per lane
+#pragma unroll
+      for (int i = 0; i < 16; i++) v[i] = 8 * i < main ? f(off + 8 * i + j) : 0.0;
+      acc = v[0];
+#pragma unroll
+      for (int i = 1; i < 16; i++)
+        if (8 * i < main) acc = dadd(acc, v[i]);
     }
     double t = dadd(acc, __shfl_xor_sync(FULL, acc, 1));
     t = dadd(t, __shfl_xor_sync(FULL, t, 2));
