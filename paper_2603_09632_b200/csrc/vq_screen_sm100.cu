@@ -196,6 +196,24 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       "h"((uint16_t)3)
       : "memory");
 }
+// Warp-wide forms for the MMA warp: all 32 lanes run the issue loop (its
+// operands stay warp-uniform and live in uniform registers), and elect.sync
+// inside the asm picks the one lane that issues.  A lane==0 branch instead
+// makes ptxas wrap every tcgen05.mma in an ELECT / R2UR.BROADCAST loop.
+__device__ __forceinline__ void mma_f16_pair_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit_pair_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
@@ -424,7 +442,7 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader CTA only) ----------------
-    if (leader && lane == 0) {
+    if (leader) {   // whole warp; one elected lane issues
       uint32_t abase = 0, bidx = 0;
       int acc = 0;
       uint32_t aphase = 0;
@@ -442,13 +460,16 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             tc_after();
             const uint32_t sa = smem_u32(smem + aslot * A_BYTES);
             const uint32_t sb = smem_u32(smem + L::OFF_B + bst * B_BYTES);
+            // K-step kk is 32 B further along the swizzled rows: +2 in the
+            // descriptor's 16-byte address field (smem < 256 KB: no carry)
+            const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; kk++)
-              mma_f16_pair(dt, sw128_desc(sa + kk * 32), sw128_desc(sb + kk * 32), (kb | kk) != 0);
-            umma_commit_pair(&emptyB[bst]);
-            if (!p.resident || nc == nnc - 1) umma_commit_pair(&emptyA[aslot]);
+              mma_f16_pair_warp(dt, da + 2 * kk, db + 2 * kk, (kb | kk) != 0);
+            umma_commit_pair_warp(&emptyB[bst]);
+            if (!p.resident || nc == nnc - 1) umma_commit_pair_warp(&emptyA[aslot]);
           }
-          umma_commit_pair(&tfull[acc]);
+          umma_commit_pair_warp(&tfull[acc]);
           acc ^= 1;
           if (acc == 0) aphase ^= 1;
         }

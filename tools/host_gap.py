@@ -32,3 +32,34 @@ pr.disable()
 torch.cuda.synchronize()
 print("ms/step wall", (time.perf_counter() - t0) / 20 * 1e3)
 pstats.Stats(pr).sort_stats("tottime").print_stats(14)
+
+# GPU-idle host window: from the end of a step's read-back (the only sync) to
+# the first libxgs call of the next step
+from paper_2603_09632_b200 import _native as nat
+be = vq.be
+marks = {"sync_end": None, "gaps": [], "calls": 0}
+orig_counts, orig_call = be.counts_host, nat.call
+
+
+def counts_host(state):
+    out = orig_counts(state)
+    marks["sync_end"] = time.perf_counter()
+    return out
+
+
+def call(name, *args):
+    if marks["sync_end"] is not None:
+        marks["gaps"].append((time.perf_counter() - marks["sync_end"]) * 1e6)
+        marks["sync_end"] = None
+    return orig_call(name, *args)
+
+
+be.counts_host = counts_host
+nat.call = call
+import paper_2603_09632_b200.vq as xvq
+xvq.nat.call = call
+for _ in range(50):
+    vq.step(x, [x.shape[0]])
+torch.cuda.synchronize()
+g = np.array(marks["gaps"][1:])
+print("host window us: p50 %.1f mean %.1f max %.1f (n=%d)" % (np.median(g), g.mean(), g.max(), g.size))
