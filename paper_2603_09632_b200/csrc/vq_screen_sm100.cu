@@ -136,6 +136,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(a, parity)) {
   }
 }
+// warp-convergent waits for the MMA warp: every lane polls, the vote keeps
+// the loop exit uniform
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  while (!__all_sync(FULL, mbar_try_wait(a, parity))) {
+  }
+}
+__device__ __forceinline__ void mbar_wait_cluster_warp(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  while (!__all_sync(FULL, ok)) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
 // wait with cluster-scope acquire (arrivals come from the peer CTA's threads)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
@@ -372,7 +391,9 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index via a shuffle so ptxas knows it is warp-uniform (role branches
+  // stay convergent and the MMA warp's loop values can live in uniform registers)
+  const int warp = __shfl_sync(FULL, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
@@ -448,15 +469,15 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       uint32_t aphase = 0;
       for (int t = cluster; t < ntiles; t += nclusters) {
         for (int nc = 0; nc < nnc; nc++) {
-          mbar_wait_cluster(&tempty[acc], aphase ^ 1);
+          mbar_wait_cluster_warp(&tempty[acc], aphase ^ 1);
           tc_after();
           const uint32_t dt = tmem_base + (uint32_t)(acc * BN);
           for (int kb = 0; kb < nkb; kb++, bidx++) {
             const uint32_t ai = abase + (uint32_t)(p.resident ? kb : nc * nkb + kb);
             const uint32_t aslot = ai % A_SLOTS;
             const uint32_t bst = bidx % L::B_STAGES;
-            mbar_wait(&fullA[aslot], (ai / A_SLOTS) & 1);
-            mbar_wait(&fullB[bst], (bidx / L::B_STAGES) & 1);
+            mbar_wait_warp(&fullA[aslot], (ai / A_SLOTS) & 1);
+            mbar_wait_warp(&fullB[bst], (bidx / L::B_STAGES) & 1);
             tc_after();
             const uint32_t sa = smem_u32(smem + aslot * A_BYTES);
             const uint32_t sb = smem_u32(smem + L::OFF_B + bst * B_BYTES);
