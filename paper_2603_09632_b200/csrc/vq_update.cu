@@ -325,6 +325,24 @@ template <> struct Raw<double, 2> {
   __device__ __forceinline__ void pin() { asm volatile("" : "+d"(w[0]), "+d"(w[1])); }
   __device__ __forceinline__ double get(int i) const { return w[i]; }
 };
+template <> struct Raw<float, 1> {
+  uint32_t w;
+  __device__ __forceinline__ void load(const float* p) {
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(w) : "l"(p));
+  }
+  __device__ __forceinline__ void pin() { asm volatile("" : "+r"(w)); }
+  __device__ __forceinline__ double get(int) const { return (double)__uint_as_float(w); }
+};
+template <> struct Raw<uint16_t, 2> {
+  uint32_t w;
+  __device__ __forceinline__ void load(const uint16_t* p) {
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(w) : "l"(p));
+  }
+  __device__ __forceinline__ void pin() { asm volatile("" : "+r"(w)); }
+  __device__ __forceinline__ double get(int i) const {
+    return (double)__uint_as_float(i ? (w & 0xffff0000u) : (w << 16));
+  }
+};
 template <typename X> struct Raw<X, 1> {
   double w;
   __device__ __forceinline__ void load(const X* p) { w = ld64(p, 0); }
@@ -337,38 +355,41 @@ template <typename X> struct Raw<X, 1> {
 // parallelism: U rows are loaded ahead (U*32*VEC*sizeof(X) bytes in flight per
 // warp) before the U dependent adds.
 constexpr int kChainWarps = 8;
+constexpr int64_t kLongCodes = 32;
 template <typename X, int VEC, int U>
-__global__ void __launch_bounds__(kChainWarps * 32, 2)
-acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
-                 const int32_t* __restrict__ code_start, const int32_t* __restrict__ sorted,
-                 const int32_t* __restrict__ order, double* __restrict__ counts, double* __restrict__ sums,
-                 int cont) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (int64_t)blockIdx.x * kChainWarps + (threadIdx.x >> 5);
-  const int64_t nchunks = (d + 32 * VEC - 1) / (32 * VEC);
-  if (gw / nchunks >= k) return;
-  const int64_t code = order[gw / nchunks];
-  const int64_t d0 = (gw % nchunks) * 32 * VEC + (int64_t)lane * VEC;
+__device__ __forceinline__ void chain_run(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t code, int64_t d0,
+                                          int lane, const int32_t* __restrict__ code_start,
+                                          const int32_t* __restrict__ sorted, double* __restrict__ counts,
+                                          double* __restrict__ sums, int cont) {
+  static_assert(U <= 32 || U % 32 == 0, "row batch: <= 32 or whole warps of ids");
+  constexpr int NI = U > 32 ? U / 32 : 1;   // sorted-index loads per lane per batch
   const bool live = d0 < d;
   const int32_t beg = code_start[code], end = code_start[code + 1];
   double acc[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; v++) acc[v] = (cont && live && d0 + v < d) ? sums[code * d + d0 + v] : 0.0;
   const X* xd = x + (live ? d0 : 0);
-  static_assert(U <= 32, "one sorted-index load per lane per batch");
   int32_t b = beg;
   // the next batch's row ids are loaded one batch ahead, so each batch waits
   // on one memory latency (the row values), not two (ids, then values)
-  int32_t rn = (lane < U && b + lane < end) ? __ldg(sorted + b + lane) : 0;
+  int32_t rn[NI];
+#pragma unroll
+  for (int q = 0; q < NI; q++) {
+    const int i = q * 32 + lane;
+    rn[q] = (i < U && b + i < end) ? __ldg(sorted + b + i) : 0;
+  }
   for (; b + U <= end; b += U) {
     Raw<X, VEC> val[U];
     int32_t rows[U];
-    const int32_t r = rn;
 #pragma unroll
-    for (int t = 0; t < U; t++) rows[t] = __shfl_sync(FULL, r, t);
+    for (int t = 0; t < U; t++) rows[t] = __shfl_sync(FULL, rn[t >> 5], t & 31);
 #pragma unroll
     for (int u = 0; u < U; u++) val[u].load(xd + (int64_t)rows[u] * ldx);
-    rn = (lane < U && b + U + lane < end) ? __ldg(sorted + b + U + lane) : 0;
+#pragma unroll
+    for (int q = 0; q < NI; q++) {
+      const int i = q * 32 + lane;
+      rn[q] = (i < U && b + U + i < end) ? __ldg(sorted + b + U + i) : 0;
+    }
 #pragma unroll
     for (int u = 0; u < U; u++) val[u].pin();   // all U loads issue before the first add
 #pragma unroll
@@ -387,6 +408,32 @@ acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
     for (int v = 0; v < VEC; v++) sums[code * d + d0 + v] = acc[v];
   }
   if (d0 == 0) counts[code] = (cont ? counts[code] : 0.0) + (double)(end - beg);   // integer-valued: exact
+}
+
+// Codes come in descending-count order.  The first n_long codes (the longest
+// chains, which bound the kernel) run on the first long_blocks blocks with
+// narrower column slices (VL) and twice the rows in flight (UL): fewer
+// dependent memory round trips per chain; the rest use (VEC, U).
+template <typename X, int VEC, int U, int VL, int UL>
+__global__ void __launch_bounds__(kChainWarps * 32, 2)
+acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
+                 const int32_t* __restrict__ code_start, const int32_t* __restrict__ sorted,
+                 const int32_t* __restrict__ order, double* __restrict__ counts, double* __restrict__ sums,
+                 int cont, int64_t n_long, unsigned long_blocks) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (blockIdx.x < long_blocks) {
+    const int64_t gw = (int64_t)blockIdx.x * kChainWarps + warp;
+    const int64_t nch = (d + 32 * VL - 1) / (32 * VL);
+    if (gw / nch >= n_long) return;
+    chain_run<X, VL, UL>(x, d, ldx, order[gw / nch], (gw % nch) * 32 * VL + (int64_t)lane * VL, lane, code_start,
+                         sorted, counts, sums, cont);
+  } else {
+    const int64_t gw = (int64_t)(blockIdx.x - long_blocks) * kChainWarps + warp;
+    const int64_t nch = (d + 32 * VEC - 1) / (32 * VEC);
+    if (gw / nch >= k - n_long) return;
+    chain_run<X, VEC, U>(x, d, ldx, order[n_long + gw / nch], (gw % nch) * 32 * VEC + (int64_t)lane * VEC, lane,
+                         code_start, sorted, counts, sums, cont);
+  }
 }
 
 // Small batches (n <= kSmallRows, e.g. the per-frame C4 stream): one launch,
@@ -415,16 +462,21 @@ acc_small_kernel(const X* __restrict__ x, int64_t n, int64_t d, int64_t ldx, con
   if (j == 0) counts[code] = (cont ? counts[code] : 0.0) + (double)cnt;
 }
 
-template <typename X, int VEC>
+template <typename X, int VEC, int VL, int UL>
 cudaError_t launch_chain(const X* x, int64_t d, int64_t ldx, int64_t k, const int32_t* cs,
                          const int32_t* sorted, const int32_t* order, double* counts, double* sums,
                          cudaStream_t s, int cont) {
-  const int64_t nchunks = (d + 32 * VEC - 1) / (32 * VEC);
-  const int64_t warps = k * nchunks;
   constexpr int U = VEC >= 4 ? 16 : 32;
+  // the 32 largest codes take the long-chain path (VL == 0: none)
+  const int64_t n_long = VL > 0 ? (k < kLongCodes ? k : kLongCodes) : 0;
+  constexpr int VLx = VL > 0 ? VL : VEC, ULx = VL > 0 ? UL : U;
+  const int64_t lw = n_long * ((d + 32 * VLx - 1) / (32 * VLx));
+  const unsigned lb = (unsigned)((lw + kChainWarps - 1) / kChainWarps);
+  const int64_t warps = (k - n_long) * ((d + 32 * VEC - 1) / (32 * VEC));
   ProfScope prof("vq_chain", s);
-  acc_chain_kernel<X, VEC, U><<<(unsigned)((warps + kChainWarps - 1) / kChainWarps), kChainWarps * 32, 0, s>>>(
-      x, d, ldx, k, cs, sorted, order, counts, sums, cont); count_launches(1);
+  acc_chain_kernel<X, VEC, U, VLx, ULx><<<lb + (unsigned)((warps + kChainWarps - 1) / kChainWarps), kChainWarps * 32, 0,
+                                         s>>>(x, d, ldx, k, cs, sorted, order, counts, sums, cont, n_long, lb);
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -546,16 +598,16 @@ cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, in
   switch (dtype) {
     case F32:
       if (d % 2 == 0 && ldx % 2 == 0 && xa % 8 == 0)
-        return launch_chain<float, 2>((const float*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
-      return launch_chain<float, 1>((const float*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
+        return launch_chain<float, 2, 1, 64>((const float*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
+      return launch_chain<float, 1, 0, 0>((const float*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
     case F64:
       if (d % 2 == 0 && ldx % 2 == 0 && xa % 16 == 0)
-        return launch_chain<double, 2>((const double*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
-      return launch_chain<double, 1>((const double*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
+        return launch_chain<double, 2, 0, 0>((const double*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
+      return launch_chain<double, 1, 0, 0>((const double*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
     default:
       if (d % 8 == 0 && ldx % 8 == 0 && xa % 16 == 0)
-        return launch_chain<uint16_t, 8>((const uint16_t*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
-      return launch_chain<uint16_t, 1>((const uint16_t*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
+        return launch_chain<uint16_t, 8, 2, 64>((const uint16_t*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
+      return launch_chain<uint16_t, 1, 0, 0>((const uint16_t*)x, d, ldx, k, code_start, sorted, order, counts, sums, s, cont);
   }
 }
 

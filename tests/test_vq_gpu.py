@@ -260,11 +260,13 @@ def test_assign_matches_oracle(xv, n, K, D):
     print(f"n={n} K={K} D={D}: rerank {nr} fallback {nf}")
 
 
-def test_assign_bf16_rows(xv):
+@pytest.mark.parametrize("D", [1152, 100])
+def test_assign_bf16_rows(xv, D):
+    """bf16 rows: D=1152 takes the 16-byte vector prep path, D=100 the scalar one."""
     import torch
     rng = np.random.default_rng(5)
-    x = torch.from_numpy(mixture(rng, 5000, 1152, 512, 0.05)).to(torch.bfloat16).cuda()
-    E = mixture(rng, 512, 1152, 512, 0.05).astype(np.float64)
+    x = torch.from_numpy(mixture(rng, 5000, D, 512, 0.05)).to(torch.bfloat16).cuda()
+    E = mixture(rng, 512, D, 512, 0.05).astype(np.float64)
     cb = make_cb(xv, E).to_device()
     got = xv.assign_batch(x, cb).cpu().numpy()
     ref = on.assign(x.cpu().view(torch.int16).numpy().view(np.uint16), E, threads=8, bf16=True)
