@@ -4,6 +4,7 @@ launches, with each kernel's share of the step (cold-cache, serialised
 replay: compare shares, not absolute times).
 
     python tools/launch_step.py gpurun_out/r_launches.csv [which=2]
+    python tools/launch_step.py profiles/r1_launches_session3.csv   (slimmed copy)
 """
 import csv
 import sys
@@ -11,6 +12,13 @@ import sys
 
 def load(path):
     rows = list(csv.reader(open(path)))
+    if rows and rows[0][:2] == ["ID", "kernel"]:   # profiles/ copy: one row per launch
+        out = []
+        for r in rows[1:]:
+            m = {"gpu__time_duration.sum": float(r[4] or 0), "dram__bytes_read.sum": float(r[5] or 0),
+                 "dram__bytes_write.sum": float(r[6] or 0)}
+            out.append([r[1], m])
+        return out
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hi]
     ik, im, iv, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
