@@ -20,6 +20,29 @@ enum DType : int { F32 = 0, F64 = 1, BF16 = 2 };
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// Programmatic dependent launch: a kernel launched with launch_pdl may start
+// while the previous kernel in the stream drains (its launch latency hides
+// behind the predecessor's tail); it must call pdl_wait() before touching
+// anything the predecessor writes.  Chains of short dependent kernels (the
+// radix-sort passes, select, emit) lose the per-boundary launch gap.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 inline size_t dtype_size(int dtype) { return dtype == F64 ? 8 : dtype == F32 ? 4 : 2; }
 inline size_t align_up(size_t b, size_t a) { return (b + a - 1) / a * a; }
 

@@ -46,6 +46,22 @@ __device__ __forceinline__ bool hs_insert(unsigned long long* table, uint64_t ma
     h = (h + 1) & mask;
   }
 }
+// Same result, probing with plain loads first: a key already in the map (most
+// segment heads at steady state) costs no atomic; only an empty slot is
+// claimed with atomicCAS (a lost race to another key moves on to the next
+// slot).  Slots never go back to EMPTY, so a stale non-empty read is exact.
+__device__ __forceinline__ bool hs_insert_probe(unsigned long long* table, uint64_t mask, uint64_t key) {
+  uint64_t h = mix64(key) & mask;
+  while (true) {
+    unsigned long long v = __ldcg(table + h);
+    if (v == EMPTY) {
+      v = atomicCAS(table + h, (unsigned long long)EMPTY, (unsigned long long)key);
+      if (v == EMPTY) return true;
+    }
+    if (v == key) return false;
+    h = (h + 1) & mask;
+  }
+}
 __device__ __forceinline__ bool hs_contains(const unsigned long long* table, uint64_t mask, uint64_t key) {
   uint64_t h = mix64(key) & mask;
   while (true) {
@@ -604,6 +620,7 @@ cudaError_t front_init();
 template <typename K>
 __global__ void __launch_bounds__(SORT_THREADS)
 sort_upsweep_kernel(const K* __restrict__ keys, int64_t n, int shift, int32_t* tile_hist, int64_t tiles) {
+  pdl_wait();
   __shared__ int32_t h[8][RADIX];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 8 * RADIX; i += SORT_THREADS) (&h[0][0])[i] = 0;
@@ -634,6 +651,7 @@ sort_upsweep_kernel(const K* __restrict__ keys, int64_t n, int shift, int32_t* t
 // relative key fits 32 bits: 4-byte keys halve the sort's key traffic)
 template <typename K>
 __global__ void rekey_kernel(const uint64_t* __restrict__ kin, int64_t n, RelKey rk, K* __restrict__ kout) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     kout[i] = (K)rk(kin[i]);
 }
@@ -645,6 +663,7 @@ template <typename K>
 __global__ void rekey_gather_kernel(const uint64_t* __restrict__ slot_k, const uint32_t* __restrict__ slot_v,
                                     const int32_t* __restrict__ block_off, int64_t nblocks, int64_t H, int64_t W,
                                     int64_t n, RelKey rk, K* __restrict__ kout, uint32_t* __restrict__ vout) {
+  pdl_wait();
   const int64_t rbf = (H + FK_ROWS - 1) / FK_ROWS;
   for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {
     const int64_t o = block_off[b], e = b + 1 < nblocks ? block_off[b + 1] : n;
@@ -661,6 +680,7 @@ __global__ void rekey_gather_kernel(const uint64_t* __restrict__ slot_k, const u
 // back to the biased 63-bit voxel keys after the sort (select / emit use them)
 template <typename K>
 __global__ void unrekey_kernel(const K* __restrict__ kin, int64_t n, RelKey rk, int bits, uint64_t* __restrict__ kout) {
+  pdl_wait();
   const uint64_t all = bits >= 64 ? ~0ull : ((1ull << bits) - 1);
   const uint64_t mz = (1ull << rk.bz) - 1, my = (1ull << rk.by) - 1;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -679,6 +699,7 @@ __global__ void unrekey_kernel(const K* __restrict__ kin, int64_t n, RelKey rk, 
 // (exclusive scan of the 256 totals) itself, so a pass has one scan launch.
 __global__ void __launch_bounds__(1024)
 sort_scan_digits_kernel(int32_t* __restrict__ hist, int64_t tiles, int32_t* __restrict__ digit_tot) {
+  pdl_wait();
   __shared__ int32_t sm[32];
   const int d = blockIdx.x;
   int32_t* row = hist + (int64_t)d * tiles;
@@ -721,6 +742,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 3)
 sort_downsweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t n, int shift,
                       const int32_t* __restrict__ scanned, const int32_t* __restrict__ digit_tot, int64_t tiles,
                       K* __restrict__ kout, uint32_t* __restrict__ vout) {
+  pdl_wait();
   __shared__ int32_t wc[8][RADIX];
   __shared__ int32_t toff[RADIX];
   __shared__ int32_t gbase[RADIX];
@@ -973,13 +995,14 @@ __global__ void __launch_bounds__(256)
 grid_select_kernel(const uint64_t* __restrict__ k, const uint32_t* __restrict__ v, int64_t n,
                    unsigned long long* table, uint64_t mask, unsigned long long* set_count, unsigned* flag_bits,
                    int32_t* head_pos, unsigned long long* nvox) {
+  pdl_wait();
   unsigned newc = 0, vox = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t key = k[i];
     if (key == KEY_INVALID) continue;
     if (i > 0 && k[i - 1] == key) continue;
     vox++;
-    if (hs_insert(table, mask, key)) {
+    if (hs_insert_probe(table, mask, key)) {
       const uint32_t pid = v[i];
       atomicOr(flag_bits + (pid >> 5), 1u << (pid & 31));
       head_pos[pid] = (int32_t)i;
@@ -1120,7 +1143,7 @@ __global__ void hs_insert_kernel(unsigned long long* table, uint64_t mask, const
                                  uint8_t* was_new, unsigned long long* count) {
   unsigned c = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const bool nw = keys[i] != KEY_INVALID && hs_insert(table, mask, keys[i]);
+    const bool nw = keys[i] != KEY_INVALID && hs_insert_probe(table, mask, keys[i]);
     if (was_new) was_new[i] = nw;
     c += nw;
   }
@@ -1249,10 +1272,16 @@ cudaError_t lsd_passes(K*& k0, uint32_t*& v0, K*& k1, uint32_t*& v1, int64_t n, 
   const int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
   const int stage = SORT_TILE * (int)(sizeof(K) + 4);
   for (int shift = 0; shift < bits; shift += 8) {
-    sort_upsweep_kernel<K><<<(unsigned)tiles, SORT_THREADS, 0, s>>>(k0, n, shift, hist, tiles); count_launches(1);
-    sort_scan_digits_kernel<<<RADIX, 1024, 0, s>>>(hist, tiles, ssum); count_launches(1);
-    sort_downsweep_kernel<K><<<(unsigned)tiles, SORT_THREADS, stage, s>>>(k0, v0, n, shift, hist, ssum, tiles, k1, v1);
-    count_launches(1);
+    cudaError_t e;
+    if ((e = launch_pdl(sort_upsweep_kernel<K>, dim3((unsigned)tiles), dim3(SORT_THREADS), 0, s, k0, n, shift, hist,
+                        tiles)) != cudaSuccess)
+      return e;
+    if ((e = launch_pdl(sort_scan_digits_kernel, dim3(RADIX), dim3(1024), 0, s, hist, tiles, ssum)) != cudaSuccess)
+      return e;
+    if ((e = launch_pdl(sort_downsweep_kernel<K>, dim3((unsigned)tiles), dim3(SORT_THREADS), (size_t)stage, s, k0, v0, n,
+                        shift, hist, ssum, tiles, k1, v1)) != cudaSuccess)
+      return e;
+    count_launches(3);
     K* tk = k0; k0 = k1; k1 = tk;
     uint32_t* tv = v0; v0 = v1; v1 = tv;
   }
@@ -1384,6 +1413,9 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   if (nitems == 0) return cudaSuccess;
   out.n_sorted = nitems;
   out.sort_passes = (bits + 7) / 8;
+  // the new-head flags are cleared ahead of the sort, so select follows the
+  // last sort kernel directly (programmatic launch, no memset in between)
+  if ((e = cudaMemsetAsync(flag, 0, (size_t)nwords * 4, s)) != cudaSuccess) return e;
   {
     ProfScope prof("grid_sort", s);
     // relative keys once (u32 when they fit), LSD passes, biased keys back into k0
@@ -1395,14 +1427,18 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
       uint32_t* r0 = reinterpret_cast<uint32_t*>(k1);
       uint32_t* r1 = r0 + nitems;
       if (fused) {   // items land in (r0, v1); the slots in (k0, v0) are dead afterwards
-        rekey_gather_kernel<uint32_t><<<grid_blocks(fblocks, 1, sms), 256, 0, s>>>(k0, v0, block_count, fblocks, in.H, in.W,
-                                                                                   nitems, rk, r0, v1); count_launches(1);
+        if ((e = launch_pdl(rekey_gather_kernel<uint32_t>, dim3(grid_blocks(fblocks, 1, sms)), dim3(256), 0, s, k0, v0,
+                            block_count, fblocks, in.H, in.W, nitems, rk, r0, v1)) != cudaSuccess)
+          return e;
+        count_launches(1);
         uint32_t* t = v0; v0 = v1; v1 = t;
       } else {
         rekey_kernel<uint32_t><<<rb, 256, 0, s>>>(k0, nitems, rk, r0); count_launches(1);
       }
       if ((e = lsd_passes<uint32_t>(r0, v0, r1, v1, nitems, bits, hist, ssum, s)) != cudaSuccess) return e;
-      unrekey_kernel<uint32_t><<<rb, 256, 0, s>>>(r0, nitems, rk, bits, k0); count_launches(1);
+      if ((e = launch_pdl(unrekey_kernel<uint32_t>, dim3(rb), dim3(256), 0, s, r0, nitems, rk, bits, k0)) != cudaSuccess)
+        return e;
+      count_launches(1);
     } else {
       if (fused) {
         rekey_gather_kernel<uint64_t><<<grid_blocks(fblocks, 1, sms), 256, 0, s>>>(k0, v0, block_count, fblocks, in.H, in.W,
@@ -1425,9 +1461,10 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   }
   {
     ProfScope prof("grid_select", s);
-    cudaMemsetAsync(flag, 0, (size_t)nwords * 4, s);
-    grid_select_kernel<<<grid_blocks(nitems, 256, sms), 256, 0, s>>>(k0, v0, nitems, hs->table, (uint64_t)hs->cap - 1,
-                                                                     hs->count_dev, reinterpret_cast<unsigned*>(flag), head, cnts + 1);
+    if ((e = launch_pdl(grid_select_kernel, dim3(grid_blocks(nitems, 256, sms)), dim3(256), 0, s, (const uint64_t*)k0,
+                        (const uint32_t*)v0, nitems, hs->table, (uint64_t)hs->cap - 1, hs->count_dev,
+                        reinterpret_cast<unsigned*>(flag), head, cnts + 1)) != cudaSuccess)
+      return e;
     count_launches(1);
   }
   {

@@ -1,4 +1,7 @@
-"""Profiling driver: C5-shard online steps (for ncu runs)."""
+"""Profiling driver: C5 per-GPU shard online_steps (for ncu runs).
+
+    python tools/prof_c5.py [iters=1]
+"""
 import os
 import sys
 
@@ -7,5 +10,6 @@ import torch
 
 import bench
 
+iters = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 torch.cuda.set_device(0)
-print(bench.run_c5(torch, int(sys.argv[1]) if len(sys.argv) > 1 else 1, torch.device("cuda", 0))["ms_per_iter"])
+print(bench.run_c5(torch, iters, torch.device("cuda", 0)))
