@@ -907,6 +907,7 @@ __device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* sm, int32
 
 template <typename T>
 __global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const T* __restrict__ in, int64_t n, int32_t* sums) {
+  pdl_wait();
   __shared__ int32_t sm[32];
   const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
   int32_t s = 0;
@@ -919,6 +920,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const T* __re
 }
 
 __global__ void __launch_bounds__(1024) scan_sums_kernel(int32_t* sums, int64_t nb, int32_t* grand) {
+  pdl_wait();
   __shared__ int32_t sm[32];
   const int64_t per = (nb + 1023) / 1024;
   const int64_t b0 = threadIdx.x * per, b1 = min(nb, b0 + per);
@@ -937,6 +939,7 @@ __global__ void __launch_bounds__(1024) scan_sums_kernel(int32_t* sums, int64_t 
 template <typename T>
 __global__ void __launch_bounds__(SCAN_THREADS)
 scan_apply_kernel(const T* __restrict__ in, int64_t n, const int32_t* __restrict__ sums, int32_t* __restrict__ out) {
+  pdl_wait();
   __shared__ int32_t sm[32];
   const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
   int32_t vals[SCAN_ITEMS];
@@ -957,6 +960,7 @@ scan_apply_kernel(const T* __restrict__ in, int64_t n, const int32_t* __restrict
 
 // one-CTA in-place exclusive scan for short arrays (one launch instead of three)
 __global__ void __launch_bounds__(1024) scan_small_kernel(int32_t* a, int64_t n, int32_t* grand) {
+  pdl_wait();
   __shared__ int32_t sm[32];
   const int64_t per = (n + 1023) / 1024;
   const int64_t b0 = threadIdx.x * per, b1 = min(n, b0 + per);
@@ -977,13 +981,17 @@ cudaError_t exclusive_scan(const T* in, int64_t n, int32_t* out, int32_t* block_
   const int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (nb == 0) return cudaSuccess;
   if (n <= 65536 && (const void*)in == (const void*)out && sizeof(T) == 4) {
-    scan_small_kernel<<<1, 1024, 0, s>>>(out, n, grand); count_launches(1);
-    return cudaGetLastError();
+    count_launches(1);
+    return launch_pdl(scan_small_kernel, dim3(1), dim3(1024), 0, s, out, n, grand);
   }
-  scan_reduce_kernel<T><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, n, block_sums); count_launches(1);
-  scan_sums_kernel<<<1, 1024, 0, s>>>(block_sums, nb, grand); count_launches(1);
-  scan_apply_kernel<T><<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, n, block_sums, out); count_launches(1);
-  return cudaGetLastError();
+  cudaError_t e;
+  if ((e = launch_pdl(scan_reduce_kernel<T>, dim3((unsigned)nb), dim3(SCAN_THREADS), 0, s, in, n, block_sums)) !=
+      cudaSuccess)
+    return e;
+  if ((e = launch_pdl(scan_sums_kernel, dim3(1), dim3(1024), 0, s, block_sums, nb, grand)) != cudaSuccess) return e;
+  count_launches(3);
+  return launch_pdl(scan_apply_kernel<T>, dim3((unsigned)nb), dim3(SCAN_THREADS), 0, s, in, n,
+                    (const int32_t*)block_sums, out);
 }
 
 // ---------------------------------------------------------------- G3 select
@@ -1046,6 +1054,7 @@ struct EmitArgs {
 };
 
 __global__ void popc_kernel(const unsigned* __restrict__ bits, int64_t nw, int32_t* __restrict__ out) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = __popc(bits[i]);
 }
@@ -1056,6 +1065,7 @@ __global__ void popc_kernel(const unsigned* __restrict__ bits, int64_t nw, int32
 __global__ void __launch_bounds__(256)
 grid_pidlist_kernel(const unsigned* __restrict__ flag_bits, const int32_t* __restrict__ wpos, int64_t nwords,
                     int64_t* __restrict__ pid_out) {
+  pdl_wait();
   for (int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; wi < nwords; wi += (int64_t)gridDim.x * blockDim.x) {
     unsigned word = flag_bits[wi];
     int64_t o = wpos[wi];
@@ -1071,6 +1081,7 @@ grid_pidlist_kernel(const unsigned* __restrict__ flag_bits, const int32_t* __res
 // GaussianField-compatible attributes.
 __global__ void __launch_bounds__(256)
 grid_emit_kernel(const int32_t* __restrict__ head_pos, int64_t nnew, EmitArgs a) {
+  pdl_wait();
   const int64_t HW = a.H * a.W;
   for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < nnew; o += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = a.pid[o];
@@ -1469,7 +1480,10 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   }
   {
     ProfScope prof("grid_emit", s);
-    popc_kernel<<<grid_blocks(nwords, 256, sms), 256, 0, s>>>(reinterpret_cast<const unsigned*>(flag), nwords, pos); count_launches(1);
+    if ((e = launch_pdl(popc_kernel, dim3(grid_blocks(nwords, 256, sms)), dim3(256), 0, s,
+                        reinterpret_cast<const unsigned*>(flag), nwords, pos)) != cudaSuccess)
+      return e;
+    count_launches(1);
     if ((e = exclusive_scan<int32_t>(pos, nwords, pos, ssum, grand, s)) != cudaSuccess) return e;
     int32_t nnew = 0;
     unsigned long long nvox = 0;
@@ -1506,10 +1520,15 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     a.dep = out.depth;
     a.ofeat = out.feat;
     a.count = out.count;
-    grid_pidlist_kernel<<<grid_blocks(nwords, 256, sms), 256, 0, s>>>(reinterpret_cast<const unsigned*>(flag), pos,
-                                                                       nwords, out.pid); count_launches(1);
+    if ((e = launch_pdl(grid_pidlist_kernel, dim3(grid_blocks(nwords, 256, sms)), dim3(256), 0, s,
+                        reinterpret_cast<const unsigned*>(flag), (const int32_t*)pos, nwords, out.pid)) != cudaSuccess)
+      return e;
+    count_launches(1);
     if (nnew > 0) {
-      grid_emit_kernel<<<grid_blocks(nnew, 128, sms), 128, 0, s>>>(head, nnew, a); count_launches(1);
+      if ((e = launch_pdl(grid_emit_kernel, dim3(grid_blocks(nnew, 128, sms)), dim3(128), 0, s, (const int32_t*)head,
+                          (int64_t)nnew, a)) != cudaSuccess)
+        return e;
+      count_launches(1);
     }
   }
   return cudaGetLastError();

@@ -80,6 +80,7 @@ __global__ void acc_hist_kernel(const int64_t* __restrict__ codes, const uint8_t
 // (2a) exclusive scan over tiles for 32 codes per block; writes per-code totals.
 __global__ void __launch_bounds__(1024)
 acc_scan_tiles_kernel(int32_t* tile_counts, int64_t tiles, int64_t k, int32_t* code_count) {
+  pdl_wait();
   __shared__ int32_t part[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t code = (int64_t)blockIdx.x * 32 + lane;
@@ -113,6 +114,7 @@ acc_scan_tiles_kernel(int32_t* tile_counts, int64_t tiles, int64_t k, int32_t* c
 // warp-shuffle scan of per-thread partials).
 __global__ void __launch_bounds__(1024)
 acc_scan_codes_kernel(const int32_t* __restrict__ code_count, int64_t k, int32_t* code_start) {
+  pdl_wait();
   __shared__ int32_t wsum[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t per = (k + 1023) / 1024;
@@ -199,6 +201,7 @@ __global__ void acc_scatter_kernel(const int64_t* __restrict__ codes, const uint
 __global__ void __launch_bounds__(256)
 acc_hist_block_kernel(const int64_t* __restrict__ codes, const uint8_t* __restrict__ mask, int64_t n, int64_t k,
                       int64_t tile_rows, int32_t* __restrict__ tile_counts) {
+  pdl_wait();
   extern __shared__ int32_t cnt[];   // k
   const int64_t t = blockIdx.x;
   for (int64_t c = threadIdx.x; c < k; c += blockDim.x) cnt[c] = 0;
@@ -219,6 +222,7 @@ acc_hist_block_kernel(const int64_t* __restrict__ codes, const uint8_t* __restri
 // (2c') codes by descending row count (ties by index), one warp per code.
 __global__ void __launch_bounds__(256)
 acc_order_warp_kernel(const int32_t* __restrict__ code_count, int64_t k, int32_t* order) {
+  pdl_wait();
   __shared__ int32_t cc[4096];
   const int lane = threadIdx.x & 31;
   const int64_t c = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -247,6 +251,7 @@ __global__ void acc_scatter_block_kernel(const int64_t* __restrict__ codes, cons
                                          int64_t n, int64_t k, int64_t tile_rows,
                                          const int32_t* __restrict__ tile_off, const int32_t* __restrict__ code_start,
                                          int32_t* __restrict__ sorted) {
+  pdl_wait();
   extern __shared__ int32_t sc[];   // warps x k
   const int W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t = blockIdx.x;
@@ -420,6 +425,7 @@ acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
                  const int32_t* __restrict__ code_start, const int32_t* __restrict__ sorted,
                  const int32_t* __restrict__ order, double* __restrict__ counts, double* __restrict__ sums,
                  int cont, int64_t n_long, unsigned long_blocks) {
+  pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (blockIdx.x < long_blocks) {
     const int64_t gw = (int64_t)blockIdx.x * kChainWarps + warp;
@@ -474,10 +480,9 @@ cudaError_t launch_chain(const X* x, int64_t d, int64_t ldx, int64_t k, const in
   const unsigned lb = (unsigned)((lw + kChainWarps - 1) / kChainWarps);
   const int64_t warps = (k - n_long) * ((d + 32 * VEC - 1) / (32 * VEC));
   ProfScope prof("vq_chain", s);
-  acc_chain_kernel<X, VEC, U, VLx, ULx><<<lb + (unsigned)((warps + kChainWarps - 1) / kChainWarps), kChainWarps * 32, 0,
-                                         s>>>(x, d, ldx, k, cs, sorted, order, counts, sums, cont, n_long, lb);
   count_launches(1);
-  return cudaGetLastError();
+  return launch_pdl(acc_chain_kernel<X, VEC, U, VLx, ULx>, dim3(lb + (unsigned)((warps + kChainWarps - 1) / kChainWarps)),
+                    dim3(kChainWarps * 32), 0, s, x, d, ldx, k, cs, sorted, order, counts, sums, cont, n_long, lb);
 }
 
 // EMA (vq.py:103-109): N' = lam*N + (1-lam)*c ; M' = lam*M + (1-lam)*s ;
@@ -567,17 +572,29 @@ cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, in
     }
     const int W = scatter_warps(k);
     if (n > 0) {
-      acc_hist_block_kernel<<<(unsigned)p.tiles, 256, sizeof(int32_t) * (size_t)k, s>>>(codes, mask, n, k, p.tile_rows,
-                                                                                         tile_counts); count_launches(1);
+      if ((e = launch_pdl(acc_hist_block_kernel, dim3((unsigned)p.tiles), dim3(256), sizeof(int32_t) * (size_t)k, s,
+                          codes, mask, n, k, p.tile_rows, tile_counts)) != cudaSuccess)
+        return e;
+      count_launches(1);
     } else if ((e = cudaMemsetAsync(tile_counts, 0, sizeof(int32_t) * (size_t)k, s)) != cudaSuccess) {
       return e;
     }
-    acc_scan_tiles_kernel<<<(unsigned)((k + 31) / 32), 1024, 0, s>>>(tile_counts, p.tiles, k, code_count); count_launches(1);
-    acc_scan_codes_kernel<<<1, 1024, 0, s>>>(code_count, k, code_start); count_launches(1);
-    acc_order_warp_kernel<<<(unsigned)((k + 7) / 8), 256, 0, s>>>(code_count, k, order); count_launches(1);
+    if ((e = launch_pdl(acc_scan_tiles_kernel, dim3((unsigned)((k + 31) / 32)), dim3(1024), 0, s, tile_counts, p.tiles,
+                        k, code_count)) != cudaSuccess)
+      return e;
+    if ((e = launch_pdl(acc_scan_codes_kernel, dim3(1), dim3(1024), 0, s, (const int32_t*)code_count, k,
+                        code_start)) != cudaSuccess)
+      return e;
+    if ((e = launch_pdl(acc_order_warp_kernel, dim3((unsigned)((k + 7) / 8)), dim3(256), 0, s,
+                        (const int32_t*)code_count, k, order)) != cudaSuccess)
+      return e;
+    count_launches(3);
     if (n > 0) {
-      acc_scatter_block_kernel<<<(unsigned)p.tiles, 32 * W, sizeof(int32_t) * (size_t)W * (size_t)k, s>>>(
-          codes, mask, n, k, p.tile_rows, tile_counts, code_start, sorted); count_launches(1);
+      if ((e = launch_pdl(acc_scatter_block_kernel, dim3((unsigned)p.tiles), dim3(32 * W),
+                          sizeof(int32_t) * (size_t)W * (size_t)k, s, codes, mask, n, k, p.tile_rows,
+                          (const int32_t*)tile_counts, (const int32_t*)code_start, sorted)) != cudaSuccess)
+        return e;
+      count_launches(1);
     }
   } else {
     if ((e = cudaMemsetAsync(tile_counts, 0, sizeof(int32_t) * (size_t)p.tiles * (size_t)k, s)) != cudaSuccess)
