@@ -189,30 +189,27 @@ class GridSampler:
         s = self.stride
         cap = max(1, F * ((H + s - 1) // s) * ((W + s - 1) // s))
         C = int(feat.shape[1]) if feat is not None else 0
-        out = dict(key=t.empty(cap, dtype=t.int64, device="cuda"), pid=t.empty(cap, dtype=t.int64, device="cuda"),
-                   mu=t.empty((cap, 3), dtype=t.float64, device="cuda"),
-                   color=t.empty((cap, 3), dtype=t.float64, device="cuda"),
-                   scale=t.empty(cap, dtype=t.float64, device="cuda"),
-                   depth=t.empty(cap, dtype=t.float64, device="cuda"),
-                   count=t.empty(cap, dtype=t.float64, device="cuda"),
-                   feature=t.empty((cap, C), dtype=t.float32, device="cuda") if feat is not None else None)
+        # one fp64 allocation for every per-voxel field (key and pid as int64
+        # views): [key | pid | mu x3 | color x3 | scale | depth | count]
+        flat = t.empty(11 * cap, dtype=t.float64, device="cuda")
+        ofeat = t.empty((cap, C), dtype=t.float32, device="cuda") if feat is not None else None
+        b = flat.data_ptr()
         fx, fy, cx, cy = self.intr
         fr = nat.GridFrames(F, H, W, d.data_ptr(), col.data_ptr() if col is not None else None, R.data_ptr(),
                             tr.data_ptr(), fx, fy, cx, cy, self.voxel, s, 0 if self.mode == "first" else 1,
                             self.min_scale, feat.data_ptr() if feat is not None else None,
                             C, int(feat.shape[2]) if feat is not None else 0,
                             int(feat.shape[3]) if feat is not None else 0)
-        res = nat.GridResult(cap, out["key"].data_ptr(), out["pid"].data_ptr(), out["mu"].data_ptr(),
-                             out["color"].data_ptr(), out["scale"].data_ptr(), out["depth"].data_ptr(),
-                             out["feature"].data_ptr() if feat is not None else None, out["count"].data_ptr(),
-                             0, 0, 0, 0, 0)
+        res = nat.GridResult(cap, b, b + 8 * cap, b + 16 * cap, b + 40 * cap, b + 64 * cap, b + 72 * cap,
+                             ofeat.data_ptr() if ofeat is not None else None, b + 80 * cap, 0, 0, 0, 0, 0)
         ws = nat.workspace("grid", nat.lib().xgs_grid_workspace(F * H * W))
         nat.call("xgs_grid_sample", ctypes.byref(fr), self.occupied._h, ctypes.byref(res), nat.ptr(ws), ws.numel(),
                  nat.stream_ptr())
         n = int(res.n_new)
-        return GridSampleResult(key=out["key"][:n], pid=out["pid"][:n], mu=out["mu"][:n], color=out["color"][:n],
-                                scale=out["scale"][:n], depth=out["depth"][:n], count=out["count"][:n],
-                                feature=out["feature"][:n] if feat is not None else None,
+        return GridSampleResult(key=flat[:n].view(t.int64), pid=flat[cap:cap + n].view(t.int64),
+                                mu=flat[2 * cap:2 * cap + 3 * n].view(n, 3), color=flat[5 * cap:5 * cap + 3 * n].view(n, 3),
+                                scale=flat[8 * cap:8 * cap + n], depth=flat[9 * cap:9 * cap + n],
+                                count=flat[10 * cap:10 * cap + n], feature=ofeat[:n] if ofeat is not None else None,
                                 n_valid=int(res.n_valid), n_voxels=int(res.n_voxels),
                                 n_sorted=int(res.n_sorted), sort_passes=int(res.sort_passes))
 
