@@ -8,6 +8,8 @@
 // (warp match_any ranks, tiles walked in order) and (4) run one chain per
 // (k, d) over the sorted row ids: lanes own consecutive d so each row read is
 // a coalesced 128-512 B segment.  HBM traffic ~ one read of X + 8 B/row.
+#include <cstdlib>
+
 #include "launchers.h"
 
 namespace xgs {
@@ -473,8 +475,17 @@ cudaError_t launch_chain(const X* x, int64_t d, int64_t ldx, int64_t k, const in
                          const int32_t* sorted, const int32_t* order, double* counts, double* sums,
                          cudaStream_t s, int cont) {
   constexpr int U = VEC >= 4 ? 16 : 32;
-  // the 32 largest codes take the long-chain path (VL == 0: none)
-  const int64_t n_long = VL > 0 ? (k < kLongCodes ? k : kLongCodes) : 0;
+  // the largest codes take the long-chain path (VL == 0: none)
+  // Measured: fp32 rows at C2 (K=1024) are fastest with the larger half of
+  // the codes on the long path (chains 0.43 ms with none, 0.39 with 32, 0.37
+  // with 512); bf16 rows at the C5 shard (K=4096) with 32 (4.65 ms vs 5.18 at
+  // 2048).  XGS_LONG_CODES overrides for tuning.
+  static const int64_t long_env = [] {
+    const char* e = std::getenv("XGS_LONG_CODES");
+    return e ? (int64_t)std::atoll(e) : (int64_t)-1;
+  }();
+  const int64_t long_codes = long_env >= 0 ? long_env : (sizeof(X) == 4 ? k / 2 : kLongCodes);
+  const int64_t n_long = VL > 0 ? (k < long_codes ? k : long_codes) : 0;
   constexpr int VLx = VL > 0 ? VL : VEC, ULx = VL > 0 ? UL : U;
   const int64_t lw = n_long * ((d + 32 * VLx - 1) / (32 * VLx));
   const unsigned lb = (unsigned)((lw + kChainWarps - 1) / kChainWarps);
