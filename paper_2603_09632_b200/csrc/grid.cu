@@ -18,7 +18,9 @@
 //                            new-head flags) and the GaussianField-compatible
 //                            outputs (mu, rgb/255, iso scale, depth, feature).
 // Semantics are pinned by oracle/grid.py.
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "launchers.h"
 
@@ -1335,6 +1337,239 @@ GridWs grid_ws(int64_t npix) {
 
 size_t grid_workspace_bytes(int64_t npix) { return grid_ws(npix).total; }
 
+// ---------------------------------------------------------------- G2' hash first-pick
+// First-pick mode does not need the items in voxel order, only each voxel's
+// lowest pixel id: a batch table (open addressing on the voxel key, one
+// atomicMin of the pixel id per slot) finds it in two passes over the items
+// instead of the radix sort + segment-head select.  Pass 1 claims / finds the
+// key's slot and lowers its pixel id; pass 2 keeps the item whose pixel id is
+// the slot's minimum (one per voxel), runs the map test (insert-if-absent into
+// the occupancy set) and flags new voxels in the pixel bitmask, from which the
+// emit stage writes the outputs in ascending pixel order exactly as before.
+// The winners' slots are cleared after the batch, so the table starts every
+// batch empty without a memset.  Probing is bounded; an overflow (table too
+// small for the batch's distinct voxels) skips pass 2 (the map is untouched)
+// and the host retries with a table sized for every item.
+constexpr int kDedupProbe = 256;
+constexpr int64_t kDedupSeg = 4096;   // dense item lists: segment length
+constexpr uint32_t PID_NONE = 0xffffffffu;
+
+struct DedupSegs {   // fused front: block b's items sit in its slot; else one dense list
+  const uint64_t* k;
+  const uint32_t* v;
+  const int32_t* count;   // per-block item counts (fused) or nullptr
+  int64_t nseg, H, W, n_dense;
+  __device__ __forceinline__ void seg(int64_t b, int64_t& base, int64_t& cnt) const {
+    if (count) {
+      const int64_t rbf = (H + FK_ROWS - 1) / FK_ROWS;
+      base = ((b / rbf) * H + (b % rbf) * FK_ROWS) * W;
+      cnt = count[b];
+    } else {
+      base = b * kDedupSeg;
+      cnt = min(kDedupSeg, n_dense - base);
+    }
+  }
+};
+
+// Table slot = 16 bytes {key u64, pixel id u32, pad u32} (all ones = empty),
+// so one 16-byte load returns a slot's key and pixel id together (each probe
+// costs one L2 sector).  Items are processed four per thread per step with
+// their table loads issued together.
+constexpr int kDedupILP = 4;
+
+__device__ __forceinline__ ulonglong2 slot_ld(const unsigned long long* slots, uint64_t h) {
+  return __ldcg(reinterpret_cast<const ulonglong2*>(slots + 2 * h));
+}
+__device__ __forceinline__ uint32_t* slot_pid(unsigned long long* slots, uint64_t h) {
+  return reinterpret_cast<uint32_t*>(slots + 2 * h + 1);
+}
+
+__global__ void __launch_bounds__(256)
+dd_insert_kernel(DedupSegs sg, unsigned long long* slots, uint64_t mask, int* overflow) {
+  pdl_wait();
+  for (int64_t b = blockIdx.x; b < sg.nseg; b += gridDim.x) {
+    int64_t base, cnt;
+    sg.seg(b, base, cnt);
+    for (int64_t i0 = threadIdx.x; i0 < cnt; i0 += kDedupILP * blockDim.x) {
+      uint64_t key[kDedupILP], h[kDedupILP];
+      uint32_t pid[kDedupILP];
+      ulonglong2 cur[kDedupILP];
+#pragma unroll
+      for (int j = 0; j < kDedupILP; j++) {
+        const int64_t i = i0 + j * blockDim.x;
+        key[j] = i < cnt ? __ldg(sg.k + base + i) : KEY_INVALID;
+        pid[j] = i < cnt ? __ldg(sg.v + base + i) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kDedupILP; j++) {
+        h[j] = mix64(key[j]) & mask;
+        cur[j] = key[j] != KEY_INVALID ? slot_ld(slots, h[j]) : make_ulonglong2(0ull, 0ull);
+      }
+#pragma unroll
+      for (int j = 0; j < kDedupILP; j++) {
+        if (key[j] == KEY_INVALID) continue;
+        int t = 0;
+        for (; t < kDedupProbe; t++) {
+          if (cur[j].x == EMPTY) {
+            const unsigned long long prev =
+                atomicCAS(slots + 2 * h[j], (unsigned long long)EMPTY, (unsigned long long)key[j]);
+            cur[j].x = prev == EMPTY ? key[j] : prev;
+          }
+          if (cur[j].x == key[j]) break;
+          h[j] = (h[j] + 1) & mask;
+          cur[j] = slot_ld(slots, h[j]);
+        }
+        if (t == kDedupProbe) {
+          *overflow = 1;
+          continue;
+        }
+        if ((uint32_t)cur[j].y > pid[j]) atomicMin(slot_pid(slots, h[j]), pid[j]);
+      }
+    }
+  }
+}
+
+// Winners record their slot at the segment's own item positions (seg_slots,
+// block-local counter; seg_wins[b] = count), so clearing needs no global
+// append counter.
+__global__ void __launch_bounds__(256)
+dd_select_kernel(DedupSegs sg, const unsigned long long* slots, uint64_t mask, const int* overflow,
+                 unsigned long long* table, uint64_t tmask, unsigned long long* set_count, unsigned* flag_bits,
+                 unsigned long long* nvox, int32_t* seg_slots, int32_t* seg_wins) {
+  pdl_wait();
+  if (*(volatile const int*)overflow) return;
+  __shared__ int s_w;
+  unsigned newc = 0, vox = 0;
+  for (int64_t b = blockIdx.x; b < sg.nseg; b += gridDim.x) {
+    int64_t base, cnt;
+    sg.seg(b, base, cnt);
+    if (threadIdx.x == 0) s_w = 0;
+    __syncthreads();
+    for (int64_t i0 = threadIdx.x; i0 < cnt; i0 += kDedupILP * blockDim.x) {
+      uint64_t key[kDedupILP], h[kDedupILP];
+      uint32_t pid[kDedupILP];
+      ulonglong2 cur[kDedupILP];
+#pragma unroll
+      for (int j = 0; j < kDedupILP; j++) {
+        const int64_t i = i0 + j * blockDim.x;
+        key[j] = i < cnt ? __ldg(sg.k + base + i) : KEY_INVALID;
+        pid[j] = i < cnt ? __ldg(sg.v + base + i) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kDedupILP; j++) {
+        h[j] = mix64(key[j]) & mask;
+        cur[j] = key[j] != KEY_INVALID ? slot_ld(slots, h[j]) : make_ulonglong2(0ull, 0ull);
+      }
+#pragma unroll
+      for (int j = 0; j < kDedupILP; j++) {
+        if (key[j] == KEY_INVALID) continue;
+        while (cur[j].x != key[j]) {   // present: pass 1 placed it
+          h[j] = (h[j] + 1) & mask;
+          cur[j] = slot_ld(slots, h[j]);
+        }
+        if ((uint32_t)cur[j].y != pid[j]) continue;   // not the voxel's lowest pixel id
+        vox++;
+        seg_slots[base + atomicAdd(&s_w, 1)] = (int32_t)h[j];
+        if (hs_insert_probe(table, tmask, key[j])) {
+          atomicOr(flag_bits + (pid[j] >> 5), 1u << (pid[j] & 31));
+          newc++;
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) seg_wins[b] = s_w;
+  }
+  for (int o = 16; o; o >>= 1) {
+    newc += __shfl_xor_sync(FULL, newc, o);
+    vox += __shfl_xor_sync(FULL, vox, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (newc) atomicAdd(set_count, (unsigned long long)newc);
+    if (vox) atomicAdd(nvox, (unsigned long long)vox);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+dd_clear_kernel(DedupSegs sg, const int* overflow, const int32_t* __restrict__ seg_slots,
+                const int32_t* __restrict__ seg_wins, unsigned long long* slots) {
+  pdl_wait();
+  if (*(volatile const int*)overflow) return;   // the host resets the whole table
+  for (int64_t b = blockIdx.x; b < sg.nseg; b += gridDim.x) {
+    int64_t base, cnt;
+    sg.seg(b, base, cnt);
+    const int n = seg_wins[b];
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+      *reinterpret_cast<ulonglong2*>(slots + 2 * (int64_t)seg_slots[base + j]) = make_ulonglong2(~0ull, ~0ull);
+  }
+}
+
+
+// per-device batch table (library-owned scratch, empty between batches)
+struct DedupTable {
+  unsigned long long* slots = nullptr;   // 2 x cap words
+  int* aux = nullptr;   // [0] overflow flag
+  int64_t cap = 0;
+  int64_t last_nvox = -1;
+};
+constexpr int kDedupDevices = 16;
+DedupTable g_dedup[kDedupDevices];
+std::mutex g_dedup_mu;
+
+// Table size: 4x the previous batch's distinct voxels (load <= 1/4 when the
+// scene changes slowly), 2x the item count for the first batch and after an
+// overflow (`all`: every item could be a distinct voxel).
+cudaError_t dedup_table(int64_t nitems, bool all, cudaStream_t s, DedupTable** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kDedupDevices) return cudaErrorInvalidDevice;
+  DedupTable& t = g_dedup[dev];
+  const int64_t want = (all || t.last_nvox < 0) ? 2 * nitems : 4 * t.last_nvox;
+  int64_t cap = 1 << 20;
+  while (cap < want) cap <<= 1;
+  // keep the table when it is big enough but not over 4x too big (probes stay L2-resident)
+  if (t.slots && t.cap >= cap && t.cap <= 4 * cap) {
+    *out = &t;
+    return cudaSuccess;
+  }
+  if (t.slots) {
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;   // earlier batches may still use it
+    cudaFree(t.slots);
+    cudaFree(t.aux);
+    t.slots = nullptr;
+  }
+  if ((e = cudaMalloc(&t.slots, sizeof(unsigned long long) * 2 * cap)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&t.aux, 64)) != cudaSuccess) return e;
+  t.cap = cap;
+  fill_u64_kernel<<<grid_blocks(2 * cap, 256, 148), 256, 0, s>>>(t.slots, 2 * cap, ~0ull); count_launches(1);
+  *out = &t;
+  return cudaGetLastError();
+}
+
+// pass 1 + pass 2 + clear; the flags, the voxel count and the table's aux
+// words are reset first (also on a retry)
+cudaError_t dedup_pass(const DedupSegs& sg, DedupTable* t, HashSet* hs, unsigned* flag, int64_t nwords,
+                       unsigned long long* nvox, int32_t* seg_slots, int32_t* seg_wins, int sms, cudaStream_t s) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(flag, 0, (size_t)nwords * 4, s)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(nvox, 0, 8, s)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(t->aux, 0, 8, s)) != cudaSuccess) return e;
+  const uint64_t mask = (uint64_t)t->cap - 1;
+  const unsigned g = (unsigned)(sg.nseg < 148 * 8 ? sg.nseg : 148 * 8);
+  if ((e = launch_pdl(dd_insert_kernel, dim3(g), dim3(256), 0, s, sg, t->slots, mask, t->aux)) != cudaSuccess)
+    return e;
+  if ((e = launch_pdl(dd_select_kernel, dim3(g), dim3(256), 0, s, sg, (const unsigned long long*)t->slots, mask,
+                      (const int*)t->aux, hs->table, (uint64_t)hs->cap - 1,
+                      hs->count_dev, flag, nvox, seg_slots, seg_wins)) != cudaSuccess)
+    return e;
+  if ((e = launch_pdl(dd_clear_kernel, dim3(g), dim3(256), 0, s, sg, (const int*)t->aux, (const int32_t*)seg_slots,
+                      (const int32_t*)seg_wins, t->slots)) != cudaSuccess)
+    return e;
+  count_launches(3);
+  return cudaSuccess;
+}
+
+
 cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, size_t ws_bytes, int sms,
                         cudaStream_t s) {
   const int64_t npix = in.frames * in.H * in.W;
@@ -1404,92 +1639,138 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   // every voxel of the batch keeps at least one item, so the sorted item count
   // bounds the new keys (first-pick dedup makes it ~3x tighter than nvalid)
   if ((e = hashset_reserve(hs, nitems, s)) != cudaSuccess) return e;
-  // bbox-relative key width; +1 on x keeps the all-ones invalid key above every valid key
-  RelKey rk;
-  rk.x0 = (uint32_t)hb[0];
-  rk.y0 = (uint32_t)hb[1];
-  rk.z0 = (uint32_t)hb[2];
-  const int bx = bits_for((int64_t)hb[3] - hb[0] + 1), by = bits_for((int64_t)hb[4] - hb[1]),
-            bz = bits_for((int64_t)hb[5] - hb[2]);
-  rk.by = by;
-  rk.bz = bz;
-  int bits = bx + by + bz;
-  if (bits > 64) {  // degenerate extent: sort the raw biased keys (identity packing)
-    rk.x0 = rk.y0 = rk.z0 = 0;
-    rk.by = rk.bz = 21;
-    bits = 64;
-  }
-  if ((e = sort_init()) != cudaSuccess) return e;
-  const int64_t tiles = (nitems + SORT_TILE - 1) / SORT_TILE;
-  if (nitems == 0) return cudaSuccess;
-  out.n_sorted = nitems;
-  out.sort_passes = (bits + 7) / 8;
-  // the new-head flags are cleared ahead of the sort, so select follows the
-  // last sort kernel directly (programmatic launch, no memset in between)
-  if ((e = cudaMemsetAsync(flag, 0, (size_t)nwords * 4, s)) != cudaSuccess) return e;
-  {
-    ProfScope prof("grid_sort", s);
-    // relative keys once (u32 when they fit), LSD passes, biased keys back into k0
-    const unsigned rb = grid_blocks(nitems, 256, sms);
-    if (fused) {   // block slots -> dense: exclusive scan of the block counts
-      if ((e = exclusive_scan_i32(block_count, fblocks, block_count, ssum, nullptr, s)) != cudaSuccess) return e;
+  // first-pick mode takes the hash path (G2'); XGS_GRID_SORT=1 forces the
+  // radix sort + select path (mean mode always sorts: its per-voxel sums run
+  // in pixel order over the voxel's segment)
+  const char* force_sort = std::getenv("XGS_GRID_SORT");
+  const bool hashed = compact && !(force_sort && force_sort[0] == '1');
+  std::unique_lock<std::mutex> dd_lock(g_dedup_mu, std::defer_lock);
+  DedupTable* dd = nullptr;
+  DedupSegs sg{};
+  if (hashed) {
+    dd_lock.lock();
+    out.n_sorted = nitems;
+    out.sort_passes = 0;
+    sg.k = k0;
+    sg.v = v0;
+    sg.H = in.H;
+    sg.W = in.W;
+    if (fused) {
+      sg.count = block_count;
+      sg.nseg = fblocks;
+    } else {
+      sg.count = nullptr;
+      sg.n_dense = nitems;
+      sg.nseg = (nitems + kDedupSeg - 1) / kDedupSeg;
     }
-    if (bits <= 32) {
-      uint32_t* r0 = reinterpret_cast<uint32_t*>(k1);
-      uint32_t* r1 = r0 + nitems;
-      if (fused) {   // items land in (r0, v1); the slots in (k0, v0) are dead afterwards
-        if ((e = launch_pdl(rekey_gather_kernel<uint32_t>, dim3(grid_blocks(fblocks, 1, sms)), dim3(256), 0, s, k0, v0,
-                            block_count, fblocks, in.H, in.W, nitems, rk, r0, v1)) != cudaSuccess)
+    {
+      ProfScope prof("grid_select", s);
+      if ((e = dedup_table(nitems, false, s, &dd)) != cudaSuccess) return e;
+      if ((e = dedup_pass(sg, dd, hs, reinterpret_cast<unsigned*>(flag), nwords, cnts + 1, head, hist, sms, s)) != cudaSuccess)
+        return e;
+    }
+  } else {
+  // bbox-relative key width; +1 on x keeps the all-ones invalid key above every valid key
+    RelKey rk;
+    rk.x0 = (uint32_t)hb[0];
+    rk.y0 = (uint32_t)hb[1];
+    rk.z0 = (uint32_t)hb[2];
+    const int bx = bits_for((int64_t)hb[3] - hb[0] + 1), by = bits_for((int64_t)hb[4] - hb[1]),
+              bz = bits_for((int64_t)hb[5] - hb[2]);
+    rk.by = by;
+    rk.bz = bz;
+    int bits = bx + by + bz;
+    if (bits > 64) {  // degenerate extent: sort the raw biased keys (identity packing)
+      rk.x0 = rk.y0 = rk.z0 = 0;
+      rk.by = rk.bz = 21;
+      bits = 64;
+    }
+    if ((e = sort_init()) != cudaSuccess) return e;
+    const int64_t tiles = (nitems + SORT_TILE - 1) / SORT_TILE;
+    if (nitems == 0) return cudaSuccess;
+    out.n_sorted = nitems;
+    out.sort_passes = (bits + 7) / 8;
+    // the new-head flags are cleared ahead of the sort, so select follows the
+    // last sort kernel directly (programmatic launch, no memset in between)
+    if ((e = cudaMemsetAsync(flag, 0, (size_t)nwords * 4, s)) != cudaSuccess) return e;
+    {
+      ProfScope prof("grid_sort", s);
+      // relative keys once (u32 when they fit), LSD passes, biased keys back into k0
+      const unsigned rb = grid_blocks(nitems, 256, sms);
+      if (fused) {   // block slots -> dense: exclusive scan of the block counts
+        if ((e = exclusive_scan_i32(block_count, fblocks, block_count, ssum, nullptr, s)) != cudaSuccess) return e;
+      }
+      if (bits <= 32) {
+        uint32_t* r0 = reinterpret_cast<uint32_t*>(k1);
+        uint32_t* r1 = r0 + nitems;
+        if (fused) {   // items land in (r0, v1); the slots in (k0, v0) are dead afterwards
+          if ((e = launch_pdl(rekey_gather_kernel<uint32_t>, dim3(grid_blocks(fblocks, 1, sms)), dim3(256), 0, s, k0, v0,
+                              block_count, fblocks, in.H, in.W, nitems, rk, r0, v1)) != cudaSuccess)
+            return e;
+          count_launches(1);
+          uint32_t* t = v0; v0 = v1; v1 = t;
+        } else {
+          rekey_kernel<uint32_t><<<rb, 256, 0, s>>>(k0, nitems, rk, r0); count_launches(1);
+        }
+        if ((e = lsd_passes<uint32_t>(r0, v0, r1, v1, nitems, bits, hist, ssum, s)) != cudaSuccess) return e;
+        if ((e = launch_pdl(unrekey_kernel<uint32_t>, dim3(rb), dim3(256), 0, s, r0, nitems, rk, bits, k0)) != cudaSuccess)
           return e;
         count_launches(1);
-        uint32_t* t = v0; v0 = v1; v1 = t;
       } else {
-        rekey_kernel<uint32_t><<<rb, 256, 0, s>>>(k0, nitems, rk, r0); count_launches(1);
+        if (fused) {
+          rekey_gather_kernel<uint64_t><<<grid_blocks(fblocks, 1, sms), 256, 0, s>>>(k0, v0, block_count, fblocks, in.H, in.W,
+                                                                                     nitems, rk, k1, v1); count_launches(1);
+          uint32_t* t = v0; v0 = v1; v1 = t;
+        } else {
+          rekey_kernel<uint64_t><<<rb, 256, 0, s>>>(k0, nitems, rk, k1); count_launches(1);
+        }
+        uint64_t* r0 = k1;
+        uint64_t* r1 = k0;
+        if ((e = lsd_passes<uint64_t>(r0, v0, r1, v1, nitems, bits, hist, ssum, s)) != cudaSuccess) return e;
+        if (r0 == k0) {   // sorted relative keys landed in k0's buffer: unpack through k1
+          unrekey_kernel<uint64_t><<<rb, 256, 0, s>>>(r0, nitems, rk, bits, k1); count_launches(1);
+          uint64_t* t = k0; k0 = k1; k1 = t;
+        } else {
+          unrekey_kernel<uint64_t><<<rb, 256, 0, s>>>(r0, nitems, rk, bits, k0); count_launches(1);
+        }
       }
-      if ((e = lsd_passes<uint32_t>(r0, v0, r1, v1, nitems, bits, hist, ssum, s)) != cudaSuccess) return e;
-      if ((e = launch_pdl(unrekey_kernel<uint32_t>, dim3(rb), dim3(256), 0, s, r0, nitems, rk, bits, k0)) != cudaSuccess)
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    {
+      ProfScope prof("grid_select", s);
+      if ((e = launch_pdl(grid_select_kernel, dim3(grid_blocks(nitems, 256, sms)), dim3(256), 0, s, (const uint64_t*)k0,
+                          (const uint32_t*)v0, nitems, hs->table, (uint64_t)hs->cap - 1, hs->count_dev,
+                          reinterpret_cast<unsigned*>(flag), head, cnts + 1)) != cudaSuccess)
         return e;
       count_launches(1);
-    } else {
-      if (fused) {
-        rekey_gather_kernel<uint64_t><<<grid_blocks(fblocks, 1, sms), 256, 0, s>>>(k0, v0, block_count, fblocks, in.H, in.W,
-                                                                                   nitems, rk, k1, v1); count_launches(1);
-        uint32_t* t = v0; v0 = v1; v1 = t;
-      } else {
-        rekey_kernel<uint64_t><<<rb, 256, 0, s>>>(k0, nitems, rk, k1); count_launches(1);
-      }
-      uint64_t* r0 = k1;
-      uint64_t* r1 = k0;
-      if ((e = lsd_passes<uint64_t>(r0, v0, r1, v1, nitems, bits, hist, ssum, s)) != cudaSuccess) return e;
-      if (r0 == k0) {   // sorted relative keys landed in k0's buffer: unpack through k1
-        unrekey_kernel<uint64_t><<<rb, 256, 0, s>>>(r0, nitems, rk, bits, k1); count_launches(1);
-        uint64_t* t = k0; k0 = k1; k1 = t;
-      } else {
-        unrekey_kernel<uint64_t><<<rb, 256, 0, s>>>(r0, nitems, rk, bits, k0); count_launches(1);
-      }
     }
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
-  {
-    ProfScope prof("grid_select", s);
-    if ((e = launch_pdl(grid_select_kernel, dim3(grid_blocks(nitems, 256, sms)), dim3(256), 0, s, (const uint64_t*)k0,
-                        (const uint32_t*)v0, nitems, hs->table, (uint64_t)hs->cap - 1, hs->count_dev,
-                        reinterpret_cast<unsigned*>(flag), head, cnts + 1)) != cudaSuccess)
-      return e;
-    count_launches(1);
   }
   {
     ProfScope prof("grid_emit", s);
-    if ((e = launch_pdl(popc_kernel, dim3(grid_blocks(nwords, 256, sms)), dim3(256), 0, s,
-                        reinterpret_cast<const unsigned*>(flag), nwords, pos)) != cudaSuccess)
-      return e;
-    count_launches(1);
-    if ((e = exclusive_scan<int32_t>(pos, nwords, pos, ssum, grand, s)) != cudaSuccess) return e;
     int32_t nnew = 0;
     unsigned long long nvox = 0;
-    if ((e = cudaMemcpyAsync(&nnew, grand, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-    if ((e = cudaMemcpyAsync(&nvox, cnts + 1, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    for (int attempt = 0;; attempt++) {
+      if ((e = launch_pdl(popc_kernel, dim3(grid_blocks(nwords, 256, sms)), dim3(256), 0, s,
+                          reinterpret_cast<const unsigned*>(flag), nwords, pos)) != cudaSuccess)
+        return e;
+      count_launches(1);
+      if ((e = exclusive_scan<int32_t>(pos, nwords, pos, ssum, grand, s)) != cudaSuccess) return e;
+      int ovf = 0;
+      if ((e = cudaMemcpyAsync(&nnew, grand, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+      if ((e = cudaMemcpyAsync(&nvox, cnts + 1, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+      if (hashed && (e = cudaMemcpyAsync(&ovf, dd->aux, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+      if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+      if (!ovf) break;
+      // the table was too small for this batch's distinct voxels: pass 2 did not
+      // run (map untouched); reset the partly filled table and redo the batch on
+      // one sized for every item
+      if (attempt > 0) return cudaErrorUnknown;
+      fill_u64_kernel<<<grid_blocks(2 * dd->cap, 256, sms), 256, 0, s>>>(dd->slots, 2 * dd->cap, ~0ull); count_launches(1);
+      if ((e = dedup_table(nitems, true, s, &dd)) != cudaSuccess) return e;
+      if ((e = dedup_pass(sg, dd, hs, reinterpret_cast<unsigned*>(flag), nwords, cnts + 1, head, hist, sms, s)) != cudaSuccess)
+        return e;
+    }
+    if (hashed) dd->last_nvox = (int64_t)nvox;
     out.n_new = nnew;
     hs->count_ub += nnew;
     out.n_voxels = (int64_t)nvox;

@@ -101,6 +101,63 @@ def test_grid_sample_matches_oracle(xs, mode, voxel):
         assert np.array_equal(got["count"], ref["count"])
 
 
+def _sample_both(grid, gs_args, batch, warm=None):
+    """The same batch through the hash first-pick path (default) and the radix
+    sort + select path (XGS_GRID_SORT=1), each on its own copy of the map."""
+    import os
+    out = []
+    for force in ("0", "1"):
+        os.environ["XGS_GRID_SORT"] = force
+        try:
+            gs = grid.GridSampler(*gs_args)
+            if warm is not None:
+                gs.occupied.insert(warm)
+            r = gs.sample(*batch)
+            out.append((r.to_numpy(), len(gs.occupied)))
+        finally:
+            os.environ.pop("XGS_GRID_SORT", None)
+    return out
+
+
+@pytest.mark.parametrize("W,voxel", [(128, 0.01), (128, 0.05), (130, 0.02)])
+def test_grid_hash_and_sort_paths_agree(xs, W, voxel):
+    """First-pick mode: the hash dedup (per-voxel atomicMin of the pixel id) and
+    the sort path give identical outputs, on the fused front end (W % 4 == 0)
+    and the two-kernel one (W = 130), with a pre-populated map."""
+    grid, _, synth = xs
+    frames, intr4 = _scene(synth, 5, 96, W, 11, spheres=True)
+    batch = (np.stack([f[0] for f in frames]), (np.stack([f[2] for f in frames]), np.stack([f[3] for f in frames])),
+             np.stack([f[1] for f in frames]))
+    ref = og.grid_sample(frames[:1], np.array(intr4), voxel, set())
+    (h, nh), (srt, ns) = _sample_both(grid, (intr4, voxel), batch, warm=ref["key"][::3])
+    assert nh == ns and h["n_voxels"] == srt["n_voxels"] and h["n_valid"] == srt["n_valid"]
+    for name in ("key", "pid", "mu", "color", "scale", "depth", "count"):
+        assert np.array_equal(h[name], srt[name]), name
+    assert h["sort_passes"] == 0 and srt["sort_passes"] > 0
+
+
+def test_grid_hash_table_overflow_retry(xs):
+    """A batch with far more distinct voxels than the table sized from the
+    previous batch: the bounded probes overflow, pass 2 is skipped (map
+    untouched) and the batch is redone on a table sized for every item."""
+    grid, _, _ = xs
+    import torch
+    rng = np.random.default_rng(5)
+    intr4 = (525.0, 525.0, 239.5, 319.5)
+    gs = grid.GridSampler(intr4, 0.05)
+    small = np.full((1, 480, 640), 2.0, np.float32)
+    gs.sample(small, (np.eye(3)[None], np.zeros((1, 3))))           # few voxels: next table is the 1M minimum
+    D = rng.uniform(0.5, 5.0, (12, 480, 640)).astype(np.float32)     # ~3.7M distinct 1 mm voxels
+    R = np.repeat(np.eye(3)[None], 12, 0)
+    T = np.zeros((12, 3))
+    (h, nh), (srt, ns) = _sample_both(grid, (intr4, 0.001), (D, (R, T)))
+    assert h["n_voxels"] > 2_000_000
+    assert nh == ns and h["n_voxels"] == srt["n_voxels"]
+    for name in ("key", "pid", "mu", "scale", "depth"):
+        assert np.array_equal(h[name], srt[name]), name
+    torch.cuda.synchronize()
+
+
 def test_grid_incremental_and_batching(xs):
     grid, _, synth = xs
     frames, intr4 = _scene(synth, 4, 64, 80, 4)
