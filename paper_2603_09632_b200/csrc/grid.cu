@@ -1340,16 +1340,16 @@ size_t grid_workspace_bytes(int64_t npix) { return grid_ws(npix).total; }
 // ---------------------------------------------------------------- G2' hash first-pick
 // First-pick mode does not need the items in voxel order, only each voxel's
 // lowest pixel id: a batch table (open addressing on the voxel key, one
-// atomicMin of the pixel id per slot) finds it in two passes over the items
+// atomicMin of the pixel id per slot) finds it in one pass over the items
 // instead of the radix sort + segment-head select.  Pass 1 claims / finds the
-// key's slot and lowers its pixel id; pass 2 keeps the item whose pixel id is
-// the slot's minimum (one per voxel), runs the map test (insert-if-absent into
-// the occupancy set) and flags new voxels in the pixel bitmask, from which the
-// emit stage writes the outputs in ascending pixel order exactly as before.
-// The winners' slots are cleared after the batch, so the table starts every
-// batch empty without a memset.  Probing is bounded; an overflow (table too
-// small for the batch's distinct voxels) skips pass 2 (the map is untouched)
-// and the host retries with a table sized for every item.
+// key's slot and lowers its pixel id; pass 2 scans the table (one occupied
+// slot per voxel), runs the map test (insert-if-absent into the occupancy
+// set), flags new voxels in the pixel bitmask -- from which the emit stage
+// writes the outputs in ascending pixel order exactly as before -- and empties
+// the slot, so the table starts every batch empty without a memset.  Probing
+// is bounded; an overflow (table too small for the batch's distinct voxels)
+// skips pass 2 (the map is untouched) and the host retries with a table sized
+// for every item.
 constexpr int kDedupProbe = 256;
 constexpr int64_t kDedupSeg = 4096;   // dense item lists: segment length
 constexpr uint32_t PID_NONE = 0xffffffffu;
@@ -1429,55 +1429,26 @@ dd_insert_kernel(DedupSegs sg, unsigned long long* slots, uint64_t mask, int* ov
   }
 }
 
-// Winners record their slot at the segment's own item positions (seg_slots,
-// block-local counter; seg_wins[b] = count), so clearing needs no global
-// append counter.
+// Pass 2: every occupied slot is one voxel of the batch and holds its lowest
+// pixel id, so a sequential scan of the table (not another probe per item)
+// runs the map test (insert-if-absent into the occupancy set), flags new
+// voxels in the pixel bitmask and empties the slot for the next batch.
 __global__ void __launch_bounds__(256)
-dd_select_kernel(DedupSegs sg, const unsigned long long* slots, uint64_t mask, const int* overflow,
-                 unsigned long long* table, uint64_t tmask, unsigned long long* set_count, unsigned* flag_bits,
-                 unsigned long long* nvox, int32_t* seg_slots, int32_t* seg_wins) {
+dd_scan_kernel(unsigned long long* slots, int64_t cap, const int* overflow, unsigned long long* table,
+               uint64_t tmask, unsigned long long* set_count, unsigned* flag_bits, unsigned long long* nvox) {
   pdl_wait();
-  if (*(volatile const int*)overflow) return;
-  __shared__ int s_w;
+  if (*(volatile const int*)overflow) return;   // the host resets the whole table
   unsigned newc = 0, vox = 0;
-  for (int64_t b = blockIdx.x; b < sg.nseg; b += gridDim.x) {
-    int64_t base, cnt;
-    sg.seg(b, base, cnt);
-    if (threadIdx.x == 0) s_w = 0;
-    __syncthreads();
-    for (int64_t i0 = threadIdx.x; i0 < cnt; i0 += kDedupILP * blockDim.x) {
-      uint64_t key[kDedupILP], h[kDedupILP];
-      uint32_t pid[kDedupILP];
-      ulonglong2 cur[kDedupILP];
-#pragma unroll
-      for (int j = 0; j < kDedupILP; j++) {
-        const int64_t i = i0 + j * blockDim.x;
-        key[j] = i < cnt ? __ldg(sg.k + base + i) : KEY_INVALID;
-        pid[j] = i < cnt ? __ldg(sg.v + base + i) : 0u;
-      }
-#pragma unroll
-      for (int j = 0; j < kDedupILP; j++) {
-        h[j] = mix64(key[j]) & mask;
-        cur[j] = key[j] != KEY_INVALID ? slot_ld(slots, h[j]) : make_ulonglong2(0ull, 0ull);
-      }
-#pragma unroll
-      for (int j = 0; j < kDedupILP; j++) {
-        if (key[j] == KEY_INVALID) continue;
-        while (cur[j].x != key[j]) {   // present: pass 1 placed it
-          h[j] = (h[j] + 1) & mask;
-          cur[j] = slot_ld(slots, h[j]);
-        }
-        if ((uint32_t)cur[j].y != pid[j]) continue;   // not the voxel's lowest pixel id
-        vox++;
-        seg_slots[base + atomicAdd(&s_w, 1)] = (int32_t)h[j];
-        if (hs_insert_probe(table, tmask, key[j])) {
-          atomicOr(flag_bits + (pid[j] >> 5), 1u << (pid[j] & 31));
-          newc++;
-        }
-      }
+  for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < cap; h += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 sl = slot_ld(slots, (uint64_t)h);
+    if (sl.x == EMPTY) continue;
+    vox++;
+    const uint32_t pid = (uint32_t)sl.y;
+    if (hs_insert_probe(table, tmask, sl.x)) {
+      atomicOr(flag_bits + (pid >> 5), 1u << (pid & 31));
+      newc++;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) seg_wins[b] = s_w;
+    *reinterpret_cast<ulonglong2*>(slots + 2 * h) = make_ulonglong2(~0ull, ~0ull);
   }
   for (int o = 16; o; o >>= 1) {
     newc += __shfl_xor_sync(FULL, newc, o);
@@ -1488,21 +1459,6 @@ dd_select_kernel(DedupSegs sg, const unsigned long long* slots, uint64_t mask, c
     if (vox) atomicAdd(nvox, (unsigned long long)vox);
   }
 }
-
-__global__ void __launch_bounds__(256)
-dd_clear_kernel(DedupSegs sg, const int* overflow, const int32_t* __restrict__ seg_slots,
-                const int32_t* __restrict__ seg_wins, unsigned long long* slots) {
-  pdl_wait();
-  if (*(volatile const int*)overflow) return;   // the host resets the whole table
-  for (int64_t b = blockIdx.x; b < sg.nseg; b += gridDim.x) {
-    int64_t base, cnt;
-    sg.seg(b, base, cnt);
-    const int n = seg_wins[b];
-    for (int j = threadIdx.x; j < n; j += blockDim.x)
-      *reinterpret_cast<ulonglong2*>(slots + 2 * (int64_t)seg_slots[base + j]) = make_ulonglong2(~0ull, ~0ull);
-  }
-}
-
 
 // per-device batch table (library-owned scratch, empty between batches)
 struct DedupTable {
@@ -1549,7 +1505,7 @@ cudaError_t dedup_table(int64_t nitems, bool all, cudaStream_t s, DedupTable** o
 // pass 1 + pass 2 + clear; the flags, the voxel count and the table's aux
 // words are reset first (also on a retry)
 cudaError_t dedup_pass(const DedupSegs& sg, DedupTable* t, HashSet* hs, unsigned* flag, int64_t nwords,
-                       unsigned long long* nvox, int32_t* seg_slots, int32_t* seg_wins, int sms, cudaStream_t s) {
+                       unsigned long long* nvox, int sms, cudaStream_t s) {
   cudaError_t e;
   if ((e = cudaMemsetAsync(flag, 0, (size_t)nwords * 4, s)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(nvox, 0, 8, s)) != cudaSuccess) return e;
@@ -1558,14 +1514,10 @@ cudaError_t dedup_pass(const DedupSegs& sg, DedupTable* t, HashSet* hs, unsigned
   const unsigned g = (unsigned)(sg.nseg < 148 * 8 ? sg.nseg : 148 * 8);
   if ((e = launch_pdl(dd_insert_kernel, dim3(g), dim3(256), 0, s, sg, t->slots, mask, t->aux)) != cudaSuccess)
     return e;
-  if ((e = launch_pdl(dd_select_kernel, dim3(g), dim3(256), 0, s, sg, (const unsigned long long*)t->slots, mask,
-                      (const int*)t->aux, hs->table, (uint64_t)hs->cap - 1,
-                      hs->count_dev, flag, nvox, seg_slots, seg_wins)) != cudaSuccess)
+  if ((e = launch_pdl(dd_scan_kernel, dim3(grid_blocks(t->cap, 256, sms)), dim3(256), 0, s, t->slots, t->cap,
+                      (const int*)t->aux, hs->table, (uint64_t)hs->cap - 1, hs->count_dev, flag, nvox)) != cudaSuccess)
     return e;
-  if ((e = launch_pdl(dd_clear_kernel, dim3(g), dim3(256), 0, s, sg, (const int*)t->aux, (const int32_t*)seg_slots,
-                      (const int32_t*)seg_wins, t->slots)) != cudaSuccess)
-    return e;
-  count_launches(3);
+  count_launches(2);
   return cudaSuccess;
 }
 
@@ -1666,7 +1618,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     {
       ProfScope prof("grid_select", s);
       if ((e = dedup_table(nitems, false, s, &dd)) != cudaSuccess) return e;
-      if ((e = dedup_pass(sg, dd, hs, reinterpret_cast<unsigned*>(flag), nwords, cnts + 1, head, hist, sms, s)) != cudaSuccess)
+      if ((e = dedup_pass(sg, dd, hs, reinterpret_cast<unsigned*>(flag), nwords, cnts + 1, sms, s)) != cudaSuccess)
         return e;
     }
   } else {
@@ -1767,7 +1719,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
       if (attempt > 0) return cudaErrorUnknown;
       fill_u64_kernel<<<grid_blocks(2 * dd->cap, 256, sms), 256, 0, s>>>(dd->slots, 2 * dd->cap, ~0ull); count_launches(1);
       if ((e = dedup_table(nitems, true, s, &dd)) != cudaSuccess) return e;
-      if ((e = dedup_pass(sg, dd, hs, reinterpret_cast<unsigned*>(flag), nwords, cnts + 1, head, hist, sms, s)) != cudaSuccess)
+      if ((e = dedup_pass(sg, dd, hs, reinterpret_cast<unsigned*>(flag), nwords, cnts + 1, sms, s)) != cudaSuccess)
         return e;
     }
     if (hashed) dd->last_nvox = (int64_t)nvox;
