@@ -1502,7 +1502,13 @@ cudaError_t dedup_table(int64_t nitems, bool all, cudaStream_t s, DedupTable** o
   return cudaGetLastError();
 }
 
-// pass 1 + pass 2 + clear; the flags, the voxel count and the table's aux
+bool dedup_sized() {
+  int dev = 0;
+  return cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < kDedupDevices && g_dedup[dev].slots &&
+         g_dedup[dev].last_nvox >= 0;
+}
+
+// pass 1 + pass 2; the flags, the voxel count and the table's aux
 // words are reset first (also on a retry)
 cudaError_t dedup_pass(const DedupSegs& sg, DedupTable* t, HashSet* hs, unsigned* flag, int64_t nwords,
                        unsigned long long* nvox, int sms, cudaStream_t s) {
@@ -1579,28 +1585,35 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
           k1, npix, in.W, k0, v0, tile_counter, lb_status, ntiles, cnts + 2); count_launches(1);
     }
   }
-  int hb[8];
-  unsigned long long hc[3] = {0, 0, 0};
-  if ((e = cudaMemcpyAsync(hb, bbox, 6 * sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-  if ((e = cudaMemcpyAsync(hc, cnts, 24, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-  const unsigned long long nvalid = hc[0];
-  out.n_valid = (int64_t)nvalid;
-  if (nvalid == 0) return cudaSuccess;
-  const int64_t nitems = compact ? (int64_t)hc[2] : npix;   // items to sort
-  // every voxel of the batch keeps at least one item, so the sorted item count
-  // bounds the new keys (first-pick dedup makes it ~3x tighter than nvalid)
-  if ((e = hashset_reserve(hs, nitems, s)) != cudaSuccess) return e;
   // first-pick mode takes the hash path (G2'); XGS_GRID_SORT=1 forces the
   // radix sort + select path (mean mode always sorts: its per-voxel sums run
   // in pixel order over the voxel's segment)
   const char* force_sort = std::getenv("XGS_GRID_SORT");
   const bool hashed = compact && !(force_sort && force_sort[0] == '1');
   std::unique_lock<std::mutex> dd_lock(g_dedup_mu, std::defer_lock);
+  if (hashed) dd_lock.lock();
+  // The hash path on the fused front end needs no host-side item count when
+  // the occupancy set already has room for a new key per pixel and the batch
+  // table was sized by an earlier batch: no read-back between the front end
+  // and the dedup (the counts are read with the final one).
+  const bool no_sync = hashed && fused && 2 * (hs->count_ub + npix) <= hs->cap && dedup_sized();
+  int hb[8];
+  unsigned long long hc[3] = {0, 0, 0};
+  int64_t nitems = 0;
+  if (!no_sync) {
+    if ((e = cudaMemcpyAsync(hb, bbox, 6 * sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(hc, cnts, 24, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    out.n_valid = (int64_t)hc[0];
+    if (hc[0] == 0) return cudaSuccess;
+    nitems = compact ? (int64_t)hc[2] : npix;   // items to sort
+    // every voxel of the batch keeps at least one item, so the sorted item count
+    // bounds the new keys (first-pick dedup makes it ~3x tighter than nvalid)
+    if ((e = hashset_reserve(hs, nitems, s)) != cudaSuccess) return e;
+  }
   DedupTable* dd = nullptr;
   DedupSegs sg{};
   if (hashed) {
-    dd_lock.lock();
     out.n_sorted = nitems;
     out.sort_passes = 0;
     sg.k = k0;
@@ -1708,10 +1721,15 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
       count_launches(1);
       if ((e = exclusive_scan<int32_t>(pos, nwords, pos, ssum, grand, s)) != cudaSuccess) return e;
       int ovf = 0;
+      if (no_sync && (e = cudaMemcpyAsync(hc, cnts, 24, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
       if ((e = cudaMemcpyAsync(&nnew, grand, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
       if ((e = cudaMemcpyAsync(&nvox, cnts + 1, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
       if (hashed && (e = cudaMemcpyAsync(&ovf, dd->aux, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
       if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+      if (no_sync) {
+        out.n_valid = (int64_t)hc[0];
+        out.n_sorted = nitems = (int64_t)hc[2];
+      }
       if (!ovf) break;
       // the table was too small for this batch's distinct voxels: pass 2 did not
       // run (map untouched); reset the partly filled table and redo the batch on

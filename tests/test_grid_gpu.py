@@ -136,10 +136,13 @@ def test_grid_hash_and_sort_paths_agree(xs, W, voxel):
     assert h["sort_passes"] == 0 and srt["sort_passes"] > 0
 
 
-def test_grid_hash_table_overflow_retry(xs):
+@pytest.mark.parametrize("map_capacity", [1 << 20, 1 << 24])
+def test_grid_hash_table_overflow_retry(xs, map_capacity):
     """A batch with far more distinct voxels than the table sized from the
     previous batch: the bounded probes overflow, pass 2 is skipped (map
-    untouched) and the batch is redone on a table sized for every item."""
+    untouched) and the batch is redone on a table sized for every item.  With
+    the large map the batch also skips the front-end read-back (item count
+    first known at the final read-back)."""
     grid, _, _ = xs
     import torch
     rng = np.random.default_rng(5)
@@ -150,8 +153,9 @@ def test_grid_hash_table_overflow_retry(xs):
     D = rng.uniform(0.5, 5.0, (12, 480, 640)).astype(np.float32)     # ~3.7M distinct 1 mm voxels
     R = np.repeat(np.eye(3)[None], 12, 0)
     T = np.zeros((12, 3))
-    (h, nh), (srt, ns) = _sample_both(grid, (intr4, 0.001), (D, (R, T)))
-    assert h["n_voxels"] > 2_000_000
+    gs.sample(small, (np.eye(3)[None], np.zeros((1, 3))))           # reset the table size after any earlier run
+    (h, nh), (srt, ns) = _sample_both(grid, (intr4, 0.001, 1, "first", 1e-3, None, map_capacity), (D, (R, T)))
+    assert h["n_voxels"] > 2_000_000 and h["n_valid"] == srt["n_valid"] and h["n_sorted"] == srt["n_sorted"]
     assert nh == ns and h["n_voxels"] == srt["n_voxels"]
     for name in ("key", "pid", "mu", "scale", "depth"):
         assert np.array_equal(h[name], srt[name]), name
