@@ -2,16 +2,21 @@
 //
 // Turns a batch of F depth frames into new Gaussians, one per voxel that is
 // not yet occupied in the map, in ascending (frame, pixel) order:
-//   G1 grid_keys_kernel    : float4 depth loads, fp64 back-projection in the
-//                            reference's operation order (slam.py:594-598),
-//                            floor(p / voxel) -> 63-bit biased voxel key, batch
-//                            bounding box of the voxel indices;
-//   G2 in-house LSD radix sort of (key, pixel id) on the bbox-relative key
-//                            (ceil(bits/8) passes of upsweep / scan /
-//                            stable downsweep with warp match_any ranks);
+//   G1 grid_front_kernel / grid_keys_kernel: depth loads, back-projection in
+//                            the reference's operation order (slam.py:594-598),
+//                            floor(p / voxel) -> 63-bit biased voxel key; the
+//                            fused front end also drops pixels whose left or
+//                            upper neighbour has the same key and compacts the
+//                            survivors in pixel order;
+//   G2' first-pick mode: dd_insert_kernel + dd_scan_kernel, a batch hash table
+//                            (per-voxel atomicMin of the pixel id) gives each
+//                            voxel's lowest pixel id; the scan runs the map
+//                            test and flags new voxels;
+//   G2 mean mode (or XGS_GRID_SORT=1): in-house LSD radix sort of (key, pixel
+//                            id) on the bbox-relative key (ceil(bits/8) passes
+//                            of upsweep / scan / stable downsweep), then
 //   G3 grid_select_kernel  : segment heads = lowest pixel id per voxel;
-//                            insert-if-absent into the GPU hash set of the map
-//                            (query-then-insert in one atomicCAS);
+//                            insert-if-absent into the GPU hash set of the map;
 //   G4 hash set            : open addressing, 64-bit keys, linear probing,
 //                            power-of-two capacity at load <= 1/2;
 //   G5 grid_emit_kernel    : pixel-order compaction (exclusive scan of the

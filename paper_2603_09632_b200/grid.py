@@ -96,8 +96,8 @@ class GridSampleResult:
     feature: Optional[object]
     n_valid: int
     n_voxels: int
-    n_sorted: int = 0        # items the radix sort moved (after first-pick compaction)
-    sort_passes: int = 0     # 8-bit LSD passes
+    n_sorted: int = 0        # items through the dedup (after the front end's first-pick compaction)
+    sort_passes: int = 0     # 8-bit LSD passes (0: first-pick hash dedup, no sort)
 
     def __len__(self):
         return int(self.pid.shape[0])
