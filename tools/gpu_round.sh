@@ -10,5 +10,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --stream-frames 50 --c5-iters 1 > gpurun_out/r_ncu_list.log 2>&1; echo "list rc=$?" >> gpurun_out/r_ncu_list.log
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"screen_kernel|prep_rows|acc_chain" -c 4 \
   -o gpurun_out/r_vq_full python tools/prof_vq.py 2 > gpurun_out/r_ncu_vq.log 2>&1; echo "vq rc=$?" >> gpurun_out/r_ncu_vq.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"grid_front|sort_downsweep|sort_upsweep|grid_select|grid_emit" -c 5 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"grid_front|dd_insert|dd_scan|grid_emit|grid_pidlist" -c 5 \
   -o gpurun_out/r_grid_full python tools/prof_grid.py 1 0.01 > gpurun_out/r_ncu_grid.log 2>&1; echo "grid rc=$?" >> gpurun_out/r_ncu_grid.log
