@@ -211,7 +211,7 @@ def run_grid(torch, steps, cpu=True):
             r = gs.sample(Dd, (Rd, Td), Cd)
             e1.record()
             torch.cuda.synchronize()
-            if it > 0:
+            if 0 < it < steps or (it == steps and not times):   # the last run is the profiled one
                 times.append(e0.elapsed_time(e1))
             n_new, n_valid, n_sorted, passes = len(r), r.n_valid, r.n_sorted, r.sort_passes
             hs.close()
@@ -715,7 +715,6 @@ def main():
     barrier()
     clk = ClockSampler(local)
     clk.start()
-    nat.profile_enable(True)
     l0 = nat.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -729,6 +728,13 @@ def main():
     launches = nat.launch_count() - l0
     clocks = clk.stop()
     ms = ev0.elapsed_time(ev1)
+    # per-kernel breakdown from a separate profiled run (its event records are
+    # host work on the launch path, so the headline loop above runs without them)
+    prof_steps = min(args.steps, 10)
+    nat.profile_enable(True)
+    for _ in range(prof_steps):
+        vq.step(x, sizes)
+    torch.cuda.synchronize()
     prof = {t: nat.profile_read(t) for t in ("vq_prep", "vq_screen", "vq_rerank", "vq_accumulate", "vq_chain",
                                                "vq_ema")}
     nat.profile_enable(False)
@@ -807,7 +813,7 @@ def main():
         torch.cuda.empty_cache()
         c5 = run_c5(torch, args.c5_iters, device)
     if rank == 0:
-        per_kernel = {t: {"ms_per_step": m / args.steps, "launches": c} for t, (m, c) in prof.items()}
+        per_kernel = {t: {"ms_per_step": m / prof_steps, "launches": c} for t, (m, c) in prof.items()}
         line = {
             "metric": METRIC, "value": value, "unit": "Mfeat/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
