@@ -912,6 +912,12 @@ __device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* sm, int32
   return before;
 }
 
+// scan input adaptor: a 32-pixel flag word counts as its popcount
+struct PopcWord {
+  unsigned w;
+  __device__ __forceinline__ explicit operator int32_t() const { return __popc(w); }
+};
+
 template <typename T>
 __global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const T* __restrict__ in, int64_t n, int32_t* sums) {
   pdl_wait();
@@ -1060,18 +1066,70 @@ struct EmitArgs {
   double* count;
 };
 
-__global__ void popc_kernel(const unsigned* __restrict__ bits, int64_t nw, int32_t* __restrict__ out) {
-  pdl_wait();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = __popc(bits[i]);
+// One new voxel: output row o, representative pixel p (frame * H * W + u * W + v).
+__device__ __forceinline__ void emit_one(int64_t o, int64_t p, const int32_t* __restrict__ head_pos,
+                                         const EmitArgs& a) {
+  const int64_t HW = a.H * a.W;
+  const int64_t f = p / HW, rem = p - f * HW;
+  const int64_t u = rem / a.W, v = rem - u * a.W;
+  const double d = (double)a.depth[p];
+  a.dep[o] = d;
+  // iso size max(min_scale, 0.5*s*depth/fx)  (slam.py:631)
+  const double sz = ddiv(dmul(dmul(0.5, (double)a.stride), d), a.cam.fx);
+  a.scale[o] = fmax(a.min_scale, sz);
+  if (a.mode == 0) {
+    double mu[3];
+    backproject(a.rot + f * 9, a.trans + f * 3, a.cam, (double)u, (double)v, d, mu);
+    int64_t q[3];
+    voxel_of(mu, a.cam.voxel, q, a.cam.inv_voxel);
+    a.key[o] = ((uint64_t)q[0] << 42) | ((uint64_t)q[1] << 21) | (uint64_t)q[2];
+    for (int c = 0; c < 3; c++) {
+      a.mu[o * 3 + c] = mu[c];
+      a.col[o * 3 + c] = a.color ? ddiv((double)a.color[p * 3 + c], 255.0) : 0.0;
+    }
+    if (a.count) a.count[o] = 1.0;
+    if (a.feat) {
+      // supervision.py:133-147 nearest-neighbour gather rule
+      const int64_t uu = (int64_t)floor(ddiv(dmul((double)u, (double)(a.fh - 1)), (double)max(a.H - 1, (int64_t)1)) + 0.5);
+      const int64_t vv = (int64_t)floor(ddiv(dmul((double)v, (double)(a.fw - 1)), (double)max(a.W - 1, (int64_t)1)) + 0.5);
+      const float* src = a.feat + f * a.fc * a.fh * a.fw + uu * a.fw + vv;
+      for (int64_t c = 0; c < a.fc; c++) a.ofeat[o * a.fc + c] = src[c * a.fh * a.fw];
+    }
+  } else {
+    // mean over the voxel's points in the head's frame, sequential in pid order
+    const int64_t i0 = head_pos[p];
+    const uint64_t key = a.skeys[i0];
+    a.key[o] = key;
+    double sm[3] = {0.0, 0.0, 0.0}, sc[3] = {0.0, 0.0, 0.0};
+    double cnt = 0.0;
+    for (int64_t i = i0; i < a.n && a.skeys[i] == key; i++) {
+      const int64_t q = a.svals[i];
+      if (q / HW != f) continue;
+      const int64_t r2 = q - f * HW;
+      const int64_t uq = r2 / a.W, vq = r2 - uq * a.W;
+      double mu[3];
+      backproject(a.rot + f * 9, a.trans + f * 3, a.cam, (double)uq, (double)vq, (double)a.depth[q], mu);
+      for (int c = 0; c < 3; c++) {
+        sm[c] = dadd(sm[c], mu[c]);
+        if (a.color) sc[c] = dadd(sc[c], ddiv((double)a.color[q * 3 + c], 255.0));
+      }
+      cnt = dadd(cnt, 1.0);
+    }
+    for (int c = 0; c < 3; c++) {
+      a.mu[o * 3 + c] = ddiv(sm[c], cnt);
+      a.col[o * 3 + c] = ddiv(sc[c], cnt);
+    }
+    if (a.count) a.count[o] = cnt;
+  }
 }
 
 // Pixel ids of the new voxels in ascending order: one thread per 32-pixel
 // word of the new-voxel bitmask writes its set bits at the word's exclusive
-// popcount offset.
+// popcount offset (rows beyond `capacity` are not written; the host reports
+// the error after the final read-back).
 __global__ void __launch_bounds__(256)
 grid_pidlist_kernel(const unsigned* __restrict__ flag_bits, const int32_t* __restrict__ wpos, int64_t nwords,
-                    int64_t* __restrict__ pid_out) {
+                    int64_t capacity, int64_t* __restrict__ pid_out) {
   pdl_wait();
   for (int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; wi < nwords; wi += (int64_t)gridDim.x * blockDim.x) {
     unsigned word = flag_bits[wi];
@@ -1079,71 +1137,21 @@ grid_pidlist_kernel(const unsigned* __restrict__ flag_bits, const int32_t* __res
     while (word) {
       const int b = __ffs(word) - 1;
       word &= word - 1;
-      pid_out[o++] = wi * 32 + b;
+      if (o < capacity) pid_out[o] = wi * 32 + b;
+      o++;
     }
   }
 }
 
-// One thread per new voxel (output row o, pixel a.pid[o]): the
-// GaussianField-compatible attributes.
-__global__ void __launch_bounds__(256)
-grid_emit_kernel(const int32_t* __restrict__ head_pos, int64_t nnew, EmitArgs a) {
+// One thread per new voxel; the count comes from device memory (the scan's
+// total), so the emit is queued before the host reads it back.
+__global__ void __launch_bounds__(128)
+grid_emit_kernel(const int32_t* __restrict__ head_pos, const int32_t* __restrict__ nnew_dev, int64_t capacity,
+                 EmitArgs a) {
   pdl_wait();
-  const int64_t HW = a.H * a.W;
-  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < nnew; o += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = a.pid[o];
-    const int64_t f = p / HW, rem = p - f * HW;
-    const int64_t u = rem / a.W, v = rem - u * a.W;
-    const double d = (double)a.depth[p];
-    a.dep[o] = d;
-    // iso size max(min_scale, 0.5*s*depth/fx)  (slam.py:631)
-    const double sz = ddiv(dmul(dmul(0.5, (double)a.stride), d), a.cam.fx);
-    a.scale[o] = fmax(a.min_scale, sz);
-    if (a.mode == 0) {
-      double mu[3];
-      backproject(a.rot + f * 9, a.trans + f * 3, a.cam, (double)u, (double)v, d, mu);
-      int64_t q[3];
-      voxel_of(mu, a.cam.voxel, q, a.cam.inv_voxel);
-      a.key[o] = ((uint64_t)q[0] << 42) | ((uint64_t)q[1] << 21) | (uint64_t)q[2];
-      for (int c = 0; c < 3; c++) {
-        a.mu[o * 3 + c] = mu[c];
-        a.col[o * 3 + c] = a.color ? ddiv((double)a.color[p * 3 + c], 255.0) : 0.0;
-      }
-      if (a.count) a.count[o] = 1.0;
-      if (a.feat) {
-        // supervision.py:133-147 nearest-neighbour gather rule
-        const int64_t uu = (int64_t)floor(ddiv(dmul((double)u, (double)(a.fh - 1)), (double)max(a.H - 1, (int64_t)1)) + 0.5);
-        const int64_t vv = (int64_t)floor(ddiv(dmul((double)v, (double)(a.fw - 1)), (double)max(a.W - 1, (int64_t)1)) + 0.5);
-        const float* src = a.feat + f * a.fc * a.fh * a.fw + uu * a.fw + vv;
-        for (int64_t c = 0; c < a.fc; c++) a.ofeat[o * a.fc + c] = src[c * a.fh * a.fw];
-      }
-    } else {
-      // mean over the voxel's points in the head's frame, sequential in pid order
-      const int64_t i0 = head_pos[p];
-      const uint64_t key = a.skeys[i0];
-      a.key[o] = key;
-      double sm[3] = {0.0, 0.0, 0.0}, sc[3] = {0.0, 0.0, 0.0};
-      double cnt = 0.0;
-      for (int64_t i = i0; i < a.n && a.skeys[i] == key; i++) {
-        const int64_t q = a.svals[i];
-        if (q / HW != f) continue;
-        const int64_t r2 = q - f * HW;
-        const int64_t uq = r2 / a.W, vq = r2 - uq * a.W;
-        double mu[3];
-        backproject(a.rot + f * 9, a.trans + f * 3, a.cam, (double)uq, (double)vq, (double)a.depth[q], mu);
-        for (int c = 0; c < 3; c++) {
-          sm[c] = dadd(sm[c], mu[c]);
-          if (a.color) sc[c] = dadd(sc[c], ddiv((double)a.color[q * 3 + c], 255.0));
-        }
-        cnt = dadd(cnt, 1.0);
-      }
-      for (int c = 0; c < 3; c++) {
-        a.mu[o * 3 + c] = ddiv(sm[c], cnt);
-        a.col[o * 3 + c] = ddiv(sc[c], cnt);
-      }
-      if (a.count) a.count[o] = cnt;
-    }
-  }
+  const int64_t nnew = min((int64_t)*nnew_dev, capacity);
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < nnew; o += (int64_t)gridDim.x * blockDim.x)
+    emit_one(o, a.pid[o], head_pos, a);
 }
 
 __global__ void fill_u64_kernel(unsigned long long* p, int64_t n, unsigned long long v) {
@@ -1477,15 +1485,16 @@ DedupTable g_dedup[kDedupDevices];
 std::mutex g_dedup_mu;
 
 // Table size: 4x the previous batch's distinct voxels (load <= 1/4 when the
-// scene changes slowly), 2x the item count for the first batch and after an
-// overflow (`all`: every item could be a distinct voxel).
+// scene changes slowly), the item count for the first batch (front-end items
+// repeat each voxel several times), 2x the item count after an overflow
+// (`all`: every item could be a distinct voxel).
 cudaError_t dedup_table(int64_t nitems, bool all, cudaStream_t s, DedupTable** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= kDedupDevices) return cudaErrorInvalidDevice;
   DedupTable& t = g_dedup[dev];
-  const int64_t want = (all || t.last_nvox < 0) ? 2 * nitems : 4 * t.last_nvox;
+  const int64_t want = all ? 2 * nitems : (t.last_nvox < 0 ? nitems : 4 * t.last_nvox);
   int64_t cap = 1 << 20;
   while (cap < want) cap <<= 1;
   // keep the table when it is big enough but not over 4x too big (probes stay L2-resident)
@@ -1719,12 +1728,46 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     ProfScope prof("grid_emit", s);
     int32_t nnew = 0;
     unsigned long long nvox = 0;
+    EmitArgs ea;
+    ea.depth = in.depth;
+    ea.color = in.color;
+    ea.rot = in.rot;
+    ea.trans = in.trans;
+    ea.cam = cam;
+    ea.H = in.H;
+    ea.W = in.W;
+    ea.stride = in.stride;
+    ea.mode = in.mode;
+    ea.min_scale = in.min_scale;
+    ea.feat = in.feat;
+    ea.fc = in.fc;
+    ea.fh = in.fh;
+    ea.fw = in.fw;
+    ea.skeys = k0;
+    ea.svals = v0;
+    ea.n = nitems;   // mean mode only (always known there: no_sync is first-pick only)
+    ea.key = out.key;
+    ea.pid = out.pid;
+    ea.mu = out.mu;
+    ea.col = out.color;
+    ea.scale = out.scale;
+    ea.dep = out.depth;
+    ea.ofeat = out.feat;
+    ea.count = out.count;
     for (int attempt = 0;; attempt++) {
-      if ((e = launch_pdl(popc_kernel, dim3(grid_blocks(nwords, 256, sms)), dim3(256), 0, s,
-                          reinterpret_cast<const unsigned*>(flag), nwords, pos)) != cudaSuccess)
+      // exclusive popcount scan of the new-voxel bitmask, pixel-id list, emit:
+      // all queued before the read-back (outputs are bounded by the capacity)
+      if ((e = exclusive_scan<PopcWord>(reinterpret_cast<const PopcWord*>(flag), nwords, pos, ssum, grand, s)) !=
+          cudaSuccess)
         return e;
-      count_launches(1);
-      if ((e = exclusive_scan<int32_t>(pos, nwords, pos, ssum, grand, s)) != cudaSuccess) return e;
+      if ((e = launch_pdl(grid_pidlist_kernel, dim3(grid_blocks(nwords, 256, sms)), dim3(256), 0, s,
+                          reinterpret_cast<const unsigned*>(flag), (const int32_t*)pos, nwords, (int64_t)out.capacity,
+                          out.pid)) != cudaSuccess)
+        return e;
+      if ((e = launch_pdl(grid_emit_kernel, dim3(grid_blocks(out.capacity, 128, sms)), dim3(128), 0, s,
+                          (const int32_t*)head, (const int32_t*)grand, (int64_t)out.capacity, ea)) != cudaSuccess)
+        return e;
+      count_launches(2);
       int ovf = 0;
       if (no_sync && (e = cudaMemcpyAsync(hc, cnts, 24, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
       if ((e = cudaMemcpyAsync(&nnew, grand, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
@@ -1737,8 +1780,8 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
       }
       if (!ovf) break;
       // the table was too small for this batch's distinct voxels: pass 2 did not
-      // run (map untouched); reset the partly filled table and redo the batch on
-      // one sized for every item
+      // run (map untouched, no flags, nothing emitted); reset the partly filled
+      // table and redo the batch on one sized for every item
       if (attempt > 0) return cudaErrorUnknown;
       fill_u64_kernel<<<grid_blocks(2 * dd->cap, 256, sms), 256, 0, s>>>(dd->slots, 2 * dd->cap, ~0ull); count_launches(1);
       if ((e = dedup_table(nitems, true, s, &dd)) != cudaSuccess) return e;
@@ -1750,42 +1793,6 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     hs->count_ub += nnew;
     out.n_voxels = (int64_t)nvox;
     if (nnew > out.capacity) return cudaErrorInvalidValue;
-    EmitArgs a;
-    a.depth = in.depth;
-    a.color = in.color;
-    a.rot = in.rot;
-    a.trans = in.trans;
-    a.cam = cam;
-    a.H = in.H;
-    a.W = in.W;
-    a.stride = in.stride;
-    a.mode = in.mode;
-    a.min_scale = in.min_scale;
-    a.feat = in.feat;
-    a.fc = in.fc;
-    a.fh = in.fh;
-    a.fw = in.fw;
-    a.skeys = k0;
-    a.svals = v0;
-    a.n = nitems;
-    a.key = out.key;
-    a.pid = out.pid;
-    a.mu = out.mu;
-    a.col = out.color;
-    a.scale = out.scale;
-    a.dep = out.depth;
-    a.ofeat = out.feat;
-    a.count = out.count;
-    if ((e = launch_pdl(grid_pidlist_kernel, dim3(grid_blocks(nwords, 256, sms)), dim3(256), 0, s,
-                        reinterpret_cast<const unsigned*>(flag), (const int32_t*)pos, nwords, out.pid)) != cudaSuccess)
-      return e;
-    count_launches(1);
-    if (nnew > 0) {
-      if ((e = launch_pdl(grid_emit_kernel, dim3(grid_blocks(nnew, 128, sms)), dim3(128), 0, s, (const int32_t*)head,
-                          (int64_t)nnew, a)) != cudaSuccess)
-        return e;
-      count_launches(1);
-    }
   }
   return cudaGetLastError();
 }
