@@ -6,7 +6,8 @@
 //                        leaf/combine order as np.sum along a contiguous
 //                        axis, see common.cuh), then per mode
 //                          WEIGHTS  mixture_weights      (core.py:473-480)
-//                          ENTROPY  semantic_entropy     (thinker.py:185-191)
+//                          ENTROPY  semantic_entropy     (thinker.py:185-191),
+//                                   now cb_entropy_kernel (two passes)
 //                          VJP      softmax_vjp          (core.py:483-487)
 //                        Non-finite logits set a flag (the reference raises).
 //   cb_contrast_kernel : one warp per decoded feature row: pairwise L2 norm
@@ -88,6 +89,46 @@ cb_rows_kernel(const double* __restrict__ L, int64_t n, int64_t k, const double*
   }
 }
 
+// semantic_entropy in two passes over the logits (row max, then one fused
+// exp pass): with d = l - max, e = exp(d), S = sum e and T = sum e*d,
+//   H = -sum p log p = log S - T / S      (p = e / S, log p = d - log S),
+// so no per-element division, log or cached exponentials.  The sums are warp
+// reductions (not NumPy's pairwise order): the result differs from the
+// reference by a few ulps of log S (inside the 1e-13 relative tolerance).
+__global__ void __launch_bounds__(kCbWarps * 32)
+cb_entropy_kernel(const double* __restrict__ L, int64_t n, int64_t k, double* __restrict__ out_h, int* __restrict__ bad) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t r = (int64_t)blockIdx.x * kCbWarps + warp; r < n; r += (int64_t)gridDim.x * kCbWarps) {
+    const double* l = L + r * k;
+    double m = -__longlong_as_double(0x7ff0000000000000ll);
+    bool fin = true;
+#pragma unroll 8
+    for (int64_t i = lane; i < k; i += 32) {
+      const double v = __ldg(l + i);
+      fin = fin && isfinite(v);
+      m = fmax(m, v);
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
+    if (!__all_sync(FULL, fin)) {
+      if (lane == 0) atomicOr(bad, 1);
+      continue;
+    }
+    double S = 0.0, T = 0.0;
+#pragma unroll 4
+    for (int64_t i = lane; i < k; i += 32) {
+      const double d = dsub(__ldg(l + i), m);
+      const double e = exp(d);
+      S = dadd(S, e);
+      T = fma(e, d, T);
+    }
+    for (int o = 16; o; o >>= 1) {
+      S += __shfl_xor_sync(FULL, S, o);
+      T += __shfl_xor_sync(FULL, T, o);
+    }
+    if (lane == 0) out_h[r] = dsub(log(S), ddiv(T, S));
+  }
+}
+
 __global__ void __launch_bounds__(kCbWarps * 32)
 cb_contrast_kernel(const double* __restrict__ F, int64_t n, int64_t d, const double* __restrict__ Q, int64_t nq,
                    double tau, double eps, double* __restrict__ scores, SumPlan pd) {
@@ -149,17 +190,19 @@ cudaError_t launch_softmax_rows(const double* logits, int64_t n, int64_t k, int 
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(cb_rows_kernel<CB_WEIGHTS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbWarps * kCbCacheK * 8);
-    cudaFuncSetAttribute(cb_rows_kernel<CB_ENTROPY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbWarps * kCbCacheK * 8);
     cudaFuncSetAttribute(cb_rows_kernel<CB_VJP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbWarps * kCbCacheK * 8);
     attr_set = true;
   }
   const unsigned b = cb_blocks(n);
   const int T = kCbWarps * 32;
+  if (mode == CB_ENTROPY) {
+    cb_entropy_kernel<<<b, T, 0, s>>>(logits, n, k, out_h, bad);
+    count_launches(1);
+    return cudaGetLastError();
+  }
   switch (mode * 2 + (cache ? 1 : 0)) {
     case CB_WEIGHTS * 2 + 1: cb_rows_kernel<CB_WEIGHTS, true><<<b, T, smem, s>>>(logits, n, k, up, out, out_h, pk, bad); break;
     case CB_WEIGHTS * 2: cb_rows_kernel<CB_WEIGHTS, false><<<b, T, 0, s>>>(logits, n, k, up, out, out_h, pk, bad); break;
-    case CB_ENTROPY * 2 + 1: cb_rows_kernel<CB_ENTROPY, true><<<b, T, smem, s>>>(logits, n, k, up, out, out_h, pk, bad); break;
-    case CB_ENTROPY * 2: cb_rows_kernel<CB_ENTROPY, false><<<b, T, 0, s>>>(logits, n, k, up, out, out_h, pk, bad); break;
     case CB_VJP * 2 + 1: cb_rows_kernel<CB_VJP, true><<<b, T, smem, s>>>(logits, n, k, up, out, out_h, pk, bad); break;
     default: cb_rows_kernel<CB_VJP, false><<<b, T, 0, s>>>(logits, n, k, up, out, out_h, pk, bad);
   }
