@@ -254,6 +254,13 @@ typedef struct {
 
 XGS_API int xgs_grid_sample(const xgs_grid_frames* in, void* hashset, xgs_grid_result* out, void* ws,
                             size_t ws_bytes, void* stream);
+/* xgs_grid_sample with in->depth / in->color in (pinned) HOST memory: the
+ * frames are copied into the caller's device staging buffers depth_dev
+ * [F,H,W] / color_dev [F,H,W,3] inside the call, frame chunk by frame chunk on
+ * a library copy stream, each chunk's front-end launch overlapping the copy of
+ * the next; returns after the host frames were read. */
+XGS_API int xgs_grid_sample_h2d(const xgs_grid_frames* in, float* depth_dev, uint8_t* color_dev, void* hashset,
+                                xgs_grid_result* out, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------- SUPERVISION */
 

@@ -59,6 +59,7 @@ SIGNATURES = {
     "xgs_grid_workspace": (_sz, [_i64]),
     "xgs_radix_sort_pairs_u64": (_i32, [_vp, _vp, _i64, _i32, _vp, _sz, _vp]),
     "xgs_grid_sample": (_i32, [_vp, _vp, _vp, _vp, _sz, _vp]),
+    "xgs_grid_sample_h2d": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "xgs_sup_gather": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _i64,
                               _i64, _vp, _vp, _vp, _vp]),
     "xgs_sup_loss": (_i32, [_vp, _vp, _vp, _i64, _i64, _f64, _vp, _vp, _vp]),

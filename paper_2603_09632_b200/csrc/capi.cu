@@ -416,8 +416,8 @@ int xgs_radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, int bits
   return OK;
 }
 
-int xgs_grid_sample(const xgs_grid_frames* in, void* hashset, xgs_grid_result* out, void* ws, size_t ws_bytes,
-                    void* stream) {
+static int grid_sample_call(const xgs_grid_frames* in, void* hashset, xgs_grid_result* out, void* ws, size_t ws_bytes,
+                            void* stream, float* depth_dev, uint8_t* color_dev) {
   if (!in || !out || !hashset) return fail(INVALID_INPUT, "null argument");
   if (in->frames < 0 || in->height < 1 || in->width < 1) return fail(INVALID_INPUT, "bad frame shape");
   if (!(in->voxel > 0) || !(in->fx > 0) || !(in->fy > 0)) return fail(INVALID_INPUT, "voxel size and focal lengths must be positive");
@@ -434,8 +434,16 @@ int xgs_grid_sample(const xgs_grid_frames* in, void* hashset, xgs_grid_result* o
   gi.frames = in->frames;
   gi.H = in->height;
   gi.W = in->width;
-  gi.depth = in->depth;
-  gi.color = in->color;
+  if (depth_dev) {   // host frames, copied into the device staging buffers inside the call
+    if (in->color && !color_dev) return fail(INVALID_INPUT, "colour staging buffer missing");
+    gi.depth = depth_dev;
+    gi.color = in->color ? color_dev : nullptr;
+    gi.depth_host = in->depth;
+    gi.color_host = in->color;
+  } else {
+    gi.depth = in->depth;
+    gi.color = in->color;
+  }
   gi.rot = in->rot;
   gi.trans = in->trans;
   gi.fx = in->fx;
@@ -469,6 +477,20 @@ int xgs_grid_sample(const xgs_grid_frames* in, void* hashset, xgs_grid_result* o
   if (e == cudaErrorInvalidValue && go.n_new > go.capacity) return fail(INVALID_INPUT, "output capacity too small");
   if (e != cudaSuccess) return cuda_fail(e, "xgs_grid_sample");
   return OK;
+}
+
+int xgs_grid_sample(const xgs_grid_frames* in, void* hashset, xgs_grid_result* out, void* ws, size_t ws_bytes,
+                    void* stream) {
+  return grid_sample_call(in, hashset, out, ws, ws_bytes, stream, nullptr, nullptr);
+}
+
+// Same, with in->depth / in->color in (pinned) host memory: copied into
+// depth_dev [F,H,W] / color_dev [F,H,W,3] frame chunk by frame chunk, each
+// chunk's front-end launch overlapping the next chunk's copy.
+int xgs_grid_sample_h2d(const xgs_grid_frames* in, float* depth_dev, uint8_t* color_dev, void* hashset,
+                        xgs_grid_result* out, void* ws, size_t ws_bytes, void* stream) {
+  if (!depth_dev) return fail(INVALID_INPUT, "null depth staging buffer");
+  return grid_sample_call(in, hashset, out, ws, ws_bytes, stream, depth_dev, color_dev);
 }
 
 // ---------------------------------------------------------------- SUPERVISION

@@ -336,7 +336,8 @@ __device__ __forceinline__ uint64_t key_exact(const double* R, const double* T, 
 __global__ void __launch_bounds__(384, 2)
 grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int stride, const double* __restrict__ rot,
                   const double* __restrict__ trans, Cam cam, CamF cf, uint64_t* __restrict__ kout,
-                  uint32_t* __restrict__ vout, int* bbox, unsigned long long* cnts, int32_t* __restrict__ block_count) {
+                  uint32_t* __restrict__ vout, int* bbox, unsigned long long* cnts, int32_t* __restrict__ block_count,
+                  unsigned bid0) {
   constexpr int NR = FK_ROWS;
   __shared__ uint64_t s_last[NR][32];
   __shared__ uint32_t s_wsum[NR][32];
@@ -349,7 +350,7 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
   uint64_t* sk = reinterpret_cast<uint64_t*>(front_smem);
   uint32_t* sv = reinterpret_cast<uint32_t*>(front_smem + (size_t)NR * W * 8);
   if (threadIdx.x == 0) {
-    s_bid = blockIdx.x;
+    s_bid = bid0 + blockIdx.x;   // bid0: first block of this launch (frame-chunked launches)
     s_npend = 0;
   }
   if (threadIdx.x < 6) s_box[threadIdx.x] = threadIdx.x < 3 ? INT_MAX : INT_MIN;
@@ -1473,6 +1474,34 @@ dd_scan_kernel(unsigned long long* slots, int64_t cap, const int* overflow, unsi
   }
 }
 
+// copy stream + events of the host-frame pipeline (per device)
+constexpr int kHostChunks = 8;
+struct HostCopy {
+  bool ready = false;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t start = nullptr, done = nullptr, chunk[kHostChunks];
+};
+HostCopy g_hostcopy[16];
+std::mutex g_hostcopy_mu;
+
+cudaError_t host_copy_res(HostCopy** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
+  HostCopy& h = g_hostcopy[dev];
+  if (!h.ready) {
+    if ((e = cudaStreamCreateWithFlags(&h.cs, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&h.start, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&h.done, cudaEventDisableTiming)) != cudaSuccess) return e;
+    for (int i = 0; i < kHostChunks; i++)
+      if ((e = cudaEventCreateWithFlags(&h.chunk[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+    h.ready = true;
+  }
+  *out = &h;
+  return cudaSuccess;
+}
+
 // per-device batch table (library-owned scratch, empty between batches)
 struct DedupTable {
   unsigned long long* slots = nullptr;   // 2 x cap words
@@ -1571,6 +1600,45 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   bool fused = false;                  // fused front end (per-block slots, gathered by the rekey pass)
   int64_t fblocks = 0;
   const int64_t nwords = (npix + 31) / 32;
+  // Host frames (xgs_grid_sample_h2d): depth is copied frame chunk by frame
+  // chunk on a copy stream and each chunk's front-end launch waits only for
+  // its own chunk, so the copies of later frames overlap the earlier frames'
+  // keys; the colour follows and is waited for before the emit.
+  const bool host_frames = in.depth_host != nullptr;
+  HostCopy* hcp = nullptr;
+  std::unique_lock<std::mutex> hc_lock(g_hostcopy_mu, std::defer_lock);
+  struct CopyDone {   // the call returns only after the host frames were read
+    HostCopy*& h;
+    ~CopyDone() {
+      if (h) cudaEventSynchronize(h->done);
+    }
+  } copy_done{hcp};
+  if (host_frames) {
+    hc_lock.lock();
+    if ((e = host_copy_res(&hcp)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(hcp->start, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(hcp->cs, hcp->start, 0)) != cudaSuccess) return e;
+  }
+  const int64_t fpx = in.H * in.W;
+  const int64_t fper = host_frames ? (in.frames + kHostChunks - 1) / kHostChunks : in.frames;
+  const int nchunk = (int)((in.frames + fper - 1) / fper);   // every chunk non-empty
+  auto copy_depth = [&](int c) -> cudaError_t {
+    const int64_t f0 = c * fper, f1 = f0 + fper < in.frames ? f0 + fper : in.frames;
+    cudaError_t ce = cudaMemcpyAsync(const_cast<float*>(in.depth) + f0 * fpx, in.depth_host + f0 * fpx,
+                                     sizeof(float) * (size_t)((f1 - f0) * fpx), cudaMemcpyHostToDevice, hcp->cs);
+    if (ce == cudaSuccess) ce = cudaEventRecord(hcp->chunk[c], hcp->cs);
+    return ce;
+  };
+  if (host_frames) {
+    for (int c = 0; c < nchunk; c++)
+      if ((e = copy_depth(c)) != cudaSuccess) return e;
+    if (in.color && in.color_host) {
+      if ((e = cudaMemcpyAsync(const_cast<uint8_t*>(in.color), in.color_host, (size_t)(in.frames * fpx * 3),
+                               cudaMemcpyHostToDevice, hcp->cs)) != cudaSuccess)
+        return e;
+    }
+    if ((e = cudaEventRecord(hcp->done, hcp->cs)) != cudaSuccess) return e;
+  }
   {
     ProfScope prof("grid_keys", s);
     init_bbox_kernel<<<1, 32, 0, s>>>(bbox, cnts); count_launches(1);
@@ -1578,13 +1646,24 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     const bool vec4 = (in.W % 4 == 0) && (reinterpret_cast<uintptr_t>(in.depth) % 16 == 0);
     fblocks = in.frames * ((in.H + FK_ROWS - 1) / FK_ROWS);
     fused = compact && vec4 && in.W <= 2048 && fblocks <= w.lb_entries;
+    if (host_frames && !fused) {   // the two-kernel front end reads every frame: wait for all of them
+      if ((e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;
+    }
     if (fused) {
       const CamF cf{(float)in.cx, (float)in.cy, (float)(1.0 / in.fx), (float)(1.0 / in.fy), (float)(1.0 / in.voxel)};
       const unsigned nt = (unsigned)((in.W / 4 + 31) / 32 * 32);
       const size_t fsmem = (size_t)FK_ROWS * in.W * 12;
       if ((e = front_init()) != cudaSuccess) return e;
-      grid_front_kernel<<<(unsigned)fblocks, nt, fsmem, s>>>(in.depth, in.H, in.W, in.stride, in.rot, in.trans, cam, cf,
-                                                              k0, v0, bbox, cnts, block_count); count_launches(1);
+      const int64_t rbf = (in.H + FK_ROWS - 1) / FK_ROWS;
+      for (int c = 0; c < nchunk; c++) {
+        const int64_t f0 = c * fper, f1 = f0 + fper < in.frames ? f0 + fper : in.frames;
+        if (f1 <= f0) break;
+        if (host_frames && (e = cudaStreamWaitEvent(s, hcp->chunk[c], 0)) != cudaSuccess) return e;
+        grid_front_kernel<<<(unsigned)((f1 - f0) * rbf), nt, fsmem, s>>>(in.depth, in.H, in.W, in.stride, in.rot,
+                                                                          in.trans, cam, cf, k0, v0, bbox, cnts,
+                                                                          block_count, (unsigned)(f0 * rbf));
+        count_launches(1);
+      }
     } else {
     grid_keys_kernel<<<grid_blocks(vec4 ? npix / 4 : npix, 256, sms), 256, 0, s>>>(
         in.depth, npix, in.H, in.W, in.stride, in.rot, in.trans, cam, compact ? k1 : k0, compact ? nullptr : v0,
@@ -1726,6 +1805,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   }
   {
     ProfScope prof("grid_emit", s);
+    if (host_frames && (e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;   // colour
     int32_t nnew = 0;
     unsigned long long nvox = 0;
     EmitArgs ea;

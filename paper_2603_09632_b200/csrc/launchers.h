@@ -131,6 +131,9 @@ struct GridIn {
   int64_t frames, H, W;
   const float* depth;
   const uint8_t* color;
+  // host frames (xgs_grid_sample_h2d): copied into depth / color inside the call
+  const float* depth_host = nullptr;
+  const uint8_t* color_host = nullptr;
   const double* rot;
   const double* trans;
   double fx, fy, cx, cy, voxel;

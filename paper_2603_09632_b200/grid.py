@@ -169,20 +169,37 @@ class GridSampler:
         self.min_scale = float(min_scale)
         self.occupied = occupied if occupied is not None else VoxelHashSet(capacity)
 
+    @staticmethod
+    def _pinned(a, dtype):
+        t = nat.torch()
+        return (isinstance(a, t.Tensor) and a.device.type == "cpu" and a.is_pinned() and a.dtype == dtype
+                and a.is_contiguous())
+
     def sample(self, depth, poses, color=None, features=None) -> GridSampleResult:
         t = nat.require_cuda()
-        d = _dev(depth, t.float32)
+        # pinned host frames go to the device inside the native call (frame
+        # chunks copied while earlier frames' keys are computed)
+        host = self._pinned(depth, t.float32) and (color is None or self._pinned(color, t.uint8))
+        d = depth if host else _dev(depth, t.float32)
         if d.dim() == 2:
             d = d.unsqueeze(0)
         if d.dim() != 3:
             raise InvalidInputError("depth must be (H, W) or (F, H, W)")
         F, H, W = (int(v) for v in d.shape)
         R, tr = _poses(poses, F)
-        col = _dev(color, t.uint8)
+        col = color if host else _dev(color, t.uint8)
         if col is not None:
             col = col.reshape(F, H, W, 3) if col.dim() != 4 else col
             if tuple(col.shape) != (F, H, W, 3):
                 raise InvalidInputError("color must be (F, H, W, 3) uint8")
+        stage = None
+        if host:   # grow-only device staging buffers
+            key = (F, H, W, col is not None)
+            stage = getattr(self, "_stage", None)
+            if stage is None or stage[0] != key:
+                stage = (key, t.empty((F, H, W), dtype=t.float32, device="cuda"),
+                         t.empty((F, H, W, 3), dtype=t.uint8, device="cuda") if col is not None else None)
+                self._stage = stage
         feat = _dev(features, t.float32) if features is not None else None
         if feat is not None and feat.dim() == 3:
             feat = feat.unsqueeze(0)
@@ -203,8 +220,13 @@ class GridSampler:
         res = nat.GridResult(cap, b, b + 8 * cap, b + 16 * cap, b + 40 * cap, b + 64 * cap, b + 72 * cap,
                              ofeat.data_ptr() if ofeat is not None else None, b + 80 * cap, 0, 0, 0, 0, 0)
         ws = nat.workspace("grid", nat.lib().xgs_grid_workspace(F * H * W))
-        nat.call("xgs_grid_sample", ctypes.byref(fr), self.occupied._h, ctypes.byref(res), nat.ptr(ws), ws.numel(),
-                 nat.stream_ptr())
+        if host:
+            nat.call("xgs_grid_sample_h2d", ctypes.byref(fr), stage[1].data_ptr(),
+                     stage[2].data_ptr() if stage[2] is not None else None, self.occupied._h, ctypes.byref(res),
+                     nat.ptr(ws), ws.numel(), nat.stream_ptr())
+        else:
+            nat.call("xgs_grid_sample", ctypes.byref(fr), self.occupied._h, ctypes.byref(res), nat.ptr(ws),
+                     ws.numel(), nat.stream_ptr())
         n = int(res.n_new)
         return GridSampleResult(key=flat[:n].view(t.int64), pid=flat[cap:cap + n].view(t.int64),
                                 mu=flat[2 * cap:2 * cap + 3 * n].view(n, 3), color=flat[5 * cap:5 * cap + 3 * n].view(n, 3),

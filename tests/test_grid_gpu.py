@@ -162,6 +162,29 @@ def test_grid_hash_table_overflow_retry(xs, map_capacity):
     torch.cuda.synchronize()
 
 
+@pytest.mark.parametrize("W,mode,with_color", [(128, "first", True), (128, "first", False), (130, "first", True),
+                                                (128, "mean", True)])
+def test_grid_pinned_host_frames_match_device(xs, W, mode, with_color):
+    """Pinned host frames (xgs_grid_sample_h2d: frame-chunked copies inside the
+    call overlapping the front end) give the same result as device frames."""
+    import torch
+    grid, _, synth = xs
+    frames, intr4 = _scene(synth, 9, 64, W, 11, spheres=True)
+    D = torch.from_numpy(np.stack([f[0] for f in frames]))
+    C = torch.from_numpy(np.stack([f[1] for f in frames]))
+    R = np.stack([f[2] for f in frames])
+    T = np.stack([f[3] for f in frames])
+    outs = []
+    for pinned in (False, True):
+        gs = grid.GridSampler(intr4, 0.02, mode=mode)
+        d = D.pin_memory() if pinned else D.cuda()
+        c = (C.pin_memory() if pinned else C.cuda()) if with_color else None
+        outs.append(gs.sample(d, (R, T), c).to_numpy())
+    for name in ("key", "pid", "mu", "color", "scale", "depth", "count"):
+        assert np.array_equal(outs[0][name], outs[1][name]), name
+    assert outs[0]["n_valid"] == outs[1]["n_valid"] and len(outs[0]["pid"]) > 0
+
+
 def test_grid_incremental_and_batching(xs):
     grid, _, synth = xs
     frames, intr4 = _scene(synth, 4, 64, 80, 4)
