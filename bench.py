@@ -380,7 +380,8 @@ def run_c5(torch, iters, device):
     vq = DataParallelVQ((E0, torch.zeros(C5_K, dtype=torch.float64, device=device),
                          torch.zeros(C5_K, C5_D, dtype=torch.float64, device=device)), cfg,
                         np.random.default_rng(41), CudaBackend(C5_K, C5_D, 0.99, 1e-5))
-    vq.step(x, [C5_ROWS])
+    for _ in range(max(1, int(os.environ.get("XGS_C5_WARM", "1")))):   # profiling aid: longer warm-up
+        vq.step(x, [C5_ROWS])
     torch.cuda.synchronize()
     nat.profile_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
