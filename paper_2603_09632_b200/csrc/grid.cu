@@ -317,6 +317,8 @@ compact_keys_kernel(const uint64_t* __restrict__ kin, int64_t n, int64_t W, uint
 // path (backproject + floor_div), bit-identical to the reference.
 constexpr int FK_ROWS = 4;
 constexpr int kFrontPend = 1024;   // per-block queue of pixels for the exact path
+// thread t covers columns 4t..4t+3 (W <= 4 * kFrontMaxThreads); 3 blocks per SM
+constexpr int kFrontMaxThreads = 320;
 
 struct CamF {
   float cx, cy, rfx, rfy, inv_voxel;
@@ -333,7 +335,7 @@ __device__ __forceinline__ uint64_t key_exact(const double* R, const double* T, 
   return ((uint64_t)q[0] << 42) | ((uint64_t)q[1] << 21) | (uint64_t)q[2];
 }
 
-__global__ void __launch_bounds__(384, 2)
+__global__ void __launch_bounds__(kFrontMaxThreads, 3)
 grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int stride, const double* __restrict__ rot,
                   const double* __restrict__ trans, Cam cam, CamF cf, uint64_t* __restrict__ kout,
                   uint32_t* __restrict__ vout, int* bbox, unsigned long long* cnts, int32_t* __restrict__ block_count,
@@ -1645,7 +1647,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     cudaMemsetAsync(cnts + 1, 0, 40, s);
     const bool vec4 = (in.W % 4 == 0) && (reinterpret_cast<uintptr_t>(in.depth) % 16 == 0);
     fblocks = in.frames * ((in.H + FK_ROWS - 1) / FK_ROWS);
-    fused = compact && vec4 && in.W <= 2048 && fblocks <= w.lb_entries;
+    fused = compact && vec4 && in.W <= 4 * kFrontMaxThreads && fblocks <= w.lb_entries;
     if (host_frames && !fused) {   // the two-kernel front end reads every frame: wait for all of them
       if ((e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;
     }
