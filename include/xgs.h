@@ -190,6 +190,14 @@ XGS_API int xgs_contrast_scores(const double* feats, int64_t n, int64_t d, const
  * "stable"), thinker.py:171, :202) through xgs_radix_sort_pairs_u64 with 64
  * key bits; -0.0 ties with +0.0 as in NumPy. */
 XGS_API int xgs_desc_order_keys(const double* v, int64_t n, uint64_t* keys, uint32_t* idx, void* stream);
+/* The first m indices of np.argsort(-v, kind="stable") (sample_tokens,
+ * thinker.py:194-206) without ordering all n: histogram of the descending
+ * keys' top 16 bits, the bucket of the m-th key, an order-preserving
+ * compaction of the keys up to it and a stable 64-bit radix sort of those.
+ * out: m int64 (device).  One host synchronisation (the candidate count). */
+XGS_API size_t xgs_desc_top_m_workspace(int64_t n);
+XGS_API int xgs_desc_top_m(const double* v, int64_t n, int64_t m, int64_t* out, void* ws, size_t ws_bytes,
+                           void* stream);
 
 /* ------------------------------------------------------------- GRID */
 

@@ -72,6 +72,8 @@ SIGNATURES = {
     "xgs_raster_free": (_i32, [_vp]),
     "xgs_contrast_scores": (_i32, [_vp, _i64, _i64, _vp, _i64, _f64, _f64, _vp, _vp]),
     "xgs_desc_order_keys": (_i32, [_vp, _i64, _vp, _vp, _vp]),
+    "xgs_desc_top_m_workspace": (_sz, [_i64]),
+    "xgs_desc_top_m": (_i32, [_vp, _i64, _i64, _vp, _vp, _sz, _vp]),
 }
 
 

@@ -568,6 +568,17 @@ int xgs_desc_order_keys(const double* v, int64_t n, uint64_t* keys, uint32_t* id
   return OK;
 }
 
+// First m entries of np.argsort(-v, kind="stable") (thinker.py:202) without
+// sorting all n: top-16-bit bucket select + stable sort of the candidates.
+size_t xgs_desc_top_m_workspace(int64_t n) { return topm_workspace_bytes(n < 0 ? 0 : n); }
+int xgs_desc_top_m(const double* v, int64_t n, int64_t m, int64_t* out, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || n > 0x7fffffffll || m < 0 || m > n) return fail(INVALID_INPUT, "bad length");
+  if (n && m && (!v || !out)) return fail(INVALID_INPUT, "null buffer");
+  if (ws_bytes < topm_workspace_bytes(n)) return fail(INVALID_INPUT, "workspace too small");
+  cudaError_t e = launch_desc_top_m(v, n, m, out, ws, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_desc_top_m");
+  return OK;
+}
 
 // ------------------------------------------------------- lattice rasterizer
 

@@ -173,6 +173,84 @@ __global__ void cb_desc_keys_kernel(const double* __restrict__ v, int64_t n, uin
   }
 }
 
+// Top-M of a stable descending order (np.argsort(-v, kind="stable")[:M]):
+// histogram of the keys' top 16 bits, the bucket holding the M-th key, an
+// order-preserving compaction of every key up to that bucket, and the full
+// 64-bit stable radix sort of only those (ties keep ascending index order).
+constexpr int kTopBits = 16;
+constexpr int kTopBuckets = 1 << kTopBits;
+
+__global__ void topm_hist_kernel(const uint64_t* __restrict__ keys, int64_t n, int32_t* __restrict__ hist) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - threadIdx.x < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int bkt = i < n ? (int)(keys[i] >> (64 - kTopBits)) : -1;
+    const unsigned peers = __match_any_sync(FULL, bkt);
+    if (bkt >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(hist + bkt, __popc(peers));
+  }
+}
+
+// one CTA: the smallest bucket b with (#keys in buckets <= b) >= m; out[0] = b,
+// out[1] = #keys in buckets <= b
+__global__ void __launch_bounds__(1024) topm_pick_kernel(const int32_t* __restrict__ hist, int64_t m, int32_t* out) {
+  __shared__ int32_t wsum[32];
+  constexpr int PER = kTopBuckets / 1024;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  int32_t c[PER], s = 0;
+#pragma unroll
+  for (int j = 0; j < PER; j++) {
+    c[j] = hist[t * PER + j];
+    s += c[j];
+  }
+  int32_t x = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int32_t w = wsum[lane];
+    int32_t wx = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, wx, o);
+      if (lane >= o) wx += y;
+    }
+    wsum[lane] = wx - w;
+  }
+  __syncthreads();
+  int64_t run = (int64_t)wsum[warp] + x - s;   // keys in buckets before this thread's
+#pragma unroll
+  for (int j = 0; j < PER; j++) {
+    if (run < m && run + c[j] >= m) {   // exactly one thread / bucket satisfies this
+      out[0] = t * PER + j;
+      out[1] = (int32_t)(run + c[j]);
+    }
+    run += c[j];
+  }
+}
+
+__global__ void topm_flag_kernel(const uint64_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ pick,
+                                 int32_t* __restrict__ flag) {
+  const uint64_t b = (uint64_t)pick[0];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = (keys[i] >> (64 - kTopBits)) <= b ? 1 : 0;
+}
+
+__global__ void topm_compact_kernel(const uint64_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ flag,
+                                    const int32_t* __restrict__ pos, uint64_t* __restrict__ ck,
+                                    uint32_t* __restrict__ cv) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (flag[i]) {
+      ck[pos[i]] = keys[i];
+      cv[pos[i]] = (uint32_t)i;
+    }
+}
+
+__global__ void topm_out_kernel(const uint32_t* __restrict__ cv, int64_t m, int64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = cv[i];
+}
+
 unsigned cb_blocks(int64_t rows) {
   int64_t b = (rows + kCbWarps - 1) / kCbWarps;
   if (b > 148 * 32) b = 148 * 32;
@@ -215,6 +293,49 @@ cudaError_t launch_contrast(const double* F, int64_t n, int64_t d, const double*
   if (n == 0) return cudaSuccess;
   ProfScope prof("cb_contrast", s);
   cb_contrast_kernel<<<cb_blocks(n), kCbWarps * 32, 0, s>>>(F, n, d, Q, nq, tau, eps, scores, pd); count_launches(1);
+  return cudaGetLastError();
+}
+
+// workspace: keys (8n) + flags (4n) + positions (4n) + compact keys / ids
+// (12n) + histogram + the radix sort's own workspace for n items
+size_t topm_workspace_bytes(int64_t n) {
+  const size_t nn = (size_t)(n > 0 ? n : 1);
+  return align_up(8 * nn, 256) + align_up(4 * nn, 256) * 2 + align_up(8 * nn, 256) + align_up(4 * nn, 256) +
+         align_up(4 * (size_t)kTopBuckets, 256) + 256 + grid_workspace_bytes(n);
+}
+
+cudaError_t launch_desc_top_m(const double* v, int64_t n, int64_t m, int64_t* out, void* ws, cudaStream_t s) {
+  if (n == 0 || m == 0) return cudaSuccess;
+  const size_t nn = (size_t)n;
+  char* p = static_cast<char*>(ws);
+  auto take = [&](size_t b) { char* r = p; p += align_up(b, 256); return r; };
+  uint64_t* keys = reinterpret_cast<uint64_t*>(take(8 * nn));
+  int32_t* flag = reinterpret_cast<int32_t*>(take(4 * nn));
+  int32_t* pos = reinterpret_cast<int32_t*>(take(4 * nn));
+  uint64_t* ck = reinterpret_cast<uint64_t*>(take(8 * nn));
+  uint32_t* cv = reinterpret_cast<uint32_t*>(take(4 * nn));
+  int32_t* hist = reinterpret_cast<int32_t*>(take(4 * (size_t)kTopBuckets));
+  int32_t* misc = reinterpret_cast<int32_t*>(take(256));   // [0] bucket, [1] selected count, [2] scan total
+  void* sws = p;
+  const size_t sws_bytes = grid_workspace_bytes(n);
+  cudaError_t e;
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  cb_desc_keys_kernel<<<(unsigned)b, 256, 0, s>>>(v, n, keys, cv);
+  if ((e = cudaMemsetAsync(hist, 0, 4 * (size_t)kTopBuckets, s)) != cudaSuccess) return e;
+  topm_hist_kernel<<<(unsigned)b, 256, 0, s>>>(keys, n, hist);
+  topm_pick_kernel<<<1, 1024, 0, s>>>(hist, m, misc);
+  topm_flag_kernel<<<(unsigned)b, 256, 0, s>>>(keys, n, misc, flag);
+  count_launches(4);
+  if ((e = exclusive_scan_i32(flag, n, pos, reinterpret_cast<int32_t*>(sws), misc + 2, s)) != cudaSuccess) return e;
+  topm_compact_kernel<<<(unsigned)b, 256, 0, s>>>(keys, n, flag, pos, ck, cv);
+  count_launches(1);
+  int32_t nsel = 0;
+  if ((e = cudaMemcpyAsync(&nsel, misc + 1, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  if ((e = radix_sort_pairs(ck, cv, nsel, 64, sws, sws_bytes, s)) != cudaSuccess) return e;
+  topm_out_kernel<<<(unsigned)((m + 255) / 256 < 148 * 16 ? (m + 255) / 256 : 148 * 16), 256, 0, s>>>(cv, m, out);
+  count_launches(1);
   return cudaGetLastError();
 }
 

@@ -200,6 +200,8 @@ cudaError_t launch_softmax_rows(const double* logits, int64_t n, int64_t k, int 
                                 double* out_h, const SumPlan& pk, int* bad, cudaStream_t s);
 cudaError_t launch_contrast(const double* F, int64_t n, int64_t d, const double* Q, int64_t nq, double tau, double eps,
                             double* scores, const SumPlan& pd, cudaStream_t s);
+size_t topm_workspace_bytes(int64_t n);
+cudaError_t launch_desc_top_m(const double* v, int64_t n, int64_t m, int64_t* out, void* ws, cudaStream_t s);
 cudaError_t launch_desc_keys(const double* v, int64_t n, uint64_t* keys, uint32_t* idx, cudaStream_t s);
 
 }  // namespace xgs

@@ -129,3 +129,27 @@ def test_gpu_large_matches_oracle(cuda):
     ts = xt.sample_tokens(type("F", (), {"logits": Ld, "__len__": lambda self: n})(), cb, 1000)
     o, Hs, _ = ot.sample_tokens(L, E, 1000)
     assert np.array_equal(ts.indices.cpu().numpy(), o)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["normal", "ties", "all_equal", "signed_zero", "wide_range"])
+@pytest.mark.parametrize("M", [1, 37, 2500])
+def test_desc_top_m_matches_stable_argsort(cuda, case, M):
+    """xgs_desc_top_m (bucket select + stable sort of the candidates) ==
+    np.argsort(-v, kind="stable")[:M], ties to the lower index."""
+    import torch
+    from paper_2603_09632_b200 import thinker
+    rng = np.random.default_rng(M)
+    n = 20_000
+    if case == "normal":
+        v = rng.normal(size=n)
+    elif case == "ties":
+        v = rng.integers(0, 7, n).astype(np.float64)
+    elif case == "all_equal":
+        v = np.full(n, 0.25)
+    elif case == "signed_zero":
+        v = np.where(rng.random(n) < 0.5, 0.0, -0.0) * (rng.random(n) < 0.9) + (rng.random(n) < 0.001)
+    else:
+        v = rng.normal(size=n) * 10.0 ** rng.integers(-30, 30, n)
+    got = thinker._desc_top_m(torch.from_numpy(v).cuda(), M).cpu().numpy()
+    assert np.array_equal(got, np.argsort(-v, kind="stable")[:M])
