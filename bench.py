@@ -522,16 +522,20 @@ def run_consumers(torch, iters, cpu=True):
         return e0.elapsed_time(e1) / reps
 
     pk, _ = peaks()
+    clk = ClockSampler(torch.cuda.current_device())
+    clk.start()
     ms_h = timed(lambda: xt.semantic_entropy(L), iters)
     ent_bytes = n * K * 8 + n * 8
     ms_tok = timed(lambda: xt.sample_tokens(field, cb, M), max(1, iters // 2))
     ms_rel = timed(lambda: xt.relevance_per_gaussian(field, cb, q), 1)
+    clocks = clk.stop()
     out = {"gaussians": n, "K": K, "D": D,
            "semantic_entropy": {"ms": ms_h, "GB_per_s": ent_bytes / (ms_h * 1e-3) / 1e9,
                                 "hbm_frac": ent_bytes / (ms_h * 1e-3) / 1e9 / pk["hbm_gbs"],
                                 "algorithmic_bytes": ent_bytes},
            "sample_tokens": {"ms": ms_tok, "M": M},
            "relevance_per_gaussian": {"ms": ms_rel, "decode_gemm_fp64_TFLOPs": 2.0 * n * K * D / (ms_rel * 1e-3) / 1e12},
+           "clocks": clocks,
            "workload": "2^21 Gaussians x K=512 fp64 logits (C4 map size), D=768 codebook, M=4096 tokens; "
                        "synthetic N(0, 2^2) logits"}
     if cpu:

@@ -160,7 +160,7 @@ class CudaBackend:
         from . import _native as nat
         self.nat = nat
         self.t = nat.require_cuda()
-        self._h2d, self._pending_host = {}, None
+        self._h2d, self._pending_host, self._packed = {}, None, None
         self.K, self.D, self.lam, self.eps = K, D, lam, eps
 
     def int_tensor(self, v):
@@ -198,11 +198,14 @@ class CudaBackend:
                  nat.stream_ptr())
 
     def local_stats(self, state, shard, cfg):
-        from .core import Codebook
-        from .vq import _accumulate_dev, _assign_accumulate_dev, _exact_dev, _rows, all_pass_provable
+        from .vq import _assign_accumulate_dev, _exact_dev, _rows, all_pass_provable
         t, nat = self.t, self.nat
         E = state[0]
-        packed = t.empty(self.K * self.D + self.K, dtype=t.float64, device="cuda")
+        # the packed [sums | counts] buffer is consumed by the EMA (and the
+        # all-reduce) on the same stream before the next step rewrites it
+        packed = self._packed
+        if packed is None or packed.device != E.device:
+            packed = self._packed = t.empty(self.K * self.D + self.K, dtype=t.float64, device=E.device)
         sums = packed[:self.K * self.D].view(self.K, self.D)
         counts = packed[self.K * self.D:]
         n = self.rows(shard)

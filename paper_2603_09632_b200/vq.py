@@ -161,6 +161,20 @@ def _accumulate_dev(xt, dt, n, d, ldx, codes, mask, K):
     return counts, sums
 
 
+_STEP_WS = {}
+
+
+def _step_ws_bytes(n, K, d, dt, ldx):
+    """xgs_vq_step_workspace, memoised (a pure function of the shape; called every step)."""
+    key = (n, K, d, dt, ldx)
+    b = _STEP_WS.get(key)
+    if b is None:
+        if len(_STEP_WS) > 64:
+            _STEP_WS.clear()
+        b = _STEP_WS[key] = int(nat.lib().xgs_vq_step_workspace(n, K, d, dt, ldx))
+    return b
+
+
 def _assign_accumulate_dev(xt, dt, n, d, ldx, E, K, counts=None, sums=None, x_host=None):
     """assign_batch + accumulate(batch) for an all-pass mask (vq.py:206) in one
     row-chunk-pipelined native call; bit-identical to _assign_dev followed by
@@ -172,7 +186,7 @@ def _assign_accumulate_dev(xt, dt, n, d, ldx, E, K, counts=None, sums=None, x_ho
         counts = t.empty(K, dtype=t.float64, device="cuda")
     if sums is None:
         sums = t.empty((K, d), dtype=t.float64, device="cuda")
-    ws = nat.workspace("step", nat.lib().xgs_vq_step_workspace(n, K, d, dt, ldx))
+    ws = nat.workspace("step", _step_ws_bytes(n, K, d, dt, ldx))
     nat.call("xgs_vq_assign_accumulate_h2d", nat.ptr(x_host), nat.ptr(xt), dt, n, d, ldx, nat.ptr(E), K,
              nat.ptr(codes), nat.ptr(counts), nat.ptr(sums), nat.ptr(ws), ws.numel(), None, nat.stream_ptr())
     return codes, counts, sums
