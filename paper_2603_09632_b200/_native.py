@@ -170,7 +170,10 @@ def require_cuda():
 
 
 def stream_ptr():
-    return ctypes.c_void_p(torch().cuda.current_stream().cuda_stream)
+    """The current CUDA stream of the current device (raw handle; the torch.cuda
+    Stream object costs ~6 us per query, this ~1 us -- it is on every call)."""
+    C = torch()._C
+    return ctypes.c_void_p(C._cuda_getCurrentRawStream(C._cuda_getDevice()))
 
 
 def ptr(t):
