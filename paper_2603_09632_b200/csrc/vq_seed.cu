@@ -8,11 +8,13 @@
 // maximum is 0 (fewer distinct rows than K; min_d stays all-zero from then on,
 // so every later seed cycles too).
 //
-// One launch per seed, all on the caller's stream: seed_step_kernel(t) reads
-// seed t-1 from device memory, folds its distances into min_d (one warp per
-// row, exact fp64 pairwise sums), reduces a per-block (max, index) and the
-// last block to finish reduces the block partials in index order and writes
-// seed t.  The K-1 launches queue back to back with no synchronisation.
+// seed_persistent_kernel runs all K-1 passes in one cooperative launch (one
+// grid barrier per seed); where a cooperative launch of that size is not
+// possible, seed_step_kernel(t) runs one launch per seed: it reads seed t-1
+// from device memory, folds its distances into min_d (one warp per row, exact
+// fp64 pairwise sums), reduces a per-block (max, index) and the last block to
+// finish reduces the block partials and writes seed t.  Either way nothing
+// synchronises with the host.
 #include "launchers.h"
 
 namespace xgs {
@@ -137,6 +139,91 @@ seed_step_kernel(const X* __restrict__ x, int64_t n, int64_t d, int64_t ldx, int
   }
 }
 
+// All K-1 passes in one cooperative launch (every block co-resident): per
+// pass the blocks fold their rows' distances into min_d, publish a block
+// (max, index) into one of two partial buffers, meet at a counter barrier,
+// and then each block reduces all partials itself (same order, same result in
+// every block), so one grid barrier per seed.
+// 16 warps per block and at most 2 blocks per SM: few blocks meet at each
+// barrier (one counter atomic each) while enough warps share the rows.
+constexpr int kPersistWarps = 16;
+
+template <typename X>
+__global__ void __launch_bounds__(kPersistWarps * 32)
+seed_persistent_kernel(const X* __restrict__ x, int64_t n, int64_t d, int64_t ldx, int64_t k,
+                       int64_t* __restrict__ seeds, SeedWs w, SumPlan pd) {
+  extern __shared__ double srow[];
+  __shared__ double scratch_all[kPersistWarps][kMaxLeaves];
+  __shared__ double sv[kPersistWarps];
+  __shared__ int64_t si[kPersistWarps];
+  __shared__ double s_v;
+  __shared__ int64_t s_j;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned nb = gridDim.x;
+  double* scratch = scratch_all[warp];
+  int64_t cur = 0;
+  for (int64_t t = 1; t < k; t++) {
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) srow[i] = ld64(x + cur * ldx, i);
+    __syncthreads();
+    double v = -__longlong_as_double(0x7ff0000000000000ll);
+    int64_t vi = INT64_MAX;
+    for (int64_t r = (int64_t)blockIdx.x * kPersistWarps + warp; r < n; r += (int64_t)nb * kPersistWarps) {
+      const X* xr = x + r * ldx;
+      const double dist = warp_pairwise(
+          pd,
+          [&](int i) {
+            const double df = dsub(ld64(xr, i), srow[i]);
+            return dmul(df, df);
+          },
+          scratch, lane);
+      const double m = t == 1 ? dist : np_minimum(w.min_d[r], dist);
+      if (lane == 0) w.min_d[r] = m;
+      if (seed_before(m, r, v, vi)) {
+        v = m;
+        vi = r;
+      }
+    }
+    block_argmax(v, vi, sv, si);
+    double* pv = w.pv + (t & 1) * nb;
+    int64_t* pi = w.pi + (t & 1) * nb;
+    if (threadIdx.x == 0) {
+      pv[blockIdx.x] = v;
+      pi[blockIdx.x] = vi;
+      __threadfence();
+      atomicAdd(w.counter, 1u);
+      while (*(volatile unsigned*)w.counter < (unsigned)t * nb) {
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    v = -__longlong_as_double(0x7ff0000000000000ll);
+    vi = INT64_MAX;
+    for (unsigned b = threadIdx.x; b < nb; b += blockDim.x) {
+      const double v2 = __ldcg(pv + b);
+      const int64_t i2 = __ldcg(pi + b);
+      if (seed_before(v2, i2, v, vi)) {
+        v = v2;
+        vi = i2;
+      }
+    }
+    __syncthreads();   // sv / si reuse
+    block_argmax(v, vi, sv, si);
+    if (threadIdx.x == 0) {
+      s_v = v;
+      s_j = vi;
+    }
+    __syncthreads();
+    if (s_v == 0.0) {   // vq.py:141-143: min_d is all zero from here on, the seeds cycle
+      if (blockIdx.x == 0)
+        for (int64_t u = t + threadIdx.x; u < k; u += blockDim.x) seeds[u] = u % n;
+      return;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) seeds[t] = s_j;
+    cur = s_j;
+    __syncthreads();   // srow is rewritten by the next pass
+  }
+}
+
 unsigned seed_blocks(int64_t n) {
   int64_t b = (n + kSeedWarps - 1) / kSeedWarps;
   if (b > 148 * 8) b = 148 * 8;
@@ -148,9 +235,34 @@ cudaError_t seed_launch(const void* x, int64_t n, int64_t d, int64_t ldx, int64_
                         const SumPlan& pd, cudaStream_t s) {
   const size_t smem = sizeof(double) * (size_t)d;
   static bool attr = false;
+  static int per_sm = 0;
   if (!attr) {
     cudaFuncSetAttribute(seed_step_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
+    cudaFuncSetAttribute(seed_persistent_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
     attr = true;
+  }
+  int dev = 0, sms = 148, coop = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seed_persistent_kernel<X>, kPersistWarps * 32, smem) !=
+      cudaSuccess)
+    per_sm = 0;
+  if (per_sm > 2) per_sm = 2;
+  const unsigned want = (unsigned)((n + kPersistWarps - 1) / kPersistWarps);
+  const unsigned nb = (unsigned)((int64_t)per_sm * sms < (int64_t)want ? per_sm * sms : want);
+  if (coop && nb >= 1 && k > 1) {
+    const X* xp = static_cast<const X*>(x);
+    SeedWs ww = w;
+    SumPlan pp = pd;
+    void* args[] = {(void*)&xp, (void*)&n, (void*)&d, (void*)&ldx, (void*)&k, (void*)&seeds, (void*)&ww, (void*)&pp};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)seed_persistent_kernel<X>, dim3(nb), dim3(kPersistWarps * 32),
+                                                args, smem, s);
+    if (e == cudaSuccess) {
+      count_launches(1);
+      return cudaSuccess;
+    }
+    cudaGetLastError();   // not co-resident here: fall back to one launch per seed
   }
   const unsigned b = seed_blocks(n);
   for (int64_t t = 1; t < k; t++) {
@@ -164,8 +276,8 @@ cudaError_t seed_launch(const void* x, int64_t n, int64_t d, int64_t ldx, int64_
 
 size_t seed_workspace_bytes(int64_t n) {
   const size_t nb = seed_blocks(n);
-  return align_up(sizeof(double) * (size_t)n, 256) + align_up(sizeof(double) * nb, 256) +
-         align_up(sizeof(int64_t) * nb, 256) + 256;
+  return align_up(sizeof(double) * (size_t)n, 256) + align_up(sizeof(double) * 2 * nb, 256) +
+         align_up(sizeof(int64_t) * 2 * nb, 256) + 256;   // partials double-buffered (persistent kernel)
 }
 
 cudaError_t launch_seed_farthest(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, int64_t k,
@@ -177,9 +289,9 @@ cudaError_t launch_seed_farthest(const void* x, int dtype, int64_t n, int64_t d,
   w.min_d = reinterpret_cast<double*>(p);
   p += align_up(sizeof(double) * (size_t)n, 256);
   w.pv = reinterpret_cast<double*>(p);
-  p += align_up(sizeof(double) * nb, 256);
+  p += align_up(sizeof(double) * 2 * nb, 256);
   w.pi = reinterpret_cast<int64_t*>(p);
-  p += align_up(sizeof(int64_t) * nb, 256);
+  p += align_up(sizeof(int64_t) * 2 * nb, 256);
   w.counter = reinterpret_cast<unsigned*>(p);
   w.cycling = reinterpret_cast<int*>(p + 128);
   cudaError_t e;
