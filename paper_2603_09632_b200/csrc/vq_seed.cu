@@ -15,6 +15,8 @@
 // fp64 pairwise sums), reduces a per-block (max, index) and the last block to
 // finish reduces the block partials and writes seed t.  Either way nothing
 // synchronises with the host.
+#include <cstdlib>
+
 #include "launchers.h"
 
 namespace xgs {
@@ -251,7 +253,8 @@ cudaError_t seed_launch(const void* x, int64_t n, int64_t d, int64_t ldx, int64_
   if (per_sm > 2) per_sm = 2;
   const unsigned want = (unsigned)((n + kPersistWarps - 1) / kPersistWarps);
   const unsigned nb = (unsigned)((int64_t)per_sm * sms < (int64_t)want ? per_sm * sms : want);
-  if (coop && nb >= 1 && k > 1) {
+  const char* no_coop = std::getenv("XGS_SEED_NO_COOP");   // tests: exercise the per-launch path
+  if (coop && nb >= 1 && k > 1 && !(no_coop && no_coop[0] == '1')) {
     const X* xp = static_cast<const X*>(x);
     SeedWs ww = w;
     SumPlan pp = pd;

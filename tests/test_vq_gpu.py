@@ -115,7 +115,8 @@ def test_warm_start_and_seeding_golden(xv):
 
 @pytest.mark.parametrize("case", ["mixture_f32", "odd_d_f64", "cycling", "single_row", "nan_row", "ties",
                                   "bf16", "k_le_1"])
-def test_seed_from_samples_matches_oracle(xv, case):
+@pytest.mark.parametrize("coop", ["1", "0"])
+def test_seed_from_samples_matches_oracle(xv, case, coop, monkeypatch):
     """Device farthest-point seeding (xgs_vq_seed_farthest) vs the oracle
     restatement of vq.py:126-147, bit-exact: argmax ties to the lower index,
     cycling once the maximum is 0, NaN rows first (np.argmax / np.minimum)."""
@@ -139,6 +140,7 @@ def test_seed_from_samples_matches_oracle(xv, case):
         buf = torch.from_numpy(mixture(rng, 500, 128, 8, 0.1)).to(torch.bfloat16).cuda()
     else:
         buf, K = rng.normal(size=(10, 5)), 0
+    monkeypatch.setenv("XGS_SEED_NO_COOP", "0" if coop == "1" else "1")   # cooperative or per-launch path
     want = ov.seed_from_samples(buf.float().cpu().numpy() if torch.is_tensor(buf) else buf, K)
     got = xv.seed_from_samples(buf, K)
     got = got.cpu().numpy() if torch.is_tensor(got) else got
