@@ -1368,7 +1368,6 @@ size_t grid_workspace_bytes(int64_t npix) { return grid_ws(npix).total; }
 // for every item.
 constexpr int kDedupProbe = 256;
 constexpr int64_t kDedupSeg = 4096;   // dense item lists: segment length
-constexpr uint32_t PID_NONE = 0xffffffffu;
 
 struct DedupSegs {   // fused front: block b's items sit in its slot; else one dense list
   const uint64_t* k;
@@ -1746,7 +1745,6 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
       bits = 64;
     }
     if ((e = sort_init()) != cudaSuccess) return e;
-    const int64_t tiles = (nitems + SORT_TILE - 1) / SORT_TILE;
     if (nitems == 0) return cudaSuccess;
     out.n_sorted = nitems;
     out.sort_passes = (bits + 7) / 8;

@@ -304,15 +304,6 @@ template <> struct Raw<float, 2> {
   __device__ __forceinline__ void pin() { asm volatile("" : "+r"(w[0]), "+r"(w[1])); }
   __device__ __forceinline__ double get(int i) const { return (double)__uint_as_float(w[i]); }
 };
-template <> struct Raw<float, 4> {
-  uint32_t w[4];
-  __device__ __forceinline__ void load(const float* p) {
-    asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p));
-  }
-  __device__ __forceinline__ void pin() { asm volatile("" : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3])); }
-  __device__ __forceinline__ double get(int i) const { return (double)__uint_as_float(w[i]); }
-};
 template <> struct Raw<uint16_t, 8> {
   uint32_t w[4];
   __device__ __forceinline__ void load(const uint16_t* p) {
