@@ -291,15 +291,21 @@ compact_keys_kernel(const uint64_t* __restrict__ kin, int64_t n, int64_t W, uint
 
 
 // ---------------------------------------------------------------- G1 fused front end
-// First-pick mode on W % 4 == 0, W <= 2048: keys, left/up dedup and ordered
-// compaction in one pass over the depth.  A block owns FK_ROWS rows of one
-// frame (thread t = columns 4t..4t+3), recomputes the keys of the row above
-// as the halo, stages its surviving (key, pixel) items in shared memory in
-// pixel order and writes them to its own fixed slot plus a count; the sort's
-// rekey pass gathers the slots densely after an exclusive scan of the counts
-// (no block waits on another), so the items enter the sort in ascending pixel
-// order, exactly as the two-kernel path writes them, and the stable sort keeps
-// each voxel's lowest pixel id first.
+// First-pick mode on W % 4 == 0, W <= 4 * kFrontMaxThreads: keys, left/up dedup
+// and ordered compaction in one pass over the depth.  A block owns FK_ROWS rows
+// of one frame (thread t = columns 4t..4t+3) plus the row above as the halo,
+// and streams over them: per row, each warp compacts its surviving (key,
+// column) items into its own shared-memory segment (warp ballots, no block
+// barrier), so only the previous row's keys stay in registers.  The segments
+// are laid out in (row, warp) = pixel order; after one barrier an exclusive
+// scan of the segment counts gives every segment its offset inside the block's
+// fixed output slot plus the block's item count.  The sort's rekey pass / the
+// hash dedup gather the slots densely (no block waits on another), so the
+// items enter the dedup in ascending pixel order, exactly as the two-kernel
+// path writes them.  A pixel is dropped when its left neighbour (same warp) or
+// upper neighbour has the same key: any earlier pixel of the same voxel may
+// stand in, so the lowest pixel id of every voxel always survives (a warp's
+// first column keeps its item; the dedup downstream removes the repeat).
 //
 // Keys are evaluated in fp32 with a rigorous error bound first.  The
 // back-projection is regrouped as p_i = d * P_i + Q_i with
@@ -310,293 +316,306 @@ compact_keys_kernel(const uint64_t* __restrict__ kin, int64_t n, int64_t W, uint
 // rounding on that path (cx, 1/fx, R and t conversions, the products and
 // sums) is bounded by u = 2^-24 times a term of M_i, about 8 of them in total,
 // and the reference's fp64 evaluation (slam.py:594-598) is within ~2^-50 M_i
-// of exact, so |p32_i - p64_i| <= 2^-20 M_i.  If floor(q - delta) ==
-// floor(q + delta) with directed rounding (q = p32 / voxel) on all three axes
-// the fp32 floor IS the reference's floor(p64 / voxel); otherwise (voxel
-// faces, non-finite values, out of key range) the pixel takes the exact fp64
-// path (backproject + floor_div), bit-identical to the reference.
+// of exact, so |p32_i - p64_i| <= 2^-20 M_i.  One bound serves the three axes:
+// M = d * (max_i Crow_i + max_i Ccol_i) + max_i D_i >= M_i (all pre-scaled by
+// 1/voxel), dl = M * (2^-20 * 1.002 + 2^-21) + 2^-40.  With q = p32 / voxel,
+// x = RD(q + 2^23 + 2^20) = floor(q) + 2^23 + 2^20 exactly (|q| < 2^20), so
+// fl = x - (2^23 + 2^20) and fr = q - fl are exact; if dl < fr < 1 - dl on all
+// three axes, floor(p64 / voxel) == fl, and the low 21 bits of x's encoding are
+// the biased key field fl + 2^20.  Otherwise (voxel faces, non-finite values,
+// out of key range) the pixel takes the exact fp64 path (backproject +
+// floor_div), bit-identical to the reference.
 constexpr int FK_ROWS = 4;
 constexpr int kFrontPend = 1024;   // per-block queue of pixels for the exact path
 // thread t covers columns 4t..4t+3 (W <= 4 * kFrontMaxThreads); 3 blocks per SM
 constexpr int kFrontMaxThreads = 320;
+constexpr int kFrontWarps = kFrontMaxThreads / 32;
+constexpr int kFrontSeg = 128;     // items per (row, warp) segment: the warp's columns
+// staged bytes per segment item: 8 (key) + 1 (column inside the warp's span)
+constexpr size_t front_smem_bytes(int64_t nw) { return (size_t)FK_ROWS * nw * kFrontSeg * 9; }
 
 struct CamF {
   float cx, cy, rfx, rfy, inv_voxel;
 };
 
 __device__ __forceinline__ uint64_t key_exact(const double* R, const double* T, const Cam& cam, uint32_t u,
-                                              uint32_t v, float d32, int* qv) {
+                                              uint32_t v, float d32) {
   double p[3];
   backproject(R, T, cam, (double)u, (double)v, (double)d32, p);
   int64_t q[3];
   if (!voxel_of(p, cam.voxel, q, cam.inv_voxel)) return KEY_INVALID;
-#pragma unroll
-  for (int a = 0; a < 3; a++) qv[a] = (int)q[a];
   return ((uint64_t)q[0] << 42) | ((uint64_t)q[1] << 21) | (uint64_t)q[2];
 }
 
+template <bool BOX>
 __global__ void __launch_bounds__(kFrontMaxThreads, 3)
 grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int stride, const double* __restrict__ rot,
                   const double* __restrict__ trans, Cam cam, CamF cf, uint64_t* __restrict__ kout,
                   uint32_t* __restrict__ vout, int* bbox, unsigned long long* cnts, int32_t* __restrict__ block_count,
                   unsigned bid0) {
   constexpr int NR = FK_ROWS;
-  __shared__ uint64_t s_last[NR][32];
-  __shared__ uint32_t s_wsum[NR][32];
-  __shared__ uint32_t s_rowbase[NR + 1];
-  __shared__ unsigned s_bid;
-  __shared__ int s_box[6];
-  __shared__ uint32_t s_npend;
-  __shared__ uint32_t s_pend[kFrontPend];     // staged slot | (j << 30) of pixels left to the exact path
-  extern __shared__ __align__(16) uint8_t front_smem[];   // NR*W keys, then NR*W pixel ids
-  uint64_t* sk = reinterpret_cast<uint64_t*>(front_smem);
-  uint32_t* sv = reinterpret_cast<uint32_t*>(front_smem + (size_t)NR * W * 8);
-  if (threadIdx.x == 0) {
-    s_bid = bid0 + blockIdx.x;   // bid0: first block of this launch (frame-chunked launches)
-    s_npend = 0;
-  }
-  if (threadIdx.x < 6) s_box[threadIdx.x] = threadIdx.x < 3 ? INT_MAX : INT_MIN;
-  __syncthreads();
-  const unsigned bid = s_bid;
-  const int rbf = (int)((H + NR - 1) / NR);   // row blocks per frame
-  const int f = (int)(bid / (unsigned)rbf);
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
-  const uint32_t Wu = (uint32_t)W, su = (uint32_t)stride;
-  const uint32_t c0 = (uint32_t)t * 4;
-  const bool col_on = c0 < Wu;
-  const double* Rd = rot + (size_t)f * 9;
-  const double* Td = trans + (size_t)f * 3;
-  const float iv = cf.inv_voxel;
-  // per-frame constants pre-scaled by 1/voxel: q_i = p_i / voxel = d * (Pr_i + Pc_ji) + Qs_i,
-  // magnitude bound M_i / voxel = d * (Cr_i + Cc_ji) + Ds_i
-  float R0[3], R2[3], A0[3], A2[3], Qs[3], Ds[3], Dmax;
-  float Pc[4][3], Cc[4][3];
-  unsigned colmask = 0;
-  {
-    const float t0 = (float)Td[0], t1 = (float)Td[1], t2 = (float)Td[2];
-    float R1[3];
-#pragma unroll
-    for (int i = 0; i < 3; i++) {
-      const float r0 = (float)Rd[i], r1 = (float)Rd[3 + i], r2 = (float)Rd[6 + i];
-      R0[i] = r0 * iv;
-      R1[i] = r1 * iv;
-      R2[i] = r2 * iv;
-      A0[i] = fabsf(R0[i]);
-      A2[i] = fabsf(R2[i]);
-      Qs[i] = -fmaf(r2, t2, fmaf(r1, t1, r0 * t0)) * iv;
-      Ds[i] = fmaf(fabsf(r2), fabsf(t2), fmaf(fabsf(r1), fabsf(t1), fabsf(r0) * fabsf(t0))) * iv;
-    }
-    Dmax = fmaxf(fmaxf(Ds[0], Ds[1]), Ds[2]);
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const float vv = (float)(c0 + j);
-      const float cv = (vv - cf.cy) * cf.rfy, bv = (vv + fabsf(cf.cy)) * cf.rfy;
-#pragma unroll
-      for (int i = 0; i < 3; i++) {
-        Pc[j][i] = R1[i] * cv;
-        Cc[j][i] = fabsf(R1[i]) * bv;
-      }
-      if (col_on && (su == 1 || ((c0 + j) % su) == 0)) colmask |= 1u << j;
-    }
-  }
-  const int r0 = (int)(bid % (unsigned)rbf) * NR;
-  const int nr = (int)min((int64_t)NR, H - r0);
-  const float4* drow = reinterpret_cast<const float4*>(depth + (size_t)f * H * W);
-  unsigned cnt = 0;
-  // ---- keys of the halo row and the block's rows, all in registers ----
+  constexpr float XB = 9437184.f;   // 2^23 + 2^20
   // PEND marks a pixel the fp32 filter could not decide: it compares unequal to
   // every key (so it and its neighbours are kept) and is resolved exactly below.
   constexpr uint64_t PEND = KEY_INVALID - 1;
-  uint64_t k[NR + 1][4];
-#pragma unroll
-  for (int rr = 0; rr <= NR; rr++) {
-    const int r = r0 - 1 + rr;
-#pragma unroll
-    for (int j = 0; j < 4; j++) k[rr][j] = KEY_INVALID;
-    if (r < 0 || rr > nr) continue;
-    const uint32_t u = (uint32_t)r;
-    const unsigned rowmask = (su == 1 || (u % su) == 0) ? colmask : 0u;
-    if (!rowmask) continue;
-    const float4 d4 = __ldg(drow + (((size_t)r * W) >> 2) + t);
-    const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
-    const float uu = (float)u;
-    const float ru = (uu - cf.cx) * cf.rfx, bu = (uu + fabsf(cf.cx)) * cf.rfx;
-    float Pr[3], Cr[3];
+  __shared__ float4 s_row[NR + 1];            // per row: P_row (3, pre-scaled) + max_i C_row
+  __shared__ float s_frame[8];                // R1 / voxel (3), Q / voxel (3), max_i D_i, max_i |R1| / voxel
+  __shared__ uint32_t s_cnt[NR * kFrontWarps];   // segment counts
+  __shared__ uint32_t s_off[NR * kFrontWarps];   // their exclusive scan
+  __shared__ uint32_t s_run;
+  __shared__ int s_box[6];
+  __shared__ uint32_t s_npend;
+  __shared__ uint32_t s_pend[kFrontPend];     // staged slots of pixels left to the exact path
+  extern __shared__ __align__(16) uint8_t front_smem[];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+  const int nseg = NR * nw;
+  uint64_t* sk = reinterpret_cast<uint64_t*>(front_smem);                         // nseg * 128 keys
+  uint8_t* sc = front_smem + (size_t)nseg * kFrontSeg * 8;                          // nseg * 128 columns
+  const unsigned bid = bid0 + blockIdx.x;   // bid0: first block of this launch (frame-chunked launches)
+  const int rbf = (int)((H + NR - 1) / NR);   // row blocks per frame
+  const int f = (int)(bid / (unsigned)rbf);
+  const int r0 = (int)(bid % (unsigned)rbf) * NR;
+  const int nr = (int)min((int64_t)NR, H - r0);
+  const double* Rd = rot + (size_t)f * 9;
+  const double* Td = trans + (size_t)f * 3;
+  const float iv = cf.inv_voxel;
+  // ---- per-frame and per-row constants: threads 0..NR the rows, thread NR+1 the frame ----
+  if (t <= NR + 1) {
+    float R0[3], R1[3], R2[3];
 #pragma unroll
     for (int i = 0; i < 3; i++) {
-      Pr[i] = fmaf(R0[i], ru, R2[i]);
-      Cr[i] = fmaf(A0[i], bu, A2[i]);
+      R0[i] = (float)Rd[i] * iv;
+      R1[i] = (float)Rd[3 + i] * iv;
+      R2[i] = (float)Rd[6 + i] * iv;
     }
+    if (t <= NR) {
+      const float uu = (float)(r0 - 1 + t);
+      const float ru = (uu - cf.cx) * cf.rfx, bu = (uu + fabsf(cf.cx)) * cf.rfx;
+      float4 rc;
+      rc.x = fmaf(R0[0], ru, R2[0]);
+      rc.y = fmaf(R0[1], ru, R2[1]);
+      rc.z = fmaf(R0[2], ru, R2[2]);
+      rc.w = fmaxf(fmaxf(fmaf(fabsf(R0[0]), bu, fabsf(R2[0])), fmaf(fabsf(R0[1]), bu, fabsf(R2[1]))),
+                   fmaf(fabsf(R0[2]), bu, fabsf(R2[2])));
+      s_row[t] = rc;
+    } else {
+      const float t0 = (float)Td[0], t1 = (float)Td[1], t2 = (float)Td[2];
+      float dm = 0.f;
+#pragma unroll
+      for (int i = 0; i < 3; i++) {
+        const float r0f = (float)Rd[i], r1f = (float)Rd[3 + i], r2f = (float)Rd[6 + i];
+        s_frame[i] = R1[i];
+        s_frame[3 + i] = -fmaf(r2f, t2, fmaf(r1f, t1, r0f * t0)) * iv;
+        dm = fmaxf(dm, fmaf(fabsf(r2f), fabsf(t2), fmaf(fabsf(r1f), fabsf(t1), fabsf(r0f) * fabsf(t0))) * iv);
+      }
+      s_frame[6] = dm;
+      s_frame[7] = fmaxf(fmaxf(fabsf(R1[0]), fabsf(R1[1])), fabsf(R1[2]));
+      s_npend = 0;
+      if (BOX) {
+#pragma unroll
+        for (int a = 0; a < 6; a++) s_box[a] = a < 3 ? INT_MAX : INT_MIN;
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t Wu = (uint32_t)W, su = (uint32_t)stride;
+  const uint32_t c0 = (uint32_t)t * 4;
+  unsigned colmask = 0;
+  // column parts: P_col_i = R1_i / voxel * cv (fused into the row part per pixel), C_col = max_i |R1_i| / voxel * bv
+  float cv[4], Cc[4];
+  const float Qs0 = s_frame[3], Qs1 = s_frame[4], Qs2 = s_frame[5], Dmax = s_frame[6];
+  const float R10 = s_frame[0], R11 = s_frame[1], R12 = s_frame[2];
+  {
+    const float A1 = s_frame[7];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const float vv = (float)(c0 + j);
+      cv[j] = (vv - cf.cy) * cf.rfy;
+      Cc[j] = A1 * ((vv + fabsf(cf.cy)) * cf.rfy);
+      if (c0 + j < Wu && (su == 1 || ((c0 + j) % su) == 0)) colmask |= 1u << j;
+    }
+  }
+  const float4* dframe = reinterpret_cast<const float4*>(depth + (size_t)f * H * W);
+  const uint32_t w4 = Wu >> 2;
+  unsigned cnt = 0;
+  uint64_t kp[4];   // previous row's keys (the halo row first)
+  float4 dn = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (r0 > 0 && colmask) dn = __ldg(dframe + (size_t)(r0 - 1) * w4 + t);
+#pragma unroll 1
+  for (int rr = 0; rr <= nr; rr++) {
+    const int r = r0 - 1 + rr;
+    const float4 d4 = dn;
+    if (rr < nr && colmask) dn = __ldg(dframe + (size_t)(r + 1) * w4 + t);   // next row in flight
+    const unsigned rowmask = (r >= 0 && (su == 1 || ((uint32_t)r % su) == 0)) ? colmask : 0u;
+    const float4 rc = s_row[rr];
+    const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+    uint64_t k[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
       const float d = dv[j];
-      if (!((rowmask >> j) & 1u) || !(d > 0.f)) continue;
-      // one guard band for the three axes from the largest magnitude bound
-      const float M = fmaf(d, fmaxf(fmaxf(Cr[0] + Cc[j][0], Cr[1] + Cc[j][1]), Cr[2] + Cc[j][2]), Dmax);
-      const float dl = fmaf(M, 0x1p-20f * 1.002f + 0x1p-21f, 0x1p-40f);
-      bool ok = M < 1048000.f;
-      int qi[3];
-#pragma unroll
-      for (int i = 0; i < 3; i++) {
-        const float q = fmaf(d, Pr[i] + Pc[j][i], Qs[i]);
-        const float fl = floorf(__fsub_rd(q, dl));
-        ok = ok && __fadd_ru(q, dl) < fl + 1.f;   // one floor on [q-dl, q+dl]
-        qi[i] = (int)fl + (int)KEY_BIAS;
-      }
-      if (ok) {
-        k[rr][j] = ((uint64_t)(uint32_t)qi[0] << 42) | ((uint64_t)(uint32_t)qi[1] << 21) | (uint64_t)(uint32_t)qi[2];
-        cnt += rr > 0 ? 1u : 0u;
-      } else {
-        k[rr][j] = PEND;
+      // branch-free: every lane evaluates the filter, invalid pixels are masked afterwards
+      {
+        const bool valid = ((rowmask >> j) & 1u) && d > 0.f;
+        const float M = fmaf(d, rc.w + Cc[j], Dmax);
+        const float dl = fmaf(M, 0x1p-20f * 1.002f + 0x1p-21f, 0x1p-40f);
+        const float q0 = fmaf(d, fmaf(R10, cv[j], rc.x), Qs0);
+        const float q1 = fmaf(d, fmaf(R11, cv[j], rc.y), Qs1);
+        const float q2 = fmaf(d, fmaf(R12, cv[j], rc.z), Qs2);
+        const float x0 = __fadd_rd(q0, XB), x1 = __fadd_rd(q1, XB), x2 = __fadd_rd(q2, XB);
+        const float f0 = q0 - (x0 - XB), f1 = q1 - (x1 - XB), f2 = q2 - (x2 - XB);
+        const float lo = fminf(fminf(f0, f1), f2), hi = fmaxf(fmaxf(f0, f1), f2);
+        const bool ok = M < 1048000.f && lo > dl && hi < __fsub_rd(1.f, dl);
+        const uint32_t b0 = __float_as_uint(x0) & 0x1fffffu, b1 = __float_as_uint(x1) & 0x1fffffu,
+                       b2 = __float_as_uint(x2) & 0x1fffffu;
+        const uint64_t key = ((uint64_t)((b0 << 10) | (b1 >> 11)) << 32) | (uint64_t)((b1 << 21) | b2);
+        k[j] = !valid ? KEY_INVALID : ok ? key : PEND;
+        cnt += (valid && ok && rr > 0) ? 1u : 0u;
       }
     }
-  }
-  // ---- left/up dedup + survivor counts per row ----
+    if (rr > 0) {
+      // ---- left/up dedup, warp-local compaction into segment (row, warp) ----
+      const uint64_t left = __shfl_up_sync(FULL, k[3], 1);
+      unsigned keep = 0;
 #pragma unroll
-  for (int rr = 1; rr <= NR; rr++) {
-    if (lane == 31) s_last[rr - 1][warp] = k[rr][3];
+      for (int j = 0; j < 4; j++) {
+        const uint64_t kk = k[j];
+        const uint64_t lk = j == 0 ? (lane > 0 ? left : KEY_INVALID) : k[j - 1];
+        if (kk != KEY_INVALID && (kk == PEND || (kk != lk && kk != kp[j]))) keep |= 1u << j;
+      }
+      const unsigned lt = (1u << lane) - 1u;
+      unsigned below = 0, total = 0;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const unsigned b = __ballot_sync(FULL, (keep >> j) & 1u);
+        below += __popc(b & lt);
+        total += __popc(b);
+      }
+      const int seg = (rr - 1) * nw + warp;
+      const uint32_t o0 = (uint32_t)seg * kFrontSeg + below;
+      unsigned pend = 0;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const uint32_t o = o0 + __popc(keep & ((1u << j) - 1u));
+        if ((keep >> j) & 1u) {   // predicated stores
+          sk[o] = k[j];
+          sc[o] = (uint8_t)(lane * 4 + j);
+        }
+        pend |= (((keep >> j) & 1u) && k[j] == PEND) ? 1u << j : 0u;
+      }
+      if (__any_sync(FULL, pend)) {   // rare: queue the undecided pixels for the exact path
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+          if ((pend >> j) & 1u) {
+            const uint32_t pi = atomicAdd(&s_npend, 1u);
+            if (pi < kFrontPend) s_pend[pi] = o0 + __popc(keep & ((1u << j) - 1u));
+          }
+      }
+      if (lane == 0) s_cnt[seg] = total;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) kp[j] = k[j];
   }
+  // rows past the frame's last row: empty segments
+  for (int s = nr * nw + t; s < nseg; s += blockDim.x) s_cnt[s] = 0;
   __syncthreads();
-  uint32_t keepm = 0, cnt_r[NR], x_r[NR];
-#pragma unroll
-  for (int rr = 1; rr <= NR; rr++) {
-    uint64_t left = __shfl_up_sync(FULL, k[rr][3], 1);
-    if (lane == 0) left = warp > 0 ? s_last[rr - 1][warp - 1] : KEY_INVALID;
-    unsigned keep = 0;
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const uint64_t kk = k[rr][j];
-      const uint64_t lk = j == 0 ? left : k[rr][j - 1];
-      // PEND never equals a key; a pending neighbour keeps this pixel
-      if (kk != KEY_INVALID && (kk == PEND || (kk != lk && kk != k[rr - 1][j]))) keep |= 1u << j;
+  // ---- exact fp64 keys of the pending pixels, one lane each ----
+  const uint32_t fbase = (uint32_t)((size_t)f * H * W);
+  auto resolve = [&](uint32_t o) {
+    const int seg = (int)(o / kFrontSeg);
+    const uint32_t u = (uint32_t)(r0 + seg / nw), v = (uint32_t)(seg % nw) * kFrontSeg + sc[o];
+    const uint64_t key = key_exact(Rd, Td, cam, u, v, depth[fbase + u * Wu + v]);
+    sk[o] = key;
+    cnt += key != KEY_INVALID ? 1u : 0u;
+  };
+  {
+    const uint32_t np = s_npend;
+    if (np <= (uint32_t)kFrontPend) {
+      for (uint32_t i = t; i < np; i += blockDim.x) resolve(s_pend[i]);
+    } else {
+      for (int s = warp; s < nseg; s += nw)
+        for (uint32_t i = lane; i < s_cnt[s]; i += 32) {
+          const uint32_t o = (uint32_t)s * kFrontSeg + i;
+          if (sk[o] == PEND) resolve(o);
+        }
     }
-    keepm |= keep << (4 * (rr - 1));
-    cnt_r[rr - 1] = __popc(keep);
-    uint32_t x = cnt_r[rr - 1];
+  }
+  // ---- exclusive scan of the segment counts (warp 0; nseg <= 96) ----
+  if (warp == 0) {
+    uint32_t v[3], run = 0;
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+      const int s = lane * 3 + i;
+      v[i] = s < nseg ? s_cnt[s] : 0u;
+      run += v[i];
+    }
+    uint32_t x = run;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(FULL, x, o);
       if (lane >= o) x += y;
     }
-    x_r[rr - 1] = x;
-    if (lane == 31) s_wsum[rr - 1][warp] = x;
-  }
-  __syncthreads();
-  // per row: exclusive warp offsets; rows staged back to back (pixel order)
-  for (int rr = warp; rr < NR; rr += nw) {
-    uint32_t w = lane < nw ? s_wsum[rr][lane] : 0, wx = w;
+    uint32_t e = x - run;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(FULL, wx, o);
-      if (lane >= o) wx += y;
+    for (int i = 0; i < 3; i++) {
+      const int s = lane * 3 + i;
+      if (s < nseg) s_off[s] = e;
+      e += v[i];
     }
-    if (lane < nw) s_wsum[rr][lane] = wx - w;
-    if (lane == nw - 1) s_rowbase[rr + 1] = wx;   // row total
+    if (lane == 31) s_run = x;
   }
+  cnt = __reduce_add_sync(FULL, cnt);
+  if (lane == 0 && cnt) atomicAdd(cnts, (unsigned long long)cnt);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t run = 0;
-    for (int rr = 0; rr < NR; rr++) {
-      const uint32_t tot = s_rowbase[rr + 1];
-      s_rowbase[rr] = run;
-      run += tot;
-    }
-    s_rowbase[NR] = run;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int rr = 1; rr <= NR; rr++) {
-    uint32_t o = s_rowbase[rr - 1] + s_wsum[rr - 1][warp] + x_r[rr - 1] - cnt_r[rr - 1];
-    const uint32_t p0 = (uint32_t)(((size_t)f * H + (r0 + rr - 1)) * W) + c0;
-#pragma unroll
-    for (int j = 0; j < 4; j++)
-      if ((keepm >> (4 * (rr - 1) + j)) & 1u) {
-        sk[o] = k[rr][j];
-        sv[o] = p0 + j;
-        if (k[rr][j] == PEND) {
-          const uint32_t pi = atomicAdd(&s_npend, 1u);
-          if (pi < kFrontPend) s_pend[pi] = o;
-        }
-        o++;
-      }
-  }
-  __syncthreads();
-  const uint32_t run = s_rowbase[NR];
-  // ---- exact fp64 keys of the pending pixels, one lane each ----
-  {
-    const uint32_t np = s_npend;
-    if (np <= (uint32_t)kFrontPend) {
-      for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
-        const uint32_t o = s_pend[i];
-        const uint32_t p = sv[o];
-        const uint32_t rem = p - (uint32_t)((size_t)f * H * W);
-        const uint32_t u = rem / Wu, v = rem - u * Wu;
-        int qv[3];
-        const uint64_t key = key_exact(Rd, Td, cam, u, v, depth[p], qv);
-        sk[o] = key;
-        cnt += key != KEY_INVALID ? 1u : 0u;
-      }
-    } else {
-      for (uint32_t o = threadIdx.x; o < run; o += blockDim.x)
-        if (sk[o] == PEND) {
-          const uint32_t p = sv[o];
-          const uint32_t rem = p - (uint32_t)((size_t)f * H * W);
-          const uint32_t u = rem / Wu, v = rem - u * Wu;
-          int qv[3];
-          const uint64_t key = key_exact(Rd, Td, cam, u, v, depth[p], qv);
-          sk[o] = key;
-          cnt += key != KEY_INVALID ? 1u : 0u;
-        }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  const uint32_t run = s_run;
+  if (t == 0) {
     block_count[bid] = (int32_t)run;
     if (run) atomicAdd(cnts + 2, (unsigned long long)run);
   }
-  // copy out to this block's slot (FK_ROWS * W items; the rekey pass gathers
-  // the slots densely in block = pixel order, so no block waits on another);
-  // pixels resolved to invalid stay as KEY_INVALID items and sort last; the
-  // voxel bounding box over the survivors equals the box over all valid pixels
-  // (every dropped pixel repeats a survivor's key)
-  const size_t gbase = ((size_t)f * H + r0) * (size_t)W;   // the block's own pixels bound its survivors
+  // ---- copy out to this block's slot (FK_ROWS * W items), one warp per segment ----
+  // Pixels resolved to invalid stay as KEY_INVALID items (they sort last / are
+  // skipped by the dedup).  The voxel bounding box over the survivors equals
+  // the box over all valid pixels (every dropped pixel repeats a survivor's key).
+  const size_t gbase = ((size_t)f * H + r0) * (size_t)W;
   int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
-  for (uint32_t i = threadIdx.x; i < run; i += blockDim.x) {
-    const uint64_t key = sk[i];
-    kout[gbase + i] = key;
-    vout[gbase + i] = sv[i];
-    if (key != KEY_INVALID) {
-      const int q[3] = {(int)(key >> 42), (int)((key >> 21) & 0x1fffff), (int)(key & 0x1fffff)};
+  for (int rr = 0; rr < nr; rr++) {   // the warp copies its own segments
+    const int s = rr * nw + warp;
+    const uint32_t beg = s_off[s], end = beg + s_cnt[s];
+    const uint32_t pbase = fbase + (uint32_t)(r0 + rr) * Wu + (uint32_t)warp * kFrontSeg;
+    for (uint32_t i = lane; i < end - beg; i += 32) {
+      const uint32_t o = (uint32_t)s * kFrontSeg + i;
+      const uint64_t key = sk[o];
+      kout[gbase + beg + i] = key;
+      vout[gbase + beg + i] = pbase + sc[o];
+      if (BOX && key != KEY_INVALID) {
+        const int q[3] = {(int)(key >> 42), (int)((key >> 21) & 0x1fffff), (int)(key & 0x1fffff)};
 #pragma unroll
-      for (int a = 0; a < 3; a++) {
-        lo[a] = min(lo[a], q[a]);
-        hi[a] = max(hi[a], q[a]);
+        for (int a = 0; a < 3; a++) {
+          lo[a] = min(lo[a], q[a]);
+          hi[a] = max(hi[a], q[a]);
+        }
       }
     }
   }
+  if (BOX) {
 #pragma unroll
-  for (int a = 0; a < 3; a++)
-    for (int o = 16; o; o >>= 1) {
-      lo[a] = min(lo[a], __shfl_xor_sync(FULL, lo[a], o));
-      hi[a] = max(hi[a], __shfl_xor_sync(FULL, hi[a], o));
+    for (int a = 0; a < 3; a++) {
+      lo[a] = __reduce_min_sync(FULL, lo[a]);
+      hi[a] = __reduce_max_sync(FULL, hi[a]);
     }
-  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
-  if (lane == 0) {
-    if (lo[0] != INT_MAX) {
+    if (lane == 0 && lo[0] != INT_MAX) {
 #pragma unroll
       for (int a = 0; a < 3; a++) {
         atomicMin(&s_box[a], lo[a]);
         atomicMax(&s_box[3 + a], hi[a]);
       }
     }
-    if (cnt) atomicAdd(cnts, (unsigned long long)cnt);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && s_box[0] != INT_MAX) {
+    __syncthreads();
+    if (t == 0 && s_box[0] != INT_MAX) {
 #pragma unroll
-    for (int a = 0; a < 3; a++) {
-      atomicMin(bbox + a, s_box[a]);
-      atomicMax(bbox + 3 + a, s_box[3 + a]);
+      for (int a = 0; a < 3; a++) {
+        atomicMin(bbox + a, s_box[a]);
+        atomicMax(bbox + 3 + a, s_box[3 + a]);
+      }
     }
   }
 }
@@ -866,10 +885,17 @@ sort_downsweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vi
   }
 }
 
+bool sort_forced() {
+  const char* force_sort = std::getenv("XGS_GRID_SORT");
+  return force_sort && force_sort[0] == '1';
+}
+
 cudaError_t front_init() {
   if (front_attr_set) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(grid_front_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       FK_ROWS * 2048 * 12);
+  const int bytes = (int)front_smem_bytes(kFrontWarps);
+  cudaError_t e = cudaFuncSetAttribute(grid_front_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(grid_front_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) front_attr_set = true;
   return e;
 }
@@ -1653,14 +1679,16 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     if (fused) {
       const CamF cf{(float)in.cx, (float)in.cy, (float)(1.0 / in.fx), (float)(1.0 / in.fy), (float)(1.0 / in.voxel)};
       const unsigned nt = (unsigned)((in.W / 4 + 31) / 32 * 32);
-      const size_t fsmem = (size_t)FK_ROWS * in.W * 12;
+      const size_t fsmem = front_smem_bytes(nt / 32);
+      // the voxel bounding box only feeds the sort path's relative keys
+      auto kern = sort_forced() ? grid_front_kernel<true> : grid_front_kernel<false>;
       if ((e = front_init()) != cudaSuccess) return e;
       const int64_t rbf = (in.H + FK_ROWS - 1) / FK_ROWS;
       for (int c = 0; c < nchunk; c++) {
         const int64_t f0 = c * fper, f1 = f0 + fper < in.frames ? f0 + fper : in.frames;
         if (f1 <= f0) break;
         if (host_frames && (e = cudaStreamWaitEvent(s, hcp->chunk[c], 0)) != cudaSuccess) return e;
-        grid_front_kernel<<<(unsigned)((f1 - f0) * rbf), nt, fsmem, s>>>(in.depth, in.H, in.W, in.stride, in.rot,
+        kern<<<(unsigned)((f1 - f0) * rbf), nt, fsmem, s>>>(in.depth, in.H, in.W, in.stride, in.rot,
                                                                           in.trans, cam, cf, k0, v0, bbox, cnts,
                                                                           block_count, (unsigned)(f0 * rbf));
         count_launches(1);
@@ -1682,8 +1710,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   // first-pick mode takes the hash path (G2'); XGS_GRID_SORT=1 forces the
   // radix sort + select path (mean mode always sorts: its per-voxel sums run
   // in pixel order over the voxel's segment)
-  const char* force_sort = std::getenv("XGS_GRID_SORT");
-  const bool hashed = compact && !(force_sort && force_sort[0] == '1');
+  const bool hashed = compact && !sort_forced();
   std::unique_lock<std::mutex> dd_lock(g_dedup_mu, std::defer_lock);
   if (hashed) dd_lock.lock();
   // The hash path on the fused front end needs no host-side item count when

@@ -1,0 +1,15 @@
+"""C3 grid sub-benchmark alone (bench.run_grid without the CPU leg): prints the per-voxel-size JSON."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import bench
+
+steps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+out = bench.run_grid(torch, steps, cpu=False)
+for v, g in out.items():
+    print(v, json.dumps({k: g[k] for k in ("Mpts_per_s", "ms_per_batch", "sorted_items", "new_voxels", "per_kernel_ms")}),
+          "frac", g["roofline"]["frac"])
