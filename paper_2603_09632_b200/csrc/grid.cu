@@ -199,7 +199,7 @@ __global__ void init_bbox_kernel(int* bbox, unsigned long long* nvalid) {
     bbox[threadIdx.x] = INT_MAX;
     bbox[3 + threadIdx.x] = INT_MIN;
   }
-  if (threadIdx.x == 0) *nvalid = 0;
+  if (threadIdx.x < 6) nvalid[threadIdx.x] = 0;   // nvalid, nvox, items, and the scratch counters after them
 }
 
 // First-pick mode: compact the per-pixel keys before the sort.  A pixel whose
@@ -325,11 +325,12 @@ compact_keys_kernel(const uint64_t* __restrict__ kin, int64_t n, int64_t W, uint
 // the biased key field fl + 2^20.  Otherwise (voxel faces, non-finite values,
 // out of key range) the pixel takes the exact fp64 path (backproject +
 // floor_div), bit-identical to the reference.
-constexpr int FK_ROWS = 4;
+constexpr int FK_ROWS = 6;
 constexpr int kFrontPend = 1024;   // per-block queue of pixels for the exact path
-// thread t covers columns 4t..4t+3 (W <= 4 * kFrontMaxThreads); 3 blocks per SM
+// thread t covers columns 4t..4t+3 (W <= 4 * kFrontMaxThreads)
 constexpr int kFrontMaxThreads = 320;
 constexpr int kFrontWarps = kFrontMaxThreads / 32;
+constexpr int kFrontBlocksPerSM = FK_ROWS <= 6 ? 3 : 2;   // bounded by the staged segments (FK_ROWS * 11.5 KB)
 constexpr int kFrontSeg = 128;     // items per (row, warp) segment: the warp's columns
 // staged bytes per segment item: 8 (key) + 1 (column inside the warp's span)
 constexpr size_t front_smem_bytes(int64_t nw) { return (size_t)FK_ROWS * nw * kFrontSeg * 9; }
@@ -347,8 +348,47 @@ __device__ __forceinline__ uint64_t key_exact(const double* R, const double* T, 
   return ((uint64_t)q[0] << 42) | ((uint64_t)q[1] << 21) | (uint64_t)q[2];
 }
 
+// sm_100 paired fp32 arithmetic on {lo, hi} = {pixel j, pixel j + 1}
+using u64 = unsigned long long;
+__device__ __forceinline__ u64 f2(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float lane_of(u64 v, int h) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return h ? b : a;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 add2_rd(u64 a, u64 b) {
+  u64 r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 sub2_rd(u64 a, u64 b) {
+  u64 r;
+  asm("sub.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+constexpr float kDl = 0x1p-20f * 1.002f + 0x1p-21f;
+
 template <bool BOX>
-__global__ void __launch_bounds__(kFrontMaxThreads, 3)
+__global__ void __launch_bounds__(kFrontMaxThreads, kFrontBlocksPerSM)
 grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int stride, const double* __restrict__ rot,
                   const double* __restrict__ trans, Cam cam, CamF cf, uint64_t* __restrict__ kout,
                   uint32_t* __restrict__ vout, int* bbox, unsigned long long* cnts, int32_t* __restrict__ block_count,
@@ -450,23 +490,30 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
     const float4 rc = s_row[rr];
     const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
     uint64_t k[4];
+    // two pixels per instruction (sm_100 paired fp32: FFMA2 / FADD2, IEEE per lane,
+    // same roundings as the scalar expressions in the comments)
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const float d = dv[j];
-      // branch-free: every lane evaluates the filter, invalid pixels are masked afterwards
-      {
-        const bool valid = ((rowmask >> j) & 1u) && d > 0.f;
-        const float M = fmaf(d, rc.w + Cc[j], Dmax);
-        const float dl = fmaf(M, 0x1p-20f * 1.002f + 0x1p-21f, 0x1p-40f);
-        const float q0 = fmaf(d, fmaf(R10, cv[j], rc.x), Qs0);
-        const float q1 = fmaf(d, fmaf(R11, cv[j], rc.y), Qs1);
-        const float q2 = fmaf(d, fmaf(R12, cv[j], rc.z), Qs2);
-        const float x0 = __fadd_rd(q0, XB), x1 = __fadd_rd(q1, XB), x2 = __fadd_rd(q2, XB);
-        const float f0 = q0 - (x0 - XB), f1 = q1 - (x1 - XB), f2 = q2 - (x2 - XB);
-        const float lo = fminf(fminf(f0, f1), f2), hi = fmaxf(fmaxf(f0, f1), f2);
-        const bool ok = M < 1048000.f && lo > dl && hi < __fsub_rd(1.f, dl);
-        const uint32_t b0 = __float_as_uint(x0) & 0x1fffffu, b1 = __float_as_uint(x1) & 0x1fffffu,
-                       b2 = __float_as_uint(x2) & 0x1fffffu;
+    for (int jp = 0; jp < 4; jp += 2) {
+      const u64 d2 = f2(dv[jp], dv[jp + 1]);
+      const u64 M = fma2(d2, add2(f2(rc.w, rc.w), f2(Cc[jp], Cc[jp + 1])), f2(Dmax, Dmax));   // d*(Crow+Ccol)+Dmax
+      const u64 dl = fma2(M, f2(kDl, kDl), f2(0x1p-40f, 0x1p-40f));
+      const u64 omd = sub2_rd(f2(1.f, 1.f), dl);                                               // RD(1 - dl)
+      const u64 cv2 = f2(cv[jp], cv[jp + 1]);
+      const u64 q0 = fma2(d2, fma2(f2(R10, R10), cv2, f2(rc.x, rc.x)), f2(Qs0, Qs0));          // d*(R1*cv+Prow)+Q
+      const u64 q1 = fma2(d2, fma2(f2(R11, R11), cv2, f2(rc.y, rc.y)), f2(Qs1, Qs1));
+      const u64 q2 = fma2(d2, fma2(f2(R12, R12), cv2, f2(rc.z, rc.z)), f2(Qs2, Qs2));
+      const u64 xb = f2(XB, XB);
+      const u64 x0 = add2_rd(q0, xb), x1 = add2_rd(q1, xb), x2 = add2_rd(q2, xb);             // floor(q) + XB
+      const u64 g0 = sub2(q0, sub2(x0, xb)), g1 = sub2(q1, sub2(x1, xb)), g2 = sub2(q2, sub2(x2, xb));  // exact fractions
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int j = jp + h;
+        const float f0 = lane_of(g0, h), f1 = lane_of(g1, h), f2v = lane_of(g2, h);
+        const float lo = fminf(fminf(f0, f1), f2v), hi = fmaxf(fmaxf(f0, f1), f2v);
+        const bool valid = ((rowmask >> j) & 1u) && dv[j] > 0.f;
+        const bool ok = lane_of(M, h) < 1048000.f && lo > lane_of(dl, h) && hi < lane_of(omd, h);
+        const uint32_t b0 = __float_as_uint(lane_of(x0, h)) & 0x1fffffu, b1 = __float_as_uint(lane_of(x1, h)) & 0x1fffffu,
+                       b2 = __float_as_uint(lane_of(x2, h)) & 0x1fffffu;
         const uint64_t key = ((uint64_t)((b0 << 10) | (b1 >> 11)) << 32) | (uint64_t)((b1 << 21) | b2);
         k[j] = !valid ? KEY_INVALID : ok ? key : PEND;
         cnt += (valid && ok && rr > 0) ? 1u : 0u;
@@ -1668,8 +1715,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   }
   {
     ProfScope prof("grid_keys", s);
-    init_bbox_kernel<<<1, 32, 0, s>>>(bbox, cnts); count_launches(1);
-    cudaMemsetAsync(cnts + 1, 0, 40, s);
+    init_bbox_kernel<<<1, 32, 0, s>>>(bbox, cnts); count_launches(1);   // also zeroes cnts[0..5]
     const bool vec4 = (in.W % 4 == 0) && (reinterpret_cast<uintptr_t>(in.depth) % 16 == 0);
     fblocks = in.frames * ((in.H + FK_ROWS - 1) / FK_ROWS);
     fused = compact && vec4 && in.W <= 4 * kFrontMaxThreads && fblocks <= w.lb_entries;
