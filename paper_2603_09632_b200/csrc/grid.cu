@@ -1645,6 +1645,27 @@ cudaError_t dedup_pass(const DedupSegs& sg, DedupTable* t, HashSet* hs, unsigned
 }
 
 
+__global__ void gather_status_kernel(const unsigned long long* cnts, const int32_t* grand, const int* aux,
+                                     unsigned long long* st) {
+  if (threadIdx.x < 3) st[threadIdx.x] = cnts[threadIdx.x];   // nvalid, nvox, items
+  if (threadIdx.x == 3) st[3] = (unsigned long long)(uint32_t)*grand;
+  if (threadIdx.x == 4) st[4] = aux ? (unsigned long long)*aux : 0ull;
+}
+
+// per-thread, per-device pinned landing buffer for the final read-back
+// (a pageable destination would stage every copy through a driver buffer)
+cudaError_t pinned_status(unsigned long long** out) {
+  thread_local unsigned long long* buf[16] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
+  if (!buf[dev] && (e = cudaHostAlloc(reinterpret_cast<void**>(&buf[dev]), 128, cudaHostAllocDefault)) != cudaSuccess)
+    return e;
+  *out = buf[dev];
+  return cudaSuccess;
+}
+
 cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, size_t ws_bytes, int sms,
                         cudaStream_t s) {
   const int64_t npix = in.frames * in.H * in.W;
@@ -1663,6 +1684,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   int* bbox = reinterpret_cast<int*>(b + w.off_misc);
   unsigned long long* cnts = reinterpret_cast<unsigned long long*>(b + w.off_misc + 64);  // nvalid, nvox
   int32_t* grand = reinterpret_cast<int32_t*>(b + w.off_misc + 128);
+  unsigned long long* status = reinterpret_cast<unsigned long long*>(b + w.off_misc + 192);   // 5 words
   unsigned long long* lb_status = reinterpret_cast<unsigned long long*>(b + w.off_lb);
   int32_t* block_count = reinterpret_cast<int32_t*>(lb_status);   // fused front end: per-block item counts
   out.n_new = out.n_valid = out.n_voxels = 0;
@@ -1768,9 +1790,13 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   unsigned long long hc[3] = {0, 0, 0};
   int64_t nitems = 0;
   if (!no_sync) {
-    if ((e = cudaMemcpyAsync(hb, bbox, 6 * sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-    if ((e = cudaMemcpyAsync(hc, cnts, 24, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    // bbox (misc + 0) and the counters (misc + 64) in one copy to pinned memory
+    unsigned long long* hst = nullptr;
+    if ((e = pinned_status(&hst)) != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(hst, bbox, 88, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    std::memcpy(hb, hst, 6 * sizeof(int));
+    std::memcpy(hc, hst + 8, 24);
     out.n_valid = (int64_t)hc[0];
     if (hc[0] == 0) return cudaSuccess;
     nitems = compact ? (int64_t)hc[2] : npix;   // items to sort
@@ -1921,12 +1947,19 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
                           (const int32_t*)head, (const int32_t*)grand, (int64_t)out.capacity, ea)) != cudaSuccess)
         return e;
       count_launches(2);
-      int ovf = 0;
-      if (no_sync && (e = cudaMemcpyAsync(hc, cnts, 24, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-      if ((e = cudaMemcpyAsync(&nnew, grand, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-      if ((e = cudaMemcpyAsync(&nvox, cnts + 1, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-      if (hashed && (e = cudaMemcpyAsync(&ovf, dd->aux, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+      // one read-back: the counters, the new-voxel total and the overflow flag
+      // gathered on the device, one copy into pinned host memory
+      unsigned long long* hst = nullptr;
+      if ((e = pinned_status(&hst)) != cudaSuccess) return e;
+      gather_status_kernel<<<1, 32, 0, s>>>(cnts, grand, hashed ? dd->aux : nullptr, status); count_launches(1);
+      if ((e = cudaMemcpyAsync(hst, status, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return e;
       if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+      hc[0] = hst[0];
+      hc[2] = hst[2];
+      nvox = hst[1];
+      nnew = (int32_t)hst[3];
+      const int ovf = (int)hst[4];
       if (no_sync) {
         out.n_valid = (int64_t)hc[0];
         out.n_sorted = nitems = (int64_t)hc[2];
