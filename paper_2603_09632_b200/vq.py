@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import csv
 import ctypes
+import threading
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
@@ -350,11 +351,30 @@ def warm_start(buffer, codebook: Codebook, cfg: VqConfig) -> WarmStartResult:
     return WarmStartResult(codebook=cb, used=used, degenerate=False)
 
 
+_pinned = threading.local()
+
+
+def _small_to_host(t):
+    """Read a small device tensor back through a reused pinned buffer (a
+    pageable destination stages the copy through a driver buffer)."""
+    torch = nat.torch()
+    cache = getattr(_pinned, "bufs", None)
+    if cache is None:
+        cache = _pinned.bufs = {}
+    key = (t.device.index, t.dtype, t.numel())
+    buf = cache.get(key)
+    if buf is None:
+        buf = cache[key] = torch.empty(t.numel(), dtype=t.dtype, pin_memory=True)
+    buf.copy_(t.reshape(-1), non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return buf.numpy().copy().reshape(tuple(t.shape))
+
+
 def _revive_dev(codebook: Codebook, E, N, M, delta_dead, rng, N_host=None):
     """vq.py:173-190 on device tensors (E, N, M are updated in place)."""
     t = nat.torch()
     if N_host is None:
-        N_host = to_host(N)
+        N_host = _small_to_host(N)
     dead = np.nonzero(N_host < delta_dead)[0]
     if dead.size == 0:
         return [], False
