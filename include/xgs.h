@@ -230,7 +230,11 @@ XGS_API int xgs_radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, 
  * voxel (mode 0) or the pixel-order mean over the voxel's points in that
  * frame (mode 1); voxels already in `hashset` are rejected and the new ones
  * inserted; outputs in ascending (frame, pixel) id.  Synchronises twice
- * (batch bounding box, output count). */
+ * (batch bounding box, output count).  A capacity of F * ceil(H/stride) *
+ * ceil(W/stride) rows can never overflow; with a smaller one the call returns
+ * XGS_INVALID_INPUT ("output capacity too small") AFTER the batch's new voxels
+ * were inserted into `hashset` (n_new reports how many): the map already holds
+ * them, so a retry of the same frames would reject them as occupied. */
 typedef struct {
   int64_t frames, height, width;
   const float* depth;      /* [F,H,W] */
@@ -254,10 +258,12 @@ typedef struct {
   double* color;           /* [cap,3] rgb/255 */
   double* scale;           /* [cap] */
   double* depth;           /* [cap] */
-  float* feat;             /* [cap,C] or NULL */
+  void* feat;              /* [cap,C] or NULL; element type feat_dtype */
   double* count;           /* [cap] points averaged (mode 1) or 1, nullable */
   int64_t n_new, n_valid, n_voxels; /* written by the call */
   int64_t n_sorted, sort_passes;     /* radix-sort work of the call (items, 8-bit passes) */
+  int32_t feat_dtype;      /* XGS_F32 (mode 0 only: the gathered value) or XGS_F64 (mode 0: widened;
+                              mode 1: the fp64 pixel-order mean over the voxel's members) */
 } xgs_grid_result;
 
 XGS_API int xgs_grid_sample(const xgs_grid_frames* in, void* hashset, xgs_grid_result* out, void* ws,

@@ -89,7 +89,7 @@ class GridResult(ctypes.Structure):
     """Mirror of xgs_grid_result (include/xgs.h)."""
     _fields_ = [("capacity", _i64), ("key", _vp), ("pid", _vp), ("mu", _vp), ("color", _vp), ("scale", _vp),
                 ("depth", _vp), ("feat", _vp), ("count", _vp), ("n_new", _i64), ("n_valid", _i64),
-                ("n_voxels", _i64), ("n_sorted", _i64), ("sort_passes", _i64)]
+                ("n_voxels", _i64), ("n_sorted", _i64), ("sort_passes", _i64), ("feat_dtype", ctypes.c_int32)]
 
 
 class RasterIn(ctypes.Structure):

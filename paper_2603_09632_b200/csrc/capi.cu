@@ -71,7 +71,7 @@ int check_rows(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx) {
 
 extern "C" {
 
-int xgs_abi_version(void) { return 1; }
+int xgs_abi_version(void) { return 2; }
 
 const char* xgs_last_error(void) { return g_err.c_str(); }
 
@@ -426,9 +426,12 @@ static int grid_sample_call(const xgs_grid_frames* in, void* hashset, xgs_grid_r
   const int64_t npix = in->frames * in->height * in->width;
   if (npix > 0x7fffffff) return fail(NOT_SUPPORTED, "more than 2^31-1 pixels per batch");
   if (npix > 0 && (!in->depth || !in->rot || !in->trans)) return fail(INVALID_INPUT, "null frame buffer");
-  if (in->feat && in->mode != 0) return fail(NOT_SUPPORTED, "feature gather is first-pick only");
   if (in->feat && (in->feat_c < 1 || in->feat_h < 1 || in->feat_w < 1 || !out->feat))
     return fail(INVALID_INPUT, "bad feature map");
+  if (in->feat && out->feat_dtype != XGS_F32 && out->feat_dtype != XGS_F64)
+    return fail(INVALID_INPUT, "feature output dtype must be XGS_F32 or XGS_F64");
+  if (in->feat && in->mode == 1 && out->feat_dtype != XGS_F64)
+    return fail(INVALID_INPUT, "mean-mode features are fp64 averages: feat_dtype must be XGS_F64");
   if (ws_bytes < grid_workspace_bytes(npix)) return fail(INVALID_INPUT, "workspace too small");
   GridIn gi;
   gi.frames = in->frames;
@@ -467,6 +470,7 @@ static int grid_sample_call(const xgs_grid_frames* in, void* hashset, xgs_grid_r
   go.scale = out->scale;
   go.depth = out->depth;
   go.feat = out->feat;
+  go.feat64 = out->feat_dtype == XGS_F64;
   go.count = out->count;
   cudaError_t e = grid_sample(gi, static_cast<HashSet*>(hashset), go, ws, ws_bytes, sm_count(), (cudaStream_t)stream);
   out->n_new = go.n_new;

@@ -1138,7 +1138,8 @@ struct EmitArgs {
   double* col;
   double* scale;
   double* dep;
-  float* ofeat;
+  void* ofeat;              // [cap, fc]: float (feat64 == 0) or double
+  int feat64;
   double* count;
 };
 
@@ -1169,7 +1170,13 @@ __device__ __forceinline__ void emit_one(int64_t o, int64_t p, const int32_t* __
       const int64_t uu = (int64_t)floor(ddiv(dmul((double)u, (double)(a.fh - 1)), (double)max(a.H - 1, (int64_t)1)) + 0.5);
       const int64_t vv = (int64_t)floor(ddiv(dmul((double)v, (double)(a.fw - 1)), (double)max(a.W - 1, (int64_t)1)) + 0.5);
       const float* src = a.feat + f * a.fc * a.fh * a.fw + uu * a.fw + vv;
-      for (int64_t c = 0; c < a.fc; c++) a.ofeat[o * a.fc + c] = src[c * a.fh * a.fw];
+      if (a.feat64) {
+        double* dst = static_cast<double*>(a.ofeat) + o * a.fc;
+        for (int64_t c = 0; c < a.fc; c++) dst[c] = (double)src[c * a.fh * a.fw];
+      } else {
+        float* dst = static_cast<float*>(a.ofeat) + o * a.fc;
+        for (int64_t c = 0; c < a.fc; c++) dst[c] = src[c * a.fh * a.fw];
+      }
     }
   } else {
     // mean over the voxel's points in the head's frame, sequential in pid order
@@ -1196,6 +1203,28 @@ __device__ __forceinline__ void emit_one(int64_t o, int64_t p, const int32_t* __
       a.col[o * 3 + c] = ddiv(sc[c], cnt);
     }
     if (a.count) a.count[o] = cnt;
+    if (a.feat) {
+      // per channel: the members' gathered features (supervision.py:133-147
+      // rule per member pixel) summed in fp64 in ascending pid order, / count
+      // (oracle/grid.py: np.add.at over the members, then acc / cnt)
+      const double su = (double)(a.fh - 1), sv = (double)(a.fw - 1);
+      const double hu = (double)max(a.H - 1, (int64_t)1), hv = (double)max(a.W - 1, (int64_t)1);
+      const float* fbase = a.feat + f * a.fc * a.fh * a.fw;
+      double* dst = static_cast<double*>(a.ofeat) + o * a.fc;
+      for (int64_t c = 0; c < a.fc; c++) {
+        double acc = 0.0;
+        for (int64_t i = i0; i < a.n && a.skeys[i] == key; i++) {
+          const int64_t q = a.svals[i];
+          if (q / HW != f) continue;
+          const int64_t r2 = q - f * HW;
+          const int64_t uq = r2 / a.W, vq = r2 - uq * a.W;
+          const int64_t uu = (int64_t)floor(ddiv(dmul((double)uq, su), hu) + 0.5);
+          const int64_t vv = (int64_t)floor(ddiv(dmul((double)vq, sv), hv) + 0.5);
+          acc = dadd(acc, (double)fbase[(c * a.fh + uu) * a.fw + vv]);
+        }
+        dst[c] = ddiv(acc, cnt);
+      }
+    }
   }
 }
 
@@ -1932,6 +1961,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     ea.scale = out.scale;
     ea.dep = out.depth;
     ea.ofeat = out.feat;
+    ea.feat64 = out.feat64;
     ea.count = out.count;
     for (int attempt = 0;; attempt++) {
       // exclusive popcount scan of the new-voxel bitmask, pixel-id list, emit:

@@ -150,7 +150,8 @@ struct GridOut {
   double* color;
   double* scale;
   double* depth;
-  float* feat;
+  void* feat;               // [cap, C], fp32 (feat64 == 0, first-pick only) or fp64
+  int feat64;
   double* count;
   int64_t n_new, n_valid, n_voxels;
   int64_t n_sorted, sort_passes;

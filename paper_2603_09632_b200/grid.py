@@ -103,11 +103,51 @@ class GridSampleResult:
         return int(self.pid.shape[0])
 
     def to_numpy(self):
-        h = lambda t: None if t is None else t.cpu().numpy()
-        return dict(key=h(self.key).view(np.uint64), pid=h(self.pid), mu=h(self.mu), color=h(self.color),
-                    scale=h(self.scale), depth=h(self.depth), count=h(self.count), feature=h(self.feature),
-                    n_valid=self.n_valid, n_voxels=self.n_voxels, n_sorted=self.n_sorted,
-                    sort_passes=self.sort_passes)
+        """All fields in ONE device->host copy: the per-voxel columns are packed
+        into one device buffer (a few µs) and read back through a reused
+        pinned landing buffer (8 pageable copies would each stage through a
+        driver buffer and run at about half the PCIe rate)."""
+        t = nat.torch()
+        n = len(self)
+        cols = [self.key.view(t.float64), self.pid.view(t.float64), self.mu.reshape(-1), self.color.reshape(-1),
+                self.scale, self.depth, self.count]
+        feat = self.feature
+        if feat is not None:
+            cols.append(feat.reshape(-1).to(t.float64) if feat.dtype == t.float64 else
+                        feat.reshape(-1).view(t.int32).to(t.float64))    # fp32 bits carried losslessly
+        packed = t.cat(cols) if n else t.empty(0, dtype=t.float64, device="cuda")
+        host = _pinned_landing(packed.numel())
+        host[:packed.numel()].copy_(packed, non_blocking=True)
+        t.cuda.current_stream().synchronize()
+        a = host[:packed.numel()].numpy().copy()
+        o = [0]
+
+        def take(m):
+            r = a[o[0]:o[0] + m]
+            o[0] += m
+            return r
+        out = dict(key=take(n).view(np.uint64), pid=take(n).view(np.int64), mu=take(3 * n).reshape(n, 3),
+                   color=take(3 * n).reshape(n, 3), scale=take(n), depth=take(n), count=take(n), feature=None,
+                   n_valid=self.n_valid, n_voxels=self.n_voxels, n_sorted=self.n_sorted,
+                   sort_passes=self.sort_passes)
+        if feat is not None:
+            C = int(feat.shape[1])
+            f = take(n * C)
+            out["feature"] = (f if feat.dtype == t.float64 else f.astype(np.int32).view(np.float32)).reshape(n, C)
+        return out
+
+
+_landing = {}
+
+
+def _pinned_landing(numel):
+    """Grow-only pinned fp64 host buffer per device for GridSampleResult reads."""
+    t = nat.torch()
+    dev = t.cuda.current_device()
+    buf = _landing.get(dev)
+    if buf is None or buf.numel() < numel:
+        buf = _landing[dev] = t.empty(max(numel, 1 << 16), dtype=t.float64, pin_memory=True)
+    return buf
 
 
 def _intr4(intr):
@@ -201,15 +241,22 @@ class GridSampler:
                          t.empty((F, H, W, 3), dtype=t.uint8, device="cuda") if col is not None else None)
                 self._stage = stage
         feat = _dev(features, t.float32) if features is not None else None
-        if feat is not None and feat.dim() == 3:
-            feat = feat.unsqueeze(0)
+        if feat is not None:
+            # (F, C, Hf, Wf): one map per frame (supervision.py:133-147 gather);
+            # a single (C, Hf, Wf) map is accepted for a one-frame batch only
+            if feat.dim() == 3 and F == 1:
+                feat = feat.unsqueeze(0)
+            if feat.dim() != 4 or int(feat.shape[0]) != F or min(int(v) for v in feat.shape[1:]) < 1:
+                raise InvalidInputError(f"features must be (F={F}, C, Hf, Wf); got {tuple(feat.shape)}")
         s = self.stride
         cap = max(1, F * ((H + s - 1) // s) * ((W + s - 1) // s))
         C = int(feat.shape[1]) if feat is not None else 0
         # one fp64 allocation for every per-voxel field (key and pid as int64
         # views): [key | pid | mu x3 | color x3 | scale | depth | count]
         flat = t.empty(11 * cap, dtype=t.float64, device="cuda")
-        ofeat = t.empty((cap, C), dtype=t.float32, device="cuda") if feat is not None else None
+        # first-pick copies the gathered fp32 value; mean mode averages in fp64
+        fdt = t.float32 if self.mode == "first" else t.float64
+        ofeat = t.empty((cap, C), dtype=fdt, device="cuda") if feat is not None else None
         b = flat.data_ptr()
         fx, fy, cx, cy = self.intr
         fr = nat.GridFrames(F, H, W, d.data_ptr(), col.data_ptr() if col is not None else None, R.data_ptr(),
@@ -218,7 +265,8 @@ class GridSampler:
                             C, int(feat.shape[2]) if feat is not None else 0,
                             int(feat.shape[3]) if feat is not None else 0)
         res = nat.GridResult(cap, b, b + 8 * cap, b + 16 * cap, b + 40 * cap, b + 64 * cap, b + 72 * cap,
-                             ofeat.data_ptr() if ofeat is not None else None, b + 80 * cap, 0, 0, 0, 0, 0)
+                             ofeat.data_ptr() if ofeat is not None else None, b + 80 * cap, 0, 0, 0, 0, 0,
+                             nat.F32 if fdt == t.float32 else nat.F64)
         ws = nat.workspace("grid", nat.lib().xgs_grid_workspace(F * H * W))
         if host:
             nat.call("xgs_grid_sample_h2d", ctypes.byref(fr), stage[1].data_ptr(),
@@ -244,20 +292,3 @@ def radix_sort_pairs(keys, vals, bits: int = 64):
     nat.call("xgs_radix_sort_pairs_u64", nat.ptr(keys), nat.ptr(vals), n, int(bits), nat.ptr(ws), ws.numel(),
              nat.stream_ptr())
     return keys, vals
-
-
-def smoke_check():
-    """One small batch against the CPU oracle (used by __graft_entry__.smoke)."""
-    from oracle import grid as og
-    rng = np.random.default_rng(0)
-    H, W = 48, 64
-    depth = rng.uniform(0.5, 5.0, (2, H, W)).astype(np.float32)
-    depth[rng.random((2, H, W)) < 0.05] = 0
-    color = rng.integers(0, 256, (2, H, W, 3), dtype=np.uint8)
-    R = np.stack([np.eye(3), np.eye(3)])
-    tr = np.array([[0.0, 0, 0], [0.05, 0, 0]])
-    intr = (60.0, 60.0, 23.5, 31.5)
-    gs = GridSampler(intr, 0.05)
-    got = gs.sample(depth, (R, tr), color).to_numpy()
-    ref = og.grid_sample([(depth[f], color[f], R[f], tr[f]) for f in range(2)], np.array(intr), 0.05, set())
-    assert np.array_equal(got["pid"], ref["pid"]) and np.array_equal(got["mu"], ref["mu"]), "grid smoke mismatch"

@@ -327,3 +327,64 @@ def test_hashset_semantics(xs):
     probe = np.concatenate([keys[:100], rng.integers(0, 1 << 62, 100, dtype=np.int64).astype(np.uint64)])
     got = hs.contains(probe).cpu().numpy()
     assert np.array_equal(got, np.array([int(p) in seen for p in probe]))
+
+
+# ------------------------------------------------------------ per-voxel features
+# Feature gather rule: supervision.py:133-147 (per-frame (C, Hf, Wf) map,
+# nearest lattice cell).  First-pick copies the representative's gathered
+# value; mean mode averages the members' values in fp64, pid order
+# (oracle/grid.py, np.add.at then / count).
+
+@pytest.mark.parametrize("mode", ["first", "mean"])
+@pytest.mark.parametrize("force_sort", ["0", "1"])
+@pytest.mark.parametrize("W", [128, 130])          # fused front end (W % 4 == 0) / two-kernel front end
+def test_grid_features_match_oracle(xs, mode, force_sort, W):
+    import os
+    grid, _, synth = xs
+    frames, intr4 = _scene(synth, 11, 96, W, 3, spheres=True)
+    rng = np.random.default_rng(12)
+    feats = rng.normal(size=(3, 16, 24, 33)).astype(np.float32)
+    D = np.stack([f[0] for f in frames])
+    C = np.stack([f[1] for f in frames])
+    R = np.stack([f[2] for f in frames])
+    T = np.stack([f[3] for f in frames])
+    os.environ["XGS_GRID_SORT"] = force_sort
+    try:
+        gs = grid.GridSampler(intr4, 0.02, mode=mode)
+        warm = og.pack_key(np.array([0, 1]), np.array([0, 0]), np.array([0, 0]))
+        gs.occupied.insert(warm)
+        got = gs.sample(D, (R, T), C, features=feats).to_numpy()
+    finally:
+        os.environ.pop("XGS_GRID_SORT", None)
+    ref = og.grid_sample(frames, np.array(intr4), 0.02, set(int(k) for k in warm), mode=mode, features=list(feats))
+    assert got["feature"].shape == ref["feature"].shape
+    assert got["feature"].dtype == (np.float32 if mode == "first" else np.float64)
+    for name in ("key", "pid", "mu", "color", "feature"):
+        assert np.array_equal(np.asarray(got[name], dtype=ref[name].dtype), ref[name]), name
+    if mode == "mean":
+        assert np.array_equal(got["count"], ref["count"])
+
+
+def test_grid_features_device_tensors_and_shape_errors(xs, cuda):
+    import torch
+    grid, _, synth = xs
+    frames, intr4 = _scene(synth, 13, 48, 64, 2)
+    feats = np.random.default_rng(14).normal(size=(2, 4, 48, 64)).astype(np.float32)
+    D = torch.from_numpy(np.stack([f[0] for f in frames])).cuda()
+    R = np.stack([f[2] for f in frames])
+    T = np.stack([f[3] for f in frames])
+    from paper_2603_09632_b200.errors import InvalidInputError
+    gs = grid.GridSampler(intr4, 0.03)
+    with pytest.raises(InvalidInputError):       # one map for a two-frame batch
+        gs.sample(D, (R, T), features=feats[0])
+    with pytest.raises(InvalidInputError):       # wrong frame count
+        gs.sample(D, (R, T), features=feats[:1])
+    r = gs.sample(D, (R, T), features=torch.from_numpy(feats).cuda())
+    assert r.feature.is_cuda and r.feature.shape == (len(r), 4)
+    ref = og.grid_sample([(f[0], f[1], f[2], f[3]) for f in frames], np.array(intr4), 0.03, set(),
+                         features=list(feats))
+    assert np.array_equal(r.feature.cpu().numpy().astype(np.float64), ref["feature"])
+    # single-frame batch: a (C, Hf, Wf) map is accepted
+    one = grid.GridSampler(intr4, 0.03).sample(D[0], (R[:1], T[:1]), features=feats[0]).to_numpy()
+    ref1 = og.grid_sample([frames[0]], np.array(intr4), 0.03, set(), features=[feats[0]])
+    assert np.array_equal(one["feature"].astype(np.float64), ref1["feature"])

@@ -23,7 +23,7 @@ def test_library_exports_every_declared_symbol():
     L = ctypes.CDLL(_native.LIB_PATH)
     missing = [n for n in declared() if not hasattr(L, n)]
     assert not missing, missing
-    assert L.xgs_abi_version() == 1
+    assert L.xgs_abi_version() == 2
 
 
 def test_ctypes_table_matches_header():

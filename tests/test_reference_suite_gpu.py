@@ -1,0 +1,77 @@
+"""The reference's OWN test module for the hot path (semsplat pkg/tests/test_vq.py,
+unmodified) run against the B200 path: paper_2603_09632_b200.reference_shim is
+installed over the pip-installed reference (baseline/_ref, see
+tools/install_reference.sh) before the module is imported, so every
+``semsplat.vq`` call in it -- with the reference's own Codebook /
+FeatureReservoir objects and error classes -- runs on libxgs.
+
+Skipped when baseline/_ref (git-ignored; it travels to the GPU box with the
+working tree) was not installed."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+SUITE = os.path.join(REF, "semsplat_tests")
+
+
+def _run(test_file, extra=()):
+    if not os.path.isfile(os.path.join(SUITE, test_file)):
+        pytest.skip("reference not installed under baseline/_ref (tools/install_reference.sh)")
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([REF, os.path.join(ROOT, "tests"), ROOT, env.get("PYTHONPATH", "")])
+    env["PYTHONDONTWRITEBYTECODE"] = "1"
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "_ref_shim_plugin", "-p", "no:cacheprovider",
+           "--rootdir", SUITE, "-o", "addopts=", os.path.join(SUITE, test_file), *extra]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1200, cwd=SUITE)
+    return r
+
+
+def test_reference_test_vq_passes_through_shim(cuda):
+    r = _run("test_vq.py")
+    print(r.stdout[-4000:])
+    assert "B200 shim installed over semsplat: 13 functions" in r.stdout
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " 24 passed" in r.stdout or "24 passed" in r.stdout, r.stdout[-2000:]
+
+
+def test_shim_routes_to_native(cuda):
+    """The installed functions are the adapters (not the NumPy reference), they
+    return the reference's types and raise the reference's errors."""
+    if not os.path.isdir(os.path.join(REF, "semsplat")):
+        pytest.skip("reference not installed under baseline/_ref")
+    sys.path.insert(0, REF)
+    try:
+        import numpy as np
+        import semsplat.core as rc
+        import semsplat.errors as re_
+        import semsplat.vq as rv
+
+        from paper_2603_09632_b200 import _native, reference_shim
+        reference_shim.install()
+        try:
+            assert getattr(rv.online_step, "__b200__", False)
+            rng = np.random.default_rng(0)
+            E = rng.normal(size=(8, 5))
+            cb = rc.Codebook(E=E, N=np.zeros(8), M=np.zeros((8, 5)), lam=0.9, epsilon=1e-5,
+                             reservoir=rc.FeatureReservoir(16, 5))
+            n0 = _native.launch_count()
+            cb2, res = rv.online_step(cb, rng.normal(size=(40, 5)), rv.VqConfig(K=8, lam=0.9), rng)
+            assert _native.launch_count() > n0          # libxgs kernels ran
+            assert isinstance(cb2, rc.Codebook) and isinstance(res, rv.ReviveResult)
+            assert cb2.reservoir is cb.reservoir and len(cb.reservoir) == 16
+            with pytest.raises(re_.InvalidInputError):
+                rv.assign(np.zeros(4), cb2)
+            with pytest.raises(re_.InvalidStateError):
+                rv.assign_batch(np.zeros((1, 0)), rc.Codebook(E=np.zeros((0, 0)), N=np.zeros(0),
+                                                              M=np.zeros((0, 0)), lam=0.5, epsilon=1e-5))
+        finally:
+            reference_shim.uninstall()
+    finally:
+        sys.path.remove(REF)
