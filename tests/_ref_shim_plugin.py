@@ -15,5 +15,8 @@ from paper_2603_09632_b200 import reference_shim  # noqa: E402
 INSTALLED = reference_shim.install()
 
 
-def pytest_report_header(config):
-    return f"B200 shim installed over semsplat: {len(INSTALLED)} functions"
+def pytest_terminal_summary(terminalreporter):
+    from paper_2603_09632_b200 import _native
+    n = _native.launch_count() if _native._lib is not None else 0
+    terminalreporter.write_line(f"B200 shim installed over semsplat: {len(INSTALLED)} functions; "
+                                f"libxgs kernel launches: {n}")

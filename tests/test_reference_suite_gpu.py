@@ -36,9 +36,11 @@ def _run(test_file, extra=()):
 def test_reference_test_vq_passes_through_shim(cuda):
     r = _run("test_vq.py")
     print(r.stdout[-4000:])
-    assert "B200 shim installed over semsplat: 13 functions" in r.stdout
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
-    assert " 24 passed" in r.stdout or "24 passed" in r.stdout, r.stdout[-2000:]
+    assert "24 passed" in r.stdout, r.stdout[-2000:]
+    import re
+    m = re.search(r"B200 shim installed over semsplat: 13 functions; libxgs kernel launches: (\d+)", r.stdout)
+    assert m and int(m.group(1)) > 1000, r.stdout[-2000:]     # the suite ran on libxgs, not NumPy
 
 
 def test_shim_routes_to_native(cuda):
