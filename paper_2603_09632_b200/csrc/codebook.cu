@@ -265,12 +265,15 @@ cudaError_t launch_softmax_rows(const double* logits, int64_t n, int64_t k, int 
   ProfScope prof("cb_rows", s);
   const bool cache = k <= kCbCacheK;
   const size_t smem = cache ? sizeof(double) * kCbWarps * (size_t)k : 0;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(cb_rows_kernel<CB_WEIGHTS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbWarps * kCbCacheK * 8);
-    cudaFuncSetAttribute(cb_rows_kernel<CB_VJP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCbWarps * kCbCacheK * 8);
-    attr_set = true;
-  }
+  cudaError_t ea = attr_once(kAttrCodebook, [] {
+    cudaError_t r = cudaFuncSetAttribute(cb_rows_kernel<CB_WEIGHTS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kCbWarps * kCbCacheK * 8);
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(cb_rows_kernel<CB_VJP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kCbWarps * kCbCacheK * 8);
+    return r;
+  });
+  if (ea != cudaSuccess) return ea;
   const unsigned b = cb_blocks(n);
   const int T = kCbWarps * 32;
   if (mode == CB_ENTROPY) {

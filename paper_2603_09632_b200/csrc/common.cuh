@@ -13,6 +13,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace xgs {
 
 enum Status : int { OK = 0, INVALID_INPUT = 1, INVALID_STATE = 2, CUDA_ERROR = 3, NOT_SUPPORTED = 4 };
@@ -41,6 +43,31 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// Kernel attributes (cudaFuncSetAttribute) belong to the device context that
+// is current when they are set, so a process driving several GPUs must set
+// them on each: attr_once runs a site's setter once per (site, device) and
+// records it only when it succeeded.
+enum AttrSite : int {
+  kAttrScreen0 = 0, kAttrScreen1, kAttrScreen2, kAttrSeed, kAttrUpdate, kAttrGridFront, kAttrGridSort,
+  kAttrGridHash, kAttrCodebook, kAttrSites
+};
+inline std::atomic<uint32_t>* attr_table() {
+  static std::atomic<uint32_t> done[64];
+  return done;
+}
+template <typename F>
+inline cudaError_t attr_once(int site, F&& set) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return set();
+  std::atomic<uint32_t>& m = attr_table()[dev];
+  if (m.load(std::memory_order_acquire) & (1u << site)) return cudaSuccess;
+  e = set();
+  if (e == cudaSuccess) m.fetch_or(1u << site, std::memory_order_acq_rel);
+  return e;
 }
 
 inline size_t dtype_size(int dtype) { return dtype == F64 ? 8 : dtype == F32 ? 4 : 2; }

@@ -290,6 +290,55 @@ compact_keys_kernel(const uint64_t* __restrict__ kin, int64_t n, int64_t W, uint
 }
 
 
+// ---------------------------------------------------------------- batch dedup table
+// First-pick mode needs only every voxel's lowest pixel id, which a batch
+// table {key, min pixel id} produces in any insertion order (one claim per
+// voxel, an atomicMin of the pixel id only when the slot's current id is
+// larger), so the front end inserts its surviving pixels straight from
+// shared memory: no item list is materialised in HBM.
+constexpr int kDedupProbe = 256;
+// Table slot = 16 bytes {key u64, pixel id u32, pad u32} (all ones = empty),
+// so one 16-byte load returns a slot's key and pixel id together (each probe
+// costs one L2 sector).  Inserts are issued four per thread with their table
+// loads together.
+
+__device__ __forceinline__ ulonglong2 slot_ld(const unsigned long long* slots, uint64_t h) {
+  return __ldcg(reinterpret_cast<const ulonglong2*>(slots + 2 * h));
+}
+__device__ __forceinline__ uint32_t* slot_pid(unsigned long long* slots, uint64_t h) {
+  return reinterpret_cast<uint32_t*>(slots + 2 * h + 1);
+}
+
+__device__ __forceinline__ uint32_t dd_hash(uint64_t key) {
+  uint32_t h = (uint32_t)key * 0x9E3779B1u ^ (uint32_t)(key >> 32) * 0x85EBCA77u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  return h ^ (h >> 13);
+}
+
+// finish one insert whose first slot `cur` (at h) was already loaded
+__device__ __forceinline__ void dd_insert_finish(unsigned long long* slots, uint64_t mask, uint64_t h, ulonglong2 cur,
+                                                 uint64_t key, uint32_t pid, int* overflow) {
+  int t = 0;
+  for (; t < kDedupProbe; t++) {
+    if (cur.x == EMPTY) {
+      const unsigned long long prev = atomicCAS(slots + 2 * h, (unsigned long long)EMPTY, (unsigned long long)key);
+      cur.x = prev == EMPTY ? key : prev;
+    }
+    if (cur.x == key) break;
+    h = (h + 1) & mask;
+    cur = slot_ld(slots, h);
+  }
+  if (t == kDedupProbe) {
+    *overflow = 1;
+    return;
+  }
+  // a stale pid read is >= the slot's current pid (pids only decrease), so
+  // skipping the atomic when it is already <= pid is exact
+  if ((uint32_t)cur.y > pid) atomicMin(slot_pid(slots, h), pid);
+}
+
+
 // ---------------------------------------------------------------- G1 fused front end
 // First-pick mode on W % 4 == 0, W <= 4 * kFrontMaxThreads: keys, left/up dedup
 // and ordered compaction in one pass over the depth.  A block owns FK_ROWS rows
@@ -299,10 +348,13 @@ compact_keys_kernel(const uint64_t* __restrict__ kin, int64_t n, int64_t W, uint
 // barrier), so only the previous row's keys stay in registers.  The segments
 // are laid out in (row, warp) = pixel order; after one barrier an exclusive
 // scan of the segment counts gives every segment its offset inside the block's
-// fixed output slot plus the block's item count.  The sort's rekey pass / the
-// hash dedup gather the slots densely (no block waits on another), so the
-// items enter the dedup in ascending pixel order, exactly as the two-kernel
-// path writes them.  A pixel is dropped when its left neighbour (same warp) or
+// fixed output slot plus the block's item count.  FRONT_SORT: the sort's
+// rekey pass gathers the slots densely (no block waits on another), so the
+// items enter the sort in ascending pixel order, exactly as the two-kernel
+// path writes them.  FRONT_INSERT (first-pick hash path): each warp inserts its
+// segments' items into the batch dedup table instead, densely (no divergence)
+// and four table loads in flight per lane; while a block waits on L2 the other
+// resident blocks compute, so no item list goes through HBM.  A pixel is dropped when its left neighbour (same warp) or
 // upper neighbour has the same key: any earlier pixel of the same voxel may
 // stand in, so the lowest pixel id of every voxel always survives (a warp's
 // first column keeps its item; the dedup downstream removes the repeat).
@@ -387,12 +439,15 @@ __device__ __forceinline__ u64 sub2_rd(u64 a, u64 b) {
 }
 constexpr float kDl = 0x1p-20f * 1.002f + 0x1p-21f;
 
-template <bool BOX>
+enum FrontMode : int { FRONT_SORT = 1, FRONT_INSERT = 2 };
+
+template <int MODE>
 __global__ void __launch_bounds__(kFrontMaxThreads, kFrontBlocksPerSM)
 grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int stride, const double* __restrict__ rot,
                   const double* __restrict__ trans, Cam cam, CamF cf, uint64_t* __restrict__ kout,
                   uint32_t* __restrict__ vout, int* bbox, unsigned long long* cnts, int32_t* __restrict__ block_count,
-                  unsigned bid0) {
+                  unsigned bid0, unsigned long long* __restrict__ slots, uint64_t mask, int* overflow) {
+  constexpr bool BOX = MODE == FRONT_SORT;
   constexpr int NR = FK_ROWS;
   constexpr float XB = 9437184.f;   // 2^23 + 2^20
   // PEND marks a pixel the fp32 filter could not decide: it compares unequal to
@@ -586,6 +641,54 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
         }
     }
   }
+  if (MODE == FRONT_INSERT) {
+    // ---- this warp's segments (rows rr, warp) into the batch table ----
+    __syncthreads();   // pending keys resolved by any thread
+    uint32_t segc[NR], tot = 0;
+#pragma unroll
+    for (int rr = 0; rr < NR; rr++) {
+      segc[rr] = rr < nr ? s_cnt[rr * nw + warp] : 0u;
+      tot += segc[rr];
+    }
+    int ovf = 0;
+    const uint32_t pcol = fbase + (uint32_t)warp * kFrontSeg;
+    for (uint32_t q0 = lane; q0 < tot; q0 += 4 * 32) {
+      uint64_t key[4], h[4];
+      uint32_t pid[4];
+      ulonglong2 cur[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        uint32_t q = q0 + 32 * j;
+        key[j] = KEY_INVALID;
+        if (q < tot) {
+          int rr = 0;
+#pragma unroll
+          for (int i = 0; i < NR - 1; i++)
+            if (rr == i && q >= segc[i]) {
+              q -= segc[i];
+              rr = i + 1;
+            }
+          const uint32_t o = (uint32_t)(rr * nw + warp) * kFrontSeg + q;
+          key[j] = sk[o];
+          pid[j] = pcol + (uint32_t)(r0 + rr) * Wu + sc[o];
+        }
+        if (key[j] != KEY_INVALID) {
+          h[j] = dd_hash(key[j]) & mask;
+          cur[j] = slot_ld(slots, h[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        if (key[j] != KEY_INVALID) dd_insert_finish(slots, mask, h[j], cur[j], key[j], pid[j], &ovf);
+    }
+    cnt = __reduce_add_sync(FULL, cnt);
+    if (lane == 0) {
+      if (cnt) atomicAdd(cnts, (unsigned long long)cnt);
+      if (tot) atomicAdd(cnts + 2, (unsigned long long)tot);
+    }
+    if (__any_sync(FULL, ovf) && lane == 0) *overflow = 1;
+    return;
+  }
   // ---- exclusive scan of the segment counts (warp 0; nseg <= 96) ----
   if (warp == 0) {
     uint32_t v[3], run = 0;
@@ -688,9 +791,7 @@ constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS; // 4096
 constexpr int RADIX = 256;
 constexpr int STAGE_BYTES_SORT = SORT_TILE * 12;   // u64 keys + u32 values (u32 keys use 8 B)
 
-bool sort_attr_set = false;
 cudaError_t sort_init();
-bool front_attr_set = false;
 cudaError_t front_init();
 
 template <typename K>
@@ -938,24 +1039,25 @@ bool sort_forced() {
 }
 
 cudaError_t front_init() {
-  if (front_attr_set) return cudaSuccess;
-  const int bytes = (int)front_smem_bytes(kFrontWarps);
-  cudaError_t e = cudaFuncSetAttribute(grid_front_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(grid_front_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) front_attr_set = true;
-  return e;
+  return attr_once(kAttrGridFront, [] {
+    const int bytes = (int)front_smem_bytes(kFrontWarps);
+    cudaError_t e = cudaFuncSetAttribute(grid_front_kernel<FRONT_SORT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         bytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(grid_front_kernel<FRONT_INSERT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    return e;
+  });
 }
 
 cudaError_t sort_init() {
-  if (sort_attr_set) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(sort_downsweep_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       STAGE_BYTES_SORT);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(sort_downsweep_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SORT_TILE * 8);
-  if (e == cudaSuccess) sort_attr_set = true;
-  return e;
+  return attr_once(kAttrGridSort, [] {
+    cudaError_t e = cudaFuncSetAttribute(sort_downsweep_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         STAGE_BYTES_SORT);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(sort_downsweep_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               SORT_TILE * 8);
+    return e;
+  });
 }
 
 // ---------------------------------------------------------------- exclusive scan (int32)
@@ -987,12 +1089,6 @@ __device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* sm, int32
   __syncthreads();
   return before;
 }
-
-// scan input adaptor: a 32-pixel flag word counts as its popcount
-struct PopcWord {
-  unsigned w;
-  __device__ __forceinline__ explicit operator int32_t() const { return __popc(w); }
-};
 
 template <typename T>
 __global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const T* __restrict__ in, int64_t n, int32_t* sums) {
@@ -1228,26 +1324,6 @@ __device__ __forceinline__ void emit_one(int64_t o, int64_t p, const int32_t* __
   }
 }
 
-// Pixel ids of the new voxels in ascending order: one thread per 32-pixel
-// word of the new-voxel bitmask writes its set bits at the word's exclusive
-// popcount offset (rows beyond `capacity` are not written; the host reports
-// the error after the final read-back).
-__global__ void __launch_bounds__(256)
-grid_pidlist_kernel(const unsigned* __restrict__ flag_bits, const int32_t* __restrict__ wpos, int64_t nwords,
-                    int64_t capacity, int64_t* __restrict__ pid_out) {
-  pdl_wait();
-  for (int64_t wi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; wi < nwords; wi += (int64_t)gridDim.x * blockDim.x) {
-    unsigned word = flag_bits[wi];
-    int64_t o = wpos[wi];
-    while (word) {
-      const int b = __ffs(word) - 1;
-      word &= word - 1;
-      if (o < capacity) pid_out[o] = wi * 32 + b;
-      o++;
-    }
-  }
-}
-
 // One thread per new voxel; the count comes from device memory (the scan's
 // total), so the emit is queued before the host reads it back.
 __global__ void __launch_bounds__(128)
@@ -1468,112 +1544,227 @@ size_t grid_workspace_bytes(int64_t npix) { return grid_ws(npix).total; }
 // is bounded; an overflow (table too small for the batch's distinct voxels)
 // skips pass 2 (the map is untouched) and the host retries with a table sized
 // for every item.
-constexpr int kDedupProbe = 256;
-constexpr int64_t kDedupSeg = 4096;   // dense item lists: segment length
 
-struct DedupSegs {   // fused front: block b's items sit in its slot; else one dense list
-  const uint64_t* k;
-  const uint32_t* v;
-  const int32_t* count;   // per-block item counts (fused) or nullptr
-  int64_t nseg, H, W, n_dense;
-  __device__ __forceinline__ void seg(int64_t b, int64_t& base, int64_t& cnt) const {
-    if (count) {
-      const int64_t rbf = (H + FK_ROWS - 1) / FK_ROWS;
-      base = ((b / rbf) * H + (b % rbf) * FK_ROWS) * W;
-      cnt = count[b];
-    } else {
-      base = b * kDedupSeg;
-      cnt = min(kDedupSeg, n_dense - base);
-    }
+// Other frame shapes (W > 4 * kFrontMaxThreads): the per-pixel keys of
+// grid_keys_kernel inserted directly (left-neighbour dedup only).
+__global__ void __launch_bounds__(256)
+dd_insert_pixels_kernel(const uint64_t* __restrict__ keys, int64_t n, int64_t W, unsigned long long* slots,
+                        uint64_t mask, unsigned long long* cnts, int* overflow) {
+  pdl_wait();
+  unsigned nitems = 0;
+  int ovf = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = __ldg(keys + i);
+    if (key == KEY_INVALID) continue;
+    if (i % W != 0 && __ldg(keys + i - 1) == key) continue;
+    const uint64_t h = dd_hash(key) & mask;
+    dd_insert_finish(slots, mask, h, slot_ld(slots, h), key, (uint32_t)i, &ovf);
+    nitems++;
   }
-};
-
-// Table slot = 16 bytes {key u64, pixel id u32, pad u32} (all ones = empty),
-// so one 16-byte load returns a slot's key and pixel id together (each probe
-// costs one L2 sector).  Items are processed four per thread per step with
-// their table loads issued together.
-constexpr int kDedupILP = 4;
-
-__device__ __forceinline__ ulonglong2 slot_ld(const unsigned long long* slots, uint64_t h) {
-  return __ldcg(reinterpret_cast<const ulonglong2*>(slots + 2 * h));
+  nitems = __reduce_add_sync(FULL, nitems);
+  if ((threadIdx.x & 31) == 0 && nitems) atomicAdd(cnts + 2, (unsigned long long)nitems);
+  if (__any_sync(FULL, ovf) && (threadIdx.x & 31) == 0) *overflow = 1;
 }
-__device__ __forceinline__ uint32_t* slot_pid(unsigned long long* slots, uint64_t h) {
-  return reinterpret_cast<uint32_t*>(slots + 2 * h + 1);
-}
+
+// Pass 2 over the table (each occupied slot = one voxel of the batch with its
+// lowest pixel id): map test (insert-if-absent into the occupancy set), new
+// voxels flagged in the pixel bitmask, slot emptied for the next batch.  Four
+// slots per thread per step with their map probes issued together.  Also
+// clears the emission look-back statuses for grid_pidlist_lb_kernel.
+constexpr int kScanILP = 4;
 
 __global__ void __launch_bounds__(256)
-dd_insert_kernel(DedupSegs sg, unsigned long long* slots, uint64_t mask, int* overflow) {
+dd_scan_map_kernel(unsigned long long* slots, int64_t cap, const int* overflow, unsigned long long* table,
+                   uint64_t tmask, unsigned long long* set_count, unsigned* flag_bits, unsigned long long* nvox,
+                   unsigned long long* lb_status, int64_t lb_tiles) {
   pdl_wait();
-  for (int64_t b = blockIdx.x; b < sg.nseg; b += gridDim.x) {
-    int64_t base, cnt;
-    sg.seg(b, base, cnt);
-    for (int64_t i0 = threadIdx.x; i0 < cnt; i0 += kDedupILP * blockDim.x) {
-      uint64_t key[kDedupILP], h[kDedupILP];
-      uint32_t pid[kDedupILP];
-      ulonglong2 cur[kDedupILP];
-#pragma unroll
-      for (int j = 0; j < kDedupILP; j++) {
-        const int64_t i = i0 + j * blockDim.x;
-        key[j] = i < cnt ? __ldg(sg.k + base + i) : KEY_INVALID;
-        pid[j] = i < cnt ? __ldg(sg.v + base + i) : 0u;
-      }
-#pragma unroll
-      for (int j = 0; j < kDedupILP; j++) {
-        h[j] = mix64(key[j]) & mask;
-        cur[j] = key[j] != KEY_INVALID ? slot_ld(slots, h[j]) : make_ulonglong2(0ull, 0ull);
-      }
-#pragma unroll
-      for (int j = 0; j < kDedupILP; j++) {
-        if (key[j] == KEY_INVALID) continue;
-        int t = 0;
-        for (; t < kDedupProbe; t++) {
-          if (cur[j].x == EMPTY) {
-            const unsigned long long prev =
-                atomicCAS(slots + 2 * h[j], (unsigned long long)EMPTY, (unsigned long long)key[j]);
-            cur[j].x = prev == EMPTY ? key[j] : prev;
-          }
-          if (cur[j].x == key[j]) break;
-          h[j] = (h[j] + 1) & mask;
-          cur[j] = slot_ld(slots, h[j]);
-        }
-        if (t == kDedupProbe) {
-          *overflow = 1;
-          continue;
-        }
-        if ((uint32_t)cur[j].y > pid[j]) atomicMin(slot_pid(slots, h[j]), pid[j]);
-      }
-    }
-  }
-}
-
-// Pass 2: every occupied slot is one voxel of the batch and holds its lowest
-// pixel id, so a sequential scan of the table (not another probe per item)
-// runs the map test (insert-if-absent into the occupancy set), flags new
-// voxels in the pixel bitmask and empties the slot for the next batch.
-__global__ void __launch_bounds__(256)
-dd_scan_kernel(unsigned long long* slots, int64_t cap, const int* overflow, unsigned long long* table,
-               uint64_t tmask, unsigned long long* set_count, unsigned* flag_bits, unsigned long long* nvox) {
-  pdl_wait();
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = gt; i < lb_tiles; i += gs) lb_status[i] = 0ull;
   if (*(volatile const int*)overflow) return;   // the host resets the whole table
   unsigned newc = 0, vox = 0;
-  for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < cap; h += (int64_t)gridDim.x * blockDim.x) {
-    const ulonglong2 sl = slot_ld(slots, (uint64_t)h);
-    if (sl.x == EMPTY) continue;
-    vox++;
-    const uint32_t pid = (uint32_t)sl.y;
-    if (hs_insert_probe(table, tmask, sl.x)) {
-      atomicOr(flag_bits + (pid >> 5), 1u << (pid & 31));
-      newc++;
+  for (int64_t h0 = gt; h0 < cap; h0 += kScanILP * gs) {
+    ulonglong2 sl[kScanILP];
+    uint64_t th[kScanILP];
+    unsigned long long tv[kScanILP];
+#pragma unroll
+    for (int j = 0; j < kScanILP; j++) {
+      const int64_t hh = h0 + j * gs;
+      sl[j] = hh < cap ? slot_ld(slots, (uint64_t)hh) : make_ulonglong2(EMPTY, EMPTY);
     }
-    *reinterpret_cast<ulonglong2*>(slots + 2 * h) = make_ulonglong2(~0ull, ~0ull);
+#pragma unroll
+    for (int j = 0; j < kScanILP; j++)
+      if (sl[j].x != EMPTY) {
+        th[j] = mix64(sl[j].x) & tmask;
+        tv[j] = __ldcg(table + th[j]);
+      }
+#pragma unroll
+    for (int j = 0; j < kScanILP; j++) {
+      if (sl[j].x == EMPTY) continue;
+      vox++;
+      const uint64_t key = sl[j].x;
+      uint64_t hh = th[j];
+      unsigned long long v = tv[j];
+      bool isnew;
+      while (true) {
+        if (v == EMPTY) {
+          v = atomicCAS(table + hh, (unsigned long long)EMPTY, (unsigned long long)key);
+          if (v == EMPTY) {
+            isnew = true;
+            break;
+          }
+        }
+        if (v == key) {
+          isnew = false;
+          break;
+        }
+        hh = (hh + 1) & tmask;
+        v = __ldcg(table + hh);
+      }
+      if (isnew) {
+        const uint32_t pid = (uint32_t)sl[j].y;
+        atomicOr(flag_bits + (pid >> 5), 1u << (pid & 31));
+        newc++;
+      }
+      *reinterpret_cast<ulonglong2*>(slots + 2 * (h0 + j * gs)) = make_ulonglong2(~0ull, ~0ull);
+    }
   }
-  for (int o = 16; o; o >>= 1) {
-    newc += __shfl_xor_sync(FULL, newc, o);
-    vox += __shfl_xor_sync(FULL, vox, o);
-  }
+  newc = __reduce_add_sync(FULL, newc);
+  vox = __reduce_add_sync(FULL, vox);
   if ((threadIdx.x & 31) == 0) {
     if (newc) atomicAdd(set_count, (unsigned long long)newc);
     if (vox) atomicAdd(nvox, (unsigned long long)vox);
+  }
+}
+
+// New-voxel pixel ids in ascending order in ONE pass over the bitmask: each
+// block takes the next 2048-word tile (dynamic tile ids, so every earlier tile
+// is running or done), reduces its popcounts, finds its output offset by a
+// decoupled look-back over the earlier tiles' published sums, writes the set
+// bits' pixel ids and clears the words (the bitmask is library-owned and
+// starts every batch zeroed).  The last tile publishes the grand total for
+// the emit kernel, copies the batch counters into the caller's mapped host
+// status words and resets them for the next batch.
+constexpr int kLbThreads = 256, kLbWords = 8, kLbTile = kLbThreads * kLbWords, kLbFlat = 1024;
+
+__global__ void __launch_bounds__(kLbThreads)
+grid_pidlist_lb_kernel(unsigned* __restrict__ flag_bits, int64_t nwords, unsigned long long* lb_status,
+                       unsigned long long* cnts, int64_t capacity, int64_t* __restrict__ pid_out,
+                       int32_t* grand, volatile unsigned long long* host_status) {
+  __shared__ unsigned s_tile;
+  __shared__ uint32_t s_wsum[kLbThreads / 32];
+  __shared__ uint32_t s_base;
+  pdl_wait();
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (t == 0) s_tile = atomicAdd(reinterpret_cast<unsigned*>(cnts + 6), 1u);
+  __syncthreads();
+  const int64_t tile = s_tile, ntiles = (nwords + kLbTile - 1) / kLbTile;
+  const int64_t w0 = tile * kLbTile + (int64_t)t * kLbWords;
+  unsigned w[kLbWords];
+  if (w0 + kLbWords <= nwords) {
+    const uint4 a = *reinterpret_cast<const uint4*>(flag_bits + w0), b = *reinterpret_cast<const uint4*>(flag_bits + w0 + 4);
+    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    if (a.x | a.y | a.z | a.w) *reinterpret_cast<uint4*>(flag_bits + w0) = make_uint4(0, 0, 0, 0);
+    if (b.x | b.y | b.z | b.w) *reinterpret_cast<uint4*>(flag_bits + w0 + 4) = make_uint4(0, 0, 0, 0);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kLbWords; j++) {
+      w[j] = w0 + j < nwords ? flag_bits[w0 + j] : 0u;
+      if (w[j]) flag_bits[w0 + j] = 0u;
+    }
+  }
+  uint32_t c = 0;
+#pragma unroll
+  for (int j = 0; j < kLbWords; j++) c += __popc(w[j]);
+  uint32_t x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t wv = lane < kLbThreads / 32 ? s_wsum[lane] : 0u;
+    uint32_t wx = wv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, wx, o);
+      if (lane >= o) wx += y;
+    }
+    const uint32_t agg = __shfl_sync(FULL, wx, kLbThreads / 32 - 1);
+    if (lane < kLbThreads / 32) s_wsum[lane] = wx - wv;
+    // look-back: lanes read 32 predecessors at a time.  Up to kLbFlat tiles
+    // every tile simply sums ALL its predecessors' aggregates (published as
+    // soon as each tile is reduced -- no chain of inclusive prefixes through
+    // the tiles of one wave); beyond, the decoupled look-back stops at the
+    // nearest inclusive prefix.
+    unsigned long long excl = 0;
+    if (ntiles <= kLbFlat) {
+      if (lane == 0) atomicExch(lb_status + tile, LB_AGG | agg);
+      for (int64_t j0 = 0; j0 < tile; j0 += 32) {
+        const int64_t jj = j0 + lane;
+        unsigned long long sv = 0;
+        if (jj < tile) {
+          do {
+            sv = *reinterpret_cast<volatile unsigned long long*>(lb_status + jj);
+          } while ((sv & ~LB_VAL) == 0);
+        }
+        unsigned long long v = jj < tile ? (sv & LB_VAL) : 0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        excl += v;
+      }
+    } else if (tile == 0) {
+      if (lane == 0) atomicExch(lb_status, LB_PRE | agg);
+    } else {
+      if (lane == 0) atomicExch(lb_status + tile, LB_AGG | agg);
+      int64_t j = tile - 1;
+      while (true) {
+        const int64_t jj = j - lane;
+        unsigned long long sv = 0;
+        if (jj >= 0) {
+          do {
+            sv = *reinterpret_cast<volatile unsigned long long*>(lb_status + jj);
+          } while ((sv & ~LB_VAL) == 0);
+        }
+        const unsigned pre = __ballot_sync(FULL, jj >= 0 && (sv & LB_PRE));
+        // lanes up to (and including) the nearest prefix contribute
+        const int stop = pre ? __ffs(pre) - 1 : 31;
+        unsigned long long v = (lane <= stop && jj >= 0) ? (sv & LB_VAL) : 0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        excl += v;
+        if (pre || j - 32 < 0) break;
+        j -= 32;
+      }
+      if (lane == 0) atomicExch(lb_status + tile, LB_PRE | (excl + agg));
+    }
+    if (lane == 0) {
+      s_base = (uint32_t)excl;
+      if (tile == ntiles - 1) {
+        const unsigned long long total = excl + agg;
+        *grand = (int32_t)total;
+        host_status[0] = cnts[0];   // valid pixels
+        host_status[1] = cnts[1];   // distinct voxels of the batch
+        host_status[2] = cnts[2];   // items inserted / sorted
+        host_status[3] = total;     // new voxels
+        host_status[4] = cnts[5];   // table overflow flag
+        for (int i = 0; i < 7; i++) cnts[i] = 0ull;
+        __threadfence_system();
+      }
+    }
+  }
+  __syncthreads();
+  int64_t o = (int64_t)s_base + s_wsum[warp] + (x - c);
+#pragma unroll
+  for (int j = 0; j < kLbWords; j++) {
+    unsigned word = w[j];
+    while (word) {
+      const int b = __ffs(word) - 1;
+      word &= word - 1;
+      if (o < capacity) pid_out[o] = (w0 + j) * 32 + b;
+      o++;
+    }
   }
 }
 
@@ -1605,80 +1796,86 @@ cudaError_t host_copy_res(HostCopy** out) {
   return cudaSuccess;
 }
 
-// per-device batch table (library-owned scratch, empty between batches)
+// Per-device grid state (library-owned; every grid_sample call on the device
+// holds g_dedup_mu): the batch dedup table (empty between batches), the
+// new-voxel pixel bitmask (zero between batches: the pid-list pass clears the
+// words it reads), the emission look-back statuses, the batch counters (reset
+// by the last emission tile) and the mapped pinned host status words the last
+// tile writes, so a batch ends with one stream synchronisation and no copy.
 struct DedupTable {
   unsigned long long* slots = nullptr;   // 2 x cap words
-  int* aux = nullptr;   // [0] overflow flag
   int64_t cap = 0;
   int64_t last_nvox = -1;
+  unsigned* flags = nullptr;             // pixel bitmask words
+  int64_t flag_words = 0;
+  unsigned long long* lb = nullptr;      // look-back status per emission tile
+  int64_t lb_tiles = 0;
+  char* misc = nullptr;                  // bbox int[6] at +0, counters u64[8] at +64, grand at +128
+  unsigned long long* host_st = nullptr;      // mapped pinned [8]
+  unsigned long long* host_st_dev = nullptr;  // its device alias
+  bool dirty = false;                    // a batch stopped before its counters were reset
 };
 constexpr int kDedupDevices = 16;
 DedupTable g_dedup[kDedupDevices];
 std::mutex g_dedup_mu;
 
-// Table size: 4x the previous batch's distinct voxels (load <= 1/4 when the
-// scene changes slowly), the item count for the first batch (front-end items
-// repeat each voxel several times), 2x the item count after an overflow
-// (`all`: every item could be a distinct voxel).
-cudaError_t dedup_table(int64_t nitems, bool all, cudaStream_t s, DedupTable** out) {
+cudaError_t grid_state(int64_t npix, cudaStream_t s, DedupTable** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= kDedupDevices) return cudaErrorInvalidDevice;
   DedupTable& t = g_dedup[dev];
-  const int64_t want = all ? 2 * nitems : (t.last_nvox < 0 ? nitems : 4 * t.last_nvox);
-  int64_t cap = 1 << 20;
-  while (cap < want) cap <<= 1;
-  // keep the table when it is big enough but not over 4x too big (probes stay L2-resident)
-  if (t.slots && t.cap >= cap && t.cap <= 4 * cap) {
-    *out = &t;
-    return cudaSuccess;
+  if (!t.misc) {
+    if ((e = cudaMalloc(&t.misc, 256)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(t.misc, 0, 256, s)) != cudaSuccess) return e;
+    if ((e = cudaHostAlloc(reinterpret_cast<void**>(&t.host_st), 64, cudaHostAllocMapped)) != cudaSuccess) return e;
+    if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&t.host_st_dev), t.host_st, 0)) != cudaSuccess)
+      return e;
   }
-  if (t.slots) {
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;   // earlier batches may still use it
-    cudaFree(t.slots);
-    cudaFree(t.aux);
-    t.slots = nullptr;
+  const int64_t nwords = (npix + 31) / 32 + 8;
+  if (t.flag_words < nwords) {
+    if (t.flags) {
+      if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+      cudaFree(t.flags);
+      t.flags = nullptr;
+    }
+    const int64_t words = nwords + nwords / 4;
+    if ((e = cudaMalloc(&t.flags, (size_t)words * 4)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(t.flags, 0, (size_t)words * 4, s)) != cudaSuccess) return e;
+    t.flag_words = words;
+    const int64_t tiles = (words + kLbTile - 1) / kLbTile;
+    if (t.lb) cudaFree(t.lb);
+    if ((e = cudaMalloc(&t.lb, (size_t)tiles * 8)) != cudaSuccess) return e;
+    t.lb_tiles = tiles;
   }
-  if ((e = cudaMalloc(&t.slots, sizeof(unsigned long long) * 2 * cap)) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&t.aux, 64)) != cudaSuccess) return e;
-  t.cap = cap;
-  fill_u64_kernel<<<grid_blocks(2 * cap, 256, 148), 256, 0, s>>>(t.slots, 2 * cap, ~0ull); count_launches(1);
+  if (t.dirty) {
+    if ((e = cudaMemsetAsync(t.misc, 0, 256, s)) != cudaSuccess) return e;
+    t.dirty = false;
+  }
   *out = &t;
-  return cudaGetLastError();
-}
-
-bool dedup_sized() {
-  int dev = 0;
-  return cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < kDedupDevices && g_dedup[dev].slots &&
-         g_dedup[dev].last_nvox >= 0;
-}
-
-// pass 1 + pass 2; the flags, the voxel count and the table's aux
-// words are reset first (also on a retry)
-cudaError_t dedup_pass(const DedupSegs& sg, DedupTable* t, HashSet* hs, unsigned* flag, int64_t nwords,
-                       unsigned long long* nvox, int sms, cudaStream_t s) {
-  cudaError_t e;
-  if ((e = cudaMemsetAsync(flag, 0, (size_t)nwords * 4, s)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(nvox, 0, 8, s)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(t->aux, 0, 8, s)) != cudaSuccess) return e;
-  const uint64_t mask = (uint64_t)t->cap - 1;
-  const unsigned g = (unsigned)(sg.nseg < 148 * 8 ? sg.nseg : 148 * 8);
-  if ((e = launch_pdl(dd_insert_kernel, dim3(g), dim3(256), 0, s, sg, t->slots, mask, t->aux)) != cudaSuccess)
-    return e;
-  if ((e = launch_pdl(dd_scan_kernel, dim3(grid_blocks(t->cap, 256, sms)), dim3(256), 0, s, t->slots, t->cap,
-                      (const int*)t->aux, hs->table, (uint64_t)hs->cap - 1, hs->count_dev, flag, nvox)) != cudaSuccess)
-    return e;
-  count_launches(2);
   return cudaSuccess;
 }
 
-
-__global__ void gather_status_kernel(const unsigned long long* cnts, const int32_t* grand, const int* aux,
-                                     unsigned long long* st) {
-  if (threadIdx.x < 3) st[threadIdx.x] = cnts[threadIdx.x];   // nvalid, nvox, items
-  if (threadIdx.x == 3) st[3] = (unsigned long long)(uint32_t)*grand;
-  if (threadIdx.x == 4) st[4] = aux ? (unsigned long long)*aux : 0ull;
+// Table size: 4x the previous batch's distinct voxels (load <= 1/4 when the
+// scene changes slowly), the item count for the first batch (front-end items
+// repeat each voxel several times), 2x the item count after an overflow
+// (`all`: every item could be a distinct voxel).
+cudaError_t dedup_table(DedupTable& t, int64_t nitems, bool all, cudaStream_t s) {
+  cudaError_t e;
+  const int64_t want = all ? 2 * nitems : (t.last_nvox < 0 ? nitems : 4 * t.last_nvox);
+  int64_t cap = 1 << 20;
+  while (cap < want) cap <<= 1;
+  // keep the table when it is big enough but not over 2x too big (probes stay L2-resident)
+  if (t.slots && t.cap >= cap && t.cap <= 2 * cap) return cudaSuccess;
+  if (t.slots) {
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;   // earlier batches may still use it
+    cudaFree(t.slots);
+    t.slots = nullptr;
+  }
+  if ((e = cudaMalloc(&t.slots, sizeof(unsigned long long) * 2 * cap)) != cudaSuccess) return e;
+  t.cap = cap;
+  fill_u64_kernel<<<grid_blocks(2 * cap, 256, 148), 256, 0, s>>>(t.slots, 2 * cap, ~0ull); count_launches(1);
+  return cudaGetLastError();
 }
 
 // per-thread, per-device pinned landing buffer for the final read-back
@@ -1695,6 +1892,58 @@ cudaError_t pinned_status(unsigned long long** out) {
   return cudaSuccess;
 }
 
+// G5: new-voxel pixel ids in ascending order (one look-back pass over the
+// bitmask) and the GaussianField-compatible outputs (one thread per row, the
+// count read from device memory), then the batch's single synchronisation:
+// the last emission tile already wrote the counters into mapped host memory.
+cudaError_t emit_outputs(const GridIn& in, const Cam& cam, DedupTable* st, const int32_t* head, const uint64_t* sk,
+                         const uint32_t* sv, int64_t nitems, GridOut& out, int sms, cudaStream_t s, HostCopy* hcp) {
+  ProfScope prof("grid_emit", s);
+  cudaError_t e;
+  const int64_t npix = in.frames * in.H * in.W;
+  const int64_t nwords = (npix + 31) / 32;
+  const int64_t lb_tiles = (nwords + kLbTile - 1) / kLbTile;
+  unsigned long long* cnts = reinterpret_cast<unsigned long long*>(st->misc + 64);
+  int32_t* grand = reinterpret_cast<int32_t*>(st->misc + 128);
+  if ((e = launch_pdl(grid_pidlist_lb_kernel, dim3((unsigned)lb_tiles), dim3(kLbThreads), 0, s, st->flags, nwords,
+                      st->lb, cnts, (int64_t)out.capacity, out.pid, grand, st->host_st_dev)) != cudaSuccess)
+    return e;
+  count_launches(1);
+  if (hcp && (e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;   // colour
+  EmitArgs ea;
+  ea.depth = in.depth;
+  ea.color = in.color;
+  ea.rot = in.rot;
+  ea.trans = in.trans;
+  ea.cam = cam;
+  ea.H = in.H;
+  ea.W = in.W;
+  ea.stride = in.stride;
+  ea.mode = in.mode;
+  ea.min_scale = in.min_scale;
+  ea.feat = in.feat;
+  ea.fc = in.fc;
+  ea.fh = in.fh;
+  ea.fw = in.fw;
+  ea.skeys = sk;
+  ea.svals = sv;
+  ea.n = nitems;   // mean mode only
+  ea.key = out.key;
+  ea.pid = out.pid;
+  ea.mu = out.mu;
+  ea.col = out.color;
+  ea.scale = out.scale;
+  ea.dep = out.depth;
+  ea.ofeat = out.feat;
+  ea.feat64 = out.feat64;
+  ea.count = out.count;
+  if ((e = launch_pdl(grid_emit_kernel, dim3(grid_blocks(out.capacity, 128, sms)), dim3(128), 0, s, head,
+                      (const int32_t*)grand, (int64_t)out.capacity, ea)) != cudaSuccess)
+    return e;
+  count_launches(1);
+  return cudaStreamSynchronize(s);
+}
+
 cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, size_t ws_bytes, int sms,
                         cudaStream_t s) {
   const int64_t npix = in.frames * in.H * in.W;
@@ -1707,24 +1956,25 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   uint32_t* v1 = reinterpret_cast<uint32_t*>(b + w.off_v1);
   int32_t* hist = reinterpret_cast<int32_t*>(b + w.off_hist);
   int32_t* ssum = reinterpret_cast<int32_t*>(b + w.off_scan_sums);
-  uint8_t* flag = reinterpret_cast<uint8_t*>(b + w.off_flag);
-  int32_t* pos = reinterpret_cast<int32_t*>(b + w.off_pos);
   int32_t* head = reinterpret_cast<int32_t*>(b + w.off_head);
-  int* bbox = reinterpret_cast<int*>(b + w.off_misc);
-  unsigned long long* cnts = reinterpret_cast<unsigned long long*>(b + w.off_misc + 64);  // nvalid, nvox
-  int32_t* grand = reinterpret_cast<int32_t*>(b + w.off_misc + 128);
-  unsigned long long* status = reinterpret_cast<unsigned long long*>(b + w.off_misc + 192);   // 5 words
   unsigned long long* lb_status = reinterpret_cast<unsigned long long*>(b + w.off_lb);
-  int32_t* block_count = reinterpret_cast<int32_t*>(lb_status);   // fused front end: per-block item counts
+  int32_t* block_count = reinterpret_cast<int32_t*>(lb_status);   // fused front end (sort path): per-block item counts
   out.n_new = out.n_valid = out.n_voxels = 0;
   out.n_sorted = out.sort_passes = 0;
   if (npix == 0) return cudaSuccess;
   cudaError_t e;
+  std::lock_guard<std::mutex> st_lock(g_dedup_mu);
+  ProfScope prof_batch("grid_batch", s);   // device span of the whole call (first launch .. status sync)
+  DedupTable* st = nullptr;
+  if ((e = grid_state(npix, s, &st)) != cudaSuccess) return e;
+  int* bbox = reinterpret_cast<int*>(st->misc);
+  unsigned long long* cnts = reinterpret_cast<unsigned long long*>(st->misc + 64);   // nvalid, nvox, items, -, -, ovf, tile
+  int* overflow = reinterpret_cast<int*>(cnts + 5);
+  unsigned* flag = st->flags;
   const Cam cam{in.fx, in.fy, in.cx, in.cy, in.voxel, 1.0 / in.voxel};
-  const bool compact = in.mode == 0;   // first-pick: dedup runs + compaction before the sort
-  bool fused = false;                  // fused front end (per-block slots, gathered by the rekey pass)
-  int64_t fblocks = 0;
+  const bool compact = in.mode == 0;   // first-pick
   const int64_t nwords = (npix + 31) / 32;
+  const int64_t lb_tiles = (nwords + kLbTile - 1) / kLbTile;
   // Host frames (xgs_grid_sample_h2d): depth is copied frame chunk by frame
   // chunk on a copy stream and each chunk's front-end launch waits only for
   // its own chunk, so the copies of later frames overlap the earlier frames'
@@ -1747,16 +1997,15 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   const int64_t fpx = in.H * in.W;
   const int64_t fper = host_frames ? (in.frames + kHostChunks - 1) / kHostChunks : in.frames;
   const int nchunk = (int)((in.frames + fper - 1) / fper);   // every chunk non-empty
-  auto copy_depth = [&](int c) -> cudaError_t {
-    const int64_t f0 = c * fper, f1 = f0 + fper < in.frames ? f0 + fper : in.frames;
-    cudaError_t ce = cudaMemcpyAsync(const_cast<float*>(in.depth) + f0 * fpx, in.depth_host + f0 * fpx,
-                                     sizeof(float) * (size_t)((f1 - f0) * fpx), cudaMemcpyHostToDevice, hcp->cs);
-    if (ce == cudaSuccess) ce = cudaEventRecord(hcp->chunk[c], hcp->cs);
-    return ce;
-  };
   if (host_frames) {
-    for (int c = 0; c < nchunk; c++)
-      if ((e = copy_depth(c)) != cudaSuccess) return e;
+    for (int c = 0; c < nchunk; c++) {
+      const int64_t f0 = c * fper, f1 = f0 + fper < in.frames ? f0 + fper : in.frames;
+      if ((e = cudaMemcpyAsync(const_cast<float*>(in.depth) + f0 * fpx, in.depth_host + f0 * fpx,
+                               sizeof(float) * (size_t)((f1 - f0) * fpx), cudaMemcpyHostToDevice, hcp->cs)) !=
+          cudaSuccess)
+        return e;
+      if ((e = cudaEventRecord(hcp->chunk[c], hcp->cs)) != cudaSuccess) return e;
+    }
     if (in.color && in.color_host) {
       if ((e = cudaMemcpyAsync(const_cast<uint8_t*>(in.color), in.color_host, (size_t)(in.frames * fpx * 3),
                                cudaMemcpyHostToDevice, hcp->cs)) != cudaSuccess)
@@ -1764,100 +2013,135 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
     }
     if ((e = cudaEventRecord(hcp->done, hcp->cs)) != cudaSuccess) return e;
   }
-  {
-    ProfScope prof("grid_keys", s);
-    init_bbox_kernel<<<1, 32, 0, s>>>(bbox, cnts); count_launches(1);   // also zeroes cnts[0..5]
-    const bool vec4 = (in.W % 4 == 0) && (reinterpret_cast<uintptr_t>(in.depth) % 16 == 0);
-    fblocks = in.frames * ((in.H + FK_ROWS - 1) / FK_ROWS);
-    fused = compact && vec4 && in.W <= 4 * kFrontMaxThreads && fblocks <= w.lb_entries;
-    if (host_frames && !fused) {   // the two-kernel front end reads every frame: wait for all of them
-      if ((e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;
-    }
-    if (fused) {
-      const CamF cf{(float)in.cx, (float)in.cy, (float)(1.0 / in.fx), (float)(1.0 / in.fy), (float)(1.0 / in.voxel)};
-      const unsigned nt = (unsigned)((in.W / 4 + 31) / 32 * 32);
-      const size_t fsmem = front_smem_bytes(nt / 32);
-      // the voxel bounding box only feeds the sort path's relative keys
-      auto kern = sort_forced() ? grid_front_kernel<true> : grid_front_kernel<false>;
-      if ((e = front_init()) != cudaSuccess) return e;
-      const int64_t rbf = (in.H + FK_ROWS - 1) / FK_ROWS;
-      for (int c = 0; c < nchunk; c++) {
-        const int64_t f0 = c * fper, f1 = f0 + fper < in.frames ? f0 + fper : in.frames;
-        if (f1 <= f0) break;
-        if (host_frames && (e = cudaStreamWaitEvent(s, hcp->chunk[c], 0)) != cudaSuccess) return e;
-        kern<<<(unsigned)((f1 - f0) * rbf), nt, fsmem, s>>>(in.depth, in.H, in.W, in.stride, in.rot,
-                                                                          in.trans, cam, cf, k0, v0, bbox, cnts,
-                                                                          block_count, (unsigned)(f0 * rbf));
+  const bool vec4 = (in.W % 4 == 0) && (reinterpret_cast<uintptr_t>(in.depth) % 16 == 0);
+  const bool front_ok = vec4 && in.W <= 4 * kFrontMaxThreads;   // the fused front end (float4 rows)
+  // first-pick takes the hash path; XGS_GRID_SORT=1 forces the radix sort +
+  // select path (mean mode always sorts: its per-voxel sums run in pixel
+  // order over the voxel's segment)
+  const bool hashed = compact && !sort_forced();
+  st->dirty = true;
+  if (hashed) {
+    // ---------------- G1+G2': front end inserting into the batch table, table scan + map test
+    if ((e = hashset_reserve(hs, npix, s)) != cudaSuccess) return e;   // room for a new key per pixel
+    if ((e = dedup_table(*st, npix / 16, false, s)) != cudaSuccess) return e;
+    out.sort_passes = 0;
+    const CamF cf{(float)in.cx, (float)in.cy, (float)(1.0 / in.fx), (float)(1.0 / in.fy), (float)(1.0 / in.voxel)};
+    if (front_ok && (e = front_init()) != cudaSuccess) return e;
+    for (int attempt = 0;; attempt++) {
+      const uint64_t mask = (uint64_t)st->cap - 1;
+      {
+        ProfScope prof("grid_keys", s);
+        if (front_ok) {
+          const unsigned nt = (unsigned)((in.W / 4 + 31) / 32 * 32);
+          const size_t fsmem = front_smem_bytes(nt / 32);
+          const int64_t rbf = (in.H + FK_ROWS - 1) / FK_ROWS;
+          for (int c = 0; c < nchunk; c++) {
+            const int64_t f0 = c * fper, f1 = f0 + fper < in.frames ? f0 + fper : in.frames;
+            if (f1 <= f0) break;
+            if (host_frames && attempt == 0 && (e = cudaStreamWaitEvent(s, hcp->chunk[c], 0)) != cudaSuccess) return e;
+            grid_front_kernel<FRONT_INSERT><<<(unsigned)((f1 - f0) * rbf), nt, fsmem, s>>>(
+                in.depth, in.H, in.W, in.stride, in.rot, in.trans, cam, cf, nullptr, nullptr, bbox, cnts, nullptr,
+                (unsigned)(f0 * rbf), st->slots, mask, overflow);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            count_launches(1);
+          }
+        } else {
+          if (host_frames && attempt == 0 && (e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;
+          grid_keys_kernel<<<grid_blocks(vec4 ? npix / 4 : npix, 256, sms), 256, 0, s>>>(
+              in.depth, npix, in.H, in.W, in.stride, in.rot, in.trans, cam, k1, nullptr, bbox, cnts, vec4);
+          count_launches(1);
+          if ((e = launch_pdl(dd_insert_pixels_kernel, dim3(grid_blocks(npix, 256, sms)), dim3(256), 0, s,
+                              (const uint64_t*)k1, npix, in.W, st->slots, mask, cnts, overflow)) != cudaSuccess)
+            return e;
+          count_launches(1);
+        }
+      }
+      {
+        ProfScope prof("grid_select", s);
+        if ((e = launch_pdl(dd_scan_map_kernel, dim3(grid_blocks(st->cap / kScanILP, 256, sms)), dim3(256), 0, s,
+                            st->slots, st->cap, (const int*)overflow, hs->table, (uint64_t)hs->cap - 1,
+                            hs->count_dev, flag, cnts + 1, st->lb, lb_tiles)) != cudaSuccess)
+          return e;
         count_launches(1);
       }
-    } else {
-    grid_keys_kernel<<<grid_blocks(vec4 ? npix / 4 : npix, 256, sms), 256, 0, s>>>(
-        in.depth, npix, in.H, in.W, in.stride, in.rot, in.trans, cam, compact ? k1 : k0, compact ? nullptr : v0,
-        bbox, cnts, vec4); count_launches(1);
-    }
-    if (compact && !fused) {
-      const int64_t ntiles = (npix + CT_TILE - 1) / CT_TILE;
-      unsigned* tile_counter = reinterpret_cast<unsigned*>(cnts + 4);
-      cudaMemsetAsync(tile_counter, 0, 4, s);
-      cudaMemsetAsync(lb_status, 0, sizeof(unsigned long long) * ntiles, s);
-      compact_keys_kernel<<<grid_blocks(ntiles * CT_THREADS, CT_THREADS, sms), CT_THREADS, 0, s>>>(
-          k1, npix, in.W, k0, v0, tile_counter, lb_status, ntiles, cnts + 2); count_launches(1);
-    }
-  }
-  // first-pick mode takes the hash path (G2'); XGS_GRID_SORT=1 forces the
-  // radix sort + select path (mean mode always sorts: its per-voxel sums run
-  // in pixel order over the voxel's segment)
-  const bool hashed = compact && !sort_forced();
-  std::unique_lock<std::mutex> dd_lock(g_dedup_mu, std::defer_lock);
-  if (hashed) dd_lock.lock();
-  // The hash path on the fused front end needs no host-side item count when
-  // the occupancy set already has room for a new key per pixel and the batch
-  // table was sized by an earlier batch: no read-back between the front end
-  // and the dedup (the counts are read with the final one).
-  const bool no_sync = hashed && fused && 2 * (hs->count_ub + npix) <= hs->cap && dedup_sized();
-  int hb[8];
-  unsigned long long hc[3] = {0, 0, 0};
-  int64_t nitems = 0;
-  if (!no_sync) {
-    // bbox (misc + 0) and the counters (misc + 64) in one copy to pinned memory
-    unsigned long long* hst = nullptr;
-    if ((e = pinned_status(&hst)) != cudaSuccess) return e;
-    if ((e = cudaMemcpyAsync(hst, bbox, 88, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-    std::memcpy(hb, hst, 6 * sizeof(int));
-    std::memcpy(hc, hst + 8, 24);
-    out.n_valid = (int64_t)hc[0];
-    if (hc[0] == 0) return cudaSuccess;
-    nitems = compact ? (int64_t)hc[2] : npix;   // items to sort
-    // every voxel of the batch keeps at least one item, so the sorted item count
-    // bounds the new keys (first-pick dedup makes it ~3x tighter than nvalid)
-    if ((e = hashset_reserve(hs, nitems, s)) != cudaSuccess) return e;
-  }
-  DedupTable* dd = nullptr;
-  DedupSegs sg{};
-  if (hashed) {
-    out.n_sorted = nitems;
-    out.sort_passes = 0;
-    sg.k = k0;
-    sg.v = v0;
-    sg.H = in.H;
-    sg.W = in.W;
-    if (fused) {
-      sg.count = block_count;
-      sg.nseg = fblocks;
-    } else {
-      sg.count = nullptr;
-      sg.n_dense = nitems;
-      sg.nseg = (nitems + kDedupSeg - 1) / kDedupSeg;
-    }
-    {
-      ProfScope prof("grid_select", s);
-      if ((e = dedup_table(nitems, false, s, &dd)) != cudaSuccess) return e;
-      if ((e = dedup_pass(sg, dd, hs, reinterpret_cast<unsigned*>(flag), nwords, cnts + 1, sms, s)) != cudaSuccess)
+      if ((e = emit_outputs(in, cam, st, head, k0, v0, 0, out, sms, s, host_frames ? hcp : nullptr)) != cudaSuccess)
         return e;
+      const unsigned long long* hst = st->host_st;
+      out.n_valid = (int64_t)hst[0];
+      out.n_voxels = (int64_t)hst[1];
+      out.n_sorted = (int64_t)hst[2];
+      out.n_new = (int64_t)hst[3];
+      if (!hst[4]) break;
+      // the table was too small for this batch's distinct voxels: the scan did
+      // not run (map untouched, nothing flagged or emitted); reset the partly
+      // filled table and redo the batch on one sized for every pixel
+      if (attempt > 0) return cudaErrorUnknown;
+      fill_u64_kernel<<<grid_blocks(2 * st->cap, 256, sms), 256, 0, s>>>(st->slots, 2 * st->cap, ~0ull);
+      count_launches(1);
+      if ((e = dedup_table(*st, npix, true, s)) != cudaSuccess) return e;
     }
+    st->last_nvox = out.n_voxels;
   } else {
-  // bbox-relative key width; +1 on x keeps the all-ones invalid key above every valid key
+    // ---------------- G1 keys, G2 radix sort, G3 select (mean mode / forced sort)
+    bool fused = false;
+    int64_t fblocks = 0;
+    {
+      ProfScope prof("grid_keys", s);
+      init_bbox_kernel<<<1, 32, 0, s>>>(bbox, cnts); count_launches(1);   // also zeroes cnts[0..5]
+      fblocks = in.frames * ((in.H + FK_ROWS - 1) / FK_ROWS);
+      fused = compact && vec4 && front_ok && fblocks <= w.lb_entries;
+      if (host_frames && !fused) {   // the two-kernel front end reads every frame: wait for all of them
+        if ((e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;
+      }
+      if (fused) {
+        const CamF cf{(float)in.cx, (float)in.cy, (float)(1.0 / in.fx), (float)(1.0 / in.fy), (float)(1.0 / in.voxel)};
+        const unsigned nt = (unsigned)((in.W / 4 + 31) / 32 * 32);
+        const size_t fsmem = front_smem_bytes(nt / 32);
+        if ((e = front_init()) != cudaSuccess) return e;
+        const int64_t rbf = (in.H + FK_ROWS - 1) / FK_ROWS;
+        for (int c = 0; c < nchunk; c++) {
+          const int64_t f0 = c * fper, f1 = f0 + fper < in.frames ? f0 + fper : in.frames;
+          if (f1 <= f0) break;
+          if (host_frames && (e = cudaStreamWaitEvent(s, hcp->chunk[c], 0)) != cudaSuccess) return e;
+          grid_front_kernel<FRONT_SORT><<<(unsigned)((f1 - f0) * rbf), nt, fsmem, s>>>(
+              in.depth, in.H, in.W, in.stride, in.rot, in.trans, cam, cf, k0, v0, bbox, cnts, block_count,
+              (unsigned)(f0 * rbf), nullptr, 0, nullptr);
+          count_launches(1);
+        }
+      } else {
+        grid_keys_kernel<<<grid_blocks(vec4 ? npix / 4 : npix, 256, sms), 256, 0, s>>>(
+            in.depth, npix, in.H, in.W, in.stride, in.rot, in.trans, cam, compact ? k1 : k0, compact ? nullptr : v0,
+            bbox, cnts, vec4); count_launches(1);
+      }
+      if (compact && !fused) {
+        const int64_t ntiles = (npix + CT_TILE - 1) / CT_TILE;
+        unsigned* tile_counter = reinterpret_cast<unsigned*>(cnts + 4);
+        cudaMemsetAsync(tile_counter, 0, 4, s);
+        cudaMemsetAsync(lb_status, 0, sizeof(unsigned long long) * ntiles, s);
+        compact_keys_kernel<<<grid_blocks(ntiles * CT_THREADS, CT_THREADS, sms), CT_THREADS, 0, s>>>(
+            k1, npix, in.W, k0, v0, tile_counter, lb_status, ntiles, cnts + 2); count_launches(1);
+      }
+    }
+    // bbox (misc + 0) and the counters (misc + 64) in one copy to pinned memory
+    int hb[8];
+    unsigned long long hc[3] = {0, 0, 0};
+    {
+      unsigned long long* hst = nullptr;
+      if ((e = pinned_status(&hst)) != cudaSuccess) return e;
+      if ((e = cudaMemcpyAsync(hst, bbox, 88, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+      if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+      std::memcpy(hb, hst, 6 * sizeof(int));
+      std::memcpy(hc, hst + 8, 24);
+    }
+    out.n_valid = (int64_t)hc[0];
+    if (hc[0] == 0) {
+      if ((e = cudaMemsetAsync(st->misc, 0, 256, s)) != cudaSuccess) return e;
+      st->dirty = false;
+      return cudaSuccess;
+    }
+    const int64_t nitems = compact ? (int64_t)hc[2] : npix;   // items to sort
+    if ((e = hashset_reserve(hs, nitems, s)) != cudaSuccess) return e;
+    // bbox-relative key width; +1 on x keeps the all-ones invalid key above every valid key
     RelKey rk;
     rk.x0 = (uint32_t)hb[0];
     rk.y0 = (uint32_t)hb[1];
@@ -1873,13 +2157,10 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
       bits = 64;
     }
     if ((e = sort_init()) != cudaSuccess) return e;
-    if (nitems == 0) return cudaSuccess;
     out.n_sorted = nitems;
     out.sort_passes = (bits + 7) / 8;
-    // the new-head flags are cleared ahead of the sort, so select follows the
-    // last sort kernel directly (programmatic launch, no memset in between)
-    if ((e = cudaMemsetAsync(flag, 0, (size_t)nwords * 4, s)) != cudaSuccess) return e;
-    {
+    if ((e = cudaMemsetAsync(st->lb, 0, (size_t)lb_tiles * 8, s)) != cudaSuccess) return e;
+    if (nitems > 0) {
       ProfScope prof("grid_sort", s);
       // relative keys once (u32 when they fit), LSD passes, biased keys back into k0
       const unsigned rb = grid_blocks(nitems, 256, sms);
@@ -1921,95 +2202,21 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
         }
       }
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
-    {
-      ProfScope prof("grid_select", s);
+      ProfScope prof2("grid_select", s);
       if ((e = launch_pdl(grid_select_kernel, dim3(grid_blocks(nitems, 256, sms)), dim3(256), 0, s, (const uint64_t*)k0,
-                          (const uint32_t*)v0, nitems, hs->table, (uint64_t)hs->cap - 1, hs->count_dev,
-                          reinterpret_cast<unsigned*>(flag), head, cnts + 1)) != cudaSuccess)
+                          (const uint32_t*)v0, nitems, hs->table, (uint64_t)hs->cap - 1, hs->count_dev, flag, head,
+                          cnts + 1)) != cudaSuccess)
         return e;
       count_launches(1);
     }
+    if ((e = emit_outputs(in, cam, st, head, k0, v0, nitems, out, sms, s, host_frames ? hcp : nullptr)) != cudaSuccess)
+      return e;
+    out.n_voxels = (int64_t)st->host_st[1];
+    out.n_new = (int64_t)st->host_st[3];
   }
-  {
-    ProfScope prof("grid_emit", s);
-    if (host_frames && (e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;   // colour
-    int32_t nnew = 0;
-    unsigned long long nvox = 0;
-    EmitArgs ea;
-    ea.depth = in.depth;
-    ea.color = in.color;
-    ea.rot = in.rot;
-    ea.trans = in.trans;
-    ea.cam = cam;
-    ea.H = in.H;
-    ea.W = in.W;
-    ea.stride = in.stride;
-    ea.mode = in.mode;
-    ea.min_scale = in.min_scale;
-    ea.feat = in.feat;
-    ea.fc = in.fc;
-    ea.fh = in.fh;
-    ea.fw = in.fw;
-    ea.skeys = k0;
-    ea.svals = v0;
-    ea.n = nitems;   // mean mode only (always known there: no_sync is first-pick only)
-    ea.key = out.key;
-    ea.pid = out.pid;
-    ea.mu = out.mu;
-    ea.col = out.color;
-    ea.scale = out.scale;
-    ea.dep = out.depth;
-    ea.ofeat = out.feat;
-    ea.feat64 = out.feat64;
-    ea.count = out.count;
-    for (int attempt = 0;; attempt++) {
-      // exclusive popcount scan of the new-voxel bitmask, pixel-id list, emit:
-      // all queued before the read-back (outputs are bounded by the capacity)
-      if ((e = exclusive_scan<PopcWord>(reinterpret_cast<const PopcWord*>(flag), nwords, pos, ssum, grand, s)) !=
-          cudaSuccess)
-        return e;
-      if ((e = launch_pdl(grid_pidlist_kernel, dim3(grid_blocks(nwords, 256, sms)), dim3(256), 0, s,
-                          reinterpret_cast<const unsigned*>(flag), (const int32_t*)pos, nwords, (int64_t)out.capacity,
-                          out.pid)) != cudaSuccess)
-        return e;
-      if ((e = launch_pdl(grid_emit_kernel, dim3(grid_blocks(out.capacity, 128, sms)), dim3(128), 0, s,
-                          (const int32_t*)head, (const int32_t*)grand, (int64_t)out.capacity, ea)) != cudaSuccess)
-        return e;
-      count_launches(2);
-      // one read-back: the counters, the new-voxel total and the overflow flag
-      // gathered on the device, one copy into pinned host memory
-      unsigned long long* hst = nullptr;
-      if ((e = pinned_status(&hst)) != cudaSuccess) return e;
-      gather_status_kernel<<<1, 32, 0, s>>>(cnts, grand, hashed ? dd->aux : nullptr, status); count_launches(1);
-      if ((e = cudaMemcpyAsync(hst, status, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-        return e;
-      if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-      hc[0] = hst[0];
-      hc[2] = hst[2];
-      nvox = hst[1];
-      nnew = (int32_t)hst[3];
-      const int ovf = (int)hst[4];
-      if (no_sync) {
-        out.n_valid = (int64_t)hc[0];
-        out.n_sorted = nitems = (int64_t)hc[2];
-      }
-      if (!ovf) break;
-      // the table was too small for this batch's distinct voxels: pass 2 did not
-      // run (map untouched, no flags, nothing emitted); reset the partly filled
-      // table and redo the batch on one sized for every item
-      if (attempt > 0) return cudaErrorUnknown;
-      fill_u64_kernel<<<grid_blocks(2 * dd->cap, 256, sms), 256, 0, s>>>(dd->slots, 2 * dd->cap, ~0ull); count_launches(1);
-      if ((e = dedup_table(nitems, true, s, &dd)) != cudaSuccess) return e;
-      if ((e = dedup_pass(sg, dd, hs, reinterpret_cast<unsigned*>(flag), nwords, cnts + 1, sms, s)) != cudaSuccess)
-        return e;
-    }
-    if (hashed) dd->last_nvox = (int64_t)nvox;
-    out.n_new = nnew;
-    hs->count_ub += nnew;
-    out.n_voxels = (int64_t)nvox;
-    if (nnew > out.capacity) return cudaErrorInvalidValue;
-  }
+  st->dirty = false;
+  hs->count_ub += out.n_new;
+  if (out.n_new > out.capacity) return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 

@@ -1000,13 +1000,10 @@ cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, 
   // (CAP 8) on the rows whose best code was not unique; larger codebooks
   // (more near-ties) use the CAP-16 list epilogue directly
   const bool big = a.k >= 2048;
-  static bool attr[3] = {false, false, false};
   cudaError_t e;
   auto prepare = [&](auto kern, int idx, int bytes) -> cudaError_t {
-    if (attr[idx]) return cudaSuccess;
-    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (r == cudaSuccess) attr[idx] = true;
-    return r;
+    return attr_once(kAttrScreen0 + idx,
+                     [&] { return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); });
   };
   auto clusters_for = [&](int64_t rows) {
     int64_t c = a.sm_count / 2, t = (rows + 2 * BM - 1) / (2 * BM);

@@ -236,13 +236,14 @@ template <typename X>
 cudaError_t seed_launch(const void* x, int64_t n, int64_t d, int64_t ldx, int64_t k, int64_t* seeds, const SeedWs& w,
                         const SumPlan& pd, cudaStream_t s) {
   const size_t smem = sizeof(double) * (size_t)d;
-  static bool attr = false;
-  static int per_sm = 0;
-  if (!attr) {
-    cudaFuncSetAttribute(seed_step_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
-    cudaFuncSetAttribute(seed_persistent_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
-    attr = true;
-  }
+  static int per_sm = 0;   // occupancy of the persistent kernel (identical B200s: same on every device)
+  cudaError_t ea = attr_once(kAttrSeed, [] {
+    cudaError_t r = cudaFuncSetAttribute(seed_step_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(seed_persistent_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
+    return r;
+  });
+  if (ea != cudaSuccess) return ea;
   int dev = 0, sms = 148, coop = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

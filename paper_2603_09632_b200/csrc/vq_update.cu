@@ -566,12 +566,15 @@ cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, in
   }
   cudaError_t e;
   if (block_tiles(k)) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(acc_hist_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatterSmem);
-      cudaFuncSetAttribute(acc_scatter_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatterSmem);
-      attr = true;
-    }
+    cudaError_t ea = attr_once(kAttrUpdate, [] {
+      cudaError_t r = cudaFuncSetAttribute(acc_hist_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kScatterSmem);
+      if (r == cudaSuccess)
+        r = cudaFuncSetAttribute(acc_scatter_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kScatterSmem);
+      return r;
+    });
+    if (ea != cudaSuccess) return ea;
     const int W = scatter_warps(k);
     if (n > 0) {
       if ((e = launch_pdl(acc_hist_block_kernel, dim3((unsigned)p.tiles), dim3(256), sizeof(int32_t) * (size_t)k, s,
