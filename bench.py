@@ -163,17 +163,23 @@ GRID_INTR = (1050.0, 1050.0, 359.5, 639.5)   # BASELINE leaves C3 intrinsics ope
 GRID_MAP = 4_000_000
 
 
-def grid_scene(seed=20):
-    """C3: 16 frames 1280x720, random planes + spheres 0.3-8 m, sigma 3 mm,
-    circle of radius 2 m with 5 deg yaw steps, uint8 colour (seeds 20/21)."""
+def grid_scene_objects(seed=20):
     from paper_2603_09632_b200 import synth
     rng = np.random.default_rng(seed)
     planes = synth.random_planes(rng, 6, spread=3.0)
     spheres = [(rng.uniform(-1.0, 1.0, 3), rng.uniform(0.2, 0.6)) for _ in range(4)]
-    poses = synth.circle_trajectory(GRID_F, radius=2.0, step_deg=5.0)
+    return planes, spheres
+
+
+def grid_scene(seed=20, frames=GRID_F):
+    """C3: 16 frames 1280x720, random planes + spheres 0.3-8 m, sigma 3 mm,
+    circle of radius 2 m with 5 deg yaw steps, uint8 colour (seeds 20/21)."""
+    from paper_2603_09632_b200 import synth
+    planes, spheres = grid_scene_objects(seed)
+    poses = synth.circle_trajectory(frames, radius=2.0, step_deg=5.0)
     crng = np.random.default_rng(seed + 1)
-    D = np.empty((GRID_F, GRID_H, GRID_W), np.float32)
-    C = np.empty((GRID_F, GRID_H, GRID_W, 3), np.uint8)
+    D = np.empty((frames, GRID_H, GRID_W), np.float32)
+    C = np.empty((frames, GRID_H, GRID_W, 3), np.uint8)
     for i, p in enumerate(poses):
         D[i], C[i] = synth.rgbd_frame(crng, p, GRID_INTR, GRID_H, GRID_W, planes=planes, spheres=spheres,
                                       dmin=0.3, dmax=8.0, noise=0.003, zero_frac=0.0)
@@ -182,60 +188,108 @@ def grid_scene(seed=20):
     return D, C, R, T
 
 
+def grid_warm_map(torch, voxel, target=GRID_MAP, seed=20, max_frames=240):
+    """The C3 running map: voxels of the SAME scene seen earlier along the
+    trajectory -- the rest of the 2 m circle (yaw 80..355 deg), then rings at
+    other heights and radii -- sampled by GridSampler itself at `voxel`, until
+    ~`target` voxels or `max_frames` frames (1 cm reaches ~4M; at 5 cm the
+    scene holds far fewer voxels, so seeded filler keys far outside the scene
+    volume bring the hash set to ~`target`).  Returns (uint64-as-int64 CUDA
+    keys, scene voxel count, frames used)."""
+    from paper_2603_09632_b200 import synth
+    from paper_2603_09632_b200.grid import GridSampler, VoxelHashSet, pack_key
+    planes, spheres = grid_scene_objects(seed)
+    rings = [(2.0, 0.0, 80.0), (2.0, 0.6, 0.0), (2.6, -0.5, 0.0), (1.4, 0.3, 0.0), (3.0, 1.0, 0.0), (2.3, -1.0, 0.0)]
+    hs = VoxelHashSet(2 * target + (1 << 22))
+    gs = GridSampler(GRID_INTR, voxel, occupied=hs)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed + 2)
+    keys, used = [], 0
+    for radius, height, a0 in rings:
+        poses = []
+        a = a0
+        while a < 360.0 and used + len(poses) < max_frames:
+            eye = np.array([radius * np.cos(np.deg2rad(a)), radius * np.sin(np.deg2rad(a)), height])
+            poses.append(synth.look_at(eye, np.zeros(3)))
+            a += 5.0
+        for i in range(0, len(poses), 16):
+            chunk = poses[i:i + 16]
+            R = torch.tensor(np.stack([p.rotation for p in chunk]), device="cuda")
+            T = torch.tensor(np.stack([p.translation for p in chunk]), device="cuda")
+            D = torch.stack([synth.render_depth_torch(torch, R[j], T[j], GRID_INTR, GRID_H, GRID_W, planes, spheres)
+                             for j in range(len(chunk))])
+            D = torch.where(D > 0, D + 0.003 * torch.randn(D.shape, generator=g, device="cuda", dtype=D.dtype), D)
+            r = gs.sample(D.float().contiguous(), (R, T))
+            keys.append(r.key.clone())
+            used += len(chunk)
+            if sum(int(k.numel()) for k in keys) >= target:
+                break
+        if sum(int(k.numel()) for k in keys) >= target or used >= max_frames:
+            break
+    scene = torch.cat(keys)
+    n_scene = int(scene.numel())
+    hs.close()
+    if n_scene < target:   # filler: seeded keys at |index| in [1e5, 2e5) voxels -- outside any batch's reach
+        rng = np.random.default_rng(seed + 3)
+        m = target - n_scene
+        q = rng.integers(100_000, 200_000, (m, 3)) * rng.choice([-1, 1], (m, 3))
+        scene = torch.cat([scene, torch.from_numpy(pack_key(q[:, 0], q[:, 1], q[:, 2]).view(np.int64)).cuda()])
+    return scene, n_scene, used
+
+
 def run_grid(torch, steps, cpu=True):
     """C3 grid sampling: Mpts/s = 16*1280*720 input pixels / batch time, map
-    reset to the ~4M-voxel warm-up state before every timed batch."""
+    reset to the scene-derived ~4M-voxel running map before every timed batch."""
     from paper_2603_09632_b200 import _native as nat
-    from paper_2603_09632_b200.grid import GridSampler, VoxelHashSet, pack_key
+    from paper_2603_09632_b200.grid import GridSampler, VoxelHashSet
     D, C, R, T = grid_scene()
     Dd, Cd = torch.from_numpy(D).cuda(), torch.from_numpy(C).cuda()
     Rd, Td = torch.from_numpy(R).cuda(), torch.from_numpy(T).cuda()
-    rng = np.random.default_rng(22)
     out = {}
+    npix = GRID_F * GRID_H * GRID_W
+    pk_, _ = peaks()
     for voxel in (0.01, 0.05):
-        # warm-up map: 4M voxels of random points in the scene volume (seeded)
-        pts = rng.uniform(-4.0, 4.0, (GRID_MAP, 3))
-        q = np.floor(pts / voxel).astype(np.int64)
-        warm = torch.from_numpy(pack_key(q[:, 0], q[:, 1], q[:, 2]).view(np.int64)).cuda()
-        times, n_new, n_valid, map_size, n_sorted, passes = [], 0, 0, 0, 0, 0
+        warm, n_scene, warm_frames = grid_warm_map(torch, voxel)
+        times, calls, spans, stage = [], [], [], {}
+        r = None
         for it in range(steps + 1):
-            hs = VoxelHashSet(GRID_MAP + GRID_F * GRID_H * GRID_W)
+            hs = VoxelHashSet(GRID_MAP + npix)
             hs.insert(warm)
             map_size = len(hs)
             gs = GridSampler(GRID_INTR, voxel, occupied=hs)
             torch.cuda.synchronize()
-            if it == steps:
-                nat.profile_enable(True)
+            nat.profile_enable(True)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
             e0.record()
             r = gs.sample(Dd, (Rd, Td), Cd)
             e1.record()
             torch.cuda.synchronize()
-            if 0 < it < steps or (it == steps and not times):   # the last run is the profiled one
+            t1 = time.perf_counter()
+            prof = {t: nat.profile_read(t)[0] for t in ("grid_batch", "grid_keys", "grid_select", "grid_emit")}
+            nat.profile_enable(False)
+            if it > 0:   # the first batch sizes the library's tables
                 times.append(e0.elapsed_time(e1))
-            n_new, n_valid, n_sorted, passes = len(r), r.n_valid, r.n_sorted, r.sort_passes
+                calls.append((t1 - t0) * 1e3)
+                spans.append(prof["grid_batch"])
+                for k_, v_ in prof.items():
+                    stage.setdefault(k_, []).append(v_)
             hs.close()
-        prof = {t: nat.profile_read(t)[0] for t in ("grid_keys", "grid_sort", "grid_select", "grid_emit")}
-        nat.profile_enable(False)
-        ms = float(np.median(times))
-        npix = GRID_F * GRID_H * GRID_W
-        pk_, _ = peaks()
-        # first-pick batches take the hash dedup (no sort passes); the sort model applies to XGS_GRID_SORT=1
-        kb = 4 if passes <= 4 else 8
-        sort_bytes = float(n_sorted) * (passes * (kb + 2 * (kb + 4)) + 2 * (8 + kb)) if passes else 0.0
-        sort_gbs = sort_bytes / (prof["grid_sort"] * 1e-3) / 1e9 if (prof["grid_sort"] and sort_bytes) else None
-        # fused front end: depth read 4 B per pixel + 12 B (key + pixel id) per surviving item
-        keys_bytes = 4.0 * npix + 12.0 * n_sorted
-        front_gbs = keys_bytes / (prof["grid_keys"] * 1e-3) / 1e9 if prof["grid_keys"] else None
-        # hash dedup: per item 12 B read + one 32 B table sector (claim / min), then one sequential pass over
-        # the 16 B slots (read + clear) -- L2-resident table
-        dedup_bytes = float(n_sorted) * (12 + 32)
+        ms = float(np.median(spans))
+        stage_ms = {k_: float(np.median(v_)) for k_, v_ in stage.items()}
+        n_new, n_vox = len(r), r.n_voxels
+        # algorithmic bytes of the batch: depth in (4 B/px) + colour of the new voxels' pixels (3 B) + the
+        # outputs written (key 8, pid 8, mu 24, colour 24, scale 8, depth 8, count 8 = 88 B per new voxel)
+        # + one 32 B map-table sector per distinct voxel of the batch
+        batch_bytes = 4.0 * npix + n_new * (3 + 88) + 32.0 * n_vox
+        front_bytes = 4.0 * npix          # the front end's compulsory HBM traffic (depth read)
+        t_front = stage_ms["grid_keys"]
         # end to end through the public API: frames in pinned host memory (H2D of depth + colour),
         # the batch, the new Gaussians back to host numpy (GridSampleResult.to_numpy)
         Dh, Ch = torch.from_numpy(D).pin_memory(), torch.from_numpy(C).pin_memory()
         e2e = []
         for it in range(3):
-            hs = VoxelHashSet(GRID_MAP + GRID_F * GRID_H * GRID_W)
+            hs = VoxelHashSet(GRID_MAP + npix)
             hs.insert(warm)
             gs = GridSampler(GRID_INTR, voxel, occupied=hs)
             torch.cuda.synchronize()
@@ -246,21 +300,27 @@ def run_grid(torch, steps, cpu=True):
         e2e_ms = float(np.median(e2e))
         e2e_h2d = Dh.numel() * 4 + Ch.numel()
         e2e_d2h = sum(v.nbytes for v in host_out.values() if isinstance(v, np.ndarray))
-        out[str(voxel)] = {"Mpts_per_s": npix / (ms * 1e-3) / 1e6, "ms_per_batch": ms, "pixels": npix,
-                           "valid_points": n_valid, "new_voxels": n_new, "map_voxels_before": map_size,
-                           "sorted_items": n_sorted, "sort_passes": passes, "per_kernel_ms": prof,
-                           "roofline": {"bound": "hbm", "kernel": "grid_front_kernel (fused back-projection, keys, "
-                                                                  "left/up dedup, ordered compaction)",
-                                        "achieved": front_gbs, "peak": pk_["hbm_gbs"], "unit": "GB/s",
-                                        "frac": front_gbs / pk_["hbm_gbs"] if front_gbs else None,
-                                        "algorithmic_bytes": keys_bytes,
-                                        "note": "issue-bound (fp32 filter + exact fp64 fallback per pixel); the "
-                                                "hash dedup and emit stages work on L2-resident data"},
-                           "dedup_GBps": dedup_bytes / (prof["grid_select"] * 1e-3) / 1e9 if prof["grid_select"] else None,
-                           "sort_GBps": sort_gbs,
-                           "e2e": {"Mpts_per_s": npix / (e2e_ms * 1e-3) / 1e6, "ms_per_batch": e2e_ms,
-                                   "h2d_bytes": e2e_h2d, "d2h_bytes": e2e_d2h,
-                                   "note": "host wall clock around sample() + to_numpy(), pinned host frames"}}
+        out[str(voxel)] = {
+            "Mpts_per_s": npix / (ms * 1e-3) / 1e6, "ms_per_batch": ms,
+            "ms_per_batch_python_call": float(np.median(calls)), "ms_per_batch_events": float(np.median(times)),
+            "pixels": npix, "valid_points": r.n_valid, "batch_voxels": n_vox, "new_voxels": n_new,
+            "rejected_voxels": n_vox - n_new, "rejected_frac": (n_vox - n_new) / max(1, n_vox),
+            "map_voxels_before": map_size, "map_scene_voxels": n_scene, "map_warm_frames": warm_frames,
+            "items_inserted": r.n_sorted, "per_stage_ms": stage_ms,
+            "batch_hbm_frac": batch_bytes / (ms * 1e-3) / 1e9 / pk_["hbm_gbs"],
+            "roofline": {"bound": "hbm", "kernel": "grid_front_kernel<FRONT_INSERT> (back-projection, keys, "
+                                                   "left/up dedup, batch-table insert)",
+                         "achieved": front_bytes / (t_front * 1e-3) / 1e9, "peak": pk_["hbm_gbs"], "unit": "GB/s",
+                         "frac": front_bytes / (t_front * 1e-3) / 1e9 / pk_["hbm_gbs"],
+                         "algorithmic_bytes": front_bytes,
+                         "note": "issue/L2-latency bound: fp32 key filter + ballot staging per pixel, one random "
+                                 "L2 sector per inserted item (tools/micro/insert_bench.cu: ~35 us floor for 4.4M "
+                                 "probes even read-only)"},
+            "e2e": {"Mpts_per_s": npix / (e2e_ms * 1e-3) / 1e6, "ms_per_batch": e2e_ms,
+                    "h2d_bytes": e2e_h2d, "d2h_bytes": e2e_d2h,
+                    "note": "host wall clock around sample() + to_numpy(), pinned host frames"}}
+    out["timing"] = ("ms_per_batch = device span of the C-ABI call xgs_grid_sample (first launch .. its status "
+                     "sync; ProfScope 'grid_batch'); ms_per_batch_python_call adds the Python wrapper")
     if cpu:
         from oracle import grid as og
         t0 = time.perf_counter()

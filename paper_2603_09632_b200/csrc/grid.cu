@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(kFrontMaxThreads, kFrontBlocksPerSM)
 grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int stride, const double* __restrict__ rot,
                   const double* __restrict__ trans, Cam cam, CamF cf, uint64_t* __restrict__ kout,
                   uint32_t* __restrict__ vout, int* bbox, unsigned long long* cnts, int32_t* __restrict__ block_count,
-                  unsigned bid0, unsigned long long* __restrict__ slots, uint64_t mask, int* overflow) {
+                  unsigned bid0, unsigned long long* __restrict__ slots, uint64_t mask, int* overflow, bool diag) {
   constexpr bool BOX = MODE == FRONT_SORT;
   constexpr int NR = FK_ROWS;
   constexpr float XB = 9437184.f;   // 2^23 + 2^20
@@ -534,13 +534,27 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
   const uint32_t w4 = Wu >> 2;
   unsigned cnt = 0;
   uint64_t kp[4];   // previous row's keys (the halo row first)
-  float4 dn = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (r0 > 0 && colmask) dn = __ldg(dframe + (size_t)(r0 - 1) * w4 + t);
+  float4 dn = make_float4(0.f, 0.f, 0.f, 0.f), dn2 = dn;
+  // row pointer stepped by one row per iteration (no per-row 64-bit index math);
+  // two rows in flight ahead of the one being keyed
+  const float4* dptr = dframe + (size_t)(r0 > 0 ? r0 - 1 : 0) * w4 + t;
+  if (colmask) {
+    if (r0 > 0) {
+      dn = __ldg(dptr);
+      dptr += w4;
+    }
+    dn2 = __ldg(dptr);
+    dptr += w4;
+  }
 #pragma unroll 1
   for (int rr = 0; rr <= nr; rr++) {
     const int r = r0 - 1 + rr;
     const float4 d4 = dn;
-    if (rr < nr && colmask) dn = __ldg(dframe + (size_t)(r + 1) * w4 + t);   // next row in flight
+    dn = dn2;
+    if (rr + 1 < nr && colmask) {
+      dn2 = __ldg(dptr);
+      dptr += w4;
+    }
     const unsigned rowmask = (r >= 0 && (su == 1 || ((uint32_t)r % su) == 0)) ? colmask : 0u;
     const float4 rc = s_row[rr];
     const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
@@ -576,13 +590,27 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
     }
     if (rr > 0) {
       // ---- left/up dedup, warp-local compaction into segment (row, warp) ----
+      // A pixel may be dropped when ANY earlier pixel of the frame carries its
+      // key (that pixel, or the one it was dropped for, stands in; the
+      // voxel's lowest pixel id never has one): left and upper neighbours,
+      // plus -- `diag` -- the upper-left / upper-right diagonals, which catch
+      // most of the repeats the depth noise scatters around voxel faces.
       const uint64_t left = __shfl_up_sync(FULL, k[3], 1);
+      uint64_t ul = KEY_INVALID, ur = KEY_INVALID;
+      if (diag) {
+        ul = __shfl_up_sync(FULL, kp[3], 1);
+        ur = __shfl_down_sync(FULL, kp[0], 1);
+        if (lane == 0) ul = KEY_INVALID;
+        if (lane == 31) ur = KEY_INVALID;
+      }
       unsigned keep = 0;
 #pragma unroll
       for (int j = 0; j < 4; j++) {
         const uint64_t kk = k[j];
         const uint64_t lk = j == 0 ? (lane > 0 ? left : KEY_INVALID) : k[j - 1];
-        if (kk != KEY_INVALID && (kk == PEND || (kk != lk && kk != kp[j]))) keep |= 1u << j;
+        bool dup = kk == lk || kk == kp[j];
+        if (diag) dup = dup || kk == (j == 0 ? ul : kp[j - 1]) || kk == (j == 3 ? ur : kp[j + 1]);
+        if (kk != KEY_INVALID && (kk == PEND || !dup)) keep |= 1u << j;
       }
       const unsigned lt = (1u << lane) - 1u;
       unsigned below = 0, total = 0;
@@ -1571,16 +1599,15 @@ dd_insert_pixels_kernel(const uint64_t* __restrict__ keys, int64_t n, int64_t W,
 // voxels flagged in the pixel bitmask, slot emptied for the next batch.  Four
 // slots per thread per step with their map probes issued together.  Also
 // clears the emission look-back statuses for grid_pidlist_lb_kernel.
-constexpr int kScanILP = 4;
+constexpr int kScanILP = 8;
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 dd_scan_map_kernel(unsigned long long* slots, int64_t cap, const int* overflow, unsigned long long* table,
                    uint64_t tmask, unsigned long long* set_count, unsigned* flag_bits, unsigned long long* nvox,
                    unsigned long long* lb_status, int64_t lb_tiles) {
   pdl_wait();
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = gt; i < lb_tiles; i += gs) lb_status[i] = 0ull;
-  if (*(volatile const int*)overflow) return;   // the host resets the whole table
   unsigned newc = 0, vox = 0;
   for (int64_t h0 = gt; h0 < cap; h0 += kScanILP * gs) {
     ulonglong2 sl[kScanILP];
@@ -1591,6 +1618,7 @@ dd_scan_map_kernel(unsigned long long* slots, int64_t cap, const int* overflow, 
       const int64_t hh = h0 + j * gs;
       sl[j] = hh < cap ? slot_ld(slots, (uint64_t)hh) : make_ulonglong2(EMPTY, EMPTY);
     }
+    if (h0 == gt && *(volatile const int*)overflow) return;   // the host resets the whole table
 #pragma unroll
     for (int j = 0; j < kScanILP; j++)
       if (sl[j].x != EMPTY) {
@@ -1701,19 +1729,25 @@ grid_pidlist_lb_kernel(unsigned* __restrict__ flag_bits, int64_t nwords, unsigne
     unsigned long long excl = 0;
     if (ntiles <= kLbFlat) {
       if (lane == 0) atomicExch(lb_status + tile, LB_AGG | agg);
-      for (int64_t j0 = 0; j0 < tile; j0 += 32) {
-        const int64_t jj = j0 + lane;
-        unsigned long long sv = 0;
-        if (jj < tile) {
-          do {
-            sv = *reinterpret_cast<volatile unsigned long long*>(lb_status + jj);
-          } while ((sv & ~LB_VAL) == 0);
-        }
-        unsigned long long v = jj < tile ? (sv & LB_VAL) : 0ull;
+      // every lane loads its share of the predecessors at once (up to 32 each)
+      unsigned long long v = 0;
+      for (int64_t j0 = lane; j0 < tile; j0 += 32 * 8) {
+        unsigned long long sv[8];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-        excl += v;
+        for (int i = 0; i < 8; i++) {
+          const int64_t jj = j0 + 32 * i;
+          sv[i] = jj < tile ? *reinterpret_cast<volatile unsigned long long*>(lb_status + jj) : (unsigned long long)(1ull << 62);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          const int64_t jj = j0 + 32 * i;
+          while ((sv[i] & ~LB_VAL) == 0) sv[i] = *reinterpret_cast<volatile unsigned long long*>(lb_status + jj);
+          v += sv[i] & LB_VAL;
+        }
       }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+      excl = v;
     } else if (tile == 0) {
       if (lane == 0) atomicExch(lb_status, LB_PRE | agg);
     } else {
@@ -2035,13 +2069,15 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
           const unsigned nt = (unsigned)((in.W / 4 + 31) / 32 * 32);
           const size_t fsmem = front_smem_bytes(nt / 32);
           const int64_t rbf = (in.H + FK_ROWS - 1) / FK_ROWS;
+          const char* dg = std::getenv("XGS_GRID_DIAG");
+          const bool diag = !(dg && dg[0] == '0');
           for (int c = 0; c < nchunk; c++) {
             const int64_t f0 = c * fper, f1 = f0 + fper < in.frames ? f0 + fper : in.frames;
             if (f1 <= f0) break;
             if (host_frames && attempt == 0 && (e = cudaStreamWaitEvent(s, hcp->chunk[c], 0)) != cudaSuccess) return e;
             grid_front_kernel<FRONT_INSERT><<<(unsigned)((f1 - f0) * rbf), nt, fsmem, s>>>(
                 in.depth, in.H, in.W, in.stride, in.rot, in.trans, cam, cf, nullptr, nullptr, bbox, cnts, nullptr,
-                (unsigned)(f0 * rbf), st->slots, mask, overflow);
+                (unsigned)(f0 * rbf), st->slots, mask, overflow, diag);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
             count_launches(1);
           }
@@ -2058,7 +2094,8 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
       }
       {
         ProfScope prof("grid_select", s);
-        if ((e = launch_pdl(dd_scan_map_kernel, dim3(grid_blocks(st->cap / kScanILP, 256, sms)), dim3(256), 0, s,
+        const int64_t sblocks = (st->cap + kScanILP * 256 - 1) / (kScanILP * 256);
+        if ((e = launch_pdl(dd_scan_map_kernel, dim3((unsigned)(sblocks < 3 * sms ? sblocks : 3 * sms)), dim3(256), 0, s,
                             st->slots, st->cap, (const int*)overflow, hs->table, (uint64_t)hs->cap - 1,
                             hs->count_dev, flag, cnts + 1, st->lb, lb_tiles)) != cudaSuccess)
           return e;
@@ -2105,7 +2142,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
           if (host_frames && (e = cudaStreamWaitEvent(s, hcp->chunk[c], 0)) != cudaSuccess) return e;
           grid_front_kernel<FRONT_SORT><<<(unsigned)((f1 - f0) * rbf), nt, fsmem, s>>>(
               in.depth, in.H, in.W, in.stride, in.rot, in.trans, cam, cf, k0, v0, bbox, cnts, block_count,
-              (unsigned)(f0 * rbf), nullptr, 0, nullptr);
+              (unsigned)(f0 * rbf), nullptr, 0, nullptr, true);
           count_launches(1);
         }
       } else {

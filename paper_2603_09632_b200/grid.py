@@ -15,7 +15,6 @@ Definitions: SURVEY.md §8(a) g8, oracle/grid.py.
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
 from typing import Optional
 
 import numpy as np
@@ -82,25 +81,56 @@ class VoxelHashSet:
             pass
 
 
-@dataclass
 class GridSampleResult:
-    """New Gaussians of one batch, ascending (frame, pixel) id (CUDA tensors)."""
+    """New Gaussians of one batch, ascending (frame, pixel) id (CUDA tensors).
 
-    key: object       # (n,) int64 view of the uint64 voxel keys
-    pid: object       # (n,) int64: frame*H*W + u*W + v
-    mu: object        # (n, 3) fp64 world positions
-    color: object     # (n, 3) fp64 rgb/255
-    scale: object     # (n,) fp64 iso size
-    depth: object     # (n,) fp64 camera depth of the representative pixel
-    count: object     # (n,) fp64 points averaged (mean mode) or 1
-    feature: Optional[object]
-    n_valid: int
-    n_voxels: int
-    n_sorted: int = 0        # items through the dedup (after the front end's first-pick compaction)
-    sort_passes: int = 0     # 8-bit LSD passes (0: first-pick hash dedup, no sort)
+    The fields are views of the call's output buffer, created on first access
+    (a batch that only needs counts, or goes straight to ``to_numpy``, builds
+    no per-field tensor views on the host):
+
+    key      (n,) int64 view of the uint64 voxel keys
+    pid      (n,) int64: frame*H*W + u*W + v
+    mu       (n, 3) fp64 world positions
+    color    (n, 3) fp64 rgb/255
+    scale    (n,) fp64 iso size
+    depth    (n,) fp64 camera depth of the representative pixel
+    count    (n,) fp64 points averaged (mean mode) or 1
+    feature  (n, C) fp32 (first-pick) / fp64 (mean) or None
+    """
+
+    __slots__ = ("_flat", "_cap", "_n", "_feat", "n_valid", "n_voxels", "n_sorted", "sort_passes", "_cache")
+
+    def __init__(self, flat, cap, n, feat, n_valid, n_voxels, n_sorted=0, sort_passes=0):
+        self._flat, self._cap, self._n, self._feat = flat, cap, n, feat
+        self.n_valid, self.n_voxels, self.n_sorted, self.sort_passes = n_valid, n_voxels, n_sorted, sort_passes
+        self._cache = {}
 
     def __len__(self):
-        return int(self.pid.shape[0])
+        return self._n
+
+    def _col(self, name):
+        v = self._cache.get(name)
+        if v is None:
+            t = nat.torch()
+            f, c, n = self._flat, self._cap, self._n
+            v = {"key": lambda: f[:n].view(t.int64), "pid": lambda: f[c:c + n].view(t.int64),
+                 "mu": lambda: f[2 * c:2 * c + 3 * n].view(n, 3), "color": lambda: f[5 * c:5 * c + 3 * n].view(n, 3),
+                 "scale": lambda: f[8 * c:8 * c + n], "depth": lambda: f[9 * c:9 * c + n],
+                 "count": lambda: f[10 * c:10 * c + n]}[name]()
+            self._cache[name] = v
+        return v
+
+    key = property(lambda self: self._col("key"))
+    pid = property(lambda self: self._col("pid"))
+    mu = property(lambda self: self._col("mu"))
+    color = property(lambda self: self._col("color"))
+    scale = property(lambda self: self._col("scale"))
+    depth = property(lambda self: self._col("depth"))
+    count = property(lambda self: self._col("count"))
+
+    @property
+    def feature(self):
+        return None if self._feat is None else self._feat[:self._n]
 
     def to_numpy(self):
         """All fields in ONE device->host copy: the per-voxel columns are packed
@@ -108,12 +138,13 @@ class GridSampleResult:
         pinned landing buffer (8 pageable copies would each stage through a
         driver buffer and run at about half the PCIe rate)."""
         t = nat.torch()
-        n = len(self)
-        cols = [self.key.view(t.float64), self.pid.view(t.float64), self.mu.reshape(-1), self.color.reshape(-1),
-                self.scale, self.depth, self.count]
+        n, c, f = self._n, self._cap, self._flat
+        cols = [f[:2 * n] if c == n else t.cat([f[:n], f[c:c + n]]) if n else f[:0]]
+        cols += [f[2 * c:2 * c + 3 * n], f[5 * c:5 * c + 3 * n], f[8 * c:8 * c + n], f[9 * c:9 * c + n],
+                 f[10 * c:10 * c + n]]
         feat = self.feature
         if feat is not None:
-            cols.append(feat.reshape(-1).to(t.float64) if feat.dtype == t.float64 else
+            cols.append(feat.reshape(-1) if feat.dtype == t.float64 else
                         feat.reshape(-1).view(t.int32).to(t.float64))    # fp32 bits carried losslessly
         packed = t.cat(cols) if n else t.empty(0, dtype=t.float64, device="cuda")
         host = _pinned_landing(packed.numel())
@@ -132,8 +163,8 @@ class GridSampleResult:
                    sort_passes=self.sort_passes)
         if feat is not None:
             C = int(feat.shape[1])
-            f = take(n * C)
-            out["feature"] = (f if feat.dtype == t.float64 else f.astype(np.int32).view(np.float32)).reshape(n, C)
+            fv = take(n * C)
+            out["feature"] = (fv if feat.dtype == t.float64 else fv.astype(np.int32).view(np.float32)).reshape(n, C)
         return out
 
 
@@ -148,6 +179,19 @@ def _pinned_landing(numel):
     if buf is None or buf.numel() < numel:
         buf = _landing[dev] = t.empty(max(numel, 1 << 16), dtype=t.float64, pin_memory=True)
     return buf
+
+
+_WS_BYTES = {}
+
+
+def _grid_ws_bytes(npix):
+    """xgs_grid_workspace, memoised (a pure function of the pixel count)."""
+    b = _WS_BYTES.get(npix)
+    if b is None:
+        if len(_WS_BYTES) > 64:
+            _WS_BYTES.clear()
+        b = _WS_BYTES[npix] = int(nat.lib().xgs_grid_workspace(npix))
+    return b
 
 
 def _intr4(intr):
@@ -267,7 +311,7 @@ class GridSampler:
         res = nat.GridResult(cap, b, b + 8 * cap, b + 16 * cap, b + 40 * cap, b + 64 * cap, b + 72 * cap,
                              ofeat.data_ptr() if ofeat is not None else None, b + 80 * cap, 0, 0, 0, 0, 0,
                              nat.F32 if fdt == t.float32 else nat.F64)
-        ws = nat.workspace("grid", nat.lib().xgs_grid_workspace(F * H * W))
+        ws = nat.workspace("grid", _grid_ws_bytes(F * H * W))
         if host:
             nat.call("xgs_grid_sample_h2d", ctypes.byref(fr), stage[1].data_ptr(),
                      stage[2].data_ptr() if stage[2] is not None else None, self.occupied._h, ctypes.byref(res),
@@ -275,13 +319,8 @@ class GridSampler:
         else:
             nat.call("xgs_grid_sample", ctypes.byref(fr), self.occupied._h, ctypes.byref(res), nat.ptr(ws),
                      ws.numel(), nat.stream_ptr())
-        n = int(res.n_new)
-        return GridSampleResult(key=flat[:n].view(t.int64), pid=flat[cap:cap + n].view(t.int64),
-                                mu=flat[2 * cap:2 * cap + 3 * n].view(n, 3), color=flat[5 * cap:5 * cap + 3 * n].view(n, 3),
-                                scale=flat[8 * cap:8 * cap + n], depth=flat[9 * cap:9 * cap + n],
-                                count=flat[10 * cap:10 * cap + n], feature=ofeat[:n] if ofeat is not None else None,
-                                n_valid=int(res.n_valid), n_voxels=int(res.n_voxels),
-                                n_sorted=int(res.n_sorted), sort_passes=int(res.sort_passes))
+        return GridSampleResult(flat, cap, int(res.n_new), ofeat, int(res.n_valid), int(res.n_voxels),
+                                int(res.n_sorted), int(res.sort_passes))
 
 
 def radix_sort_pairs(keys, vals, bits: int = 64):

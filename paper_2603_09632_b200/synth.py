@@ -96,6 +96,33 @@ def render_depth(pose, intr4, H, W, planes=(), spheres=(), dmin=0.3, dmax=8.0):
     return best
 
 
+def render_depth_torch(torch, R, t, intr4, H, W, planes=(), spheres=(), dmin=0.3, dmax=8.0, device="cuda"):
+    """render_depth on the device (fp64): R, t fp64 tensors of one world->camera pose."""
+    fx, fy, cx, cy = intr4
+    f64 = torch.float64
+    u = torch.arange(H, device=device, dtype=f64)[:, None].expand(H, W)
+    v = torch.arange(W, device=device, dtype=f64)[None, :].expand(H, W)
+    dcam = torch.stack([(u - cx) / fx, (v - cy) / fy, torch.ones_like(u)], dim=-1)
+    dw = dcam @ R                      # R^T d for every pixel
+    C = -(R.T @ t)
+    inf = torch.full((H, W), float("inf"), device=device, dtype=f64)
+    best = inf.clone()
+    for nrm, c in planes:
+        n = torch.as_tensor(nrm, device=device, dtype=f64)
+        den = dw @ n
+        tt = (float(c) - n @ C) / den
+        best = torch.minimum(best, torch.where((tt > 0) & torch.isfinite(tt), tt, inf))
+    for centre, rad in spheres:
+        oc = C - torch.as_tensor(centre, device=device, dtype=f64)
+        a = (dw * dw).sum(-1)
+        b = 2 * (dw @ oc)
+        cc = oc @ oc - rad * rad
+        disc = b * b - 4 * a * cc
+        tt = (-b - torch.sqrt(torch.clamp(disc, min=0))) / (2 * a)
+        best = torch.minimum(best, torch.where((disc >= 0) & (tt > 0), tt, inf))
+    return torch.where((best >= dmin) & (best <= dmax), best, torch.zeros_like(best))
+
+
 def rgbd_frame(rng, pose, intr4, H, W, planes=(), spheres=(), dmin=0.3, dmax=8.0, noise=0.005, zero_frac=0.05,
                clip=None):
     d = render_depth(pose, intr4, H, W, planes, spheres, dmin, dmax)

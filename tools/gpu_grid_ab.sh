@@ -1,4 +1,3 @@
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_grid_gpu.py -q -x > gpurun_out/g_tests.log 2>&1; echo "rc=$?" >> gpurun_out/g_tests.log
-for gr in 1 0; do XGS_GRID_GROUP=$gr timeout 300 python tools/grid_bench.py 5 > gpurun_out/g_bench_$gr.log 2>&1; done
-timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum,sm__warps_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file gpurun_out/g_launches.csv python tools/prof_grid.py 3 0.01 > gpurun_out/g_list.log 2>&1
+for pf in 2 3; do XGS_GRID_PF=$pf timeout 600 python tools/grid_bench.py 5 > gpurun_out/g_bench_$pf.log 2>&1; done

@@ -11,5 +11,10 @@ import bench
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 out = bench.run_grid(torch, steps, cpu=False)
 for v, g in out.items():
-    print(v, json.dumps({k: g[k] for k in ("Mpts_per_s", "ms_per_batch", "sorted_items", "new_voxels", "per_kernel_ms")}),
-          "frac", g["roofline"]["frac"])
+    if not isinstance(g, dict):
+        continue
+    print(v, json.dumps({k: g[k] for k in ("Mpts_per_s", "ms_per_batch", "ms_per_batch_python_call",
+                                            "ms_per_batch_events", "items_inserted", "batch_voxels", "new_voxels",
+                                            "rejected_frac", "map_voxels_before", "map_scene_voxels",
+                                            "map_warm_frames", "per_stage_ms", "batch_hbm_frac")}),
+          "front_frac", g["roofline"]["frac"])

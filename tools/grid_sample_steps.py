@@ -44,17 +44,13 @@ for it in range(50):
     fr = nat.GridFrames(F, H, W, d.data_ptr(), col.data_ptr(), Rr.data_ptr(), tr.data_ptr(), fx, fy, cx, cy, gs.voxel, 1,
                         0, gs.min_scale, None, 0, 0, 0); t0 = mark("frames struct", t0)
     res = nat.GridResult(cap, b, b + 8 * cap, b + 16 * cap, b + 40 * cap, b + 64 * cap, b + 72 * cap, None,
-                         b + 80 * cap, 0, 0, 0, 0, 0); t0 = mark("result struct", t0)
+                         b + 80 * cap, 0, 0, 0, 0, 0, 0); t0 = mark("result struct", t0)
     ws = nat.workspace("grid", nat.lib().xgs_grid_workspace(F * H * W)); t0 = mark("workspace", t0)
     sp = nat.stream_ptr(); t0 = mark("stream_ptr", t0)
     nat.call("xgs_grid_sample", ctypes.byref(fr), hs._h, ctypes.byref(res), nat.ptr(ws), ws.numel(), sp)
     t0 = mark("native call", t0)
     n = int(res.n_new)
-    out = g.GridSampleResult(key=flat[:n].view(t.int64), pid=flat[cap:cap + n].view(t.int64),
-                             mu=flat[2 * cap:2 * cap + 3 * n].view(n, 3), color=flat[5 * cap:5 * cap + 3 * n].view(n, 3),
-                             scale=flat[8 * cap:8 * cap + n], depth=flat[9 * cap:9 * cap + n],
-                             count=flat[10 * cap:10 * cap + n], feature=None, n_valid=int(res.n_valid),
-                             n_voxels=int(res.n_voxels), n_sorted=int(res.n_sorted),
-                             sort_passes=int(res.sort_passes)); t0 = mark("wrap", t0)
+    out = g.GridSampleResult(flat, cap, n, None, int(res.n_valid), int(res.n_voxels), int(res.n_sorted),
+                             int(res.sort_passes)); t0 = mark("wrap", t0)
 for k, v in acc.items():
     print(f"{k:16s} {np.median(v[5:]):8.1f} us")
