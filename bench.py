@@ -416,54 +416,67 @@ def run_stream(torch, frames, device):
                         "VQ K=512 D=768 on the new points (synthetic 512-centre features)"}
 
 
-C5_ROWS, C5_D, C5_K = 67_108_864 // 8, 1152, 4096
+C5_TOTAL, C5_D, C5_K, C5_CENTRES = 67_108_864, 1152, 4096, 4096
+C5_WORKLOAD = ("C5: multi-GPU VQ, N=67,108,864 rows in total x D=1152 bf16 (fp64-exact assignment), K=4096, "
+               "lam=0.99, delta=1e-3, gamma=0.5/K; rows sharded across the ranks (strong scaling)")
+
+
+def c5_data(torch, rank, world, device):
+    """This rank's contiguous shard of the C5 batch, generated on the device
+    (4096-centre unit-norm mixture, sigma 0.05, stored bf16; centres and the
+    initial codebook are identical on every rank), plus E0 (K random rows of
+    the same mixture, fp64)."""
+    from paper_2603_09632_b200.distributed import strong_shard
+    _, rows = strong_shard(C5_TOTAL, world, rank)
+    g = torch.Generator(device=device)
+    g.manual_seed(40)
+    C = torch.randn(C5_CENTRES, C5_D, generator=g, device=device)
+    C /= C.norm(dim=1, keepdim=True)
+    x = torch.empty(rows, C5_D, device=device, dtype=torch.bfloat16)
+    chunk = 1 << 20
+    for s0 in range(0, rows, chunk):
+        g.manual_seed(1_000_003 * (rank + 1) + s0 // chunk)    # per-(rank, chunk) stream
+        m = min(chunk, rows - s0)
+        v = C[torch.randint(0, C5_CENTRES, (m,), generator=g, device=device)] + 0.05 * torch.randn(
+            m, C5_D, generator=g, device=device)
+        x[s0:s0 + m] = (v / v.norm(dim=1, keepdim=True)).to(torch.bfloat16)
+        del v
+    g.manual_seed(41)
+    e = C[torch.randint(0, C5_CENTRES, (C5_K,), generator=g, device=device)] + 0.05 * torch.randn(
+        C5_K, C5_D, generator=g, device=device)
+    E0 = (e / e.norm(dim=1, keepdim=True)).to(torch.bfloat16).double()
+    del C, e
+    torch.cuda.empty_cache()
+    return x, E0
 
 
 def run_c5(torch, iters, device):
-    """C5 per-GPU shard: N = 67,108,864/8 bf16 unit-norm D=1152 rows (4096-centre
-    mixture, sigma 0.05), K=4096 -- the share of one GPU in the 8-GPU C5 run."""
+    """C5 on ONE GPU (all 67,108,864 rows), for tools and the N=1 evidence:
+    ms per online_step iteration and the per-stage split."""
     from paper_2603_09632_b200 import _native as nat
     from paper_2603_09632_b200.distributed import CudaBackend, DataParallelVQ
     import paper_2603_09632_b200 as xv
-    g = torch.Generator(device=device)
-    g.manual_seed(40)
-    C = torch.randn(C5_K, C5_D, generator=g, device=device)
-    C /= C.norm(dim=1, keepdim=True)
-    x = torch.empty(C5_ROWS, C5_D, device=device, dtype=torch.bfloat16)
-    for s0 in range(0, C5_ROWS, 1 << 20):
-        m = min(1 << 20, C5_ROWS - s0)
-        v = C[torch.randint(0, C5_K, (m,), generator=g, device=device)] + 0.05 * torch.randn(
-            m, C5_D, generator=g, device=device)
-        x[s0:s0 + m] = (v / v.norm(dim=1, keepdim=True)).to(torch.bfloat16)
-    E0 = x[torch.randint(0, C5_ROWS, (C5_K,), generator=g, device=device)].double()
+    x, E0 = c5_data(torch, 0, 1, device)
     cfg = xv.VqConfig(K=C5_K, lam=0.99, gamma=0.5 / C5_K, delta_dead=1e-3)
     vq = DataParallelVQ((E0, torch.zeros(C5_K, dtype=torch.float64, device=device),
                          torch.zeros(C5_K, C5_D, dtype=torch.float64, device=device)), cfg,
                         np.random.default_rng(41), CudaBackend(C5_K, C5_D, 0.99, 1e-5))
-    for _ in range(max(1, int(os.environ.get("XGS_C5_WARM", "1")))):   # profiling aid: longer warm-up
-        vq.step(x, [C5_ROWS])
+    vq.step(x, [x.shape[0]])
     torch.cuda.synchronize()
     nat.profile_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(iters):
-        vq.step(x, [C5_ROWS])
+        vq.step(x, [x.shape[0]])
     e1.record()
     torch.cuda.synchronize()
     prof = {t: nat.profile_read(t)[0] / iters for t in ("vq_prep", "vq_screen", "vq_rerank", "vq_accumulate",
                                                           "vq_chain", "vq_ema")}
-    scr = nat.profile_read("vq_screen")
     nat.profile_enable(False)
     ms = e0.elapsed_time(e1) / iters
-    flops = 2.0 * C5_ROWS * C5_K * C5_D
-    cb_now = xv.Codebook._make(vq.state[0], vq.state[1], vq.state[2], 0.99, 1e-5, None)
-    _, (n_rerank, n_fallback) = xv.vq.assign_batch_stats(x, cb_now)
-    del x
-    return {"rows": C5_ROWS, "D": C5_D, "K": C5_K, "dtype": "bf16 rows", "iters": iters, "ms_per_iter": ms,
-            "Mfeat_per_s": C5_ROWS / (ms * 1e-3) / 1e6, "screen_ms": scr[0] / max(1, scr[1]),
-            "screen_TFLOPs": flops / (scr[0] / max(1, scr[1]) * 1e-3) / 1e12 if scr[1] else None,
-            "per_kernel_ms": prof, "assign_exact_rows": {"rerank": n_rerank, "fallback": n_fallback},
-            "workload": "C5 per-GPU shard (67,108,864 rows / 8 GPUs), one online_step per iteration"}
+    return {"rows": int(x.shape[0]), "iters": iters, "ms_per_iter": ms, "per_stage_ms": prof,
+            "max_memory_allocated_GB": torch.cuda.max_memory_allocated() / 1e9,
+            "device_memory_GB": torch.cuda.get_device_properties(device).total_memory / 1e9}
 
 
 def run_targets(torch, iters, cpu=True):
@@ -694,41 +707,233 @@ def cpu_port_rate(x_host, E, seconds=10.0, threads=None):
     return rows / el / 1e6, threads, rows, el
 
 
+def c5_host_sample(n, seed=40):
+    """A seeded host sample of the C5 distribution (4096-centre unit-norm
+    mixture, sigma 0.05, bf16-rounded rows as uint16 bit patterns) and an
+    initial codebook of K rows of it (fp64)."""
+    import torch
+    rng = np.random.default_rng(seed)
+    C = rng.normal(size=(C5_CENTRES, C5_D))
+    C /= np.linalg.norm(C, axis=1, keepdims=True)
+    x = C[rng.integers(0, C5_CENTRES, n)] + 0.05 * rng.normal(size=(n, C5_D))
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    xb = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16)
+    e = C[rng.integers(0, C5_CENTRES, C5_K)] + 0.05 * rng.normal(size=(C5_K, C5_D))
+    e /= np.linalg.norm(e, axis=1, keepdims=True)
+    E0 = torch.from_numpy(e.astype(np.float32)).to(torch.bfloat16).double().numpy()
+    return xb.view(torch.int16).numpy().view(np.uint16), E0
+
+
+def port_online_step(cb, xb, threads, rng):
+    """The reference's online_step (vq.py:193-212) with the mask provably
+    all-true (gamma = 0.5/K): assign + accumulate in the C restatement
+    (oracle/oracle.c, fp64, NumPy pairwise order, `threads` host threads),
+    reservoir extend, EMA and dead-code revival in NumPy (oracle/vq.py)."""
+    from oracle import native as on
+    from oracle import vq as ov
+    import torch
+    codes = on.assign(xb, cb.E, threads=threads, bf16=True)
+    counts, sums = on.accumulate(xb, codes, cb.K, bf16=True)
+    cb.reservoir.extend(torch.from_numpy(xb.view(np.int16)).view(torch.bfloat16).double().numpy())
+    cb = ov.ema_step(cb, counts, sums)
+    cb, _, _ = ov.revive_dead_codes(cb, DELTA, rng)
+    return cb
+
+
+def cpu_port_c5(seconds=10.0, threads=None):
+    """C5 config on the host cores: port_online_step over chunks of 64 rows
+    per thread until ~`seconds` elapse (bounded sample of the workload)."""
+    from oracle import vq as ov
+    threads = threads or os.cpu_count() or 1
+    chunk = 64 * threads
+    xs, E0 = c5_host_sample(max(4 * chunk, 8192))
+    cb = ov.OracleCodebook(E0, np.zeros(C5_K), np.zeros((C5_K, C5_D)), LAM, EPS, ov.OracleReservoir(CAP, C5_D))
+    rng = np.random.default_rng(42)
+    cb = port_online_step(cb, xs[:chunk], threads, rng)      # warm (page-in, thread pool)
+    rows, t0 = 0, time.perf_counter()
+    while True:
+        lo = (rows // chunk) % (xs.shape[0] // chunk) * chunk
+        cb = port_online_step(cb, xs[lo:lo + chunk], threads, rng)
+        rows += chunk
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return {"value": rows / el / 1e6, "unit": "Mfeat/s", "cores": threads, "kind": "port",
+            "sample": f"{rows} rows of the C5 distribution in {el:.1f}s, {chunk} rows per online_step "
+                      f"(assign+accumulate in oracle/oracle.c on {threads} threads, reservoir/EMA/revival in NumPy)"}
+
+
+def reference_numpy_leg(seconds=20.0):
+    """The UNMODIFIED reference's own semsplat.vq.online_step (baseline/_ref,
+    NumPy, single-threaded) on C5-shaped batches of 8 rows (its (n, K, D) fp64
+    broadcast temporary is 302 MB at 8 rows), timed for ~`seconds`."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "semsplat")):
+        return None
+    sys.path.insert(0, ref)
+    try:
+        from semsplat.core import Codebook, FeatureReservoir
+        from semsplat.vq import VqConfig, online_step
+    finally:
+        sys.path.remove(ref)
+    import torch
+    xs, E0 = c5_host_sample(256)
+    x = torch.from_numpy(xs.view(np.int16)).view(torch.bfloat16).double().numpy()
+    cb = Codebook(E=E0, N=np.zeros(C5_K), M=np.zeros((C5_K, C5_D)), lam=LAM, epsilon=EPS,
+                  reservoir=FeatureReservoir(CAP, C5_D))
+    cfg = VqConfig(K=C5_K, lam=LAM, gamma=0.5 / C5_K, delta_dead=DELTA, epsilon=EPS, reservoir_capacity=CAP)
+    rng = np.random.default_rng(42)
+    b = 8
+    cb, _ = online_step(cb, x[:b], cfg, rng)
+    rows, t0 = 0, time.perf_counter()
+    while True:
+        lo = rows % (x.shape[0] - b)
+        cb, _ = online_step(cb, x[lo:lo + b], cfg, rng)
+        rows += b
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return {"value": rows / el / 1e6, "unit": "Mfeat/s", "cores": 1, "kind": "reference",
+            "sample": f"{rows} rows of the C5 distribution through semsplat.vq.online_step (baseline/_ref, "
+                      f"unmodified NumPy) in {b}-row batches, {el:.1f}s"}
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the reference path's CPU port on all host cores."""
+    """--impl reference: the reference path's CPU implementation on the box's
+    host cores for the headline config (C5): the C restatement of online_step
+    (all host threads, 64 rows per thread per step), plus a labelled leg with
+    the reference's own NumPy online_step."""
     if rank != 0:
         return
-    rng = np.random.default_rng(10)
-    C = rng.normal(size=(CENTRES, D))
-    C /= np.linalg.norm(C, axis=1, keepdims=True)
-    n = 65536
-    x = C[rng.integers(0, CENTRES, n)] + SIGMA * rng.normal(size=(n, D))
-    x = (x / np.linalg.norm(x, axis=1, keepdims=True)).astype(np.float32)
-    E = x[rng.choice(n, K, replace=False)].astype(np.float64)
-    from oracle import native as on
+    from oracle import vq as ov
     threads = os.cpu_count() or 1
-    per_step = 8 * threads          # ~1-2 s of CPU per step on the box's cores
+    chunk = 64 * threads
+    xs, E0 = c5_host_sample(max(4 * chunk, 8192))
+    cb = ov.OracleCodebook(E0, np.zeros(C5_K), np.zeros((C5_K, C5_D)), LAM, EPS, ov.OracleReservoir(CAP, C5_D))
+    rng = np.random.default_rng(42)
     t_all, rows_all = 0.0, 0
     for it in range(args.warmup + args.steps):
-        lo = (it * per_step) % (n - per_step)
-        b = x[lo:lo + per_step]
+        lo = (it * chunk) % (xs.shape[0] - chunk + 1)
         t0 = time.perf_counter()
-        codes = on.assign(b, E, threads=threads)
-        on.accumulate(b, codes, K)
+        cb = port_online_step(cb, xs[lo:lo + chunk], threads, rng)
         dt = time.perf_counter() - t0
         if it >= args.warmup:
             t_all += dt
-            rows_all += per_step
+            rows_all += chunk
     v = rows_all / t_all / 1e6
-    line = {"metric": METRIC, "value": v, "unit": "Mfeat/s", "impl": "reference", "n_gpus": world,
+    line = {"metric": "VQ Mfeat/s (online_step: assign + accumulate + EMA + revival), C5 strong scaling",
+            "value": v, "unit": "Mfeat/s", "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "cpu_rows_per_step": per_step},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded 4096-centre unit-norm mixture, bf16-rounded)",
+            "config": {"workload": C5_WORKLOAD, "cpu_rows_per_step": chunk},
             "cpu_baseline": {"value": v, "unit": "Mfeat/s", "cores": threads, "kind": "port",
-                             "sample": f"{per_step} rows/step of the C2 distribution, K={K}, D={D}; "
-                                       "oracle/oracle.c restatement of vq.py assign_batch+accumulate"},
+                             "sample": f"{chunk} rows/step of the C5 distribution, K={C5_K}, D={C5_D}: "
+                                       "oracle/oracle.c assign+accumulate + NumPy reservoir/EMA/revival "
+                                       "(vq.py:193-212)"},
             "e2e": {"value": v, "unit": "Mfeat/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if not args.no_cpu:
+        line["reference_numpy"] = reference_numpy_leg(min(20.0, args.cpu_seconds * 2))
     print(json.dumps(line), flush=True)
+
+
+def timed_steps(torch, vq, x, sizes, steps, barrier, world, device):
+    """K timed online_steps bracketed by barrier + synchronize, CUDA events on
+    the launching stream, max over ranks."""
+    torch.cuda.synchronize()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(steps):
+        vq.step(x, sizes)
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def profiled_steps(torch, vq, x, sizes, steps):
+    from paper_2603_09632_b200 import _native as nat
+    nat.profile_enable(True)
+    for _ in range(steps):
+        vq.step(x, sizes)
+    torch.cuda.synchronize()
+    prof = {t: nat.profile_read(t) for t in ("vq_prep", "vq_screen", "vq_rerank", "vq_accumulate", "vq_chain",
+                                               "vq_ema")}
+    nat.profile_enable(False)
+    return prof
+
+
+def screen_roofline(prof, flops_per_step, steps):
+    pk, pk_kind = peaks()
+    scr_ms, scr_n = prof["vq_screen"]
+    # per step: the screen stage's event-timed span (main pass + rescreen of
+    # every row chunk) on the launching stream
+    t_step = scr_ms / max(1, steps)
+    achieved = flops_per_step / (t_step * 1e-3) / 1e12 if scr_n else None
+    peak = pk.get("bf16_tflops", pk.get("bf16_tflops_sustained"))
+    peak_sus = pk.get("bf16_tflops_sustained")
+    return {"bound": "tensor", "kernel": "screen_kernel (tcgen05 kind::f16, cta_group::2)",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": None,
+            "peak_kind": f"{pk_kind} bf16 dense burst (f16 rate == bf16 rate)",
+            "frac_vs_sustained": (achieved / peak_sus) if (achieved and peak_sus) else None,
+            "algorithmic_flops_per_step": flops_per_step, "screen_ms_per_step": t_step}
+
+
+def run_c2(torch, args, device):
+    """BASELINE configs[1] (C2) on one GPU: N = 1,048,576 fp32 D=512 rows, K=1024,
+    device-resident batch; plus its e2e through the public API with a pinned
+    host batch (H2D inside the timed region) and the CPU port."""
+    from paper_2603_09632_b200 import _native as nat
+    from paper_2603_09632_b200.distributed import CudaBackend, DataParallelVQ
+    import paper_2603_09632_b200 as xv
+    cfg = xv.VqConfig(K=K, lam=LAM, gamma=0.5 / K, delta_dead=DELTA, epsilon=EPS, reservoir_capacity=CAP)
+    x, E0 = make_data(torch, 0, device)
+    be = CudaBackend(K, D, LAM, EPS)
+    vq = DataParallelVQ((E0.clone(), torch.zeros(K, dtype=torch.float64, device=device),
+                         torch.zeros(K, D, dtype=torch.float64, device=device)), cfg, np.random.default_rng(12), be)
+    for _ in range(args.warmup):
+        vq.step(x, [N_ROWS])
+    steps = max(args.steps, 20)
+    ms = timed_steps(torch, vq, x, [N_ROWS], steps, lambda: None, 1, device) / steps
+    prof = profiled_steps(torch, vq, x, [N_ROWS], 10)
+    cb_now = xv.Codebook._make(vq.state[0], vq.state[1], vq.state[2], LAM, EPS, None)
+    _, (n_rerank, n_fallback) = xv.vq.assign_batch_stats(x, cb_now)
+    xh = x.cpu().pin_memory()
+    vq2 = DataParallelVQ((E0.clone(), torch.zeros(K, dtype=torch.float64, device=device),
+                          torch.zeros(K, D, dtype=torch.float64, device=device)), cfg, np.random.default_rng(12), be)
+    vq2.step(xh, [N_ROWS])
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        vq2.step(xh, [N_ROWS])
+        vq2.state[0].cpu()
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / 3
+    out = {"workload": WORKLOAD, "Mfeat_per_s": N_ROWS / (ms * 1e-3) / 1e6, "ms_per_step": ms, "steps": steps,
+           "roofline": screen_roofline(prof, 2.0 * N_ROWS * K * D, 10),
+           "per_kernel": {t: {"ms_per_step": m / 10, "launches": c} for t, (m, c) in prof.items()},
+           "assign_exact_rows": {"rerank": n_rerank, "fallback": n_fallback},
+           "e2e": {"value": N_ROWS / (e2e_ms * 1e-3) / 1e6, "unit": "Mfeat/s", "h2d_bytes_per_step": N_ROWS * D * 4,
+                   "d2h_bytes_per_step": K * D * 8, "ms_per_step": e2e_ms}}
+    if not args.no_cpu:
+        xs = x[:65536].cpu().numpy()
+        v, thr, rows, el = cpu_port_rate(xs, E0.cpu().numpy(), seconds=args.cpu_seconds)
+        out["cpu_baseline"] = {"value": v, "unit": "Mfeat/s", "cores": thr, "kind": "port",
+                               "sample": f"{rows} rows of the C2 batch in {el:.1f}s (assign+accumulate, "
+                                         f"oracle/oracle.c, {thr} threads)"}
+    del x, xh, vq, vq2
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():
@@ -737,13 +942,13 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-grid", action="store_true")
+    ap.add_argument("--no-c2", action="store_true")
     ap.add_argument("--grid-steps", type=int, default=5)
     ap.add_argument("--stream-frames", type=int, default=1000)
-    ap.add_argument("--c5-iters", type=int, default=20)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -764,146 +969,114 @@ def main():
     from paper_2603_09632_b200 import _native as nat
     from paper_2603_09632_b200.distributed import CudaBackend, DataParallelVQ
 
-    cfg = xv.VqConfig(K=K, lam=LAM, gamma=0.5 / K, delta_dead=DELTA, epsilon=EPS, reservoir_capacity=CAP)
-    x, E0 = make_data(torch, rank, device)
-    state = (E0.clone(), torch.zeros(K, dtype=torch.float64, device=device),
-             torch.zeros(K, D, dtype=torch.float64, device=device))
-    be = CudaBackend(K, D, LAM, EPS)
-    vq = DataParallelVQ(state, cfg, np.random.default_rng(12), be)
-    sizes = [N_ROWS] * world
-
     def barrier():
         if world > 1:
             dist.barrier()
 
+    # ---------------- headline: C5 strong scaling (67,108,864 rows split over the ranks)
+    cfg = xv.VqConfig(K=C5_K, lam=LAM, gamma=0.5 / C5_K, delta_dead=DELTA, epsilon=EPS, reservoir_capacity=CAP)
+    x, E0 = c5_data(torch, rank, world, device)
+    rows = int(x.shape[0])
+    from paper_2603_09632_b200.distributed import strong_shard
+    sizes = [strong_shard(C5_TOTAL, world, r)[1] for r in range(world)]
+    be = CudaBackend(C5_K, C5_D, LAM, EPS)
+    state0 = (E0, torch.zeros(C5_K, dtype=torch.float64, device=device),
+              torch.zeros(C5_K, C5_D, dtype=torch.float64, device=device))
+    vq = DataParallelVQ(tuple(t.clone() for t in state0), cfg, np.random.default_rng(42), be)
     for _ in range(args.warmup):
         vq.step(x, sizes)
-    torch.cuda.synchronize()
-    barrier()
     clk = ClockSampler(local)
     clk.start()
     l0 = nat.launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    barrier()
-    ev0.record()
-    for _ in range(args.steps):
-        vq.step(x, sizes)
-    ev1.record()
-    torch.cuda.synchronize()
-    barrier()
+    ms = timed_steps(torch, vq, x, sizes, args.steps, barrier, world, device)
     launches = nat.launch_count() - l0
     clocks = clk.stop()
-    ms = ev0.elapsed_time(ev1)
-    # per-kernel breakdown from a separate profiled run (its event records are
-    # host work on the launch path, so the headline loop above runs without them)
-    prof_steps = min(args.steps, 10)
-    nat.profile_enable(True)
-    for _ in range(prof_steps):
-        vq.step(x, sizes)
-    torch.cuda.synchronize()
-    prof = {t: nat.profile_read(t) for t in ("vq_prep", "vq_screen", "vq_rerank", "vq_accumulate", "vq_chain",
-                                               "vq_ema")}
-    nat.profile_enable(False)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     ms_step = ms / args.steps
-    value = world * N_ROWS / (ms_step * 1e-3) / 1e6
-
-    # rows re-ranked / rescanned exactly in one assign (evidence for the screening bound)
+    value = C5_TOTAL / (ms_step * 1e-3) / 1e6
+    prof_steps = 3
+    prof = profiled_steps(torch, vq, x, sizes, prof_steps)
     cb_now = xv.Codebook._make(vq.state[0], vq.state[1], vq.state[2], LAM, EPS, None)
     _, (n_rerank, n_fallback) = xv.vq.assign_batch_stats(x, cb_now)
+    roof = screen_roofline(prof, 2.0 * rows * C5_K * C5_D, prof_steps)
 
-    # end-to-end through the public API with host buffers (pinned), per step:
-    # H2D of the shard + device step + D2H of the updated codebook E
-    xh = x.cpu().pin_memory()
-    e2e_steps = max(1, args.e2e_steps)
-    vq2 = DataParallelVQ((E0.clone(), torch.zeros_like(state[1]), torch.zeros_like(state[2])), cfg,
-                         np.random.default_rng(12), be)
-    vq2.step(xh, sizes)
+    # e2e through the public API: every step copies its rows from pinned host
+    # memory (H2D inside the timed region, overlapped chunk by chunk with the
+    # device work) and reads the updated codebook back.  Pinning the whole
+    # 154.6 GB / N shard is not done: each step streams E2E_ROWS rows per rank
+    # (the same distribution, K, D and dtype); the rate is PCIe-bound.
+    del vq
+    e2e_rows = min(min(sizes), 1 << 22)
+    xh = x[:e2e_rows].cpu().pin_memory()
+    del x
+    torch.cuda.empty_cache()
+    vq2 = DataParallelVQ(tuple(t.clone() for t in state0), cfg, np.random.default_rng(42), be)
+    e2e_sizes = [e2e_rows] * world
+    vq2.step(xh, e2e_sizes)
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(e2e_steps):
-        vq2.step(xh, sizes)
-        Eh = vq2.state[0].cpu()
+    for _ in range(max(1, args.e2e_steps)):
+        vq2.step(xh, e2e_sizes)
+        vq2.state[0].cpu()
     e1.record()
     torch.cuda.synchronize()
     barrier()
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    e2e_ms = e0.elapsed_time(e1) / max(1, args.e2e_steps)
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_val = world * N_ROWS / (e2e_ms * 1e-3) / 1e6
+    e2e_val = world * e2e_rows / (e2e_ms * 1e-3) / 1e6
+    del vq2, xh
+    torch.cuda.empty_cache()
 
-    pk, pk_kind = peaks()
-    scr_ms, scr_n = prof["vq_screen"]
-    traffic = None
-    try:   # DRAM bytes of screen_kernel from the committed `ncu --set full` capture
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get("screen_kernel_C2")
-    except (OSError, ValueError):
-        pass
-    flops = 2.0 * N_ROWS * K * D
-    achieved = flops / (scr_ms / max(1, scr_n) * 1e-3) / 1e12 if scr_n else None
-    # burst figure: the sampled SM clock stays at its maximum through the timed
-    # region (no power-cap throttling), so the sustained figure would flatter
-    peak = pk.get("bf16_tflops", pk.get("bf16_tflops_sustained"))
-    peak_sus = pk.get("bf16_tflops_sustained")
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        xs = x[:65536].cpu().numpy()
-        v, thr, rows, el = cpu_port_rate(xs, E0.cpu().numpy(), seconds=args.cpu_seconds)
-        cpu = {"value": v, "unit": "Mfeat/s", "cores": thr, "kind": "port",
-               "sample": f"{rows} rows of the C2 batch in {el:.1f}s (assign+accumulate, oracle/oracle.c, "
-                         f"{thr} threads)"}
-    grid = stream = None
-    if rank == 0 and world == 1 and not args.no_grid:
-        grid = run_grid(torch, args.grid_steps, cpu=not args.no_cpu)
-    if rank == 0 and world == 1 and args.stream_frames > 0:
-        stream = run_stream(torch, args.stream_frames, device)
-    targets = None
-    if rank == 0 and world == 1 and not args.no_grid:
-        targets = run_targets(torch, 10, cpu=not args.no_cpu)
-    consumers = raster = init = None
-    if rank == 0 and world == 1 and not args.no_grid:
-        init = run_init(torch, cpu=not args.no_cpu)
-        consumers = run_consumers(torch, 5, cpu=not args.no_cpu)
-        raster = run_raster(torch, 3, cpu=not args.no_cpu)
-    c5 = None
-    if rank == 0 and world == 1 and args.c5_iters > 0:
-        del x
-        torch.cuda.empty_cache()
-        c5 = run_c5(torch, args.c5_iters, device)
+    cpu = c2 = grid = stream = targets = consumers = raster = init = None
+    if rank == 0 and world == 1:
+        if not args.no_cpu:
+            cpu = cpu_port_c5(args.cpu_seconds)
+        if not args.no_c2:
+            c2 = run_c2(torch, args, device)
+        if not args.no_grid:
+            grid = run_grid(torch, args.grid_steps, cpu=not args.no_cpu)
+        if args.stream_frames > 0:
+            stream = run_stream(torch, args.stream_frames, device)
+        if not args.no_grid:
+            targets = run_targets(torch, 10, cpu=not args.no_cpu)
+            init = run_init(torch, cpu=not args.no_cpu)
+            consumers = run_consumers(torch, 5, cpu=not args.no_cpu)
+            raster = run_raster(torch, 3, cpu=not args.no_cpu)
     if rank == 0:
         per_kernel = {t: {"ms_per_step": m / prof_steps, "launches": c} for t, (m, c) in prof.items()}
+        g1 = (grid or {}).get("0.01") or {}
         line = {
-            "metric": METRIC, "value": value, "unit": "Mfeat/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f16-screen/f64-exact", "data": "synthetic (seeded 1024-centre mixture)",
-            "config": {"workload": WORKLOAD, "global_batch": world * N_ROWS, "rows_per_gpu": N_ROWS, "K": K,
-                       "D": D, "parallelism": f"dp{world}", "iterations": args.steps,
-                       "l2": "batch 2 GiB/GPU > 126 MB L2 (no flush needed)"},
-            "e2e": {"value": e2e_val, "unit": "Mfeat/s", "h2d_bytes_per_step": N_ROWS * D * 4,
-                    "d2h_bytes_per_step": K * D * 8, "ms_per_step": e2e_ms},
+            "metric": "VQ Mfeat/s (online_step: assign + accumulate + EMA + revival), C5 strong scaling",
+            "value": value, "unit": "Mfeat/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16 rows, f16-screen/f64-exact",
+            "data": "synthetic (seeded 4096-centre unit-norm mixture, generated on device)",
+            "config": {"workload": C5_WORKLOAD, "global_batch": C5_TOTAL, "rows_per_gpu": rows, "K": C5_K,
+                       "D": C5_D, "parallelism": f"dp{world}", "iterations": args.steps,
+                       "l2": "batch 154.6 GB / N per GPU > 126 MB L2 (no flush needed)"},
+            "c5_ms_per_iter": ms_step, "c2_Mfeat_s": (c2 or {}).get("Mfeat_per_s"),
+            "grid_c3_Gpts_s": (g1.get("Mpts_per_s") or 0) / 1e3 if g1 else None,
+            "grid_c3_ms": g1.get("ms_per_batch"), "grid_front_hbm_frac": (g1.get("roofline") or {}).get("frac"),
+            "grid_batch_hbm_frac": g1.get("batch_hbm_frac"),
+            "stream_p50_ms": (stream or {}).get("p50_ms"), "stream_p99_ms": (stream or {}).get("p99_ms"),
+            "e2e": {"value": e2e_val, "unit": "Mfeat/s", "h2d_bytes_per_step": world * e2e_rows * C5_D * 2,
+                    "d2h_bytes_per_step": C5_K * C5_D * 8, "ms_per_step": e2e_ms,
+                    "rows_per_step": world * e2e_rows,
+                    "note": "pinned host rows streamed into the step (H2D chunks overlapped with the device work); "
+                            "4,194,304 rows per rank per step (the whole shard is not pinned), same K/D/dtype"},
             "gpu_launches": launches,
-            "roofline": {"bound": "tensor", "kernel": "screen_kernel (tcgen05 kind::f16)",
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "peak_kind": f"{pk_kind} bf16 dense burst (f16 rate == bf16 rate)",
-                         "frac_vs_sustained": (achieved / peak_sus) if (achieved and peak_sus) else None,
-                         "algorithmic_flops_per_launch": flops},
+            "roofline": roof,
             "per_kernel": per_kernel,
             "assign_exact_rows": {"rerank": n_rerank, "fallback": n_fallback},
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "c2": c2,
             "grid": grid,
             "stream": stream,
-            "c5_shard": c5,
             "targets": targets,
             "consumers": consumers,
             "raster": raster,

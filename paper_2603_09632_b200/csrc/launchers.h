@@ -2,6 +2,8 @@
 // C-ABI layer (capi.cu).  No torch types anywhere: plain pointers + sizes.
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stddef.h>
@@ -77,8 +79,24 @@ cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* h
 // staged form used by the row-chunk pipeline: codebook prep once, then per
 // chunk of rows [r0, r1): operand prep, screen + re-rank + exact rescan
 constexpr int kMaxChunks = 64;
+// Rows per screening chunk (the unit the per-row screening buffers are sized
+// for): the whole batch up to 2^21 rows, else 2^21 (or n / kMaxChunks rounded
+// up to a 256-row tile pair when that is larger).
+// XGS_SCREEN_CHUNK_ROWS overrides the 2^21 (tests drive the multi-chunk
+// slot ring with small batches).
+inline int64_t screen_chunk_rows(int64_t n) {
+  static const int64_t env = [] {
+    const char* v = std::getenv("XGS_SCREEN_CHUNK_ROWS");
+    return v ? (int64_t)std::atoll(v) : (int64_t)0;
+  }();
+  const int64_t base = env >= 256 ? env / 256 * 256 : (int64_t)1 << 21;
+  if (n <= base) return n > 0 ? n : 1;
+  int64_t c = (n + kMaxChunks - 1) / kMaxChunks;
+  c = (c + 255) / 256 * 256;
+  return c > base ? c : base;
+}
 cudaError_t screen_prepare(const ScreenArgs& a, cudaStream_t s);
-cudaError_t screen_prep_rows(const ScreenArgs& a, int64_t r0, int64_t r1, cudaStream_t s);
+cudaError_t screen_prep_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, cudaStream_t s);
 cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, cudaStream_t s);
 cudaError_t screen_finish(const ScreenArgs& a, int chunks, cudaStream_t s, int32_t* host_stats);
 

@@ -75,6 +75,9 @@ int pipeline_chunks(int64_t n, int sm_count, int64_t* chunk_rows, bool host_src)
   if (chunks < 1) chunks = 1;
   const int64_t wpc = (waves + chunks - 1) / chunks;
   *chunk_rows = wpc * wave;
+  // never more rows than one slot of the screening buffers holds
+  const int64_t cap = screen_chunk_rows(n);
+  if (*chunk_rows > cap) *chunk_rows = cap;
   return (int)((n + *chunk_rows - 1) / *chunk_rows);
 }
 
@@ -103,7 +106,11 @@ cudaError_t launch_assign_accumulate(const ScreenArgs& a, double* counts, double
           cudaSuccess)
         return e;
     }
-    if ((e = screen_prep_rows(a, r0, r1, r->sp)) != cudaSuccess) return e;
+    // chunk c reuses the screening-buffer slot of chunk c - slots: its prep
+    // waits until that chunk's screen + re-rank (which read the slot) ran
+    const int slots = a.n > screen_chunk_rows(a.n) ? 2 : 1;
+    if (c >= slots && (e = cudaStreamWaitEvent(r->sp, r->eva[c - slots], 0)) != cudaSuccess) return e;
+    if ((e = screen_prep_rows(a, r0, r1, c, r->sp)) != cudaSuccess) return e;
     if ((e = cudaEventRecord(r->evp[c], r->sp)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(s, r->evp[c], 0)) != cudaSuccess) return e;
     if ((e = screen_rows(a, r0, r1, c, s)) != cudaSuccess) return e;

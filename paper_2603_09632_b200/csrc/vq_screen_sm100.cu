@@ -791,19 +791,29 @@ prep_rows_kernel(const X* __restrict__ x, int64_t n, int64_t d, int64_t ldx, int
 constexpr int kCntBase = 8;
 constexpr int kCntStride = 4;
 
+// Per-row screening buffers (fp16 operand copy, bound terms, re-rank and
+// fallback queues) exist for one row CHUNK only, in slots: one slot when the
+// batch is a single chunk, two otherwise (chunk c uses slot c % 2; the prep of
+// chunk c waits until the screen of chunk c - 2 released the slot).  So the
+// workspace is bounded by the chunk, not the batch: at C5 (67,108,864 bf16
+// rows x 1152 on one GPU) it is ~10 GB next to the 154.6 GB batch instead of
+// another full-size fp16 copy of it.
 struct ScreenWs {
   size_t off_ab, off_xn, off_xf, off_eb, off_cn, off_rq, off_fq, off_cnt, total;
   size_t off_sq, off_ab2, off_xn2, off_xf2;   // top-2 rescreen: row queue + compact operand copies
   int64_t kp, dp, sq_cap;
+  int64_t chunk_rows, slots;                  // rows per slot, number of slots
 };
 
 ScreenWs screen_ws(int64_t n, int64_t k, int64_t d) {
   ScreenWs w;
   w.kp = (k + BN - 1) / BN * BN;
   w.dp = (d + BK - 1) / BK * BK;
+  w.chunk_rows = screen_chunk_rows(n);
+  w.slots = n > w.chunk_rows ? 2 : 1;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 1023) / 1024 * 1024; return r; };
-  const size_t nn = (size_t)(n > 0 ? n : 1);
+  const size_t nn = (size_t)(w.chunk_rows > 0 ? w.chunk_rows : 1) * (size_t)w.slots;
   w.off_ab = take(nn * (size_t)w.dp * 2);
   w.off_xn = take(nn * 4);
   w.off_xf = take(nn * 4);
@@ -812,7 +822,7 @@ ScreenWs screen_ws(int64_t n, int64_t k, int64_t d) {
   w.off_rq = take(nn * sizeof(RerankEntry));
   w.off_fq = take(nn * 4);
   w.off_cnt = take(sizeof(int32_t) * (kCntBase + kCntStride * kMaxChunks));
-  w.sq_cap = n / 8 > 4096 ? n / 8 : 4096;
+  w.sq_cap = w.chunk_rows / 8 > 4096 ? w.chunk_rows / 8 : 4096;
   const size_t sc = (size_t)w.sq_cap;
   w.off_sq = take(sc * 4);
   w.off_ab2 = take(sc * (size_t)w.dp * 2);
@@ -942,17 +952,19 @@ cudaError_t screen_prepare(const ScreenArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t screen_prep_rows(const ScreenArgs& a, int64_t r0, int64_t r1, cudaStream_t s) {
+cudaError_t screen_prep_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, cudaStream_t s) {
   const ScreenBufs b = screen_bufs(a);
   const int64_t n = r1 - r0;
   if (n <= 0) return cudaSuccess;
+  if (n > b.w.chunk_rows) return cudaErrorInvalidValue;
   ProfScope prof("vq_prep", s);
   const float inflate = 1.f + (float)(a.d + 8) * 1.2e-7f;
   const unsigned rblocks = (unsigned)((n + 7) / 8);
   const int64_t dp = b.w.dp;
-  __half* Ab = b.Ab + r0 * dp;
-  float* xn = b.xn + r0;
-  float* xf = b.xf + r0;
+  const int64_t sb = (chunk % b.w.slots) * b.w.chunk_rows;   // this chunk's slot
+  __half* Ab = b.Ab + sb * dp;
+  float* xn = b.xn + sb;
+  float* xf = b.xf + sb;
   switch (a.dtype) {
     case F32: prep_rows_kernel<float><<<rblocks, 256, 0, s>>>((const float*)a.x + r0 * a.ldx, n, a.d, a.ldx, dp, b.emax, b.emax + 1, 1.0e-12f, Ab, xn, xf, inflate); count_launches(1); break;
     case F64: prep_rows_kernel<double><<<rblocks, 256, 0, s>>>((const double*)a.x + r0 * a.ldx, n, a.d, a.ldx, dp, b.emax, b.emax + 1, 1.0e-12f, Ab, xn, xf, inflate); count_launches(1); break;
@@ -967,13 +979,15 @@ cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, 
   if (n <= 0) return cudaSuccess;
   if (chunk < 0 || chunk >= kMaxChunks) return cudaErrorInvalidValue;
   const int64_t dp = b.w.dp;
+  if (n > b.w.chunk_rows) return cudaErrorInvalidValue;
+  const int64_t sb = (chunk % b.w.slots) * b.w.chunk_rows;   // this chunk's slot
   CUtensorMap tmA, tmB;
-  if (!make_map(&tmA, b.Ab + r0 * dp, (uint64_t)dp, (uint64_t)n, (uint64_t)dp * 2, BK, BM) ||
+  if (!make_map(&tmA, b.Ab + sb * dp, (uint64_t)dp, (uint64_t)n, (uint64_t)dp * 2, BK, BM) ||
       !make_map(&tmB, b.Eb, (uint64_t)dp, (uint64_t)b.w.kp, (uint64_t)dp * 2, BK, BNH))
     return cudaErrorInvalidValue;
   int32_t* cnt = b.cnt + kCntBase + kCntStride * chunk;
-  RerankEntry* rq = b.rq + r0;
-  int32_t* fq = b.fq + r0;
+  RerankEntry* rq = b.rq + sb;
+  int32_t* fq = b.fq + sb;
   const void* x = static_cast<const char*>(a.x) + (size_t)r0 * (size_t)a.ldx * dtype_size(a.dtype);
   int64_t* codes = a.codes + r0;
 
@@ -988,8 +1002,8 @@ cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, 
   p.num_n_chunks = (int)(b.w.kp / BN);
   p.num_k_blocks = (int)(dp / BK);
   p.resident = p.num_k_blocks <= A_SLOTS;
-  p.xband = b.xn + r0;
-  p.xf = b.xf + r0;
+  p.xband = b.xn + sb;
+  p.xf = b.xf + sb;
   p.cn = b.cn;
   p.codes = codes;
   p.rq = rq;
@@ -1023,7 +1037,7 @@ cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, 
       count_launches(1);
       const int64_t cap = b.w.sq_cap;
       rescreen_gather_kernel<<<(unsigned)((cap + 7) / 8 < 148 * 8 ? (cap + 7) / 8 : 148 * 8), 256, 0, s>>>(
-          b.sq, cnt + 2, (int32_t)cap, b.Ab + r0 * dp, b.xn + r0, b.xf + r0, dp, b.Ab2, b.xn2, b.xf2);
+          b.sq, cnt + 2, (int32_t)cap, b.Ab + sb * dp, b.xn + sb, b.xf + sb, dp, b.Ab2, b.xn2, b.xf2);
       count_launches(1);
       CUtensorMap tmA2;
       if (!make_map(&tmA2, b.Ab2, (uint64_t)dp, (uint64_t)cap, (uint64_t)dp * 2, BK, BM)) return cudaErrorInvalidValue;
@@ -1075,9 +1089,14 @@ cudaError_t screen_finish(const ScreenArgs& a, int chunks, cudaStream_t s, int32
 cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* host_stats) {
   cudaError_t e;
   if ((e = screen_prepare(a, s)) != cudaSuccess) return e;
-  if ((e = screen_prep_rows(a, 0, a.n, s)) != cudaSuccess) return e;
-  if ((e = screen_rows(a, 0, a.n, 0, s)) != cudaSuccess) return e;
-  return screen_finish(a, 1, s, host_stats);
+  const int64_t crows = screen_chunk_rows(a.n);
+  const int chunks = (int)((a.n + crows - 1) / crows);
+  for (int c = 0; c < chunks; c++) {   // one stream: a slot is free again once the previous chunk's screen ran
+    const int64_t r0 = c * crows, r1 = r0 + crows < a.n ? r0 + crows : a.n;
+    if ((e = screen_prep_rows(a, r0, r1, c, s)) != cudaSuccess) return e;
+    if ((e = screen_rows(a, r0, r1, c, s)) != cudaSuccess) return e;
+  }
+  return screen_finish(a, chunks, s, host_stats);
 }
 
 }  // namespace xgs

@@ -86,6 +86,19 @@ class ReservoirMap:
         return first, cnt, (own0 + first) % cap
 
 
+def strong_shard(total: int, world: int, rank: int):
+    """Strong scaling (BASELINE configs[4]): the fixed global
+    batch of ``total`` rows split into contiguous shards in rank order, the
+    first ``total % world`` ranks taking one row more.  Returns (first global
+    row, rows) of ``rank``; the shards tile [0, total) exactly."""
+    if world < 1 or not (0 <= rank < world) or total < 0:
+        raise ValueError("bad shard request")
+    base, extra = divmod(int(total), int(world))
+    rows = base + (1 if rank < extra else 0)
+    first = rank * base + min(rank, extra)
+    return first, rows
+
+
 class DataParallelVQ:
     """Online VQ over row shards; ``backend`` does the device work."""
 

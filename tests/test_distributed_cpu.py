@@ -21,7 +21,7 @@ import torch.multiprocessing as mp
 
 from oracle import native as on
 from oracle import vq as ov
-from paper_2603_09632_b200.distributed import DataParallelVQ, ReservoirMap
+from paper_2603_09632_b200.distributed import DataParallelVQ, ReservoirMap, strong_shard
 from paper_2603_09632_b200.vq import VqConfig
 
 
@@ -130,10 +130,14 @@ def free_port():
     return p
 
 
-@pytest.mark.parametrize("sizes", [(100, 100), (30, 170)])
-def test_two_rank_vq_matches_single_process(tmp_path, sizes):
+@pytest.mark.parametrize("sizes", [(100, 100), (30, 170), tuple(strong_shard(200, 4, r)[1] for r in range(4))])
+def test_multi_rank_vq_matches_single_process(tmp_path, sizes):
+    """A FIXED global batch split across the ranks (strong scaling, as the
+    bench's C5 mode shards 67,108,864 rows / N) gives the single-process
+    online_step result."""
     out = str(tmp_path / "r.npz")
-    mp.start_processes(worker, args=(2, free_port(), out, sizes), nprocs=2, join=True, start_method="spawn")
+    world = len(sizes)
+    mp.start_processes(worker, args=(world, free_port(), out, sizes), nprocs=world, join=True, start_method="spawn")
     got = np.load(out)
     K, D, steps = 8, 5, 12
     E0, batches = make_stream(3, steps, sum(sizes), K, D)
@@ -148,6 +152,18 @@ def test_two_rank_vq_matches_single_process(tmp_path, sizes):
     assert np.array_equal(got["N"], cb.N)
     np.testing.assert_allclose(got["M"], cb.M, rtol=1e-12, atol=1e-13)
     np.testing.assert_allclose(got["E"], cb.E, rtol=1e-12, atol=1e-13)
+
+
+def test_strong_shard_tiles_the_batch():
+    for total, world in ((67_108_864, 1), (67_108_864, 2), (67_108_864, 8), (1000, 3), (7, 8)):
+        parts = [strong_shard(total, world, r) for r in range(world)]
+        assert parts[0][0] == 0 and sum(n for _, n in parts) == total
+        for (f0, n0), (f1, _) in zip(parts, parts[1:]):
+            assert f1 == f0 + n0
+        assert max(n for _, n in parts) - min(n for _, n in parts) <= 1
+    assert strong_shard(67_108_864, 8, 3) == (3 * 8_388_608, 8_388_608)
+    with pytest.raises(ValueError):
+        strong_shard(10, 2, 2)
 
 
 def test_reservoir_map_ownership():
