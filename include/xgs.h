@@ -248,7 +248,19 @@ typedef struct {
   double min_scale;        /* size = max(min_scale, 0.5*stride*depth/fx) (slam.py:631) */
   const float* feat;       /* [F,C,Hf,Wf] or NULL, gathered by supervision.py:133-147 */
   int64_t feat_c, feat_h, feat_w;
+  int32_t flags;           /* XGS_GRID_ASYNC: see below */
 } xgs_grid_frames;
+
+/* flags: XGS_GRID_ASYNC -- no host synchronisation and no allocation inside
+ * the call, so it can be captured in a CUDA graph: first-pick mode, device
+ * frames only, a library state sized by an earlier synchronous call on this
+ * device (same or larger frame batch), and a hash set created with room for
+ * every voxel the stream will insert (load <= 1/2).  n_new / n_valid /
+ * n_voxels are NOT returned in the struct (set to -1); out->dev_status
+ * (device int64[4]) receives {n_new, n_valid, n_voxels, error} when the
+ * batch's last kernel ends; error != 0 (batch table or map probing overflow)
+ * means the batch must be redone synchronously. */
+enum { XGS_GRID_ASYNC = 1 };
 
 typedef struct {
   int64_t capacity;        /* rows of every output array */
@@ -264,6 +276,7 @@ typedef struct {
   int64_t n_sorted, sort_passes;     /* radix-sort work of the call (items, 8-bit passes) */
   int32_t feat_dtype;      /* XGS_F32 (mode 0 only: the gathered value) or XGS_F64 (mode 0: widened;
                               mode 1: the fp64 pixel-order mean over the voxel's members) */
+  int64_t* dev_status;     /* device int64[4] {n_new, n_valid, n_voxels, error}, nullable (XGS_GRID_ASYNC) */
 } xgs_grid_result;
 
 XGS_API int xgs_grid_sample(const xgs_grid_frames* in, void* hashset, xgs_grid_result* out, void* ws,
@@ -275,6 +288,11 @@ XGS_API int xgs_grid_sample(const xgs_grid_frames* in, void* hashset, xgs_grid_r
  * the next; returns after the host frames were read. */
 XGS_API int xgs_grid_sample_h2d(const xgs_grid_frames* in, float* depth_dev, uint8_t* color_dev, void* hashset,
                                 xgs_grid_result* out, void* ws, size_t ws_bytes, void* stream);
+
+/* mask[i] = i < *n_dev for i < cap (uint8): the valid-row mask of a
+ * fixed-capacity batch whose row count is known only on the device (the
+ * graph-captured stream step feeds the grid's new voxels to the VQ this way). */
+XGS_API int xgs_prefix_mask(const int64_t* n_dev, int64_t cap, uint8_t* mask, void* stream);
 
 /* ------------------------------------------- SUPERVISION */
 

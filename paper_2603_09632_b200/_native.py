@@ -16,6 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libxgs.so")
 
 F32, F64, BF16 = 0, 1, 2
+GRID_ASYNC = 1
 EX_DIST, EX_CODE, EX_MASK, EX_PROB = 1, 2, 4, 8
 
 _lib = None
@@ -60,6 +61,7 @@ SIGNATURES = {
     "xgs_radix_sort_pairs_u64": (_i32, [_vp, _vp, _i64, _i32, _vp, _sz, _vp]),
     "xgs_grid_sample": (_i32, [_vp, _vp, _vp, _vp, _sz, _vp]),
     "xgs_grid_sample_h2d": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "xgs_prefix_mask": (_i32, [_vp, _i64, _vp, _vp]),
     "xgs_sup_gather": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _i64,
                               _i64, _vp, _vp, _vp, _vp]),
     "xgs_sup_loss": (_i32, [_vp, _vp, _vp, _i64, _i64, _f64, _vp, _vp, _vp]),
@@ -82,14 +84,15 @@ class GridFrames(ctypes.Structure):
     _fields_ = [("frames", _i64), ("height", _i64), ("width", _i64), ("depth", _vp), ("color", _vp),
                 ("rot", _vp), ("trans", _vp), ("fx", _f64), ("fy", _f64), ("cx", _f64), ("cy", _f64),
                 ("voxel", _f64), ("stride", ctypes.c_int32), ("mode", ctypes.c_int32), ("min_scale", _f64),
-                ("feat", _vp), ("feat_c", _i64), ("feat_h", _i64), ("feat_w", _i64)]
+                ("feat", _vp), ("feat_c", _i64), ("feat_h", _i64), ("feat_w", _i64), ("flags", ctypes.c_int32)]
 
 
 class GridResult(ctypes.Structure):
     """Mirror of xgs_grid_result (include/xgs.h)."""
     _fields_ = [("capacity", _i64), ("key", _vp), ("pid", _vp), ("mu", _vp), ("color", _vp), ("scale", _vp),
                 ("depth", _vp), ("feat", _vp), ("count", _vp), ("n_new", _i64), ("n_valid", _i64),
-                ("n_voxels", _i64), ("n_sorted", _i64), ("sort_passes", _i64), ("feat_dtype", ctypes.c_int32)]
+                ("n_voxels", _i64), ("n_sorted", _i64), ("sort_passes", _i64), ("feat_dtype", ctypes.c_int32),
+                ("dev_status", _vp)]
 
 
 class RasterIn(ctypes.Structure):

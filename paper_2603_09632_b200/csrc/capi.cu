@@ -461,6 +461,8 @@ static int grid_sample_call(const xgs_grid_frames* in, void* hashset, xgs_grid_r
   gi.fc = in->feat_c;
   gi.fh = in->feat_h;
   gi.fw = in->feat_w;
+  gi.async = (in->flags & XGS_GRID_ASYNC) != 0;
+  if (gi.async && (in->mode != 0 || depth_dev)) return fail(NOT_SUPPORTED, "XGS_GRID_ASYNC: first-pick, device frames only");
   GridOut go;
   go.capacity = out->capacity;
   go.key = out->key;
@@ -472,7 +474,10 @@ static int grid_sample_call(const xgs_grid_frames* in, void* hashset, xgs_grid_r
   go.feat = out->feat;
   go.feat64 = out->feat_dtype == XGS_F64;
   go.count = out->count;
+  go.dev_status = out->dev_status;
   cudaError_t e = grid_sample(gi, static_cast<HashSet*>(hashset), go, ws, ws_bytes, sm_count(), (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported) return fail(NOT_SUPPORTED, "XGS_GRID_ASYNC needs the library state sized by an "
+                                                "earlier synchronous batch of at least this size");
   out->n_new = go.n_new;
   out->n_valid = go.n_valid;
   out->n_voxels = go.n_voxels;
@@ -495,6 +500,14 @@ int xgs_grid_sample_h2d(const xgs_grid_frames* in, float* depth_dev, uint8_t* co
                         xgs_grid_result* out, void* ws, size_t ws_bytes, void* stream) {
   if (!depth_dev) return fail(INVALID_INPUT, "null depth staging buffer");
   return grid_sample_call(in, hashset, out, ws, ws_bytes, stream, depth_dev, color_dev);
+}
+
+int xgs_prefix_mask(const int64_t* n_dev, int64_t cap, uint8_t* mask, void* stream) {
+  if (cap < 0 || (cap > 0 && (!n_dev || !mask))) return fail(INVALID_INPUT, "bad prefix mask");
+  if (cap == 0) return OK;
+  cudaError_t e = launch_prefix_mask(n_dev, cap, mask, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_prefix_mask");
+  return OK;
 }
 
 // ---------------------------------------------------------------- SUPERVISION

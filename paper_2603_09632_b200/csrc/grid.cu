@@ -1363,6 +1363,13 @@ grid_emit_kernel(const int32_t* __restrict__ head_pos, const int32_t* __restrict
     emit_one(o, a.pid[o], head_pos, a);
 }
 
+__global__ void prefix_mask_kernel(const int64_t* __restrict__ n_dev, int64_t cap, uint8_t* __restrict__ mask) {
+  pdl_wait();
+  const int64_t n = *n_dev;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x)
+    mask[i] = i < n ? 1 : 0;
+}
+
 __global__ void fill_u64_kernel(unsigned long long* p, int64_t n, unsigned long long v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
@@ -1600,6 +1607,7 @@ dd_insert_pixels_kernel(const uint64_t* __restrict__ keys, int64_t n, int64_t W,
 // slots per thread per step with their map probes issued together.  Also
 // clears the emission look-back statuses for grid_pidlist_lb_kernel.
 constexpr int kScanILP = 8;
+constexpr int kMapProbe = 1 << 16;
 
 __global__ void __launch_bounds__(256, 3)
 dd_scan_map_kernel(unsigned long long* slots, int64_t cap, const int* overflow, unsigned long long* table,
@@ -1632,8 +1640,8 @@ dd_scan_map_kernel(unsigned long long* slots, int64_t cap, const int* overflow, 
       const uint64_t key = sl[j].x;
       uint64_t hh = th[j];
       unsigned long long v = tv[j];
-      bool isnew;
-      while (true) {
+      bool isnew = false;
+      for (int probe = 0;; probe++) {
         if (v == EMPTY) {
           v = atomicCAS(table + hh, (unsigned long long)EMPTY, (unsigned long long)key);
           if (v == EMPTY) {
@@ -1641,8 +1649,9 @@ dd_scan_map_kernel(unsigned long long* slots, int64_t cap, const int* overflow, 
             break;
           }
         }
-        if (v == key) {
-          isnew = false;
+        if (v == key) break;
+        if (probe == kMapProbe) {   // map set (nearly) full: report, never spin
+          atomicOr(const_cast<int*>(overflow), 2);
           break;
         }
         hh = (hh + 1) & tmask;
@@ -1677,7 +1686,7 @@ constexpr int kLbThreads = 256, kLbWords = 8, kLbTile = kLbThreads * kLbWords, k
 __global__ void __launch_bounds__(kLbThreads)
 grid_pidlist_lb_kernel(unsigned* __restrict__ flag_bits, int64_t nwords, unsigned long long* lb_status,
                        unsigned long long* cnts, int64_t capacity, int64_t* __restrict__ pid_out,
-                       int32_t* grand, volatile unsigned long long* host_status) {
+                       int32_t* grand, volatile unsigned long long* host_status, int64_t* dev_status) {
   __shared__ unsigned s_tile;
   __shared__ uint32_t s_wsum[kLbThreads / 32];
   __shared__ uint32_t s_base;
@@ -1783,6 +1792,12 @@ grid_pidlist_lb_kernel(unsigned* __restrict__ flag_bits, int64_t nwords, unsigne
         host_status[2] = cnts[2];   // items inserted / sorted
         host_status[3] = total;     // new voxels
         host_status[4] = cnts[5];   // table overflow flag
+        if (dev_status) {
+          dev_status[0] = (int64_t)total;
+          dev_status[1] = (int64_t)cnts[0];
+          dev_status[2] = (int64_t)cnts[1];
+          dev_status[3] = (int64_t)(cnts[5] & 0xffffffffull);
+        }
         for (int i = 0; i < 7; i++) cnts[i] = 0ull;
         __threadfence_system();
       }
@@ -1853,12 +1868,14 @@ constexpr int kDedupDevices = 16;
 DedupTable g_dedup[kDedupDevices];
 std::mutex g_dedup_mu;
 
-cudaError_t grid_state(int64_t npix, cudaStream_t s, DedupTable** out) {
+cudaError_t grid_state(int64_t npix, cudaStream_t s, DedupTable** out, bool may_alloc = true) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= kDedupDevices) return cudaErrorInvalidDevice;
   DedupTable& t = g_dedup[dev];
+  if (!may_alloc && (!t.misc || t.flag_words < (npix + 31) / 32 + 8 || t.dirty || !t.slots))
+    return cudaErrorNotSupported;
   if (!t.misc) {
     if ((e = cudaMalloc(&t.misc, 256)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(t.misc, 0, 256, s)) != cudaSuccess) return e;
@@ -1931,7 +1948,8 @@ cudaError_t pinned_status(unsigned long long** out) {
 // count read from device memory), then the batch's single synchronisation:
 // the last emission tile already wrote the counters into mapped host memory.
 cudaError_t emit_outputs(const GridIn& in, const Cam& cam, DedupTable* st, const int32_t* head, const uint64_t* sk,
-                         const uint32_t* sv, int64_t nitems, GridOut& out, int sms, cudaStream_t s, HostCopy* hcp) {
+                         const uint32_t* sv, int64_t nitems, GridOut& out, int sms, cudaStream_t s, HostCopy* hcp,
+                         bool sync = true) {
   ProfScope prof("grid_emit", s);
   cudaError_t e;
   const int64_t npix = in.frames * in.H * in.W;
@@ -1940,7 +1958,8 @@ cudaError_t emit_outputs(const GridIn& in, const Cam& cam, DedupTable* st, const
   unsigned long long* cnts = reinterpret_cast<unsigned long long*>(st->misc + 64);
   int32_t* grand = reinterpret_cast<int32_t*>(st->misc + 128);
   if ((e = launch_pdl(grid_pidlist_lb_kernel, dim3((unsigned)lb_tiles), dim3(kLbThreads), 0, s, st->flags, nwords,
-                      st->lb, cnts, (int64_t)out.capacity, out.pid, grand, st->host_st_dev)) != cudaSuccess)
+                      st->lb, cnts, (int64_t)out.capacity, out.pid, grand, st->host_st_dev,
+                      out.dev_status)) != cudaSuccess)
     return e;
   count_launches(1);
   if (hcp && (e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;   // colour
@@ -1975,7 +1994,13 @@ cudaError_t emit_outputs(const GridIn& in, const Cam& cam, DedupTable* st, const
                       (const int32_t*)grand, (int64_t)out.capacity, ea)) != cudaSuccess)
     return e;
   count_launches(1);
-  return cudaStreamSynchronize(s);
+  return sync ? cudaStreamSynchronize(s) : cudaGetLastError();
+}
+
+cudaError_t launch_prefix_mask(const int64_t* n_dev, int64_t cap, uint8_t* mask, cudaStream_t s) {
+  cudaError_t e = launch_pdl(prefix_mask_kernel, dim3(grid_blocks(cap, 256, 148)), dim3(256), 0, s, n_dev, cap, mask);
+  count_launches(1);
+  return e;
 }
 
 cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, size_t ws_bytes, int sms,
@@ -2000,7 +2025,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   std::lock_guard<std::mutex> st_lock(g_dedup_mu);
   ProfScope prof_batch("grid_batch", s);   // device span of the whole call (first launch .. status sync)
   DedupTable* st = nullptr;
-  if ((e = grid_state(npix, s, &st)) != cudaSuccess) return e;
+  if ((e = grid_state(npix, s, &st, !in.async)) != cudaSuccess) return e;
   int* bbox = reinterpret_cast<int*>(st->misc);
   unsigned long long* cnts = reinterpret_cast<unsigned long long*>(st->misc + 64);   // nvalid, nvox, items, -, -, ovf, tile
   int* overflow = reinterpret_cast<int*>(cnts + 5);
@@ -2053,11 +2078,14 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   // select path (mean mode always sorts: its per-voxel sums run in pixel
   // order over the voxel's segment)
   const bool hashed = compact && !sort_forced();
+  if (in.async && !hashed) return cudaErrorNotSupported;
   st->dirty = true;
   if (hashed) {
     // ---------------- G1+G2': front end inserting into the batch table, table scan + map test
-    if ((e = hashset_reserve(hs, npix, s)) != cudaSuccess) return e;   // room for a new key per pixel
-    if ((e = dedup_table(*st, npix / 16, false, s)) != cudaSuccess) return e;
+    if (!in.async) {   // async: the caller sized the map; the batch table exists (grid_state checked)
+      if ((e = hashset_reserve(hs, npix, s)) != cudaSuccess) return e;   // room for a new key per pixel
+      if ((e = dedup_table(*st, npix / 16, false, s)) != cudaSuccess) return e;
+    }
     out.sort_passes = 0;
     const CamF cf{(float)in.cx, (float)in.cy, (float)(1.0 / in.fx), (float)(1.0 / in.fy), (float)(1.0 / in.voxel)};
     if (front_ok && (e = front_init()) != cudaSuccess) return e;
@@ -2101,13 +2129,21 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
           return e;
         count_launches(1);
       }
-      if ((e = emit_outputs(in, cam, st, head, k0, v0, 0, out, sms, s, host_frames ? hcp : nullptr)) != cudaSuccess)
+      if ((e = emit_outputs(in, cam, st, head, k0, v0, 0, out, sms, s, host_frames ? hcp : nullptr, !in.async)) !=
+          cudaSuccess)
         return e;
+      if (in.async) {   // counts on the device (out.dev_status); the map bound grows by the pixel count
+        out.n_new = out.n_valid = out.n_voxels = out.n_sorted = -1;
+        hs->count_ub += npix;
+        st->dirty = false;
+        return cudaGetLastError();
+      }
       const unsigned long long* hst = st->host_st;
       out.n_valid = (int64_t)hst[0];
       out.n_voxels = (int64_t)hst[1];
       out.n_sorted = (int64_t)hst[2];
       out.n_new = (int64_t)hst[3];
+      if (hst[4] & 2) return cudaErrorUnknown;   // the map set is full (reserve keeps load <= 1/2: not reached)
       if (!hst[4]) break;
       // the table was too small for this batch's distinct voxels: the scan did
       // not run (map untouched, nothing flagged or emitted); reset the partly

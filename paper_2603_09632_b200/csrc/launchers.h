@@ -159,6 +159,7 @@ struct GridIn {
   double min_scale;
   const float* feat;
   int64_t fc, fh, fw;
+  bool async = false;       // XGS_GRID_ASYNC: no host sync / allocation (graph-capturable)
 };
 struct GridOut {
   int64_t capacity;
@@ -171,9 +172,11 @@ struct GridOut {
   void* feat;               // [cap, C], fp32 (feat64 == 0, first-pick only) or fp64
   int feat64;
   double* count;
+  int64_t* dev_status = nullptr;   // device {n_new, n_valid, n_voxels, error}
   int64_t n_new, n_valid, n_voxels;
   int64_t n_sorted, sort_passes;
 };
+cudaError_t launch_prefix_mask(const int64_t* n_dev, int64_t cap, uint8_t* mask, cudaStream_t s);
 cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, size_t ws_bytes, int sms,
                         cudaStream_t s);
 cudaError_t radix_sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n, int bits, void* ws, size_t ws_bytes,

@@ -1,0 +1,226 @@
+"""Per-frame Perceiver step as ONE CUDA graph (BASELINE configs[3], C4).
+
+The reference's per-keyframe path is: new Gaussians from the RGB-D frame
+(``slam.densify_and_prune``'s insertion, slam.py:601-651, here the voxel
+sampler of grid.py) whose semantic features then feed ``vq.online_step``
+(vq.py:193-212).  At ~2K new points per 640x480 frame the work is a few
+microseconds of kernels, so the per-frame latency is set by launches and
+host round trips.  ``PerceiverStream`` therefore captures the device part
+once and replays it per frame over fixed-capacity buffers:
+
+  graph:  grid sampling (xgs_grid_sample, XGS_GRID_ASYNC: no host sync) of the
+          staged frame -> new voxels in pixel order + their features gathered
+          from the frame's feature map (supervision.py:133-147 rule)
+          -> valid-row mask of the first n_new rows (xgs_prefix_mask; n_new
+          lives on the device) -> assign (tcgen05 screen + exact re-rank) of a
+          fixed `vq_capacity`-row window of the feature buffer -> masked
+          accumulate (counting sort + sequential fp64 chains; rows past n_new
+          contribute nothing, so the statistics equal the reference's on the
+          n_new rows) -> EMA in place.
+  host:   ONE device->host read of {N (K fp64), n_new, n_valid, n_voxels,
+          error} -> reservoir ring write of the n_new rows (vq.py:203) ->
+          the reference's host RNG draws for dead codes -> revival kernel.
+
+The codebook before the step is kept inside the graph (two device copies),
+so a frame with more than `vq_capacity` new points -- rare at C4, its VQ
+would have seen only the window -- is rolled back and redone through the
+synchronous ``online_step`` on exactly its n_new rows.  Results are
+bit-identical to ``GridSampler.sample(...)`` followed by ``online_step`` on
+the returned features (tests/test_stream_gpu.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .core import Codebook, FeatureReservoir
+from .errors import InvalidInputError
+from .grid import GridSampler, VoxelHashSet, _grid_ws_bytes, _intr4
+
+
+@dataclass
+class StreamStepResult:
+    n_new: int            # new Gaussians (voxels) of the frame
+    n_valid: int          # valid depth pixels
+    n_voxels: int         # distinct voxels of the frame (new or already mapped)
+    revived: list         # dead codes revived this step (vq.py:173-190)
+    graph: bool           # served by the graph replay (False: synchronous fallback)
+
+
+class PerceiverStream:
+    """Grid sampling -> online VQ per frame, device part replayed as a CUDA graph."""
+
+    def __init__(self, intrinsics, height: int, width: int, voxel_size: float, codebook: Codebook, cfg,
+                 feat_shape, rng: np.random.Generator, map_capacity: int = 1 << 23, vq_capacity: int = 16384,
+                 min_scale: float = 1e-3):
+        t = nat.require_cuda()
+        if not codebook.on_device:
+            codebook = codebook.to_device()
+        C, Hf, Wf = (int(v) for v in feat_shape)
+        if C != codebook.D:
+            raise InvalidInputError(f"feature channels {C} != codebook D={codebook.D}")
+        self.t, self.cfg, self.rng = t, cfg, rng
+        self.H, self.W, self.C = int(height), int(width), C
+        self.K, self.D = codebook.K, codebook.D
+        self.lam, self.eps = float(codebook.lam), float(codebook.epsilon)
+        self.intr = _intr4(intrinsics)
+        self.voxel = float(voxel_size)
+        self.min_scale = float(min_scale)
+        dev = "cuda"
+        # codebook state: updated in place by the graph (EMA) and the revival
+        self.E = codebook.E.clone().contiguous()
+        self.N = codebook.N.clone().contiguous()
+        self.M = codebook.M.clone().contiguous()
+        self.E0, self.N0, self.M0 = t.empty_like(self.E), t.empty_like(self.N), t.empty_like(self.M)
+        self.reservoir = codebook.reservoir if codebook.reservoir is not None else FeatureReservoir(
+            cfg.reservoir_capacity, self.D)
+        # staged frame (the graph reads these addresses)
+        self.depth = t.zeros((1, self.H, self.W), dtype=t.float32, device=dev)
+        self.color = t.zeros((1, self.H, self.W, 3), dtype=t.uint8, device=dev)
+        self.R = t.zeros((1, 9), dtype=t.float64, device=dev)
+        self.T = t.zeros((1, 3), dtype=t.float64, device=dev)
+        self.feat = t.zeros((1, C, Hf, Wf), dtype=t.float32, device=dev)
+        # fixed-capacity outputs (every pixel could be a new voxel)
+        self.cap = self.H * self.W
+        self.flat = t.zeros(11 * self.cap, dtype=t.float64, device=dev)
+        self.ofeat = t.zeros((self.cap, C), dtype=t.float32, device=dev)
+        self.vcap = min(int(vq_capacity), self.cap)
+        self.mask = t.zeros(self.vcap, dtype=t.uint8, device=dev)
+        self.codes = t.zeros(self.vcap, dtype=t.int64, device=dev)
+        self.packed = t.zeros(self.K * self.D + self.K, dtype=t.float64, device=dev)
+        self.dev_status = t.zeros(4, dtype=t.int64, device=dev)
+        self.host_N = t.empty(self.K, dtype=t.float64, pin_memory=True)
+        self.host_status = t.empty(4, dtype=t.int64, pin_memory=True)
+        self.occupied = VoxelHashSet(map_capacity)
+        self.sampler = GridSampler(intrinsics, voxel_size, occupied=self.occupied, min_scale=min_scale)
+        self.ws_grid = nat.workspace("stream_grid", _grid_ws_bytes(self.cap))
+        L = nat.lib()
+        self.ws_assign = nat.workspace("stream_assign", L.xgs_vq_assign_workspace(self.vcap, self.K, C, nat.F32, C))
+        self.ws_acc = nat.workspace("stream_acc", L.xgs_vq_accumulate_workspace(self.vcap, self.K))
+        fx, fy, cx, cy = self.intr
+        self._frames = nat.GridFrames(1, self.H, self.W, self.depth.data_ptr(), self.color.data_ptr(),
+                                      self.R.data_ptr(), self.T.data_ptr(), fx, fy, cx, cy, self.voxel, 1, 0,
+                                      self.min_scale, self.feat.data_ptr(), C, Hf, Wf, nat.GRID_ASYNC)
+        b, c = self.flat.data_ptr(), self.cap
+        self._result = nat.GridResult(c, b, b + 8 * c, b + 16 * c, b + 40 * c, b + 64 * c, b + 72 * c,
+                                      self.ofeat.data_ptr(), b + 80 * c, 0, 0, 0, 0, 0, nat.F32,
+                                      self.dev_status.data_ptr())
+        # rows past n_new in the assign window hold stale finite features; start
+        # them as a real codeword (a unique nearest code: no re-rank work)
+        self.ofeat[:self.vcap].copy_(self.E[0].to(t.float32).expand(self.vcap, C))
+        self.graph = None
+        self.frames = 0
+
+    # ------------------------------------------------------------ device part
+    def _enqueue(self):
+        """The graph body (all on the current stream, no host sync)."""
+        t, L, sp = self.t, nat.lib(), nat.stream_ptr()
+        self.E0.copy_(self.E)
+        self.N0.copy_(self.N)
+        self.M0.copy_(self.M)
+        nat.check(L.xgs_grid_sample(ctypes.byref(self._frames), self.occupied._h, ctypes.byref(self._result),
+                                    nat.ptr(self.ws_grid), self.ws_grid.numel(), sp))
+        nat.check(L.xgs_prefix_mask(nat.ptr(self.dev_status), self.vcap, nat.ptr(self.mask), sp))
+        nat.check(L.xgs_vq_assign(nat.ptr(self.ofeat), nat.F32, self.vcap, self.C, self.C, nat.ptr(self.E), self.K,
+                                  nat.ptr(self.codes), nat.ptr(self.ws_assign), self.ws_assign.numel(), None, sp))
+        sums = self.packed[:self.K * self.D]
+        counts = self.packed[self.K * self.D:]
+        nat.check(L.xgs_vq_accumulate(nat.ptr(self.ofeat), nat.F32, self.vcap, self.C, self.C, nat.ptr(self.codes),
+                                      nat.ptr(self.mask), self.K, nat.ptr(counts), nat.ptr(sums),
+                                      nat.ptr(self.ws_acc), self.ws_acc.numel(), sp))
+        nat.check(L.xgs_vq_ema(self.lam, self.eps, self.K, self.D, nat.ptr(self.N), nat.ptr(self.M),
+                               nat.ptr(counts), nat.ptr(sums), nat.ptr(self.N), nat.ptr(self.M), nat.ptr(self.E),
+                               sp))
+        self.host_N.copy_(self.N, non_blocking=True)
+        self.host_status.copy_(self.dev_status, non_blocking=True)
+
+    def _capture(self):
+        t = self.t
+        g = t.cuda.CUDAGraph()
+        s = t.cuda.Stream()
+        s.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(s):
+            with t.cuda.graph(g, stream=s):
+                self._enqueue()
+        t.cuda.current_stream().wait_stream(s)
+        self.graph = g
+
+    # ------------------------------------------------------------ per frame
+    def _stage(self, depth, R, T, color, feats):
+        t = self.t
+        self.depth.view(self.H, self.W).copy_(depth.reshape(self.H, self.W), non_blocking=True)
+        self.color.view(-1).copy_(color.reshape(-1), non_blocking=True)
+        self.R.view(-1).copy_(R.reshape(-1), non_blocking=True)
+        self.T.view(-1).copy_(T.reshape(-1), non_blocking=True)
+        self.feat.view(-1).copy_(feats.reshape(-1), non_blocking=True)
+
+    def _sync_frame(self):
+        """Synchronous path on the staged frame (first frame: sizes the library
+        state the async call needs)."""
+        from .vq import online_step
+        r = self.sampler.sample(self.depth, (self.R, self.T), self.color, features=self.feat)
+        cb = Codebook._make(self.E, self.N, self.M, self.lam, self.eps, self.reservoir)
+        if len(r):
+            cb, res = online_step(cb, r.feature, self.cfg, self.rng)
+            self.E.copy_(cb.E)
+            self.N.copy_(cb.N)
+            self.M.copy_(cb.M)
+            revived = res.revived
+        else:
+            revived = []
+        self.t.cuda.current_stream().synchronize()
+        return StreamStepResult(len(r), r.n_valid, r.n_voxels, revived, False)
+
+    def step(self, depth, pose, color, feats) -> StreamStepResult:
+        """One frame: depth (H, W) fp32, pose (R (3, 3), t (3,)) fp64, colour
+        (H, W, 3) uint8, features (C, Hf, Wf) fp32 -- CUDA tensors."""
+        from .vq import _revive_dev, online_step
+        R, T = pose
+        self._stage(depth, R, T, color, feats)
+        self.frames += 1
+        if self.graph is None:
+            out = self._sync_frame()
+            self._capture()
+            return out
+        self.graph.replay()
+        self.t.cuda.current_stream().synchronize()
+        st = self.host_status.numpy()
+        n_new, n_valid, n_vox, err = (int(v) for v in st)
+        if err:
+            raise RuntimeError(f"grid batch overflow (code {err}): the map set or batch table is full")
+        if n_new == 0:          # no new points: the stream makes no VQ step (online_step needs a nonempty batch)
+            self.E.copy_(self.E0)
+            self.N.copy_(self.N0)
+            self.M.copy_(self.M0)
+            return StreamStepResult(0, n_valid, n_vox, [], True)
+        if n_new > self.vcap:   # the window missed rows: roll the codebook back, redo the VQ on all n_new rows
+            self.E.copy_(self.E0)
+            self.N.copy_(self.N0)
+            self.M.copy_(self.M0)
+            cb = Codebook._make(self.E, self.N, self.M, self.lam, self.eps, self.reservoir)
+            cb, res = online_step(cb, self.ofeat[:n_new], self.cfg, self.rng)
+            self.E.copy_(cb.E)
+            self.N.copy_(cb.N)
+            self.M.copy_(cb.M)
+            self.t.cuda.current_stream().synchronize()
+            return StreamStepResult(n_new, n_valid, n_vox, res.revived, False)
+        revived = []
+        if n_new:
+            # reservoir ring write of the batch (vq.py:203), then the host RNG revival
+            self.reservoir._extend_rows(self.ofeat, nat.F32, n_new, self.C)
+            cb = Codebook._make(self.E, self.N, self.M, self.lam, self.eps, self.reservoir)
+            revived, _ = _revive_dev(cb, self.E, self.N, self.M, self.cfg.delta_dead, self.rng,
+                                     N_host=self.host_N.numpy())
+        return StreamStepResult(n_new, n_valid, n_vox, revived, True)
+
+    def codebook(self) -> Codebook:
+        return Codebook._make(self.E, self.N, self.M, self.lam, self.eps, self.reservoir)
+
+    def new_voxels(self, n):
+        """The last frame's first n new voxels (key, pid, mu, colour, scale, depth, count, feature)."""
+        from .grid import GridSampleResult
+        return GridSampleResult(self.flat, self.cap, int(n), self.ofeat, -1, -1)

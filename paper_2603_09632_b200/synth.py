@@ -67,6 +67,17 @@ def random_planes(rng, n, centre=np.zeros(3), spread=3.0):
     return planes
 
 
+def facing_planes(rng, n, dmin=3.0, dmax=7.0, tilt=0.3):
+    """n walls roughly facing a camera at the origin looking down +z (normal
+    ~ +z tilted by N(0, tilt) per axis) at distances U(dmin, dmax)."""
+    planes = []
+    for _ in range(n):
+        nrm = np.array([rng.normal(0, tilt), rng.normal(0, tilt), 1.0])
+        nrm /= np.linalg.norm(nrm)
+        planes.append((nrm, float(rng.uniform(dmin, dmax))))
+    return planes
+
+
 def render_depth(pose, intr4, H, W, planes=(), spheres=(), dmin=0.3, dmax=8.0):
     """Camera-z depth of the first surface hit; 0 where nothing is hit in range."""
     fx, fy, cx, cy = intr4
