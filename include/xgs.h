@@ -68,7 +68,9 @@ XGS_API int xgs_vq_assign(const void* x, int dtype, int64_t n, int64_t d, int64_
 /* Exact fp64 path, one CTA per row:
  *   XGS_EX_DIST  squared_distances (vq.py:69-73) -> out_dist (n, k)
  *   XGS_EX_CODE  argmin -> codes (n)
- *   XGS_EX_MASK  confidence_mask (vq.py:121-124) -> mask (n) u8
+ *   XGS_EX_MASK  confidence_mask (vq.py:121-124) -> mask (n) u8: 1 pass, 0 reject, 2 undecided (fl(1/S)
+ *                within 1e-12 relative of gamma: CUDA exp and the host libm may differ by an ulp;
+ *                the caller decides these rows with the reference's host expression)
  *   XGS_EX_PROB  confidence_scores (vq.py:112-118) -> out_prob (n, k) */
 XGS_API int xgs_vq_exact(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E, int64_t k,
                          int mode, double tau, double gamma, double* out_dist, double* out_prob, int64_t* codes,

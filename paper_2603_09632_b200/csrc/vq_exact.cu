@@ -69,7 +69,14 @@ exact_rows_kernel(ExactArgs a, SumPlan pd, SumPlan pk) {
             [&](int i) { return exp(dsub(ddiv(-__dsqrt_rn(dist[i]), a.tau), lmax)); },
             scratch, lane);
         if (lane == 0) {
-          if (a.mode & EX_CONF_MASK) a.mask[row] = ddiv(1.0, S) >= a.gamma;
+          if (a.mode & EX_CONF_MASK) {
+            // p.max = fl(1/S) (vq.py:118-124).  CUDA's exp and the host
+            // libm's may differ in the last ulp, moving S by up to ~K ulps:
+            // rows whose 1/S lies within 1e-12 relative of gamma are marked 2
+            // and decided on the host with the reference's own NumPy ops.
+            const double inv = ddiv(1.0, S);
+            a.mask[row] = fabs(inv - a.gamma) <= 1e-12 * a.gamma ? 2 : (inv >= a.gamma ? 1 : 0);
+          }
           red_v[1] = S;
         }
       }

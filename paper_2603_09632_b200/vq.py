@@ -149,7 +149,31 @@ def _exact_dev(xt, dt, n, d, ldx, E, K, mode, tau=1.0, gamma=0.5):
     if n:
         nat.call("xgs_vq_exact", nat.ptr(xt), dt, n, d, ldx, nat.ptr(E), K, mode, float(tau), float(gamma),
                  nat.ptr(dist), nat.ptr(prob), nat.ptr(codes), nat.ptr(mask), nat.stream_ptr())
+        if mask is not None:
+            _decide_borderline(xt, dt, n, d, ldx, E, K, mask, tau, gamma)
     return dist, prob, codes, mask
+
+
+def _decide_borderline(xt, dt, n, d, ldx, E, K, mask, tau, gamma):
+    """Rows the kernel marked 2 (fl(1/S) within 1e-12 relative of gamma,
+    where a last-ulp difference between CUDA's exp and the host libm's could
+    flip the decision) are decided with the reference's own NumPy expression
+    (vq.py:112-124) on their exact fp64 distances (bit-identical to
+    squared_distances)."""
+    t = nat.torch()
+    idx = (mask == 2).nonzero().reshape(-1)
+    if idx.numel() == 0:
+        return
+    sub = xt[:n].index_select(0, idx).contiguous()
+    dist, _, _, _ = _exact_dev(sub, dt, int(idx.numel()), d, d, E, K, nat.EX_DIST)
+    sq = dist.cpu().numpy()
+    dd = np.sqrt(sq)
+    logits = -dd / tau
+    logits -= logits.max(axis=1, keepdims=True)
+    e = np.exp(logits)
+    p = e / e.sum(axis=1, keepdims=True)
+    ok = p.max(axis=1) >= gamma
+    mask[idx] = t.from_numpy(ok.astype(np.uint8)).to(mask.device)
 
 
 def _accumulate_dev(xt, dt, n, d, ldx, codes, mask, K):

@@ -423,3 +423,23 @@ def test_pinned_host_batch_streams_bit_identical(xv):
         runs.append([s.cpu().numpy() for s in vq.state] + [vq.ring.cpu().numpy()])
     for a, b in zip(*runs):
         assert np.array_equal(a, b)
+
+
+def test_confidence_mask_rows_at_gamma(xv):
+    """Rows whose max softmax lies at / within an ulp of gamma (SURVEY §7 hard
+    part 5): the kernel marks them undecided and they are decided with the
+    reference's own NumPy expression -- the mask equals the reference's."""
+    rng = np.random.default_rng(17)
+    E = rng.normal(size=(40, 24))
+    x = rng.normal(size=(300, 24))
+    x[0] = 0.5 * (E[3] + E[7])          # exactly equidistant from two codes
+    cb = make_cb(xv, E)
+    sq = ((x[:, None, :] - E[None, :, :]) ** 2).sum(axis=2)
+    lg = -np.sqrt(sq) / 0.7
+    lg -= lg.max(axis=1, keepdims=True)
+    e = np.exp(lg)
+    pmax = (e / e.sum(axis=1, keepdims=True)).max(axis=1)
+    for gamma in (pmax[0], pmax[5], np.nextafter(pmax[5], 1.0), np.nextafter(pmax[9], 0.0), 0.3):
+        cfg = xv.VqConfig(K=40, tau_warm=0.7, gamma=float(gamma))
+        got = xv.confidence_mask(x, cb, cfg)
+        assert np.array_equal(got, pmax >= gamma), gamma
