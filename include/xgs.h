@@ -224,6 +224,14 @@ XGS_API size_t xgs_grid_workspace(int64_t npix);
 XGS_API int xgs_radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, int bits, void* ws,
                                      size_t ws_bytes, void* stream);
 
+/* slam.pose_depths (slam.py:654-655): z (n) = camera depth of the Gaussian
+ * centres mu (n, 3) fp64 under the world->camera pose R9 / t3 (HOST arrays),
+ * in the reference's BLAS evaluation order.  With key / idx non-NULL also the
+ * ascending IEEE order keys of z and the identity indices, ready for
+ * xgs_radix_sort_pairs_u64 (the median fallback depth of densify_and_prune). */
+XGS_API int xgs_pose_depths(const double* mu, int64_t n, const double* R9, const double* t3, double* z,
+                            uint64_t* key, uint32_t* idx, void* stream);
+
 /* Voxel grid sampling of a batch of frames (the insertion half of
  * densify_and_prune, slam.py:601-651, with the coverage render replaced by
  * the occupied-voxel hash set; SURVEY.md 8(a) g8 definitions):

@@ -62,6 +62,7 @@ SIGNATURES = {
     "xgs_grid_sample": (_i32, [_vp, _vp, _vp, _vp, _sz, _vp]),
     "xgs_grid_sample_h2d": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "xgs_prefix_mask": (_i32, [_vp, _i64, _vp, _vp]),
+    "xgs_pose_depths": (_i32, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "xgs_sup_gather": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _i64,
                               _i64, _vp, _vp, _vp, _vp]),
     "xgs_sup_loss": (_i32, [_vp, _vp, _vp, _i64, _i64, _f64, _vp, _vp, _vp]),

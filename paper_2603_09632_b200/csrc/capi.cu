@@ -368,6 +368,17 @@ int xgs_backproject(const double* R, const double* t, const double* intr4, const
   return OK;
 }
 
+int xgs_pose_depths(const double* mu, int64_t n, const double* R9, const double* t3, double* z, uint64_t* key,
+                    uint32_t* idx, void* stream) {
+  if (n < 0 || !R9 || !t3) return fail(INVALID_INPUT, "bad pose_depths arguments");
+  if (n > 0 && (!mu || !z)) return fail(INVALID_INPUT, "null buffer");
+  if (key && !idx) return fail(INVALID_INPUT, "order keys need the index buffer");
+  if (key && n > 0xffffffffll) return fail(NOT_SUPPORTED, "more than 2^32 points");
+  cudaError_t e = launch_pose_depths(mu, n, R9, t3, z, key, idx, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_pose_depths");
+  return OK;
+}
+
 int xgs_hashset_create(int64_t capacity, void** handle) {
   if (!handle || capacity < 0) return fail(INVALID_INPUT, "bad hashset arguments");
   HashSet* h = nullptr;

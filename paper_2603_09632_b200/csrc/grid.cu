@@ -1405,6 +1405,26 @@ __global__ void backproject_kernel(const double* R, const double* t, Cam cam, co
     backproject(R, t, cam, u[i], v[i], d[i], out + 3 * i);
 }
 
+// slam.py:654-655 pose_depths: camera z of every centre, pose.transform(mu)[:, 2]
+// = (mu @ R.T + t)[:, 2]; the BLAS evaluation is fma(m2,R22, fma(m1,R21, m0*R20))
+// + t2 (pinned against the reference on 200,000 points, tests/test_grid_gpu.py).
+// `key` (nullable): the ascending order key of z (IEEE total order as uint64)
+// for the in-house radix sort -> median.
+__global__ void pose_depths_kernel(const double* __restrict__ mu, int64_t n, double R20, double R21, double R22,
+                                   double t2, double* __restrict__ z, uint64_t* __restrict__ key,
+                                   uint32_t* __restrict__ idx) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double* m = mu + 3 * i;
+    const double v = dadd(__fma_rn(m[2], R22, __fma_rn(m[1], R21, dmul(m[0], R20))), t2);
+    z[i] = v;
+    if (key) {
+      const uint64_t b = (uint64_t)__double_as_longlong(v);
+      key[i] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+      idx[i] = (uint32_t)i;
+    }
+  }
+}
+
 unsigned grid_blocks(int64_t n, int threads, int sms) {
   int64_t b = (n + threads - 1) / threads;
   const int64_t cap = (int64_t)sms * 16;
@@ -1495,6 +1515,14 @@ cudaError_t hashset_insert(HashSet* h, const uint64_t* keys, int64_t n, uint8_t*
 cudaError_t hashset_contains(HashSet* h, const uint64_t* keys, int64_t n, uint8_t* out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   hs_contains_kernel<<<grid_blocks(n, 256, 148), 256, 0, s>>>(h->table, (uint64_t)h->cap - 1, keys, n, out); count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pose_depths(const double* mu, int64_t n, const double* R9, const double* t3, double* z,
+                               uint64_t* key, uint32_t* idx, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  pose_depths_kernel<<<grid_blocks(n, 256, 148), 256, 0, s>>>(mu, n, R9[6], R9[7], R9[8], t3[2], z, key, idx);
+  count_launches(1);
   return cudaGetLastError();
 }
 

@@ -177,6 +177,8 @@ struct GridOut {
   int64_t n_sorted, sort_passes;
 };
 cudaError_t launch_prefix_mask(const int64_t* n_dev, int64_t cap, uint8_t* mask, cudaStream_t s);
+cudaError_t launch_pose_depths(const double* mu, int64_t n, const double* R9, const double* t3, double* z,
+                               uint64_t* key, uint32_t* idx, cudaStream_t s);
 cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, size_t ws_bytes, int sms,
                         cudaStream_t s);
 cudaError_t radix_sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n, int bits, void* ws, size_t ws_bytes,

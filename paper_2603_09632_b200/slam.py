@@ -110,9 +110,41 @@ def backproject(pose: CameraPose, intr: CameraIntrinsics, u: float, v: float, de
     return backproject_pixels(pose, intr, [u], [v], [depth])[0]
 
 
-def pose_depths(field_: GaussianField, pose: CameraPose) -> np.ndarray:
-    """slam.py:654-655 — camera z of every Gaussian centre."""
-    return pose.transform(field_.mu)[:, 2]
+def _pose_depths_dev(mu, pose, with_keys=False):
+    t = nat.require_cuda()
+    M = mu if hasattr(mu, "data_ptr") else t.from_numpy(np.ascontiguousarray(np.asarray(mu, dtype=np.float64)))
+    M = M.to(device="cuda", dtype=t.float64).reshape(-1, 3).contiguous()
+    n = int(M.shape[0])
+    z = t.empty(n, dtype=t.float64, device="cuda")
+    key = t.empty(n, dtype=t.int64, device="cuda") if with_keys else None
+    idx = t.empty(n, dtype=t.int32, device="cuda") if with_keys else None
+    R9 = (ctypes.c_double * 9)(*np.asarray(pose.rotation, dtype=np.float64).reshape(-1))
+    t3 = (ctypes.c_double * 3)(*np.asarray(pose.translation, dtype=np.float64).reshape(-1))
+    nat.call("xgs_pose_depths", nat.ptr(M), n, R9, t3, nat.ptr(z), nat.ptr(key), nat.ptr(idx), nat.stream_ptr())
+    return z, key, idx
+
+
+def pose_depths(field_: GaussianField, pose: CameraPose):
+    """slam.py:654-655 — camera z of every Gaussian centre (device kernel, the
+    reference's BLAS evaluation order; NumPy in -> NumPy out)."""
+    mu = field_.mu
+    z, _, _ = _pose_depths_dev(mu, pose)
+    return z if hasattr(mu, "data_ptr") else z.cpu().numpy()
+
+
+def median_pose_depth(field_: GaussianField, pose: CameraPose) -> float:
+    """np.median(pose_depths(field_, pose)) (slam.py:611-613) on the device: the
+    IEEE order keys of z through the in-house radix sort, then the middle
+    element (odd n) or fl(fl(a + b) / 2) of the two middle ones (even n), as
+    np.median computes it."""
+    from .grid import radix_sort_pairs
+    t = nat.torch()
+    z, key, idx = _pose_depths_dev(field_.mu, pose, with_keys=True)
+    n = int(z.numel())
+    radix_sort_pairs(key, idx, 64)
+    mid = idx[(n - 1) // 2:n // 2 + 1].to(t.int64)
+    v = z[mid].cpu().numpy()
+    return float(v[0]) if n % 2 else float((v[0] + v[1]) / 2)
 
 
 def densify_and_prune(field_: GaussianField, window, cfg: SlamConfig, K: Optional[int] = None, *,
@@ -134,11 +166,7 @@ def densify_and_prune(field_: GaussianField, window, cfg: SlamConfig, K: Optiona
     intr = frame_intrinsics(kf.frame, cfg)
     K = field_.K if K is None else K
     s = cfg.insert_stride
-    if len(field_):
-        cam_depth = pose_depths(field_, kf.pose)
-        median_depth = float(np.median(cam_depth)) if cam_depth.size else cfg.default_depth
-    else:
-        median_depth = cfg.default_depth
+    median_depth = median_pose_depth(field_, kf.pose) if len(field_) else cfg.default_depth
     uu, vv = np.meshgrid(np.arange(0, intr.height, s), np.arange(0, intr.width, s), indexing="ij")
     uu, vv = uu.reshape(-1), vv.reshape(-1)
     if kf.frame.depth is not None:

@@ -388,3 +388,24 @@ def test_grid_features_device_tensors_and_shape_errors(xs, cuda):
     one = grid.GridSampler(intr4, 0.03).sample(D[0], (R[:1], T[:1]), features=feats[0]).to_numpy()
     ref1 = og.grid_sample([frames[0]], np.array(intr4), 0.03, set(), features=[feats[0]])
     assert np.array_equal(one["feature"].astype(np.float64), ref1["feature"])
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 100_000, 100_001])
+def test_pose_depths_and_median_on_device(xs, n):
+    """slam.pose_depths (slam.py:654-655) in the reference's BLAS evaluation
+    order (bit-identical to pose.transform(mu)[:, 2]) and np.median of it
+    (the densify fallback depth) through the device radix sort."""
+    _, slam, _ = xs
+    from paper_2603_09632_b200.core import CameraPose, GaussianField
+    rng = np.random.default_rng(n)
+    Q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+    if np.linalg.det(Q) < 0:
+        Q[:, 0] *= -1
+    pose = CameraPose(Q, rng.normal(size=3) * 3)
+    mu = rng.normal(size=(n, 3)) * 4
+    mu[::13] = mu[0]                        # duplicate depths
+    field = GaussianField(mu=mu, quat=np.tile([1.0, 0, 0, 0], (n, 1)), scale=np.full((n, 3), 0.01),
+                          opacity=np.full(n, 0.5), color=np.zeros((n, 3)), logits=np.zeros((n, 2)))
+    ref = pose.transform(mu)[:, 2]
+    assert np.array_equal(slam.pose_depths(field, pose), ref)
+    assert slam.median_pose_depth(field, pose) == float(np.median(ref))
