@@ -158,6 +158,7 @@ def make_data(torch, rank, device):
     return x, E0
 
 
+FP64_DMMA_TFLOPS = 37.1   # tools/micro/fp64_peak.cu on the B200 pool (profiles/r2_fp64_peak_microbench.txt)
 GRID_F, GRID_H, GRID_W = 16, 720, 1280
 GRID_INTR = (1050.0, 1050.0, 359.5, 639.5)   # BASELINE leaves C3 intrinsics open
 GRID_MAP = 4_000_000
@@ -335,6 +336,65 @@ def run_grid(torch, steps, cpu=True):
 
 STREAM_H, STREAM_W, STREAM_D, STREAM_K = 480, 640, 768, 512
 STREAM_INTR = (525.0, 525.0, 239.5, 319.5)
+
+
+def run_c1(torch, reps=20, cpu=True):
+    """C1 (BASELINE configs[0], the reference's CPU-runnable case): one 640x480
+    frame (6 planes 0.5-5 m, sigma 5 mm, 5% zeros, fx=fy=525, identity pose),
+    grid sampling at 0.02 m into an empty map, one 512-dim unit-norm feature
+    per new point (64-centre mixture, sigma 0.1), K=256 codebook from random
+    rows of them, one online_step (lam 0.99).  Latency = host wall clock of
+    GridSampler.sample + online_step on device-resident inputs (median of
+    `reps`; fresh map each time), and the same through the CPU port."""
+    from paper_2603_09632_b200 import synth
+    from paper_2603_09632_b200.grid import GridSampler, VoxelHashSet
+    import paper_2603_09632_b200 as xv
+    d, col, pose, intr4 = synth.config1_frame(0)
+    dd, cd = torch.from_numpy(d).cuda(), torch.from_numpy(col).cuda()
+    R = torch.from_numpy(pose.rotation[None].copy()).cuda()
+    T = torch.from_numpy(pose.translation[None].copy()).cuda()
+    probe = GridSampler(intr4, 0.02).sample(dd, (R, T), cd)
+    n = len(probe)
+    rng = np.random.default_rng(2)
+    x = synth.mixture_features(rng, n, 512, 64, 0.1)
+    E0 = x[np.random.default_rng(3).choice(n, 256, replace=False)].astype(np.float64)
+    xd = torch.from_numpy(x).cuda()
+    cfg = xv.VqConfig(K=256, lam=0.99, gamma=0.5 / 256, delta_dead=1e-3)
+    times = []
+    for _ in range(reps + 3):
+        hs = VoxelHashSet(1 << 20)
+        gs = GridSampler(intr4, 0.02, occupied=hs)
+        cb = xv.Codebook._make(torch.from_numpy(E0).cuda(), torch.zeros(256, dtype=torch.float64, device="cuda"),
+                               torch.zeros(256, 512, dtype=torch.float64, device="cuda"), 0.99, 1e-5,
+                               xv.FeatureReservoir(4096, 512))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = gs.sample(dd, (R, T), cd)
+        cb, _ = xv.online_step(cb, xd[:len(r)], cfg, np.random.default_rng(4))
+        torch.cuda.synchronize()
+        times.append((time.perf_counter() - t0) * 1e3)
+        hs.close()
+    ms = float(np.median(times[3:]))
+    out = {"ms_per_frame_step": ms, "new_gaussians": n, "pixels": d.size,
+           "workload": "C1: one 640x480 RGB-D frame (6 planes 0.5-5 m), grid 0.02 m, K=256 D=512 online_step on the "
+                       "new points' features; host wall clock of GridSampler.sample + online_step"}
+    if cpu:
+        from oracle import grid as og
+        from oracle import native as on
+        from oracle import vq as ov
+        t0 = time.perf_counter()
+        og.grid_sample([(d, col, pose.rotation, pose.translation)], np.array(intr4), 0.02, set())
+        oc = ov.OracleCodebook(E0, np.zeros(256), np.zeros((256, 512)), 0.99, 1e-5, ov.OracleReservoir(4096, 512))
+        oc.reservoir.extend(x)
+        codes = on.assign(x, oc.E, threads=1)
+        counts, sums = on.accumulate(x, codes, 256)
+        oc = ov.ema_step(oc, counts, sums)
+        ov.revive_dead_codes(oc, 1e-3, np.random.default_rng(4))
+        el = (time.perf_counter() - t0) * 1e3
+        out["cpu_baseline"] = {"ms_per_frame_step": el, "cores": 1, "kind": "port",
+                               "sample": "the whole C1 step: oracle/grid.py (C back-projection + NumPy voxel "
+                                         "dedup) + online_step with the C assign/accumulate (1 thread)"}
+    return out
 
 
 STREAM_FEAT_HW = (60, 80)     # VFM-resolution feature map (stride 8 on 480x640)
@@ -597,7 +657,12 @@ def run_consumers(torch, iters, cpu=True):
                                 "hbm_frac": ent_bytes / (ms_h * 1e-3) / 1e9 / pk["hbm_gbs"],
                                 "algorithmic_bytes": ent_bytes},
            "sample_tokens": {"ms": ms_tok, "M": M},
-           "relevance_per_gaussian": {"ms": ms_rel, "decode_gemm_fp64_TFLOPs": 2.0 * n * K * D / (ms_rel * 1e-3) / 1e12},
+           "relevance_per_gaussian": {
+               "ms": ms_rel, "fp64_TFLOPs": 2.0 * n * K * D / (ms_rel * 1e-3) / 1e12,
+               "fp64_frac": 2.0 * n * K * D / (ms_rel * 1e-3) / 1e12 / FP64_DMMA_TFLOPS,
+               "note": "softmax weights (xgs_softmax_rows) + xgs_gemm_f64 (DMMA.8x8x4 fp64, contrast fused in the "
+                       "epilogue, no (n, D) features); frac vs the measured DMMA peak "
+                       f"{FP64_DMMA_TFLOPS} TF/s (profiles/r2_fp64_peak_microbench.txt)"},
            "clocks": clocks,
            "workload": "2^21 Gaussians x K=512 fp64 logits (C4 map size), D=768 codebook, M=4096 tokens; "
                        "synthetic N(0, 2^2) logits"}
@@ -1020,12 +1085,14 @@ def main():
     del vq2, xh
     torch.cuda.empty_cache()
 
-    cpu = c2 = grid = stream = targets = consumers = raster = init = None
+    cpu = c1 = c2 = grid = stream = targets = consumers = raster = init = None
     if rank == 0 and world == 1:
         if not args.no_cpu:
             cpu = cpu_port_c5(args.cpu_seconds)
         if not args.no_c2:
             c2 = run_c2(torch, args, device)
+        if not args.no_grid:
+            c1 = run_c1(torch, cpu=not args.no_cpu)
         if not args.no_grid:
             grid = run_grid(torch, args.grid_steps, cpu=not args.no_cpu)
         if args.stream_frames > 0:
@@ -1052,6 +1119,7 @@ def main():
             "grid_c3_ms": g1.get("ms_per_batch"), "grid_front_hbm_frac": (g1.get("roofline") or {}).get("frac"),
             "grid_batch_hbm_frac": g1.get("batch_hbm_frac"),
             "stream_p50_ms": (stream or {}).get("p50_ms"), "stream_p99_ms": (stream or {}).get("p99_ms"),
+            "c1_ms": (c1 or {}).get("ms_per_frame_step"),
             "e2e": {"value": e2e_val, "unit": "Mfeat/s", "h2d_bytes_per_step": world * e2e_rows * C5_D * 2,
                     "d2h_bytes_per_step": C5_K * C5_D * 8, "ms_per_step": e2e_ms,
                     "rows_per_step": world * e2e_rows,
@@ -1063,6 +1131,7 @@ def main():
             "assign_exact_rows": {"rerank": n_rerank, "fallback": n_fallback},
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "c1": c1,
             "c2": c2,
             "grid": grid,
             "stream": stream,

@@ -304,6 +304,23 @@ XGS_API int xgs_grid_sample_h2d(const xgs_grid_frames* in, float* depth_dev, uin
  * graph-captured stream step feeds the grid's new voxels to the VQ this way). */
 XGS_API int xgs_prefix_mask(const int64_t* n_dev, int64_t cap, uint8_t* mask, void* stream);
 
+/* fp64 codeword contraction on the fp64 tensor pipe (DMMA), SURVEY 8(f) #3:
+ * C[n x m] = op(A)[n x kr] . B[kr x m], element (r, k) of A at A[r*lda_r +
+ * k*lda_k], of B at B[k*ldb_k + j*ldb_m].  softmax_rows: A holds logits and
+ * enters as softmax over each row (mixture_weights, core.py:473-480).
+ *   decode_feature (core.py:490-496): A = logits (n x K), B = E (K x D), C out.
+ *   relevance_per_gaussian (thinker.py:122-129): scores (n) = the contrast of
+ *     the decoded rows against Q = [positive; negatives] (nq x m) with tau /
+ *     eps, no (n x D) feature matrix (C may be NULL).
+ *   feature_gradients (rasterizer.py:309-335): A = fg (n x D), B = E^T.
+ * Workspace: xgs_gemm_f64_workspace(n, kr, m, nq or 0, softmax_rows).  Agrees with the
+ * reference's BLAS dgemm to ~1e-15 relative (different summation order). */
+XGS_API size_t xgs_gemm_f64_workspace(int64_t n, int64_t kr, int64_t m, int64_t nq, int softmax_rows);
+XGS_API int xgs_gemm_f64(const double* A, int64_t n, int64_t kr, int64_t lda_r, int64_t lda_k, int softmax_rows,
+                         const double* B, int64_t m, int64_t ldb_k, int64_t ldb_m, double* C, int64_t ldc,
+                         const double* Q, int64_t nq, double tau, double eps, double* scores, void* ws,
+                         size_t ws_bytes, void* stream);
+
 /* ------------------------------------------- SUPERVISION */
 
 /* Grid-sampled supervision targets for n_off lattice offsets in one launch

@@ -63,6 +63,9 @@ SIGNATURES = {
     "xgs_grid_sample_h2d": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "xgs_prefix_mask": (_i32, [_vp, _i64, _vp, _vp]),
     "xgs_pose_depths": (_i32, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "xgs_gemm_f64_workspace": (_sz, [_i64, _i64, _i64, _i64, _i32]),
+    "xgs_gemm_f64": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _f64,
+                            _f64, _vp, _vp, _sz, _vp]),
     "xgs_sup_gather": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _i64,
                               _i64, _vp, _vp, _vp, _vp]),
     "xgs_sup_loss": (_i32, [_vp, _vp, _vp, _i64, _i64, _f64, _vp, _vp, _vp]),

@@ -276,7 +276,8 @@ class GaussianField:
 # core.py:473-496 of the reference.  NumPy in -> NumPy out (one H2D/D2H copy per
 # call); CUDA tensors in -> CUDA tensors out.  The row ops run in libxgs
 # (xgs_softmax_rows: fp64, NumPy's max / exp / pairwise-sum order); the
-# codeword mixture softmax(logits) @ E is a plain fp64 GEMM (cuBLAS via torch).
+# codeword mixture softmax(logits) @ E is xgs_gemm_f64 (softmax fused into the
+# fp64 DMMA contraction).
 
 SOFTMAX_WEIGHTS, SOFTMAX_ENTROPY, SOFTMAX_VJP = 1, 2, 4
 
@@ -322,10 +323,40 @@ def softmax_vjp(logits, upstream):
     return _ret(_softmax_rows(L, SOFTMAX_VJP, U), host, squeeze)
 
 
+def gemm_f64(A, B, softmax=False, b_transposed=False, a_transposed=False, query=None, tau=1.0, eps=0.0,
+             want_c=True):
+    """xgs_gemm_f64 (fp64 DMMA contraction, csrc/decode_f64.cu) on CUDA fp64
+    tensors: C = op(A) . B where op(A) = softmax over A's rows when `softmax`;
+    A is (n, kr) (or (kr, n) read transposed), B is (kr, m) (or (m, kr) read
+    transposed).  With `query` (nq, m) also / instead returns the contrast
+    scores of thinker.py:110-129 per row (no C needed)."""
+    t = nat.torch()
+    n, kr = (A.shape[1], A.shape[0]) if a_transposed else (A.shape[0], A.shape[1])
+    m = B.shape[0] if b_transposed else B.shape[1]
+    if (B.shape[1] if b_transposed else B.shape[0]) != kr:
+        raise InvalidInputError("inner dimensions disagree")
+    lda_r, lda_k = (A.stride(1), A.stride(0)) if a_transposed else (A.stride(0), A.stride(1))
+    ldb_k, ldb_m = (B.stride(1), B.stride(0)) if b_transposed else (B.stride(0), B.stride(1))
+    C = t.empty((n, m), dtype=t.float64, device="cuda") if want_c else None
+    scores = t.empty(n, dtype=t.float64, device="cuda") if query is not None else None
+    nq = int(query.shape[0]) if query is not None else 0
+    if softmax and a_transposed:
+        A = A.t().contiguous()
+        lda_r, lda_k = A.stride(0), A.stride(1)
+    ws = nat.workspace("gemm_f64", nat.lib().xgs_gemm_f64_workspace(n, kr, m, nq, 1 if softmax else 0))
+    nat.call("xgs_gemm_f64", nat.ptr(A), n, kr, lda_r, lda_k, 1 if softmax else 0, nat.ptr(B), m, ldb_k, ldb_m,
+             nat.ptr(C), m, nat.ptr(query), nq, float(tau), float(eps), nat.ptr(scores), nat.ptr(ws), ws.numel(),
+             nat.stream_ptr())
+    return C if query is None else (C, scores)
+
+
 def decode_feature(logits, codebook: "Codebook"):
-    """core.py:490-496 — softmax-weighted codeword mixture, (K,) or (N, K) logits."""
+    """core.py:490-496 — softmax-weighted codeword mixture, (K,) or (N, K) logits:
+    softmax and contraction fused in one fp64 DMMA kernel (xgs_gemm_f64)."""
     t, L, host, squeeze = _logits_dev(logits)
     if L.shape[-1] != codebook.K:
         raise InvalidInputError(f"logit length {L.shape[-1]} does not match codebook K={codebook.K}")
+    if not bool(t.isfinite(L).all()):
+        raise InvalidInputError("logits must be finite")
     E = codebook.E if codebook.on_device else device_f64(codebook.E, True)
-    return _ret(t.matmul(_softmax_rows(L, SOFTMAX_WEIGHTS), E), host, squeeze)
+    return _ret(gemm_f64(L, E.contiguous(), softmax=True), host, squeeze)

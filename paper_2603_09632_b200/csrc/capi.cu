@@ -368,6 +368,27 @@ int xgs_backproject(const double* R, const double* t, const double* intr4, const
   return OK;
 }
 
+size_t xgs_gemm_f64_workspace(int64_t n, int64_t kr, int64_t m, int64_t nq, int softmax_rows) {
+  return gemm_f64_workspace_bytes(n, m, nq, kr, softmax_rows != 0);
+}
+
+int xgs_gemm_f64(const double* A, int64_t n, int64_t kr, int64_t lda_r, int64_t lda_k, int softmax_rows,
+                 const double* B, int64_t m, int64_t ldb_k, int64_t ldb_m, double* C, int64_t ldc, const double* Q,
+                 int64_t nq, double tau, double eps, double* scores, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || kr < 1 || m < 0 || (n > 0 && (!A || !B))) return fail(INVALID_INPUT, "bad gemm operands");
+  if (!C && !scores) return fail(INVALID_INPUT, "need an output (C or scores)");
+  if (C && ldc < m) return fail(INVALID_INPUT, "ldc < m");
+  if (scores && (!Q || nq < 2)) return fail(INVALID_INPUT, "relevance needs a positive and >= 1 negative query");
+  if (nq > 16) return fail(NOT_SUPPORTED, "more than 16 query vectors");
+  if (ws_bytes < gemm_f64_workspace_bytes(n, m, scores ? nq : 0, kr, softmax_rows != 0))
+    return fail(INVALID_INPUT, "workspace too small");
+  if (softmax_rows && (lda_k != 1 || lda_r != kr)) return fail(NOT_SUPPORTED, "softmax rows must be dense (lda_k == 1, lda_r == kr)");
+  cudaError_t e = launch_gemm_f64(A, n, kr, lda_r, lda_k, softmax_rows != 0, B, m, ldb_k, ldb_m, C, ldc, Q,
+                                  scores ? nq : 0, tau, eps, scores, ws, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_gemm_f64");
+  return OK;
+}
+
 int xgs_pose_depths(const double* mu, int64_t n, const double* R9, const double* t3, double* z, uint64_t* key,
                     uint32_t* idx, void* stream) {
   if (n < 0 || !R9 || !t3) return fail(INVALID_INPUT, "bad pose_depths arguments");

@@ -51,7 +51,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 // records it only when it succeeded.
 enum AttrSite : int {
   kAttrScreen0 = 0, kAttrScreen1, kAttrScreen2, kAttrSeed, kAttrUpdate, kAttrGridFront, kAttrGridSort,
-  kAttrGridHash, kAttrCodebook, kAttrSites
+  kAttrGridHash, kAttrCodebook, kAttrGemmF64, kAttrSites
 };
 inline std::atomic<uint32_t>* attr_table() {
   static std::atomic<uint32_t> done[64];

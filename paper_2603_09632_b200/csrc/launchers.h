@@ -218,6 +218,13 @@ cudaError_t raster_accumulate(RasterState* st, const double* payload, int64_t C,
 cudaError_t raster_argmax(RasterState* st, int64_t* out, cudaStream_t s);
 cudaError_t raster_vjp(RasterState* st, const double* upstream, int64_t D, double* fg, cudaStream_t s);
 
+// ---------------- fp64 codeword contractions (decode_f64.cu) ----------------
+size_t gemm_f64_workspace_bytes(int64_t n, int64_t m, int64_t nq, int64_t kr, bool softmax);
+cudaError_t launch_gemm_f64(const double* A, int64_t n, int64_t kr, int64_t lda_r, int64_t lda_k, bool softmax,
+                            const double* B, int64_t m, int64_t ldb_k, int64_t ldb_m, double* C, int64_t ldc,
+                            const double* Q, int64_t nq, double tau, double eps, double* scores, void* ws,
+                            cudaStream_t s);
+
 // ---------------- codebook consumers (codebook.cu) ----------------
 enum CbMode : int { CB_WEIGHTS = 1, CB_ENTROPY = 2, CB_VJP = 4 };
 cudaError_t launch_softmax_rows(const double* logits, int64_t n, int64_t k, int mode, const double* up, double* out,

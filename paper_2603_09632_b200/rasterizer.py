@@ -25,7 +25,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as nat
-from .core import Codebook, decode_feature, device_f64, is_tensor, softmax_vjp, to_host
+from .core import Codebook, decode_feature, device_f64, gemm_f64, is_tensor, softmax_vjp, to_host
 from .errors import EmptySceneError, InvalidInputError
 from .supervision import GridSpec
 
@@ -269,5 +269,5 @@ def feature_gradients(field, codebook: Codebook, pose, intr, grid: GridSpec, ups
         finally:
             pr.close()
     E = codebook.E if codebook.on_device else device_f64(codebook.E, True)
-    lg = softmax_vjp(device_f64(field.logits, True), t.matmul(fg, E.t()))
+    lg = softmax_vjp(device_f64(field.logits, True), gemm_f64(fg.contiguous(), E.contiguous(), b_transposed=True))
     return FeatureGradients(logit_grads=to_host(lg) if host else lg, feature_grads=to_host(fg) if host else fg)

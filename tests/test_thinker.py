@@ -153,3 +153,44 @@ def test_desc_top_m_matches_stable_argsort(cuda, case, M):
         v = rng.normal(size=n) * 10.0 ** rng.integers(-30, 30, n)
     got = thinker._desc_top_m(torch.from_numpy(v).cuda(), M).cpu().numpy()
     assert np.array_equal(got, np.argsort(-v, kind="stable")[:M])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,kr,m", [(1, 5, 3), (33, 17, 385), (1000, 512, 768), (257, 100, 1000)])
+@pytest.mark.parametrize("layout", ["softmax", "plain", "a_t", "b_t"])
+def test_gemm_f64_dmma_shapes(cuda, n, kr, m, layout):
+    """xgs_gemm_f64 (DMMA fp64, softmax prologue / strided operands / contrast
+    epilogue) against NumPy fp64 at tile-edge shapes."""
+    import torch
+    from paper_2603_09632_b200 import core
+    rng = np.random.default_rng(n + kr + m)
+    A = rng.normal(scale=2.0, size=(n, kr))
+    B = rng.normal(size=(kr, m))
+    if layout == "softmax":
+        W = np.exp(A - A.max(axis=1, keepdims=True))
+        W /= W.sum(axis=1, keepdims=True)
+        ref = W @ B
+        got = core.gemm_f64(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), softmax=True)
+    elif layout == "plain":
+        ref = A @ B
+        got = core.gemm_f64(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    elif layout == "a_t":
+        ref = A @ B
+        got = core.gemm_f64(torch.from_numpy(np.ascontiguousarray(A.T)).cuda(), torch.from_numpy(B).cuda(),
+                            a_transposed=True)
+    else:
+        ref = A @ B
+        got = core.gemm_f64(torch.from_numpy(A).cuda(), torch.from_numpy(np.ascontiguousarray(B.T)).cuda(),
+                            b_transposed=True)
+    np.testing.assert_allclose(got.cpu().numpy(), ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+    if layout == "softmax" and m >= 2:
+        Q = rng.normal(size=(3, m))
+        Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+        f = ref / (np.linalg.norm(ref, axis=1, keepdims=True) + 1e-8)
+        pos = f @ Q[0]
+        sc = np.ones(n)
+        for q in Q[1:]:
+            sc = np.minimum(sc, 1.0 / (1.0 + np.exp(-(10.0 * (pos - f @ q)))))
+        _, s2 = core.gemm_f64(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), softmax=True,
+                              query=torch.from_numpy(Q).cuda(), tau=10.0, eps=1e-8, want_c=False)
+        np.testing.assert_allclose(s2.cpu().numpy(), sc, rtol=1e-12, atol=1e-14)
