@@ -924,7 +924,16 @@ def profiled_steps(torch, vq, x, sizes, steps):
     return prof
 
 
-def screen_roofline(prof, flops_per_step, steps):
+def ncu_traffic(key):
+    try:   # DRAM bytes of the screen kernel from a committed ncu capture (profiles/ncu_traffic.json)
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            v = json.load(f).get(key)
+        return v.get("bytes") if isinstance(v, dict) else v
+    except (OSError, ValueError):
+        return None
+
+
+def screen_roofline(prof, flops_per_step, steps, traffic=None):
     pk, pk_kind = peaks()
     scr_ms, scr_n = prof["vq_screen"]
     # per step: the screen stage's event-timed span (main pass + rescreen of
@@ -935,7 +944,7 @@ def screen_roofline(prof, flops_per_step, steps):
     peak_sus = pk.get("bf16_tflops_sustained")
     return {"bound": "tensor", "kernel": "screen_kernel (tcgen05 kind::f16, cta_group::2)",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": (achieved / peak) if achieved else None, "traffic": None,
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "peak_kind": f"{pk_kind} bf16 dense burst (f16 rate == bf16 rate)",
             "frac_vs_sustained": (achieved / peak_sus) if (achieved and peak_sus) else None,
             "algorithmic_flops_per_step": flops_per_step, "screen_ms_per_step": t_step}
@@ -974,7 +983,7 @@ def run_c2(torch, args, device):
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / 3
     out = {"workload": WORKLOAD, "Mfeat_per_s": N_ROWS / (ms * 1e-3) / 1e6, "ms_per_step": ms, "steps": steps,
-           "roofline": screen_roofline(prof, 2.0 * N_ROWS * K * D, 10),
+           "roofline": screen_roofline(prof, 2.0 * N_ROWS * K * D, 10, ncu_traffic("screen_kernel_C2")),
            "per_kernel": {t: {"ms_per_step": m / 10, "launches": c} for t, (m, c) in prof.items()},
            "assign_exact_rows": {"rerank": n_rerank, "fallback": n_fallback},
            "e2e": {"value": N_ROWS / (e2e_ms * 1e-3) / 1e6, "unit": "Mfeat/s", "h2d_bytes_per_step": N_ROWS * D * 4,
@@ -1051,7 +1060,11 @@ def main():
     prof = profiled_steps(torch, vq, x, sizes, prof_steps)
     cb_now = xv.Codebook._make(vq.state[0], vq.state[1], vq.state[2], LAM, EPS, None)
     _, (n_rerank, n_fallback) = xv.vq.assign_batch_stats(x, cb_now)
-    roof = screen_roofline(prof, 2.0 * rows * C5_K * C5_D, prof_steps)
+    t5 = ncu_traffic("screen_kernel_C5_per_step")
+    roof = screen_roofline(prof, 2.0 * rows * C5_K * C5_D, prof_steps,
+                           t5 * rows / C5_TOTAL if t5 else None)
+    roof["traffic_note"] = ("DRAM bytes per step of the screen kernel (all row-chunk launches) from the N=1 ncu "
+                            "capture profiles/r2_c5_launches.csv, scaled by this rank's rows")
 
     # e2e through the public API: every step copies its rows from pinned host
     # memory (H2D inside the timed region, overlapped chunk by chunk with the

@@ -583,16 +583,26 @@ int xgs_softmax_rows(const double* logits, int64_t n, int64_t k, int mode, const
   SumPlan pk;
   if (!build_sum_plan((int)k, &pk)) return fail(NOT_SUPPORTED, "K too large for the pairwise plan");
   cudaStream_t s = (cudaStream_t)stream;
-  int* bad = nullptr;
-  cudaError_t e = cudaMallocAsync(&bad, sizeof(int), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int), s);
-  if (e == cudaSuccess) e = launch_softmax_rows(logits, n, k, mode, upstream, out, out_h, pk, bad, s);
-  int hbad = 0;
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
-  if (bad) cudaFreeAsync(bad, s);
+  // non-finite flag: a per-thread, per-device mapped pinned word the kernel
+  // sets directly (no allocation, no copy per call)
+  thread_local volatile int* hflag[16] = {};
+  thread_local int* dflag[16] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess && (dev < 0 || dev >= 16)) e = cudaErrorInvalidDevice;
+  if (e == cudaSuccess && !hflag[dev]) {
+    void* h = nullptr;
+    e = cudaHostAlloc(&h, 64, cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&dflag[dev]), h, 0);
+    if (e == cudaSuccess) hflag[dev] = static_cast<volatile int*>(h);
+  }
+  if (e == cudaSuccess) {
+    *hflag[dev] = 0;
+    e = launch_softmax_rows(logits, n, k, mode, upstream, out, out_h, pk, dflag[dev], s);
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "xgs_softmax_rows");
-  if (hbad) return fail(INVALID_INPUT, "logits must be finite");
+  if (*hflag[dev]) return fail(INVALID_INPUT, "logits must be finite");
   return OK;
 }
 

@@ -57,7 +57,7 @@ cb_rows_kernel(const double* __restrict__ L, int64_t n, int64_t k, const double*
     }
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
     if (!__all_sync(FULL, fin)) {
-      if (lane == 0) atomicOr(bad, 1);
+      if (lane == 0) *(volatile int*)bad = 1;   // idempotent flag (may live in mapped host memory)
       continue;
     }
     if (CACHE) {
@@ -110,7 +110,7 @@ cb_entropy_kernel(const double* __restrict__ L, int64_t n, int64_t k, double* __
     }
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
     if (!__all_sync(FULL, fin)) {
-      if (lane == 0) atomicOr(bad, 1);
+      if (lane == 0) *(volatile int*)bad = 1;   // idempotent flag (may live in mapped host memory)
       continue;
     }
     double S = 0.0, T = 0.0;
