@@ -91,6 +91,7 @@ struct ScreenParams {
   int32_t sq_cap;
   int num_pair_tiles, num_n_chunks, num_k_blocks;
   int resident;         // A row tile stays in smem across the N chunks (num_k_blocks <= A_SLOTS)
+  int pf_late;          // streaming A: prefetch the next row tile during the last codebook chunk only
   const float* xband;   // per row: 2 * max_k B_k + fp64-reference slack
   const float* xf;
   const float* cn;
@@ -407,12 +408,18 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       const uint32_t lead_full = mapa(smem_u32(fullA), 0);
       uint32_t idx = 0;
       const int nload = p.resident ? nkb : nkb * nnc;
+      // warm L2 with the next tile's rows: at the tile start when the A tile is
+      // resident (one load per tile), else only during the tile's last
+      // codebook chunk -- streaming A re-reads the tile once per chunk, and an
+      // early prefetch doubles the L2 footprint of the row tiles (at C5 the
+      // evicted re-reads doubled the screen's DRAM traffic)
+      const int pf_at = (p.resident || !p.pf_late) ? 0 : (nnc - 1) * nkb;
       for (int t = cluster; t < ntiles; t += nclusters) {
         const int row0 = t * 2 * BM + (int)rank * BM;
         const int tn = t + nclusters;
-        if (tn < ntiles)   // warm L2 with the next tile's rows
-          for (int kb = 0; kb < nkb; kb++) tma_prefetch_2d(&tmA, kb * BK, tn * 2 * BM + (int)rank * BM);
         for (int j = 0; j < nload; j++, idx++) {
+          if (j == pf_at && tn < ntiles)
+            for (int kb = 0; kb < nkb; kb++) tma_prefetch_2d(&tmA, kb * BK, tn * 2 * BM + (int)rank * BM);
           const int kb = j % nkb;
           const uint32_t slot = idx % A_SLOTS, ph = (idx / A_SLOTS) & 1;
           mbar_wait(&emptyA[slot], ph ^ 1);
@@ -1002,6 +1009,13 @@ cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, 
   p.num_n_chunks = (int)(b.w.kp / BN);
   p.num_k_blocks = (int)(dp / BK);
   p.resident = p.num_k_blocks <= A_SLOTS;
+  {
+    static const int pf_early = [] {
+      const char* v = std::getenv("XGS_SCREEN_PF_EARLY");   // A/B switch for the measurement
+      return v && v[0] == '1';
+    }();
+    p.pf_late = pf_early ? 0 : 1;
+  }
   p.xband = b.xn + sb;
   p.xf = b.xf + sb;
   p.cn = b.cn;

@@ -150,13 +150,17 @@ class PerceiverStream:
         self.graph = g
 
     # ------------------------------------------------------------ per frame
+    def inputs(self):
+        """The staging tensors the graph reads: (depth (1, H, W) fp32, R (1, 9)
+        fp64, t (1, 3) fp64, colour (1, H, W, 3) u8, features (1, C, Hf, Wf)
+        fp32).  A producer that writes the next frame into them directly
+        saves step() the staging copies."""
+        return self.depth, self.R, self.T, self.color, self.feat
+
     def _stage(self, depth, R, T, color, feats):
-        t = self.t
-        self.depth.view(self.H, self.W).copy_(depth.reshape(self.H, self.W), non_blocking=True)
-        self.color.view(-1).copy_(color.reshape(-1), non_blocking=True)
-        self.R.view(-1).copy_(R.reshape(-1), non_blocking=True)
-        self.T.view(-1).copy_(T.reshape(-1), non_blocking=True)
-        self.feat.view(-1).copy_(feats.reshape(-1), non_blocking=True)
+        for dst, src in ((self.depth, depth), (self.color, color), (self.R, R), (self.T, T), (self.feat, feats)):
+            if src.data_ptr() != dst.data_ptr():
+                dst.view(-1).copy_(src.reshape(-1), non_blocking=True)
 
     def _sync_frame(self):
         """Synchronous path on the staged frame (first frame: sizes the library
