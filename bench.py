@@ -1081,7 +1081,7 @@ def main():
     # 154.6 GB / N shard is not done: each step streams E2E_ROWS rows per rank
     # (the same distribution, K, D and dtype); the rate is PCIe-bound.
     del vq
-    e2e_rows = min(min(sizes), 1 << 22)
+    e2e_rows = min(min(sizes), (1 << 22) // world)   # ~9.7 GB of pinned host rows in total over the ranks
     xh = x[:e2e_rows].cpu().pin_memory()
     del x
     torch.cuda.empty_cache()
@@ -1146,7 +1146,7 @@ def main():
                     "d2h_bytes_per_step": C5_K * C5_D * 8, "ms_per_step": e2e_ms,
                     "rows_per_step": world * e2e_rows,
                     "note": "pinned host rows streamed into the step (H2D chunks overlapped with the device work); "
-                            "4,194,304 rows per rank per step (the whole shard is not pinned), same K/D/dtype"},
+                            "4,194,304 / N rows per rank per step (the whole shard is not pinned), same K/D/dtype"},
             "gpu_launches": launches,
             "roofline": roof,
             "per_kernel": per_kernel,
