@@ -429,7 +429,7 @@ def run_stream(torch, frames, device):
                            xv.FeatureReservoir(cfg.reservoir_capacity, STREAM_D))
     Hf, Wf = STREAM_FEAT_HW
     st = PerceiverStream(STREAM_INTR, STREAM_H, STREAM_W, 0.02, cb, cfg, (STREAM_D, Hf, Wf),
-                         np.random.default_rng(32), map_capacity=1 << 23, vq_capacity=16384)
+                         np.random.default_rng(32), map_capacity=1 << 23, vq_capacity=8192)
     noise = torch.Generator(device=device)
     noise.manual_seed(33)
     lat, newpts, graph = [], [], 0

@@ -1289,19 +1289,6 @@ __device__ __forceinline__ void emit_one(int64_t o, int64_t p, const int32_t* __
       a.col[o * 3 + c] = a.color ? ddiv((double)a.color[p * 3 + c], 255.0) : 0.0;
     }
     if (a.count) a.count[o] = 1.0;
-    if (a.feat) {
-      // supervision.py:133-147 nearest-neighbour gather rule
-      const int64_t uu = (int64_t)floor(ddiv(dmul((double)u, (double)(a.fh - 1)), (double)max(a.H - 1, (int64_t)1)) + 0.5);
-      const int64_t vv = (int64_t)floor(ddiv(dmul((double)v, (double)(a.fw - 1)), (double)max(a.W - 1, (int64_t)1)) + 0.5);
-      const float* src = a.feat + f * a.fc * a.fh * a.fw + uu * a.fw + vv;
-      if (a.feat64) {
-        double* dst = static_cast<double*>(a.ofeat) + o * a.fc;
-        for (int64_t c = 0; c < a.fc; c++) dst[c] = (double)src[c * a.fh * a.fw];
-      } else {
-        float* dst = static_cast<float*>(a.ofeat) + o * a.fc;
-        for (int64_t c = 0; c < a.fc; c++) dst[c] = src[c * a.fh * a.fw];
-      }
-    }
   } else {
     // mean over the voxel's points in the head's frame, sequential in pid order
     const int64_t i0 = head_pos[p];
@@ -1327,28 +1314,6 @@ __device__ __forceinline__ void emit_one(int64_t o, int64_t p, const int32_t* __
       a.col[o * 3 + c] = ddiv(sc[c], cnt);
     }
     if (a.count) a.count[o] = cnt;
-    if (a.feat) {
-      // per channel: the members' gathered features (supervision.py:133-147
-      // rule per member pixel) summed in fp64 in ascending pid order, / count
-      // (oracle/grid.py: np.add.at over the members, then acc / cnt)
-      const double su = (double)(a.fh - 1), sv = (double)(a.fw - 1);
-      const double hu = (double)max(a.H - 1, (int64_t)1), hv = (double)max(a.W - 1, (int64_t)1);
-      const float* fbase = a.feat + f * a.fc * a.fh * a.fw;
-      double* dst = static_cast<double*>(a.ofeat) + o * a.fc;
-      for (int64_t c = 0; c < a.fc; c++) {
-        double acc = 0.0;
-        for (int64_t i = i0; i < a.n && a.skeys[i] == key; i++) {
-          const int64_t q = a.svals[i];
-          if (q / HW != f) continue;
-          const int64_t r2 = q - f * HW;
-          const int64_t uq = r2 / a.W, vq = r2 - uq * a.W;
-          const int64_t uu = (int64_t)floor(ddiv(dmul((double)uq, su), hu) + 0.5);
-          const int64_t vv = (int64_t)floor(ddiv(dmul((double)vq, sv), hv) + 0.5);
-          acc = dadd(acc, (double)fbase[(c * a.fh + uu) * a.fw + vv]);
-        }
-        dst[c] = ddiv(acc, cnt);
-      }
-    }
   }
 }
 
@@ -1368,6 +1333,53 @@ __global__ void prefix_mask_kernel(const int64_t* __restrict__ n_dev, int64_t ca
   const int64_t n = *n_dev;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x)
     mask[i] = i < n ? 1 : 0;
+}
+
+// Per-voxel features (supervision.py:133-147 nearest-lattice gather rule), one
+// thread per (new voxel, channel) -- consecutive threads write consecutive
+// channels of a row.  First-pick: the representative pixel's value; mean: the
+// fp64 sum of the members' gathered values in ascending pid order (the voxel's
+// points in the representative's frame, as for mu), / count.  (A thread per
+// voxel copying all C channels serialises C strided loads: 0.45 ms for ~2.8K
+// voxels x 768 channels at C4.)
+__global__ void __launch_bounds__(256)
+grid_emit_feat_kernel(const int32_t* __restrict__ head_pos, const int32_t* __restrict__ nnew_dev, int64_t capacity,
+                      EmitArgs a) {
+  pdl_wait();
+  const int64_t nnew = min((int64_t)*nnew_dev, capacity);
+  const int64_t total = nnew * a.fc;
+  const int64_t HW = a.H * a.W;
+  const double su = (double)(a.fh - 1), sv = (double)(a.fw - 1);
+  const double hu = (double)max(a.H - 1, (int64_t)1), hv = (double)max(a.W - 1, (int64_t)1);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = i / a.fc, c = i - o * a.fc;
+    const int64_t p = a.pid[o];
+    const int64_t f = p / HW, rem = p - f * HW;
+    const float* plane = a.feat + (f * a.fc + c) * a.fh * a.fw;
+    if (a.mode == 0) {
+      const int64_t u = rem / a.W, v = rem - u * a.W;
+      const int64_t uu = (int64_t)floor(ddiv(dmul((double)u, su), hu) + 0.5);
+      const int64_t vv = (int64_t)floor(ddiv(dmul((double)v, sv), hv) + 0.5);
+      const float x = plane[uu * a.fw + vv];
+      if (a.feat64) static_cast<double*>(a.ofeat)[i] = (double)x;
+      else static_cast<float*>(a.ofeat)[i] = x;
+    } else {
+      const int64_t i0 = head_pos[p];
+      const uint64_t key = a.skeys[i0];
+      double acc = 0.0, cnt = 0.0;
+      for (int64_t j = i0; j < a.n && a.skeys[j] == key; j++) {
+        const int64_t q = a.svals[j];
+        if (q / HW != f) continue;
+        const int64_t r2 = q - f * HW;
+        const int64_t uq = r2 / a.W, vq = r2 - uq * a.W;
+        const int64_t uu = (int64_t)floor(ddiv(dmul((double)uq, su), hu) + 0.5);
+        const int64_t vv = (int64_t)floor(ddiv(dmul((double)vq, sv), hv) + 0.5);
+        acc = dadd(acc, (double)plane[uu * a.fw + vv]);
+        cnt = dadd(cnt, 1.0);
+      }
+      static_cast<double*>(a.ofeat)[i] = ddiv(acc, cnt);
+    }
+  }
 }
 
 __global__ void fill_u64_kernel(unsigned long long* p, int64_t n, unsigned long long v) {
@@ -2022,6 +2034,12 @@ cudaError_t emit_outputs(const GridIn& in, const Cam& cam, DedupTable* st, const
                       (const int32_t*)grand, (int64_t)out.capacity, ea)) != cudaSuccess)
     return e;
   count_launches(1);
+  if (in.feat) {
+    if ((e = launch_pdl(grid_emit_feat_kernel, dim3(grid_blocks(out.capacity * in.fc, 256, sms)), dim3(256), 0, s,
+                        head, (const int32_t*)grand, (int64_t)out.capacity, ea)) != cudaSuccess)
+      return e;
+    count_launches(1);
+  }
   return sync ? cudaStreamSynchronize(s) : cudaGetLastError();
 }
 
