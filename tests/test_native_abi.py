@@ -39,6 +39,22 @@ def test_workspace_queries_without_gpu():
     assert L.xgs_vq_accumulate_workspace(1000, 16) > 4000
 
 
+def test_screening_workspace_is_bounded_by_the_row_chunk():
+    """The per-row screening buffers cover one row chunk (two slots), not the
+    batch: at C5 on one GPU (67,108,864 bf16 rows x 1152, K=4096) the step
+    workspace stays ~10 GB beside the 154.6 GB batch (it used to be another
+    full fp16 copy of the batch plus N-sized queues)."""
+    from paper_2603_09632_b200 import _native
+    L = _native.lib()
+    n, k, d = 67_108_864, 4096, 1152
+    step = L.xgs_vq_step_workspace(n, k, d, 2, d)
+    assert step < 12e9, step
+    small = L.xgs_vq_step_workspace(1 << 22, k, d, 2, d)
+    big = L.xgs_vq_step_workspace(1 << 24, k, d, 2, d)
+    # beyond one chunk the screening part is flat; only the 4-byte-per-row accumulate part grows
+    assert big - small < (1 << 24) * 16
+
+
 def test_error_codes_map_to_reference_exceptions():
     """Argument validation happens before any CUDA call, so the status codes
     and the InvalidInputError / InvalidStateError mapping are checkable here."""
