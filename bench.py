@@ -1073,7 +1073,7 @@ def main():
     roof = screen_roofline(prof, 2.0 * rows * C5_K * C5_D, prof_steps,
                            t5 * rows / C5_TOTAL if t5 else None)
     roof["traffic_note"] = ("DRAM bytes per step of the screen kernel (all row-chunk launches) from the N=1 ncu "
-                            "capture profiles/r2_c5_launches.csv, scaled by this rank's rows")
+                            "capture profiles/r2_c5_screen_pflate.csv, scaled by this rank's rows")
 
     # e2e through the public API: every step copies its rows from pinned host
     # memory (H2D inside the timed region, overlapped chunk by chunk with the
