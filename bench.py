@@ -1035,6 +1035,9 @@ def main():
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
+        # NCCL's init lines (transport: NVLink / NVLS) go to stderr; the JSON line stays on stdout
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,GRAPH")
         dist.init_process_group("nccl", device_id=device)
 
     import paper_2603_09632_b200 as xv

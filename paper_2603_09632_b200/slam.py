@@ -3,10 +3,13 @@
 ``backproject`` (slam.py:594-598) and ``densify_and_prune`` (slam.py:601-651)
 keep their reference signatures; the arithmetic runs in libxgs
 (``xgs_backproject``: fp64, reference operation order, bit-identical).
-``densify_and_prune`` reproduces the reference exactly on an empty map; on a
-non-empty map the rasterizer coverage test (a full render, out of scope) is
-replaced by the voxel occupancy test of :mod:`grid`.
-The voxel-grid sampler for whole RGB-D frames is :class:`grid.GridSampler`.
+``densify_and_prune`` reproduces the reference exactly: on a non-empty map
+the coverage test renders the field with the GPU rasterizer
+(``rasterizer.render``, slam.py:608-626) and the median fallback depth comes
+from ``xgs_pose_depths`` + the in-house radix sort (slam.py:611-613, 654-655).
+Passing ``occupied`` / ``voxel_size`` selects the voxel-occupancy variant
+instead of the render.  The voxel-grid sampler for
+whole RGB-D frames is :class:`grid.GridSampler`.
 """
 
 from __future__ import annotations
