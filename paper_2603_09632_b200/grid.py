@@ -195,7 +195,7 @@ def _grid_ws_bytes(npix):
 
 
 def _intr4(intr):
-    if isinstance(intr, CameraIntrinsics):
+    if isinstance(intr, CameraIntrinsics) or hasattr(intr, "fx"):   # ours or semsplat.core's
         return float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy)
     fx, fy, cx, cy = (float(v) for v in intr)
     return fx, fy, cx, cy
@@ -204,9 +204,11 @@ def _intr4(intr):
 def _poses(poses, F):
     """list[CameraPose] | (R [F,3,3], t [F,3]) -> device fp64 (R, t)."""
     t = nat.torch()
-    if isinstance(poses, CameraPose):
+    def _is_pose(p):   # ours or semsplat.core.CameraPose
+        return isinstance(p, CameraPose) or (hasattr(p, "rotation") and hasattr(p, "translation"))
+    if _is_pose(poses):
         poses = [poses]
-    if isinstance(poses, (list, tuple)) and poses and isinstance(poses[0], CameraPose):
+    if isinstance(poses, (list, tuple)) and poses and _is_pose(poses[0]):
         R = np.stack([p.rotation for p in poses])
         tr = np.stack([p.translation for p in poses])
     else:

@@ -90,7 +90,7 @@ def frame_intrinsics(frame, cfg=None, fov_deg: float = 60.0) -> CameraIntrinsics
 def backproject_pixels(pose: CameraPose, intr, u, v, depth):
     """Batched slam.backproject: (n,) rows u, columns v, depths -> (n, 3) fp64."""
     t = nat.require_cuda()
-    fx, fy, cx, cy = ((intr.fx, intr.fy, intr.cx, intr.cy) if isinstance(intr, CameraIntrinsics)
+    fx, fy, cx, cy = ((intr.fx, intr.fy, intr.cx, intr.cy) if hasattr(intr, "fx")   # ours or the reference's
                       else tuple(float(x) for x in intr))
     host = not any(hasattr(a, "data_ptr") for a in (u, v, depth))
     dev = lambda a: (a if hasattr(a, "data_ptr") else t.from_numpy(np.ascontiguousarray(

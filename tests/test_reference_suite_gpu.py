@@ -77,3 +77,52 @@ def test_shim_routes_to_native(cuda):
             reference_shim.uninstall()
     finally:
         sys.path.remove(REF)
+
+
+def test_shim_slam_matches_reference(cuda):
+    """backproject / densify_and_prune through the shim on the reference's own
+    types (a scene, trajectory and frames from semsplat.world) give the same
+    splats as the reference's NumPy functions on the same inputs."""
+    if not os.path.isdir(os.path.join(REF, "semsplat")):
+        pytest.skip("reference not installed under baseline/_ref")
+    sys.path.insert(0, REF)
+    try:
+        import numpy as np
+        import semsplat.core as rc
+        import semsplat.slam as rs
+        import semsplat.world as rw
+
+        from paper_2603_09632_b200 import _native, reference_shim
+        recipe = rw.standard_recipe(height=48, width=64, n_gaussians=90)
+        field, labels, phi = rw.generate_scene(recipe)
+        poses = rw.generate_trajectory(recipe)
+        frames = rw.render_ground_truth(field, labels, phi, poses[:12:4], recipe.intrinsics())
+        cfg = rs.SlamConfig()
+        reference_shim.install()
+        try:
+            ref_bp, ref_dp = rs.backproject.__wrapped_reference__, rs.densify_and_prune.__wrapped_reference__
+            intr = rs.frame_intrinsics(frames[0], cfg)
+            for (u, v, d) in ((0.0, 0.0, 1.0), (17.5, 30.25, 2.75), (63.0, 47.0, 0.4)):
+                assert np.array_equal(rs.backproject(poses[4], intr, u, v, d), ref_bp(poses[4], intr, u, v, d))
+            keep = np.random.default_rng(3).random(len(field)) < 0.5      # leave holes to fill
+            part = rc.GaussianField(mu=field.mu[keep], quat=field.quat[keep], scale=field.scale[keep],
+                                    opacity=np.where(np.arange(keep.sum()) % 9 == 0, 0.004, field.opacity[keep]),
+                                    color=field.color[keep], logits=np.zeros((int(keep.sum()), 4)))
+            empty = rc.GaussianField(mu=np.zeros((0, 3)), quat=np.zeros((0, 4)), scale=np.zeros((0, 3)),
+                                     opacity=np.zeros(0), color=np.zeros((0, 3)), logits=np.zeros((0, 4)))
+            for fr in frames:
+                win = rs.KeyframeWindow(3)
+                win.insert(fr, fr.pose)
+                for start in (part, empty):
+                    n0 = _native.launch_count()
+                    got = rs.densify_and_prune(start, win, cfg, K=4)
+                    assert _native.launch_count() > n0
+                    ref = ref_dp(start, win, cfg, K=4)
+                    assert isinstance(got, rc.GaussianField) and len(got) == len(ref), fr.frame_id
+                    for name in ("mu", "quat", "scale", "opacity", "color", "logits"):
+                        assert np.array_equal(getattr(got, name), getattr(ref, name)), (fr.frame_id, name)
+                    assert got.generation == ref.generation
+        finally:
+            reference_shim.uninstall()
+    finally:
+        sys.path.remove(REF)
