@@ -253,12 +253,17 @@ def run_grid(torch, steps, cpu=True):
         warm, n_scene, warm_frames = grid_warm_map(torch, voxel)
         times, calls, spans, stage = [], [], [], {}
         r = None
-        for it in range(steps + 1):
+        # iterations 1..steps: the batch span alone (profile_only: no events between its
+        # kernels, so the launches chain as in production); then `steps` more with every
+        # stage scope for the per-stage split
+        for it in range(2 * steps + 1):
+            staged = it > steps
             hs = VoxelHashSet(GRID_MAP + npix)
             hs.insert(warm)
             map_size = len(hs)
             gs = GridSampler(GRID_INTR, voxel, occupied=hs)
             torch.cuda.synchronize()
+            nat.profile_only(None if staged else "grid_batch")
             nat.profile_enable(True)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0 = time.perf_counter()
@@ -269,10 +274,12 @@ def run_grid(torch, steps, cpu=True):
             t1 = time.perf_counter()
             prof = {t: nat.profile_read(t)[0] for t in ("grid_batch", "grid_keys", "grid_select", "grid_emit")}
             nat.profile_enable(False)
-            if it > 0:   # the first batch sizes the library's tables
+            nat.profile_only(None)
+            if it > 0 and not staged:   # the first batch sizes the library's tables
                 times.append(e0.elapsed_time(e1))
                 calls.append((t1 - t0) * 1e3)
                 spans.append(prof["grid_batch"])
+            if staged:
                 for k_, v_ in prof.items():
                     stage.setdefault(k_, []).append(v_)
             hs.close()
@@ -321,7 +328,9 @@ def run_grid(torch, steps, cpu=True):
                     "h2d_bytes": e2e_h2d, "d2h_bytes": e2e_d2h,
                     "note": "host wall clock around sample() + to_numpy(), pinned host frames"}}
     out["timing"] = ("ms_per_batch = device span of the C-ABI call xgs_grid_sample (first launch .. its status "
-                     "sync; ProfScope 'grid_batch'); ms_per_batch_python_call adds the Python wrapper")
+                     "sync; ProfScope 'grid_batch' recorded alone, no events between the kernels); per_stage_ms "
+                     "from separate batches with every stage scope on; ms_per_batch_python_call adds the Python "
+                     "wrapper")
     if cpu:
         from oracle import grid as og
         t0 = time.perf_counter()

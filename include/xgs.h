@@ -49,6 +49,9 @@ XGS_API long long xgs_launch_count(void);
  * named kernel group ("vq_prep", "vq_screen", "vq_rerank", "vq_accumulate",
  * "vq_chain", "vq_ema", "grid_*"); enable(1) clears, read() synchronises. */
 XGS_API int xgs_profile_enable(int on);
+/* restrict the profiler to one tag (NULL / "" = every tag): e.g. "grid_batch"
+ * alone times a whole grid batch without events between its kernels */
+XGS_API int xgs_profile_only(const char* tag);
 XGS_API int xgs_profile_read(const char* tag, double* total_ms, long long* count);
 /* CSV "tag,start_ms,end_ms" of every profiled launch, relative to the earliest */
 XGS_API int xgs_profile_dump(const char* path);

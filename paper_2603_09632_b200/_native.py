@@ -32,6 +32,7 @@ SIGNATURES = {
     "xgs_device_sm_count": (_i32, []),
     "xgs_launch_count": (ctypes.c_longlong, []),
     "xgs_profile_enable": (_i32, [_i32]),
+    "xgs_profile_only": (_i32, [ctypes.c_char_p]),
     "xgs_profile_read": (_i32, [ctypes.c_char_p, _vp, _vp]),
     "xgs_profile_dump": (_i32, [ctypes.c_char_p]),
     "xgs_vq_assign_workspace": (_sz, [_i64, _i64, _i64, _i32, _i64]),
@@ -132,6 +133,11 @@ def launch_count():
 
 def profile_enable(on=True):
     check(lib().xgs_profile_enable(1 if on else 0))
+
+
+def profile_only(tag=None):
+    """Record only scopes named `tag` (None: all)."""
+    check(lib().xgs_profile_only(tag.encode() if tag else None))
 
 
 def profile_read(tag):

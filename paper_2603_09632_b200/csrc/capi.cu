@@ -24,11 +24,13 @@ static std::atomic<long long> g_launches{0};
 static std::atomic<int> g_prof_on{0};
 static std::mutex g_prof_mu;
 static std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> g_prof;
+static char g_prof_only[32] = {0};   // non-empty: only this tag records (no events between its kernels)
 
 void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 ProfScope::ProfScope(const char* t, cudaStream_t st) : tag(t), s(st), ev0(nullptr) {
   if (!g_prof_on.load()) return;
+  if (g_prof_only[0] && std::strcmp(g_prof_only, t) != 0) return;
   cudaEvent_t e;
   if (cudaEventCreate(&e) == cudaSuccess && cudaEventRecord(e, s) == cudaSuccess) ev0 = e;
 }
@@ -78,6 +80,13 @@ const char* xgs_last_error(void) { return g_err.c_str(); }
 int xgs_device_sm_count(void) { return sm_count(); }
 
 long long xgs_launch_count(void) { return g_launches.load(); }
+
+int xgs_profile_only(const char* tag) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (tag && std::strlen(tag) >= sizeof(g_prof_only)) return fail(INVALID_INPUT, "profile tag too long");
+  std::snprintf(g_prof_only, sizeof(g_prof_only), "%s", tag ? tag : "");
+  return OK;
+}
 
 int xgs_profile_enable(int on) {
   std::lock_guard<std::mutex> g(g_prof_mu);
