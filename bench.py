@@ -238,6 +238,40 @@ def grid_warm_map(torch, voxel, target=GRID_MAP, seed=20, max_frames=240):
     return scene, n_scene, used
 
 
+def grid_graph_times(torch, voxel, warm, frames, steps, ref):
+    """The same C3 batch through GridGraph (XGS_GRID_ASYNC captured in a CUDA
+    graph): one graph launch, kernels back to back with no host work between
+    them.  The map is restored from a snapshot (VoxelHashSet.copy_from, outside
+    the timed region) before every replay, so each replay sees the ~4M-voxel
+    running map; CUDA events around the replay on its stream."""
+    from paper_2603_09632_b200.grid import GridGraph, GridSampler, VoxelHashSet
+    Dd, Rd, Td, Cd = frames
+    npix = int(Dd.numel())
+    snap = VoxelHashSet(GRID_MAP + npix)
+    snap.insert(warm)
+    work = VoxelHashSet(GRID_MAP + npix)
+    work.copy_from(snap)
+    gg = GridGraph(GridSampler(GRID_INTR, voxel, occupied=work), Dd, (Rd, Td), Cd)
+    times = []
+    res = None
+    for it in range(steps + 1):
+        work.copy_from(snap)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        gg.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        res = gg.result()
+        if it > 0:
+            times.append(e0.elapsed_time(e1))
+    same = (len(res) == len(ref) and res.n_voxels == ref.n_voxels and
+            bool(torch.equal(res.key, ref.key)) and bool(torch.equal(res.pid, ref.pid)))
+    snap.close()
+    work.close()
+    return {"ms_per_batch": float(np.median(times)), "new_voxels": len(res), "matches_sync_call": same}
+
+
 def run_grid(torch, steps, cpu=True):
     """C3 grid sampling: Mpts/s = 16*1280*720 input pixels / batch time, map
     reset to the scene-derived ~4M-voxel running map before every timed batch."""
@@ -286,6 +320,7 @@ def run_grid(torch, steps, cpu=True):
         ms = float(np.median(spans))
         stage_ms = {k_: float(np.median(v_)) for k_, v_ in stage.items()}
         n_new, n_vox = len(r), r.n_voxels
+        graph = grid_graph_times(torch, voxel, warm, (Dd, Rd, Td, Cd), steps, r)
         # algorithmic bytes of the batch: depth in (4 B/px) + colour of the new voxels' pixels (3 B) + the
         # outputs written (key 8, pid 8, mu 24, colour 24, scale 8, depth 8, count 8 = 88 B per new voxel)
         # + one 32 B map-table sector per distinct voxel of the batch
@@ -314,7 +349,7 @@ def run_grid(torch, steps, cpu=True):
             "pixels": npix, "valid_points": r.n_valid, "batch_voxels": n_vox, "new_voxels": n_new,
             "rejected_voxels": n_vox - n_new, "rejected_frac": (n_vox - n_new) / max(1, n_vox),
             "map_voxels_before": map_size, "map_scene_voxels": n_scene, "map_warm_frames": warm_frames,
-            "items_inserted": r.n_sorted, "per_stage_ms": stage_ms,
+            "items_inserted": r.n_sorted, "per_stage_ms": stage_ms, "graph": graph,
             "batch_hbm_frac": batch_bytes / (ms * 1e-3) / 1e9 / pk_["hbm_gbs"],
             "roofline": {"bound": "hbm", "kernel": "grid_front_kernel<FRONT_INSERT> (back-projection, keys, "
                                                    "left/up dedup, batch-table insert)",

@@ -221,6 +221,8 @@ XGS_API int xgs_hashset_destroy(void* handle);
 XGS_API int xgs_hashset_insert(void* handle, const uint64_t* keys, int64_t n, uint8_t* was_new, void* stream);
 XGS_API int xgs_hashset_contains(void* handle, const uint64_t* keys, int64_t n, uint8_t* out, void* stream);
 XGS_API int xgs_hashset_size(void* handle, int64_t* n_out, void* stream); /* synchronises */
+/* snapshot / restore: dst's keys become src's (tables of equal capacity; stream-ordered copy) */
+XGS_API int xgs_hashset_copy(void* dst, const void* src, void* stream);
 
 /* In-house stable LSD radix sort of (u64 key, u32 value) pairs on bits [0, bits). */
 XGS_API size_t xgs_grid_workspace(int64_t npix);
@@ -272,7 +274,12 @@ typedef struct {
  * n_voxels are NOT returned in the struct (set to -1); out->dev_status
  * (device int64[4]) receives {n_new, n_valid, n_voxels, error} when the
  * batch's last kernel ends; error != 0 (batch table or map probing overflow)
- * means the batch must be redone synchronously. */
+ * means the batch must be redone synchronously.  A captured graph holds the
+ * addresses of the library's per-device grid state: after the first async
+ * call those buffers are never freed (a synchronous batch that outgrows one
+ * gets a new buffer; the old one stays allocated for the graphs) -- and the
+ * state's counters are shared, so grid batches of one device must run on one
+ * stream at a time. */
 enum { XGS_GRID_ASYNC = 1 };
 
 typedef struct {

@@ -58,6 +58,7 @@ SIGNATURES = {
     "xgs_hashset_insert": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "xgs_hashset_contains": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "xgs_hashset_size": (_i32, [_vp, _vp, _vp]),
+    "xgs_hashset_copy": (_i32, [_vp, _vp, _vp]),
     "xgs_grid_workspace": (_sz, [_i64]),
     "xgs_radix_sort_pairs_u64": (_i32, [_vp, _vp, _i64, _i32, _vp, _sz, _vp]),
     "xgs_grid_sample": (_i32, [_vp, _vp, _vp, _vp, _sz, _vp]),

@@ -437,6 +437,15 @@ int xgs_hashset_contains(void* handle, const uint64_t* keys, int64_t n, uint8_t*
   return OK;
 }
 
+int xgs_hashset_copy(void* dst, const void* src, void* stream) {
+  if (!dst || !src) return fail(INVALID_INPUT, "bad hashset copy");
+  if (dst == src) return OK;
+  cudaError_t e = hashset_copy(static_cast<HashSet*>(dst), static_cast<const HashSet*>(src), (cudaStream_t)stream);
+  if (e == cudaErrorInvalidValue) return fail(INVALID_INPUT, "hashset copy needs equal table capacities");
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_hashset_copy");
+  return OK;
+}
+
 int xgs_hashset_size(void* handle, int64_t* n_out, void* stream) {
   if (!handle || !n_out) return fail(INVALID_INPUT, "bad hashset size");
   cudaError_t e = hashset_size(static_cast<HashSet*>(handle), n_out, (cudaStream_t)stream);

@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "launchers.h"
 
@@ -1541,6 +1542,17 @@ cudaError_t hashset_insert(HashSet* h, const uint64_t* keys, int64_t n, uint8_t*
   return cudaGetLastError();
 }
 
+// snapshot / restore: dst takes src's keys (same capacity: the table is copied as is)
+cudaError_t hashset_copy(HashSet* dst, const HashSet* src, cudaStream_t s) {
+  if (dst->cap != src->cap) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemcpyAsync(dst->table, src->table, sizeof(unsigned long long) * src->cap,
+                                  cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(dst->count_dev, src->count_dev, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s);
+  dst->count_ub = src->count_ub;
+  return e;
+}
+
 cudaError_t hashset_contains(HashSet* h, const uint64_t* keys, int64_t n, uint8_t* out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   hs_contains_kernel<<<grid_blocks(n, 256, 148), 256, 0, s>>>(h->table, (uint64_t)h->cap - 1, keys, n, out); count_launches(1);
@@ -1920,6 +1932,17 @@ struct DedupTable {
   unsigned long long* host_st = nullptr;      // mapped pinned [8]
   unsigned long long* host_st_dev = nullptr;  // its device alias
   bool dirty = false;                    // a batch stopped before its counters were reset
+  // set by the first XGS_GRID_ASYNC call: CUDA graphs may hold these buffers'
+  // addresses from then on, so a buffer the synchronous path outgrows is
+  // retired (kept allocated, never reused) instead of freed, and the batch
+  // table is no longer shrunk
+  bool pinned = false;
+  std::vector<void*> retired;
+  void release(void* p) {
+    if (!p) return;
+    if (pinned) retired.push_back(p);
+    else cudaFree(p);
+  }
 };
 constexpr int kDedupDevices = 16;
 DedupTable g_dedup[kDedupDevices];
@@ -1944,7 +1967,7 @@ cudaError_t grid_state(int64_t npix, cudaStream_t s, DedupTable** out, bool may_
   if (t.flag_words < nwords) {
     if (t.flags) {
       if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-      cudaFree(t.flags);
+      t.release(t.flags);
       t.flags = nullptr;
     }
     const int64_t words = nwords + nwords / 4;
@@ -1952,7 +1975,7 @@ cudaError_t grid_state(int64_t npix, cudaStream_t s, DedupTable** out, bool may_
     if ((e = cudaMemsetAsync(t.flags, 0, (size_t)words * 4, s)) != cudaSuccess) return e;
     t.flag_words = words;
     const int64_t tiles = (words + kLbTile - 1) / kLbTile;
-    if (t.lb) cudaFree(t.lb);
+    t.release(t.lb);
     if ((e = cudaMalloc(&t.lb, (size_t)tiles * 8)) != cudaSuccess) return e;
     t.lb_tiles = tiles;
   }
@@ -1974,10 +1997,10 @@ cudaError_t dedup_table(DedupTable& t, int64_t nitems, bool all, cudaStream_t s)
   int64_t cap = 1 << 20;
   while (cap < want) cap <<= 1;
   // keep the table when it is big enough but not over 2x too big (probes stay L2-resident)
-  if (t.slots && t.cap >= cap && t.cap <= 2 * cap) return cudaSuccess;
+  if (t.slots && t.cap >= cap && (t.cap <= 2 * cap || t.pinned)) return cudaSuccess;
   if (t.slots) {
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;   // earlier batches may still use it
-    cudaFree(t.slots);
+    t.release(t.slots);
     t.slots = nullptr;
   }
   if ((e = cudaMalloc(&t.slots, sizeof(unsigned long long) * 2 * cap)) != cudaSuccess) return e;
@@ -2142,6 +2165,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   // order over the voxel's segment)
   const bool hashed = compact && !sort_forced();
   if (in.async && !hashed) return cudaErrorNotSupported;
+  if (in.async) st->pinned = true;   // a graph may capture this call: keep the state's buffers alive
   st->dirty = true;
   if (hashed) {
     // ---------------- G1+G2': front end inserting into the batch table, table scan + map test

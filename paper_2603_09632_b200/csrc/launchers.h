@@ -142,6 +142,7 @@ cudaError_t hashset_size(HashSet* h, int64_t* n, cudaStream_t s);
 cudaError_t hashset_reserve(HashSet* h, int64_t extra, cudaStream_t s);
 cudaError_t hashset_insert(HashSet* h, const uint64_t* keys, int64_t n, uint8_t* was_new, cudaStream_t s);
 cudaError_t hashset_contains(HashSet* h, const uint64_t* keys, int64_t n, uint8_t* out, cudaStream_t s);
+cudaError_t hashset_copy(HashSet* dst, const HashSet* src, cudaStream_t s);
 cudaError_t launch_backproject(const double* R, const double* t, const double* intr4, double voxel, const double* u,
                                const double* v, const double* d, int64_t n, double* out, cudaStream_t s);
 size_t grid_workspace_bytes(int64_t npix);

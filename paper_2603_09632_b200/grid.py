@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _native as nat
 from .core import CameraIntrinsics, CameraPose, is_tensor
-from .errors import InvalidInputError
+from .errors import InvalidInputError, InvalidStateError
 
 KEY_BIAS = 1 << 20
 KEY_INVALID = (1 << 64) - 1
@@ -68,6 +68,12 @@ class VoxelHashSet:
         out = t.empty(k.numel(), dtype=t.uint8, device="cuda")
         nat.call("xgs_hashset_contains", self._h, nat.ptr(k), k.numel(), nat.ptr(out), nat.stream_ptr())
         return out.bool()
+
+    def copy_from(self, other: "VoxelHashSet"):
+        """Snapshot / restore: this set's keys become `other`'s (stream-ordered;
+        both created with the same capacity and not grown since)."""
+        nat.call("xgs_hashset_copy", self._h, other._h, nat.stream_ptr())
+        return self
 
     def close(self):
         if getattr(self, "_h", None) is not None and nat._lib is not None:
@@ -323,6 +329,76 @@ class GridSampler:
                      ws.numel(), nat.stream_ptr())
         return GridSampleResult(flat, cap, int(res.n_new), ofeat, int(res.n_valid), int(res.n_voxels),
                                 int(res.n_sorted), int(res.sort_passes))
+
+
+class GridGraph:
+    """A first-pick grid batch captured into a CUDA graph (xgs_grid_sample with
+    XGS_GRID_ASYNC): :meth:`replay` re-runs the whole batch -- front end, table
+    scan + map test, pid list, emit -- with one graph launch and no host sync,
+    on the same device buffers (write the next batch into :attr:`depth`,
+    :attr:`R`, :attr:`T`, :attr:`color`, :attr:`features`); :meth:`result`
+    synchronises and returns it as a :class:`GridSampleResult`.
+
+    Building it runs the given batch once synchronously through
+    :meth:`GridSampler.sample` (that call sizes the library's per-device state
+    the asynchronous call needs; its voxels enter the map as usual) and keeps
+    that result as :attr:`first`.  The map must keep its capacity afterwards:
+    the asynchronous call does not grow it (``VoxelHashSet`` sized for the
+    stream, as PerceiverStream does)."""
+
+    def __init__(self, sampler: "GridSampler", depth, poses, color=None, features=None):
+        t = nat.require_cuda()
+        if sampler.mode != "first":
+            raise InvalidInputError("graph capture supports first-pick sampling only")
+        self.sampler = sampler
+        d = _dev(depth, t.float32)
+        d = d.unsqueeze(0) if d.dim() == 2 else d
+        F, H, W = (int(v) for v in d.shape)
+        R, tr = _poses(poses, F)
+        self.depth, self.R, self.T = d.clone(), R.clone(), tr.clone()
+        self.color = _dev(color, t.uint8).reshape(F, H, W, 3).clone() if color is not None else None
+        self.features = _dev(features, t.float32).clone() if features is not None else None
+        self.first = sampler.sample(self.depth, (self.R, self.T), self.color, features=self.features)
+        s = sampler.stride
+        self.cap = cap = max(1, F * ((H + s - 1) // s) * ((W + s - 1) // s))
+        C = int(self.features.shape[1]) if self.features is not None else 0
+        self.flat = t.empty(11 * cap, dtype=t.float64, device="cuda")
+        self.ofeat = t.empty((cap, C), dtype=t.float32, device="cuda") if C else None
+        self.dev_status = t.zeros(4, dtype=t.int64, device="cuda")
+        self.ws = nat.workspace(f"grid_graph_{id(self)}", _grid_ws_bytes(F * H * W))
+        fx, fy, cx, cy = sampler.intr
+        ft = self.features
+        self._fr = nat.GridFrames(F, H, W, self.depth.data_ptr(),
+                                  self.color.data_ptr() if self.color is not None else None, self.R.data_ptr(),
+                                  self.T.data_ptr(), fx, fy, cx, cy, sampler.voxel, s, 0, sampler.min_scale,
+                                  ft.data_ptr() if ft is not None else None, C,
+                                  int(ft.shape[2]) if ft is not None else 0, int(ft.shape[3]) if ft is not None else 0,
+                                  nat.GRID_ASYNC)
+        b = self.flat.data_ptr()
+        self._res = nat.GridResult(cap, b, b + 8 * cap, b + 16 * cap, b + 40 * cap, b + 64 * cap, b + 72 * cap,
+                                   self.ofeat.data_ptr() if self.ofeat is not None else None, b + 80 * cap, 0, 0, 0,
+                                   0, 0, nat.F32, self.dev_status.data_ptr())
+        g = t.cuda.CUDAGraph()
+        st = t.cuda.Stream()
+        st.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(st):
+            with t.cuda.graph(g, stream=st):
+                nat.call("xgs_grid_sample", ctypes.byref(self._fr), sampler.occupied._h, ctypes.byref(self._res),
+                         nat.ptr(self.ws), self.ws.numel(), nat.stream_ptr())
+        t.cuda.current_stream().wait_stream(st)
+        self.graph = g
+
+    def replay(self):
+        """Enqueue the batch on the current stream (no host sync)."""
+        self.graph.replay()
+
+    def result(self) -> GridSampleResult:
+        """Synchronise and return the last replayed batch (views of the graph's
+        output buffers: valid until the next replay)."""
+        n_new, n_valid, n_vox, err = (int(v) for v in self.dev_status.cpu())
+        if err:
+            raise InvalidStateError(f"grid batch overflow (code {err}): the map set or batch table is full")
+        return GridSampleResult(self.flat, self.cap, n_new, self.ofeat, n_valid, n_vox)
 
 
 def radix_sort_pairs(keys, vals, bits: int = 64):

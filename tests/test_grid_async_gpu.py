@@ -83,3 +83,66 @@ def test_async_matches_sync(cuda):
         assert err == 0 and n_new == len(rr["pid"]) and n_valid == rr["n_valid"] and n_vox == rr["n_voxels"]
         assert np.array_equal(flat[cap:cap + n_new].view(torch.int64).cpu().numpy(), rr["pid"])
         assert np.array_equal(flat[2 * cap:2 * cap + 3 * n_new].cpu().numpy().reshape(-1, 3), rr["mu"])
+
+
+def test_grid_graph_replays_match_sync_and_snapshot_restore(cuda):
+    """GridGraph: batches written into the graph's buffers and replayed give
+    the synchronous sampler's outputs (keys, pids, mu, colour, scale, depth,
+    features) on a twin map; VoxelHashSet.copy_from restores a map snapshot,
+    after which a replay reproduces the same batch exactly."""
+    import torch
+
+    from paper_2603_09632_b200 import synth
+    from paper_2603_09632_b200.grid import GridGraph, GridSampler, VoxelHashSet
+    rng = np.random.default_rng(11)
+    H, W, F = 48, 128, 2
+    intr4 = (0.8 * W, 0.8 * W, (H - 1) / 2, (W - 1) / 2)
+    planes = synth.random_planes(rng, 5, spread=3.0)
+    poses = synth.circle_trajectory(3 * F, radius=2.0, step_deg=5.0)
+    D = np.empty((3 * F, H, W), np.float32)
+    C = np.empty((3 * F, H, W, 3), np.uint8)
+    for i, p in enumerate(poses):
+        D[i], C[i] = synth.rgbd_frame(rng, p, intr4, H, W, planes=planes, noise=0.003, zero_frac=0.05)
+    R = np.stack([p.rotation for p in poses])
+    T = np.stack([p.translation for p in poses])
+    P = rng.normal(size=(3 * F, 6, 6, 16)).astype(np.float32)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    batch = lambda b: (dev(D[b * F:(b + 1) * F]), (dev(R[b * F:(b + 1) * F]), dev(T[b * F:(b + 1) * F])),
+                       dev(C[b * F:(b + 1) * F]), dev(P[b * F:(b + 1) * F]))
+    ref_gs = GridSampler(intr4, 0.03, occupied=VoxelHashSet(1 << 16))
+    gr_gs = GridSampler(intr4, 0.03, occupied=VoxelHashSet(1 << 16))
+    d0, p0, c0, f0 = batch(0)
+    gg = GridGraph(gr_gs, d0, p0, c0, f0)
+    r0 = ref_gs.sample(d0, p0, c0, features=f0).to_numpy()
+    g0 = gg.first.to_numpy()
+    assert np.array_equal(r0["key"], g0["key"]) and len(r0["key"]) > 0
+    snap = VoxelHashSet(1 << 16)
+    snap.copy_from(gr_gs.occupied)                      # map after batch 0
+    outs = []
+    for b in (1, 2):
+        d, (Rb, Tb), c, f = batch(b)
+        gg.depth.copy_(d)
+        gg.R.copy_(Rb.reshape(-1, 9))
+        gg.T.copy_(Tb)
+        gg.color.copy_(c)
+        gg.features.copy_(f)
+        gg.replay()
+        got = gg.result().to_numpy()
+        ref = ref_gs.sample(d, (Rb, Tb), c, features=f).to_numpy()
+        assert got["n_valid"] == ref["n_valid"] and got["n_voxels"] == ref["n_voxels"]
+        for name in ("key", "pid", "mu", "color", "scale", "depth", "feature"):
+            assert np.array_equal(got[name], ref[name]), (b, name)
+        outs.append(got)
+    # restore the map as it was after batch 0 and replay batch 2 as if batch 1 never happened
+    gr_gs.occupied.copy_from(snap)
+    gg.replay()
+    again = gg.result().to_numpy()
+    twin = GridSampler(intr4, 0.03, occupied=VoxelHashSet(1 << 16))
+    twin.occupied.copy_from(snap)
+    d, (Rb, Tb), c, f = batch(2)
+    ref2 = twin.sample(d, (Rb, Tb), c, features=f).to_numpy()
+    assert len(again["key"]) >= len(outs[1]["key"])
+    for name in ("key", "pid", "mu", "feature"):
+        assert np.array_equal(again[name], ref2[name]), name
+    with pytest.raises(Exception):
+        VoxelHashSet(1 << 20).copy_from(snap)            # capacities differ

@@ -15,6 +15,6 @@ for v, g in out.items():
         continue
     print(v, json.dumps({k: g[k] for k in ("Mpts_per_s", "ms_per_batch", "ms_per_batch_python_call",
                                             "ms_per_batch_events", "items_inserted", "batch_voxels", "new_voxels",
-                                            "rejected_frac", "map_voxels_before", "map_scene_voxels",
+                                            "rejected_frac", "map_voxels_before", "map_scene_voxels", "graph",
                                             "map_warm_frames", "per_stage_ms", "batch_hbm_frac")}),
           "front_frac", g["roofline"]["frac"])
