@@ -380,7 +380,7 @@ __device__ __forceinline__ void dd_insert_finish(unsigned long long* slots, uint
 // floor_div), bit-identical to the reference.
 constexpr int FK_ROWS = 6;
 constexpr int kInsILP = 4;   // table loads in flight per lane in FRONT_INSERT's tail (8: spills, 0.213 vs 0.199 ms)
-constexpr int kFrontPend = 1024;   // per-block queue of pixels for the exact path
+constexpr int kFrontPend = 256;    // per-block queue of pixels for the exact path (overflow: segment scan)
 // thread t covers columns 4t..4t+3 (W <= 4 * kFrontMaxThreads)
 constexpr int kFrontMaxThreads = 320;
 constexpr int kFrontWarps = kFrontMaxThreads / 32;
@@ -448,7 +448,8 @@ __global__ void __launch_bounds__(kFrontMaxThreads, kFrontBlocksPerSM)
 grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int stride, const double* __restrict__ rot,
                   const double* __restrict__ trans, Cam cam, CamF cf, uint64_t* __restrict__ kout,
                   uint32_t* __restrict__ vout, int* bbox, unsigned long long* cnts, int32_t* __restrict__ block_count,
-                  unsigned bid0, unsigned long long* __restrict__ slots, uint64_t mask, int* overflow, int diag) {
+                  unsigned bid0, unsigned long long* __restrict__ slots, uint64_t mask, int* overflow, int diag,
+                  bool halo, int csplit) {
   constexpr bool BOX = MODE == FRONT_SORT;
   constexpr int NR = FK_ROWS;
   constexpr float XB = 9437184.f;   // 2^23 + 2^20
@@ -469,9 +470,13 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
   uint64_t* sk = reinterpret_cast<uint64_t*>(front_smem);                         // nseg * 128 keys
   uint8_t* sc = front_smem + (size_t)nseg * kFrontSeg * 8;                          // nseg * 128 columns
   const unsigned bid = bid0 + blockIdx.x;   // bid0: first block of this launch (frame-chunked launches)
+  // csplit blocks side by side per row band (FRONT_INSERT): each covers
+  // blockDim.x * 4 columns from colbase; shorter blocks shorten the last wave
+  const unsigned bb = bid / (unsigned)csplit;
+  const uint32_t colbase = (bid % (unsigned)csplit) * blockDim.x * 4;
   const int rbf = (int)((H + NR - 1) / NR);   // row blocks per frame
-  const int f = (int)(bid / (unsigned)rbf);
-  const int r0 = (int)(bid % (unsigned)rbf) * NR;
+  const int f = (int)(bb / (unsigned)rbf);
+  const int r0 = (int)(bb % (unsigned)rbf) * NR;
   const int nr = (int)min((int64_t)NR, H - r0);
   const double* Rd = rot + (size_t)f * 9;
   const double* Td = trans + (size_t)f * 3;
@@ -516,7 +521,7 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
   }
   __syncthreads();
   const uint32_t Wu = (uint32_t)W, su = (uint32_t)stride;
-  const uint32_t c0 = (uint32_t)t * 4;
+  const uint32_t c0 = colbase + (uint32_t)t * 4;
   unsigned colmask = 0;
   // column parts: P_col_i = R1_i / voxel * cv (fused into the row part per pixel), C_col = max_i |R1_i| / voxel * bv
   float cv[4], Cc[4];
@@ -535,21 +540,25 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
   const float4* dframe = reinterpret_cast<const float4*>(depth + (size_t)f * H * W);
   const uint32_t w4 = Wu >> 2;
   unsigned cnt = 0;
-  uint64_t kp[4];   // previous row's keys (the halo row first)
+  // previous row's keys: the halo row's (rr = 0) when it is keyed, else none --
+  // without the halo (halo == false, or the frame's first row) the block's first
+  // row is deduplicated within the row only (more table inserts, one row fewer keyed)
+  uint64_t kp[4] = {KEY_INVALID, KEY_INVALID, KEY_INVALID, KEY_INVALID};
+  const int rr0 = (r0 > 0 && halo) ? 0 : 1;
   float4 dn = make_float4(0.f, 0.f, 0.f, 0.f), dn2 = dn;
   // row pointer stepped by one row per iteration (no per-row 64-bit index math);
   // two rows in flight ahead of the one being keyed
-  const float4* dptr = dframe + (size_t)(r0 > 0 ? r0 - 1 : 0) * w4 + t;
+  const float4* dptr = dframe + (size_t)(r0 - 1 + rr0) * w4 + colbase / 4 + t;
   if (colmask) {
-    if (r0 > 0) {
-      dn = __ldg(dptr);
+    dn = __ldg(dptr);
+    dptr += w4;
+    if (rr0 + 1 <= nr) {
+      dn2 = __ldg(dptr);
       dptr += w4;
     }
-    dn2 = __ldg(dptr);
-    dptr += w4;
   }
 #pragma unroll 1
-  for (int rr = 0; rr <= nr; rr++) {
+  for (int rr = rr0; rr <= nr; rr++) {
     const int r = r0 - 1 + rr;
     const float4 d4 = dn;
     dn = dn2;
@@ -670,7 +679,7 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
   const uint32_t fbase = (uint32_t)((size_t)f * H * W);
   auto resolve = [&](uint32_t o) {
     const int seg = (int)(o / kFrontSeg);
-    const uint32_t u = (uint32_t)(r0 + seg / nw), v = (uint32_t)(seg % nw) * kFrontSeg + sc[o];
+    const uint32_t u = (uint32_t)(r0 + seg / nw), v = colbase + (uint32_t)(seg % nw) * kFrontSeg + sc[o];
     const uint64_t key = key_exact(Rd, Td, cam, u, v, depth[fbase + u * Wu + v]);
     sk[o] = key;
     cnt += key != KEY_INVALID ? 1u : 0u;
@@ -697,7 +706,7 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
       tot += segc[rr];
     }
     int ovf = 0;
-    const uint32_t pcol = fbase + (uint32_t)warp * kFrontSeg;
+    const uint32_t pcol = fbase + colbase + (uint32_t)warp * kFrontSeg;
     for (uint32_t q0 = lane; q0 < tot; q0 += kInsILP * 32) {
       uint64_t key[kInsILP], h[kInsILP];
       uint32_t pid[kInsILP];
@@ -2181,20 +2190,27 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
       {
         ProfScope prof("grid_keys", s);
         if (front_ok) {
-          const unsigned nt = (unsigned)((in.W / 4 + 31) / 32 * 32);
-          const size_t fsmem = front_smem_bytes(nt / 32);
           const int64_t rbf = (in.H + FK_ROWS - 1) / FK_ROWS;
           const char* dg = std::getenv("XGS_GRID_DIAG");
           // neighbour dedup: 0 left/up, 1 + diagonals, 2 (default) + two columns away
           // (C3 1 cm: 2.82M -> 1.92M table inserts, front end 143.4 -> 139.8 us)
           const int diag = dg ? (dg[0] == '0' ? 0 : dg[0] == '1' ? 1 : 2) : 2;
+          const char* hl = std::getenv("XGS_GRID_HALO");
+          const bool halo = !(hl && hl[0] == '0');
+          // two half-row blocks per band when rows are wide (W > 512): the blocks'
+          // lifetime halves, and so does the partial last wave
+          const char* cs = std::getenv("XGS_GRID_CSPLIT");
+          int csplit = cs ? std::atoi(cs) : (in.W > 512 && in.W % 8 == 0 ? 2 : 1);
+          if (csplit < 1 || in.W / 4 / csplit < 32) csplit = 1;
+          const unsigned ntc = (unsigned)((in.W / 4 + 32 * csplit - 1) / (32 * csplit) * 32);
           for (int c = 0; c < nchunk; c++) {
             const int64_t f0 = c * fper, f1 = f0 + fper < in.frames ? f0 + fper : in.frames;
             if (f1 <= f0) break;
             if (host_frames && attempt == 0 && (e = cudaStreamWaitEvent(s, hcp->chunk[c], 0)) != cudaSuccess) return e;
-            grid_front_kernel<FRONT_INSERT><<<(unsigned)((f1 - f0) * rbf), nt, fsmem, s>>>(
+            grid_front_kernel<FRONT_INSERT><<<(unsigned)((f1 - f0) * rbf * csplit), ntc,
+                                              front_smem_bytes(ntc / 32), s>>>(
                 in.depth, in.H, in.W, in.stride, in.rot, in.trans, cam, cf, nullptr, nullptr, bbox, cnts, nullptr,
-                (unsigned)(f0 * rbf), st->slots, mask, overflow, diag);
+                (unsigned)(f0 * rbf * csplit), st->slots, mask, overflow, diag, halo, csplit);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
             count_launches(1);
           }
@@ -2267,7 +2283,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
           if (host_frames && (e = cudaStreamWaitEvent(s, hcp->chunk[c], 0)) != cudaSuccess) return e;
           grid_front_kernel<FRONT_SORT><<<(unsigned)((f1 - f0) * rbf), nt, fsmem, s>>>(
               in.depth, in.H, in.W, in.stride, in.rot, in.trans, cam, cf, k0, v0, bbox, cnts, block_count,
-              (unsigned)(f0 * rbf), nullptr, 0, nullptr, 1);
+              (unsigned)(f0 * rbf), nullptr, 0, nullptr, 1, true, 1);
           count_launches(1);
         }
       } else {
