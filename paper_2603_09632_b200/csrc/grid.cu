@@ -1764,10 +1764,11 @@ constexpr int kLbThreads = 256, kLbWords = 8, kLbTile = kLbThreads * kLbWords, k
 __global__ void __launch_bounds__(kLbThreads)
 grid_pidlist_lb_kernel(unsigned* __restrict__ flag_bits, int64_t nwords, unsigned long long* lb_status,
                        unsigned long long* cnts, int64_t capacity, int64_t* __restrict__ pid_out,
-                       int32_t* grand, volatile unsigned long long* host_status, int64_t* dev_status) {
+                       int32_t* grand, volatile unsigned long long* host_status, int64_t* dev_status, EmitArgs ea,
+                       bool fuse) {
   __shared__ unsigned s_tile;
   __shared__ uint32_t s_wsum[kLbThreads / 32];
-  __shared__ uint32_t s_base;
+  __shared__ uint32_t s_base, s_agg;
   pdl_wait();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   if (t == 0) s_tile = atomicAdd(reinterpret_cast<unsigned*>(cnts + 6), 1u);
@@ -1862,6 +1863,7 @@ grid_pidlist_lb_kernel(unsigned* __restrict__ flag_bits, int64_t nwords, unsigne
     }
     if (lane == 0) {
       s_base = (uint32_t)excl;
+      s_agg = agg;
       if (tile == ntiles - 1) {
         const unsigned long long total = excl + agg;
         *grand = (int32_t)total;
@@ -1892,6 +1894,13 @@ grid_pidlist_lb_kernel(unsigned* __restrict__ flag_bits, int64_t nwords, unsigne
       if (o < capacity) pid_out[o] = (w0 + j) * 32 + b;
       o++;
     }
+  }
+  if (fuse) {
+    // first-pick emission of this tile's new voxels, spread over the block's
+    // threads (the pid list entries the block just wrote): no separate emit launch
+    __syncthreads();
+    const int64_t beg = s_base, end = min((int64_t)s_base + (int64_t)s_agg, capacity);
+    for (int64_t oo = beg + t; oo < end; oo += kLbThreads) emit_one(oo, pid_out[oo], nullptr, ea);
   }
 }
 
@@ -2046,12 +2055,6 @@ cudaError_t emit_outputs(const GridIn& in, const Cam& cam, DedupTable* st, const
   const int64_t lb_tiles = (nwords + kLbTile - 1) / kLbTile;
   unsigned long long* cnts = reinterpret_cast<unsigned long long*>(st->misc + 64);
   int32_t* grand = reinterpret_cast<int32_t*>(st->misc + 128);
-  if ((e = launch_pdl(grid_pidlist_lb_kernel, dim3((unsigned)lb_tiles), dim3(kLbThreads), 0, s, st->flags, nwords,
-                      st->lb, cnts, (int64_t)out.capacity, out.pid, grand, st->host_st_dev,
-                      out.dev_status)) != cudaSuccess)
-    return e;
-  count_launches(1);
-  if (hcp && (e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;   // colour
   EmitArgs ea;
   ea.depth = in.depth;
   ea.color = in.color;
@@ -2079,10 +2082,22 @@ cudaError_t emit_outputs(const GridIn& in, const Cam& cam, DedupTable* st, const
   ea.ofeat = out.feat;
   ea.feat64 = out.feat64;
   ea.count = out.count;
-  if ((e = launch_pdl(grid_emit_kernel, dim3(grid_blocks(out.capacity, 128, sms)), dim3(128), 0, s, head,
-                      (const int32_t*)grand, (int64_t)out.capacity, ea)) != cudaSuccess)
+  // first-pick: the pid-list kernel emits each tile's voxels itself (the colour
+  // copy of a host-frame batch is waited for first); mean mode: separate emit
+  const bool fuse = in.mode == 0;
+  if (fuse && hcp && (e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;   // colour
+  if ((e = launch_pdl(grid_pidlist_lb_kernel, dim3((unsigned)lb_tiles), dim3(kLbThreads), 0, s, st->flags, nwords,
+                      st->lb, cnts, (int64_t)out.capacity, out.pid, grand, st->host_st_dev, out.dev_status, ea,
+                      fuse)) != cudaSuccess)
     return e;
   count_launches(1);
+  if (!fuse) {
+    if (hcp && (e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;   // colour
+    if ((e = launch_pdl(grid_emit_kernel, dim3(grid_blocks(out.capacity, 128, sms)), dim3(128), 0, s, head,
+                        (const int32_t*)grand, (int64_t)out.capacity, ea)) != cudaSuccess)
+      return e;
+    count_launches(1);
+  }
   if (in.feat) {
     if ((e = launch_pdl(grid_emit_feat_kernel, dim3(grid_blocks(out.capacity * in.fc, 256, sms)), dim3(256), 0, s,
                         head, (const int32_t*)grand, (int64_t)out.capacity, ea)) != cudaSuccess)
