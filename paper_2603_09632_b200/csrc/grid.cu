@@ -443,6 +443,12 @@ constexpr float kDl = 0x1p-20f * 1.002f + 0x1p-21f;
 
 enum FrontMode : int { FRONT_SORT = 1, FRONT_INSERT = 2 };
 
+// the front end's pre-key -> the packed voxel key (see the keying loop)
+__device__ __forceinline__ uint64_t pre_to_key(uint64_t k) {
+  const uint32_t lo = (uint32_t)k - 0x4B000000u, hi = (uint32_t)(k >> 32) - 0x96000u;
+  return ((uint64_t)hi << 32) | lo;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kFrontMaxThreads, kFrontBlocksPerSM)
 grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int stride, const double* __restrict__ rot,
@@ -592,9 +598,13 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
         const float lo = fminf(fminf(f0, f1), f2v), hi = fmaxf(fmaxf(f0, f1), f2v);
         const bool valid = ((rowmask >> j) & 1u) && dv[j] > 0.f;
         const bool ok = lane_of(M, h) < 1048000.f && lo > lane_of(dl, h) && hi < lane_of(omd, h);
-        const uint32_t b0 = __float_as_uint(lane_of(x0, h)) & 0x1fffffu, b1 = __float_as_uint(lane_of(x1, h)) & 0x1fffffu,
-                       b2 = __float_as_uint(lane_of(x2, h)) & 0x1fffffu;
-        const uint64_t key = ((uint64_t)((b0 << 10) | (b1 >> 11)) << 32) | (uint64_t)((b1 << 21) | b2);
+        // pre-key: the key packing without masking the constant exponent bits
+        // of x = b + 2^23 + 2^20 (bits(x) = 0x4B000000 + b): lo = key_lo +
+        // 0x4B000000, hi = key_hi + 0x96000 (each mod 2^32) -- injective, so
+        // the neighbour dedup compares pre-keys; staging converts (pre_to_key)
+        const uint32_t u0 = __float_as_uint(lane_of(x0, h)), u1 = __float_as_uint(lane_of(x1, h)),
+                       u2 = __float_as_uint(lane_of(x2, h));
+        const uint64_t key = ((uint64_t)(u0 * 1024u + (u1 >> 11)) << 32) | (uint64_t)(u1 * 0x200000u + u2);
         k[j] = !valid ? KEY_INVALID : ok ? key : PEND;
         cnt += (valid && ok && rr > 0) ? 1u : 0u;
       }
@@ -654,7 +664,7 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
       for (int j = 0; j < 4; j++) {
         const uint32_t o = o0 + __popc(keep & ((1u << j) - 1u));
         if ((keep >> j) & 1u) {   // predicated stores
-          sk[o] = k[j];
+          sk[o] = k[j] == PEND ? PEND : pre_to_key(k[j]);
           sc[o] = (uint8_t)(lane * 4 + j);
         }
         pend |= (((keep >> j) & 1u) && k[j] == PEND) ? 1u << j : 0u;
