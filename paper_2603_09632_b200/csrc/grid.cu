@@ -2226,7 +2226,9 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
           // two half-row blocks per band when rows are wide (W > 512): the blocks'
           // lifetime halves, and so does the partial last wave
           const char* cs = std::getenv("XGS_GRID_CSPLIT");
-          int csplit = cs ? std::atoi(cs) : (in.W > 512 && in.W % 8 == 0 ? 2 : 1);
+          // (only when the halves are whole warps: W = 640 would leave a 3-warp block one
+          // third idle)
+          int csplit = cs ? std::atoi(cs) : (in.W > 512 && in.W % 256 == 0 ? 2 : 1);
           if (csplit < 1 || in.W / 4 / csplit < 32) csplit = 1;
           const unsigned ntc = (unsigned)((in.W / 4 + 32 * csplit - 1) / (32 * csplit) * 32);
           for (int c = 0; c < nchunk; c++) {
