@@ -356,6 +356,8 @@ def run_grid(torch, steps, cpu=True):
                          "achieved": front_bytes / (t_front * 1e-3) / 1e9, "peak": pk_["hbm_gbs"], "unit": "GB/s",
                          "frac": front_bytes / (t_front * 1e-3) / 1e9 / pk_["hbm_gbs"],
                          "algorithmic_bytes": front_bytes,
+                         "traffic": (ncu_traffic("grid_front_kernel_C3_1cm") if voxel == 0.01 else None),
+                         "issue": grid_issue_roofline(),
                          "note": "issue/L2-latency bound: fp32 key filter + ballot staging per pixel, one random "
                                  "L2 sector per inserted item (tools/micro/insert_bench.cu: ~35 us floor for 4.4M "
                                  "probes even read-only)"},
@@ -975,6 +977,23 @@ def profiled_steps(torch, vq, x, sizes, steps):
                                                "vq_ema")}
     nat.profile_enable(False)
     return prof
+
+
+def grid_issue_roofline():
+    """The grid front end is issue-bound, not HBM-bound: its instruction rate
+    against the SM issue peak (4 warp instructions per SM per cycle at the max
+    SM clock), from the committed ncu capture (profiles/ncu_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            v = json.load(f).get("grid_front_kernel_C3_1cm")
+    except (OSError, ValueError):
+        return None
+    if not isinstance(v, dict):
+        return None
+    ach = v["warp_instructions"] / (v["duration_us"] * 1e-6)
+    return {"achieved": ach, "peak": v["sm_issue_peak_warp_inst_per_s"], "unit": "warp inst/s",
+            "frac": ach / v["sm_issue_peak_warp_inst_per_s"], "issue_active_pct": v["issue_active_pct"],
+            "source": v["source"]}
 
 
 def ncu_traffic(key):
