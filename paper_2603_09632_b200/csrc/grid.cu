@@ -384,6 +384,7 @@ constexpr int kFrontPend = 256;    // per-block queue of pixels for the exact pa
 // thread t covers columns 4t..4t+3 (W <= 4 * kFrontMaxThreads)
 constexpr int kFrontMaxThreads = 320;
 constexpr int kFrontWarps = kFrontMaxThreads / 32;
+constexpr int kPendW = kFrontPend / kFrontWarps;   // FRONT_INSERT: per-warp share of that queue
 constexpr int kFrontBlocksPerSM = FK_ROWS <= 6 ? 3 : 2;   // bounded by the staged segments (FK_ROWS * 11.5 KB)
 constexpr int kFrontSeg = 128;     // items per (row, warp) segment: the warp's columns
 // staged bytes per segment item: 8 (key) + 1 (column inside the warp's span)
@@ -546,6 +547,7 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
   const float4* dframe = reinterpret_cast<const float4*>(depth + (size_t)f * H * W);
   const uint32_t w4 = Wu >> 2;
   unsigned cnt = 0;
+  uint32_t wpend = 0;   // FRONT_INSERT: this warp's queued pending pixels (warp-uniform)
   // previous row's keys: the halo row's (rr = 0) when it is keyed, else none --
   // without the halo (halo == false, or the frame's first row) the block's first
   // row is deduplicated within the row only (more table inserts, one row fewer keyed)
@@ -670,21 +672,30 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
         pend |= (((keep >> j) & 1u) && k[j] == PEND) ? 1u << j : 0u;
       }
       if (__any_sync(FULL, pend)) {   // rare: queue the undecided pixels for the exact path
+        if constexpr (MODE == FRONT_INSERT) {
+          // the warp's own queue (no block barrier before the inserts)
 #pragma unroll
-        for (int j = 0; j < 4; j++)
-          if ((pend >> j) & 1u) {
-            const uint32_t pi = atomicAdd(&s_npend, 1u);
-            if (pi < kFrontPend) s_pend[pi] = o0 + __popc(keep & ((1u << j) - 1u));
+          for (int j = 0; j < 4; j++) {
+            const unsigned b = __ballot_sync(FULL, (pend >> j) & 1u);
+            const uint32_t pi = wpend + __popc(b & lt);
+            if (((pend >> j) & 1u) && pi < (uint32_t)kPendW)
+              s_pend[warp * kPendW + pi] = o0 + __popc(keep & ((1u << j) - 1u));
+            wpend += __popc(b);
           }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; j++)
+            if ((pend >> j) & 1u) {
+              const uint32_t pi = atomicAdd(&s_npend, 1u);
+              if (pi < kFrontPend) s_pend[pi] = o0 + __popc(keep & ((1u << j) - 1u));
+            }
+        }
       }
       if (lane == 0) s_cnt[seg] = total;
     }
 #pragma unroll
     for (int j = 0; j < 4; j++) kp[j] = k[j];
   }
-  // rows past the frame's last row: empty segments
-  for (int s = nr * nw + t; s < nseg; s += blockDim.x) s_cnt[s] = 0;
-  __syncthreads();
   // ---- exact fp64 keys of the pending pixels, one lane each ----
   const uint32_t fbase = (uint32_t)((size_t)f * H * W);
   auto resolve = [&](uint32_t o) {
@@ -694,6 +705,26 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
     sk[o] = key;
     cnt += key != KEY_INVALID ? 1u : 0u;
   };
+  if constexpr (MODE == FRONT_INSERT) {
+    // each warp resolves its own pending pixels (its queue, or on overflow a
+    // scan of its own segments) -- no block barrier
+    __syncwarp();
+    if (wpend <= (uint32_t)kPendW) {
+      for (uint32_t i = lane; i < wpend; i += 32) resolve(s_pend[warp * kPendW + i]);
+    } else {
+      for (int rr = 0; rr < nr; rr++) {
+        const int sg = rr * nw + warp;
+        for (uint32_t i = lane; i < s_cnt[sg]; i += 32) {
+          const uint32_t o = (uint32_t)sg * kFrontSeg + i;
+          if (sk[o] == PEND) resolve(o);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+  // rows past the frame's last row: empty segments
+  for (int s = nr * nw + t; s < nseg; s += blockDim.x) s_cnt[s] = 0;
+  __syncthreads();
   {
     const uint32_t np = s_npend;
     if (np <= (uint32_t)kFrontPend) {
@@ -706,9 +737,9 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
         }
     }
   }
+  }
   if (MODE == FRONT_INSERT) {
     // ---- this warp's segments (rows rr, warp) into the batch table ----
-    __syncthreads();   // pending keys resolved by any thread
     uint32_t segc[NR], tot = 0;
 #pragma unroll
     for (int rr = 0; rr < NR; rr++) {
