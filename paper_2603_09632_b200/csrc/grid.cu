@@ -2125,8 +2125,10 @@ cudaError_t emit_outputs(const GridIn& in, const Cam& cam, DedupTable* st, const
   ea.count = out.count;
   // first-pick: the pid-list kernel emits each tile's voxels itself (the colour
   // copy of a host-frame batch is waited for first); mean mode: separate emit
+  // (only with at least one look-back tile per SM: a small frame has a few
+  // 65K-pixel tiles, whose blocks would emit every voxel between them)
   const char* fe = std::getenv("XGS_GRID_FUSE_EMIT");
-  const bool fuse = in.mode == 0 && !(fe && fe[0] == '0');
+  const bool fuse = in.mode == 0 && !(fe && fe[0] == '0') && (lb_tiles >= sms || (fe && fe[0] == '1'));
   if (fuse && hcp && (e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;   // colour
   if ((e = launch_pdl(grid_pidlist_lb_kernel, dim3((unsigned)lb_tiles), dim3(kLbThreads), 0, s, st->flags, nwords,
                       st->lb, cnts, (int64_t)out.capacity, out.pid, grand, st->host_st_dev, out.dev_status, ea,
