@@ -450,13 +450,14 @@ __device__ __forceinline__ uint64_t pre_to_key(uint64_t k) {
   return ((uint64_t)hi << 32) | lo;
 }
 
-template <int MODE>
+template <int MODE, int DIAG>
 __global__ void __launch_bounds__(kFrontMaxThreads, kFrontBlocksPerSM)
 grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int stride, const double* __restrict__ rot,
                   const double* __restrict__ trans, Cam cam, CamF cf, uint64_t* __restrict__ kout,
                   uint32_t* __restrict__ vout, int* bbox, unsigned long long* cnts, int32_t* __restrict__ block_count,
-                  unsigned bid0, unsigned long long* __restrict__ slots, uint64_t mask, int* overflow, int diag,
+                  unsigned bid0, unsigned long long* __restrict__ slots, uint64_t mask, int* overflow,
                   bool halo, int csplit) {
+  constexpr int diag = DIAG;   // neighbour dedup width (compile time: no per-pixel predicates)
   constexpr bool BOX = MODE == FRONT_SORT;
   constexpr int NR = FK_ROWS;
   constexpr float XB = 9437184.f;   // 2^23 + 2^20
@@ -1137,10 +1138,14 @@ bool sort_forced() {
 cudaError_t front_init() {
   return attr_once(kAttrGridFront, [] {
     const int bytes = (int)front_smem_bytes(kFrontWarps);
-    cudaError_t e = cudaFuncSetAttribute(grid_front_kernel<FRONT_SORT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(grid_front_kernel<FRONT_SORT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          bytes);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(grid_front_kernel<FRONT_INSERT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      e = cudaFuncSetAttribute(grid_front_kernel<FRONT_INSERT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(grid_front_kernel<FRONT_INSERT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(grid_front_kernel<FRONT_INSERT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     return e;
   });
 }
@@ -2268,10 +2273,11 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
             const int64_t f0 = c * fper, f1 = f0 + fper < in.frames ? f0 + fper : in.frames;
             if (f1 <= f0) break;
             if (host_frames && attempt == 0 && (e = cudaStreamWaitEvent(s, hcp->chunk[c], 0)) != cudaSuccess) return e;
-            grid_front_kernel<FRONT_INSERT><<<(unsigned)((f1 - f0) * rbf * csplit), ntc,
-                                              front_smem_bytes(ntc / 32), s>>>(
+            auto kern = diag == 0 ? grid_front_kernel<FRONT_INSERT, 0>
+                                  : diag == 1 ? grid_front_kernel<FRONT_INSERT, 1> : grid_front_kernel<FRONT_INSERT, 2>;
+            kern<<<(unsigned)((f1 - f0) * rbf * csplit), ntc, front_smem_bytes(ntc / 32), s>>>(
                 in.depth, in.H, in.W, in.stride, in.rot, in.trans, cam, cf, nullptr, nullptr, bbox, cnts, nullptr,
-                (unsigned)(f0 * rbf * csplit), st->slots, mask, overflow, diag, halo, csplit);
+                (unsigned)(f0 * rbf * csplit), st->slots, mask, overflow, halo, csplit);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
             count_launches(1);
           }
@@ -2342,9 +2348,9 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
           const int64_t f0 = c * fper, f1 = f0 + fper < in.frames ? f0 + fper : in.frames;
           if (f1 <= f0) break;
           if (host_frames && (e = cudaStreamWaitEvent(s, hcp->chunk[c], 0)) != cudaSuccess) return e;
-          grid_front_kernel<FRONT_SORT><<<(unsigned)((f1 - f0) * rbf), nt, fsmem, s>>>(
+          grid_front_kernel<FRONT_SORT, 1><<<(unsigned)((f1 - f0) * rbf), nt, fsmem, s>>>(
               in.depth, in.H, in.W, in.stride, in.rot, in.trans, cam, cf, k0, v0, bbox, cnts, block_count,
-              (unsigned)(f0 * rbf), nullptr, 0, nullptr, 1, true, 1);
+              (unsigned)(f0 * rbf), nullptr, 0, nullptr, true, 1);
           count_launches(1);
         }
       } else {
