@@ -365,7 +365,8 @@ class GridGraph:
         self.flat = t.empty(11 * cap, dtype=t.float64, device="cuda")
         self.ofeat = t.empty((cap, C), dtype=t.float32, device="cuda") if C else None
         self.dev_status = t.zeros(4, dtype=t.int64, device="cuda")
-        self.ws = nat.workspace(f"grid_graph_{id(self)}", _grid_ws_bytes(F * H * W))
+        # the graph holds the workspace's address: owned by this object (freed with it)
+        self.ws = t.empty(max(int(_grid_ws_bytes(F * H * W)), 256), dtype=t.uint8, device="cuda")
         fx, fy, cx, cy = sampler.intr
         ft = self.features
         self._fr = nat.GridFrames(F, H, W, self.depth.data_ptr(),

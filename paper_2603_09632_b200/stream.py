@@ -97,10 +97,13 @@ class PerceiverStream:
         self.host_status = t.empty(4, dtype=t.int64, pin_memory=True)
         self.occupied = VoxelHashSet(map_capacity)
         self.sampler = GridSampler(intrinsics, voxel_size, occupied=self.occupied, min_scale=min_scale)
-        self.ws_grid = nat.workspace("stream_grid", _grid_ws_bytes(self.cap))
+        # the graph holds the workspaces' addresses: owned by this stream (a shared,
+        # grow-only library workspace could be reallocated under the graph)
         L = nat.lib()
-        self.ws_assign = nat.workspace("stream_assign", L.xgs_vq_assign_workspace(self.vcap, self.K, C, nat.F32, C))
-        self.ws_acc = nat.workspace("stream_acc", L.xgs_vq_accumulate_workspace(self.vcap, self.K))
+        ws = lambda n: t.empty(max(int(n), 256), dtype=t.uint8, device=dev)
+        self.ws_grid = ws(_grid_ws_bytes(self.cap))
+        self.ws_assign = ws(L.xgs_vq_assign_workspace(self.vcap, self.K, C, nat.F32, C))
+        self.ws_acc = ws(L.xgs_vq_accumulate_workspace(self.vcap, self.K))
         fx, fy, cx, cy = self.intr
         self._frames = nat.GridFrames(1, self.H, self.W, self.depth.data_ptr(), self.color.data_ptr(),
                                       self.R.data_ptr(), self.T.data_ptr(), fx, fy, cx, cy, self.voxel, 1, 0,

@@ -146,3 +146,37 @@ def test_grid_graph_replays_match_sync_and_snapshot_restore(cuda):
         assert np.array_equal(again[name], ref2[name]), name
     with pytest.raises(Exception):
         VoxelHashSet(1 << 20).copy_from(snap)            # capacities differ
+
+
+def test_grid_graph_survives_state_growth(cuda):
+    """A captured GridGraph keeps working after a much larger synchronous batch
+    grew the library's per-device grid state (outgrown buffers are retired,
+    not freed, once an async call happened)."""
+    import torch
+
+    from paper_2603_09632_b200.grid import GridGraph, GridSampler, VoxelHashSet
+    rng = np.random.default_rng(21)
+    H, W = 48, 64
+    intr = (50.0, 50.0, 23.5, 31.5)
+    R = torch.eye(3, dtype=torch.float64, device="cuda").reshape(1, 9).contiguous()
+    T = torch.zeros(1, 3, dtype=torch.float64, device="cuda")
+    frame = lambda: torch.from_numpy(rng.uniform(0.5, 4.0, (1, H, W)).astype(np.float32)).cuda()
+    gs = GridSampler(intr, 0.03, occupied=VoxelHashSet(1 << 16))
+    twin = GridSampler(intr, 0.03, occupied=VoxelHashSet(1 << 16))
+    d0 = frame()
+    gg = GridGraph(gs, d0, (R, T))
+    twin.sample(d0, (R, T))
+    # a large synchronous batch on another map: ~1.2M distinct 1 mm voxels
+    big = torch.from_numpy(rng.uniform(0.5, 5.0, (4, 480, 640)).astype(np.float32)).cuda()
+    GridSampler((525.0, 525.0, 239.5, 319.5), 0.001, occupied=VoxelHashSet(1 << 22)).sample(
+        big, (torch.eye(3, dtype=torch.float64, device="cuda").reshape(1, 9).repeat(4, 1),
+              torch.zeros(4, 3, dtype=torch.float64, device="cuda")))
+    for _ in range(2):
+        d = frame()
+        gg.depth.copy_(d)
+        gg.replay()
+        got = gg.result().to_numpy()
+        ref = twin.sample(d, (R, T)).to_numpy()
+        assert got["n_voxels"] == ref["n_voxels"] and len(got["key"]) == len(ref["key"])
+        for name in ("key", "pid", "mu", "scale", "depth"):
+            assert np.array_equal(got[name], ref[name]), name
