@@ -214,7 +214,9 @@ XGS_API int xgs_backproject(const double* R, const double* t, const double* intr
                             const double* v, const double* d, int64_t n, double* out, void* stream);
 
 /* GPU hash set of occupied voxel keys (the map).  Opaque handle; open
- * addressing with 64-bit keys, load factor kept <= 1/2 (grows on demand).
+ * addressing with 64-bit keys, load factor kept <= 1/2 (grows on demand --
+ * except after an XGS_GRID_ASYNC call used it: a graph may hold its table, so
+ * a call that would have to grow it returns XGS_NOT_SUPPORTED).
  * insert = insert-if-absent; was_new (nullable) reports keys that were absent. */
 XGS_API int xgs_hashset_create(int64_t capacity, void** handle);
 XGS_API int xgs_hashset_destroy(void* handle);

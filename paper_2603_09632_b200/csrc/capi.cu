@@ -426,6 +426,9 @@ int xgs_hashset_destroy(void* handle) {
 int xgs_hashset_insert(void* handle, const uint64_t* keys, int64_t n, uint8_t* was_new, void* stream) {
   if (!handle || n < 0 || (n > 0 && !keys)) return fail(INVALID_INPUT, "bad hashset insert");
   cudaError_t e = hashset_insert(static_cast<HashSet*>(handle), keys, n, was_new, (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported)
+    return fail(NOT_SUPPORTED, "the map was used by an XGS_GRID_ASYNC call (a CUDA graph may hold its table) and "
+                               "cannot grow");
   if (e != cudaSuccess) return cuda_fail(e, "xgs_hashset_insert");
   return OK;
 }
@@ -526,8 +529,11 @@ static int grid_sample_call(const xgs_grid_frames* in, void* hashset, xgs_grid_r
   go.count = out->count;
   go.dev_status = out->dev_status;
   cudaError_t e = grid_sample(gi, static_cast<HashSet*>(hashset), go, ws, ws_bytes, sm_count(), (cudaStream_t)stream);
-  if (e == cudaErrorNotSupported) return fail(NOT_SUPPORTED, "XGS_GRID_ASYNC needs the library state sized by an "
-                                                "earlier synchronous batch of at least this size");
+  if (e == cudaErrorNotSupported)
+    return fail(NOT_SUPPORTED, gi.async ? "XGS_GRID_ASYNC needs the library state sized by an earlier synchronous "
+                                          "batch of at least this size"
+                                        : "the map was used by an XGS_GRID_ASYNC call (a CUDA graph may hold its "
+                                          "table) and cannot grow: create it with room for the whole stream");
   out->n_new = go.n_new;
   out->n_valid = go.n_valid;
   out->n_voxels = go.n_voxels;

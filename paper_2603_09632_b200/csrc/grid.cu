@@ -1532,6 +1532,7 @@ struct HashSet {
   int64_t cap = 0;
   unsigned long long* count_dev = nullptr;
   int64_t count_ub = 0;   // host upper bound of the key count (no sync needed to size the table)
+  bool pinned = false;    // an XGS_GRID_ASYNC call used it: a graph may hold the table address, never regrow
 };
 
 cudaError_t hashset_create(int64_t capacity, HashSet** out) {
@@ -1576,6 +1577,7 @@ cudaError_t hashset_reserve(HashSet* h, int64_t extra, cudaStream_t s) {
   if ((e = hashset_size(h, &cur, s)) != cudaSuccess) return e;
   h->count_ub = cur;
   if (2 * (cur + extra) <= h->cap) return cudaSuccess;
+  if (h->pinned) return cudaErrorNotSupported;   // a captured graph would keep using the old table
   int64_t cap = h->cap;
   while (2 * (cur + extra) > cap) cap <<= 1;
   unsigned long long* t = nullptr;
@@ -2238,7 +2240,10 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   // order over the voxel's segment)
   const bool hashed = compact && !sort_forced();
   if (in.async && !hashed) return cudaErrorNotSupported;
-  if (in.async) st->pinned = true;   // a graph may capture this call: keep the state's buffers alive
+  if (in.async) {   // a graph may capture this call: keep the state's buffers alive, never regrow the map
+    st->pinned = true;
+    hs->pinned = true;
+  }
   st->dirty = true;
   if (hashed) {
     // ---------------- G1+G2': front end inserting into the batch table, table scan + map test

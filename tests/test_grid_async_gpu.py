@@ -180,3 +180,21 @@ def test_grid_graph_survives_state_growth(cuda):
         assert got["n_voxels"] == ref["n_voxels"] and len(got["key"]) == len(ref["key"])
         for name in ("key", "pid", "mu", "scale", "depth"):
             assert np.array_equal(got[name], ref[name]), name
+
+
+def test_map_captured_by_a_graph_refuses_to_grow(cuda):
+    """After an XGS_GRID_ASYNC call used a map, a call that would have to grow
+    it fails loudly (a captured graph would keep using the old table)."""
+    import torch
+
+    from paper_2603_09632_b200.errors import NativeError
+    from paper_2603_09632_b200.grid import GridGraph, GridSampler, VoxelHashSet
+    rng = np.random.default_rng(5)
+    d = torch.from_numpy(rng.uniform(0.5, 4.0, (1, 48, 64)).astype(np.float32)).cuda()
+    R = torch.eye(3, dtype=torch.float64, device="cuda").reshape(1, 9).contiguous()
+    T = torch.zeros(1, 3, dtype=torch.float64, device="cuda")
+    hs = VoxelHashSet(1 << 13)
+    GridGraph(GridSampler((50.0, 50.0, 23.5, 31.5), 0.03, occupied=hs), d, (R, T))
+    hs.insert(np.arange(1, 1000, dtype=np.uint64))            # fits: fine
+    with pytest.raises(NativeError, match="cannot grow"):
+        hs.insert(np.arange(1, 200_000, dtype=np.uint64))
