@@ -132,6 +132,13 @@ XGS_API int xgs_vq_revive(int64_t k, int64_t d, double eps, const double* ring, 
  * rows [row0, row0+nrows) of x -> ring[(phys0 + j) % cap] as fp64. */
 XGS_API int xgs_vq_ring_write(const void* x, int dtype, int64_t ldx, int64_t row0, int64_t nrows, int64_t d,
                               double* ring, int64_t cap, int64_t phys0, void* stream);
+/* xgs_vq_ring_write with the row count on the device (graph-capturable): rows
+ * [0, min(*n_dev, n_max)) of x are appended to the ring at the device-resident
+ * write position *start_dev, which is then advanced ((start + n) % cap; n >= cap
+ * keeps the last cap rows at ring rows [0, cap) and resets it to 0).  The
+ * caller mirrors the FIFO bookkeeping on the host after reading n. */
+XGS_API int xgs_vq_ring_write_dev(const void* x, int dtype, int64_t ldx, const int64_t* n_dev, int64_t n_max,
+                                  int64_t d, double* ring, int64_t cap, int64_t* start_dev, void* stream);
 XGS_API int xgs_gather_rows_f64(const double* src, int64_t d, const int64_t* rows, int64_t n, double* dst,
                                 void* stream);
 

@@ -51,6 +51,7 @@ SIGNATURES = {
     "xgs_vq_ema": (_i32, [_f64, _f64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "xgs_vq_revive": (_i32, [_i64, _i64, _f64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "xgs_vq_ring_write": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _vp]),
+    "xgs_vq_ring_write_dev": (_i32, [_vp, _i32, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _vp]),
     "xgs_gather_rows_f64": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
     "xgs_backproject": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "xgs_hashset_create": (_i32, [_i64, _vp]),

@@ -80,12 +80,27 @@ class FeatureReservoir:
         start = (self._head + self._len) % cap
         nat.call("xgs_vq_ring_write", nat.ptr(xt), dtype, ldx, 0, n, self.dim, nat.ptr(ring), cap, start,
                  nat.stream_ptr())
+        self._account(n)
+
+    def _account(self, n):
+        """FIFO bookkeeping of an append of n rows (the rows themselves written
+        by the caller, e.g. xgs_vq_ring_write_dev inside a CUDA graph)."""
+        cap = self.capacity
+        if n <= 0:
+            return
+        if n >= cap:
+            self._head, self._len = 0, cap
+            return
         total = self._len + n
         if total > cap:
             self._head = (self._head + total - cap) % cap
             self._len = cap
         else:
             self._len = total
+
+    def _write_pos(self):
+        """Physical ring row of the next append."""
+        return (self._head + self._len) % self.capacity
 
     def extend(self, x) -> None:
         from .vq import _rows

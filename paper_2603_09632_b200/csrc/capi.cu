@@ -348,6 +348,16 @@ int xgs_vq_revive(int64_t k, int64_t d, double eps, const double* ring, int64_t 
   return OK;
 }
 
+int xgs_vq_ring_write_dev(const void* x, int dtype, int64_t ldx, const int64_t* n_dev, int64_t n_max, int64_t d,
+                          double* ring, int64_t cap, int64_t* start_dev, void* stream) {
+  if (!valid_dtype(dtype)) return fail(INVALID_INPUT, "unsupported dtype");
+  if (n_max < 0 || d < 1 || ldx < d || cap < 1) return fail(INVALID_INPUT, "bad ring write shape");
+  if (n_max > 0 && (!x || !n_dev || !ring || !start_dev)) return fail(INVALID_INPUT, "null buffer");
+  cudaError_t e = launch_ring_write_dev(x, dtype, ldx, n_dev, n_max, d, ring, cap, start_dev, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_vq_ring_write_dev");
+  return OK;
+}
+
 int xgs_vq_ring_write(const void* x, int dtype, int64_t ldx, int64_t row0, int64_t nrows, int64_t d,
                       double* ring, int64_t cap, int64_t phys0, void* stream) {
   if (!valid_dtype(dtype) || nrows < 0 || row0 < 0 || cap < 1 || nrows > cap || phys0 < 0 || phys0 >= cap)

@@ -128,6 +128,8 @@ cudaError_t launch_ema(double lam, double one_minus_lam, double eps, int64_t k, 
 cudaError_t launch_revive(int64_t k, int64_t d, double n_new, double denom, const double* ring,
                           int64_t cap, const int64_t* dead_k, const int64_t* ring_rows,
                           int64_t n_dead, double* N, double* M, double* E, cudaStream_t s);
+cudaError_t launch_ring_write_dev(const void* x, int dtype, int64_t ldx, const int64_t* n_dev, int64_t n_max,
+                                  int64_t d, double* ring, int64_t cap, int64_t* start_dev, cudaStream_t s);
 cudaError_t launch_ring_write(const void* x, int dtype, int64_t ldx, int64_t row0, int64_t nrows,
                               int64_t d, double* ring, int64_t cap, int64_t phys0,
                               cudaStream_t s);

@@ -530,6 +530,30 @@ __global__ void ring_write_kernel(const X* __restrict__ x, int64_t ldx, int64_t 
   for (int64_t i = threadIdx.x; i < d; i += blockDim.x) dst[i] = ld64(src, i);
 }
 
+// The same with the row count and the ring's write position on the device
+// (a graph-captured step whose batch size is known only on the device): one
+// block per potential row (n_max), rows >= n exit.  n >= cap keeps the last cap
+// rows at ring rows [0, cap).  ring_advance_kernel then moves the position.
+template <typename X>
+__global__ void ring_write_dev_kernel(const X* __restrict__ x, int64_t ldx, const int64_t* __restrict__ n_dev,
+                                      int64_t n_max, int64_t d, double* ring, int64_t cap,
+                                      const int64_t* __restrict__ start_dev) {
+  pdl_wait();
+  const int64_t n = min(*n_dev, n_max);
+  const int64_t j = blockIdx.x;
+  if (j >= n || (n > cap && j < n - cap)) return;
+  const int64_t phys = n >= cap ? j - (n - cap) : (*start_dev + j) % cap;
+  double* dst = ring + phys * d;
+  const X* src = x + j * ldx;
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) dst[i] = ld64(src, i);
+}
+
+__global__ void ring_advance_kernel(const int64_t* __restrict__ n_dev, int64_t n_max, int64_t cap, int64_t* start_dev) {
+  pdl_wait();
+  const int64_t n = min(*n_dev, n_max);
+  *start_dev = n >= cap ? 0 : (*start_dev + n) % cap;
+}
+
 __global__ void gather_rows_kernel(const double* __restrict__ src, int64_t d, const int64_t* __restrict__ rows,
                                    double* dst) {
   const int64_t i = blockIdx.x;
@@ -650,6 +674,30 @@ cudaError_t launch_revive(int64_t k, int64_t d, double n_new, double denom, cons
   if (n_dead == 0) return cudaSuccess;
   revive_kernel<<<(unsigned)n_dead, 128, 0, s>>>(d, n_new, denom, ring, dead_k, ring_rows, N, M, E); count_launches(1);
   return cudaGetLastError();
+}
+
+cudaError_t launch_ring_write_dev(const void* x, int dtype, int64_t ldx, const int64_t* n_dev, int64_t n_max,
+                                  int64_t d, double* ring, int64_t cap, int64_t* start_dev, cudaStream_t s) {
+  if (n_max <= 0) return cudaSuccess;
+  cudaError_t e;
+  switch (dtype) {
+    case F32:
+      e = launch_pdl(ring_write_dev_kernel<float>, dim3((unsigned)n_max), dim3(128), 0, s, (const float*)x, ldx, n_dev,
+                     n_max, d, ring, cap, (const int64_t*)start_dev);
+      break;
+    case F64:
+      e = launch_pdl(ring_write_dev_kernel<double>, dim3((unsigned)n_max), dim3(128), 0, s, (const double*)x, ldx,
+                     n_dev, n_max, d, ring, cap, (const int64_t*)start_dev);
+      break;
+    default:
+      e = launch_pdl(ring_write_dev_kernel<uint16_t>, dim3((unsigned)n_max), dim3(128), 0, s, (const uint16_t*)x, ldx,
+                     n_dev, n_max, d, ring, cap, (const int64_t*)start_dev);
+  }
+  if (e != cudaSuccess) return e;
+  count_launches(1);
+  e = launch_pdl(ring_advance_kernel, dim3(1), dim3(1), 0, s, n_dev, n_max, cap, start_dev);
+  count_launches(1);
+  return e;
 }
 
 cudaError_t launch_ring_write(const void* x, int dtype, int64_t ldx, int64_t row0, int64_t nrows, int64_t d,

@@ -93,8 +93,13 @@ class PerceiverStream:
         self.codes = t.zeros(self.vcap, dtype=t.int64, device=dev)
         self.packed = t.zeros(self.K * self.D + self.K, dtype=t.float64, device=dev)
         self.dev_status = t.zeros(4, dtype=t.int64, device=dev)
+        # the reservoir ring's next write row on the device (the graph appends the
+        # frame's new rows there; the host mirrors the FIFO after reading n_new)
+        self.reservoir._ensure()
+        self.ring_start = t.zeros(1, dtype=t.int64, device=dev)
         self.host_N = t.empty(self.K, dtype=t.float64, pin_memory=True)
         self.host_status = t.empty(4, dtype=t.int64, pin_memory=True)
+        self._host_N_np, self._host_status_np = self.host_N.numpy(), self.host_status.numpy()   # views, made once
         self.occupied = VoxelHashSet(map_capacity)
         self.sampler = GridSampler(intrinsics, voxel_size, occupied=self.occupied, min_scale=min_scale)
         # the graph holds the workspaces' addresses: owned by this stream (a shared,
@@ -138,11 +143,20 @@ class PerceiverStream:
         nat.check(L.xgs_vq_ema(self.lam, self.eps, self.K, self.D, nat.ptr(self.N), nat.ptr(self.M),
                                nat.ptr(counts), nat.ptr(sums), nat.ptr(self.N), nat.ptr(self.M), nat.ptr(self.E),
                                sp))
+        # reservoir extend of the frame's new rows (vq.py:203; rows past vcap are the
+        # host fallback's, which rewinds the position first)
+        res = self.reservoir
+        nat.check(L.xgs_vq_ring_write_dev(nat.ptr(self.ofeat), nat.F32, self.C, nat.ptr(self.dev_status), self.vcap,
+                                          self.C, nat.ptr(res._ring), res.capacity, nat.ptr(self.ring_start), sp))
         self.host_N.copy_(self.N, non_blocking=True)
         self.host_status.copy_(self.dev_status, non_blocking=True)
 
+    def _sync_ring_start(self):
+        self.ring_start.fill_(self.reservoir._write_pos())
+
     def _capture(self):
         t = self.t
+        self._sync_ring_start()
         g = t.cuda.CUDAGraph()
         s = t.cuda.Stream()
         s.wait_stream(t.cuda.current_stream())
@@ -195,8 +209,7 @@ class PerceiverStream:
             return out
         self.graph.replay()
         self.t.cuda.current_stream().synchronize()
-        st = self.host_status.numpy()
-        n_new, n_valid, n_vox, err = (int(v) for v in st)
+        n_new, n_valid, n_vox, err = self._host_status_np.tolist()
         if err:
             raise RuntimeError(f"grid batch overflow (code {err}): the map set or batch table is full")
         if n_new == 0:          # no new points: the stream makes no VQ step (online_step needs a nonempty batch)
@@ -209,19 +222,23 @@ class PerceiverStream:
             self.N.copy_(self.N0)
             self.M.copy_(self.M0)
             cb = Codebook._make(self.E, self.N, self.M, self.lam, self.eps, self.reservoir)
+            # (its reservoir extend rewrites, from the same position, the vcap rows the
+            # graph appended; the host FIFO was not advanced for them)
             cb, res = online_step(cb, self.ofeat[:n_new], self.cfg, self.rng)
             self.E.copy_(cb.E)
             self.N.copy_(cb.N)
             self.M.copy_(cb.M)
+            self._sync_ring_start()
             self.t.cuda.current_stream().synchronize()
             return StreamStepResult(n_new, n_valid, n_vox, res.revived, False)
         revived = []
         if n_new:
-            # reservoir ring write of the batch (vq.py:203), then the host RNG revival
-            self.reservoir._extend_rows(self.ofeat, nat.F32, n_new, self.C)
+            # the graph appended the batch to the reservoir ring (vq.py:203): mirror
+            # the FIFO, then the host RNG revival
+            self.reservoir._account(n_new)
             cb = Codebook._make(self.E, self.N, self.M, self.lam, self.eps, self.reservoir)
             revived, _ = _revive_dev(cb, self.E, self.N, self.M, self.cfg.delta_dead, self.rng,
-                                     N_host=self.host_N.numpy())
+                                     N_host=self._host_N_np)
         return StreamStepResult(n_new, n_valid, n_vox, revived, True)
 
     def codebook(self) -> Codebook:

@@ -84,3 +84,6 @@ def test_stream_graph_matches_sync_pipeline(cuda):
     mine = st.codebook()
     for a, b in ((mine.E, cb.E), (mine.N, cb.N), (mine.M, cb.M)):
         assert torch.equal(a, b)
+    # the reservoir FIFO the graph appends to (xgs_vq_ring_write_dev) equals the synchronous one
+    assert len(mine.reservoir) == len(cb.reservoir)
+    assert np.array_equal(mine.reservoir.as_array(), cb.reservoir.as_array())
