@@ -1338,6 +1338,7 @@ struct EmitArgs {
   void* ofeat;              // [cap, fc]: float (feat64 == 0) or double
   int feat64;
   double* count;
+  int32_t* cell;            // first-pick with features: [cap] feature-map cell of each voxel (emit -> feat kernel)
 };
 
 // One new voxel: output row o, representative pixel p (frame * H * W + u * W + v).
@@ -1362,6 +1363,13 @@ __device__ __forceinline__ void emit_one(int64_t o, int64_t p, const int32_t* __
       a.col[o * 3 + c] = a.color ? ddiv((double)a.color[p * 3 + c], 255.0) : 0.0;
     }
     if (a.count) a.count[o] = 1.0;
+    if (a.cell) {   // the gather rule's cell (supervision.py:133-147), once per voxel for the feature kernel
+      const double su = (double)(a.fh - 1), sv = (double)(a.fw - 1);
+      const double hu = (double)max(a.H - 1, (int64_t)1), hv = (double)max(a.W - 1, (int64_t)1);
+      const int64_t uu = (int64_t)floor(ddiv(dmul((double)u, su), hu) + 0.5);
+      const int64_t vv = (int64_t)floor(ddiv(dmul((double)v, sv), hv) + 0.5);
+      a.cell[o] = (int32_t)(uu * a.fw + vv);
+    }
   } else {
     // mean over the voxel's points in the head's frame, sequential in pid order
     const int64_t i0 = head_pos[p];
@@ -1430,10 +1438,16 @@ grid_emit_feat_kernel(const int32_t* __restrict__ head_pos, const int32_t* __res
     const int64_t f = p / HW, rem = p - f * HW;
     const float* plane = a.feat + (f * a.fc + c) * a.fh * a.fw;
     if (a.mode == 0) {
-      const int64_t u = rem / a.W, v = rem - u * a.W;
-      const int64_t uu = (int64_t)floor(ddiv(dmul((double)u, su), hu) + 0.5);
-      const int64_t vv = (int64_t)floor(ddiv(dmul((double)v, sv), hv) + 0.5);
-      const float x = plane[uu * a.fw + vv];
+      int64_t cell;
+      if (a.cell) {
+        cell = a.cell[o];   // computed once per voxel by the emission
+      } else {
+        const int64_t u = rem / a.W, v = rem - u * a.W;
+        const int64_t uu = (int64_t)floor(ddiv(dmul((double)u, su), hu) + 0.5);
+        const int64_t vv = (int64_t)floor(ddiv(dmul((double)v, sv), hv) + 0.5);
+        cell = uu * a.fw + vv;
+      }
+      const float x = plane[cell];
       if (a.feat64) static_cast<double*>(a.ofeat)[i] = (double)x;
       else static_cast<float*>(a.ofeat)[i] = x;
     } else {
@@ -2130,6 +2144,9 @@ cudaError_t emit_outputs(const GridIn& in, const Cam& cam, DedupTable* st, const
   ea.ofeat = out.feat;
   ea.feat64 = out.feat64;
   ea.count = out.count;
+  // first-pick features: the emission records each voxel's feature-map cell in
+  // the (otherwise unused on this path) per-pixel head buffer
+  ea.cell = (in.feat && in.mode == 0 && head) ? const_cast<int32_t*>(head) : nullptr;
   // first-pick: the pid-list kernel emits each tile's voxels itself (the colour
   // copy of a host-frame batch is waited for first); mean mode: separate emit
   // (only with at least one look-back tile per SM: a small frame has a few
