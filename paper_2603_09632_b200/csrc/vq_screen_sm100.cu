@@ -1026,8 +1026,14 @@ cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, 
   p.fq_count = cnt + 1;
   // K < 2048: top-2 epilogue on all rows, then the candidate-list epilogue
   // (CAP 8) on the rows whose best code was not unique; larger codebooks
-  // (more near-ties) use the CAP-16 list epilogue directly
-  const bool big = a.k >= 2048;
+  // (more near-ties) use the CAP-16 list epilogue directly, and so do small
+  // batches (<= 16384 rows: one launch instead of screen + gather + rescreen,
+  // whose fixed latencies dominate there -- the C4 per-frame step)
+  static const int64_t small_rows = [] {
+    const char* v = std::getenv("XGS_SCREEN_SMALL_ROWS");
+    return v ? (int64_t)std::atoll(v) : (int64_t)16384;
+  }();
+  const bool big = a.k >= 2048 || n <= small_rows;
   cudaError_t e;
   auto prepare = [&](auto kern, int idx, int bytes) -> cudaError_t {
     return attr_once(kAttrScreen0 + idx,
