@@ -2283,12 +2283,24 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
           const int diag = dg ? (dg[0] == '0' ? 0 : dg[0] == '1' ? 1 : 2) : 2;
           const char* hl = std::getenv("XGS_GRID_HALO");
           const bool halo = !(hl && hl[0] == '0');
-          // two half-row blocks per band when rows are wide (W > 512): the blocks'
-          // lifetime halves, and so does the partial last wave
+          // Blocks per row band (each a whole number of 128-column warps): the
+          // smallest split giving >= 16 blocks per SM, else one warp per block --
+          // short-lived blocks shorten the last wave, and a single 640-wide frame
+          // (80 bands) needs the split to fill the GPU at all.  C3 (16 x 1280x720):
+          // 2; C4 (640x480): 5.
           const char* cs = std::getenv("XGS_GRID_CSPLIT");
-          // (only when the halves are whole warps: W = 640 would leave a 3-warp block one
-          // third idle)
-          int csplit = cs ? std::atoi(cs) : (in.W > 512 && in.W % 256 == 0 ? 2 : 1);
+          int csplit = 1;
+          if (cs) {
+            csplit = std::atoi(cs);
+          } else if (in.W % 128 == 0) {
+            const int64_t nwr = in.W / 128, blocks1 = in.frames * rbf;
+            csplit = (int)nwr;
+            for (int64_t dd = 1; dd <= nwr; dd++)
+              if (nwr % dd == 0 && blocks1 * dd >= 16 * (int64_t)sms) {
+                csplit = (int)dd;
+                break;
+              }
+          }
           if (csplit < 1 || in.W / 4 / csplit < 32) csplit = 1;
           const unsigned ntc = (unsigned)((in.W / 4 + 32 * csplit - 1) / (32 * csplit) * 32);
           for (int c = 0; c < nchunk; c++) {
