@@ -71,11 +71,15 @@ class PerceiverStream:
         self.voxel = float(voxel_size)
         self.min_scale = float(min_scale)
         dev = "cuda"
-        # codebook state: updated in place by the graph (EMA) and the revival
-        self.E = codebook.E.clone().contiguous()
-        self.N = codebook.N.clone().contiguous()
-        self.M = codebook.M.clone().contiguous()
-        self.E0, self.N0, self.M0 = t.empty_like(self.E), t.empty_like(self.N), t.empty_like(self.M)
+        # codebook state, double-buffered: graph i reads state i and writes the EMA
+        # into state 1 - i, so a frame whose VQ step must not apply (no new points,
+        # or more than the window) simply keeps the current state -- no snapshot
+        # copies per frame.  The revival and the host fallback update the current one.
+        E = codebook.E.clone().contiguous()
+        N = codebook.N.clone().contiguous()
+        M = codebook.M.clone().contiguous()
+        self._S = [(E, N, M), (t.empty_like(E), t.empty_like(N), t.empty_like(M))]
+        self._cur = 0
         self.reservoir = codebook.reservoir if codebook.reservoir is not None else FeatureReservoir(
             cfg.reservoir_capacity, self.D)
         # staged frame (the graph reads these addresses)
@@ -123,32 +127,35 @@ class PerceiverStream:
         self.graph = None
         self.frames = 0
 
+    E = property(lambda self: self._S[self._cur][0])
+    N = property(lambda self: self._S[self._cur][1])
+    M = property(lambda self: self._S[self._cur][2])
+
     # ------------------------------------------------------------ device part
-    def _enqueue(self):
-        """The graph body (all on the current stream, no host sync)."""
+    def _enqueue(self, i):
+        """Graph i's body (all on the current stream, no host sync): state i in,
+        the EMA into state 1 - i."""
         t, L, sp = self.t, nat.lib(), nat.stream_ptr()
-        self.E0.copy_(self.E)
-        self.N0.copy_(self.N)
-        self.M0.copy_(self.M)
+        Ei, Ni, Mi = self._S[i]
+        Eo, No, Mo = self._S[1 - i]
         nat.check(L.xgs_grid_sample(ctypes.byref(self._frames), self.occupied._h, ctypes.byref(self._result),
                                     nat.ptr(self.ws_grid), self.ws_grid.numel(), sp))
         nat.check(L.xgs_prefix_mask(nat.ptr(self.dev_status), self.vcap, nat.ptr(self.mask), sp))
-        nat.check(L.xgs_vq_assign(nat.ptr(self.ofeat), nat.F32, self.vcap, self.C, self.C, nat.ptr(self.E), self.K,
+        nat.check(L.xgs_vq_assign(nat.ptr(self.ofeat), nat.F32, self.vcap, self.C, self.C, nat.ptr(Ei), self.K,
                                   nat.ptr(self.codes), nat.ptr(self.ws_assign), self.ws_assign.numel(), None, sp))
         sums = self.packed[:self.K * self.D]
         counts = self.packed[self.K * self.D:]
         nat.check(L.xgs_vq_accumulate(nat.ptr(self.ofeat), nat.F32, self.vcap, self.C, self.C, nat.ptr(self.codes),
                                       nat.ptr(self.mask), self.K, nat.ptr(counts), nat.ptr(sums),
                                       nat.ptr(self.ws_acc), self.ws_acc.numel(), sp))
-        nat.check(L.xgs_vq_ema(self.lam, self.eps, self.K, self.D, nat.ptr(self.N), nat.ptr(self.M),
-                               nat.ptr(counts), nat.ptr(sums), nat.ptr(self.N), nat.ptr(self.M), nat.ptr(self.E),
-                               sp))
+        nat.check(L.xgs_vq_ema(self.lam, self.eps, self.K, self.D, nat.ptr(Ni), nat.ptr(Mi),
+                               nat.ptr(counts), nat.ptr(sums), nat.ptr(No), nat.ptr(Mo), nat.ptr(Eo), sp))
         # reservoir extend of the frame's new rows (vq.py:203; rows past vcap are the
         # host fallback's, which rewinds the position first)
         res = self.reservoir
         nat.check(L.xgs_vq_ring_write_dev(nat.ptr(self.ofeat), nat.F32, self.C, nat.ptr(self.dev_status), self.vcap,
                                           self.C, nat.ptr(res._ring), res.capacity, nat.ptr(self.ring_start), sp))
-        self.host_N.copy_(self.N, non_blocking=True)
+        self.host_N.copy_(No, non_blocking=True)
         self.host_status.copy_(self.dev_status, non_blocking=True)
 
     def _sync_ring_start(self):
@@ -157,14 +164,18 @@ class PerceiverStream:
     def _capture(self):
         t = self.t
         self._sync_ring_start()
-        g = t.cuda.CUDAGraph()
-        s = t.cuda.Stream()
-        s.wait_stream(t.cuda.current_stream())
-        with t.cuda.stream(s):
-            with t.cuda.graph(g, stream=s):
-                self._enqueue()
-        t.cuda.current_stream().wait_stream(s)
-        self.graph = g
+        graphs = []
+        for i in (0, 1):
+            g = t.cuda.CUDAGraph()
+            s = t.cuda.Stream()
+            s.wait_stream(t.cuda.current_stream())
+            with t.cuda.stream(s):
+                with t.cuda.graph(g, stream=s):
+                    self._enqueue(i)
+            t.cuda.current_stream().wait_stream(s)
+            graphs.append(g)
+        self.graphs = graphs
+        self.graph = graphs[0]
 
     # ------------------------------------------------------------ per frame
     def inputs(self):
@@ -207,20 +218,14 @@ class PerceiverStream:
             out = self._sync_frame()
             self._capture()
             return out
-        self.graph.replay()
+        self.graphs[self._cur].replay()
         self.t.cuda.current_stream().synchronize()
         n_new, n_valid, n_vox, err = self._host_status_np.tolist()
         if err:
             raise RuntimeError(f"grid batch overflow (code {err}): the map set or batch table is full")
         if n_new == 0:          # no new points: the stream makes no VQ step (online_step needs a nonempty batch)
-            self.E.copy_(self.E0)
-            self.N.copy_(self.N0)
-            self.M.copy_(self.M0)
-            return StreamStepResult(0, n_valid, n_vox, [], True)
-        if n_new > self.vcap:   # the window missed rows: roll the codebook back, redo the VQ on all n_new rows
-            self.E.copy_(self.E0)
-            self.N.copy_(self.N0)
-            self.M.copy_(self.M0)
+            return StreamStepResult(0, n_valid, n_vox, [], True)   # (the current state is untouched)
+        if n_new > self.vcap:   # the window missed rows: redo the VQ on all n_new rows from the current state
             cb = Codebook._make(self.E, self.N, self.M, self.lam, self.eps, self.reservoir)
             # (its reservoir extend rewrites, from the same position, the vcap rows the
             # graph appended; the host FIFO was not advanced for them)
@@ -231,6 +236,7 @@ class PerceiverStream:
             self._sync_ring_start()
             self.t.cuda.current_stream().synchronize()
             return StreamStepResult(n_new, n_valid, n_vox, res.revived, False)
+        self._cur = 1 - self._cur   # the EMA'd state becomes current
         revived = []
         if n_new:
             # the graph appended the batch to the reservoir ring (vq.py:203): mirror

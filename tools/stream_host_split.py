@@ -18,7 +18,7 @@ _step = S.PerceiverStream.step
 def step(self, *a, **k):
     if self.graph is None:
         return _step(self, *a, **k)
-    g = self.graph
+    g = self.graphs[self._cur]
     t = {}
     R0 = g.replay
     stream = torch.cuda.current_stream()

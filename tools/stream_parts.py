@@ -33,12 +33,6 @@ def grid_part():
                                 nat.ptr(st.ws_grid), st.ws_grid.numel(), nat.stream_ptr()))
 
 
-def copies():
-    st.E0.copy_(st.E)
-    st.N0.copy_(st.N)
-    st.M0.copy_(st.M)
-
-
 def assign():
     nat.check(L.xgs_prefix_mask(nat.ptr(st.dev_status), st.vcap, nat.ptr(st.mask), nat.stream_ptr()))
     nat.check(L.xgs_vq_assign(nat.ptr(st.ofeat), nat.F32, st.vcap, st.C, st.C, nat.ptr(st.E), st.K,
@@ -56,14 +50,15 @@ def accumulate():
 def ema_ring():
     sums = st.packed[:st.K * st.D]
     counts = st.packed[st.K * st.D:]
-    nat.check(L.xgs_vq_ema(st.lam, st.eps, st.K, st.D, nat.ptr(st.N0), nat.ptr(st.M0), nat.ptr(counts),
-                           nat.ptr(sums), nat.ptr(st.N0), nat.ptr(st.M0), nat.ptr(st.E0), nat.stream_ptr()))
+    Eo, No, Mo = st._S[1 - st._cur]
+    nat.check(L.xgs_vq_ema(st.lam, st.eps, st.K, st.D, nat.ptr(st.N), nat.ptr(st.M), nat.ptr(counts),
+                           nat.ptr(sums), nat.ptr(No), nat.ptr(Mo), nat.ptr(Eo), nat.stream_ptr()))
 
 
-for name, fn in (("copies", copies), ("grid", grid_part), ("prefix+assign", assign), ("accumulate", accumulate),
+for name, fn in (("grid", grid_part), ("prefix+assign", assign), ("accumulate", accumulate),
                  ("ema", ema_ring), ("whole step graph", None)):
     if fn is None:
-        g = st.graph
+        g = st.graphs[st._cur]
     else:
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()

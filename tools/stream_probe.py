@@ -21,18 +21,19 @@ _step = S.PerceiverStream.step
 def step(self, *a, **k):
     if self.graph is None:
         return _step(self, *a, **k)
-    R0 = self.graph.replay
+    g = self.graphs[self._cur]
+    R0 = g.replay
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def rep():
         e0.record()
         R0()
         e1.record()
-    self.graph.replay = rep
+    g.replay = rep
     t0 = time.perf_counter()
     out = _step(self, *a, **k)
     t1 = time.perf_counter()
-    self.graph.replay = R0
+    g.replay = R0
     torch.cuda.synchronize()
     gpu_ms.append(e0.elapsed_time(e1))
     host_ms.append((t1 - t0) * 1e3)
