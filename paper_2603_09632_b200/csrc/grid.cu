@@ -2151,8 +2151,11 @@ cudaError_t emit_outputs(const GridIn& in, const Cam& cam, DedupTable* st, const
   // copy of a host-frame batch is waited for first); mean mode: separate emit
   // (only with at least one look-back tile per SM: a small frame has a few
   // 65K-pixel tiles, whose blocks would emit every voxel between them)
-  const char* fe = std::getenv("XGS_GRID_FUSE_EMIT");
-  const bool fuse = in.mode == 0 && !(fe && fe[0] == '0') && (lb_tiles >= sms || (fe && fe[0] == '1'));
+  static const int fe = [] {   // tuning knob, read once: -1 auto, 0 off, 1 on
+    const char* v = std::getenv("XGS_GRID_FUSE_EMIT");
+    return v ? (v[0] == '0' ? 0 : v[0] == '1' ? 1 : -1) : -1;
+  }();
+  const bool fuse = in.mode == 0 && fe != 0 && (lb_tiles >= sms || fe == 1);
   if (fuse && hcp && (e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;   // colour
   if ((e = launch_pdl(grid_pidlist_lb_kernel, dim3((unsigned)lb_tiles), dim3(kLbThreads), 0, s, st->flags, nwords,
                       st->lb, cnts, (int64_t)out.capacity, out.pid, grand, st->host_st_dev, out.dev_status, ea,
@@ -2277,21 +2280,29 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
         ProfScope prof("grid_keys", s);
         if (front_ok) {
           const int64_t rbf = (in.H + FK_ROWS - 1) / FK_ROWS;
-          const char* dg = std::getenv("XGS_GRID_DIAG");
-          // neighbour dedup: 0 left/up, 1 + diagonals, 2 (default) + two columns away
-          // (C3 1 cm: 2.82M -> 1.92M table inserts, front end 143.4 -> 139.8 us)
-          const int diag = dg ? (dg[0] == '0' ? 0 : dg[0] == '1' ? 1 : 2) : 2;
-          const char* hl = std::getenv("XGS_GRID_HALO");
-          const bool halo = !(hl && hl[0] == '0');
+          // tuning knobs, read once.  Neighbour dedup: 0 left/up, 1 + diagonals, 2
+          // (default) + two columns away (C3 1 cm: 2.82M -> 1.92M table inserts,
+          // front end 143.4 -> 139.8 us)
+          static const int diag = [] {
+            const char* v = std::getenv("XGS_GRID_DIAG");
+            return v ? (v[0] == '0' ? 0 : v[0] == '1' ? 1 : 2) : 2;
+          }();
+          static const bool halo = [] {
+            const char* v = std::getenv("XGS_GRID_HALO");
+            return !(v && v[0] == '0');
+          }();
           // Blocks per row band (each a whole number of 128-column warps): the
           // smallest split giving >= 16 blocks per SM, else one warp per block --
           // short-lived blocks shorten the last wave, and a single 640-wide frame
           // (80 bands) needs the split to fill the GPU at all.  C3 (16 x 1280x720):
           // 2; C4 (640x480): 5.
-          const char* cs = std::getenv("XGS_GRID_CSPLIT");
+          static const int cs = [] {
+            const char* v = std::getenv("XGS_GRID_CSPLIT");
+            return v ? std::atoi(v) : 0;
+          }();
           int csplit = 1;
-          if (cs) {
-            csplit = std::atoi(cs);
+          if (cs > 0) {
+            csplit = cs;
           } else if (in.W % 128 == 0) {
             const int64_t nwr = in.W / 128, blocks1 = in.frames * rbf;
             csplit = (int)nwr;
