@@ -98,6 +98,7 @@ inline int64_t screen_chunk_rows(int64_t n) {
 cudaError_t screen_prepare(const ScreenArgs& a, cudaStream_t s);
 cudaError_t screen_prep_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, cudaStream_t s);
 cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, cudaStream_t s);
+cudaError_t screen_rerank(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, cudaStream_t s);
 cudaError_t screen_finish(const ScreenArgs& a, int chunks, cudaStream_t s, int32_t* host_stats);
 
 // ---------------- row-chunk pipelined assign + accumulate (vq_pipeline.cu) ----------------

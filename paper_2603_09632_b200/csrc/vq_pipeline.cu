@@ -8,8 +8,11 @@
 // waves and the stages run on three streams:
 //
 //   prep stream   : prep_rows(c)                      -> ev_prep[c]
-//   caller stream : wait ev_prep[c]; screen + re-rank(c) -> ev_codes[c]
-//   acc stream    : wait ev_codes[c]; accumulate(c, continue chains)
+//   caller stream : wait ev_prep[c]; screen(c)        -> ev_screen[c]
+//   acc stream    : wait ev_screen[c]; re-rank(c) -> ev_rerank[c]; accumulate(c, continue chains)
+//
+// (the latency-bound re-rank of chunk c runs beside the prep of chunk c + 1
+// instead of delaying the next screen)
 //
 // so prep(c+1) and accumulate(c-1) can run on the SM resources the persistent
 // screening kernel leaves free.  Measured on the B200 the co-resident blocks
@@ -31,7 +34,7 @@ struct PipeRes {
   bool ready = false;
   cudaStream_t sp = nullptr, sa = nullptr;
   cudaEvent_t ev0 = nullptr, done = nullptr;
-  cudaEvent_t evp[kMaxChunks], eva[kMaxChunks];
+  cudaEvent_t evp[kMaxChunks], eva[kMaxChunks], evr[kMaxChunks];
 };
 
 constexpr int kMaxDevices = 16;
@@ -50,6 +53,7 @@ cudaError_t res_for(int dev, PipeRes** out) {
     for (int i = 0; i < kMaxChunks; i++) {
       if ((e = cudaEventCreateWithFlags(&r.evp[i], cudaEventDisableTiming)) != cudaSuccess) return e;
       if ((e = cudaEventCreateWithFlags(&r.eva[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&r.evr[i], cudaEventDisableTiming)) != cudaSuccess) return e;
     }
     r.ready = true;
   }
@@ -107,15 +111,17 @@ cudaError_t launch_assign_accumulate(const ScreenArgs& a, double* counts, double
         return e;
     }
     // chunk c reuses the screening-buffer slot of chunk c - slots: its prep
-    // waits until that chunk's screen + re-rank (which read the slot) ran
+    // waits until that chunk's screen and re-rank (which read the slot) ran
     const int slots = a.n > screen_chunk_rows(a.n) ? 2 : 1;
-    if (c >= slots && (e = cudaStreamWaitEvent(r->sp, r->eva[c - slots], 0)) != cudaSuccess) return e;
+    if (c >= slots && (e = cudaStreamWaitEvent(r->sp, r->evr[c - slots], 0)) != cudaSuccess) return e;
     if ((e = screen_prep_rows(a, r0, r1, c, r->sp)) != cudaSuccess) return e;
     if ((e = cudaEventRecord(r->evp[c], r->sp)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(s, r->evp[c], 0)) != cudaSuccess) return e;
     if ((e = screen_rows(a, r0, r1, c, s)) != cudaSuccess) return e;
     if ((e = cudaEventRecord(r->eva[c], s)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(r->sa, r->eva[c], 0)) != cudaSuccess) return e;
+    if ((e = screen_rerank(a, r0, r1, c, r->sa)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(r->evr[c], r->sa)) != cudaSuccess) return e;
     const void* xc = static_cast<const char*>(a.x) + (size_t)r0 * xrow;
     if ((e = launch_accumulate(xc, a.dtype, r1 - r0, a.d, a.ldx, a.codes + r0, nullptr, a.k, counts, sums, acc_ws,
                                acc_ws_bytes, a.sm_count, r->sa, c > 0)) != cudaSuccess)

@@ -1073,9 +1073,23 @@ cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, 
       count_launches(1);
     }
   }
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return cudaGetLastError();
+}
 
-  // exact re-rank of the multi-candidate rows, exact scan of overflowed rows
+// exact re-rank of the multi-candidate rows, exact scan of overflowed rows
+// (after screen_rows of the same chunk; may run on another stream)
+cudaError_t screen_rerank(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, cudaStream_t s) {
+  const ScreenBufs b = screen_bufs(a);
+  const int64_t n = r1 - r0;
+  if (n <= 0) return cudaSuccess;
+  if (chunk < 0 || chunk >= kMaxChunks) return cudaErrorInvalidValue;
+  const int64_t sb = (chunk % b.w.slots) * b.w.chunk_rows;
+  int32_t* cnt = b.cnt + kCntBase + kCntStride * chunk;
+  RerankEntry* rq = b.rq + sb;
+  int32_t* fq = b.fq + sb;
+  const void* x = static_cast<const char*>(a.x) + (size_t)r0 * (size_t)a.ldx * dtype_size(a.dtype);
+  int64_t* codes = a.codes + r0;
+  cudaError_t e;
   ProfScope prof("vq_rerank", s);
   if ((e = launch_rerank(x, a.dtype, a.d, a.ldx, a.E, rq, cnt, n, codes, *a.pd, s)) != cudaSuccess) return e;
   ExactArgs ea{};
@@ -1115,6 +1129,7 @@ cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* h
     const int64_t r0 = c * crows, r1 = r0 + crows < a.n ? r0 + crows : a.n;
     if ((e = screen_prep_rows(a, r0, r1, c, s)) != cudaSuccess) return e;
     if ((e = screen_rows(a, r0, r1, c, s)) != cudaSuccess) return e;
+    if ((e = screen_rerank(a, r0, r1, c, s)) != cudaSuccess) return e;
   }
   return screen_finish(a, chunks, s, host_stats);
 }
