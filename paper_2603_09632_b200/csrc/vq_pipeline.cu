@@ -46,8 +46,14 @@ cudaError_t res_for(int dev, PipeRes** out) {
   PipeRes& r = g_res[dev];
   if (!r.ready) {
     cudaError_t e;
-    if ((e = cudaStreamCreateWithFlags(&r.sp, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    if ((e = cudaStreamCreateWithFlags(&r.sa, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    // the prep of the next chunk gates the next screen: its stream gets the
+    // highest priority, the accumulate stream the lowest (XGS_PIPE_PRIO=0: equal)
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    const char* pv = std::getenv("XGS_PIPE_PRIO");
+    if (pv && pv[0] == '0') lo = hi = 0;
+    if ((e = cudaStreamCreateWithPriority(&r.sp, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithPriority(&r.sa, cudaStreamNonBlocking, lo)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&r.ev0, cudaEventDisableTiming)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming)) != cudaSuccess) return e;
     for (int i = 0; i < kMaxChunks; i++) {
