@@ -14,6 +14,7 @@ stats are combined with one NCCL all-reduce per step.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -1085,6 +1086,12 @@ def main():
     ap.add_argument("--grid-steps", type=int, default=5)
     ap.add_argument("--stream-frames", type=int, default=1000)
     args = ap.parse_args()
+    # The timed regions must not see Python's cyclic-GC pauses (the CPU legs allocate
+    # enough objects to trigger gen-2 collections in the middle of a later GPU
+    # measurement: the rasterizer build read 33 ms instead of 1 ms): collect between
+    # the sub-benchmarks instead.
+    gc.collect()
+    gc.disable()
     args.warmup = max(3, args.warmup)
 
     rank = int(os.environ.get("RANK", "0"))
@@ -1175,21 +1182,24 @@ def main():
 
     cpu = c1 = c2 = grid = stream = targets = consumers = raster = init = None
     if rank == 0 and world == 1:
+        def sub(fn, *a, **k):   # each sub-benchmark starts from a collected heap
+            gc.collect()
+            return fn(*a, **k)
         if not args.no_cpu:
-            cpu = cpu_port_c5(args.cpu_seconds)
+            cpu = sub(cpu_port_c5, args.cpu_seconds)
         if not args.no_c2:
-            c2 = run_c2(torch, args, device)
+            c2 = sub(run_c2, torch, args, device)
         if not args.no_grid:
-            c1 = run_c1(torch, cpu=not args.no_cpu)
+            c1 = sub(run_c1, torch, cpu=not args.no_cpu)
         if not args.no_grid:
-            grid = run_grid(torch, args.grid_steps, cpu=not args.no_cpu)
+            grid = sub(run_grid, torch, args.grid_steps, cpu=not args.no_cpu)
         if args.stream_frames > 0:
-            stream = run_stream(torch, args.stream_frames, device)
+            stream = sub(run_stream, torch, args.stream_frames, device)
         if not args.no_grid:
-            targets = run_targets(torch, 10, cpu=not args.no_cpu)
-            init = run_init(torch, cpu=not args.no_cpu)
-            consumers = run_consumers(torch, 5, cpu=not args.no_cpu)
-            raster = run_raster(torch, 3, cpu=not args.no_cpu)
+            targets = sub(run_targets, torch, 10, cpu=not args.no_cpu)
+            init = sub(run_init, torch, cpu=not args.no_cpu)
+            consumers = sub(run_consumers, torch, 5, cpu=not args.no_cpu)
+            raster = sub(run_raster, torch, 3, cpu=not args.no_cpu)
     if rank == 0:
         per_kernel = {t: {"ms_per_step": m / prof_steps, "launches": c} for t, (m, c) in prof.items()}
         g1 = (grid or {}).get("0.01") or {}

@@ -8,6 +8,11 @@ import torch
 
 import bench
 
+import gc
+
+gc.collect()
+gc.disable()   # as bench.main: no cyclic-GC pauses inside the timed regions
+
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 torch.cuda.set_device(0)
 print(json.dumps(bench.run_c5(torch, iters, torch.device("cuda", 0))), flush=True)

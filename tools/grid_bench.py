@@ -8,6 +8,11 @@ import torch
 
 import bench
 
+import gc
+
+gc.collect()
+gc.disable()   # as bench.main: no cyclic-GC pauses inside the timed regions
+
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 out = bench.run_grid(torch, steps, cpu=False)
 for v, g in out.items():

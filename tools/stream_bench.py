@@ -8,6 +8,11 @@ import torch
 
 import bench
 
+import gc
+
+gc.collect()
+gc.disable()   # as bench.main: no cyclic-GC pauses inside the timed regions
+
 frames = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
 torch.cuda.set_device(0)
 print(json.dumps(bench.run_stream(torch, frames, torch.device("cuda", 0))))
