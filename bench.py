@@ -595,7 +595,8 @@ def run_targets(torch, iters, cpu=True):
     g.manual_seed(50)
     P = torch.randn(D, H // 16, W // 16, generator=g, device="cuda")
     src = sup.ContinuousFeatureSource(P)
-    sup.prefetch_targets(src, H, W, s, range(16))
+    for _ in range(3):   # warm-up as the timed loop runs (two output sets alive at once: both blocks cached)
+        G, V = sup.prefetch_targets(src, H, W, s, range(16))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
