@@ -406,11 +406,34 @@ def _revive_dev(codebook: Codebook, E, N, M, delta_dead, rng, N_host=None):
     if len(res) == 0:
         return [], True
     rows = np.array([res._draw(rng) for _ in dead], dtype=np.int64)
-    dk = t.from_numpy(dead.astype(np.int64)).to("cuda")
-    rr = t.from_numpy(rows).to("cuda")
+    # the (dead code, ring row) pairs go to the device in one async copy from a
+    # reused pinned buffer (two pageable copies had cost ~50 us per revival)
+    nd = int(dead.size)
+    hbuf, dbuf, ev = _revive_bufs(t, codebook.K)
+    ev.synchronize()                      # the previous revival's copy has read the host buffer
+    hbuf[:nd] = t.from_numpy(dead.astype(np.int64))
+    hbuf[codebook.K:codebook.K + nd] = t.from_numpy(rows)
+    dbuf.copy_(hbuf, non_blocking=True)
+    ev.record()
     nat.call("xgs_vq_revive", codebook.K, codebook.D, float(codebook.epsilon), nat.ptr(res._ring), res.capacity,
-             nat.ptr(dk), nat.ptr(rr), int(dead.size), nat.ptr(N), nat.ptr(M), nat.ptr(E), nat.stream_ptr())
+             nat.ptr(dbuf), nat.ptr(dbuf[codebook.K:]), nd, nat.ptr(N), nat.ptr(M), nat.ptr(E), nat.stream_ptr())
     return [int(k) for k in dead], False
+
+
+_REVIVE_BUFS = {}
+
+
+def _revive_bufs(t, K):
+    """Per (device, K): pinned host int64[2K], device int64[2K] and the event of
+    the last copy out of the host buffer."""
+    key = (t.cuda.current_device(), K)
+    b = _REVIVE_BUFS.get(key)
+    if b is None:
+        b = (t.empty(2 * K, dtype=t.int64, pin_memory=True), t.empty(2 * K, dtype=t.int64, device="cuda"),
+             t.cuda.Event())
+        b[2].record()
+        _REVIVE_BUFS[key] = b
+    return b
 
 
 def revive_dead_codes(codebook: Codebook, cfg: VqConfig, rng: np.random.Generator) -> ReviveResult:
