@@ -67,6 +67,13 @@ XGS_API int xgs_profile_dump(const char* path);
 XGS_API size_t xgs_vq_assign_workspace(int64_t n, int64_t k, int64_t d, int dtype, int64_t ldx);
 XGS_API int xgs_vq_assign(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E, int64_t k,
                           int64_t* codes, void* ws, size_t ws_bytes, int32_t* stats_out, void* stream);
+/* xgs_vq_assign on rows [0, min(*n_dev, n)) only, the count read on the device
+ * (graph-capturable: a fixed-capacity window whose valid row count a previous
+ * kernel wrote, e.g. the new points of a grid batch); codes of the rows past it
+ * are not written.  Single-chunk batches (n <= 2^21). */
+XGS_API int xgs_vq_assign_dev(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E,
+                              int64_t k, int64_t* codes, void* ws, size_t ws_bytes, const int64_t* n_dev,
+                              void* stream);
 
 /* Exact fp64 path, one CTA per row:
  *   XGS_EX_DIST  squared_distances (vq.py:69-73) -> out_dist (n, k)

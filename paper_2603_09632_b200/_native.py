@@ -37,6 +37,7 @@ SIGNATURES = {
     "xgs_profile_dump": (_i32, [ctypes.c_char_p]),
     "xgs_vq_assign_workspace": (_sz, [_i64, _i64, _i64, _i32, _i64]),
     "xgs_vq_assign": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _sz, _vp, _vp]),
+    "xgs_vq_assign_dev": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _sz, _vp, _vp]),
     "xgs_vq_exact": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _i32, _f64, _f64, _vp, _vp, _vp, _vp,
                             _vp]),
     "xgs_vq_step_workspace": (_sz, [_i64, _i64, _i64, _i32, _i64]),

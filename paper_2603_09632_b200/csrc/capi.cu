@@ -218,6 +218,24 @@ int xgs_vq_assign(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, c
   return OK;
 }
 
+int xgs_vq_assign_dev(const void* x, int dtype, int64_t n, int64_t d, int64_t ldx, const double* E, int64_t k,
+                      int64_t* codes, void* ws, size_t ws_bytes, const int64_t* n_dev, void* stream) {
+  int rc = check_assign(x, dtype, n, d, ldx, E, k, codes);
+  if (rc) return rc;
+  if (!n_dev) return fail(INVALID_INPUT, "null device row count");
+  if (n == 0) return OK;
+  if (n > screen_chunk_rows(n) || n != screen_chunk_rows(n))
+    return fail(NOT_SUPPORTED, "a device row count needs a single-chunk batch (n <= 2^21)");
+  if (ws_bytes < screen_workspace_bytes(n, k, d, dtype, ldx)) return fail(INVALID_INPUT, "workspace too small");
+  SumPlan pd;
+  if (!build_sum_plan((int)d, &pd)) return fail(NOT_SUPPORTED, "feature dim too large for the exact plan");
+  ScreenArgs a = screen_args(x, dtype, n, d, ldx, E, k, codes, ws, ws_bytes, &pd);
+  a.n_dev = n_dev;
+  cudaError_t e = launch_screen_assign(a, (cudaStream_t)stream, nullptr);
+  if (e != cudaSuccess) return cuda_fail(e, "xgs_vq_assign_dev");
+  return OK;
+}
+
 size_t xgs_vq_step_workspace(int64_t n, int64_t k, int64_t d, int dtype, int64_t ldx) {
   const size_t a = (screen_workspace_bytes(n, k, d, dtype, ldx) + 1023) / 1024 * 1024;
   return a + accumulate_workspace_bytes(n, k);

@@ -73,6 +73,7 @@ struct ScreenArgs {
   float c1, c2, c4;     // error-bound coefficients (host computed)
   const SumPlan* pd;
   int sm_count;
+  const int64_t* n_dev = nullptr;   // nullable: rows [0, min(*n_dev, n)) only (single-chunk batches)
 };
 size_t screen_workspace_bytes(int64_t n, int64_t k, int64_t d, int dtype, int64_t ldx);
 cudaError_t launch_screen_assign(const ScreenArgs& a, cudaStream_t s, int32_t* host_stats);

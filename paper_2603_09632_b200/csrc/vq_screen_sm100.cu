@@ -85,6 +85,7 @@ constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)
 struct ScreenParams {
   int64_t n;
   const int32_t* n_dev;   // nullable: device row count (rescreen pass; n is then the capacity)
+  const int64_t* n_dev64; // nullable: caller's device row count, clamped to n (main pass)
   const int32_t* rowmap;  // nullable: output row of local row i (rescreen pass)
   int32_t* sq;            // top-2 epilogue: rows whose best code is not unique -> rescreen
   int32_t* sq_count;
@@ -374,7 +375,7 @@ screen_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   const int nkb = p.num_k_blocks, nnc = p.num_n_chunks;
-  const int64_t nrows = p.n_dev ? (int64_t)*p.n_dev : p.n;
+  const int64_t nrows = p.n_dev ? (int64_t)*p.n_dev : p.n_dev64 ? min(*p.n_dev64, p.n) : p.n;
   const int ntiles = (int)((nrows + 2 * BM - 1) / (2 * BM));
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < A_SLOTS; i++) {
@@ -711,11 +712,11 @@ __global__ void __launch_bounds__(256)
 prep_rows_kernel(const X* __restrict__ x, int64_t n, int64_t d, int64_t ldx, int64_t dp,
                  const unsigned* __restrict__ emax_bits, const unsigned* __restrict__ cmax_bits,
                  float c3, __half* __restrict__ Ab, float* __restrict__ xband, float* __restrict__ xf,
-                 float inflate) {
+                 float inflate, const int64_t* __restrict__ n_dev) {
   using T = typename RowMath<X>::T;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (row >= n) return;
+  if (row >= n || (n_dev && row >= *n_dev)) return;
   const X* xr = x + row * ldx;
   T ss = 0;
   float mx = 0.f;
@@ -973,9 +974,9 @@ cudaError_t screen_prep_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int ch
   float* xn = b.xn + sb;
   float* xf = b.xf + sb;
   switch (a.dtype) {
-    case F32: prep_rows_kernel<float><<<rblocks, 256, 0, s>>>((const float*)a.x + r0 * a.ldx, n, a.d, a.ldx, dp, b.emax, b.emax + 1, 1.0e-12f, Ab, xn, xf, inflate); count_launches(1); break;
-    case F64: prep_rows_kernel<double><<<rblocks, 256, 0, s>>>((const double*)a.x + r0 * a.ldx, n, a.d, a.ldx, dp, b.emax, b.emax + 1, 1.0e-12f, Ab, xn, xf, inflate); count_launches(1); break;
-    default: prep_rows_kernel<uint16_t><<<rblocks, 256, 0, s>>>((const uint16_t*)a.x + r0 * a.ldx, n, a.d, a.ldx, dp, b.emax, b.emax + 1, 1.0e-12f, Ab, xn, xf, inflate); count_launches(1);
+    case F32: prep_rows_kernel<float><<<rblocks, 256, 0, s>>>((const float*)a.x + r0 * a.ldx, n, a.d, a.ldx, dp, b.emax, b.emax + 1, 1.0e-12f, Ab, xn, xf, inflate, a.n_dev); count_launches(1); break;
+    case F64: prep_rows_kernel<double><<<rblocks, 256, 0, s>>>((const double*)a.x + r0 * a.ldx, n, a.d, a.ldx, dp, b.emax, b.emax + 1, 1.0e-12f, Ab, xn, xf, inflate, a.n_dev); count_launches(1); break;
+    default: prep_rows_kernel<uint16_t><<<rblocks, 256, 0, s>>>((const uint16_t*)a.x + r0 * a.ldx, n, a.d, a.ldx, dp, b.emax, b.emax + 1, 1.0e-12f, Ab, xn, xf, inflate, a.n_dev); count_launches(1);
   }
   return cudaGetLastError();
 }
@@ -1001,6 +1002,7 @@ cudaError_t screen_rows(const ScreenArgs& a, int64_t r0, int64_t r1, int chunk, 
   ScreenParams p;
   p.n = n;
   p.n_dev = nullptr;
+  p.n_dev64 = a.n_dev;   // (single-chunk batches only: the C ABI checks)
   p.rowmap = nullptr;
   p.sq = b.sq;
   p.sq_count = cnt + 2;

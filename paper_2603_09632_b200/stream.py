@@ -141,8 +141,10 @@ class PerceiverStream:
         nat.check(L.xgs_grid_sample(ctypes.byref(self._frames), self.occupied._h, ctypes.byref(self._result),
                                     nat.ptr(self.ws_grid), self.ws_grid.numel(), sp))
         nat.check(L.xgs_prefix_mask(nat.ptr(self.dev_status), self.vcap, nat.ptr(self.mask), sp))
-        nat.check(L.xgs_vq_assign(nat.ptr(self.ofeat), nat.F32, self.vcap, self.C, self.C, nat.ptr(Ei), self.K,
-                                  nat.ptr(self.codes), nat.ptr(self.ws_assign), self.ws_assign.numel(), None, sp))
+        # only the frame's new rows (the count the grid batch wrote on the device)
+        nat.check(L.xgs_vq_assign_dev(nat.ptr(self.ofeat), nat.F32, self.vcap, self.C, self.C, nat.ptr(Ei), self.K,
+                                      nat.ptr(self.codes), nat.ptr(self.ws_assign), self.ws_assign.numel(),
+                                      nat.ptr(self.dev_status), sp))
         sums = self.packed[:self.K * self.D]
         counts = self.packed[self.K * self.D:]
         nat.check(L.xgs_vq_accumulate(nat.ptr(self.ofeat), nat.F32, self.vcap, self.C, self.C, nat.ptr(self.codes),
