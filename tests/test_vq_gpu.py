@@ -443,3 +443,29 @@ def test_confidence_mask_rows_at_gamma(xv):
         cfg = xv.VqConfig(K=40, tau_warm=0.7, gamma=float(gamma))
         got = xv.confidence_mask(x, cb, cfg)
         assert np.array_equal(got, pmax >= gamma), gamma
+
+
+@pytest.mark.parametrize("K", [256, 4096])
+def test_assign_with_device_row_count(xv, K):
+    """xgs_vq_assign_dev: rows [0, min(*n_dev, n)) get the codes xgs_vq_assign
+    gives them; rows past the count are left untouched."""
+    import torch
+
+    from paper_2603_09632_b200 import _native as nat
+    rng = np.random.default_rng(77)
+    n, D = 3000, 96
+    x = torch.from_numpy(rng.normal(size=(n, D)).astype(np.float32)).cuda()
+    E = torch.from_numpy(rng.normal(size=(K, D))).cuda()
+    L = nat.lib()
+    ws = nat.workspace("t_assign_dev", L.xgs_vq_assign_workspace(n, K, D, nat.F32, D))
+    ref = torch.empty(n, dtype=torch.int64, device="cuda")
+    nat.call("xgs_vq_assign", nat.ptr(x), nat.F32, n, D, D, nat.ptr(E), K, nat.ptr(ref), nat.ptr(ws), ws.numel(),
+             None, nat.stream_ptr())
+    for cnt in (0, 1, 1234, n, n + 500):
+        codes = torch.full((n,), -7, dtype=torch.int64, device="cuda")
+        n_dev = torch.tensor([cnt], dtype=torch.int64, device="cuda")
+        nat.call("xgs_vq_assign_dev", nat.ptr(x), nat.F32, n, D, D, nat.ptr(E), K, nat.ptr(codes), nat.ptr(ws),
+                 ws.numel(), nat.ptr(n_dev), nat.stream_ptr())
+        m = min(cnt, n)
+        assert torch.equal(codes[:m], ref[:m]), cnt
+        assert bool((codes[m:] == -7).all()), cnt
