@@ -1821,8 +1821,15 @@ dd_scan_map_kernel(unsigned long long* slots, int64_t cap, const int* overflow, 
 // starts every batch zeroed).  The last tile publishes the grand total for
 // the emit kernel, copies the batch counters into the caller's mapped host
 // status words and resets them for the next batch.
-constexpr int kLbThreads = 256, kLbWords = 8, kLbTile = kLbThreads * kLbWords, kLbFlat = 1024;
+constexpr int kLbThreads = 256, kLbFlat = 1024;
+// words per thread: 8 (2048-word tiles) when that still gives a tile per SM,
+// else 1 (256-word tiles: a single small frame gets tens of blocks, not a few)
+__host__ __device__ constexpr int64_t lb_tiles_for(int64_t nwords, int words) {
+  return (nwords + (int64_t)kLbThreads * words - 1) / ((int64_t)kLbThreads * words);
+}
+inline int lb_words_for(int64_t nwords, int sms) { return lb_tiles_for(nwords, 8) >= sms ? 8 : 1; }
 
+template <int kLbWords>
 __global__ void __launch_bounds__(kLbThreads)
 grid_pidlist_lb_kernel(unsigned* __restrict__ flag_bits, int64_t nwords, unsigned long long* lb_status,
                        unsigned long long* cnts, int64_t capacity, int64_t* __restrict__ pid_out,
@@ -1835,12 +1842,15 @@ grid_pidlist_lb_kernel(unsigned* __restrict__ flag_bits, int64_t nwords, unsigne
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   if (t == 0) s_tile = atomicAdd(reinterpret_cast<unsigned*>(cnts + 6), 1u);
   __syncthreads();
+  constexpr int kLbTile = kLbThreads * kLbWords;
   const int64_t tile = s_tile, ntiles = (nwords + kLbTile - 1) / kLbTile;
   const int64_t w0 = tile * kLbTile + (int64_t)t * kLbWords;
   unsigned w[kLbWords];
-  if (w0 + kLbWords <= nwords) {
+  if (kLbWords == 8 && w0 + kLbWords <= nwords) {
     const uint4 a = *reinterpret_cast<const uint4*>(flag_bits + w0), b = *reinterpret_cast<const uint4*>(flag_bits + w0 + 4);
-    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    const unsigned ww[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int j = 0; j < kLbWords; j++) w[j] = ww[j];
     if (a.x | a.y | a.z | a.w) *reinterpret_cast<uint4*>(flag_bits + w0) = make_uint4(0, 0, 0, 0);
     if (b.x | b.y | b.z | b.w) *reinterpret_cast<uint4*>(flag_bits + w0 + 4) = make_uint4(0, 0, 0, 0);
   } else {
@@ -2054,7 +2064,7 @@ cudaError_t grid_state(int64_t npix, cudaStream_t s, DedupTable** out, bool may_
     if ((e = cudaMalloc(&t.flags, (size_t)words * 4)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(t.flags, 0, (size_t)words * 4, s)) != cudaSuccess) return e;
     t.flag_words = words;
-    const int64_t tiles = (words + kLbTile - 1) / kLbTile;
+    const int64_t tiles = lb_tiles_for(words, 1);   // the most tiles any word count per thread needs
     t.release(t.lb);
     if ((e = cudaMalloc(&t.lb, (size_t)tiles * 8)) != cudaSuccess) return e;
     t.lb_tiles = tiles;
@@ -2114,7 +2124,8 @@ cudaError_t emit_outputs(const GridIn& in, const Cam& cam, DedupTable* st, const
   cudaError_t e;
   const int64_t npix = in.frames * in.H * in.W;
   const int64_t nwords = (npix + 31) / 32;
-  const int64_t lb_tiles = (nwords + kLbTile - 1) / kLbTile;
+  const int lbw = lb_words_for(nwords, sms);
+  const int64_t lb_tiles = lb_tiles_for(nwords, lbw);
   unsigned long long* cnts = reinterpret_cast<unsigned long long*>(st->misc + 64);
   int32_t* grand = reinterpret_cast<int32_t*>(st->misc + 128);
   EmitArgs ea;
@@ -2157,7 +2168,8 @@ cudaError_t emit_outputs(const GridIn& in, const Cam& cam, DedupTable* st, const
   }();
   const bool fuse = in.mode == 0 && fe != 0 && (lb_tiles >= sms || fe == 1);
   if (fuse && hcp && (e = cudaStreamWaitEvent(s, hcp->done, 0)) != cudaSuccess) return e;   // colour
-  if ((e = launch_pdl(grid_pidlist_lb_kernel, dim3((unsigned)lb_tiles), dim3(kLbThreads), 0, s, st->flags, nwords,
+  if ((e = launch_pdl(lbw == 8 ? grid_pidlist_lb_kernel<8> : grid_pidlist_lb_kernel<1>, dim3((unsigned)lb_tiles),
+                      dim3(kLbThreads), 0, s, st->flags, nwords,
                       st->lb, cnts, (int64_t)out.capacity, out.pid, grand, st->host_st_dev, out.dev_status, ea,
                       fuse)) != cudaSuccess)
     return e;
@@ -2214,7 +2226,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   const Cam cam{in.fx, in.fy, in.cx, in.cy, in.voxel, 1.0 / in.voxel};
   const bool compact = in.mode == 0;   // first-pick
   const int64_t nwords = (npix + 31) / 32;
-  const int64_t lb_tiles = (nwords + kLbTile - 1) / kLbTile;
+  const int64_t lb_tiles = lb_tiles_for(nwords, lb_words_for(nwords, sms));
   // Host frames (xgs_grid_sample_h2d): depth is copied frame chunk by frame
   // chunk on a copy stream and each chunk's front-end launch waits only for
   // its own chunk, so the copies of later frames overlap the earlier frames'
