@@ -1192,10 +1192,12 @@ def main():
             c2 = sub(run_c2, torch, args, device)
         if not args.no_grid:
             c1 = sub(run_c1, torch, cpu=not args.no_cpu)
-        if not args.no_grid:
-            grid = sub(run_grid, torch, args.grid_steps, cpu=not args.no_cpu)
+        # the C4 stream before the C3 grid: the per-device grid state (batch table)
+        # would otherwise keep the size the 16-frame C3 batches gave it
         if args.stream_frames > 0:
             stream = sub(run_stream, torch, args.stream_frames, device)
+        if not args.no_grid:
+            grid = sub(run_grid, torch, args.grid_steps, cpu=not args.no_cpu)
         if not args.no_grid:
             targets = sub(run_targets, torch, 10, cpu=not args.no_cpu)
             init = sub(run_init, torch, cpu=not args.no_cpu)
