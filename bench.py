@@ -13,10 +13,19 @@ stats are combined with one NCCL all-reduce per step.
 
 from __future__ import annotations
 
+import os
+
+# NumPy's OpenBLAS threads keep spinning after a BLAS call in the CPU legs and
+# take the host cores from the thread that drives the GPU (a rasterizer build
+# right after a CPU leg read 88-136 ms instead of 1.3 ms).  The NumPy parts of
+# the CPU baselines are single-threaded (their "cores": 1); the C port runs
+# its own threads.
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
 import argparse
 import gc
 import json
-import os
 import subprocess
 import sys
 import threading
