@@ -773,16 +773,20 @@ def run_raster(torch, iters, cpu=True):
     up = torch.randn(D, grid.H_s, grid.W_s, generator=g, device="cuda", dtype=torch.float64)
 
     def timed(fn, reps):
+        """Median over `reps` calls, each bracketed by events (the build syncs on
+        the host inside: one descheduled host thread must not skew a mean)."""
         fn()
         fn()   # two warm-up calls: the first touches freshly allocated scratch / output pages
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+        ts, r = [], None
         for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
             r = fn()
-        e1.record()
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / reps, r
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return float(np.median(ts)), r
 
     ms_build, pr = timed(lambda: rz._Pairs(field, pose, intr, grid.rows(), grid.cols(), rz.DEFAULT_RASTER), iters)
     ms_acc, _ = timed(lambda: pr.accumulate(payload), iters)
@@ -1211,7 +1215,7 @@ def main():
             targets = sub(run_targets, torch, 10, cpu=not args.no_cpu)
             init = sub(run_init, torch, cpu=not args.no_cpu)
             consumers = sub(run_consumers, torch, 5, cpu=not args.no_cpu)
-            raster = sub(run_raster, torch, 3, cpu=not args.no_cpu)
+            raster = sub(run_raster, torch, 7, cpu=not args.no_cpu)
     if rank == 0:
         per_kernel = {t: {"ms_per_step": m / prof_steps, "launches": c} for t, (m, c) in prof.items()}
         g1 = (grid or {}).get("0.01") or {}
