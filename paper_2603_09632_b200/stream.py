@@ -12,21 +12,25 @@ once and replays it per frame over fixed-capacity buffers:
           staged frame -> new voxels in pixel order + their features gathered
           from the frame's feature map (supervision.py:133-147 rule)
           -> valid-row mask of the first n_new rows (xgs_prefix_mask; n_new
-          lives on the device) -> assign (tcgen05 screen + exact re-rank) of a
-          fixed `vq_capacity`-row window of the feature buffer -> masked
-          accumulate (counting sort + sequential fp64 chains; rows past n_new
-          contribute nothing, so the statistics equal the reference's on the
-          n_new rows) -> EMA in place.
+          lives on the device) -> assign (tcgen05 screen + exact re-rank) of
+          the first min(n_new, `vq_capacity`) rows of the feature window
+          (xgs_vq_assign_dev) -> masked accumulate (counting sort + sequential
+          fp64 chains; rows past n_new contribute nothing, so the statistics
+          equal the reference's on the n_new rows) -> EMA into the other of two
+          codebook states -> reservoir append of the n_new rows (vq.py:203,
+          xgs_vq_ring_write_dev: row count and ring position on the device).
   host:   ONE device->host read of {N (K fp64), n_new, n_valid, n_voxels,
-          error} -> reservoir ring write of the n_new rows (vq.py:203) ->
-          the reference's host RNG draws for dead codes -> revival kernel.
+          error} -> the FIFO bookkeeping of the append -> the reference's host
+          RNG draws for dead codes -> revival kernel.
 
-The codebook before the step is kept inside the graph (two device copies),
-so a frame with more than `vq_capacity` new points -- rare at C4, its VQ
-would have seen only the window -- is rolled back and redone through the
-synchronous ``online_step`` on exactly its n_new rows.  Results are
-bit-identical to ``GridSampler.sample(...)`` followed by ``online_step`` on
-the returned features (tests/test_stream_gpu.py).
+Two graphs alternate between the two codebook states (graph i reads state i,
+writes state 1 - i), so a frame whose VQ step must not apply keeps the
+current state: a frame without new points, or one with more than
+`vq_capacity` -- rare at C4, its VQ would have seen only the window -- which is
+redone through the synchronous ``online_step`` on exactly its n_new rows.
+Results are bit-identical to ``GridSampler.sample(...)`` followed by
+``online_step`` on the returned features, reservoir included
+(tests/test_stream_gpu.py).
 """
 
 from __future__ import annotations
