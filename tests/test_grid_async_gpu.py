@@ -198,3 +198,15 @@ def test_map_captured_by_a_graph_refuses_to_grow(cuda):
     hs.insert(np.arange(1, 1000, dtype=np.uint64))            # fits: fine
     with pytest.raises(NativeError, match="cannot grow"):
         hs.insert(np.arange(1, 200_000, dtype=np.uint64))
+
+
+def test_grid_graph_refuses_mean_mode(cuda):
+    import torch
+
+    from paper_2603_09632_b200.errors import InvalidInputError
+    from paper_2603_09632_b200.grid import GridGraph, GridSampler, VoxelHashSet
+    d = torch.full((1, 16, 32), 2.0, device="cuda")
+    R = torch.eye(3, dtype=torch.float64, device="cuda").reshape(1, 9).contiguous()
+    T = torch.zeros(1, 3, dtype=torch.float64, device="cuda")
+    with pytest.raises(InvalidInputError):
+        GridGraph(GridSampler((20.0, 20.0, 7.5, 15.5), 0.05, mode="mean", occupied=VoxelHashSet(1 << 12)), d, (R, T))
