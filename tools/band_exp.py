@@ -1,3 +1,7 @@
+"""Re-rank / fallback row counts over 6 online steps on 2M C5 rows.  The
+wider-band emulation in DESIGN.md §10 ran it with a temporary local patch of
+capi.cu's screen_args (c1 scaled by XGS_BAND_SCALE); without that patch the
+variable has no effect and this prints the true band's counts."""
 import os, sys, json
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "."))
 import numpy as np, torch
