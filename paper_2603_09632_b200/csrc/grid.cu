@@ -378,7 +378,7 @@ __device__ __forceinline__ void dd_insert_finish(unsigned long long* slots, uint
 // the biased key field fl + 2^20.  Otherwise (voxel faces, non-finite values,
 // out of key range) the pixel takes the exact fp64 path (backproject +
 // floor_div), bit-identical to the reference.
-constexpr int FK_ROWS = 6;
+constexpr int FK_ROWS = 5;   // rows per front block (A/B at C3 1 cm: 4 0.157, 5 0.151, 6 0.157, 7 0.160 ms)
 constexpr int kInsILP = 4;   // table loads in flight per lane in FRONT_INSERT's tail (8: spills, 0.213 vs 0.199 ms)
 constexpr int kFrontPend = 256;    // per-block queue of pixels for the exact path (overflow: segment scan)
 // thread t covers columns 4t..4t+3 (W <= 4 * kFrontMaxThreads)
