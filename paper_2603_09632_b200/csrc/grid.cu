@@ -387,8 +387,10 @@ constexpr int kFrontWarps = kFrontMaxThreads / 32;
 constexpr int kPendW = kFrontPend / kFrontWarps;   // FRONT_INSERT: per-warp share of that queue
 constexpr int kFrontBlocksPerSM = FK_ROWS <= 6 ? 3 : 2;   // bounded by the staged segments (FK_ROWS * 11.5 KB)
 constexpr int kFrontSeg = 128;     // items per (row, warp) segment: the warp's columns
-// staged bytes per segment item: 8 (key) + 1 (column inside the warp's span)
-constexpr size_t front_smem_bytes(int64_t nw) { return (size_t)FK_ROWS * nw * kFrontSeg * 9; }
+// a segment in shared memory: 128 keys (8 B) then 128 columns inside the warp's span (1 B),
+// so item o = seg * 128 + i sits at a compile-time stride from its segment (no block-size math)
+constexpr int kSegBytes = kFrontSeg * 9;
+constexpr size_t front_smem_bytes(int64_t nw) { return (size_t)FK_ROWS * nw * kSegBytes; }
 
 struct CamF {
   float cx, cy, rfx, rfy, inv_voxel;
@@ -445,9 +447,16 @@ constexpr float kDl = 0x1p-20f * 1.002f + 0x1p-21f;
 enum FrontMode : int { FRONT_SORT = 1, FRONT_INSERT = 2 };
 
 // the front end's pre-key -> the packed voxel key (see the keying loop)
-__device__ __forceinline__ uint64_t pre_to_key(uint64_t k) {
-  const uint32_t lo = (uint32_t)k - 0x4B000000u, hi = (uint32_t)(k >> 32) - 0x96000u;
-  return ((uint64_t)hi << 32) | lo;
+__host__ __device__ constexpr uint64_t pre_to_key(uint64_t k) {
+  return ((uint64_t)((uint32_t)(k >> 32) - 0x96000u) << 32) | (uint32_t)((uint32_t)k - 0x4B000000u);
+}
+// staged image of the PEND sentinel (pre_to_key is injective; bit 63 set, so no real key)
+constexpr uint64_t kPendStaged = pre_to_key(KEY_INVALID - 1);
+__device__ __forceinline__ uint64_t& seg_key(uint8_t* smem, uint32_t o) {
+  return *reinterpret_cast<uint64_t*>(smem + (o / kFrontSeg) * kSegBytes + (o % kFrontSeg) * 8);
+}
+__device__ __forceinline__ uint8_t& seg_col(uint8_t* smem, uint32_t o) {
+  return smem[(o / kFrontSeg) * kSegBytes + kFrontSeg * 8 + (o % kFrontSeg)];
 }
 
 template <int MODE, int DIAG>
@@ -475,8 +484,7 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
   extern __shared__ __align__(16) uint8_t front_smem[];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
   const int nseg = NR * nw;
-  uint64_t* sk = reinterpret_cast<uint64_t*>(front_smem);                         // nseg * 128 keys
-  uint8_t* sc = front_smem + (size_t)nseg * kFrontSeg * 8;                          // nseg * 128 columns
+  const uint32_t smem_base = (uint32_t)__cvta_generic_to_shared(front_smem);
   const unsigned bid = bid0 + blockIdx.x;   // bid0: first block of this launch (frame-chunked launches)
   // csplit blocks side by side per row band (FRONT_INSERT): each covers
   // blockDim.x * 4 columns from colbase; shorter blocks shorten the last wave
@@ -579,6 +587,7 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
     const float4 rc = s_row[rr];
     const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
     uint64_t k[4];
+    unsigned vb = 0, pb = 0;   // per column j: valid pixel / left to the exact path (PEND)
     // two pixels per instruction (sm_100 paired fp32: FFMA2 / FADD2, IEEE per lane,
     // same roundings as the scalar expressions in the comments)
 #pragma unroll
@@ -609,7 +618,8 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
                        u2 = __float_as_uint(lane_of(x2, h));
         const uint64_t key = ((uint64_t)(u0 * 1024u + (u1 >> 11)) << 32) | (uint64_t)(u1 * 0x200000u + u2);
         k[j] = !valid ? KEY_INVALID : ok ? key : PEND;
-        cnt += (valid && ok && rr > 0) ? 1u : 0u;
+        vb |= valid ? 1u << j : 0u;
+        pb |= (valid && !ok) ? 1u << j : 0u;
       }
     }
     if (rr > 0) {
@@ -637,7 +647,8 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
         if (lane == 0) ll = ul2 = KEY_INVALID;
         if (lane == 31) ur2 = KEY_INVALID;
       }
-      unsigned keep = 0;
+      cnt += __popc(vb & ~pb);
+      unsigned dupm = 0;
 #pragma unroll
       for (int j = 0; j < 4; j++) {
         const uint64_t kk = k[j];
@@ -650,27 +661,33 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
           const uint64_t b2 = j == 3 ? ur2 : j == 2 ? ur : kp[j + 2];
           dup = dup || kk == l2 || kk == a2 || kk == b2;
         }
-        if (kk != KEY_INVALID && (kk == PEND || !dup)) keep |= 1u << j;
+        dupm |= dup ? 1u << j : 0u;
       }
+      // kept: valid and not a repeat, or undecided (PEND compares equal to a
+      // PEND neighbour above, but is always kept); invalid pixels never
+      const unsigned keep = vb & (pb | ~dupm), pend = pb;
       const unsigned lt = (1u << lane) - 1u;
       unsigned below = 0, total = 0;
 #pragma unroll
       for (int j = 0; j < 4; j++) {
-        const unsigned b = __ballot_sync(FULL, (keep >> j) & 1u);
+        const unsigned b = __ballot_sync(FULL, keep & (1u << j));
         below += __popc(b & lt);
         total += __popc(b);
       }
       const int seg = (rr - 1) * nw + warp;
       const uint32_t o0 = (uint32_t)seg * kFrontSeg + below;
-      unsigned pend = 0;
+      // predicated st.shared (a C++ `if` here becomes four branches that each
+      // rematerialise the segment address under the 64-register cap)
+      const uint32_t segs = smem_base + (uint32_t)seg * kSegBytes;
 #pragma unroll
       for (int j = 0; j < 4; j++) {
-        const uint32_t o = o0 + __popc(keep & ((1u << j) - 1u));
-        if ((keep >> j) & 1u) {   // predicated stores
-          sk[o] = k[j] == PEND ? PEND : pre_to_key(k[j]);
-          sc[o] = (uint8_t)(lane * 4 + j);
-        }
-        pend |= (((keep >> j) & 1u) && k[j] == PEND) ? 1u << j : 0u;
+        const uint32_t i = below + __popc(keep & ((1u << j) - 1u));
+        const uint64_t sv = pre_to_key(k[j]);   // PEND -> kPendStaged
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+            "@p st.shared.u64 [%1], %2;\n\t@p st.shared.u8 [%3], %4;\n\t}"
+            ::"r"(keep & (1u << j)), "r"(segs + i * 8), "l"(sv), "r"(segs + kFrontSeg * 8 + i),
+            "r"((uint32_t)(lane * 4 + j)) : "memory");
       }
       if (__any_sync(FULL, pend)) {   // rare: queue the undecided pixels for the exact path
         if constexpr (MODE == FRONT_INSERT) {
@@ -701,9 +718,10 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
   const uint32_t fbase = (uint32_t)((size_t)f * H * W);
   auto resolve = [&](uint32_t o) {
     const int seg = (int)(o / kFrontSeg);
-    const uint32_t u = (uint32_t)(r0 + seg / nw), v = colbase + (uint32_t)(seg % nw) * kFrontSeg + sc[o];
+    const uint32_t u = (uint32_t)(r0 + seg / nw), v = colbase + (uint32_t)(seg % nw) * kFrontSeg +
+                                                     seg_col(front_smem, o);
     const uint64_t key = key_exact(Rd, Td, cam, u, v, depth[fbase + u * Wu + v]);
-    sk[o] = key;
+    seg_key(front_smem, o) = key;
     cnt += key != KEY_INVALID ? 1u : 0u;
   };
   if constexpr (MODE == FRONT_INSERT) {
@@ -717,7 +735,7 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
         const int sg = rr * nw + warp;
         for (uint32_t i = lane; i < s_cnt[sg]; i += 32) {
           const uint32_t o = (uint32_t)sg * kFrontSeg + i;
-          if (sk[o] == PEND) resolve(o);
+          if (seg_key(front_smem, o) == kPendStaged) resolve(o);
         }
       }
     }
@@ -734,7 +752,7 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
       for (int s = warp; s < nseg; s += nw)
         for (uint32_t i = lane; i < s_cnt[s]; i += 32) {
           const uint32_t o = (uint32_t)s * kFrontSeg + i;
-          if (sk[o] == PEND) resolve(o);
+          if (seg_key(front_smem, o) == kPendStaged) resolve(o);
         }
     }
   }
@@ -766,8 +784,8 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
               rr = i + 1;
             }
           const uint32_t o = (uint32_t)(rr * nw + warp) * kFrontSeg + q;
-          key[j] = sk[o];
-          pid[j] = pcol + (uint32_t)(r0 + rr) * Wu + sc[o];
+          key[j] = seg_key(front_smem, o);
+          pid[j] = pcol + (uint32_t)(r0 + rr) * Wu + seg_col(front_smem, o);
         }
         if (key[j] != KEY_INVALID) {
           h[j] = dd_hash(key[j]) & mask;
@@ -830,9 +848,9 @@ grid_front_kernel(const float* __restrict__ depth, int64_t H, int64_t W, int str
     const uint32_t pbase = fbase + (uint32_t)(r0 + rr) * Wu + (uint32_t)warp * kFrontSeg;
     for (uint32_t i = lane; i < end - beg; i += 32) {
       const uint32_t o = (uint32_t)s * kFrontSeg + i;
-      const uint64_t key = sk[o];
+      const uint64_t key = seg_key(front_smem, o);
       kout[gbase + beg + i] = key;
-      vout[gbase + beg + i] = pbase + sc[o];
+      vout[gbase + beg + i] = pbase + seg_col(front_smem, o);
       if (BOX && key != KEY_INVALID) {
         const int q[3] = {(int)(key >> 42), (int)((key >> 21) & 0x1fffff), (int)(key & 0x1fffff)};
 #pragma unroll
