@@ -9,3 +9,9 @@ for f in sorted(glob.glob("gpurun_out/ab_*_[0-9].log")):
             d = json.loads(rest[:rest.rindex("}") + 1])
             print(os.path.basename(f)[3:-4], v, round(d["ms_per_batch"], 4), round(d["graph"]["ms_per_batch"], 4),
                   round(d["per_stage_ms"]["grid_keys"], 4))
+for f in sorted(glob.glob("gpurun_out/abs_*_[0-9].log")):
+    for l in open(f):
+        if l.startswith("{"):
+            d = json.loads(l)
+            print(os.path.basename(f)[4:-4], "C4 p50", round(d["p50_ms"], 4), "p99", round(d["p99_ms"], 4),
+                  "mean", round(d["mean_ms"], 4))
