@@ -23,6 +23,7 @@
 //                            new-head flags) and the GaussianField-compatible
 //                            outputs (mu, rgb/255, iso scale, depth, feature).
 // Semantics are pinned by oracle/grid.py.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -1427,6 +1428,55 @@ grid_emit_kernel(const int32_t* __restrict__ head_pos, const int32_t* __restrict
     emit_one(o, a.pid[o], head_pos, a);
 }
 
+// First-pick features with the cells already computed by the emission: a work
+// item is 32 voxels x 64 channels.  Lanes gather one channel plane at the 32
+// voxels' cells (voxels in pid order sit on nearby cells, so a warp load
+// touches few sectors; eight loads in flight per thread), a shared-memory
+// transpose, then warps write voxel rows 64 channels wide.  (The thread-per-
+// (voxel, channel) kernel below reads 32 planes 19 KB apart per warp load:
+// one sector per element.)
+constexpr int kFeatTV = 32, kFeatTC = 64;
+template <typename T>
+__global__ void __launch_bounds__(256)
+grid_emit_feat_tile_kernel(const int32_t* __restrict__ nnew_dev, int64_t capacity, EmitArgs a) {
+  pdl_wait();
+  __shared__ float tile[kFeatTC][kFeatTV + 1];
+  const int64_t nnew = min((int64_t)*nnew_dev, capacity);
+  const int64_t nch = (a.fc + kFeatTC - 1) / kFeatTC;
+  const int64_t items = (nnew + kFeatTV - 1) / kFeatTV * nch;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t HW = a.H * a.W, plane = a.fh * a.fw;
+  T* out = static_cast<T*>(a.ofeat);
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t o0 = it / nch * kFeatTV, c0 = it % nch * kFeatTC;
+    const int nv = (int)min((int64_t)kFeatTV, nnew - o0);
+    int64_t base = 0;
+    if (lane < nv) {
+      const int64_t p = a.pid[o0 + lane];
+      base = p / HW * a.fc * plane + a.cell[o0 + lane];
+    }
+    float x[kFeatTC / 8];
+#pragma unroll
+    for (int k = 0; k < kFeatTC / 8; k++) {
+      const int64_t c = c0 + warp + 8 * k;
+      x[k] = (lane < nv && c < a.fc) ? __ldg(a.feat + base + c * plane) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < kFeatTC / 8; k++) tile[warp + 8 * k][lane] = x[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kFeatTV / 8; k++) {
+      const int v = warp + 8 * k;
+#pragma unroll
+      for (int h = 0; h < kFeatTC / 32; h++) {
+        const int64_t c = c0 + 32 * h + lane;
+        if (v < nv && c < a.fc) out[(o0 + v) * a.fc + c] = (T)tile[32 * h + lane][v];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void prefix_mask_kernel(const int64_t* __restrict__ n_dev, int64_t cap, uint8_t* __restrict__ mask) {
   pdl_wait();
   const int64_t n = *n_dev;
@@ -2199,7 +2249,16 @@ cudaError_t emit_outputs(const GridIn& in, const Cam& cam, DedupTable* st, const
       return e;
     count_launches(1);
   }
-  if (in.feat) {
+  if (in.feat && ea.cell) {
+    const int64_t items = (out.capacity + kFeatTV - 1) / kFeatTV * ((in.fc + kFeatTC - 1) / kFeatTC);
+    const dim3 g((unsigned)std::min<int64_t>(std::max<int64_t>(items, 1), (int64_t)sms * 8));
+    e = ea.feat64 ? launch_pdl(grid_emit_feat_tile_kernel<double>, g, dim3(256), 0, s, (const int32_t*)grand,
+                               (int64_t)out.capacity, ea)
+                  : launch_pdl(grid_emit_feat_tile_kernel<float>, g, dim3(256), 0, s, (const int32_t*)grand,
+                               (int64_t)out.capacity, ea);
+    if (e != cudaSuccess) return e;
+    count_launches(1);
+  } else if (in.feat) {
     if ((e = launch_pdl(grid_emit_feat_kernel, dim3(grid_blocks(out.capacity * in.fc, 256, sms)), dim3(256), 0, s,
                         head, (const int32_t*)grand, (int64_t)out.capacity, ea)) != cudaSuccess)
       return e;
