@@ -8,6 +8,7 @@
 // (warp match_any ranks, tiles walked in order) and (4) run one chain per
 // (k, d) over the sorted row ids: lanes own consecutive d so each row read is
 // a coalesced 128-512 B segment.  HBM traffic ~ one read of X + 8 B/row.
+#include <algorithm>
 #include <cstdlib>
 
 #include "launchers.h"
@@ -540,12 +541,15 @@ __global__ void ring_write_dev_kernel(const X* __restrict__ x, int64_t ldx, cons
                                       const int64_t* __restrict__ start_dev) {
   pdl_wait();
   const int64_t n = min(*n_dev, n_max);
-  const int64_t j = blockIdx.x;
-  if (j >= n || (n > cap && j < n - cap)) return;
-  const int64_t phys = n >= cap ? j - (n - cap) : (*start_dev + j) % cap;
-  double* dst = ring + phys * d;
-  const X* src = x + j * ldx;
-  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) dst[i] = ld64(src, i);
+  const int64_t start = *start_dev;
+  // rows strided over a bounded grid: n_max (the caller's capacity) is usually
+  // far above the frame's n, and a block per potential row paid for the empty ones
+  for (int64_t j = max((int64_t)0, n - cap) + blockIdx.x; j < n; j += gridDim.x) {
+    const int64_t phys = n >= cap ? j - (n - cap) : (start + j) % cap;
+    double* dst = ring + phys * d;
+    const X* src = x + j * ldx;
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) dst[i] = ld64(src, i);
+  }
 }
 
 __global__ void ring_advance_kernel(const int64_t* __restrict__ n_dev, int64_t n_max, int64_t cap, int64_t* start_dev) {
@@ -676,21 +680,22 @@ cudaError_t launch_revive(int64_t k, int64_t d, double n_new, double denom, cons
   return cudaGetLastError();
 }
 
+constexpr int64_t kRingBlocks = 148 * 8;
 cudaError_t launch_ring_write_dev(const void* x, int dtype, int64_t ldx, const int64_t* n_dev, int64_t n_max,
                                   int64_t d, double* ring, int64_t cap, int64_t* start_dev, cudaStream_t s) {
   if (n_max <= 0) return cudaSuccess;
   cudaError_t e;
   switch (dtype) {
     case F32:
-      e = launch_pdl(ring_write_dev_kernel<float>, dim3((unsigned)n_max), dim3(128), 0, s, (const float*)x, ldx, n_dev,
+      e = launch_pdl(ring_write_dev_kernel<float>, dim3((unsigned)std::min<int64_t>(n_max, kRingBlocks)), dim3(256), 0, s, (const float*)x, ldx, n_dev,
                      n_max, d, ring, cap, (const int64_t*)start_dev);
       break;
     case F64:
-      e = launch_pdl(ring_write_dev_kernel<double>, dim3((unsigned)n_max), dim3(128), 0, s, (const double*)x, ldx,
+      e = launch_pdl(ring_write_dev_kernel<double>, dim3((unsigned)std::min<int64_t>(n_max, kRingBlocks)), dim3(256), 0, s, (const double*)x, ldx,
                      n_dev, n_max, d, ring, cap, (const int64_t*)start_dev);
       break;
     default:
-      e = launch_pdl(ring_write_dev_kernel<uint16_t>, dim3((unsigned)n_max), dim3(128), 0, s, (const uint16_t*)x, ldx,
+      e = launch_pdl(ring_write_dev_kernel<uint16_t>, dim3((unsigned)std::min<int64_t>(n_max, kRingBlocks)), dim3(256), 0, s, (const uint16_t*)x, ldx,
                      n_dev, n_max, d, ring, cap, (const int64_t*)start_dev);
   }
   if (e != cudaSuccess) return e;

@@ -1,0 +1,4 @@
+# C4 quick check: stream + VQ parity tests, then the stream bench twice
+cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_stream_gpu.py tests/test_vq_gpu.py -q -x > gpurun_out/sq_tests.log 2>&1; echo "rc=$?" >> gpurun_out/sq_tests.log
+for i in 1 2; do timeout 600 python tools/stream_bench.py 1000 > gpurun_out/sq_bench_$i.log 2>&1; done
