@@ -2369,12 +2369,14 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
         ProfScope prof("grid_keys", s);
         if (front_ok) {
           const int64_t rbf = (in.H + FK_ROWS - 1) / FK_ROWS;
-          // tuning knobs, read once.  Neighbour dedup: 0 left/up, 1 + diagonals, 2
-          // (default) + two columns away (C3 1 cm: 2.82M -> 1.92M table inserts,
-          // front end 143.4 -> 139.8 us)
+          // tuning knobs, read once.  Neighbour dedup: 0 left/up, 1 (default) +
+          // diagonals, 2 + two columns away.  C3 1 cm: 1 and 2 tie (2 cuts the
+          // table inserts 2.82M -> 1.92M but costs three 64-bit compares per
+          // pixel); 5 cm, where left/up already catch most repeats: 0.100 (1) vs
+          // 0.109 ms (2); C4 unchanged
           static const int diag = [] {
             const char* v = std::getenv("XGS_GRID_DIAG");
-            return v ? (v[0] == '0' ? 0 : v[0] == '1' ? 1 : 2) : 2;
+            return v ? (v[0] == '0' ? 0 : v[0] == '1' ? 1 : 2) : 1;
           }();
           static const bool halo = [] {
             const char* v = std::getenv("XGS_GRID_HALO");
