@@ -1232,6 +1232,8 @@ def main():
             "grid_c3_Gpts_s": (g1.get("Mpts_per_s") or 0) / 1e3 if g1 else None,
             "grid_c3_ms": g1.get("ms_per_batch"), "grid_front_hbm_frac": (g1.get("roofline") or {}).get("frac"),
             "grid_batch_hbm_frac": g1.get("batch_hbm_frac"),
+            "grid_c3_graph_ms": (g1.get("graph") or {}).get("ms_per_batch"),
+            "grid_front_issue_frac": ((g1.get("roofline") or {}).get("issue") or {}).get("frac"),
             "stream_p50_ms": (stream or {}).get("p50_ms"), "stream_p99_ms": (stream or {}).get("p99_ms"),
             "c1_ms": (c1 or {}).get("ms_per_frame_step"),
             "e2e": {"value": e2e_val, "unit": "Mfeat/s", "h2d_bytes_per_step": world * e2e_rows * C5_D * 2,
