@@ -15,9 +15,10 @@
 // as exp(l - max_row) * (1 / sum_row exp(l - max_row)), the row statistics
 // computed by a first pass (the reference's mixture_weights, core.py:473-480).
 //
-// Tile: 32 rows x 384 columns per CTA, 8 warps each owning 32 x 48 (4 x 6
-// MMA tiles, 48 fp64 accumulators per lane); K-chunks of 16 staged in shared
-// memory, double-buffered (B by cp.async when its columns are contiguous).
+// Tile: 64 rows x 256 columns per CTA, 16 warps each owning 32 x 32 (4 x 4
+// MMA tiles, 32 fp64 accumulators per lane); K-chunks of 32 staged in shared
+// memory, double-buffered by cp.async (chunks of 16: one barrier per 16 k,
+// 71.8 vs 69.2 ms at the relevance benchmark).
 // Shared-memory row strides are 4 (mod 16) doubles so the fragment loads
 // (A: lane -> (row l/4, k l%4); B: lane -> (k l%4, col l/4)) are conflict-free.
 //
@@ -30,8 +31,8 @@ namespace xgs {
 
 namespace {
 
-constexpr int kGBM = 64, kGBN = 256, kGKC = 16, kGThreads = 512;   // 16 warps: 2 (rows) x 8 (columns)
-constexpr int kGAStride = kGKC + 4;      // 20 == 4 (mod 16)
+constexpr int kGBM = 64, kGBN = 256, kGKC = 32, kGThreads = 512;   // 16 warps: 2 (rows) x 8 (columns)
+constexpr int kGAStride = kGKC + 4;      // 36 == 4 (mod 16)
 constexpr int kGBStride = kGBN + 4;      // 260 == 4 (mod 16)
 constexpr int kGMaxQ = 16;               // query vectors in the relevance epilogue
 constexpr size_t kGSmem = sizeof(double) * (2 * kGBM * kGAStride + 2 * kGKC * kGBStride);
@@ -81,9 +82,13 @@ __global__ void __launch_bounds__(kGThreads, 1) gemm_f64_kernel(GemmArgs a) {
     double* as = As + buf * kGBM * kGAStride;
     double* bs = Bs + buf * kGKC * kGBStride;
     const bool full_k = k0 + kGKC <= a.kr;
-    if (a_cp && full_k) {   // 64 rows x 16 doubles: 512 16-byte copies, one per thread
-      const int rr = t >> 3, kk = (t & 7) * 2;
-      cp_async16(as + rr * kGAStride + kk, a.A + (r0 + rr) * a.lda_r + (k0 + kk));
+    if (a_cp && full_k) {   // kGBM rows x kGKC doubles in 16-byte copies
+#pragma unroll
+      for (int i = 0; i < kGBM * kGKC / 2 / kGThreads; i++) {
+        const int idx = t + kGThreads * i;
+        const int rr = idx / (kGKC / 2), kk = (idx % (kGKC / 2)) * 2;
+        cp_async16(as + rr * kGAStride + kk, a.A + (r0 + rr) * a.lda_r + (k0 + kk));
+      }
     } else {
       for (int idx = t; idx < kGBM * kGKC; idx += kGThreads) {
         const int rr = a.lda_k == 1 ? idx / kGKC : idx % kGBM, kk = a.lda_k == 1 ? idx % kGKC : idx / kGBM;
@@ -91,9 +96,9 @@ __global__ void __launch_bounds__(kGThreads, 1) gemm_f64_kernel(GemmArgs a) {
             (rr < nrows && k0 + kk < a.kr) ? a.A[(r0 + rr) * a.lda_r + (k0 + kk) * a.lda_k] : 0.0;
       }
     }
-    if (b_cp && full_k) {   // 16 rows x 256 doubles: 2048 16-byte copies, 4 per thread
+    if (b_cp && full_k) {   // kGKC rows x kGBN doubles in 16-byte copies
 #pragma unroll
-      for (int i = 0; i < 4; i++) {
+      for (int i = 0; i < kGKC * kGBN / 2 / kGThreads; i++) {
         const int idx = t + kGThreads * i;
         const int kk = idx / (kGBN / 2), cc = (idx % (kGBN / 2)) * 2;
         cp_async16(bs + kk * kGBStride + cc, a.B + (k0 + kk) * a.ldb_k + (c0 + cc));
