@@ -437,29 +437,55 @@ acc_chain_kernel(const X* __restrict__ x, int64_t d, int64_t ldx, int64_t k,
 }
 
 // Small batches (n <= kSmallRows, e.g. the per-frame C4 stream): one launch,
-// one warp per (code, 32-dim chunk) walking all n rows in ascending order and
-// adding the rows of its code -- the same per-(k, d) sequential chains in row
-// order (np.add.at) without the counting-sort kernels.
+// one warp per (code, group of kSmallG 32-dim chunks) walking the rows in
+// ascending order, 256 at a time (each lane reads 8 codes, eight ballots mark
+// the rows of the warp's code, the set bits are added lowest first) -- the same
+// per-(k, d) sequential chains in row order (np.add.at) without the
+// counting-sort kernels.  Each hit row costs the warp one load latency (the
+// chain is serial), so the path stays for batches of at most 1024 rows: with
+// a device-side row count over a 16K-row window (the C4 graph) it measured
+// 0.189 vs 0.177 ms per frame against the counting sort.
 constexpr int64_t kSmallRows = 1024;
+constexpr int kSmallG = 8;
 template <typename X>
 __global__ void __launch_bounds__(256)
 acc_small_kernel(const X* __restrict__ x, int64_t n, int64_t d, int64_t ldx, const int64_t* __restrict__ codes,
                  const uint8_t* __restrict__ mask, int64_t k, double* __restrict__ counts, double* __restrict__ sums,
                  int cont) {
   const int lane = threadIdx.x & 31;
-  const int64_t chunks = (d + 31) / 32;
+  const int64_t groups = ((d + 31) / 32 + kSmallG - 1) / kSmallG;
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= k * chunks) return;
-  const int64_t code = w / chunks, j = (w - code * chunks) * 32 + lane;
-  double acc = (cont && j < d) ? sums[code * d + j] : 0.0;
+  if (w >= k * groups) return;   // warp-uniform
+  const int64_t code = w / groups, j0 = (w - code * groups) * kSmallG * 32 + lane;
+  const int64_t nn = n;
+  double acc[kSmallG];
+#pragma unroll
+  for (int c = 0; c < kSmallG; c++) acc[c] = (cont && j0 + 32 * c < d) ? sums[code * d + j0 + 32 * c] : 0.0;
   int64_t cnt = 0;
-  for (int64_t r = 0; r < n; r++) {
-    if (row_code(codes, mask, r) != (int)code) continue;
-    cnt++;
-    if (j < d) acc = dadd(acc, ld64(x + r * ldx, j));
+  for (int64_t r0 = 0; r0 < nn; r0 += 256) {
+    unsigned b[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int64_t r = r0 + 32 * u + lane;
+      b[u] = __ballot_sync(0xffffffffu, r < nn && row_code(codes, mask, r) == (int)code);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      cnt += __popc(b[u]);
+      while (b[u]) {
+        const int i = __ffs(b[u]) - 1;
+        b[u] &= b[u] - 1;
+        const X* row = x + (r0 + 32 * u + i) * ldx;
+#pragma unroll
+        for (int c = 0; c < kSmallG; c++)
+          if (j0 + 32 * c < d) acc[c] = dadd(acc[c], ld64(row, j0 + 32 * c));
+      }
+    }
   }
-  if (j < d) sums[code * d + j] = acc;
-  if (j == 0) counts[code] = (cont ? counts[code] : 0.0) + (double)cnt;
+#pragma unroll
+  for (int c = 0; c < kSmallG; c++)
+    if (j0 + 32 * c < d) sums[code * d + j0 + 32 * c] = acc[c];
+  if (j0 == 0) counts[code] = (cont ? counts[code] : 0.0) + (double)cnt;
 }
 
 template <typename X, int VEC, int VL, int UL>
@@ -582,7 +608,7 @@ cudaError_t launch_accumulate(const void* x, int dtype, int64_t n, int64_t d, in
   int32_t* order = reinterpret_cast<int32_t*>(w + p.off_order);
   ProfScope prof("vq_accumulate", s);
   if (n <= kSmallRows) {
-    const int64_t warps = k * ((d + 31) / 32);
+    const int64_t warps = k * (((d + 31) / 32 + kSmallG - 1) / kSmallG);
     const unsigned blocks = (unsigned)((warps + 7) / 8);
     switch (dtype) {
       case F32: acc_small_kernel<float><<<blocks, 256, 0, s>>>((const float*)x, n, d, ldx, codes, mask, k, counts, sums, cont); break;
