@@ -172,6 +172,9 @@ FP64_DMMA_TFLOPS = 37.1   # tools/micro/fp64_peak.cu on the B200 pool (profiles/
 GRID_F, GRID_H, GRID_W = 16, 720, 1280
 GRID_INTR = (1050.0, 1050.0, 359.5, 639.5)   # BASELINE leaves C3 intrinsics open
 GRID_MAP = 4_000_000
+# the scene map's hash set: 16M slots (128 MB) for the 4M voxels plus a batch's new ones at load
+# <= 1/2 (the library reserves room for min(pixels, batch-table slots) new keys per batch)
+GRID_MAP_SLOTS = 4 * GRID_MAP
 
 
 def grid_scene_objects(seed=20):
@@ -257,9 +260,9 @@ def grid_graph_times(torch, voxel, warm, frames, steps, ref):
     from paper_2603_09632_b200.grid import GridGraph, GridSampler, VoxelHashSet
     Dd, Rd, Td, Cd = frames
     npix = int(Dd.numel())
-    snap = VoxelHashSet(GRID_MAP + npix)
+    snap = VoxelHashSet(GRID_MAP_SLOTS)
     snap.insert(warm)
-    work = VoxelHashSet(GRID_MAP + npix)
+    work = VoxelHashSet(GRID_MAP_SLOTS)
     work.copy_from(snap)
     gg = GridGraph(GridSampler(GRID_INTR, voxel, occupied=work), Dd, (Rd, Td), Cd)
     times = []
@@ -302,7 +305,7 @@ def run_grid(torch, steps, cpu=True):
         # stage scope for the per-stage split
         for it in range(2 * steps + 1):
             staged = it > steps
-            hs = VoxelHashSet(GRID_MAP + npix)
+            hs = VoxelHashSet(GRID_MAP_SLOTS)
             hs.insert(warm)
             map_size = len(hs)
             gs = GridSampler(GRID_INTR, voxel, occupied=hs)
@@ -342,7 +345,7 @@ def run_grid(torch, steps, cpu=True):
         Dh, Ch = torch.from_numpy(D).pin_memory(), torch.from_numpy(C).pin_memory()
         e2e = []
         for it in range(3):
-            hs = VoxelHashSet(GRID_MAP + npix)
+            hs = VoxelHashSet(GRID_MAP_SLOTS)
             hs.insert(warm)
             gs = GridSampler(GRID_INTR, voxel, occupied=hs)
             torch.cuda.synchronize()

@@ -2357,8 +2357,12 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
   if (hashed) {
     // ---------------- G1+G2': front end inserting into the batch table, table scan + map test
     if (!in.async) {   // async: the caller sized the map; the batch table exists (grid_state checked)
-      if ((e = hashset_reserve(hs, npix, s)) != cudaSuccess) return e;   // room for a new key per pixel
       if ((e = dedup_table(*st, npix / 16, false, s)) != cudaSuccess) return e;
+      // the scan adds at most one key per occupied batch-table slot (an overflowing
+      // batch is redone on a larger table, reserved again below): room for
+      // min(pixels, table slots) new keys keeps the map's load <= 1/2 (a bound of
+      // one key per pixel grew the C3 map to 64M slots, 512 MB, for 4M keys)
+      if ((e = hashset_reserve(hs, std::min<int64_t>(npix, st->cap), s)) != cudaSuccess) return e;
     }
     out.sort_passes = 0;
     const CamF cf{(float)in.cx, (float)in.cy, (float)(1.0 / in.fx), (float)(1.0 / in.fy), (float)(1.0 / in.voxel)};
@@ -2442,7 +2446,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
         return e;
       if (in.async) {   // counts on the device (out.dev_status); the map bound grows by the pixel count
         out.n_new = out.n_valid = out.n_voxels = out.n_sorted = -1;
-        hs->count_ub += npix;
+        hs->count_ub += std::min<int64_t>(npix, st->cap);
         st->dirty = false;
         return cudaGetLastError();
       }
@@ -2460,6 +2464,7 @@ cudaError_t grid_sample(const GridIn& in, HashSet* hs, GridOut& out, void* ws, s
       fill_u64_kernel<<<grid_blocks(2 * st->cap, 256, sms), 256, 0, s>>>(st->slots, 2 * st->cap, ~0ull);
       count_launches(1);
       if ((e = dedup_table(*st, npix, true, s)) != cudaSuccess) return e;
+      if ((e = hashset_reserve(hs, std::min<int64_t>(npix, st->cap), s)) != cudaSuccess) return e;
     }
     st->last_nvox = out.n_voxels;
   } else {
