@@ -30,7 +30,9 @@
 //                             equal weights as in the stable lexsort);
 //   R7 raster_vjp_kernel    : feature_gradients' np.add.at (pairs stably sorted
 //                             by Gaussian, one sequential fp64 chain per
-//                             (Gaussian, channel) in pair order).
+//                             (Gaussian, channel) in pair order; Gaussians with
+//                             more than 512 pairs: 32 in-order segment chains
+//                             added in order, raster_vjp_long_kernel).
 // The reference's transmittance comes from one global cumsum over all pairs;
 // the per-pixel running sum here is the same quantity without the global
 // rounding drift, so T and the weights agree to ~1e-12 relative (exp, log1p,
@@ -409,16 +411,50 @@ __global__ void raster_transpose_kernel(const double* __restrict__ in, int64_t D
 // sequential fp64 chain (np.add.at order), so a splat covering many pixels is
 // spread over D/32 warps instead of serialising one; pair metadata is fetched
 // 32 pairs at a time and broadcast by shuffles.
+// One lane's chain over pairs [a, b) of a Gaussian (channel dd of upT).
+__device__ __forceinline__ double vjp_chain(const uint32_t* __restrict__ pidx, const int32_t* __restrict__ pixel,
+                                            const double* __restrict__ weight, const double* __restrict__ upT,
+                                            int64_t D, int64_t dd, int32_t a, int32_t b, int lane) {
+  double acc = 0.0;
+  for (int32_t i0 = a; i0 < b; i0 += 32) {
+    int32_t mp = 0;
+    double mw = 0.0;
+    if (i0 + lane < b) {
+      const uint32_t q = pidx[i0 + lane];
+      mp = pixel[q];
+      mw = weight[q];
+    }
+    const int cnt = min(32, b - i0);
+#pragma unroll 8
+    for (int j = 0; j < cnt; j++) {
+      const int64_t px = __shfl_sync(FULL, mp, j);
+      const double w = __shfl_sync(FULL, mw, j);
+      acc = dadd(acc, dmul(w, __ldg(upT + px * D + dd)));
+    }
+  }
+  return acc;
+}
+
+// Gaussians with more than kVjpLong pairs (large splats near the camera: up to
+// ~20K lattice pixels) are left to raster_vjp_long_kernel: one sequential
+// chain per lane there set the whole kernel's time (4.1 ms at the bench's 2^18
+// Gaussians).  The warp of their first chunk appends them to a list.
+constexpr int32_t kVjpLong = 512;
 __global__ void __launch_bounds__(256)
 raster_vjp_kernel(const uint32_t* __restrict__ pidx, const int32_t* __restrict__ pixel,
                   const double* __restrict__ weight, const double* __restrict__ upT, int64_t D,
-                  const int32_t* __restrict__ gstart, int64_t n, double* __restrict__ fg) {
+                  const int32_t* __restrict__ gstart, int64_t n, double* __restrict__ fg,
+                  int32_t* __restrict__ long_list, int32_t* __restrict__ long_count) {
   const int lane = threadIdx.x & 31;
   const int64_t chunks = (D + 31) / 32;
   for (int64_t wi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < n * chunks;
        wi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t g = wi / chunks, d = (wi - g * chunks) * 32 + lane;
     const int32_t a = gstart[g], b = gstart[g + 1];
+    if (b - a > kVjpLong) {
+      if (wi % chunks == 0 && lane == 0) long_list[atomicAdd(long_count, 1)] = (int32_t)g;
+      continue;
+    }
     double acc = 0.0;
     for (int32_t i0 = a; i0 < b; i0 += 32) {
       int32_t mp = 0;
@@ -438,6 +474,39 @@ raster_vjp_kernel(const uint32_t* __restrict__ pidx, const int32_t* __restrict__
       }
     }
     if (d < D && b > a) fg[g * D + d] = acc;
+  }
+}
+
+// A long Gaussian's (chunk of 32 channels) per block: the 32 warps sum 32
+// contiguous segments of its pairs, then warp 0 adds the 32 partials in segment
+// order -- deterministic; the reassociation differs from one sequential chain
+// by ~1e-16 relative (the pair weights themselves carry ~1e-12).
+constexpr int kVjpSegs = 32;
+__global__ void __launch_bounds__(32 * kVjpSegs)
+raster_vjp_long_kernel(const uint32_t* __restrict__ pidx, const int32_t* __restrict__ pixel,
+                       const double* __restrict__ weight, const double* __restrict__ upT, int64_t D,
+                       const int32_t* __restrict__ gstart, const int32_t* __restrict__ long_list,
+                       const int32_t* __restrict__ long_count, double* __restrict__ fg) {
+  __shared__ double part[kVjpSegs][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t chunks = (D + 31) / 32;
+  const int64_t items = (int64_t)*long_count * chunks;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t g = long_list[it / chunks], d = (it % chunks) * 32 + lane;
+    const int64_t dd = d < D ? d : D - 1;
+    const int32_t a = gstart[g], b = gstart[g + 1];
+    const int32_t len = b - a;
+    const int32_t s0 = a + (int32_t)((int64_t)len * warp / kVjpSegs),
+                  s1 = a + (int32_t)((int64_t)len * (warp + 1) / kVjpSegs);
+    part[warp][lane] = vjp_chain(pidx, pixel, weight, upT, D, dd, s0, s1, lane);
+    __syncthreads();
+    if (warp == 0 && d < D) {
+      double acc = part[0][lane];
+#pragma unroll
+      for (int w = 1; w < kVjpSegs; w++) acc = dadd(acc, part[w][lane]);
+      fg[g * D + d] = acc;
+    }
+    __syncthreads();
   }
 }
 
@@ -691,6 +760,9 @@ cudaError_t raster_vjp(RasterState* st, const double* upstream, int64_t D, doubl
   if ((e = dalloc(&vals, np, s)) != cudaSuccess) return e;
   if ((e = dalloc(&upT, P * D, s)) != cudaSuccess) return e;
   if ((e = dalloc(&gstart, n + 1, s)) != cudaSuccess) return e;
+  int32_t* long_list = nullptr;   // [n] Gaussians with more than kVjpLong pairs, then the count
+  if ((e = dalloc(&long_list, n + 1, s)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(long_list + n, 0, sizeof(int32_t), s)) != cudaSuccess) return e;
   if ((e = cudaMallocAsync(&ws, wsb, s)) != cudaSuccess) return e;
   raster_gauss_keys_kernel<<<blocks_for(np, 256), 256, 0, s>>>(st->po.gauss, np, keys, vals); count_launches(1);
   if ((e = radix_sort_pairs(keys, vals, np, bits_for_count(n), ws, wsb, s)) != cudaSuccess) return e;
@@ -700,12 +772,16 @@ cudaError_t raster_vjp(RasterState* st, const double* upstream, int64_t D, doubl
     raster_transpose_kernel<<<gb, tb, 0, s>>>(upstream, D, P, upT); count_launches(1);
   }
   raster_vjp_kernel<<<blocks_for(n * ((D + 31) / 32) * 32, 256), 256, 0, s>>>(vals, st->po.pixel, st->po.weight, upT,
-                                                                             D, gstart, n, fg); count_launches(1);
+                                                                             D, gstart, n, fg, long_list,
+                                                                             long_list + n); count_launches(1);
+  raster_vjp_long_kernel<<<148 * 2, 32 * kVjpSegs, 0, s>>>(vals, st->po.pixel, st->po.weight, upT, D, gstart, long_list,
+                                                 long_list + n, fg); count_launches(1);
   e = cudaGetLastError();
   cudaFreeAsync(keys, s);
   cudaFreeAsync(vals, s);
   cudaFreeAsync(upT, s);
   cudaFreeAsync(gstart, s);
+  cudaFreeAsync(long_list, s);
   cudaFreeAsync(ws, s);
   return e;
 }
