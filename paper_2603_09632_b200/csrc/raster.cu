@@ -436,25 +436,35 @@ __device__ __forceinline__ double vjp_chain(const uint32_t* __restrict__ pidx, c
 }
 
 // Gaussians with more than kVjpLong pairs (large splats near the camera: up to
-// ~20K lattice pixels) are left to raster_vjp_long_kernel: one sequential
-// chain per lane there set the whole kernel's time (4.1 ms at the bench's 2^18
-// Gaussians).  The warp of their first chunk appends them to a list.
+// ~20K lattice pixels) go to raster_vjp_long_kernel: one sequential chain per
+// lane there set the whole kernel's time (4.1 ms at the bench's 2^18
+// Gaussians).  A classify pass lists the short and the long Gaussians with
+// pairs (list order is irrelevant: every item is computed on its own), so no
+// warp walks the Gaussians without pairs (a (Gaussian, chunk) item each had
+// cost 0.6 ms of dependent range loads).
 constexpr int32_t kVjpLong = 512;
+__global__ void raster_vjp_classify_kernel(const int32_t* __restrict__ gstart, int64_t n,
+                                           int32_t* __restrict__ short_list, int32_t* __restrict__ short_count,
+                                           int32_t* __restrict__ long_list, int32_t* __restrict__ long_count) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t len = gstart[g + 1] - gstart[g];
+    if (len > kVjpLong) long_list[atomicAdd(long_count, 1)] = (int32_t)g;
+    else if (len > 0) short_list[atomicAdd(short_count, 1)] = (int32_t)g;
+  }
+}
+
 __global__ void __launch_bounds__(256)
 raster_vjp_kernel(const uint32_t* __restrict__ pidx, const int32_t* __restrict__ pixel,
                   const double* __restrict__ weight, const double* __restrict__ upT, int64_t D,
-                  const int32_t* __restrict__ gstart, int64_t n, double* __restrict__ fg,
-                  int32_t* __restrict__ long_list, int32_t* __restrict__ long_count) {
+                  const int32_t* __restrict__ gstart, const int32_t* __restrict__ short_list,
+                  const int32_t* __restrict__ short_count, double* __restrict__ fg) {
   const int lane = threadIdx.x & 31;
   const int64_t chunks = (D + 31) / 32;
-  for (int64_t wi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < n * chunks;
+  const int64_t items = (int64_t)*short_count * chunks;
+  for (int64_t wi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < items;
        wi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t g = wi / chunks, d = (wi - g * chunks) * 32 + lane;
+    const int64_t g = short_list[wi / chunks], d = (wi % chunks) * 32 + lane;
     const int32_t a = gstart[g], b = gstart[g + 1];
-    if (b - a > kVjpLong) {
-      if (wi % chunks == 0 && lane == 0) long_list[atomicAdd(long_count, 1)] = (int32_t)g;
-      continue;
-    }
     double acc = 0.0;
     for (int32_t i0 = a; i0 < b; i0 += 32) {
       int32_t mp = 0;
@@ -760,9 +770,12 @@ cudaError_t raster_vjp(RasterState* st, const double* upstream, int64_t D, doubl
   if ((e = dalloc(&vals, np, s)) != cudaSuccess) return e;
   if ((e = dalloc(&upT, P * D, s)) != cudaSuccess) return e;
   if ((e = dalloc(&gstart, n + 1, s)) != cudaSuccess) return e;
-  int32_t* long_list = nullptr;   // [n] Gaussians with more than kVjpLong pairs, then the count
-  if ((e = dalloc(&long_list, n + 1, s)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(long_list + n, 0, sizeof(int32_t), s)) != cudaSuccess) return e;
+  // [n] Gaussians with more than kVjpLong pairs, [n] the others with pairs, then the two counts
+  int32_t* long_list = nullptr;
+  if ((e = dalloc(&long_list, 2 * n + 2, s)) != cudaSuccess) return e;
+  int32_t* short_list = long_list + n;
+  int32_t* counts = long_list + 2 * n;   // {long, short}
+  if ((e = cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), s)) != cudaSuccess) return e;
   if ((e = cudaMallocAsync(&ws, wsb, s)) != cudaSuccess) return e;
   raster_gauss_keys_kernel<<<blocks_for(np, 256), 256, 0, s>>>(st->po.gauss, np, keys, vals); count_launches(1);
   if ((e = radix_sort_pairs(keys, vals, np, bits_for_count(n), ws, wsb, s)) != cudaSuccess) return e;
@@ -771,11 +784,13 @@ cudaError_t raster_vjp(RasterState* st, const double* upstream, int64_t D, doubl
     dim3 tb(32, 8), gb((unsigned)((P + 31) / 32 < 4096 ? (P + 31) / 32 : 4096), (unsigned)((D + 31) / 32 < 64 ? (D + 31) / 32 : 64));
     raster_transpose_kernel<<<gb, tb, 0, s>>>(upstream, D, P, upT); count_launches(1);
   }
-  raster_vjp_kernel<<<blocks_for(n * ((D + 31) / 32) * 32, 256), 256, 0, s>>>(vals, st->po.pixel, st->po.weight, upT,
-                                                                             D, gstart, n, fg, long_list,
-                                                                             long_list + n); count_launches(1);
+  raster_vjp_classify_kernel<<<blocks_for(n, 256), 256, 0, s>>>(gstart, n, short_list, counts + 1, long_list, counts);
+  count_launches(1);
+  raster_vjp_kernel<<<blocks_for(np * ((D + 31) / 32) * 32, 256), 256, 0, s>>>(vals, st->po.pixel, st->po.weight, upT,
+                                                                              D, gstart, short_list, counts + 1, fg);
+  count_launches(1);
   raster_vjp_long_kernel<<<148 * 2, 32 * kVjpSegs, 0, s>>>(vals, st->po.pixel, st->po.weight, upT, D, gstart, long_list,
-                                                 long_list + n, fg); count_launches(1);
+                                                           counts, fg); count_launches(1);
   e = cudaGetLastError();
   cudaFreeAsync(keys, s);
   cudaFreeAsync(vals, s);
